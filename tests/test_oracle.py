@@ -1,0 +1,205 @@
+"""Pins the CPU oracle (oracle/ace_oracle.c) before anything is checked against it.
+
+Known answers come from tests/golden/kats.json, which tests/golden/make_golden.py
+printed from the reference's own code; the RFC/FIPS vectors are the ones the
+reference's tests hold (test_sha256.cpp:31-47, test_crypto.cpp:27-52). Where the
+reference library itself is present (oracle/_ref), the oracle is also compared
+with it live on fresh inputs.
+"""
+import ctypes as C
+import random
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+
+def test_sha256_fips_vectors(kats):
+    assert O.sha256(b"").hex() == "e3b0c44298fc1c149afbf4c8996fb92427ae41e4649b934ca495991b7852b855"
+    assert O.sha256(b"abc").hex() == "ba7816bf8f01cfea414140de5dae2223b00361a396177a9cb410ff61f20015ad"
+    for v in kats["sha256"].values():
+        assert O.sha256(bytes.fromhex(v["msg"])).hex() == v["digest"]
+
+
+def test_hmac_rfc4231(kats):
+    assert O.hmac(b"\x0b" * 20, b"Hi There").hex() == (
+        "b0344c61d8db38535ca8afceaf0bf12b881dc200c9833da726e9376c2e32cff7")
+    for v in kats["hmac"]:
+        assert O.hmac(bytes.fromhex(v["key"]), bytes.fromhex(v["msg"])).hex() == v["mac"]
+
+
+def test_hkdf_rfc5869(kats):
+    lib = O.oracle()
+    for v in kats["hkdf"]:
+        ikm, salt, info = (bytes.fromhex(v[k]) for k in ("ikm", "salt", "info"))
+        out = O.buf(v["L"])
+        rc = lib.or_hkdf_sha256(O.ptr(ikm), C.c_uint64(len(ikm)), O.ptr(salt) if salt else None,
+                                C.c_uint64(len(salt)), O.ptr(info), C.c_uint64(len(info)), out,
+                                C.c_uint64(v["L"]))
+        assert rc == 0 and bytes(out).hex() == v["okm"]
+    # RFC 5869 TC1 literal (test_crypto.cpp:37-52)
+    assert kats["hkdf"][1]["okm"].startswith("3cb25f25faacd57a90434f64d0362f2a2d2d0a90cf1a5a4c")
+    # L > 8160 rejected (hkdf.cpp:65-67)
+    assert lib.or_hkdf_sha256(O.ptr(b"k"), C.c_uint64(1), None, C.c_uint64(0), O.ptr(b"i"),
+                              C.c_uint64(1), O.buf(8161), C.c_uint64(8161)) == -1
+
+
+def test_fixture_values(kats):
+    f = kats["fixture"]
+    rev = O.rev_from_seed(20240801)
+    assert rev.hex() == f["rev"]
+    assert O.id_commitment(rev, b"\0" * 32, 1, 40).hex() == f["id_com"]
+    assert O.derive_attest_key(rev, O.domain_encode(1, 40)).hex() == f["attest_key"]
+    pay = O.transfer_payload(b"\x01" * 32, b"\x02" * 32, 10, 0, b"\0" * 32)
+    assert pay.hex() == f["payload0"]
+    att = O.generate_attestation(rev, pay, O.domain_encode(1, 40), bytes.fromhex(f["id_com"]))
+    assert att.hex() == f["attestation0"]
+    out = O.buf(289)
+    O.oracle().or_prove_tx(O.ptr(pay), C.c_uint64(len(pay)), O.ptr(att), out)
+    assert bytes(out).hex() == f["proof0"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 5, 7, 100, 1024, 1025, 4097, 16384])
+def test_canonical_block_roots(kats, n):
+    k = kats["canonical_blocks"][str(n)]
+    fb = O.canonical_block(n)
+    root, lv, pr = O.oracle_prove_block(fb)
+    assert (lv, pr) == (k["levels"], k["pairs"])
+    assert root[256:288].hex() == k["root_digest"]
+    assert root[288] == k["root_kind"]
+    fc = O.oracle_build_fc(fb, root)
+    assert fc.hex() == k["fc"]
+    assert (O.oracle_attest_codes(fb) == 0).sum() == k["accept"]
+    assert O.oracle_verify_fc(fc, fb) == 0
+
+
+@pytest.mark.slow
+def test_canonical_block_100k(kats):
+    k = kats["canonical_blocks"]["100000"]
+    fb = O.canonical_block(100000)
+    root, lv, pr = O.oracle_prove_block(fb)
+    assert O.oracle_build_fc(fb, root).hex() == k["fc"]
+
+
+@pytest.mark.parametrize("n", [64, 1024])
+def test_forged_codes(kats, n):
+    k = kats["forged"][str(n)]
+    fb = O.forge(O.canonical_block(n))
+    assert O.sha256(fb.payloads.tobytes() + fb.atts.tobytes()).hex() == k["inputs_sha"]
+    codes = O.oracle_attest_codes(fb)
+    assert bytes(codes).hex() == k["codes"]
+    assert set(codes.tolist()) == {0, 1, 2}
+
+
+def test_multi_user_and_prover_blocks(kats):
+    mu = O.multi_user_block(1000, 16)
+    root, _, _ = O.oracle_prove_block(mu)
+    assert O.oracle_build_fc(mu, root).hex() == kats["multi_user_1000"]["fc"]
+    assert (O.oracle_attest_codes(mu) == 0).sum() == 1000
+    for n, fc in kats["prover_test_blocks"].items():
+        fb = O.prover_test_block(int(n))
+        root, _, _ = O.oracle_prove_block(fb)
+        assert O.oracle_build_fc(fb, root).hex() == fc
+
+
+def test_witness_and_scheme(kats):
+    w = kats["witness"]
+    lib = O.oracle()
+    key = bytes.fromhex(kats["fixture"]["attest_key"])
+    th = bytes.fromhex(w["tx_hash"])
+    out = O.buf(256)
+    lib.or_build_witness(O.ptr(key), O.ptr(th), out)
+    assert bytes(out).hex() == w["witness"]
+    att = bytes.fromhex(kats["fixture"]["attestation0"])
+    assert lib.or_witness_matches_tx(out, C.c_uint64(256), O.ptr(att)) == 1
+    assert lib.or_witness_matches_tx(out, C.c_uint64(255), O.ptr(att)) == 0
+    lib.or_scheme_share_mask.restype = C.c_uint64
+    for n, t in w["thresholds"].items():
+        assert lib.or_scheme_threshold(C.c_uint(int(n))) == t
+    for n, masks in w["share_masks"].items():
+        assert [lib.or_scheme_share_mask(C.c_uint(int(n)), C.c_uint(v))
+                for v in range(int(n))] == masks
+    master = bytes.fromhex(w["master"])
+    ct = O.buf(256)
+    lib.or_scheme_encapsulate(C.c_uint(4), O.ptr(master), O.ptr(th), out, C.c_uint64(256), ct)
+    assert bytes(ct).hex() == w["ciphertext_n4"]
+    for skip in range(4):
+        contrib = (C.c_uint * 3)(*[v for v in range(4) if v != skip])
+        pt = O.buf(256)
+        lib.or_scheme_decrypt(C.c_uint(4), O.ptr(master), O.ptr(th), ct, C.c_uint64(256), contrib,
+                              C.c_uint(3), pt)
+        assert bytes(pt) == bytes(out)
+    pair = (C.c_uint * 2)(0, 1)
+    pt = O.buf(256)
+    lib.or_scheme_decrypt(C.c_uint(4), O.ptr(master), O.ptr(th), ct, C.c_uint64(256), pair,
+                          C.c_uint(2), pt)
+    assert bytes(pt) != bytes(out)
+    assert lib.or_witness_matches_tx(pt, C.c_uint64(256), O.ptr(att)) == 0
+
+
+def test_aggregate_tree_structure():
+    """test_prover.cpp:64-104 restated against the oracle."""
+    lib = O.oracle()
+    fb = O.prover_test_block(5)
+    proofs = []
+    for i in range(5):
+        p = O.buf(289)
+        lib.or_prove_tx(O.ptr(fb.payload(i)), C.c_uint64(154), O.ptr(fb.att(i)), p)
+        proofs.append(bytes(p))
+        assert lib.or_verify_mock(p) == 1
+        bad = bytearray(p)
+        bad[5] ^= 1
+        assert lib.or_verify_mock(O.ptr(bytes(bad))) == 0
+    lv, pr = C.c_uint64(), C.c_uint64()
+    out = O.buf(289)
+    assert lib.or_aggregate_tree(None, C.c_uint64(0), out, C.byref(lv), C.byref(pr)) == -1
+    lib.or_aggregate_tree(O.ptr(proofs[0]), C.c_uint64(1), out, C.byref(lv), C.byref(pr))
+    assert bytes(out) == proofs[0] and lv.value == 0
+    base = O.buf(289)
+    lib.or_aggregate_tree(O.ptr(b"".join(proofs)), C.c_uint64(5), base, C.byref(lv), C.byref(pr))
+    assert lv.value == 3
+    sw = [proofs[0], proofs[2], proofs[1], proofs[3], proofs[4]]
+    lib.or_aggregate_tree(O.ptr(b"".join(sw)), C.c_uint64(5), out, C.byref(lv), C.byref(pr))
+    assert bytes(out)[:256] != bytes(base)[:256]
+    for n in (1, 2, 3, 4, 5, 7, 8, 9, 64, 100, 1024, 4095, 4096):
+        # shape only: trees over a duplicated proof; levels = ceil(log2 n), pair_ops = n-1
+        arr = proofs[0] * n if n <= 128 else None
+        if arr is None:
+            continue
+        lib.or_aggregate_tree(O.ptr(arr), C.c_uint64(n), out, C.byref(lv), C.byref(pr))
+        assert lv.value == (n - 1).bit_length() and pr.value == n - 1
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_oracle_matches_reference_random():
+    """Live differential check: random payload lengths, domains, REVs, ids."""
+    rng = random.Random(1234)
+    lib, R = O.oracle(), O.ref()
+    for trial in range(40):
+        n = rng.choice([1, 2, 3, 5, 8, 13, 33, 64])
+        payloads, atts, revs = [], [], []
+        for i in range(n):
+            rev = bytes(rng.getrandbits(8) for _ in range(32))
+            p = bytes(rng.getrandbits(8) for _ in range(rng.randrange(0, 400)))
+            dom = O.domain_encode(rng.randrange(65536), rng.randrange(1 << 48))
+            idc = bytes(rng.getrandbits(8) for _ in range(32))
+            a = O.generate_attestation(rev, p, dom, idc)
+            if rng.random() < 0.3:
+                a = a[:72] + bytes(rng.getrandbits(8) for _ in range(32))
+            payloads.append(p)
+            atts.append(a)
+            revs.append(rev)
+        hdr = bytes(rng.getrandbits(8) for _ in range(212)) + b"\0" * 44
+        fb = O.flat_from_lists(payloads, atts, hdr, revs, list(range(n)))
+        assert O.oracle_prove_block(fb) == O.ref_prove_block(fb)
+        root, _, _ = O.oracle_prove_block(fb)
+        assert O.oracle_build_fc(fb, root) == O.ref_prove_and_certify(fb)
+        assert (O.oracle_attest_codes(fb) == O.ref_attest_codes(fb)).all()
+    # merkle edge cases vs reference
+    for n in list(range(0, 20)) + [31, 32, 33, 100, 257]:
+        leaves = bytes(rng.getrandbits(8) for _ in range(32 * n))
+        a, b = O.buf(32), O.buf(32)
+        lib.or_merkle_root(O.ptr(leaves), C.c_uint64(n), a)
+        R.ref_merkle_root(O.ptr(leaves), C.c_uint64(n), b)
+        assert bytes(a) == bytes(b)
