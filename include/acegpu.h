@@ -1,0 +1,176 @@
+/* acegpu.h — the C ABI of the B200-native ACE Prove phase (libacegpu.so).
+ *
+ * Drop-in boundary. The reference has no FFI: its Prove phase is the C++
+ * header proj/include/ace/prover.hpp (+ crypto.hpp:84-121, hkdf.hpp:9-18,
+ * wire.hpp:85-116, sha256.hpp:50-58), statically linked. This ABI is what a
+ * replacement prover.cpp binds (paper_2603_10242_b200/dropin/prover_b200.cpp,
+ * see INTEGRATION.md), and what the Python mirror binds via ctypes. Plain
+ * pointers and sizes; no C++ or torch types; status codes instead of
+ * exceptions (the C++ shim maps ACEGPU_EINVAL -> std::invalid_argument).
+ *
+ * Flat layouts (identical in oracle/ace_oracle.h):
+ *   payloads      concatenated payload bytes; tx i = payloads[offs[i], offs[i+1])
+ *   offs          n+1 uint64 offsets (offs[0] normally 0)
+ *   atts          n x 104 B Attestation::encode (crypto.cpp:56-65):
+ *                 obj_hash(32) | id_com(32) | domain(8) | credential(32)
+ *   header        256 B BlockHeader::encode (wire.cpp:74-98); slot = bytes 0..8 BE
+ *   proof         289 B MockProof = bytes(256) | public_inputs_digest(32) | kind(1),
+ *                 kind 0 = ProofKind::Tx, 1 = ProofKind::Aggregate (prover.hpp:33-43)
+ *   fc            328 B FinalityCertificate::encode (wire.cpp:125-133)
+ *   revs          table of 32-B REVs; rev_index[i] selects tx i's REV
+ *   codes         AttestationCheck: 0 Accept, 1 PayloadMismatch, 2 CredentialMismatch
+ *                 (crypto.hpp:84-88)
+ *
+ * Host-pointer functions ("*" without _dev) copy inputs host->device, run
+ * and copy results back; they are synchronous and thread-safe per context
+ * (calls on one context serialise, like ThreadPool::job_mu_ in
+ * thread_pool.hpp:40-49). `_dev` functions take DEVICE pointers and a
+ * cudaStream_t (as void*, NULL = the context's stream), enqueue only, and
+ * never synchronise. Device byte buffers must be 16-B aligned (cudaMalloc).
+ */
+#ifndef ACEGPU_H
+#define ACEGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ACEGPU_OK 0
+#define ACEGPU_EINVAL (-1) /* std::invalid_argument in the reference */
+#define ACEGPU_ECUDA (-2)  /* CUDA error; acegpu_last_error() has the text */
+#define ACEGPU_ENODEV (-3) /* no usable sm_100 device */
+
+typedef struct acegpu_ctx acegpu_ctx;
+
+/* Message of the last failing call on this thread. */
+const char* acegpu_last_error(void);
+/* Build identity, e.g. "acegpu sm_100a <git describe>". */
+const char* acegpu_version(void);
+
+/* One context per device (one process per GPU; torch.distributed plumbing). */
+int acegpu_create(int device, acegpu_ctx** out);
+void acegpu_destroy(acegpu_ctx* ctx);
+/* Kernel launches issued by this context so far (telemetry / bench). */
+uint64_t acegpu_launch_count(const acegpu_ctx* ctx);
+/* Per-phase CUDA-event timing of the block pipeline (on the launching
+ * stream): ms3 = {leaves(+attestation), tree levels, finalize} of the most
+ * recent attest_prove_certify call. */
+int acegpu_set_phase_timing(acegpu_ctx* ctx, int enable);
+int acegpu_phase_times(acegpu_ctx* ctx, float* ms3);
+/* Pinned host memory for fast host<->device copies. */
+void* acegpu_host_alloc(size_t bytes);
+void acegpu_host_free(void* p);
+
+/* ---- SHA-256 (replaces sha256::digest / hash_batch_strided, sha256.hpp:42-58) */
+int acegpu_sha256_varlen(acegpu_ctx* ctx, const uint8_t* data, const uint64_t* offs, uint64_t n,
+                         uint8_t* out32);
+int acegpu_sha256_strided(acegpu_ctx* ctx, const uint8_t* base, uint64_t stride, uint64_t msg_len,
+                          uint64_t n, uint8_t* out32);
+
+/* ---- mock prover (prover.hpp:52-79) --------------------------------------- */
+/* prove_public_inputs (prover.cpp:78-85), batched: pubs = n x 160 B (5 words). */
+int acegpu_prove_public_inputs(acegpu_ctx* ctx, const uint8_t* pubs160, uint64_t n,
+                               uint8_t* out289);
+/* prove_tx (prover.cpp:87-89), batched over a flat tx list. */
+int acegpu_prove_txs(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                     const uint8_t* atts, uint64_t n, uint8_t* out289);
+/* verify_mock (prover.cpp:91-95), batched: ok[i] in {0,1}. */
+int acegpu_verify_mock(acegpu_ctx* ctx, const uint8_t* proofs289, uint64_t n, uint8_t* ok);
+/* aggregate_pair (prover.cpp:97-104), batched: out[i] = pair(a[i], b[i]). */
+int acegpu_aggregate_pairs(acegpu_ctx* ctx, const uint8_t* a289, const uint8_t* b289, uint64_t n,
+                           uint8_t* out289);
+/* aggregate_tree (prover.cpp:106-127). n == 0 -> ACEGPU_EINVAL. */
+int acegpu_aggregate_tree(acegpu_ctx* ctx, const uint8_t* proofs289, uint64_t n, uint8_t* out289,
+                          uint64_t* levels, uint64_t* pair_ops);
+/* prove_block (prover.cpp:129-142). */
+int acegpu_prove_block(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                       const uint8_t* atts, uint64_t n, const uint8_t* header256, uint8_t* out289,
+                       uint64_t* levels, uint64_t* pair_ops);
+/* build_finality_certificate (prover.cpp:144-156). */
+int acegpu_build_fc(acegpu_ctx* ctx, const uint8_t* atts, uint64_t n, const uint8_t* header256,
+                    const uint8_t* proof289, uint8_t* out_fc328);
+/* verify_finality_certificate (prover.cpp:158-169): *out_check = FcCheck
+ * (0 Valid, 1 SlotMismatch, 2 HashMismatch, 3 ProofMismatch). */
+int acegpu_verify_fc(acegpu_ctx* ctx, const uint8_t* fc328, const uint8_t* payloads,
+                     const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                     const uint8_t* header256, int* out_check);
+/* merkle_root (wire.cpp:223-255); block_hash (wire.cpp:214-221). */
+int acegpu_merkle_root(acegpu_ctx* ctx, const uint8_t* leaves32, uint64_t n, uint8_t* out32);
+int acegpu_block_hash(acegpu_ctx* ctx, const uint8_t* header256, uint8_t* out32);
+
+/* The Phase-2 step (ProverService::run body, prover.cpp:350-351) with the
+ * batched full attestation check fused in (crypto.cpp:141-154): per tx
+ * verdict into codes (NULL = skip attestation), the block's root proof and
+ * its finality certificate. Either output may be NULL. */
+int acegpu_attest_prove_certify(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                                const uint8_t* atts, uint64_t n, const uint8_t* header256,
+                                const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,
+                                uint8_t* codes, uint8_t* out289, uint8_t* out_fc328,
+                                uint64_t* levels, uint64_t* pair_ops);
+int acegpu_attest_prove_certify_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
+                                    const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
+                                    const uint8_t* d_header256, const uint8_t* d_revs,
+                                    const uint32_t* d_rev_index, uint8_t* d_codes,
+                                    uint8_t* d_out289, uint8_t* d_out_fc328);
+
+/* ---- multi-GPU sharding (power-of-two aligned chunks) -------- */
+/* Reduce one rank's shard (txs [start, start+n) of an n_total-tx block, start
+ * a multiple of 2^log2_chunk) to its chunk roots: ceil(n / 2^log2_chunk)
+ * proofs (289 B) and Merkle nodes (32 B) of level log2_chunk of the global
+ * trees. The last block chunk's Merkle node is lifted by self-pairing when
+ * n_total > 2^log2_chunk, so that chunk roots combine exactly like the global
+ * tree (prover.cpp:112-124 promotes, wire.cpp:240 duplicates). */
+int acegpu_shard_roots_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
+                           const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
+                           uint64_t n_total, uint32_t log2_chunk, const uint8_t* d_revs,
+                           const uint32_t* d_rev_index, uint8_t* d_codes, uint8_t* d_roots289,
+                           uint8_t* d_merkle32);
+/* Combine the ordered chunk roots of all ranks into the block proof + FC. */
+int acegpu_combine_roots_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_roots289,
+                             const uint8_t* d_merkle32, uint64_t n_chunks, uint64_t n_total,
+                             const uint8_t* d_header256, uint8_t* d_out289, uint8_t* d_out_fc328);
+
+/* ---- attestation (crypto.hpp:113-118) ------------------------------------ */
+int acegpu_attest_verify(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                         const uint8_t* atts, uint64_t n, const uint8_t* revs, uint64_t n_revs,
+                         const uint32_t* rev_index, uint8_t* codes);
+/* generate_attestation (crypto.cpp:129-139), batched: doms8 = n x 8-B Domain
+ * encodings, id_coms = n x 32. */
+int acegpu_attest_generate(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                           uint64_t n, const uint8_t* revs, uint64_t n_revs,
+                           const uint32_t* rev_index, const uint8_t* doms8,
+                           const uint8_t* id_coms, uint8_t* out104);
+int acegpu_attest_generate_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
+                               const uint64_t* d_offs, uint64_t n, const uint8_t* d_revs,
+                               const uint32_t* d_rev_index, const uint8_t* d_doms8,
+                               const uint8_t* d_id_coms, uint8_t* d_out104);
+/* derive_attest_key (crypto.cpp:124-127), batched over (REV, domain) pairs. */
+int acegpu_derive_attest_keys(acegpu_ctx* ctx, const uint8_t* revs32, const uint8_t* doms8,
+                              uint64_t n, uint8_t* out32);
+
+/* ---- witnesses (prover.hpp:81-137) ---------------------------------------- */
+/* witness_matches_tx (prover.cpp:190-197): witnesses n x 256 B; wlens may be
+ * NULL (all 256) — a length other than 256 fails like the reference. */
+int acegpu_witness_check(acegpu_ctx* ctx, const uint8_t* witnesses, const uint32_t* wlens,
+                         const uint8_t* atts, uint64_t n, uint8_t* ok);
+/* build_witness (prover.cpp:181-188), batched. */
+int acegpu_build_witness(acegpu_ctx* ctx, const uint8_t* keys32, const uint8_t* tx_hashes32,
+                         uint64_t n, uint8_t* out256);
+/* WitnessScheme encapsulate / decrypt (prover.cpp:229-264): out = in XOR
+ * keystream(XOR of share values selected by share_masks[i]); len bytes each. */
+int acegpu_witness_xor(acegpu_ctx* ctx, const uint8_t* master32, const uint8_t* tx_hashes32,
+                       const uint64_t* share_masks, const uint8_t* in, uint64_t len, uint64_t n,
+                       uint8_t* out);
+
+/* ---- measurement ----------------------------------------------------------- */
+/* SHA-256 compressions/s of a register-resident chain over the whole GPU (the
+ * integer-ALU roofline of the mock path). */
+int acegpu_sha256_peak(acegpu_ctx* ctx, double* compressions_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,881 @@
+// The C ABI of include/acegpu.h: contexts, device workspaces, host<->device
+// marshalling and the pipelines that chain the mock-Prove kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/acegpu.h"
+#include "mock_kernels.cuh"
+
+#ifndef ACEGPU_GIT
+#define ACEGPU_GIT "dev"
+#endif
+
+using namespace ace_gpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(expr)                                                                        \
+    do {                                                                                \
+        cudaError_t _e = (expr);                                                        \
+        if (_e != cudaSuccess)                                                          \
+            return fail(ACEGPU_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define CKL()                                                                           \
+    do {                                                                                \
+        cudaError_t _e = cudaGetLastError();                                            \
+        if (_e != cudaSuccess)                                                          \
+            return fail(ACEGPU_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+    } while (0)
+
+#define RET(expr)                   \
+    do {                            \
+        int _r = (expr);            \
+        if (_r != ACEGPU_OK) return _r; \
+    } while (0)
+
+enum Slot {
+    kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
+    kBlockHash, kOut, kIn2, kMisc, kNumSlots
+};
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+uint32_t ceil_log2(uint64_t n) {
+    uint32_t l = 0;
+    while ((1ull << l) < n) ++l;
+    return l;
+}
+
+}  // namespace
+
+struct acegpu_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    std::mutex mu;
+    std::atomic<uint64_t> launches{0};
+    DevBuf bufs[kNumSlots];
+    // Optional per-phase CUDA events (leaves | levels | finalize) recorded on
+    // the launching stream by the block pipeline.
+    bool timing = false;
+    bool ev_recorded = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Grow-only device workspace. Growth synchronises the device (the old buffer
+// may still be read by in-flight work on any stream).
+int ensure(acegpu_ctx* c, Slot s, size_t bytes, void** out) {
+    DevBuf& b = c->bufs[s];
+    if (bytes == 0) bytes = 16;
+    if (b.cap < bytes) {
+        if (b.p) {
+            CK(cudaDeviceSynchronize());
+            CK(cudaFree(b.p));
+            b.p = nullptr;
+            b.cap = 0;
+        }
+        size_t cap = std::max(bytes + 64, b.cap * 3 / 2);
+        CK(cudaMalloc(&b.p, cap));
+        b.cap = cap;
+    }
+    *out = b.p;
+    return ACEGPU_OK;
+}
+
+template <class T>
+int ws(acegpu_ctx* c, Slot s, size_t bytes, T** out) {
+    void* p = nullptr;
+    RET(ensure(c, s, bytes, &p));
+    *out = static_cast<T*>(p);
+    return ACEGPU_OK;
+}
+
+int h2d(acegpu_ctx* c, Slot s, const void* src, size_t bytes, cudaStream_t st, void** out) {
+    RET(ensure(c, s, bytes, out));
+    if (bytes) CK(cudaMemcpyAsync(*out, src, bytes, cudaMemcpyHostToDevice, st));
+    return ACEGPU_OK;
+}
+
+template <class T>
+int h2d_t(acegpu_ctx* c, Slot s, const T* src, size_t bytes, cudaStream_t st, T** out) {
+    void* p = nullptr;
+    RET(h2d(c, s, src, bytes, st, &p));
+    *out = static_cast<T*>(p);
+    return ACEGPU_OK;
+}
+
+cudaStream_t pick(acegpu_ctx* c, void* stream) {
+    return stream ? static_cast<cudaStream_t>(stream) : c->stream;
+}
+
+struct TreeResult {
+    uint8_t* nodes = nullptr;   // level nodes (320 B each)
+    uint8_t* merkle = nullptr;  // level merkle nodes (32 B each)
+    uint8_t* bh = nullptr;      // block hash (when a header was given)
+    uint32_t count = 0;
+};
+
+// Leaves (+attestation verdicts, merkle leaves, header hash) and up to
+// `max_levels` fused proof/merkle levels. With lift, a lone merkle node keeps
+// self-pairing until max_levels (aligned-chunk roots).
+int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
+             const uint8_t* atts, uint32_t n, const uint8_t* header, const uint8_t* revs,
+             const uint32_t* rev_index, uint8_t* codes, bool prove, uint32_t max_levels,
+             bool lift, TreeResult* r) {
+    uint8_t *na = nullptr, *nb = nullptr, *ma = nullptr, *mb = nullptr, *bh = nullptr;
+    const size_t half = n / 2 + 1;
+    if (prove) {
+        RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &na));
+        RET(ws(c, kNodesB, size_t(kNodeBytes) * half, &nb));
+    }
+    RET(ws(c, kMerkA, 32ull * n, &ma));
+    RET(ws(c, kMerkB, 32ull * half, &mb));
+    RET(ws(c, kBlockHash, 32, &bh));
+    LeafArgs a{};
+    a.payloads = payloads;
+    a.offs = offs;
+    a.atts = atts;
+    a.n = n;
+    a.revs = revs;
+    a.rev_index = rev_index;
+    a.codes = codes;
+    a.nodes = prove ? na : nullptr;
+    a.merkle = ma;
+    a.header = header;
+    a.block_hash = bh;
+    if (c->timing) CK(cudaEventRecord(c->ev[0], s));
+    if (n || header) {
+        launch_leaves(a, s);
+        CKL();
+        c->launches++;
+    }
+    if (c->timing) CK(cudaEventRecord(c->ev[1], s));
+    uint32_t cur = n, lv = 0;
+    uint8_t *nin = na, *nout = nb, *min_ = ma, *mout = mb;
+    while (lv < max_levels && (cur > 1 || (lift && cur == 1))) {
+        launch_level(prove ? nin : nullptr, cur, nout, min_, cur, mout, lift, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        std::swap(nin, nout);
+        std::swap(min_, mout);
+        ++lv;
+    }
+    if (c->timing) CK(cudaEventRecord(c->ev[2], s));
+    r->nodes = nin;
+    r->merkle = min_;
+    r->bh = bh;
+    r->count = cur;
+    return ACEGPU_OK;
+}
+
+int check_n(uint64_t n) {
+    if (n > 0xFFFFFFFFull / kNodeBytes) return fail(ACEGPU_EINVAL, "batch too large");
+    return ACEGPU_OK;
+}
+
+// Whole-block pipeline on device buffers: -> proof289 + fc328 (either may be null).
+int block_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
+                   const uint8_t* atts, uint32_t n, const uint8_t* header, const uint8_t* revs,
+                   const uint32_t* rev_index, uint8_t* codes, uint8_t* out289, uint8_t* out328) {
+    TreeResult t;
+    RET(run_tree(c, s, payloads, offs, atts, n, header, revs, rev_index, codes, true, 64, false,
+                 &t));
+    launch_finalize(t.nodes, n ? t.merkle : nullptr, header, t.bh, n == 0, out289, out328, s);
+    CKL();
+    c->launches++;
+    if (c->timing) {
+        CK(cudaEventRecord(c->ev[3], s));
+        c->ev_recorded = true;
+    }
+    return ACEGPU_OK;
+}
+
+struct HostBlock {
+    const uint8_t* payloads;
+    const uint64_t* offs;
+    const uint8_t* atts;
+    uint64_t n;
+};
+
+// Upload a flat block; returns device pointers (payload offsets are kept as given).
+int upload_block(acegpu_ctx* c, cudaStream_t s, const HostBlock& h, uint8_t** dp, uint64_t** doff,
+                 uint8_t** da) {
+    if (h.n == 0) {  // empty block: inputs may be NULL
+        RET(ws(c, kPayloads, 16, dp));
+        RET(ws(c, kOffs, 16, doff));
+        RET(ws(c, kAtts, 16, da));
+        return ACEGPU_OK;
+    }
+    const uint64_t pbytes = h.offs[h.n];
+    RET(h2d_t(c, kPayloads, h.payloads, pbytes, s, dp));
+    RET(h2d_t(c, kOffs, h.offs, 8 * (h.n + 1), s, doff));
+    RET(h2d_t(c, kAtts, h.atts, 104 * h.n, s, da));
+    return ACEGPU_OK;
+}
+
+}  // namespace
+
+// =========================================================================
+extern "C" {
+
+const char* acegpu_last_error(void) { return g_err.c_str(); }
+
+const char* acegpu_version(void) { return "acegpu sm_100a " ACEGPU_GIT; }
+
+int acegpu_create(int device, acegpu_ctx** out) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        return fail(ACEGPU_ENODEV, "no CUDA device");
+    }
+    if (device < 0 || device >= count) return fail(ACEGPU_ENODEV, "bad device index");
+    cudaDeviceProp prop{};
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) {
+        return fail(ACEGPU_ENODEV, std::string("libacegpu is built for sm_100a; device is ") +
+                                       prop.name);
+    }
+    DeviceGuard g(device);
+    auto* c = new acegpu_ctx();
+    c->device = device;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(ACEGPU_ECUDA, cudaGetErrorString(e));
+    }
+    *out = c;
+    return ACEGPU_OK;
+}
+
+void acegpu_destroy(acegpu_ctx* c) {
+    if (!c) return;
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& b : c->bufs)
+        if (b.p) cudaFree(b.p);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+uint64_t acegpu_launch_count(const acegpu_ctx* c) { return c ? c->launches.load() : 0; }
+
+int acegpu_set_phase_timing(acegpu_ctx* c, int enable) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    if (enable && !c->ev[0]) {
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    }
+    c->timing = enable != 0;
+    c->ev_recorded = false;
+    return ACEGPU_OK;
+}
+
+int acegpu_phase_times(acegpu_ctx* c, float* ms3) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (!c->timing || !c->ev_recorded) return fail(ACEGPU_EINVAL, "no timed block pipeline yet");
+    DeviceGuard g(c->device);
+    CK(cudaEventSynchronize(c->ev[3]));
+    for (int i = 0; i < 3; ++i) CK(cudaEventElapsedTime(&ms3[i], c->ev[i], c->ev[i + 1]));
+    return ACEGPU_OK;
+}
+
+void* acegpu_host_alloc(size_t bytes) {
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes ? bytes : 1) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+
+void acegpu_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
+// ---------------------------------------------------------------- SHA-256
+int acegpu_sha256_varlen(acegpu_ctx* c, const uint8_t* data, const uint64_t* offs, uint64_t n,
+                         uint8_t* out) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t* dd;
+    uint64_t* doff;
+    uint8_t* dout;
+    RET(h2d_t(c, kPayloads, data, offs[n], s, &dd));
+    RET(h2d_t(c, kOffs, offs, 8 * (n + 1), s, &doff));
+    RET(ws(c, kOut, 32 * n, &dout));
+    launch_sha256_varlen(dd, doff, uint32_t(n), dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_sha256_strided(acegpu_ctx* c, const uint8_t* base, uint64_t stride, uint64_t len,
+                          uint64_t n, uint8_t* out) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    if (len > 0xFFFFFFFFull) return fail(ACEGPU_EINVAL, "message too long");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dd, *dout;
+    RET(h2d_t(c, kPayloads, base, stride * (n - 1) + len, s, &dd));
+    RET(ws(c, kOut, 32 * n, &dout));
+    launch_sha256_strided(dd, stride, uint32_t(len), uint32_t(n), dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+// ------------------------------------------------------------ mock prover
+int acegpu_prove_public_inputs(acegpu_ctx* c, const uint8_t* pubs, uint64_t n, uint8_t* out289) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *nodes, *dout;
+    RET(h2d_t(c, kIn2, pubs, 160 * n, s, &dp));
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &nodes));
+    RET(ws(c, kOut, 289 * n, &dout));
+    launch_prove_public_inputs(dp, uint32_t(n), nodes, s);
+    launch_pack_nodes(nodes, uint32_t(n), dout, s);
+    CKL();
+    c->launches += 2;
+    CK(cudaMemcpyAsync(out289, dout, 289 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_prove_txs(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                     const uint8_t* atts, uint64_t n, uint8_t* out289) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *da, *nodes, *dout;
+    uint64_t* doff;
+    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &nodes));
+    RET(ws(c, kOut, 289 * n, &dout));
+    LeafArgs a{};
+    a.payloads = dp;
+    a.offs = doff;
+    a.atts = da;
+    a.n = uint32_t(n);
+    a.nodes = nodes;
+    launch_leaves(a, s);
+    launch_pack_nodes(nodes, uint32_t(n), dout, s);
+    CKL();
+    c->launches += 2;
+    CK(cudaMemcpyAsync(out289, dout, 289 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_verify_mock(acegpu_ctx* c, const uint8_t* proofs, uint64_t n, uint8_t* ok) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *nodes, *dok;
+    RET(h2d_t(c, kIn2, proofs, 289 * n, s, &dp));
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &nodes));
+    RET(ws(c, kOut, n, &dok));
+    launch_unpack_nodes(dp, uint32_t(n), nodes, s);
+    launch_verify_mock(nodes, uint32_t(n), dok, s);
+    CKL();
+    c->launches += 2;
+    CK(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_aggregate_pairs(acegpu_ctx* c, const uint8_t* a289, const uint8_t* b289, uint64_t n,
+                           uint8_t* out289) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *da, *db, *na, *nb, *dout;
+    RET(h2d_t(c, kIn2, a289, 289 * n, s, &da));
+    RET(h2d_t(c, kMisc, b289, 289 * n, s, &db));
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * 2 * n, &na));
+    RET(ws(c, kNodesB, size_t(kNodeBytes) * n, &nb));
+    RET(ws(c, kOut, 289 * n, &dout));
+    launch_unpack_nodes(da, uint32_t(n), na, s);
+    launch_unpack_nodes(db, uint32_t(n), na + size_t(kNodeBytes) * n, s);
+    launch_aggregate_pairs(na, na + size_t(kNodeBytes) * n, uint32_t(n), nb, s);
+    launch_pack_nodes(nb, uint32_t(n), dout, s);
+    CKL();
+    c->launches += 4;
+    CK(cudaMemcpyAsync(out289, dout, 289 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_aggregate_tree(acegpu_ctx* c, const uint8_t* proofs, uint64_t n, uint8_t* out289,
+                          uint64_t* levels, uint64_t* pair_ops) {
+    if (n == 0) return fail(ACEGPU_EINVAL, "aggregate_tree: empty proof list");
+    RET(check_n(n));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *na, *nb, *dout;
+    RET(h2d_t(c, kIn2, proofs, 289 * n, s, &dp));
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &na));
+    RET(ws(c, kNodesB, size_t(kNodeBytes) * (n / 2 + 1), &nb));
+    RET(ws(c, kOut, 289, &dout));
+    launch_unpack_nodes(dp, uint32_t(n), na, s);
+    CKL();
+    c->launches++;
+    uint32_t cur = uint32_t(n);
+    while (cur > 1) {
+        launch_level(na, cur, nb, nullptr, 0, nullptr, false, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        std::swap(na, nb);
+    }
+    launch_pack_nodes(na, 1, dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out289, dout, 289, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (levels) *levels = ceil_log2(n);
+    if (pair_ops) *pair_ops = n - 1;
+    return ACEGPU_OK;
+}
+
+int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                                const uint8_t* atts, uint64_t n, const uint8_t* header,
+                                const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,
+                                uint8_t* codes, uint8_t* out289, uint8_t* out328,
+                                uint64_t* levels, uint64_t* pair_ops) {
+    RET(check_n(n));
+    if (codes && n && (!revs || !rev_index || n_revs == 0))
+        return fail(ACEGPU_EINVAL, "attestation needs a REV table and index");
+    if (codes && n) {
+        for (uint64_t i = 0; i < n; ++i)
+            if (rev_index[i] >= n_revs) return fail(ACEGPU_EINVAL, "rev_index out of range");
+    }
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *da, *dh, *dout, *dr = nullptr, *dc = nullptr;
+    uint64_t* doff;
+    uint32_t* dri = nullptr;
+    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+    RET(h2d_t(c, kHeader, header, 256, s, &dh));
+    if (codes && n) {
+        RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+        RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
+        RET(ws(c, kCodes, n, &dc));
+    }
+    RET(ws(c, kOut, 289 + 328 + 16, &dout));
+    RET(block_pipeline(c, s, dp, doff, da, uint32_t(n), dh, dr, dri, dc, dout, dout + 304));
+    if (dc) CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
+    if (out289) CK(cudaMemcpyAsync(out289, dout, 289, cudaMemcpyDeviceToHost, s));
+    if (out328) CK(cudaMemcpyAsync(out328, dout + 304, 328, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (levels) *levels = n ? ceil_log2(n) : 0;
+    if (pair_ops) *pair_ops = n ? n - 1 : 0;
+    return ACEGPU_OK;
+}
+
+int acegpu_attest_prove_certify_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                                    const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                                    const uint8_t* header, const uint8_t* revs,
+                                    const uint32_t* rev_index, uint8_t* codes, uint8_t* out289,
+                                    uint8_t* out328) {
+    RET(check_n(n));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return block_pipeline(c, pick(c, stream), payloads, offs, atts, uint32_t(n), header, revs,
+                          rev_index, n ? codes : nullptr, out289, out328);
+}
+
+int acegpu_prove_block(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                       const uint8_t* atts, uint64_t n, const uint8_t* header, uint8_t* out289,
+                       uint64_t* levels, uint64_t* pair_ops) {
+    return acegpu_attest_prove_certify(c, payloads, offs, atts, n, header, nullptr, 0, nullptr,
+                                       nullptr, out289, nullptr, levels, pair_ops);
+}
+
+int acegpu_build_fc(acegpu_ctx* c, const uint8_t* atts, uint64_t n, const uint8_t* header,
+                    const uint8_t* proof289, uint8_t* out328) {
+    RET(check_n(n));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *da, *dh, *dproof, *node, *dout;
+    RET(h2d_t(c, kAtts, atts, 104 * n, s, &da));
+    RET(h2d_t(c, kHeader, header, 256, s, &dh));
+    RET(h2d_t(c, kIn2, proof289, 289, s, &dproof));
+    RET(ws(c, kMisc, kNodeBytes, &node));
+    RET(ws(c, kOut, 328, &dout));
+    launch_unpack_nodes(dproof, 1, node, s);
+    CKL();
+    c->launches++;
+    TreeResult t;
+    RET(run_tree(c, s, nullptr, nullptr, da, uint32_t(n), dh, nullptr, nullptr, nullptr, false,
+                 64, false, &t));
+    launch_finalize(node, n ? t.merkle : nullptr, dh, t.bh, false, nullptr, dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out328, dout, 328, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_verify_fc(acegpu_ctx* c, const uint8_t* fc, const uint8_t* payloads,
+                     const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                     const uint8_t* header, int* out_check) {
+    // prover.cpp:158-169: slot, then block hash, then the full recompute.
+    if (std::memcmp(fc + 32, header, 8) != 0) {
+        *out_check = 1;
+        return ACEGPU_OK;
+    }
+    uint8_t expect[328];
+    RET(acegpu_attest_prove_certify(c, payloads, offs, atts, n, header, nullptr, 0, nullptr,
+                                    nullptr, nullptr, expect, nullptr, nullptr));
+    if (std::memcmp(expect, fc, 32) != 0) *out_check = 2;
+    else if (std::memcmp(expect + 40, fc + 40, 256) != 0) *out_check = 3;
+    else if (std::memcmp(expect + 296, fc + 296, 32) != 0) *out_check = 3;
+    else *out_check = 0;
+    return ACEGPU_OK;
+}
+
+int acegpu_merkle_root(acegpu_ctx* c, const uint8_t* leaves, uint64_t n, uint8_t* out32) {
+    RET(check_n(n));
+    if (n == 0) {
+        std::memset(out32, 0, 32);
+        return ACEGPU_OK;
+    }
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dl, *ma, *mb;
+    RET(h2d_t(c, kIn2, leaves, 32 * n, s, &dl));
+    RET(ws(c, kMerkA, 32 * n, &ma));
+    RET(ws(c, kMerkB, 32 * (n / 2 + 1), &mb));
+    launch_merkle_leaves(dl, uint32_t(n), ma, s);
+    CKL();
+    c->launches++;
+    uint32_t cur = uint32_t(n);
+    while (cur > 1) {
+        launch_level(nullptr, 0, nullptr, ma, cur, mb, false, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        std::swap(ma, mb);
+    }
+    CK(cudaMemcpyAsync(out32, ma, 32, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_block_hash(acegpu_ctx* c, const uint8_t* header, uint8_t* out32) {
+    return acegpu_sha256_strided(c, header, 256, 256, 1, out32);
+}
+
+// ------------------------------------------------------------- sharding
+int acegpu_shard_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                           const uint64_t* offs, const uint8_t* atts, uint64_t n, uint64_t n_total,
+                           uint32_t log2_chunk, const uint8_t* revs, const uint32_t* rev_index,
+                           uint8_t* codes, uint8_t* roots289, uint8_t* merkle32) {
+    RET(check_n(n));
+    if (n == 0 || log2_chunk > 31) return fail(ACEGPU_EINVAL, "empty shard or chunk too large");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    const bool lift = n_total > (1ull << log2_chunk);
+    TreeResult t;
+    RET(run_tree(c, s, payloads, offs, atts, uint32_t(n), nullptr, revs, rev_index, codes, true,
+                 log2_chunk, lift, &t));
+    const uint64_t chunks = (n + (1ull << log2_chunk) - 1) >> log2_chunk;
+    if (t.count != chunks) return fail(ACEGPU_EINVAL, "internal: chunk count mismatch");
+    launch_pack_nodes(t.nodes, t.count, roots289, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(merkle32, t.merkle, 32ull * t.count, cudaMemcpyDeviceToDevice, s));
+    return ACEGPU_OK;
+}
+
+int acegpu_combine_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* roots289,
+                             const uint8_t* merkle32, uint64_t n_chunks, uint64_t n_total,
+                             const uint8_t* header, uint8_t* out289, uint8_t* out328) {
+    RET(check_n(n_chunks));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    uint8_t *na, *nb, *ma, *mb, *bh;
+    RET(ws(c, kBlockHash, 32, &bh));
+    launch_sha256_strided(header, 256, 256, 1, bh, s);
+    CKL();
+    c->launches++;
+    if (n_total == 0 || n_chunks == 0) {
+        launch_finalize(nullptr, nullptr, header, bh, true, out289, out328, s);
+        CKL();
+        c->launches++;
+        return ACEGPU_OK;
+    }
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n_chunks, &na));
+    RET(ws(c, kNodesB, size_t(kNodeBytes) * (n_chunks / 2 + 1), &nb));
+    RET(ws(c, kMerkA, 32 * n_chunks, &ma));
+    RET(ws(c, kMerkB, 32 * (n_chunks / 2 + 1), &mb));
+    launch_unpack_nodes(roots289, uint32_t(n_chunks), na, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(ma, merkle32, 32 * n_chunks, cudaMemcpyDeviceToDevice, s));
+    uint32_t cur = uint32_t(n_chunks);
+    while (cur > 1) {
+        launch_level(na, cur, nb, ma, cur, mb, false, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        std::swap(na, nb);
+        std::swap(ma, mb);
+    }
+    launch_finalize(na, ma, header, bh, false, out289, out328, s);
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
+}
+
+// ------------------------------------------------------------ attestation
+int acegpu_attest_verify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                         const uint8_t* atts, uint64_t n, const uint8_t* revs, uint64_t n_revs,
+                         const uint32_t* rev_index, uint8_t* codes) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    if (!revs || !rev_index || n_revs == 0) return fail(ACEGPU_EINVAL, "REV table required");
+    for (uint64_t i = 0; i < n; ++i)
+        if (rev_index[i] >= n_revs) return fail(ACEGPU_EINVAL, "rev_index out of range");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *da, *dr, *dc;
+    uint64_t* doff;
+    uint32_t* dri;
+    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+    RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+    RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
+    RET(ws(c, kCodes, n, &dc));
+    LeafArgs a{};
+    a.payloads = dp;
+    a.offs = doff;
+    a.atts = da;
+    a.n = uint32_t(n);
+    a.revs = dr;
+    a.rev_index = dri;
+    a.codes = dc;
+    launch_leaves(a, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_attest_generate_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                               const uint64_t* offs, uint64_t n, const uint8_t* revs,
+                               const uint32_t* rev_index, const uint8_t* doms8,
+                               const uint8_t* id_coms, uint8_t* out104) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    DeviceGuard g(c->device);
+    launch_attest_generate(payloads, offs, uint32_t(n), revs, rev_index, doms8, id_coms, out104,
+                           pick(c, stream));
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
+}
+
+int acegpu_attest_generate(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                           uint64_t n, const uint8_t* revs, uint64_t n_revs,
+                           const uint32_t* rev_index, const uint8_t* doms8,
+                           const uint8_t* id_coms, uint8_t* out104) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    for (uint64_t i = 0; i < n; ++i)
+        if (rev_index[i] >= n_revs) return fail(ACEGPU_EINVAL, "rev_index out of range");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *dr, *dd, *di, *dout;
+    uint64_t* doff;
+    uint32_t* dri;
+    RET(h2d_t(c, kPayloads, payloads, offs[n], s, &dp));
+    RET(h2d_t(c, kOffs, offs, 8 * (n + 1), s, &doff));
+    RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+    RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
+    RET(h2d_t(c, kIn2, doms8, 8 * n, s, &dd));
+    RET(h2d_t(c, kMisc, id_coms, 32 * n, s, &di));
+    RET(ws(c, kOut, 104 * n, &dout));
+    launch_attest_generate(dp, doff, uint32_t(n), dr, dri, dd, di, dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out104, dout, 104 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_derive_attest_keys(acegpu_ctx* c, const uint8_t* revs, const uint8_t* doms8,
+                              uint64_t n, uint8_t* out32) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dr, *dd, *dout;
+    RET(h2d_t(c, kRevs, revs, 32 * n, s, &dr));
+    RET(h2d_t(c, kIn2, doms8, 8 * n, s, &dd));
+    RET(ws(c, kOut, 32 * n, &dout));
+    launch_derive_attest_keys(dr, dd, uint32_t(n), dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out32, dout, 32 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+// --------------------------------------------------------------- witnesses
+int acegpu_witness_check(acegpu_ctx* c, const uint8_t* w, const uint32_t* wlens,
+                         const uint8_t* atts, uint64_t n, uint8_t* ok) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dw, *da, *dok;
+    uint32_t* dl = nullptr;
+    RET(h2d_t(c, kIn2, w, 256 * n, s, &dw));
+    RET(h2d_t(c, kAtts, atts, 104 * n, s, &da));
+    if (wlens) RET(h2d_t(c, kRevIdx, wlens, 4 * n, s, &dl));
+    RET(ws(c, kOut, n, &dok));
+    launch_witness_check(dw, dl, da, uint32_t(n), dok, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(ok, dok, n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_build_witness(acegpu_ctx* c, const uint8_t* keys, const uint8_t* txh, uint64_t n,
+                         uint8_t* out) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dk, *dt, *dout;
+    RET(h2d_t(c, kIn2, keys, 32 * n, s, &dk));
+    RET(h2d_t(c, kMisc, txh, 32 * n, s, &dt));
+    RET(ws(c, kOut, 256 * n, &dout));
+    launch_build_witness(dk, dt, uint32_t(n), dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, 256 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_witness_xor(acegpu_ctx* c, const uint8_t* master, const uint8_t* txh,
+                       const uint64_t* masks, const uint8_t* in, uint64_t len, uint64_t n,
+                       uint8_t* out) {
+    RET(check_n(n));
+    if (n == 0 || len == 0) return ACEGPU_OK;
+    if (len > (1u << 20)) return fail(ACEGPU_EINVAL, "witness too long");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dm, *dt, *din, *dout;
+    uint64_t* dmask;
+    RET(h2d_t(c, kHeader, master, 32, s, &dm));
+    RET(h2d_t(c, kMisc, txh, 32 * n, s, &dt));
+    RET(h2d_t(c, kOffs, masks, 8 * n, s, &dmask));
+    RET(h2d_t(c, kIn2, in, len * n, s, &din));
+    RET(ws(c, kOut, len * n, &dout));
+    launch_witness_xor(dm, dt, dmask, din, uint32_t(len), uint32_t(n), dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, len * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+// ------------------------------------------------------------- measurement
+int acegpu_sha256_peak(acegpu_ctx* c, double* cps) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    uint32_t* sink;
+    RET(ws(c, kMisc, 16, &sink));
+    const int threads = 128, blocks = sms * 8;
+    const uint32_t iters = 1024;
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    launch_sha256_peak(sink, 64, blocks, threads, s);  // warm-up
+    CK(cudaEventRecord(e0, s));
+    launch_sha256_peak(sink, iters, blocks, threads, s);
+    CK(cudaEventRecord(e1, s));
+    CKL();
+    c->launches += 2;
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *cps = double(blocks) * threads * iters / (ms * 1e-3);
+    return ACEGPU_OK;
+}
+
+}  // extern "C"

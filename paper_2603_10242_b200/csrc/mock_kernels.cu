@@ -1,0 +1,581 @@
+// sm_100a kernels for the mock Prove path (reference proj/src/prover.cpp,
+// crypto.cpp, hkdf.cpp, wire.cpp). Integer-ALU bound: every kernel is a batch
+// of independent SHA-256 chains, one chain per thread.
+//
+//   leaf_kernel    K1 (+K4 fused): per tx SHA(payload) -> PublicInputs digest
+//                  -> expand256 = 15 compressions (prover.cpp:65-89); optional
+//                  full attestation verdict sharing the payload hash (+12,
+//                  crypto.cpp:141-154); Merkle leaf H(0x00|id_com) (+1,
+//                  wire.cpp:229-238); an extra CTA hashes the header.
+//   level_kernel   K2+K3: one level of the proof tree (18 compressions/pair,
+//                  prover.cpp:97-124) fused with one Merkle level (2/pair,
+//                  wire.cpp:240-253) in the same launch.
+//   finalize       FC assembly (prover.cpp:144-156, wire.cpp:125-133).
+#include "mock_kernels.cuh"
+#include "sha256.cuh"
+
+namespace ace_gpu {
+
+namespace {
+
+constexpr int kThreads = 128;
+constexpr uint32_t kStageBytes = 192 * kThreads;  // payload staging per CTA (24 KB)
+
+__device__ __forceinline__ void load_be8(const uint8_t* p, uint32_t w[8]) { load_digest(p, w); }
+
+// 8 BE words from an 8-B aligned pointer.
+__device__ __forceinline__ void load_be8_u64(const uint8_t* p, uint32_t w[8]) {
+    const uint2* q = reinterpret_cast<const uint2*>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        uint2 v = q[k];
+        w[2 * k] = bswap32(v.x);
+        w[2 * k + 1] = bswap32(v.y);
+    }
+}
+
+// Merkle leaf H(0x00 | h) (wire.cpp:229-238): 33 B, one compression.
+__device__ __forceinline__ void merkle_leaf(const uint32_t h[8], uint32_t out[8]) {
+    uint32_t w[16];
+    w[0] = h[0] >> 8;
+#pragma unroll
+    for (int k = 1; k < 8; ++k) w[k] = __funnelshift_l(h[k], h[k - 1], 24);
+    w[8] = (h[7] << 24) | 0x00800000u;
+#pragma unroll
+    for (int k = 9; k < 15; ++k) w[k] = 0;
+    w[15] = 33 * 8;
+    sha256_init(out);
+    sha256_compress(out, w);
+}
+
+// Merkle inner node H(0x01 | l | r) (wire.cpp:243-252): 65 B, two compressions.
+__device__ __forceinline__ void merkle_inner(const uint32_t l[8], const uint32_t r[8],
+                                             uint32_t out[8]) {
+    uint32_t w[16];
+    w[0] = 0x01000000u | (l[0] >> 8);
+#pragma unroll
+    for (int k = 1; k < 8; ++k) w[k] = __funnelshift_l(l[k], l[k - 1], 24);
+    w[8] = __funnelshift_l(r[0], l[7], 24);
+#pragma unroll
+    for (int k = 9; k < 16; ++k) w[k] = __funnelshift_l(r[k - 8], r[k - 9], 24);
+    sha256_init(out);
+    sha256_compress(out, w);
+    w[0] = (r[7] << 24) | 0x00800000u;
+#pragma unroll
+    for (int k = 1; k < 15; ++k) w[k] = 0;
+    w[15] = 65 * 8;
+    sha256_compress(out, w);
+}
+
+// aggregate_pair (prover.cpp:97-104): digest = SHA(a.bytes | b.bytes) (512 B:
+// eight data blocks + one constant padding block), bytes = expand256(agg tag).
+__device__ __forceinline__ void pair_digest(const uint8_t* a, const uint8_t* b, uint32_t d[8]) {
+    sha256_init(d);
+#pragma unroll 1
+    for (int blk = 0; blk < 8; ++blk) {
+        const uint4* q = reinterpret_cast<const uint4*>((blk < 4 ? a : b) + 64 * (blk & 3));
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            uint4 v = q[k];
+            w[4 * k] = bswap32(v.x);
+            w[4 * k + 1] = bswap32(v.y);
+            w[4 * k + 2] = bswap32(v.z);
+            w[4 * k + 3] = bswap32(v.w);
+        }
+        sha256_compress(d, w);
+    }
+    uint32_t w[16];
+    w[0] = 0x80000000u;
+#pragma unroll
+    for (int k = 1; k < 15; ++k) w[k] = 0;
+    w[15] = 512 * 8;
+    sha256_compress(d, w);
+}
+
+__device__ __forceinline__ void write_node_tail(uint8_t* node, const uint32_t d[8], uint32_t kind) {
+    store_digest(node + 256, d);
+    *reinterpret_cast<uint4*>(node + 288) = make_uint4(kind, 0, 0, 0);
+}
+
+__device__ __forceinline__ void aggregate_node(const uint8_t* a, const uint8_t* b, uint8_t* out) {
+    uint32_t d[8];
+    pair_digest(a, b, d);
+    expand256_store(1, d, out);
+    write_node_tail(out, d, 1);
+}
+
+__device__ __forceinline__ bool eq8(const uint32_t a[8], const uint32_t b[8]) {
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x |= a[k] ^ b[k];
+    return x == 0;
+}
+
+// ------------------------------------------------------------------ leaves
+__global__ void __launch_bounds__(kThreads) leaf_kernel(LeafArgs a) {
+    __shared__ uint4 stage[kStageBytes / 16];
+    const uint32_t n_tx_blocks = (a.n + kThreads - 1) / kThreads;
+    if (blockIdx.x >= n_tx_blocks) {
+        // The extra CTA: block_hash = SHA-256(256-B header) (wire.cpp:214-221).
+        if (threadIdx.x == 0 && a.header) {
+            uint32_t h[8];
+            sha256_bytes(a.header, 0, 256, h);
+            store_digest(a.block_hash, h);
+        }
+        return;
+    }
+    const uint32_t i0 = blockIdx.x * kThreads;
+    const uint32_t i1 = min(i0 + kThreads, a.n);
+    const bool need_tx = a.codes || a.nodes;  // build_fc needs only the id_coms
+    const uint64_t b0 = need_tx ? a.offs[i0] : 0, b1 = need_tx ? a.offs[i1] : 0;
+    const uint64_t s16 = b0 & ~15ull;
+    const bool staged = need_tx && (b1 - s16) <= kStageBytes;
+    if (staged) {
+        // Coalesced 16-B copy of this CTA's contiguous payload span.
+        const uint32_t nvec = static_cast<uint32_t>((b1 - s16 + 15) >> 4);
+        const uint4* g = reinterpret_cast<const uint4*>(a.payloads) + (s16 >> 4);
+        for (uint32_t v = threadIdx.x; v < nvec; v += kThreads) stage[v] = g[v];
+    }
+    __syncthreads();
+    const uint32_t i = i0 + threadIdx.x;
+    if (i >= i1) return;
+
+    uint32_t txh[8];
+    if (need_tx) {
+        const uint64_t o = a.offs[i];
+        const uint32_t len = static_cast<uint32_t>(a.offs[i + 1] - o);
+        if (staged) sha256_bytes(reinterpret_cast<const uint8_t*>(stage), o - s16, len, txh);
+        else sha256_bytes(a.payloads, o, len, txh);
+    }
+
+    const uint8_t* att = a.atts + 104ull * i;
+    uint32_t id[8];
+    load_be8_u64(att + 32, id);
+    const uint2 dv = *reinterpret_cast<const uint2*>(att + 64);
+    const uint32_t dom0 = bswap32(dv.x), dom1 = bswap32(dv.y);
+
+    if (a.codes) {
+        // verify_attestation_full: payload check first, then the credential.
+        uint32_t obj[8], cred[8], rev[8], key[8], expect[8];
+        load_be8_u64(att, obj);
+        load_be8_u64(att + 72, cred);
+        load_be8(a.revs + 32ull * a.rev_index[i], rev);
+        derive_attest_key(rev, dom0, dom1, key);
+        credential_hmac(key, obj, dom0, dom1, expect);
+        a.codes[i] = !eq8(txh, obj) ? 1 : (!eq8(expect, cred) ? 2 : 0);
+    }
+    if (a.nodes) {
+        uint32_t d[8];
+        public_inputs_digest(id, txh, dom0, dom1, d);
+        uint8_t* node = a.nodes + static_cast<uint64_t>(kNodeBytes) * i;
+        expand256_store(0, d, node);
+        write_node_tail(node, d, 0);
+    }
+    if (a.merkle) {
+        uint32_t m[8];
+        merkle_leaf(id, m);
+        store_digest(a.merkle + 32ull * i, m);
+    }
+}
+
+// ------------------------------------------------------------------ levels
+__global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restrict__ nin,
+                                                         uint32_t nn, uint8_t* __restrict__ nout,
+                                                         const uint8_t* __restrict__ min_,
+                                                         uint32_t nm, uint8_t* __restrict__ mout,
+                                                         int lift, uint32_t proof_blocks) {
+    if (blockIdx.x < proof_blocks) {
+        const uint32_t t = blockIdx.x * kThreads + threadIdx.x;
+        const uint32_t p = nn / 2;
+        if (t < p) {
+            aggregate_node(nin + static_cast<uint64_t>(kNodeBytes) * (2 * t),
+                           nin + static_cast<uint64_t>(kNodeBytes) * (2 * t + 1),
+                           nout + static_cast<uint64_t>(kNodeBytes) * t);
+        } else if (t == p && (nn & 1)) {
+            // odd node promoted unchanged (prover.cpp:119-121)
+            const uint4* s = reinterpret_cast<const uint4*>(nin + static_cast<uint64_t>(kNodeBytes) * (nn - 1));
+            uint4* d = reinterpret_cast<uint4*>(nout + static_cast<uint64_t>(kNodeBytes) * p);
+#pragma unroll
+            for (int k = 0; k < kNodeBytes / 16; ++k) d[k] = s[k];
+        }
+        return;
+    }
+    const uint32_t u = (blockIdx.x - proof_blocks) * kThreads + threadIdx.x;
+    const uint32_t mp = (nm == 1 && !lift) ? 0 : (nm + 1) / 2;
+    if (u < mp) {
+        uint32_t l[8], r[8], h[8];
+        load_be8(min_ + 64ull * u, l);
+        if (2 * u + 1 < nm) load_be8(min_ + 64ull * u + 32, r);
+        else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = l[k];  // duplicate last (wire.cpp:240)
+        }
+        merkle_inner(l, r, h);
+        store_digest(mout + 32ull * u, h);
+    }
+}
+
+__global__ void merkle_leaves_kernel(const uint8_t* leaves, uint32_t n, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t h[8], m[8];
+    load_be8(leaves + 32ull * i, h);
+    merkle_leaf(h, m);
+    store_digest(out + 32ull * i, m);
+}
+
+// ---------------------------------------------------------------- finalize
+__global__ void finalize_kernel(const uint8_t* root, const uint8_t* mroot, const uint8_t* header,
+                                const uint8_t* bh, int prove_empty, uint8_t* out_proof,
+                                uint8_t* out_fc) {
+    __shared__ __align__(16) uint8_t node[kNodeBytes];
+    __shared__ __align__(16) uint8_t mr[32];
+    if (threadIdx.x < 32) mr[threadIdx.x] = 0;  // merkle_root of no leaves = 0^32 (wire.cpp:224)
+    if (threadIdx.x == 0) {
+        if (prove_empty) {
+            // Empty block: prove PublicInputs{tx_hash = block_hash} (prover.cpp:134-139).
+            uint32_t zero[8] = {0, 0, 0, 0, 0, 0, 0, 0}, h[8], d[8];
+            load_be8(bh, h);
+            public_inputs_digest(zero, h, 0, 0, d);
+            expand256_store(0, d, node);
+            write_node_tail(node, d, 0);
+        }
+    }
+    __syncthreads();
+    const uint8_t* src = prove_empty ? node : root;
+    const uint8_t* msrc = mroot ? mroot : mr;
+    for (int k = threadIdx.x; k < 289; k += blockDim.x) {
+        uint8_t v = k < 288 ? src[k] : src[288];
+        if (out_proof) out_proof[k] = v;
+    }
+    if (out_fc) {
+        for (int k = threadIdx.x; k < 328; k += blockDim.x) {
+            uint8_t v;
+            if (k < 32) v = bh[k];
+            else if (k < 40) v = header[k - 32];  // slot_number u64be = header bytes 0..8
+            else if (k < 296) v = src[k - 40];
+            else v = msrc[k - 296];
+            out_fc[k] = v;
+        }
+    }
+}
+
+__global__ void pack_kernel(const uint8_t* nodes, uint32_t n, uint8_t* out) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= 289ull * n) return;
+    const uint64_t i = t / 289, k = t % 289;
+    out[t] = nodes[i * kNodeBytes + k];
+}
+
+__global__ void unpack_kernel(const uint8_t* in, uint32_t n, uint8_t* nodes) {
+    const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+    if (t >= static_cast<uint64_t>(kNodeBytes) * n) return;
+    const uint64_t i = t / kNodeBytes, k = t % kNodeBytes;
+    nodes[t] = k < 289 ? in[i * 289 + k] : 0;
+}
+
+// --------------------------------------------------------------- batch API
+__global__ void sha256_varlen_kernel(const uint8_t* data, const uint64_t* offs, uint32_t n,
+                                     uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t h[8];
+    sha256_bytes(data, offs[i], static_cast<uint32_t>(offs[i + 1] - offs[i]), h);
+    store_digest(out + 32ull * i, h);
+}
+
+__global__ void sha256_strided_kernel(const uint8_t* base, uint64_t stride, uint32_t len,
+                                      uint32_t n, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t h[8];
+    sha256_bytes(base, stride * i, len, h);
+    store_digest(out + 32ull * i, h);
+}
+
+__global__ void prove_public_inputs_kernel(const uint8_t* pubs, uint32_t n, uint8_t* nodes) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t pub[40], d[8];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) load_be8(pubs + 160ull * i + 32 * k, pub + 8 * k);
+    public_inputs_digest_full(pub, d);
+    uint8_t* node = nodes + static_cast<uint64_t>(kNodeBytes) * i;
+    expand256_store(0, d, node);
+    write_node_tail(node, d, 0);
+}
+
+__global__ void verify_mock_kernel(const uint8_t* nodes, uint32_t n, uint8_t* ok) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* node = nodes + static_cast<uint64_t>(kNodeBytes) * i;
+    uint32_t d[8], seed[8];
+    load_be8(node + 256, d);
+    // verify_mock (prover.cpp:91-95): any kind other than Tx uses the agg tag.
+    expand_seed(node[288] == 0 ? 0 : 1, d, seed);
+    uint32_t diff = 0;
+    for (uint32_t c = 0; c < 8; ++c) {
+        uint32_t o[8], got[8];
+        expand_block(seed, c, o);
+        load_be8(node + 32 * c, got);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) diff |= o[k] ^ got[k];
+    }
+    ok[i] = diff == 0;
+}
+
+__global__ void aggregate_pairs_kernel(const uint8_t* an, const uint8_t* bn, uint32_t n,
+                                       uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    aggregate_node(an + static_cast<uint64_t>(kNodeBytes) * i,
+                   bn + static_cast<uint64_t>(kNodeBytes) * i,
+                   out + static_cast<uint64_t>(kNodeBytes) * i);
+}
+
+// generate_attestation (crypto.cpp:129-139), batched: the fixture generator.
+__global__ void attest_generate_kernel(const uint8_t* payloads, const uint64_t* offs, uint32_t n,
+                                       const uint8_t* revs, const uint32_t* rev_index,
+                                       const uint8_t* doms8, const uint8_t* id_coms,
+                                       uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t obj[8], rev[8], key[8], cred[8];
+    sha256_bytes(payloads, offs[i], static_cast<uint32_t>(offs[i + 1] - offs[i]), obj);
+    load_be8(revs + 32ull * rev_index[i], rev);
+    const uint8_t* dp = doms8 + 8ull * i;
+    const uint32_t dom0 = (uint32_t(dp[0]) << 24) | (uint32_t(dp[1]) << 16) | (uint32_t(dp[2]) << 8) | dp[3];
+    const uint32_t dom1 = (uint32_t(dp[4]) << 24) | (uint32_t(dp[5]) << 16) | (uint32_t(dp[6]) << 8) | dp[7];
+    derive_attest_key(rev, dom0, dom1, key);
+    credential_hmac(key, obj, dom0, dom1, cred);
+    uint8_t* o = out + 104ull * i;
+    uint2* o8 = reinterpret_cast<uint2*>(o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o8[k] = make_uint2(bswap32(obj[2 * k]), bswap32(obj[2 * k + 1]));
+    const uint8_t* idp = id_coms + 32ull * i;
+    for (int k = 0; k < 32; ++k) o[32 + k] = idp[k];
+    o8[8] = make_uint2(bswap32(dom0), bswap32(dom1));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o8[9 + k] = make_uint2(bswap32(cred[2 * k]), bswap32(cred[2 * k + 1]));
+}
+
+__global__ void derive_keys_kernel(const uint8_t* revs, const uint8_t* doms8, uint32_t n,
+                                   uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint32_t rev[8], key[8];
+    load_be8(revs + 32ull * i, rev);
+    const uint8_t* dp = doms8 + 8ull * i;
+    const uint32_t dom0 = (uint32_t(dp[0]) << 24) | (uint32_t(dp[1]) << 16) | (uint32_t(dp[2]) << 8) | dp[3];
+    const uint32_t dom1 = (uint32_t(dp[4]) << 24) | (uint32_t(dp[5]) << 16) | (uint32_t(dp[6]) << 8) | dp[7];
+    derive_attest_key(rev, dom0, dom1, key);
+    store_digest(out + 32ull * i, key);
+}
+
+// witness_matches_tx (prover.cpp:190-197): size == 256 and
+// HMAC(w[0:32], obj_hash | domain) == credential. 4 compressions.
+__global__ void witness_check_kernel(const uint8_t* w, const uint32_t* wlens, const uint8_t* atts,
+                                     uint32_t n, uint8_t* ok) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (wlens && wlens[i] != 256) {
+        ok[i] = 0;
+        return;
+    }
+    const uint8_t* att = atts + 104ull * i;
+    uint32_t key[8], obj[8], cred[8], expect[8];
+    load_be8(w + 256ull * i, key);
+    load_be8_u64(att, obj);
+    load_be8_u64(att + 72, cred);
+    const uint2 dv = *reinterpret_cast<const uint2*>(att + 64);
+    credential_hmac(key, obj, bswap32(dv.x), bswap32(dv.y), expect);
+    ok[i] = eq8(expect, cred);
+}
+
+__device__ __forceinline__ void put_be32(uint8_t* p, uint32_t v) {
+    p[0] = v >> 24; p[1] = v >> 16; p[2] = v >> 8; p[3] = v;
+}
+
+// keystream block c (prover.cpp:41-56): SHA("witness-stream-v1" | key | c_be32).
+__device__ void keystream_block(const uint8_t key[32], uint32_t c, uint32_t o[8]) {
+    __align__(16) uint8_t m[64];
+    const char tag[] = "witness-stream-v1";
+    for (int k = 0; k < 17; ++k) m[k] = tag[k];
+    for (int k = 0; k < 32; ++k) m[17 + k] = key[k];
+    put_be32(m + 49, c);
+    sha256_bytes(m, 0, 53, o);
+}
+
+// build_witness (prover.cpp:181-188).
+__global__ void build_witness_kernel(const uint8_t* keys, const uint8_t* txh, uint32_t n,
+                                     uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    __align__(16) uint8_t m[96];
+    __align__(16) uint8_t seed[32];
+    const char tag[] = "witness-pad-v1";
+    for (int k = 0; k < 14; ++k) m[k] = tag[k];
+    for (int k = 0; k < 32; ++k) { m[14 + k] = keys[32ull * i + k]; m[46 + k] = txh[32ull * i + k]; }
+    uint32_t s[8];
+    sha256_bytes(m, 0, 78, s);
+    store_digest(seed, s);
+    uint8_t* o = out + 256ull * i;
+    for (int k = 0; k < 32; ++k) o[k] = keys[32ull * i + k];
+    for (uint32_t c = 0; c < 7; ++c) {
+        uint32_t blk[8];
+        keystream_block(seed, c, blk);
+        store_digest(o + 32 + 32 * c, blk);
+    }
+}
+
+// WitnessScheme encapsulate/decrypt (prover.cpp:229-264) in one kernel: the
+// key is the XOR of the share values selected by masks[i] (share j =
+// SHA("witness-share-v1" | master | tx_hash | j_be32), :221-226), and the
+// payload is XORed with the keystream of that key.
+__global__ void witness_xor_kernel(const uint8_t* master, const uint8_t* txh,
+                                   const uint64_t* masks, const uint8_t* in, uint32_t len,
+                                   uint32_t n, uint8_t* out) {
+    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    __align__(16) uint8_t m[96];
+    const char tag[] = "witness-share-v1";
+    for (int k = 0; k < 16; ++k) m[k] = tag[k];
+    for (int k = 0; k < 32; ++k) { m[16 + k] = master[k]; m[48 + k] = txh[32ull * i + k]; }
+    uint32_t key[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const uint64_t mask = masks[i];
+    for (uint32_t j = 0; j < 64; ++j) {
+        if (!((mask >> j) & 1)) continue;
+        put_be32(m + 80, j);
+        uint32_t s[8];
+        sha256_bytes(m, 0, 84, s);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) key[k] ^= s[k];
+    }
+    __align__(16) uint8_t kb[32];
+    store_digest(kb, key);
+    const uint8_t* src = in + static_cast<uint64_t>(len) * i;
+    uint8_t* dst = out + static_cast<uint64_t>(len) * i;
+    for (uint32_t c = 0; 32 * c < len; ++c) {
+        uint32_t blk[8];
+        keystream_block(kb, c, blk);
+        for (uint32_t k = 0; k < 32 && 32 * c + k < len; ++k)
+            dst[32 * c + k] = src[32 * c + k] ^ static_cast<uint8_t>(blk[k >> 2] >> (24 - 8 * (k & 3)));
+    }
+}
+
+// Register-resident compression chain: the SHA-256 integer-ALU roofline probe.
+__global__ void sha256_peak_kernel(uint32_t* sink, uint32_t iters) {
+    uint32_t s[8];
+    sha256_init(s);
+    s[0] ^= blockIdx.x * blockDim.x + threadIdx.x;
+    for (uint32_t it = 0; it < iters; ++it) {
+        uint32_t w[16];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) { w[k] = s[k]; w[k + 8] = s[k] ^ it; }
+        sha256_compress(s, w);
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x ^= s[k];
+    if (x == 0x12345678u) sink[0] = x;  // keeps the chain live
+}
+
+inline uint32_t blocks_for(uint64_t n, int t = kThreads) {
+    return static_cast<uint32_t>((n + t - 1) / t);
+}
+
+}  // namespace
+
+void launch_leaves(const LeafArgs& a, cudaStream_t s) {
+    const uint32_t blocks = blocks_for(a.n) + (a.header ? 1 : 0);
+    if (blocks == 0) return;
+    leaf_kernel<<<blocks, kThreads, 0, s>>>(a);
+}
+
+void launch_level(const uint8_t* nin, uint32_t nn, uint8_t* nout, const uint8_t* min_,
+                  uint32_t nm, uint8_t* mout, bool lift, cudaStream_t s) {
+    const uint32_t pt = nin ? nn / 2 + (nn & 1) : 0;
+    const uint32_t pb = blocks_for(pt);
+    const uint32_t mt = (!min_ || (nm == 1 && !lift)) ? 0 : (nm + 1) / 2;
+    const uint32_t mb = blocks_for(mt);
+    if (pb + mb == 0) return;
+    level_kernel<<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lift ? 1 : 0, pb);
+}
+
+void launch_merkle_leaves(const uint8_t* leaves, uint32_t n, uint8_t* out, cudaStream_t s) {
+    if (n) merkle_leaves_kernel<<<blocks_for(n), kThreads, 0, s>>>(leaves, n, out);
+}
+
+void launch_finalize(const uint8_t* root, const uint8_t* mroot, const uint8_t* header,
+                     const uint8_t* bh, bool prove_empty, uint8_t* out_proof, uint8_t* out_fc,
+                     cudaStream_t s) {
+    finalize_kernel<<<1, 64, 0, s>>>(root, mroot, header, bh, prove_empty ? 1 : 0, out_proof,
+                                     out_fc);
+}
+
+void launch_pack_nodes(const uint8_t* nodes, uint32_t n, uint8_t* out, cudaStream_t s) {
+    if (n) pack_kernel<<<blocks_for(289ull * n, 256), 256, 0, s>>>(nodes, n, out);
+}
+
+void launch_unpack_nodes(const uint8_t* in, uint32_t n, uint8_t* nodes, cudaStream_t s) {
+    if (n) unpack_kernel<<<blocks_for(uint64_t(kNodeBytes) * n, 256), 256, 0, s>>>(in, n, nodes);
+}
+
+void launch_sha256_varlen(const uint8_t* data, const uint64_t* offs, uint32_t n, uint8_t* out,
+                          cudaStream_t s) {
+    if (n) sha256_varlen_kernel<<<blocks_for(n), kThreads, 0, s>>>(data, offs, n, out);
+}
+
+void launch_sha256_strided(const uint8_t* base, uint64_t stride, uint32_t len, uint32_t n,
+                           uint8_t* out, cudaStream_t s) {
+    if (n) sha256_strided_kernel<<<blocks_for(n), kThreads, 0, s>>>(base, stride, len, n, out);
+}
+
+void launch_prove_public_inputs(const uint8_t* pubs, uint32_t n, uint8_t* nodes, cudaStream_t s) {
+    if (n) prove_public_inputs_kernel<<<blocks_for(n), kThreads, 0, s>>>(pubs, n, nodes);
+}
+
+void launch_verify_mock(const uint8_t* nodes, uint32_t n, uint8_t* ok, cudaStream_t s) {
+    if (n) verify_mock_kernel<<<blocks_for(n), kThreads, 0, s>>>(nodes, n, ok);
+}
+
+void launch_aggregate_pairs(const uint8_t* an, const uint8_t* bn, uint32_t n, uint8_t* out,
+                            cudaStream_t s) {
+    if (n) aggregate_pairs_kernel<<<blocks_for(n), kThreads, 0, s>>>(an, bn, n, out);
+}
+
+void launch_attest_generate(const uint8_t* payloads, const uint64_t* offs, uint32_t n,
+                            const uint8_t* revs, const uint32_t* rev_index, const uint8_t* doms8,
+                            const uint8_t* id_coms, uint8_t* out, cudaStream_t s) {
+    if (n)
+        attest_generate_kernel<<<blocks_for(n), kThreads, 0, s>>>(payloads, offs, n, revs,
+                                                                  rev_index, doms8, id_coms, out);
+}
+
+void launch_derive_attest_keys(const uint8_t* revs, const uint8_t* doms8, uint32_t n,
+                               uint8_t* out, cudaStream_t s) {
+    if (n) derive_keys_kernel<<<blocks_for(n), kThreads, 0, s>>>(revs, doms8, n, out);
+}
+
+void launch_witness_check(const uint8_t* w, const uint32_t* wlens, const uint8_t* atts,
+                          uint32_t n, uint8_t* ok, cudaStream_t s) {
+    if (n) witness_check_kernel<<<blocks_for(n), kThreads, 0, s>>>(w, wlens, atts, n, ok);
+}
+
+void launch_build_witness(const uint8_t* keys, const uint8_t* txh, uint32_t n, uint8_t* out,
+                          cudaStream_t s) {
+    if (n) build_witness_kernel<<<blocks_for(n), kThreads, 0, s>>>(keys, txh, n, out);
+}
+
+void launch_witness_xor(const uint8_t* master, const uint8_t* txh, const uint64_t* masks,
+                        const uint8_t* in, uint32_t len, uint32_t n, uint8_t* out,
+                        cudaStream_t s) {
+    if (n) witness_xor_kernel<<<blocks_for(n), kThreads, 0, s>>>(master, txh, masks, in, len, n, out);
+}
+
+void launch_sha256_peak(uint32_t* sink, uint32_t iters, int blocks, int threads, cudaStream_t s) {
+    sha256_peak_kernel<<<blocks, threads, 0, s>>>(sink, iters);
+}
+
+}  // namespace ace_gpu

@@ -1,0 +1,168 @@
+"""Multi-GPU Prove: power-of-two-aligned transaction chunks sharded across
+ranks (one process per GPU, torch.distributed over NCCL for the plumbing).
+
+Why it is bit-exact: the reference pairs nodes (2i, 2i+1) and
+promotes an odd last node (prover.cpp:112-124), so the root of every aligned
+2^k-leaf chunk IS a level-k node of the global proof tree. The id_com Merkle
+tree duplicates an odd last node (wire.cpp:240); the block's last chunk is
+therefore lifted by self-pairing up to level k (acegpu_shard_roots_dev does
+this when n_total > 2^k). The only exchange is one all-gather of the chunk
+roots (289 B proof + 32 B Merkle node per chunk) before the top levels.
+
+Device work goes through the C ABI (acegpu_shard_roots_dev /
+acegpu_combine_roots_dev) on torch's current stream; torch supplies device
+memory, streams and the collective.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+
+LOG2_CHUNK = 10  # 1,024-tx chunks: the Groth16 chunk size of SURVEY §8d
+
+
+def partition(n_total: int, world: int, log2_chunk: int = LOG2_CHUNK) -> list[tuple[int, int]]:
+    """Contiguous whole chunks per rank, balanced by chunk count: [(start, count)].
+    (Not one power-of-two range per rank, which strands ranks at 100k, §8e.)"""
+    C = 1 << log2_chunk
+    chunks = -(-n_total // C)
+    out = []
+    for r in range(world):
+        c0, c1 = chunks * r // world, chunks * (r + 1) // world
+        s, e = min(c0 * C, n_total), min(c1 * C, n_total)
+        out.append((s, e - s))
+    return out
+
+
+def n_chunks(count: int, log2_chunk: int) -> int:
+    return -(-count // (1 << log2_chunk))
+
+
+@dataclass
+class DeviceBlock:
+    """A block (or one rank's slice of it) resident in device memory."""
+    payloads: "object"   # torch.uint8 [bytes (+pad)]
+    offs: "object"       # torch.int64 [n+1] (uint64 bit pattern), rebased to payloads
+    atts: "object"       # torch.uint8 [n*104]
+    header: "object"     # torch.uint8 [256]
+    n: int
+    revs: "object" = None       # torch.uint8 [32*users]
+    rev_index: "object" = None  # torch.int32 [n]
+
+    @staticmethod
+    def upload(fb, start: int = 0, count: int | None = None, revs=None, rev_index=None,
+               device=None, pin: bool = True) -> "DeviceBlock":
+        """Host FlatBlock slice [start, start+count) -> device tensors."""
+        import torch
+        count = fb.n - start if count is None else count
+        dev = torch.device("cuda", N.default_device() if device is None else device)
+        b0 = int(fb.offs[start]) if count else 0
+        b1 = int(fb.offs[start + count]) if count else 0
+        offs = (fb.offs[start:start + count + 1].astype(np.int64) - b0) if count else np.zeros(1, np.int64)
+
+        def put(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            if pin:
+                t = t.pin_memory()
+            return t.to(dev, non_blocking=True)
+        pl = np.zeros(b1 - b0 + 16, np.uint8)
+        pl[:b1 - b0] = fb.payloads[b0:b1]
+        at = fb.atts[104 * start:104 * (start + count)] if count else np.zeros(8, np.uint8)
+        hdr = fb.header if isinstance(fb.header, np.ndarray) else np.frombuffer(fb.header, np.uint8)
+        db = DeviceBlock(put(pl), put(offs), put(at), put(np.ascontiguousarray(hdr)), count)
+        if revs is not None:
+            db.revs = put(np.ascontiguousarray(revs, np.uint8))
+            ri = np.ascontiguousarray(rev_index, np.uint32)[start:start + count]
+            db.rev_index = put(ri.view(np.int32) if count else np.zeros(1, np.int32))
+        return db
+
+
+def _ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def _stream():
+    import torch
+    return torch.cuda.current_stream().cuda_stream
+
+
+class GpuBackend:
+    """Chunk roots and their combination on the local GPU (libacegpu)."""
+
+    def __init__(self, ctx: N.Context | None = None):
+        self.ctx = ctx or N.context()
+
+    def shard_roots(self, db: DeviceBlock, n_total: int, log2_chunk: int, codes=None):
+        import torch
+        c = n_chunks(db.n, log2_chunk)
+        roots = torch.empty(max(c, 1) * 289, dtype=torch.uint8, device=db.atts.device)
+        merk = torch.empty(max(c, 1) * 32, dtype=torch.uint8, device=db.atts.device)
+        if db.n:
+            self.ctx.call("acegpu_shard_roots_dev", _stream(), _ptr(db.payloads), _ptr(db.offs),
+                          _ptr(db.atts), db.n, n_total, log2_chunk, _ptr(db.revs),
+                          _ptr(db.rev_index), _ptr(codes), _ptr(roots), _ptr(merk))
+        return roots[:c * 289], merk[:c * 32]
+
+    def combine(self, roots, merk, chunks: int, n_total: int, header):
+        import torch
+        out = torch.empty(289 + 15 + 328, dtype=torch.uint8, device=header.device)
+        self.ctx.call("acegpu_combine_roots_dev", _stream(), _ptr(roots) if chunks else None,
+                      _ptr(merk) if chunks else None, chunks, n_total, _ptr(header), _ptr(out),
+                      out.data_ptr() + 304)
+        return out[:289], out[304:304 + 328]
+
+
+def gather_roots(roots, merk, counts: list[int], group=None):
+    """All-gather each rank's chunk roots (padded to the largest rank) and
+    return them concatenated in rank order."""
+    import torch
+    import torch.distributed as dist
+    world = len(counts)
+    mx = max(max(counts), 1)
+    pr = torch.zeros(mx * 289, dtype=torch.uint8, device=roots.device)
+    pm = torch.zeros(mx * 32, dtype=torch.uint8, device=merk.device)
+    pr[:roots.numel()] = roots
+    pm[:merk.numel()] = merk
+    gr = [torch.empty_like(pr) for _ in range(world)]
+    gm = [torch.empty_like(pm) for _ in range(world)]
+    dist.all_gather(gr, pr, group=group)
+    dist.all_gather(gm, pm, group=group)
+    allr = torch.cat([g[:c * 289] for g, c in zip(gr, counts)])
+    allm = torch.cat([g[:c * 32] for g, c in zip(gm, counts)])
+    return allr, allm
+
+
+def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
+                  log2_chunk: int = LOG2_CHUNK, backend=None, group=None, codes=None):
+    """One rank's part of a sharded block proof; every rank returns the same
+    (proof289, fc328) device tensors."""
+    backend = backend or GpuBackend()
+    parts = partition(n_total, world, log2_chunk)
+    counts = [n_chunks(c, log2_chunk) for _, c in parts]
+    assert local.n == parts[rank][1]
+    roots, merk = backend.shard_roots(local, n_total, log2_chunk, codes)
+    if world > 1:
+        roots, merk = gather_roots(roots, merk, counts, group)
+    return backend.combine(roots, merk, sum(counts), n_total, local.header)
+
+
+def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None):
+    """Emulates `world` ranks one after another on one GPU (no collective):
+    used to check shard/combine bit-exactness with a single device."""
+    import torch
+    be = GpuBackend(ctx)
+    parts = partition(fb.n, world, log2_chunk)
+    rs, ms = [], []
+    for s, c in parts:
+        db = DeviceBlock.upload(fb, s, c)
+        r, m = be.shard_roots(db, fb.n, log2_chunk)
+        rs.append(r)
+        ms.append(m)
+        hdr = db.header
+    roots, merk = torch.cat(rs), torch.cat(ms)
+    proof, fc = be.combine(roots, merk, sum(n_chunks(c, log2_chunk) for _, c in parts), fb.n, hdr)
+    torch.cuda.synchronize()
+    return proof.cpu().numpy().tobytes(), fc.cpu().numpy().tobytes()
