@@ -306,6 +306,9 @@ def run_ours(args, rank: int, world: int) -> None:
     peak = C.c_double()
     ctx.call("acegpu_sha256_peak", C.byref(peak))
     peak_cps = peak.value
+    lat = C.c_double()
+    ctx.call("acegpu_sha256_probe", 1, 32, 512, C.byref(lat))
+    lat_us = lat.value / 512 * 1e6  # one warp's chained compression latency
 
     if rank != 0:
         return
@@ -324,6 +327,7 @@ def run_ours(args, rank: int, world: int) -> None:
                 "hbm_gbs_achieved": (int(fb.offs[n]) + 104 * n + 352 * n) / (phase[0] * 1e-3) / 1e9,
                 "phase_ms": {"leaves": phase[0], "tree_levels": phase[1], "finalize": phase[2]},
                 "tree_frac_of_peak": tree_c / (phase[1] * 1e-3) / peak_cps,
+                "single_warp_compression_latency_us": lat_us,
                 "peak_source": "acegpu_sha256_peak register-resident microkernel, same run"}
     cpu = cpu_baseline(args, n)
     cl = clocks.summary()

@@ -25,8 +25,10 @@
  * and copy results back; they are synchronous and thread-safe per context
  * (calls on one context serialise, like ThreadPool::job_mu_ in
  * thread_pool.hpp:40-49). `_dev` functions take DEVICE pointers and a
- * cudaStream_t (as void*, NULL = the context's stream), enqueue only, and
- * never synchronise. Device byte buffers must be 16-B aligned (cudaMalloc).
+ * cudaStream_t (as void*, used as given: NULL = CUDA's legacy default
+ * stream), enqueue only, and never synchronise; the context workspace they
+ * use is stream-ordered, so drive one context from one stream. Device byte
+ * buffers must be 16-B aligned (cudaMalloc).
  */
 #ifndef ACEGPU_H
 #define ACEGPU_H
@@ -169,6 +171,10 @@ int acegpu_witness_xor(acegpu_ctx* ctx, const uint8_t* master32, const uint8_t* 
 /* SHA-256 compressions/s of a register-resident chain over the whole GPU (the
  * integer-ALU roofline of the mock path). */
 int acegpu_sha256_peak(acegpu_ctx* ctx, double* compressions_per_s);
+/* Wall time of `iters` chained compressions per thread on a blocks x threads
+ * grid (blocks = 1, threads = 32 gives the single-warp compression latency). */
+int acegpu_sha256_probe(acegpu_ctx* ctx, int blocks, int threads, uint32_t iters,
+                        double* seconds);
 
 #ifdef __cplusplus
 }

@@ -59,6 +59,7 @@ _SIGS = {
     "acegpu_build_witness": (C.c_int, [ctxp, vp, vp, u64, vp]),
     "acegpu_witness_xor": (C.c_int, [ctxp, vp, vp, vp, vp, u64, u64, vp]),
     "acegpu_sha256_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
+    "acegpu_sha256_probe": (C.c_int, [ctxp, C.c_int, C.c_int, C.c_uint32, C.POINTER(C.c_double)]),
 }
 
 
@@ -147,7 +148,11 @@ class Context:
         return int(self.lib.acegpu_launch_count(self.h))
 
     def call(self, name: str, *args) -> None:
-        check(getattr(self.lib, name)(self.h, *args))
+        """Arrays / tensors may be passed directly: they stay referenced (alive)
+        for the duration of the call, unlike a bare ``addr(temporary)``."""
+        conv = [addr(a) if isinstance(a, np.ndarray) or hasattr(a, "data_ptr") else a
+                for a in args]
+        check(getattr(self.lib, name)(self.h, *conv))
 
 
 _ctx: dict[int, Context] = {}

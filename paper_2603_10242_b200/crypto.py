@@ -157,8 +157,7 @@ def verify_attestations(fb: FlatBlock, revs: np.ndarray, rev_index: np.ndarray,
     codes = np.zeros(max(fb.n, 1), np.uint8)
     if fb.n:
         ctx.call("acegpu_attest_verify", N.addr(fb.payloads), N.addr(fb.offs), N.addr(fb.atts),
-                 fb.n, N.addr(revs), len(revs) // 32, N.addr(np.ascontiguousarray(rev_index,
-                                                                                  np.uint32)),
+                 fb.n, N.addr(revs), len(revs) // 32, np.ascontiguousarray(rev_index, np.uint32),
                  N.addr(codes))
     return codes[:fb.n]
 

@@ -136,9 +136,9 @@ int h2d_t(acegpu_ctx* c, Slot s, const T* src, size_t bytes, cudaStream_t st, T*
     return ACEGPU_OK;
 }
 
-cudaStream_t pick(acegpu_ctx* c, void* stream) {
-    return stream ? static_cast<cudaStream_t>(stream) : c->stream;
-}
+// `_dev` calls run on the caller's stream exactly as given: NULL is CUDA's
+// legacy default stream (what torch.cuda.current_stream() reports as 0).
+cudaStream_t pick(acegpu_ctx*, void* stream) { return static_cast<cudaStream_t>(stream); }
 
 struct TreeResult {
     uint8_t* nodes = nullptr;   // level nodes (320 B each)
@@ -879,3 +879,28 @@ int acegpu_sha256_peak(acegpu_ctx* c, double* cps) {
 }
 
 }  // extern "C"
+
+extern "C" int acegpu_sha256_probe(acegpu_ctx* c, int blocks, int threads, uint32_t iters,
+                                   double* seconds) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint32_t* sink;
+    RET(ws(c, kMisc, 16, &sink));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    launch_sha256_peak(sink, 16, blocks, threads, s);  // warm-up
+    CK(cudaEventRecord(e0, s));
+    launch_sha256_peak(sink, iters, blocks, threads, s);
+    CK(cudaEventRecord(e1, s));
+    CKL();
+    c->launches += 2;
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *seconds = ms * 1e-3;
+    return ACEGPU_OK;
+}

@@ -180,19 +180,35 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(LeafArgs a) {
 }
 
 // ------------------------------------------------------------------ levels
+// G lanes per pair. Every lane of a group runs the 9-block digest chain and
+// the seed in lock-step (SIMT: no extra issue slots, no shuffles) and then
+// its own 8/G expand blocks, so a level's critical path drops from 18 to
+// 10 + 8/G serial compressions. Wide levels use G = 1 (throughput-bound),
+// the narrow top of the tree G = 8 (latency-bound); see launch_level.
+template <int G>
 __global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restrict__ nin,
                                                          uint32_t nn, uint8_t* __restrict__ nout,
                                                          const uint8_t* __restrict__ min_,
                                                          uint32_t nm, uint8_t* __restrict__ mout,
                                                          int lift, uint32_t proof_blocks) {
     if (blockIdx.x < proof_blocks) {
-        const uint32_t t = blockIdx.x * kThreads + threadIdx.x;
+        const uint32_t g = blockIdx.x * kThreads + threadIdx.x;
+        const uint32_t t = g / G, lane = g % G;
         const uint32_t p = nn / 2;
         if (t < p) {
-            aggregate_node(nin + static_cast<uint64_t>(kNodeBytes) * (2 * t),
-                           nin + static_cast<uint64_t>(kNodeBytes) * (2 * t + 1),
-                           nout + static_cast<uint64_t>(kNodeBytes) * t);
-        } else if (t == p && (nn & 1)) {
+            const uint8_t* a = nin + static_cast<uint64_t>(kNodeBytes) * (2 * t);
+            uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
+            uint32_t d[8], seed[8];
+            pair_digest(a, a + kNodeBytes, d);
+            expand_seed(1, d, seed);
+#pragma unroll 1
+            for (uint32_t c = lane; c < 8; c += G) {
+                uint32_t o[8];
+                expand_block(seed, c, o);
+                store_digest(out + 32 * c, o);
+            }
+            if (lane == 0) write_node_tail(out, d, 1);
+        } else if (t == p && (nn & 1) && lane == 0) {
             // odd node promoted unchanged (prover.cpp:119-121)
             const uint4* s = reinterpret_cast<const uint4*>(nin + static_cast<uint64_t>(kNodeBytes) * (nn - 1));
             uint4* d = reinterpret_cast<uint4*>(nout + static_cast<uint64_t>(kNodeBytes) * p);
@@ -495,12 +511,21 @@ void launch_leaves(const LeafArgs& a, cudaStream_t s) {
 
 void launch_level(const uint8_t* nin, uint32_t nn, uint8_t* nout, const uint8_t* min_,
                   uint32_t nm, uint8_t* mout, bool lift, cudaStream_t s) {
-    const uint32_t pt = nin ? nn / 2 + (nn & 1) : 0;
+    const uint32_t pt0 = nin ? nn / 2 + (nn & 1) : 0;
+    // Lanes per pair: cost ~ max(latency (10 + 8/G) L, throughput P (10 + 8/G) G / 32).
+    const int G = pt0 >= 24576 ? 1 : pt0 >= 6144 ? 2 : pt0 >= 1536 ? 4 : 8;
+    const uint32_t pt = pt0 * G;
     const uint32_t pb = blocks_for(pt);
     const uint32_t mt = (!min_ || (nm == 1 && !lift)) ? 0 : (nm + 1) / 2;
     const uint32_t mb = blocks_for(mt);
     if (pb + mb == 0) return;
-    level_kernel<<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lift ? 1 : 0, pb);
+    const int lf = lift ? 1 : 0;
+    switch (G) {
+        case 1: level_kernel<1><<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lf, pb); break;
+        case 2: level_kernel<2><<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lf, pb); break;
+        case 4: level_kernel<4><<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lf, pb); break;
+        default: level_kernel<8><<<pb + mb, kThreads, 0, s>>>(nin, nn, nout, min_, nm, mout, lf, pb); break;
+    }
 }
 
 void launch_merkle_leaves(const uint8_t* leaves, uint32_t n, uint8_t* out, cudaStream_t s) {

@@ -170,7 +170,7 @@ def aggregate_pairs(a: list[MockProof], b: list[MockProof], ctx=None) -> list[Mo
         return []
     ctx = ctx or N.context()
     out = np.zeros(289 * len(a), np.uint8)
-    ctx.call("acegpu_aggregate_pairs", N.addr(_proofs_array(a)), N.addr(_proofs_array(b)),
+    ctx.call("acegpu_aggregate_pairs", _proofs_array(a), _proofs_array(b),
              len(a), N.addr(out))
     _counters.add(aggregations=len(a))
     return _split(out, len(a))
@@ -189,7 +189,7 @@ def aggregate_tree(proofs: list[MockProof], stats: AggregationStats | None = Non
     ctx = ctx or N.context()
     out = np.zeros(289, np.uint8)
     lv, pr = N.C.c_uint64(), N.C.c_uint64()
-    ctx.call("acegpu_aggregate_tree", N.addr(_proofs_array(proofs)), len(proofs), N.addr(out),
+    ctx.call("acegpu_aggregate_tree", _proofs_array(proofs), len(proofs), N.addr(out),
              N.C.byref(lv), N.C.byref(pr))
     _counters.add(aggregations=pr.value)
     if stats is not None:
@@ -244,7 +244,7 @@ def build_finality_certificate(block, aggregate: MockProof, ctx=None) -> Finalit
     ctx = ctx or N.context()
     out = np.zeros(328, np.uint8)
     ctx.call("acegpu_build_fc", N.addr(fb.atts), fb.n, N.addr(fb.header),
-             N.addr(np.frombuffer(aggregate.to_bytes(), np.uint8).copy()), N.addr(out))
+             np.frombuffer(aggregate.to_bytes(), np.uint8).copy(), N.addr(out))
     return FinalityCertificate.decode(out.tobytes())
 
 
@@ -261,7 +261,7 @@ def verify_finality_certificate(fc: FinalityCertificate, block, cost_units: Cost
     fb = _flat(block)
     ctx = ctx or N.context()
     res = N.C.c_int()
-    ctx.call("acegpu_verify_fc", N.addr(np.frombuffer(fc.encode(), np.uint8).copy()),
+    ctx.call("acegpu_verify_fc", np.frombuffer(fc.encode(), np.uint8).copy(),
              N.addr(fb.payloads), N.addr(fb.offs), N.addr(fb.atts), fb.n, N.addr(fb.header),
              N.C.byref(res))
     if res.value == FcCheck.Valid or res.value == FcCheck.ProofMismatch:
@@ -346,9 +346,9 @@ class WitnessScheme:
         assert all(len(d) == L for d in data)
         inp = np.frombuffer(b"".join(data), np.uint8).copy()
         out = np.zeros(len(inp), np.uint8)
-        ctx.call("acegpu_witness_xor", N.addr(np.frombuffer(self.master_, np.uint8).copy()),
-                 N.addr(np.frombuffer(b"".join(tx_hashes), np.uint8).copy()),
-                 N.addr(np.asarray(masks, np.uint64)), N.addr(inp), L, len(data), N.addr(out))
+        ctx.call("acegpu_witness_xor", np.frombuffer(self.master_, np.uint8).copy(),
+                 np.frombuffer(b"".join(tx_hashes), np.uint8).copy(),
+                 np.asarray(masks, np.uint64), inp, L, len(data), out)
         return [out[L * i:L * (i + 1)].tobytes() for i in range(len(data))]
 
     def encapsulate(self, tx_hash: bytes, witness: bytes, ctx=None) -> WitnessBundle:
