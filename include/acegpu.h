@@ -176,6 +176,44 @@ int acegpu_sha256_peak(acegpu_ctx* ctx, double* compressions_per_s);
 int acegpu_sha256_probe(acegpu_ctx* ctx, int blocks, int threads, uint32_t iters,
                         double* seconds);
 
+/* ---- BN254 (north-star additions; the reference has none) ----
+ * Field elements: 32-B little-endian canonical integers at the host
+ * boundary (standard form); Montgomery form (R = 2^256) on device for the
+ * `_dev` calls. G1 affine = x|y (64 B), G2 affine = x.c0|x.c1|y.c0|y.c1
+ * (128 B), infinity = all zeros. Parity: oracle/bn254_oracle.c (unpinned by
+ * the reference). */
+/* field: 0 = Fq, 1 = Fr. op: 0 mul, 1 add, 2 sub, 3 sqr, 4 inv (inv(0) = 0). */
+int acegpu_bn_field_batch(acegpu_ctx* ctx, int field, int op, const uint8_t* a, const uint8_t* b,
+                          uint64_t n, uint8_t* out);
+/* In-place standard <-> Montgomery conversion of n device elements. */
+int acegpu_bn_convert_dev(acegpu_ctx* ctx, void* stream, int field, uint8_t* d_data, uint64_t n,
+                          int to_mont);
+/* Fr NTT over 2^logn elements (logn <= 22), natural order in and out:
+ * omega = 5^((r-1)/2^logn); inverse scales by n^-1; coset multiplies the
+ * input by g^i (g = 5) before the forward transform / the output by g^-i
+ * after the inverse. Host version: standard form in place. */
+int acegpu_bn_ntt(acegpu_ctx* ctx, uint8_t* data, uint32_t logn, int inverse, int coset);
+/* Device version: Montgomery form; d_in may equal d_out. */
+int acegpu_bn_ntt_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_in, uint8_t* d_out,
+                      uint32_t logn, int inverse, int coset);
+/* out[i] = scalars[i] * base (group 1 or 2), affine, standard form. */
+int acegpu_bn_scalar_muls(acegpu_ctx* ctx, int group, const uint8_t* base, const uint8_t* scalars,
+                          uint64_t n, uint8_t* out);
+/* Fixed-base Pippenger MSM: prepare once per base set (proving key), run per
+ * scalar vector. Scalars: n x 32-B canonical Fr, standard form. */
+typedef struct acegpu_msm_bases acegpu_msm_bases;
+int acegpu_bn_msm_prepare(acegpu_ctx* ctx, int group, const uint8_t* points, uint64_t n,
+                          int points_on_device, acegpu_msm_bases** out);
+void acegpu_bn_msm_free(acegpu_msm_bases* bases);
+int acegpu_bn_msm_run(acegpu_ctx* ctx, const acegpu_msm_bases* bases, const uint8_t* scalars,
+                      uint8_t* out_affine);
+/* Device version: d_scalars standard form, d_out affine Montgomery form. */
+int acegpu_bn_msm_run_dev(acegpu_ctx* ctx, void* stream, const acegpu_msm_bases* bases,
+                          const uint8_t* d_scalars, uint8_t* d_out);
+/* Integer-pipe microbenchmarks (roofline denominators for MSM / NTT). */
+int acegpu_imad_peak(acegpu_ctx* ctx, double* imad_per_s);
+int acegpu_bn_mul_rate(acegpu_ctx* ctx, int field, double* muls_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,696 @@
+/* TEST INFRASTRUCTURE ONLY — from-scratch BN254 CPU oracle (see bn254_oracle.h:
+ * parity unpinned by the reference, which has no BN254 code). 4 x 64-bit limbs,
+ * Montgomery form internally (R = 2^256), CIOS multiplication with
+ * unsigned __int128. */
+#define _POSIX_C_SOURCE 200809L
+#include "bn254_oracle.h"
+
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+typedef struct { uint64_t v[4]; } fe;
+
+typedef struct {
+    uint64_t m[4];   /* modulus */
+    uint64_t r2[4];  /* R^2 mod m */
+    uint64_t one[4]; /* R mod m */
+    uint64_t n0;     /* -m^-1 mod 2^64 */
+} field_t;
+
+static const field_t FQ = {
+    {0x3c208c16d87cfd47ull, 0x97816a916871ca8dull, 0xb85045b68181585dull, 0x30644e72e131a029ull},
+    {0xf32cfc5b538afa89ull, 0xb5e71911d44501fbull, 0x47ab1eff0a417ff6ull, 0x06d89f71cab8351full},
+    {0xd35d438dc58f0d9dull, 0x0a78eb28f5c70b3dull, 0x666ea36f7879462cull, 0x0e0a77c19a07df2full},
+    0x87d20782e4866389ull};
+static const field_t FR = {
+    {0x43e1f593f0000001ull, 0x2833e84879b97091ull, 0xb85045b68181585dull, 0x30644e72e131a029ull},
+    {0x1bb8e645ae216da7ull, 0x53fe3ab1e35c59e3ull, 0x8c49833d53bb8085ull, 0x0216d0b17f4e44a5ull},
+    {0xac96341c4ffffffbull, 0x36fc76959f60cd29ull, 0x666ea36f7879462eull, 0x0e0a77c19a07df2full},
+    0xc2e1f593efffffffull};
+
+static const field_t* F_of(int f) { return f ? &FR : &FQ; }
+
+static int geq(const uint64_t a[4], const uint64_t b[4]) {
+    for (int i = 3; i >= 0; --i) {
+        if (a[i] > b[i]) return 1;
+        if (a[i] < b[i]) return 0;
+    }
+    return 1;
+}
+
+static void sub4(uint64_t a[4], const uint64_t b[4]) {
+    uint64_t br = 0;
+    for (int i = 0; i < 4; ++i) {
+        u128 d = (u128)a[i] - b[i] - br;
+        a[i] = (uint64_t)d;
+        br = (uint64_t)(d >> 64) ? 1 : 0;
+    }
+}
+
+static void fmul(const field_t* F, const fe* a, const fe* b, fe* o) {
+    uint64_t t[6] = {0, 0, 0, 0, 0, 0};
+    for (int i = 0; i < 4; ++i) {
+        uint64_t c = 0;
+        for (int j = 0; j < 4; ++j) {
+            u128 x = (u128)a->v[j] * b->v[i] + t[j] + c;
+            t[j] = (uint64_t)x;
+            c = (uint64_t)(x >> 64);
+        }
+        u128 x = (u128)t[4] + c;
+        t[4] = (uint64_t)x;
+        t[5] = (uint64_t)(x >> 64);
+        uint64_t m = t[0] * F->n0;
+        x = (u128)m * F->m[0] + t[0];
+        c = (uint64_t)(x >> 64);
+        for (int j = 1; j < 4; ++j) {
+            x = (u128)m * F->m[j] + t[j] + c;
+            t[j - 1] = (uint64_t)x;
+            c = (uint64_t)(x >> 64);
+        }
+        x = (u128)t[4] + c;
+        t[3] = (uint64_t)x;
+        t[4] = t[5] + (uint64_t)(x >> 64);
+    }
+    if (t[4] || geq(t, F->m)) sub4(t, F->m);
+    memcpy(o->v, t, 32);
+}
+
+static void fadd(const field_t* F, const fe* a, const fe* b, fe* o) {
+    uint64_t t[4], c = 0;
+    for (int i = 0; i < 4; ++i) {
+        u128 x = (u128)a->v[i] + b->v[i] + c;
+        t[i] = (uint64_t)x;
+        c = (uint64_t)(x >> 64);
+    }
+    if (c || geq(t, F->m)) sub4(t, F->m);
+    memcpy(o->v, t, 32);
+}
+
+static void fsub(const field_t* F, const fe* a, const fe* b, fe* o) {
+    uint64_t t[4], br = 0;
+    for (int i = 0; i < 4; ++i) {
+        u128 d = (u128)a->v[i] - b->v[i] - br;
+        t[i] = (uint64_t)d;
+        br = (uint64_t)(d >> 64) ? 1 : 0;
+    }
+    if (br) {
+        uint64_t c = 0;
+        for (int i = 0; i < 4; ++i) {
+            u128 x = (u128)t[i] + F->m[i] + c;
+            t[i] = (uint64_t)x;
+            c = (uint64_t)(x >> 64);
+        }
+    }
+    memcpy(o->v, t, 32);
+}
+
+static int fis_zero(const fe* a) { return !(a->v[0] | a->v[1] | a->v[2] | a->v[3]); }
+static int feq(const fe* a, const fe* b) { return !memcmp(a->v, b->v, 32); }
+
+static void to_mont(const field_t* F, const uint8_t* in, fe* o) {
+    fe x, r2;
+    memcpy(x.v, in, 32);
+    while (geq(x.v, F->m)) sub4(x.v, F->m);
+    memcpy(r2.v, F->r2, 32);
+    fmul(F, &x, &r2, o);
+}
+
+static void from_mont(const field_t* F, const fe* a, uint8_t* out) {
+    fe one = {{1, 0, 0, 0}}, x;
+    fmul(F, a, &one, &x);
+    memcpy(out, x.v, 32);
+}
+
+static void fpow(const field_t* F, const fe* a, const uint64_t e[4], fe* o) {
+    fe r, b = *a;
+    memcpy(r.v, F->one, 32);
+    for (int i = 0; i < 256; ++i) {
+        if (e[i >> 6] >> (i & 63) & 1) fmul(F, &r, &b, &r);
+        fmul(F, &b, &b, &b);
+    }
+    *o = r;
+}
+
+static void finv(const field_t* F, const fe* a, fe* o) {
+    uint64_t e[4];
+    memcpy(e, F->m, 32);
+    e[0] -= 2;  /* m - 2 (m odd, low limb > 2) */
+    fpow(F, a, e, o);
+}
+
+/* ------------------------------------------------------------ field API */
+void bn_mul(int f, const uint8_t* a, const uint8_t* b, uint8_t* out) {
+    const field_t* F = F_of(f);
+    fe x, y, z;
+    to_mont(F, a, &x);
+    to_mont(F, b, &y);
+    fmul(F, &x, &y, &z);
+    from_mont(F, &z, out);
+}
+void bn_add(int f, const uint8_t* a, const uint8_t* b, uint8_t* out) {
+    const field_t* F = F_of(f);
+    fe x, y, z;
+    to_mont(F, a, &x);
+    to_mont(F, b, &y);
+    fadd(F, &x, &y, &z);
+    from_mont(F, &z, out);
+}
+void bn_sub(int f, const uint8_t* a, const uint8_t* b, uint8_t* out) {
+    const field_t* F = F_of(f);
+    fe x, y, z;
+    to_mont(F, a, &x);
+    to_mont(F, b, &y);
+    fsub(F, &x, &y, &z);
+    from_mont(F, &z, out);
+}
+void bn_inv(int f, const uint8_t* a, uint8_t* out) {
+    const field_t* F = F_of(f);
+    fe x, z;
+    to_mont(F, a, &x);
+    finv(F, &x, &z);
+    from_mont(F, &z, out);
+}
+void bn_pow(int f, const uint8_t* a, const uint8_t* e, uint8_t* out) {
+    const field_t* F = F_of(f);
+    fe x, z;
+    uint64_t ev[4];
+    memcpy(ev, e, 32);
+    to_mont(F, a, &x);
+    fpow(F, &x, ev, &z);
+    from_mont(F, &z, out);
+}
+void bn_batch(int f, int op, const uint8_t* a, const uint8_t* b, uint64_t n, uint8_t* out) {
+    for (uint64_t i = 0; i < n; ++i) {
+        const uint8_t* x = a + 32 * i;
+        const uint8_t* y = op == 3 ? x : b + 32 * i;
+        if (op == 0 || op == 3) bn_mul(f, x, y, out + 32 * i);
+        else if (op == 1) bn_add(f, x, y, out + 32 * i);
+        else bn_sub(f, x, y, out + 32 * i);
+    }
+}
+void bn_reduce(int f, const uint8_t* a, uint64_t n, uint8_t* out) {
+    const field_t* F = F_of(f);
+    for (uint64_t i = 0; i < n; ++i) {
+        uint64_t x[4];
+        memcpy(x, a + 32 * i, 32);
+        while (geq(x, F->m)) sub4(x, F->m);
+        memcpy(out + 32 * i, x, 32);
+    }
+}
+
+/* ------------------------------------------------------------------ NTT */
+typedef struct {
+    fe* a;
+    const fe* tw;  /* tw[k] = w^k, k < n/2 */
+    uint64_t n, half, step;
+    int t, T;
+} ntt_job;
+
+static void* ntt_stage(void* p) {
+    ntt_job* j = (ntt_job*)p;
+    /* butterflies of this stage, split over T workers by butterfly index */
+    uint64_t nb = j->n / 2;
+    uint64_t b0 = nb * j->t / j->T, b1 = nb * (j->t + 1) / j->T;
+    for (uint64_t b = b0; b < b1; ++b) {
+        uint64_t grp = b / j->half, k = b % j->half;
+        uint64_t i = grp * 2 * j->half + k, i2 = i + j->half;
+        fe u = j->a[i], v;
+        fmul(&FR, &j->a[i2], &j->tw[k * j->step], &v);
+        fadd(&FR, &u, &v, &j->a[i]);
+        fsub(&FR, &u, &v, &j->a[i2]);
+    }
+    return NULL;
+}
+
+static void fr_root(uint32_t logn, int inverse, fe* w) {
+    /* w = 5^((r-1)/2^logn) */
+    fe g;
+    uint8_t five[32] = {5};
+    to_mont(&FR, five, &g);
+    uint64_t e[4];
+    memcpy(e, FR.m, 32);
+    e[0] -= 1;
+    for (uint32_t s = 0; s < logn; ++s) { /* e >>= 1 */
+        for (int i = 0; i < 4; ++i) e[i] = (e[i] >> 1) | (i < 3 ? e[i + 1] << 63 : 0);
+    }
+    fpow(&FR, &g, e, w);
+    if (inverse) finv(&FR, w, w);
+}
+
+void bn_ntt(uint8_t* data, uint32_t logn, int inverse, int coset, int threads) {
+    uint64_t n = 1ull << logn;
+    fe* a = (fe*)malloc(sizeof(fe) * n);
+    for (uint64_t i = 0; i < n; ++i) to_mont(&FR, data + 32 * i, &a[i]);
+    fe gpow, g, ginv;
+    uint8_t five[32] = {5};
+    to_mont(&FR, five, &g);
+    finv(&FR, &g, &ginv);
+    if (coset && !inverse) { /* a_i *= g^i */
+        memcpy(gpow.v, FR.one, 32);
+        for (uint64_t i = 0; i < n; ++i) {
+            fmul(&FR, &a[i], &gpow, &a[i]);
+            fmul(&FR, &gpow, &g, &gpow);
+        }
+    }
+    /* bit reversal */
+    for (uint64_t i = 0, j = 0; i < n; ++i) {
+        if (i < j) { fe t = a[i]; a[i] = a[j]; a[j] = t; }
+        uint64_t bit = n >> 1;
+        for (; j & bit; bit >>= 1) j ^= bit;
+        j |= bit;
+    }
+    fe w;
+    fr_root(logn, inverse, &w);
+    uint64_t half_n = n > 1 ? n / 2 : 1;
+    fe* tw = (fe*)malloc(sizeof(fe) * half_n);
+    memcpy(tw[0].v, FR.one, 32);
+    for (uint64_t k = 1; k < half_n; ++k) fmul(&FR, &tw[k - 1], &w, &tw[k]);
+    if (threads < 1) threads = 1;
+    if (threads > 64) threads = 64;
+    for (uint64_t half = 1; half < n; half <<= 1) {
+        ntt_job jobs[64];
+        pthread_t tid[64];
+        int T = (n >= 4096) ? threads : 1;
+        for (int t = 0; t < T; ++t) {
+            jobs[t] = (ntt_job){a, tw, n, half, n / (2 * half), t, T};
+            if (T > 1) pthread_create(&tid[t], NULL, ntt_stage, &jobs[t]);
+            else ntt_stage(&jobs[t]);
+        }
+        if (T > 1)
+            for (int t = 0; t < T; ++t) pthread_join(tid[t], NULL);
+    }
+    if (inverse) {
+        fe ninv, nn;
+        uint8_t nb[32] = {0};
+        memcpy(nb, &n, 8);
+        to_mont(&FR, nb, &nn);
+        finv(&FR, &nn, &ninv);
+        fe gi;
+        memcpy(gi.v, FR.one, 32);
+        for (uint64_t i = 0; i < n; ++i) {
+            fmul(&FR, &a[i], &ninv, &a[i]);
+            if (coset) {
+                fmul(&FR, &a[i], &gi, &a[i]);
+                fmul(&FR, &gi, &ginv, &gi);
+            }
+        }
+    }
+    for (uint64_t i = 0; i < n; ++i) from_mont(&FR, &a[i], data + 32 * i);
+    free(a);
+    free(tw);
+}
+
+void bn_dft_naive(const uint8_t* in, uint32_t logn, int inverse, uint8_t* out) {
+    uint64_t n = 1ull << logn;
+    fe* a = (fe*)malloc(sizeof(fe) * n);
+    for (uint64_t i = 0; i < n; ++i) to_mont(&FR, in + 32 * i, &a[i]);
+    fe w, wi;
+    fr_root(logn, inverse, &w);
+    memcpy(wi.v, FR.one, 32); /* w^i */
+    fe ninv;
+    {
+        uint8_t nb[32] = {0};
+        memcpy(nb, &n, 8);
+        fe nn;
+        to_mont(&FR, nb, &nn);
+        finv(&FR, &nn, &ninv);
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        fe acc = {{0, 0, 0, 0}}, x;
+        memcpy(x.v, FR.one, 32); /* (w^i)^j */
+        for (uint64_t j = 0; j < n; ++j) {
+            fe t;
+            fmul(&FR, &a[j], &x, &t);
+            fadd(&FR, &acc, &t, &acc);
+            fmul(&FR, &x, &wi, &x);
+        }
+        if (inverse) fmul(&FR, &acc, &ninv, &acc);
+        from_mont(&FR, &acc, out + 32 * i);
+        fmul(&FR, &wi, &w, &wi);
+    }
+    free(a);
+}
+
+/* ------------------------------------------------------------- Fq2 */
+typedef struct { fe c0, c1; } fe2;
+
+static void f2add(const fe2* a, const fe2* b, fe2* o) {
+    fadd(&FQ, &a->c0, &b->c0, &o->c0);
+    fadd(&FQ, &a->c1, &b->c1, &o->c1);
+}
+static void f2sub(const fe2* a, const fe2* b, fe2* o) {
+    fsub(&FQ, &a->c0, &b->c0, &o->c0);
+    fsub(&FQ, &a->c1, &b->c1, &o->c1);
+}
+static void f2mul(const fe2* a, const fe2* b, fe2* o) {
+    fe t0, t1, t2, s0, s1;
+    fmul(&FQ, &a->c0, &b->c0, &t0);
+    fmul(&FQ, &a->c1, &b->c1, &t1);
+    fadd(&FQ, &a->c0, &a->c1, &s0);
+    fadd(&FQ, &b->c0, &b->c1, &s1);
+    fmul(&FQ, &s0, &s1, &t2);
+    fsub(&FQ, &t0, &t1, &o->c0);  /* u^2 = -1 */
+    fsub(&FQ, &t2, &t0, &t2);
+    fsub(&FQ, &t2, &t1, &o->c1);
+}
+static void f2inv(const fe2* a, fe2* o) {
+    fe t0, t1, n, ni;
+    fmul(&FQ, &a->c0, &a->c0, &t0);
+    fmul(&FQ, &a->c1, &a->c1, &t1);
+    fadd(&FQ, &t0, &t1, &n);
+    finv(&FQ, &n, &ni);
+    fmul(&FQ, &a->c0, &ni, &o->c0);
+    fe z = {{0, 0, 0, 0}};
+    fmul(&FQ, &a->c1, &ni, &t0);
+    fsub(&FQ, &z, &t0, &o->c1);
+}
+
+/* --------------------------------------------------------- generic curve
+ * Jacobian coordinates over a field with ops table; a = 0 (y^2 = x^3 + b). */
+typedef struct {
+    int deg;  /* 1: Fq, 2: Fq2 */
+} curve_t;
+
+/* element = up to 2 fe; store as fe2 and ignore c1 for G1 */
+typedef fe2 E;
+
+static void eadd(int g, const E* a, const E* b, E* o) {
+    if (g == 1) { fadd(&FQ, &a->c0, &b->c0, &o->c0); memset(&o->c1, 0, 32); }
+    else f2add(a, b, o);
+}
+static void esub(int g, const E* a, const E* b, E* o) {
+    if (g == 1) { fsub(&FQ, &a->c0, &b->c0, &o->c0); memset(&o->c1, 0, 32); }
+    else f2sub(a, b, o);
+}
+static void emul(int g, const E* a, const E* b, E* o) {
+    if (g == 1) { fmul(&FQ, &a->c0, &b->c0, &o->c0); memset(&o->c1, 0, 32); }
+    else f2mul(a, b, o);
+}
+static void einv(int g, const E* a, E* o) {
+    if (g == 1) { finv(&FQ, &a->c0, &o->c0); memset(&o->c1, 0, 32); }
+    else f2inv(a, o);
+}
+static int eis_zero(const E* a) { return fis_zero(&a->c0) && fis_zero(&a->c1); }
+static int eeq(const E* a, const E* b) { return feq(&a->c0, &b->c0) && feq(&a->c1, &b->c1); }
+static void eone(E* o) { memcpy(o->c0.v, FQ.one, 32); memset(&o->c1, 0, 32); }
+
+typedef struct { E X, Y, Z; } jac;  /* Z = 0: infinity */
+
+static void jdbl(int g, const jac* p, jac* o) {
+    if (eis_zero(&p->Z)) { *o = *p; return; }
+    /* dbl-2009-l (a = 0) */
+    E A, B, C, D, E_, F, t, X3, Y3, Z3;
+    emul(g, &p->X, &p->X, &A);
+    emul(g, &p->Y, &p->Y, &B);
+    emul(g, &B, &B, &C);
+    eadd(g, &p->X, &B, &t);
+    emul(g, &t, &t, &t);
+    esub(g, &t, &A, &t);
+    esub(g, &t, &C, &t);
+    eadd(g, &t, &t, &D);
+    eadd(g, &A, &A, &E_);
+    eadd(g, &E_, &A, &E_);
+    emul(g, &E_, &E_, &F);
+    esub(g, &F, &D, &X3);
+    esub(g, &X3, &D, &X3);
+    esub(g, &D, &X3, &t);
+    emul(g, &E_, &t, &Y3);
+    E c8;
+    eadd(g, &C, &C, &c8);
+    eadd(g, &c8, &c8, &c8);
+    eadd(g, &c8, &c8, &c8);
+    esub(g, &Y3, &c8, &Y3);
+    emul(g, &p->Y, &p->Z, &Z3);
+    eadd(g, &Z3, &Z3, &Z3);
+    o->X = X3; o->Y = Y3; o->Z = Z3;
+}
+
+static void jadd(int g, const jac* p, const jac* q, jac* o) {
+    if (eis_zero(&p->Z)) { *o = *q; return; }
+    if (eis_zero(&q->Z)) { *o = *p; return; }
+    /* add-2007-bl */
+    E Z1Z1, Z2Z2, U1, U2, S1, S2, H, I, J, r, V, t, X3, Y3, Z3;
+    emul(g, &p->Z, &p->Z, &Z1Z1);
+    emul(g, &q->Z, &q->Z, &Z2Z2);
+    emul(g, &p->X, &Z2Z2, &U1);
+    emul(g, &q->X, &Z1Z1, &U2);
+    emul(g, &q->Z, &Z2Z2, &t);
+    emul(g, &p->Y, &t, &S1);
+    emul(g, &p->Z, &Z1Z1, &t);
+    emul(g, &q->Y, &t, &S2);
+    if (eeq(&U1, &U2)) {
+        if (eeq(&S1, &S2)) { jdbl(g, p, o); return; }
+        memset(o, 0, sizeof *o);
+        eone(&o->X); eone(&o->Y);
+        return;
+    }
+    esub(g, &U2, &U1, &H);
+    eadd(g, &H, &H, &I);
+    emul(g, &I, &I, &I);
+    emul(g, &H, &I, &J);
+    esub(g, &S2, &S1, &r);
+    eadd(g, &r, &r, &r);
+    emul(g, &U1, &I, &V);
+    emul(g, &r, &r, &X3);
+    esub(g, &X3, &J, &X3);
+    esub(g, &X3, &V, &X3);
+    esub(g, &X3, &V, &X3);
+    esub(g, &V, &X3, &t);
+    emul(g, &r, &t, &Y3);
+    emul(g, &S1, &J, &t);
+    eadd(g, &t, &t, &t);
+    esub(g, &Y3, &t, &Y3);
+    eadd(g, &p->Z, &q->Z, &t);
+    emul(g, &t, &t, &t);
+    esub(g, &t, &Z1Z1, &t);
+    esub(g, &t, &Z2Z2, &t);
+    emul(g, &t, &H, &Z3);
+    o->X = X3; o->Y = Y3; o->Z = Z3;
+}
+
+static int bytes_zero(const uint8_t* p, int n) {
+    for (int i = 0; i < n; ++i) if (p[i]) return 0;
+    return 1;
+}
+
+static void load_aff(int g, const uint8_t* in, jac* o) {
+    int sz = 32 * g;
+    memset(o, 0, sizeof *o);
+    if (bytes_zero(in, 2 * sz)) { eone(&o->X); eone(&o->Y); return; }  /* infinity */
+    to_mont(&FQ, in, &o->X.c0);
+    to_mont(&FQ, in + sz, &o->Y.c0);
+    if (g == 2) {
+        to_mont(&FQ, in + 32, &o->X.c1);
+        to_mont(&FQ, in + 96, &o->Y.c1);
+        to_mont(&FQ, in + 64, &o->Y.c0);
+    }
+    eone(&o->Z);
+}
+
+static void store_aff(int g, const jac* p, uint8_t* out) {
+    int sz = 32 * g;
+    if (eis_zero(&p->Z)) { memset(out, 0, 2 * sz); return; }
+    E zi, zi2, zi3, x, y;
+    einv(g, &p->Z, &zi);
+    emul(g, &zi, &zi, &zi2);
+    emul(g, &zi2, &zi, &zi3);
+    emul(g, &p->X, &zi2, &x);
+    emul(g, &p->Y, &zi3, &y);
+    from_mont(&FQ, &x.c0, out);
+    if (g == 2) {
+        from_mont(&FQ, &x.c1, out + 32);
+        from_mont(&FQ, &y.c0, out + 64);
+        from_mont(&FQ, &y.c1, out + 96);
+    } else {
+        from_mont(&FQ, &y.c0, out + 32);
+    }
+}
+
+static void curve_b(int g, E* b) {
+    memset(b, 0, sizeof *b);
+    uint8_t three[32] = {3};
+    to_mont(&FQ, three, &b->c0);
+    if (g == 2) { /* 3 / (9 + u) */
+        E d;
+        uint8_t nine[32] = {9}, one[32] = {1};
+        to_mont(&FQ, nine, &d.c0);
+        to_mont(&FQ, one, &d.c1);
+        E di;
+        einv(2, &d, &di);
+        emul(2, b, &di, b);
+    }
+}
+
+int bn_on_curve(int g, const uint8_t* p) {
+    if (bytes_zero(p, 64 * g)) return 1;
+    jac P;
+    load_aff(g, p, &P);
+    E y2, x3, b;
+    emul(g, &P.Y, &P.Y, &y2);
+    emul(g, &P.X, &P.X, &x3);
+    emul(g, &x3, &P.X, &x3);
+    curve_b(g, &b);
+    eadd(g, &x3, &b, &x3);
+    return eeq(&y2, &x3);
+}
+
+static const char* G2X0 = "10857046999023057135944570762232829481370756359578518086990519993285655852781";
+static const char* G2X1 = "11559732032986387107991004021392285783925812861821192530917403151452391805634";
+static const char* G2Y0 = "8495653923123431417604973247489272438418190587263600148770280649306958101930";
+static const char* G2Y1 = "4082367875863433681332203403145435568316851327593401208105741076214120093531";
+
+static void dec_to_le(const char* s, uint8_t* out) {
+    uint64_t v[4] = {0, 0, 0, 0};
+    for (; *s; ++s) { /* v = v*10 + d */
+        uint64_t c = (uint64_t)(*s - '0');
+        for (int i = 0; i < 4; ++i) {
+            u128 x = (u128)v[i] * 10 + c;
+            v[i] = (uint64_t)x;
+            c = (uint64_t)(x >> 64);
+        }
+    }
+    memcpy(out, v, 32);
+}
+
+void bn_generator(int g, uint8_t* out) {
+    if (g == 1) {
+        memset(out, 0, 64);
+        out[0] = 1;
+        out[32] = 2;
+    } else {
+        dec_to_le(G2X0, out);
+        dec_to_le(G2X1, out + 32);
+        dec_to_le(G2Y0, out + 64);
+        dec_to_le(G2Y1, out + 96);
+    }
+}
+
+void bn_point_add(int g, const uint8_t* a, const uint8_t* b, uint8_t* out) {
+    jac P, Q, R;
+    load_aff(g, a, &P);
+    load_aff(g, b, &Q);
+    jadd(g, &P, &Q, &R);
+    store_aff(g, &R, out);
+}
+
+void bn_point_double(int g, const uint8_t* a, uint8_t* out) {
+    jac P, R;
+    load_aff(g, a, &P);
+    jdbl(g, &P, &R);
+    store_aff(g, &R, out);
+}
+
+void bn_point_neg(int g, const uint8_t* a, uint8_t* out) {
+    jac P;
+    load_aff(g, a, &P);
+    E z;
+    memset(&z, 0, sizeof z);
+    esub(g, &z, &P.Y, &P.Y);
+    store_aff(g, &P, out);
+}
+
+static void jmul(int g, const jac* P, const uint64_t s[4], jac* o) {
+    jac R;
+    memset(&R, 0, sizeof R);
+    eone(&R.X); eone(&R.Y);
+    for (int i = 255; i >= 0; --i) {
+        jdbl(g, &R, &R);
+        if (s[i >> 6] >> (i & 63) & 1) jadd(g, &R, P, &R);
+    }
+    *o = R;
+}
+
+void bn_scalar_mul(int g, const uint8_t* p, const uint8_t* scalar, uint8_t* out) {
+    jac P, R;
+    uint64_t s[4];
+    memcpy(s, scalar, 32);
+    load_aff(g, p, &P);
+    jmul(g, &P, s, &R);
+    store_aff(g, &R, out);
+}
+
+typedef struct {
+    int g;
+    const uint8_t *base, *scalars;
+    uint8_t* out;
+    uint64_t b, e;
+} fbm_job;
+
+static void* fbm_run(void* p) {
+    fbm_job* j = (fbm_job*)p;
+    for (uint64_t i = j->b; i < j->e; ++i)
+        bn_scalar_mul(j->g, j->base, j->scalars + 32 * i, j->out + 64 * j->g * i);
+    return NULL;
+}
+
+void bn_fixed_base_muls(int g, const uint8_t* base, const uint8_t* scalars, uint64_t n,
+                        uint8_t* out, int threads) {
+    if (threads < 1) threads = 1;
+    if (threads > 64) threads = 64;
+    pthread_t tid[64];
+    fbm_job jobs[64];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (fbm_job){g, base, scalars, out, n * t / threads, n * (t + 1) / threads};
+        pthread_create(&tid[t], NULL, fbm_run, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+}
+
+/* Bucket MSM, window 8: each thread owns a subset of windows. */
+typedef struct {
+    int g;
+    const uint8_t *pts, *sc;
+    uint64_t n;
+    int w0, w1;
+    jac* wsum;
+} msm_job;
+
+static void* msm_run(void* p) {
+    msm_job* j = (msm_job*)p;
+    const int g = j->g;
+    jac* bk = (jac*)malloc(sizeof(jac) * 256);
+    for (int w = j->w0; w < j->w1; ++w) {
+        for (int k = 0; k < 256; ++k) {
+            memset(&bk[k], 0, sizeof(jac));
+            eone(&bk[k].X); eone(&bk[k].Y);
+        }
+        for (uint64_t i = 0; i < j->n; ++i) {
+            unsigned d = j->sc[32 * i + w];
+            if (!d) continue;
+            jac P;
+            load_aff(g, j->pts + 64 * g * i, &P);
+            jadd(g, &bk[d], &P, &bk[d]);
+        }
+        jac run, tot;
+        memset(&run, 0, sizeof run); eone(&run.X); eone(&run.Y);
+        tot = run;
+        for (int k = 255; k >= 1; --k) {
+            jadd(g, &run, &bk[k], &run);
+            jadd(g, &tot, &run, &tot);
+        }
+        j->wsum[w] = tot;
+    }
+    free(bk);
+    return NULL;
+}
+
+void bn_msm(int g, const uint8_t* pts, const uint8_t* sc, uint64_t n, uint8_t* out, int threads) {
+    jac wsum[32];
+    if (threads < 1) threads = 1;
+    if (threads > 32) threads = 32;
+    pthread_t tid[32];
+    msm_job jobs[32];
+    for (int t = 0; t < threads; ++t) {
+        jobs[t] = (msm_job){g, pts, sc, n, 32 * t / threads, 32 * (t + 1) / threads, wsum};
+        pthread_create(&tid[t], NULL, msm_run, &jobs[t]);
+    }
+    for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
+    jac acc = wsum[31];
+    for (int w = 30; w >= 0; --w) {
+        for (int k = 0; k < 8; ++k) jdbl(g, &acc, &acc);
+        jadd(g, &acc, &wsum[w], &acc);
+    }
+    store_aff(g, &acc, out);
+}

@@ -60,6 +60,17 @@ _SIGS = {
     "acegpu_witness_xor": (C.c_int, [ctxp, vp, vp, vp, vp, u64, u64, vp]),
     "acegpu_sha256_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
     "acegpu_sha256_probe": (C.c_int, [ctxp, C.c_int, C.c_int, C.c_uint32, C.POINTER(C.c_double)]),
+    "acegpu_bn_field_batch": (C.c_int, [ctxp, C.c_int, C.c_int, vp, vp, u64, vp]),
+    "acegpu_bn_convert_dev": (C.c_int, [ctxp, vp, C.c_int, vp, u64, C.c_int]),
+    "acegpu_bn_ntt": (C.c_int, [ctxp, vp, C.c_uint32, C.c_int, C.c_int]),
+    "acegpu_bn_ntt_dev": (C.c_int, [ctxp, vp, vp, vp, C.c_uint32, C.c_int, C.c_int]),
+    "acegpu_bn_scalar_muls": (C.c_int, [ctxp, C.c_int, vp, vp, u64, vp]),
+    "acegpu_bn_msm_prepare": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, C.POINTER(C.c_void_p)]),
+    "acegpu_bn_msm_free": (None, [C.c_void_p]),
+    "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),
+    "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),
+    "acegpu_imad_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
+    "acegpu_bn_mul_rate": (C.c_int, [ctxp, C.c_int, C.POINTER(C.c_double)]),
 }
 
 

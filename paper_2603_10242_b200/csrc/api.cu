@@ -11,7 +11,10 @@
 #include <vector>
 
 #include "../../include/acegpu.h"
+#include "bn_kernels.cuh"
 #include "mock_kernels.cuh"
+#include "msm.cuh"
+#include "ntt.cuh"
 
 #ifndef ACEGPU_GIT
 #define ACEGPU_GIT "dev"
@@ -50,7 +53,7 @@ int fail(int code, const std::string& msg) {
 
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
-    kBlockHash, kOut, kIn2, kMisc, kNumSlots
+    kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kNumSlots
 };
 
 struct DevBuf {
@@ -77,6 +80,17 @@ struct acegpu_ctx {
     bool timing = false;
     bool ev_recorded = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // BN254: NTT twiddle tables per log-size, MSM scratch.
+    ace_gpu::bn::NttTables ntt[ace_gpu::bn::kNttMaxLog + 1];
+    ace_gpu::bn::MsmScratch msm;
+};
+
+// A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
+struct acegpu_msm_bases {
+    int device = 0;
+    int group = 1;
+    uint64_t n = 0;
+    uint8_t* table = nullptr;  // kMsmWindows * n affine points, Montgomery form
 };
 
 namespace {
@@ -286,6 +300,8 @@ void acegpu_destroy(acegpu_ctx* c) {
     cudaStreamSynchronize(c->stream);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& t : c->ntt) t.release();
+    c->msm.release();
     for (auto& b : c->bufs)
         if (b.p) cudaFree(b.p);
     cudaStreamDestroy(c->stream);
@@ -902,5 +918,237 @@ extern "C" int acegpu_sha256_probe(acegpu_ctx* c, int blocks, int threads, uint3
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     *seconds = ms * 1e-3;
+    return ACEGPU_OK;
+}
+
+// ===================================================================== BN254
+// North-star additions. No reference counterpart.
+namespace {
+
+int bn_time(acegpu_ctx* c, cudaStream_t s, void (*launch)(void*), void* arg, float* ms) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    launch(arg);  // warm-up
+    CK(cudaEventRecord(e0, s));
+    launch(arg);
+    CK(cudaEventRecord(e1, s));
+    CKL();
+    CK(cudaEventSynchronize(e1));
+    CK(cudaEventElapsedTime(ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    (void)c;
+    return ACEGPU_OK;
+}
+
+}  // namespace
+
+extern "C" int acegpu_bn_field_batch(acegpu_ctx* c, int field, int op, const uint8_t* a,
+                                     const uint8_t* b, uint64_t n, uint8_t* out) {
+    if (field < 0 || field > 1 || op < 0 || op > 4) return fail(ACEGPU_EINVAL, "bad field/op");
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *da, *db = nullptr, *dout;
+    RET(h2d_t(c, kBnA, a, 32 * n, s, &da));
+    if (b && op <= 2) RET(h2d_t(c, kBnB, b, 32 * n, s, &db));
+    RET(ws(c, kBnOut, 32 * n, &dout));
+    bn::launch_field_batch(field, op, da, db, n, dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_convert_dev(acegpu_ctx* c, void* stream, int field, uint8_t* d_data,
+                                     uint64_t n, int to_mont) {
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    if (field == 1) bn::launch_fr_convert(d_data, n, to_mont, s);
+    else bn::launch_fq_convert(d_data, n, to_mont, s);
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_ntt_dev(acegpu_ctx* c, void* stream, const uint8_t* d_in, uint8_t* d_out,
+                                 uint32_t logn, int inverse, int coset) {
+    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^22");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    if (bn::ntt_tables(c->ntt[logn], (int)logn, s)) return fail(ACEGPU_ECUDA, "NTT tables");
+    uint8_t* scratch = nullptr;
+    if ((int)logn > bn::kNttSingleMax) RET(ws(c, kBnScratch, 32ull << logn, &scratch));
+    if (bn::ntt_run(c->ntt[logn], d_in, d_out, scratch, inverse, coset, 1, s))
+        return fail(ACEGPU_ECUDA, std::string("NTT launch: ") + cudaGetErrorString(cudaGetLastError()));
+    c->launches += (int)logn > bn::kNttSingleMax ? 2 : 1;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_ntt(acegpu_ctx* c, uint8_t* data, uint32_t logn, int inverse,
+                             int coset) {
+    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^22");
+    const uint64_t n = 1ull << logn;
+    uint8_t* d;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard g(c->device);
+        RET(h2d_t(c, kBnA, data, 32 * n, c->stream, &d));
+        bn::launch_fr_convert(d, n, 1, c->stream);
+        CKL();
+    }
+    RET(acegpu_bn_ntt_dev(c, c->stream, d, d, logn, inverse, coset));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    bn::launch_fr_convert(d, n, 0, c->stream);
+    CKL();
+    c->launches += 2;
+    CK(cudaMemcpyAsync(data, d, 32 * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_scalar_muls(acegpu_ctx* c, int group, const uint8_t* base,
+                                     const uint8_t* scalars, uint64_t n, uint8_t* out) {
+    if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
+    if (n == 0) return ACEGPU_OK;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t pb = 64ull * group;
+    uint8_t *dbase, *dsc, *dout;
+    RET(h2d_t(c, kBnA, base, pb, s, &dbase));
+    RET(h2d_t(c, kBnB, scalars, 32 * n, s, &dsc));
+    RET(ws(c, kBnOut, pb * n, &dout));
+    bn::launch_points_convert(group, dbase, 1, 1, s);
+    bn::launch_scalar_muls(group, dbase, dsc, n, dout, s);
+    bn::launch_points_convert(group, dout, n, 0, s);
+    CKL();
+    c->launches += 3;
+    CK(cudaMemcpyAsync(out, dout, pb * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* points,
+                                     uint64_t n, int on_device, acegpu_msm_bases** out) {
+    if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
+    if (n == 0 || n > (1ull << 27)) return fail(ACEGPU_EINVAL, "MSM size must be 1..2^27");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t pb = 64ull * group;
+    auto* b = new acegpu_msm_bases();
+    b->device = c->device;
+    b->group = group;
+    b->n = n;
+    uint8_t* tmp = nullptr;
+    cudaError_t e = cudaMalloc(&b->table, pb * n * bn::kMsmWindows);
+    if (e == cudaSuccess) e = cudaMalloc(&tmp, pb * n);
+    if (e != cudaSuccess) {
+        if (b->table) cudaFree(b->table);
+        delete b;
+        return fail(ACEGPU_ECUDA, std::string("msm_prepare alloc: ") + cudaGetErrorString(e));
+    }
+    CK(cudaMemcpyAsync(tmp, points, pb * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    bn::launch_points_convert(group, tmp, n, 1, s);
+    if (bn::msm_prepare(group, tmp, n, b->table, s)) {
+        cudaFree(tmp);
+        return fail(ACEGPU_ECUDA, "msm_prepare launch");
+    }
+    CK(cudaStreamSynchronize(s));
+    cudaFree(tmp);
+    c->launches += 2;
+    *out = b;
+    return ACEGPU_OK;
+}
+
+extern "C" void acegpu_bn_msm_free(acegpu_msm_bases* b) {
+    if (!b) return;
+    DeviceGuard g(b->device);
+    if (b->table) cudaFree(b->table);
+    delete b;
+}
+
+extern "C" int acegpu_bn_msm_run_dev(acegpu_ctx* c, void* stream, const acegpu_msm_bases* b,
+                                     const uint8_t* d_scalars, uint8_t* d_out) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    if (bn::msm_run(b->group, b->table, b->n, d_scalars, c->msm, d_out, s))
+        return fail(ACEGPU_ECUDA, std::string("msm_run: ") + cudaGetErrorString(cudaGetLastError()));
+    c->launches += 7;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_msm_run(acegpu_ctx* c, const acegpu_msm_bases* b,
+                                 const uint8_t* scalars, uint8_t* out) {
+    uint8_t *dsc, *dout;
+    const uint64_t pb = 64ull * b->group;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard g(c->device);
+        RET(h2d_t(c, kBnB, scalars, 32 * b->n, c->stream, &dsc));
+        RET(ws(c, kBnOut, pb, &dout));
+    }
+    RET(acegpu_bn_msm_run_dev(c, c->stream, b, dsc, dout));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    bn::launch_points_convert(b->group, dout, 1, 0, c->stream);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out, dout, pb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ACEGPU_OK;
+}
+
+namespace {
+struct PeakArg {
+    uint32_t* sink;
+    int blocks, threads, field;
+    uint32_t iters;
+    cudaStream_t s;
+};
+void imad_launch(void* p) {
+    auto* a = static_cast<PeakArg*>(p);
+    bn::launch_imad_peak(a->sink, a->iters, a->blocks, a->threads, a->s);
+}
+void mulrate_launch(void* p) {
+    auto* a = static_cast<PeakArg*>(p);
+    bn::launch_mul_rate(a->field, a->sink, a->iters, a->blocks, a->threads, a->s);
+}
+}  // namespace
+
+extern "C" int acegpu_imad_peak(acegpu_ctx* c, double* imad_per_s) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    uint32_t* sink;
+    RET(ws(c, kMisc, 16, &sink));
+    PeakArg a{sink, sms * 8, 256, 0, 4096, c->stream};
+    float ms = 0;
+    RET(bn_time(c, c->stream, imad_launch, &a, &ms));
+    c->launches += 2;
+    *imad_per_s = double(a.blocks) * a.threads * a.iters * 16 * 8 / (ms * 1e-3);
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_mul_rate(acegpu_ctx* c, int field, double* muls_per_s) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    uint32_t* sink;
+    RET(ws(c, kMisc, 16, &sink));
+    PeakArg a{sink, sms * 4, 256, field, 2048, c->stream};
+    float ms = 0;
+    RET(bn_time(c, c->stream, mulrate_launch, &a, &ms));
+    c->launches += 2;
+    *muls_per_s = double(a.blocks) * a.threads * a.iters * 4 / (ms * 1e-3);
     return ACEGPU_OK;
 }

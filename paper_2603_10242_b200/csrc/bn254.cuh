@@ -1,0 +1,302 @@
+// BN254 field arithmetic for sm_100a: 8 x 32-bit limbs (little-endian),
+// Montgomery form (R = 2^256), CIOS multiplication as PTX carry chains
+// (mad.lo.cc / madc.hi.cc on the IMAD pipe). Fq = base field p, Fr = scalar
+// field r. The reference has no BN254 code;
+// parity is against the from-scratch CPU oracle (oracle/bn254_oracle.c).
+//
+// Bounds: both moduli are < 2^254, so the CIOS accumulator stays < 2p + p*2^32
+// < 2^288 (nine limbs, no tenth) and results are fully reduced to [0, m).
+#pragma once
+#include <cstdint>
+
+namespace ace_gpu {
+namespace bn {
+
+struct FqCfg {
+    static constexpr uint32_t M[8] = {0xd87cfd47u, 0x3c208c16u, 0x6871ca8du, 0x97816a91u,
+                                      0x8181585du, 0xb85045b6u, 0xe131a029u, 0x30644e72u};
+    static constexpr uint32_t ONE[8] = {0xc58f0d9du, 0xd35d438du, 0xf5c70b3du, 0x0a78eb28u,
+                                        0x7879462cu, 0x666ea36fu, 0x9a07df2fu, 0x0e0a77c1u};
+    static constexpr uint32_t R2[8] = {0x538afa89u, 0xf32cfc5bu, 0xd44501fbu, 0xb5e71911u,
+                                       0x0a417ff6u, 0x47ab1effu, 0xcab8351fu, 0x06d89f71u};
+    static constexpr uint32_t N0 = 0xe4866389u;
+};
+
+struct FrCfg {
+    static constexpr uint32_t M[8] = {0xf0000001u, 0x43e1f593u, 0x79b97091u, 0x2833e848u,
+                                      0x8181585du, 0xb85045b6u, 0xe131a029u, 0x30644e72u};
+    static constexpr uint32_t ONE[8] = {0x4ffffffbu, 0xac96341cu, 0x9f60cd29u, 0x36fc7695u,
+                                        0x7879462eu, 0x666ea36fu, 0x9a07df2fu, 0x0e0a77c1u};
+    static constexpr uint32_t R2[8] = {0xae216da7u, 0x1bb8e645u, 0xe35c59e3u, 0x53fe3ab1u,
+                                       0x53bb8085u, 0x8c49833du, 0x7f4e44a5u, 0x0216d0b1u};
+    static constexpr uint32_t N0 = 0xefffffffu;
+};
+
+// Limb accessors usable in device code with run-time indices (a static
+// constexpr member array may not be odr-used on the device).
+template <class C>
+__device__ __forceinline__ uint32_t mod_limb(int i) {
+    constexpr uint32_t a[8] = {C::M[0], C::M[1], C::M[2], C::M[3],
+                               C::M[4], C::M[5], C::M[6], C::M[7]};
+    return a[i];
+}
+template <class C>
+__device__ __forceinline__ uint32_t one_limb(int i) {
+    constexpr uint32_t a[8] = {C::ONE[0], C::ONE[1], C::ONE[2], C::ONE[3],
+                               C::ONE[4], C::ONE[5], C::ONE[6], C::ONE[7]};
+    return a[i];
+}
+template <class C>
+__device__ __forceinline__ uint32_t r2_limb(int i) {
+    constexpr uint32_t a[8] = {C::R2[0], C::R2[1], C::R2[2], C::R2[3],
+                               C::R2[4], C::R2[5], C::R2[6], C::R2[7]};
+    return a[i];
+}
+
+template <class C>
+struct Fp {
+    uint32_t v[8];
+
+    __device__ __forceinline__ static Fp zero() {
+        Fp r;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r.v[i] = 0;
+        return r;
+    }
+    __device__ __forceinline__ static Fp one() {
+        Fp r;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r.v[i] = one_limb<C>(i);
+        return r;
+    }
+    __device__ __forceinline__ bool is_zero() const {
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x |= v[i];
+        return x == 0;
+    }
+    __device__ __forceinline__ bool operator==(const Fp& o) const {
+        uint32_t x = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x |= v[i] ^ o.v[i];
+        return x == 0;
+    }
+};
+
+using Fq = Fp<FqCfg>;
+using Fr = Fp<FrCfg>;
+
+// t (9 limbs) -> t - m if t >= m (t < 2m guaranteed).
+template <class C>
+__device__ __forceinline__ void final_sub(uint32_t t[9], uint32_t r[8]) {
+    uint32_t s[8], br;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, %25, 0;"
+        : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]),
+          "=r"(s[7]), "=r"(br)
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]),
+          "n"(C::M[0]), "n"(C::M[1]), "n"(C::M[2]), "n"(C::M[3]), "n"(C::M[4]), "n"(C::M[5]),
+          "n"(C::M[6]), "n"(C::M[7]), "r"(t[8]));
+    // br == 0xffffffff iff t < m (borrow out of the 9-limb subtraction)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = br ? t[i] : s[i];
+}
+
+// CIOS Montgomery multiplication: r = a * b * 2^-256 mod m.
+template <class C>
+__device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
+    uint32_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0, t7 = 0, t8 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t bi = b.v[i];
+        // t += a * b_i : low halves into t0..t7 (carry into t8), high halves into t1..t8.
+        asm("mad.lo.cc.u32  %0, %9,  %17, %0;\n\t"
+            "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"
+            "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"
+            "madc.lo.cc.u32 %3, %12, %17, %3;\n\t"
+            "madc.lo.cc.u32 %4, %13, %17, %4;\n\t"
+            "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"
+            "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"
+            "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"
+            "addc.u32       %8, %8, 0;"
+            : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7),
+              "+r"(t8)
+            : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+              "r"(a.v[6]), "r"(a.v[7]), "r"(bi));
+        asm("mad.hi.cc.u32  %0, %8,  %16, %0;\n\t"
+            "madc.hi.cc.u32 %1, %9,  %16, %1;\n\t"
+            "madc.hi.cc.u32 %2, %10, %16, %2;\n\t"
+            "madc.hi.cc.u32 %3, %11, %16, %3;\n\t"
+            "madc.hi.cc.u32 %4, %12, %16, %4;\n\t"
+            "madc.hi.cc.u32 %5, %13, %16, %5;\n\t"
+            "madc.hi.cc.u32 %6, %14, %16, %6;\n\t"
+            "madc.hi.u32    %7, %15, %16, %7;"
+            : "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7), "+r"(t8)
+            : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+              "r"(a.v[6]), "r"(a.v[7]), "r"(bi));
+        const uint32_t m = t0 * C::N0;
+        // t += m * M, then t >>= 32 (t0 becomes 0 and is dropped).
+        asm("mad.lo.cc.u32  %0, %9,  %10, %0;\n\t"
+            "madc.lo.cc.u32 %1, %9,  %11, %1;\n\t"
+            "madc.lo.cc.u32 %2, %9,  %12, %2;\n\t"
+            "madc.lo.cc.u32 %3, %9,  %13, %3;\n\t"
+            "madc.lo.cc.u32 %4, %9,  %14, %4;\n\t"
+            "madc.lo.cc.u32 %5, %9,  %15, %5;\n\t"
+            "madc.lo.cc.u32 %6, %9,  %16, %6;\n\t"
+            "madc.lo.cc.u32 %7, %9,  %17, %7;\n\t"
+            "addc.u32       %8, %8, 0;"
+            : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7),
+              "+r"(t8)
+            : "r"(m), "n"(C::M[0]), "n"(C::M[1]), "n"(C::M[2]), "n"(C::M[3]), "n"(C::M[4]),
+              "n"(C::M[5]), "n"(C::M[6]), "n"(C::M[7]));
+        asm("mad.hi.cc.u32  %0, %8,  %9,  %0;\n\t"
+            "madc.hi.cc.u32 %1, %8,  %10, %1;\n\t"
+            "madc.hi.cc.u32 %2, %8,  %11, %2;\n\t"
+            "madc.hi.cc.u32 %3, %8,  %12, %3;\n\t"
+            "madc.hi.cc.u32 %4, %8,  %13, %4;\n\t"
+            "madc.hi.cc.u32 %5, %8,  %14, %5;\n\t"
+            "madc.hi.cc.u32 %6, %8,  %15, %6;\n\t"
+            "madc.hi.u32    %7, %8,  %16, %7;"
+            : "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7), "+r"(t8)
+            : "r"(m), "n"(C::M[0]), "n"(C::M[1]), "n"(C::M[2]), "n"(C::M[3]), "n"(C::M[4]),
+              "n"(C::M[5]), "n"(C::M[6]), "n"(C::M[7]));
+        t0 = t1; t1 = t2; t2 = t3; t3 = t4; t4 = t5; t5 = t6; t6 = t7; t7 = t8; t8 = 0;
+    }
+    uint32_t t[9] = {t0, t1, t2, t3, t4, t5, t6, t7, t8};
+    Fp<C> r;
+    final_sub<C>(t, r.v);
+    return r;
+}
+
+template <class C>
+__device__ __forceinline__ Fp<C> sqr(const Fp<C>& a) { return mul(a, a); }
+
+template <class C>
+__device__ __forceinline__ Fp<C> add(const Fp<C>& a, const Fp<C>& b) {
+    uint32_t t[9];
+    asm("add.cc.u32  %0, %9,  %17;\n\t"
+        "addc.cc.u32 %1, %10, %18;\n\t"
+        "addc.cc.u32 %2, %11, %19;\n\t"
+        "addc.cc.u32 %3, %12, %20;\n\t"
+        "addc.cc.u32 %4, %13, %21;\n\t"
+        "addc.cc.u32 %5, %14, %22;\n\t"
+        "addc.cc.u32 %6, %15, %23;\n\t"
+        "addc.cc.u32 %7, %16, %24;\n\t"
+        "addc.u32    %8, 0, 0;"
+        : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]),
+          "=r"(t[7]), "=r"(t[8])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+          "r"(a.v[6]), "r"(a.v[7]), "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]),
+          "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    Fp<C> r;
+    final_sub<C>(t, r.v);
+    return r;
+}
+
+template <class C>
+__device__ __forceinline__ Fp<C> sub(const Fp<C>& a, const Fp<C>& b) {
+    uint32_t t[8], br;
+    asm("sub.cc.u32  %0, %9,  %17;\n\t"
+        "subc.cc.u32 %1, %10, %18;\n\t"
+        "subc.cc.u32 %2, %11, %19;\n\t"
+        "subc.cc.u32 %3, %12, %20;\n\t"
+        "subc.cc.u32 %4, %13, %21;\n\t"
+        "subc.cc.u32 %5, %14, %22;\n\t"
+        "subc.cc.u32 %6, %15, %23;\n\t"
+        "subc.cc.u32 %7, %16, %24;\n\t"
+        "subc.u32    %8, 0, 0;"
+        : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]),
+          "=r"(t[7]), "=r"(br)
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+          "r"(a.v[6]), "r"(a.v[7]), "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]),
+          "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    // add back m & borrow-mask
+    Fp<C> r;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+          "=r"(r.v[6]), "=r"(r.v[7])
+        : "r"(t[0]), "r"(t[1]), "r"(t[2]), "r"(t[3]), "r"(t[4]), "r"(t[5]), "r"(t[6]), "r"(t[7]),
+          "r"(C::M[0] & br), "r"(C::M[1] & br), "r"(C::M[2] & br), "r"(C::M[3] & br),
+          "r"(C::M[4] & br), "r"(C::M[5] & br), "r"(C::M[6] & br), "r"(C::M[7] & br));
+    return r;
+}
+
+template <class C>
+__device__ __forceinline__ Fp<C> neg(const Fp<C>& a) {
+    return a.is_zero() ? a : sub(Fp<C>::zero(), a);
+}
+
+template <class C>
+__device__ __forceinline__ Fp<C> dbl(const Fp<C>& a) { return add(a, a); }
+
+// Standard (canonical, little-endian limbs) <-> Montgomery.
+template <class C>
+__device__ __forceinline__ Fp<C> to_mont(const Fp<C>& a) {
+    Fp<C> r2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r2.v[i] = r2_limb<C>(i);
+    return mul(a, r2);
+}
+
+template <class C>
+__device__ __forceinline__ Fp<C> from_mont(const Fp<C>& a) {
+    Fp<C> one;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) one.v[i] = i == 0 ? 1u : 0u;
+    return mul(a, one);
+}
+
+// a^e for a small public exponent given as 8 limbs (square-and-multiply).
+template <class C>
+__device__ Fp<C> pow(const Fp<C>& a, const uint32_t e[8]) {
+    Fp<C> r = Fp<C>::one(), b = a;
+    for (int i = 0; i < 256; ++i) {
+        if ((e[i >> 5] >> (i & 31)) & 1) r = mul(r, b);
+        b = sqr(b);
+    }
+    return r;
+}
+
+// Fermat inverse a^(m-2).
+template <class C>
+__device__ Fp<C> inv(const Fp<C>& a) {
+    uint32_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = mod_limb<C>(i);
+    e[0] -= 2;
+    return pow(a, e);
+}
+
+// 16-B vector loads / stores of one element (32 B, 16-B aligned).
+template <class C>
+__device__ __forceinline__ Fp<C> load(const void* p) {
+    const uint4* q = static_cast<const uint4*>(p);
+    uint4 x = q[0], y = q[1];
+    Fp<C> r;
+    r.v[0] = x.x; r.v[1] = x.y; r.v[2] = x.z; r.v[3] = x.w;
+    r.v[4] = y.x; r.v[5] = y.y; r.v[6] = y.z; r.v[7] = y.w;
+    return r;
+}
+template <class C>
+__device__ __forceinline__ void store(void* p, const Fp<C>& a) {
+    uint4* q = static_cast<uint4*>(p);
+    q[0] = make_uint4(a.v[0], a.v[1], a.v[2], a.v[3]);
+    q[1] = make_uint4(a.v[4], a.v[5], a.v[6], a.v[7]);
+}
+
+}  // namespace bn
+}  // namespace ace_gpu

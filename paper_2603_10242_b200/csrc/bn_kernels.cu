@@ -1,0 +1,139 @@
+// BN254 support kernels: batched field ops (parity tests), per-point scalar
+// multiplication (fixture generation: known-discrete-log bases k_i * G),
+// and the integer-pipe microbenchmarks that give the MSM/NTT roofline its
+// denominator (MEASURED_PEAKS.json has no integer peak).
+#include <cuda_runtime.h>
+
+#include "bn_kernels.cuh"
+#include "curve.cuh"
+
+namespace ace_gpu {
+namespace bn {
+
+namespace {
+
+template <class C>
+__global__ void field_batch_kernel(int op, const uint8_t* a, const uint8_t* b, uint64_t n,
+                                   uint8_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Fp<C> x = to_mont(load<C>(a + 32 * i));
+    Fp<C> y = (op == 3 || op == 4) ? x : to_mont(load<C>(b + 32 * i));
+    Fp<C> r;
+    switch (op) {
+        case 0: r = mul(x, y); break;
+        case 1: r = add(x, y); break;
+        case 2: r = sub(x, y); break;
+        case 3: r = sqr(x); break;
+        default: r = x.is_zero() ? x : inv(x); break;
+    }
+    store<C>(out + 32 * i, from_mont(r));
+}
+
+__device__ __forceinline__ Fq finv1(const Fq& a) { return inv(a); }
+__device__ __forceinline__ Fq2 finv1(const Fq2& a) {
+    Fq n = add(mul(a.c0, a.c0), mul(a.c1, a.c1));
+    Fq ni = inv(n);
+    return {mul(a.c0, ni), neg(mul(a.c1, ni))};
+}
+
+// out[i] = s_i * P (P affine Montgomery; s standard form); affine Montgomery out.
+template <class F>
+__global__ void scalar_muls_kernel(const uint8_t* base, const uint8_t* scalars, uint64_t n,
+                                   uint8_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    constexpr int E = felem_bytes<F>();
+    F x, y;
+    fload(x, base);
+    fload(y, base + E);
+    const uint4* q = reinterpret_cast<const uint4*>(scalars + 32 * i);
+    uint4 lo = q[0], hi = q[1];
+    const uint32_t s[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    XYZZ<F> acc = XYZZ<F>::inf();
+    for (int bit = 255; bit >= 0; --bit) {
+        acc = xyzz_dbl(acc);
+        if ((s[bit >> 5] >> (bit & 31)) & 1) acc = xyzz_madd(acc, x, y);
+    }
+    uint8_t* o = out + 2 * E * i;
+    if (acc.is_inf()) {
+        F z;
+        fset_zero(z);
+        fstore(o, z);
+        fstore(o + E, z);
+        return;
+    }
+    F t = finv1(fmul(acc.ZZ, acc.ZZZ));
+    fstore(o, fmul(acc.X, fmul(t, acc.ZZZ)));
+    fstore(o + E, fmul(acc.Y, fmul(t, acc.ZZ)));
+}
+
+// IMAD pipe: 8 independent mad.lo chains per thread.
+__global__ void imad_peak_kernel(uint32_t* sink, uint32_t iters) {
+    uint32_t a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 7u + k;
+    const uint32_t m = blockIdx.x | 0x9E3779B1u;
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[k]) : "r"(m), "r"(it));
+        }
+    }
+    uint32_t x = 0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x ^= a[k];
+    if (x == 0x1234567u) sink[0] = x;
+}
+
+// Montgomery multiplications: 4 independent chains per thread.
+template <class C>
+__global__ void mul_rate_kernel(uint32_t* sink, uint32_t iters) {
+    Fp<C> x[4], y = Fp<C>::one();
+    y.v[0] ^= blockIdx.x;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        x[k] = Fp<C>::one();
+        x[k].v[1] ^= threadIdx.x + k;
+    }
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = mul(x[k], y);
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc ^= x[k].v[0];
+    if (acc == 0x1234567u) sink[0] = acc;
+}
+
+}  // namespace
+
+void launch_field_batch(int field, int op, const uint8_t* a, const uint8_t* b, uint64_t n,
+                        uint8_t* out, cudaStream_t s) {
+    if (!n) return;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    if (field == 0) field_batch_kernel<FqCfg><<<g, 128, 0, s>>>(op, a, b, n, out);
+    else field_batch_kernel<FrCfg><<<g, 128, 0, s>>>(op, a, b, n, out);
+}
+
+void launch_scalar_muls(int group, const uint8_t* base, const uint8_t* scalars, uint64_t n,
+                        uint8_t* out, cudaStream_t s) {
+    if (!n) return;
+    const unsigned g = (unsigned)((n + 63) / 64);
+    if (group == 2) scalar_muls_kernel<Fq2><<<g, 64, 0, s>>>(base, scalars, n, out);
+    else scalar_muls_kernel<Fq><<<g, 64, 0, s>>>(base, scalars, n, out);
+}
+
+void launch_imad_peak(uint32_t* sink, uint32_t iters, int blocks, int threads, cudaStream_t s) {
+    imad_peak_kernel<<<blocks, threads, 0, s>>>(sink, iters);
+}
+
+void launch_mul_rate(int field, uint32_t* sink, uint32_t iters, int blocks, int threads,
+                     cudaStream_t s) {
+    if (field == 0) mul_rate_kernel<FqCfg><<<blocks, threads, 0, s>>>(sink, iters);
+    else mul_rate_kernel<FrCfg><<<blocks, threads, 0, s>>>(sink, iters);
+}
+
+}  // namespace bn
+}  // namespace ace_gpu

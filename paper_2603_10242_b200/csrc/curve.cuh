@@ -1,0 +1,193 @@
+// BN254 G1 (y^2 = x^3 + 3 over Fq) and G2 (y^2 = x^3 + 3/(9+u) over
+// Fq2 = Fq[u]/(u^2 + 1)) for sm_100a. Bucket accumulators use XYZZ
+// coordinates (x = X/ZZ, y = Y/ZZZ; ZZ = 0 is the point at infinity) with the
+// madd-2008-s / add-2008-s / dbl-2008-s-1 formulas (a = 0): a mixed add costs
+// 8M + 2S, a general add 12M + 2S. Fq2 multiplication is Karatsuba (3 Fq muls).
+#pragma once
+#include "bn254.cuh"
+
+namespace ace_gpu {
+namespace bn {
+
+struct Fq2 {
+    Fq c0, c1;
+};
+
+// ---- uniform field interface (Fq and Fq2) ---------------------------------
+__device__ __forceinline__ Fq fmul(const Fq& a, const Fq& b) { return mul(a, b); }
+__device__ __forceinline__ Fq fsqr(const Fq& a) { return mul(a, a); }
+__device__ __forceinline__ Fq fadd(const Fq& a, const Fq& b) { return add(a, b); }
+__device__ __forceinline__ Fq fsub(const Fq& a, const Fq& b) { return sub(a, b); }
+__device__ __forceinline__ bool fzero(const Fq& a) { return a.is_zero(); }
+__device__ __forceinline__ void fset_one(Fq& a) { a = Fq::one(); }
+__device__ __forceinline__ void fset_zero(Fq& a) { a = Fq::zero(); }
+__device__ __forceinline__ bool feq(const Fq& a, const Fq& b) { return a == b; }
+
+__device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
+    Fq t0 = mul(a.c0, b.c0), t1 = mul(a.c1, b.c1);
+    Fq t2 = mul(add(a.c0, a.c1), add(b.c0, b.c1));
+    return {sub(t0, t1), sub(sub(t2, t0), t1)};
+}
+__device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
+    // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u
+    Fq t = mul(a.c0, a.c1);
+    return {mul(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
+}
+__device__ __forceinline__ Fq2 fadd(const Fq2& a, const Fq2& b) {
+    return {add(a.c0, b.c0), add(a.c1, b.c1)};
+}
+__device__ __forceinline__ Fq2 fsub(const Fq2& a, const Fq2& b) {
+    return {sub(a.c0, b.c0), sub(a.c1, b.c1)};
+}
+__device__ __forceinline__ bool fzero(const Fq2& a) { return a.c0.is_zero() && a.c1.is_zero(); }
+__device__ __forceinline__ void fset_one(Fq2& a) { a.c0 = Fq::one(); a.c1 = Fq::zero(); }
+__device__ __forceinline__ void fset_zero(Fq2& a) { a.c0 = Fq::zero(); a.c1 = Fq::zero(); }
+__device__ __forceinline__ bool feq(const Fq2& a, const Fq2& b) { return a.c0 == b.c0 && a.c1 == b.c1; }
+
+template <class F>
+struct Affine {
+    F x, y;  // infinity encoded by the caller (all-zero record)
+};
+
+template <class F>
+struct XYZZ {
+    F X, Y, ZZ, ZZZ;
+
+    __device__ __forceinline__ static XYZZ inf() {
+        XYZZ p;
+        fset_one(p.X);
+        fset_one(p.Y);
+        fset_zero(p.ZZ);
+        fset_zero(p.ZZZ);
+        return p;
+    }
+    __device__ __forceinline__ bool is_inf() const { return fzero(ZZ); }
+};
+
+// dbl-2008-s-1 on an XYZZ point (a = 0).
+template <class F>
+__device__ __forceinline__ XYZZ<F> xyzz_dbl(const XYZZ<F>& p) {
+    if (p.is_inf()) return p;
+    F U = fadd(p.Y, p.Y);
+    F V = fsqr(U);
+    F W = fmul(U, V);
+    F S = fmul(p.X, V);
+    F X2 = fsqr(p.X);
+    F M = fadd(fadd(X2, X2), X2);
+    XYZZ<F> r;
+    r.X = fsub(fsub(fsqr(M), S), S);
+    r.Y = fsub(fmul(M, fsub(S, r.X)), fmul(W, p.Y));
+    r.ZZ = fmul(V, p.ZZ);
+    r.ZZZ = fmul(W, p.ZZZ);
+    return r;
+}
+
+// mdbl: double an affine point into XYZZ.
+template <class F>
+__device__ __forceinline__ XYZZ<F> xyzz_mdbl(const F& x, const F& y) {
+    F U = fadd(y, y);
+    F V = fsqr(U);
+    F W = fmul(U, V);
+    F S = fmul(x, V);
+    F X2 = fsqr(x);
+    F M = fadd(fadd(X2, X2), X2);
+    XYZZ<F> r;
+    r.X = fsub(fsub(fsqr(M), S), S);
+    r.Y = fsub(fmul(M, fsub(S, r.X)), fmul(W, y));
+    r.ZZ = V;
+    r.ZZZ = W;
+    return r;
+}
+
+// madd-2008-s: p + (x, y) with (x, y) affine, not infinity.
+template <class F>
+__device__ __forceinline__ XYZZ<F> xyzz_madd(const XYZZ<F>& p, const F& x, const F& y) {
+    if (p.is_inf()) {
+        XYZZ<F> r;
+        r.X = x;
+        r.Y = y;
+        fset_one(r.ZZ);
+        fset_one(r.ZZZ);
+        return r;
+    }
+    F U2 = fmul(x, p.ZZ);
+    F S2 = fmul(y, p.ZZZ);
+    F P = fsub(U2, p.X);
+    F R = fsub(S2, p.Y);
+    if (fzero(P)) {
+        if (fzero(R)) return xyzz_mdbl(x, y);
+        return XYZZ<F>::inf();
+    }
+    F PP = fsqr(P);
+    F PPP = fmul(P, PP);
+    F Q = fmul(p.X, PP);
+    XYZZ<F> r;
+    r.X = fsub(fsub(fsub(fsqr(R), PPP), Q), Q);
+    r.Y = fsub(fmul(R, fsub(Q, r.X)), fmul(p.Y, PPP));
+    r.ZZ = fmul(p.ZZ, PP);
+    r.ZZZ = fmul(p.ZZZ, PPP);
+    return r;
+}
+
+// add-2008-s: general XYZZ + XYZZ.
+template <class F>
+__device__ __forceinline__ XYZZ<F> xyzz_add(const XYZZ<F>& p, const XYZZ<F>& q) {
+    if (p.is_inf()) return q;
+    if (q.is_inf()) return p;
+    F U1 = fmul(p.X, q.ZZ);
+    F U2 = fmul(q.X, p.ZZ);
+    F S1 = fmul(p.Y, q.ZZZ);
+    F S2 = fmul(q.Y, p.ZZZ);
+    F P = fsub(U2, U1);
+    F R = fsub(S2, S1);
+    if (fzero(P)) {
+        if (fzero(R)) return xyzz_dbl(p);
+        return XYZZ<F>::inf();
+    }
+    F PP = fsqr(P);
+    F PPP = fmul(P, PP);
+    F Q = fmul(U1, PP);
+    XYZZ<F> r;
+    r.X = fsub(fsub(fsub(fsqr(R), PPP), Q), Q);
+    r.Y = fsub(fmul(R, fsub(Q, r.X)), fmul(S1, PPP));
+    r.ZZ = fmul(fmul(p.ZZ, q.ZZ), PP);
+    r.ZZZ = fmul(fmul(p.ZZZ, q.ZZZ), PPP);
+    return r;
+}
+
+template <class F>
+__device__ __forceinline__ XYZZ<F> xyzz_neg(const XYZZ<F>& p) {
+    XYZZ<F> r = p;
+    F z;
+    fset_zero(z);
+    r.Y = fsub(z, p.Y);
+    return r;
+}
+
+// k * p for a small scalar k (double-and-add, MSB first).
+template <class F>
+__device__ XYZZ<F> xyzz_mul_small(const XYZZ<F>& p, uint32_t k) {
+    XYZZ<F> r = XYZZ<F>::inf();
+    for (int b = 31; b >= 0; --b) {
+        r = xyzz_dbl(r);
+        if ((k >> b) & 1) r = xyzz_add(r, p);
+    }
+    return r;
+}
+
+// ---- element / point I/O (Montgomery form in memory, 16-B aligned) --------
+__device__ __forceinline__ void fload(Fq& a, const uint8_t* p) { a = load<FqCfg>(p); }
+__device__ __forceinline__ void fload(Fq2& a, const uint8_t* p) {
+    a.c0 = load<FqCfg>(p);
+    a.c1 = load<FqCfg>(p + 32);
+}
+__device__ __forceinline__ void fstore(uint8_t* p, const Fq& a) { store<FqCfg>(p, a); }
+__device__ __forceinline__ void fstore(uint8_t* p, const Fq2& a) {
+    store<FqCfg>(p, a.c0);
+    store<FqCfg>(p + 32, a.c1);
+}
+template <class F>
+constexpr int felem_bytes() { return sizeof(F) == sizeof(Fq) ? 32 : 64; }
+
+}  // namespace bn
+}  // namespace ace_gpu

@@ -1,0 +1,297 @@
+// Fr NTT / iNTT / coset-NTT for sm_100a (north-star row a21; the reference
+// has none). Natural order in and out.
+//
+// Four-step decomposition n = n1 * n2 (n1 = 2^L1, n2 = 2^L2, L2 = ceil(L/2)):
+//   i = i1 + n1*i2, k = k2 + n2*k1
+//   pass A: for each column i1, the size-n2 DFT over i2 of a[i1 + n1*i2],
+//           times the twiddle w^(i1*k2), stored at i1 + n1*k2 (scratch);
+//   pass C: for each k2, the size-n1 DFT over i1 of that row, stored at
+//           X[k2 + n2*k1] (natural order).
+// Each CTA owns R adjacent columns (pass A) / rows (pass C) so global
+// accesses are R*32-B contiguous; the sub-DFT runs entirely in shared memory
+// (bit-reversed load + radix-2 DIT stages), twiddles from small L1-resident
+// tables. Coset scaling (g^i on input) and the inverse's n^-1 (and g^-k) are
+// fused into the loads / stores. Compute: log2(n)/2 + 2 Fr muls per element,
+// IMAD-pipe bound (NTT at 2^21-2^22 is ~8x above the HBM ridge).
+#include <cuda_runtime.h>
+
+#include "bn254.cuh"
+#include "ntt.cuh"
+
+namespace ace_gpu {
+namespace bn {
+
+namespace {
+
+__device__ __forceinline__ Fr ld(const Fr* p) { return load<FrCfg>(p); }
+__device__ __forceinline__ void st(Fr* p, const Fr& x) { store<FrCfg>(p, x); }
+
+__device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
+    return __brev(x) >> (32 - bits);
+}
+
+// Shared-memory sub-DFT of size 2^m over R interleaved batches:
+// element (r, j) lives at s[j * R + r]. In: bit-reversed; out: natural.
+__device__ __forceinline__ void smem_dit(Fr* s, int m, int R, const Fr* __restrict__ w) {
+    const int half_n = 1 << (m - 1);
+    const int total = half_n * R;
+    for (int stage = 0; stage < m; ++stage) {
+        const int half = 1 << stage;
+        const int tw_shift = m - 1 - stage;  // w_sub^(j << tw_shift)
+        for (int b = threadIdx.x; b < total; b += blockDim.x) {
+            const int r = b % R;
+            const int bf = b / R;
+            const int j = bf & (half - 1);
+            const int base = ((bf >> stage) << (stage + 1)) + j;
+            Fr* pu = &s[base * R + r];
+            Fr* pv = &s[(base + half) * R + r];
+            Fr u = ld(pu), v = ld(pv);
+            if (j) v = mul(v, ld(&w[j << tw_shift]));
+            st(pu, add(u, v));
+            st(pv, sub(u, v));
+        }
+        __syncthreads();
+    }
+}
+
+struct PassArgs {
+    const uint8_t* in;
+    uint8_t* out;
+    int L, L1, L2, R;
+    const Fr* w_sub;     // roots of the sub-DFT (size 2^(m-1))
+    const Fr* tw_lo;     // pass A: w^e for e < n2 ; pass C: unused
+    const Fr* tw_hi;     // pass A: w^(n2*e) for e < n1
+    const Fr* pre_lo;    // pass A coset: g^i1 (n1) ; single: g^i (n)
+    const Fr* pre_hi;    // pass A coset: g^(n1*i2) (n2)
+    const Fr* post_lo;   // pass C: scale_k2 (n2), e.g. n^-1 g^-k2
+    const Fr* post_hi;   // pass C: g^(-n2*k1) (n1)
+    const Fr* scale;     // uniform output scale (n^-1) when post tables are absent
+};
+
+// Pass A: columns i1 in [cb*R, cb*R+R), DFT length n2 over i2.
+__global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
+    extern __shared__ uint4 smem_raw[];
+    Fr* s = reinterpret_cast<Fr*>(smem_raw);
+    const int n1 = 1 << a.L1, n2 = 1 << a.L2, R = a.R;
+    const int i1_0 = blockIdx.x * R;
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+        const int r = e % R, i2 = e / R;
+        const int i1 = i1_0 + r;
+        const uint64_t idx = i1 + (uint64_t)n1 * i2;
+        Fr x = load<FrCfg>(a.in + 32 * idx);
+        if (a.pre_lo) x = mul(x, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[i2])));
+        st(&s[bitrev(i2, a.L2) * R + r], x);
+    }
+    __syncthreads();
+    smem_dit(s, a.L2, R, a.w_sub);
+    for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
+        const int r = e % R, k2 = e / R;
+        const int i1 = i1_0 + r;
+        Fr x = ld(&s[k2 * R + r]);
+        // twiddle w^(i1*k2), exponent < n, split as lo (L2 bits) + hi
+        const uint64_t ex = (uint64_t)i1 * k2;
+        const uint32_t lo = ex & (n2 - 1), hi = ex >> a.L2;
+        if (ex) x = mul(x, mul(ld(&a.tw_lo[lo]), ld(&a.tw_hi[hi])));
+        store<FrCfg>(a.out + 32 * (i1 + (uint64_t)n1 * k2), x);
+    }
+}
+
+// Pass C: rows k2 in [rb*R, rb*R+R), DFT length n1 over i1; natural output.
+__global__ void __launch_bounds__(512) ntt_pass_c(PassArgs a) {
+    extern __shared__ uint4 smem_raw[];
+    Fr* s = reinterpret_cast<Fr*>(smem_raw);
+    const int n1 = 1 << a.L1, n2 = 1 << a.L2, R = a.R;
+    const int k2_0 = blockIdx.x * R;
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+        const int r = e % R, i1 = e / R;
+        const uint64_t idx = i1 + (uint64_t)n1 * (k2_0 + r);
+        st(&s[bitrev(i1, a.L1) * R + r], load<FrCfg>(a.in + 32 * idx));
+    }
+    __syncthreads();
+    smem_dit(s, a.L1, R, a.w_sub);
+    for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
+        const int r = e % R, k1 = e / R;
+        const int k2 = k2_0 + r;
+        Fr x = ld(&s[k1 * R + r]);
+        if (a.post_lo) x = mul(x, mul(ld(&a.post_lo[k2]), ld(&a.post_hi[k1])));
+        else if (a.scale) x = mul(x, ld(a.scale));
+        store<FrCfg>(a.out + 32 * (k2 + (uint64_t)n2 * k1), x);
+    }
+}
+
+// Whole transform in one CTA (n <= 2^12): pre table g^i (n), post table
+// scale*g^-k (n) or uniform scale.
+__global__ void __launch_bounds__(512) ntt_single(PassArgs a) {
+    extern __shared__ uint4 smem_raw[];
+    Fr* s = reinterpret_cast<Fr*>(smem_raw);
+    const int n = 1 << a.L;
+    const uint64_t off = (uint64_t)blockIdx.x * n;  // batch of independent transforms
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        Fr x = load<FrCfg>(a.in + 32 * (off + i));
+        if (a.pre_lo) x = mul(x, ld(&a.pre_lo[i]));
+        st(&s[a.L ? bitrev(i, a.L) : 0], x);
+    }
+    __syncthreads();
+    if (a.L) smem_dit(s, a.L, 1, a.w_sub);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        Fr x = ld(&s[k]);
+        if (a.post_lo) x = mul(x, ld(&a.post_lo[k]));
+        else if (a.scale) x = mul(x, ld(a.scale));
+        store<FrCfg>(a.out + 32 * (off + k), x);
+    }
+}
+
+// table[k] = base^(k * step) for k < n (each thread: square-and-multiply).
+__global__ void powers_kernel(const Fr* base, uint32_t step, uint32_t n, const Fr* scale,
+                              Fr* table) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    uint64_t e = (uint64_t)k * step;
+    Fr r = Fr::one(), b = *base;
+    while (e) {
+        if (e & 1) r = mul(r, b);
+        b = sqr(b);
+        e >>= 1;
+    }
+    if (scale) r = mul(r, *scale);
+    table[k] = r;
+}
+
+// Scalars: w = 5^((r-1)/2^L) (inverse: its inverse), g = 5, n^-1.
+__global__ void roots_kernel(int L, Fr* out /* [0]=w [1]=w^-1 [2]=g [3]=g^-1 [4]=n^-1 */) {
+    if (threadIdx.x || blockIdx.x) return;
+    // e = (r - 1) >> L
+    uint32_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = mod_limb<FrCfg>(i);
+    e[0] -= 1;
+    for (int s = 0; s < L; ++s) {
+        for (int i = 0; i < 8; ++i) e[i] = (e[i] >> 1) | (i < 7 ? (e[i + 1] << 31) : 0u);
+    }
+    Fr five = Fr::zero();
+    five.v[0] = 5;
+    five = to_mont(five);
+    Fr w = pow(five, e);
+    out[0] = w;
+    out[1] = inv(w);
+    out[2] = five;
+    out[3] = inv(five);
+    Fr n = Fr::zero();
+    if (L < 32) n.v[0] = 1u << L;
+    out[4] = inv(to_mont(n));
+}
+
+__global__ void convert_kernel(uint8_t* data, uint64_t n, int to) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Fr x = load<FrCfg>(data + 32 * i);
+    store<FrCfg>(data + 32 * i, to ? to_mont(x) : from_mont(x));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+int ntt_tables(NttTables& t, int L, cudaStream_t s) {
+    if (t.L == L && t.w_a) return 0;
+    t.release();
+    t.L = L;
+    const int L2 = (L + 1) / 2, L1 = L - L2;
+    t.L1 = L1;
+    t.L2 = L2;
+    const uint32_t n = 1u << L, n1 = 1u << L1, n2 = 1u << L2;
+    auto alloc = [&](Fr** p, size_t cnt) { return cudaMalloc(p, sizeof(Fr) * (cnt ? cnt : 1)); };
+    if (alloc(&t.consts, 8)) return -1;
+    roots_kernel<<<1, 1, 0, s>>>(L, t.consts);
+    Fr* w = t.consts + 0;
+    Fr* wi = t.consts + 1;
+    Fr* g = t.consts + 2;
+    Fr* gi = t.consts + 3;
+    Fr* ninv = t.consts + 4;
+    auto pw = [&](Fr** dst, const Fr* base, uint32_t step, uint32_t cnt, const Fr* scale) {
+        if (alloc(dst, cnt)) return -1;
+        powers_kernel<<<(cnt + 255) / 256, 256, 0, s>>>(base, step, cnt, scale, *dst);
+        return 0;
+    };
+    if (L <= kNttSingleMax) {
+        // single-CTA transform: sub-DFT roots of size n, coset tables of size n
+        if (pw(&t.w_a, w, 1, n / 2 ? n / 2 : 1, nullptr) || pw(&t.wi_a, wi, 1, n / 2 ? n / 2 : 1, nullptr) ||
+            pw(&t.g_lo, g, 1, n, nullptr) || pw(&t.gi_post_lo, gi, 1, n, ninv))
+            return -1;
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
+    // pass A: sub-DFT of size n2 -> root w^n1 ; pass C: size n1 -> root w^n2
+    if (pw(&t.w_a, w, n1, n2 / 2, nullptr) || pw(&t.wi_a, wi, n1, n2 / 2, nullptr) ||
+        pw(&t.w_c, w, n2, n1 / 2, nullptr) || pw(&t.wi_c, wi, n2, n1 / 2, nullptr) ||
+        pw(&t.tw_lo, w, 1, n2, nullptr) || pw(&t.tw_hi, w, n2, n1, nullptr) ||
+        pw(&t.twi_lo, wi, 1, n2, nullptr) || pw(&t.twi_hi, wi, n2, n1, nullptr) ||
+        pw(&t.g_lo, g, 1, n1, nullptr) || pw(&t.g_hi, g, n1, n2, nullptr) ||
+        pw(&t.gi_post_lo, gi, 1, n2, ninv) || pw(&t.gi_post_hi, gi, n2, n1, nullptr))
+        return -1;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+void NttTables::release() {
+    Fr** all[] = {&consts, &w_a, &wi_a, &w_c, &wi_c, &tw_lo, &tw_hi, &twi_lo, &twi_hi,
+                  &g_lo, &g_hi, &gi_post_lo, &gi_post_hi};
+    for (Fr** p : all) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    L = -1;
+}
+
+int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratch, int inverse,
+            int coset, int batch, cudaStream_t s) {
+    const int L = t.L;
+    PassArgs a{};
+    a.L = L;
+    a.L1 = t.L1;
+    a.L2 = t.L2;
+    a.scale = nullptr;
+    if (L <= kNttSingleMax) {
+        a.in = in;
+        a.out = out;
+        a.w_sub = inverse ? t.wi_a : t.w_a;
+        a.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
+        a.post_lo = (coset && inverse) ? t.gi_post_lo : nullptr;
+        if (inverse && !coset) a.scale = t.consts + 4;
+        const size_t smem = sizeof(Fr) << L;
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(ntt_single, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        ntt_single<<<batch, 512, smem, s>>>(a);
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
+    const int n1 = 1 << t.L1, n2 = 1 << t.L2;
+    // pass A: in -> scratch
+    a.in = in;
+    a.out = scratch;
+    a.R = kNttR;
+    a.w_sub = inverse ? t.wi_a : t.w_a;
+    a.tw_lo = inverse ? t.twi_lo : t.tw_lo;
+    a.tw_hi = inverse ? t.twi_hi : t.tw_hi;
+    a.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
+    a.pre_hi = (coset && !inverse) ? t.g_hi : nullptr;
+    size_t smem = sizeof(Fr) * (size_t)n2 * kNttR;
+    cudaFuncSetAttribute(ntt_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ntt_pass_a<<<n1 / kNttR, 512, smem, s>>>(a);
+    // pass C: scratch -> out
+    PassArgs c = a;
+    c.in = scratch;
+    c.out = out;
+    c.w_sub = inverse ? t.wi_c : t.w_c;
+    c.pre_lo = c.pre_hi = nullptr;
+    c.post_lo = (coset && inverse) ? t.gi_post_lo : nullptr;
+    c.post_hi = (coset && inverse) ? t.gi_post_hi : nullptr;
+ if (inverse && !coset) c.scale = t.consts + 4;
+    smem = sizeof(Fr) * (size_t)n1 * kNttR;
+    cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    ntt_pass_c<<<n2 / kNttR, 512, smem, s>>>(c);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+void launch_fr_convert(uint8_t* data, uint64_t n, int to_mont, cudaStream_t s) {
+    if (n) convert_kernel<<<(n + 255) / 256, 256, 0, s>>>(data, n, to_mont);
+}
+
+}  // namespace bn
+}  // namespace ace_gpu

@@ -1,0 +1,34 @@
+// Fr NTT launchers (ntt.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "bn254.cuh"
+
+namespace ace_gpu {
+namespace bn {
+
+constexpr int kNttSingleMax = 12;  // n <= 2^12: one CTA per transform
+constexpr int kNttMaxLog = 22;     // pass A tile = 2^11 x R x 32 B = 128 KB smem
+constexpr int kNttR = 2;           // adjacent columns / rows per CTA
+
+// Device tables for one size (Montgomery form).
+struct NttTables {
+    int L = -1, L1 = 0, L2 = 0;
+    Fr* consts = nullptr;  // w, w^-1, g, g^-1, n^-1
+    Fr *w_a = nullptr, *wi_a = nullptr, *w_c = nullptr, *wi_c = nullptr;
+    Fr *tw_lo = nullptr, *tw_hi = nullptr, *twi_lo = nullptr, *twi_hi = nullptr;
+    Fr *g_lo = nullptr, *g_hi = nullptr, *gi_post_lo = nullptr, *gi_post_hi = nullptr;
+    void release();
+};
+
+int ntt_tables(NttTables& t, int L, cudaStream_t s);
+// in/out may alias; scratch (n x 32 B) is needed when L > kNttSingleMax.
+// Data in Montgomery form. batch > 1 only for L <= kNttSingleMax.
+int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratch, int inverse,
+            int coset, int batch, cudaStream_t s);
+void launch_fr_convert(uint8_t* data, uint64_t n, int to_mont, cudaStream_t s);
+
+}  // namespace bn
+}  // namespace ace_gpu

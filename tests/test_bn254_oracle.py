@@ -1,0 +1,117 @@
+"""Pins the from-scratch BN254 oracle (oracle/bn254_oracle.c) with
+self-consistency known answers — the reference has no BN254 code, so parity
+for this part is UNPINNED by the reference. Constants per SURVEY
+Appendix C; field ops cross-checked with Python big integers."""
+import ctypes as C
+import random
+
+import pytest
+
+import oracle_lib as O
+
+P = 0x30644E72E131A029B85045B68181585D97816A916871CA8D3C208C16D87CFD47
+R = 0x30644E72E131A029B85045B68181585D2833E84879B9709143E1F593F0000001
+
+
+def le(x):
+    return x.to_bytes(32, "little")
+
+
+def to_int(b):
+    return int.from_bytes(bytes(b), "little")
+
+
+@pytest.mark.parametrize("field,m", [(0, P), (1, R)])
+def test_field_ops_vs_python(field, m):
+    L = O.oracle()
+    rng = random.Random(field)
+    for _ in range(300):
+        a, b = rng.randrange(m), rng.randrange(m)
+        o = O.buf(32)
+        L.bn_mul(field, O.ptr(le(a)), O.ptr(le(b)), o)
+        assert to_int(o) == a * b % m
+        L.bn_add(field, O.ptr(le(a)), O.ptr(le(b)), o)
+        assert to_int(o) == (a + b) % m
+        L.bn_sub(field, O.ptr(le(a)), O.ptr(le(b)), o)
+        assert to_int(o) == (a - b) % m
+        if a:
+            L.bn_inv(field, O.ptr(le(a)), o)
+            assert to_int(o) * a % m == 1
+
+
+def test_curve_constants():
+    L = O.oracle()
+    for g in (1, 2):
+        G = O.buf(64 * g)
+        L.bn_generator(g, G)
+        assert L.bn_on_curve(g, G) == 1
+        out = O.buf(64 * g)
+        L.bn_scalar_mul(g, G, O.ptr(le(R)), out)
+        assert not any(bytes(out)), "r * G must be the point at infinity"
+        L.bn_scalar_mul(g, G, O.ptr(le(R + 5)), out)
+        five = O.buf(64 * g)
+        L.bn_scalar_mul(g, G, O.ptr(le(5)), five)
+        assert bytes(out) == bytes(five)
+    G1 = O.buf(64)
+    L.bn_generator(1, G1)
+    assert to_int(bytes(G1)[:32]) == 1 and to_int(bytes(G1)[32:]) == 2
+
+
+def test_group_law():
+    L = O.oracle()
+    rng = random.Random(3)
+    for g in (1, 2):
+        G = O.buf(64 * g)
+        L.bn_generator(g, G)
+        for _ in range(10):
+            a, b = rng.randrange(R), rng.randrange(R)
+            A, B, AB, S = (O.buf(64 * g) for _ in range(4))
+            L.bn_scalar_mul(g, G, O.ptr(le(a)), A)
+            L.bn_scalar_mul(g, G, O.ptr(le(b)), B)
+            L.bn_point_add(g, A, B, AB)
+            L.bn_scalar_mul(g, G, O.ptr(le((a + b) % R)), S)
+            assert bytes(AB) == bytes(S) and L.bn_on_curve(g, AB) == 1
+            N_ = O.buf(64 * g)
+            L.bn_point_neg(g, A, N_)
+            Z = O.buf(64 * g)
+            L.bn_point_add(g, A, N_, Z)
+            assert not any(bytes(Z))
+
+
+def test_root_of_unity_constants():
+    """w_28 = 5^((r-1)/2^28); NTT vs naive DFT."""
+    assert pow(5, (R - 1) >> 28, R) == 0x2A3C09F0A58A7E8500E0A7EB8EF62ABC402D111E41112ED49BD61B6E725B19F0
+    L = O.oracle()
+    for logn in range(0, 7):
+        n = 1 << logn
+        vals = [random.randrange(R) for _ in range(n)]
+        raw = b"".join(le(v) for v in vals)
+        buf = (C.c_uint8 * (32 * n)).from_buffer_copy(raw)
+        L.bn_ntt(buf, logn, 0, 0, 1)
+        ref = O.buf(32 * n)
+        L.bn_dft_naive(O.ptr(raw), logn, 0, ref)
+        assert bytes(buf) == bytes(ref)
+        # Python restatement of the DFT
+        w = pow(5, (R - 1) >> logn, R)
+        py = [sum(v * pow(w, i * j, R) for j, v in enumerate(vals)) % R for i in range(n)]
+        assert [to_int(bytes(buf)[32 * i:32 * i + 32]) for i in range(n)] == py
+        L.bn_ntt(buf, logn, 1, 0, 1)
+        assert bytes(buf) == raw
+
+
+def test_msm_oracle_vs_discrete_log():
+    L = O.oracle()
+    G = O.buf(64)
+    L.bn_generator(1, G)
+    rng = random.Random(9)
+    n = 64
+    ks = [rng.randrange(R) for _ in range(n)]
+    ss = [rng.randrange(R) for _ in range(n)]
+    pts = O.buf(64 * n)
+    L.bn_fixed_base_muls(1, G, O.ptr(b"".join(le(k) for k in ks)), C.c_uint64(n), pts, 4)
+    out = O.buf(64)
+    L.bn_msm(1, pts, O.ptr(b"".join(le(s) for s in ss)), C.c_uint64(n), out, 4)
+    e = sum(a * b for a, b in zip(ss, ks)) % R
+    ref = O.buf(64)
+    L.bn_scalar_mul(1, G, O.ptr(le(e)), ref)
+    assert bytes(out) == bytes(ref)

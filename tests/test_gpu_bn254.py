@@ -1,0 +1,220 @@
+"""BN254 field / NTT / curve / MSM kernels vs the from-scratch CPU oracle
+(oracle/bn254_oracle.c — parity unpinned by the reference, which has no BN254
+code; the oracle itself is pinned by tests/test_bn254_oracle.py)."""
+import ctypes as C
+import random
+
+import numpy as np
+import pytest
+
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+P = 0x30644E72E131A029B85045B68181585D97816A916871CA8D3C208C16D87CFD47
+R = 0x30644E72E131A029B85045B68181585D2833E84879B9709143E1F593F0000001
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2603_10242_b200 import _native as N
+    return N.context(0)
+
+
+def le(x):
+    return x.to_bytes(32, "little")
+
+
+def arr(vals):
+    return np.frombuffer(b"".join(le(v) for v in vals), np.uint8).copy()
+
+
+def ints(a):
+    b = a.tobytes()
+    return [int.from_bytes(b[32 * i:32 * i + 32], "little") for i in range(len(b) // 32)]
+
+
+def edge(m):
+    return [0, 1, 2, m - 1, m - 2, (m - 1) // 2, (m + 1) // 2, 1 << 253, (1 << 254) % m,
+            0xFFFFFFFF, 1 << 32, (1 << 128) - 1]
+
+
+@pytest.mark.parametrize("field,m", [(0, P), (1, R)])
+def test_field_ops_match_python_and_oracle(ctx, field, m):
+    rng = random.Random(field + 10)
+    a = edge(m) + [rng.randrange(m) for _ in range(4000)]
+    b = list(reversed(edge(m))) + [rng.randrange(m) for _ in range(4000)]
+    A, B = arr(a), arr(b)
+    n = len(a)
+    for op, f in [(0, lambda x, y: x * y % m), (1, lambda x, y: (x + y) % m),
+                  (2, lambda x, y: (x - y) % m), (3, lambda x, y: x * x % m),
+                  (4, lambda x, y: pow(x, m - 2, m))]:
+        out = np.zeros(32 * n, np.uint8)
+        ctx.call("acegpu_bn_field_batch", field, op, A, B, n, out)
+        got = ints(out)
+        assert got == [f(x, y) for x, y in zip(a, b)], f"op {op}"
+    # oracle agreement (the oracle is the checker of record)
+    out = np.zeros(32 * n, np.uint8)
+    ctx.call("acegpu_bn_field_batch", field, 0, A, B, n, out)
+    ref = O.buf(32 * n)
+    O.oracle().bn_batch(C.c_int(field), C.c_int(0), O.ptr(A), O.ptr(B), C.c_uint64(n), ref)
+    assert out.tobytes() == bytes(ref)
+
+
+def oracle_ntt(vals, logn, inverse, coset):
+    buf = (C.c_uint8 * (32 << logn)).from_buffer_copy(b"".join(le(v) for v in vals))
+    O.oracle().bn_ntt(buf, C.c_uint32(logn), C.c_int(inverse), C.c_int(coset), C.c_int(8))
+    return ints(np.frombuffer(bytes(buf), np.uint8))
+
+
+@pytest.mark.parametrize("logn", [0, 1, 2, 3, 5, 8, 11, 12, 13, 14, 16, 17])
+def test_ntt_matches_oracle(ctx, logn):
+    rng = random.Random(logn)
+    vals = [rng.randrange(R) for _ in range(1 << logn)]
+    for inverse in (0, 1):
+        for coset in (0, 1):
+            data = arr(vals)
+            ctx.call("acegpu_bn_ntt", data, logn, inverse, coset)
+            assert ints(data) == oracle_ntt(vals, logn, inverse, coset), (inverse, coset)
+
+
+def test_ntt_small_vs_naive_dft(ctx):
+    for logn in range(0, 8):
+        vals = [random.randrange(R) for _ in range(1 << logn)]
+        data = arr(vals)
+        ctx.call("acegpu_bn_ntt", data, logn, 0, 0)
+        ref = O.buf(32 << logn)
+        O.oracle().bn_dft_naive(O.ptr(arr(vals)), C.c_uint32(logn), C.c_int(0), ref)
+        assert data.tobytes() == bytes(ref)
+
+
+@pytest.mark.parametrize("logn", [20, 22])
+def test_ntt_large_roundtrip_and_oracle(ctx, logn):
+    """2^22 (BASELINE configs[1]) and 2^20: iNTT(NTT(x)) = x, coset round trip,
+    linearity, and (2^20) bit-exact vs the oracle."""
+    rng = np.random.default_rng(logn)
+    n = 1 << logn
+    raw = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64)
+    raw[:, 3] &= (1 << 61) - 1  # < 2^253 < r: canonical
+    data = raw.view(np.uint8).reshape(-1).copy()
+    orig = data.copy()
+    ctx.call("acegpu_bn_ntt", data, logn, 0, 0)
+    fwd = data.copy()
+    assert not np.array_equal(fwd, orig)
+    ctx.call("acegpu_bn_ntt", data, logn, 1, 0)
+    assert np.array_equal(data, orig)
+    ctx.call("acegpu_bn_ntt", data, logn, 0, 1)
+    ctx.call("acegpu_bn_ntt", data, logn, 1, 1)
+    assert np.array_equal(data, orig)
+    if logn == 20:
+        buf = (C.c_uint8 * (32 * n)).from_buffer(orig)
+        O.oracle().bn_ntt(buf, C.c_uint32(logn), C.c_int(0), C.c_int(0), C.c_int(8))
+        assert np.array_equal(orig, fwd)
+
+
+def g_gen(group):
+    g = O.buf(64 * group)
+    O.oracle().bn_generator(C.c_int(group), g)
+    return bytes(g)
+
+
+@pytest.mark.parametrize("group", [1, 2])
+def test_scalar_muls_match_oracle(ctx, group):
+    rng = random.Random(group)
+    ks = [0, 1, 2, 3, R - 1, R - 2] + [rng.randrange(R) for _ in range(200)]
+    G = np.frombuffer(g_gen(group), np.uint8).copy()
+    out = np.zeros(64 * group * len(ks), np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", group, G, arr(ks), len(ks), out)
+    for i, k in enumerate(ks):
+        ref = O.buf(64 * group)
+        O.oracle().bn_scalar_mul(C.c_int(group), O.ptr(bytes(G)), O.ptr(le(k)), ref)
+        assert out[64 * group * i:64 * group * (i + 1)].tobytes() == bytes(ref), (i, k)
+
+
+def msm_gpu(ctx, group, pts, scalars, n):
+    from paper_2603_10242_b200 import _native as N
+    h = C.c_void_p()
+    ctx.call("acegpu_bn_msm_prepare", group, pts, n, 0, C.byref(h))
+    try:
+        out = np.zeros(64 * group, np.uint8)
+        ctx.call("acegpu_bn_msm_run", h, scalars, out)
+        return out.tobytes()
+    finally:
+        N.lib().acegpu_bn_msm_free(h)
+
+
+@pytest.mark.parametrize("group,n", [(1, 1), (1, 2), (1, 700), (1, 5000), (2, 300)])
+def test_msm_matches_oracle(ctx, group, n):
+    rng = random.Random(1000 * group + n)
+    ks = [rng.randrange(1, R) for _ in range(n)]
+    G = np.frombuffer(g_gen(group), np.uint8).copy()
+    pts = np.zeros(64 * group * n, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", group, G, arr(ks), n, pts)
+    sc = [rng.randrange(R) for _ in range(n)]
+    special = [0, 1, R - 1, 2, R - 2, 1 << 253]
+    for j, v in enumerate(special[:n]):
+        sc[j] = v
+    got = msm_gpu(ctx, group, pts, arr(sc), n)
+    ref = O.buf(64 * group)
+    O.oracle().bn_msm(C.c_int(group), O.ptr(pts.tobytes()), O.ptr(arr(sc).tobytes()),
+                      C.c_uint64(n), ref, C.c_int(8))
+    assert got == bytes(ref)
+    # discrete-log cross-check: sum s_i k_i mod r times G
+    e = sum(s * k for s, k in zip(sc, ks)) % R
+    dl = O.buf(64 * group)
+    O.oracle().bn_scalar_mul(C.c_int(group), O.ptr(bytes(G)), O.ptr(le(e)), dl)
+    assert got == bytes(dl)
+
+
+def test_msm_degenerate_scalars(ctx):
+    """Skewed digit distributions: all-equal scalars (one huge bucket), all
+    zero, repeated bases, an infinity base."""
+    n = 20000
+    G = np.frombuffer(g_gen(1), np.uint8).copy()
+    ks = [(i % 7) + 1 for i in range(n)]
+    pts = np.zeros(64 * n, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", 1, G, arr(ks), n, pts)
+    pts[64 * 5:64 * 6] = 0  # infinity base
+    for sc, label in [([1] * n, "ones"), ([0] * n, "zeros"), ([R - 1] * n, "minus ones"),
+                      ([(1 << 16) + 3] * n, "two windows")]:
+        got = msm_gpu(ctx, 1, pts, arr(sc), n)
+        e = sum(s * (k if i != 5 else 0) for i, (s, k) in enumerate(zip(sc, ks))) % R
+        dl = O.buf(64)
+        O.oracle().bn_scalar_mul(C.c_int(1), O.ptr(bytes(G)), O.ptr(le(e)), dl)
+        assert got == bytes(dl), label
+
+
+def test_msm_2_20_discrete_log(ctx):
+    """BASELINE configs[1]: G1 MSM of 2^20 points, checked exactly through
+    known discrete logs (bases k_i * G)."""
+    n = 1 << 20
+    rng = np.random.default_rng(20)
+    kraw = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64)
+    kraw[:, 3] &= (1 << 61) - 1
+    sraw = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64)
+    sraw[:, 3] &= (1 << 61) - 1
+    K = kraw.view(np.uint8).reshape(-1).copy()
+    S = sraw.view(np.uint8).reshape(-1).copy()
+    G = np.frombuffer(g_gen(1), np.uint8).copy()
+    pts = np.zeros(64 * n, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", 1, G, K, n, pts)
+    for i in (0, 1, n // 2, n - 1):  # spot-check the generated bases
+        ref = O.buf(64)
+        O.oracle().bn_scalar_mul(C.c_int(1), O.ptr(bytes(G)), O.ptr(K[32 * i:32 * i + 32].tobytes()), ref)
+        assert pts[64 * i:64 * i + 64].tobytes() == bytes(ref)
+    got = msm_gpu(ctx, 1, pts, S, n)
+    ki = [int.from_bytes(K[32 * i:32 * i + 32].tobytes(), "little") for i in range(n)]
+    si = [int.from_bytes(S[32 * i:32 * i + 32].tobytes(), "little") for i in range(n)]
+    e = sum(a * b for a, b in zip(si, ki)) % R
+    dl = O.buf(64)
+    O.oracle().bn_scalar_mul(C.c_int(1), O.ptr(bytes(G)), O.ptr(le(e)), dl)
+    assert got == bytes(dl)
+
+
+def test_integer_peaks_positive(ctx):
+    v = C.c_double()
+    ctx.call("acegpu_imad_peak", C.byref(v))
+    assert v.value > 1e12
+    for f in (0, 1):
+        ctx.call("acegpu_bn_mul_rate", f, C.byref(v))
+        assert v.value > 1e9
