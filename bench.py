@@ -309,6 +309,11 @@ def run_ours(args, rank: int, world: int) -> None:
     lat = C.c_double()
     ctx.call("acegpu_sha256_probe", 1, 32, 512, C.byref(lat))
     lat_us = lat.value / 512 * 1e6  # one warp's chained compression latency
+    bn = None
+    if world == 1 and not args.no_bn254:
+        bn = bench_bn254(ctx, dev)
+        if not args.no_cpu_baseline:
+            bn["cpu_oracle"] = bn254_cpu_baseline()
 
     if rank != 0:
         return
@@ -341,7 +346,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "e2e": {"value": n / (e2e_ms / 1e3), "unit": "tx/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "clocks": cl, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-        "parity": parity, "impl": "ours",
+        "parity": parity, "impl": "ours", "bn254": bn,
     }
     print(json.dumps(line), flush=True)
 
@@ -412,6 +417,105 @@ def run_e2e(args, ctx, fb, revs, rev_index, rank, world, start, count, be, dev):
     return ms, h2d, d2h
 
 
+def bench_bn254(ctx, dev: int, reps: int = 5) -> dict:
+    """BASELINE configs[1]: Fr NTT/iNTT 2^22 and G1 MSM 2^20 (device-resident,
+    CUDA events on the launching stream), with the integer-pipe roofline."""
+    import torch
+    from paper_2603_10242_b200 import bn254
+    out: dict = {}
+    imad = bn254.imad_peak(ctx)
+    fq_rate, fr_rate = bn254.mul_rate(0, ctx), bn254.mul_rate(1, ctx)
+    out["peaks"] = {"imad_per_s": imad, "fq_mul_per_s": fq_rate, "fr_mul_per_s": fr_rate,
+                    "imad_per_fq_mul_implied": imad / fq_rate,
+                    "source": "acegpu_imad_peak / acegpu_bn_mul_rate microkernels, same run"}
+    s = torch.cuda.current_stream()
+    sp = s.cuda_stream
+
+    def timed(fn, k=reps):
+        fn()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k)]
+        for a, b in evs:
+            a.record(s)
+            fn()
+            b.record(s)
+        torch.cuda.synchronize()
+        return statistics.median(x.elapsed_time(y) for x, y in evs)
+
+    # ---- NTT 2^22
+    L = 22
+    n = 1 << L
+    x = torch.from_numpy(bn254.random_scalars(n, 22)).to(f"cuda:{dev}")
+    ctx.call("acegpu_bn_convert_dev", sp, 1, x.data_ptr(), n, 1)
+    y = torch.empty_like(x)
+    f_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, x.data_ptr(), y.data_ptr(), L, 0, 0))
+    i_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, y.data_ptr(), y.data_ptr(), L, 1, 0))
+    c_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, x.data_ptr(), y.data_ptr(), L, 0, 1))
+    muls = (n // 2) * L + 2 * n  # butterflies + pass-A twiddles
+    bytes_moved = 2 * 2 * n * 32  # two passes, read + write
+    out["ntt_2^22"] = {
+        "forward_ms": f_ms, "inverse_ms": i_ms, "coset_forward_ms": c_ms,
+        "fr_muls": muls, "achieved_fr_mul_per_s": muls / (f_ms * 1e-3),
+        "frac_of_fr_mul_peak": muls / (f_ms * 1e-3) / fr_rate,
+        "hbm_gbs": bytes_moved / (f_ms * 1e-3) / 1e9,
+        "bound": "imad (Fr CIOS multiplications)"}
+    del x, y
+    # ---- G1 MSM 2^20 (bases k_i*G generated on the GPU, prepared once)
+    n = 1 << 20
+    ks = bn254.random_scalars(n, 1)
+    pts = bn254.scalar_muls(1, bn254.generator(1), ks, ctx)
+    t0 = time.perf_counter()
+    bases = bn254.MsmBases(1, pts, n, ctx=ctx)
+    setup_ms = (time.perf_counter() - t0) * 1e3
+    sc = torch.from_numpy(bn254.random_scalars(n, 2)).to(f"cuda:{dev}")
+    res = torch.zeros(64, dtype=torch.uint8, device=f"cuda:{dev}")
+    m_ms = timed(lambda: bases.run_dev(sc.data_ptr(), res.data_ptr(), sp), k=3)
+    entries = 16 * n  # nonzero signed digits (uniform scalars)
+    fq_muls = entries * 10  # mixed XYZZ add = 8M + 2S
+    out["msm_g1_2^20"] = {
+        "ms": m_ms, "setup_ms_once_per_base_set": setup_ms, "window_bits": 16,
+        "fq_muls_accumulate": fq_muls,
+        "achieved_fq_mul_per_s": fq_muls / (m_ms * 1e-3),
+        "frac_of_fq_mul_peak": fq_muls / (m_ms * 1e-3) / fq_rate,
+        "achieved_imad_per_s": fq_muls * 264 / (m_ms * 1e-3),
+        "frac_of_imad_peak": fq_muls * 264 / (m_ms * 1e-3) / imad,
+        "bound": "imad (Fq CIOS multiplications, 264 IMAD each)"}
+    bases.close()
+    return out
+
+
+def bn254_cpu_baseline(dev_unused=None) -> dict | None:
+    """Framework CPU oracle (NOT the reference: it has no BN254 code) on a
+    bounded sample: NTT 2^20 and G1 MSM 2^14, all host threads."""
+    so = os.path.join(ROOT, "oracle", "liboracle.so")
+    if not os.path.exists(so):
+        return None
+    L = C.CDLL(so)
+    thr = os.cpu_count() or 1
+    from paper_2603_10242_b200 import bn254
+    logn = 20
+    data = bn254.random_scalars(1 << logn, 5)
+    t0 = time.perf_counter()
+    L.bn_ntt(data.ctypes.data_as(C.c_void_p), C.c_uint32(logn), 0, 0, thr)
+    ntt_ms = (time.perf_counter() - t0) * 1e3
+    n = 1 << 14
+    ks = bn254.random_scalars(n, 6)
+    g = bn254.generator(1)
+    pts = np.zeros(64 * n, np.uint8)
+    L.bn_fixed_base_muls(1, g.ctypes.data_as(C.c_void_p), ks.ctypes.data_as(C.c_void_p),
+                         C.c_uint64(n), pts.ctypes.data_as(C.c_void_p), thr)
+    sc = bn254.random_scalars(n, 7)
+    res = np.zeros(64, np.uint8)
+    t0 = time.perf_counter()
+    L.bn_msm(1, pts.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p), C.c_uint64(n),
+             res.ctypes.data_as(C.c_void_p), thr)
+    msm_ms = (time.perf_counter() - t0) * 1e3
+    return {"kind": "framework CPU oracle, not reference", "cores": thr,
+            "ntt_2^20_ms": ntt_ms, "msm_g1_2^14_ms": msm_ms,
+            "sample": "one NTT 2^20 + one G1 MSM 2^14 (window-8 buckets)"}
+
+
 def cpu_baseline(args, n: int) -> dict | None:
     """The reference's CPU path (oracle/_ref) on this host, bounded sample."""
     so = os.path.join(ROOT, "oracle", "_ref", "libaceref.so")
@@ -439,6 +543,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-tx", type=int, default=N_TX)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bn254", action="store_true", help="skip the NTT/MSM microbenchmarks")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))

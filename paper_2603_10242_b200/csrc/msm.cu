@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(const uint8_t* table,
         }
         const uint32_t v = sorted[pos];
         F x, y;
-        load_affine<F>(table + (uint64_t)A * (v & 0x7FFFFFFFu), x, y);
+        if (!load_affine<F>(table + (uint64_t)A * (v & 0x7FFFFFFFu), x, y)) continue;  // infinity
         if (v >> 31) y = fneg(y);
         acc = xyzz_madd(acc, x, y);
     }
