@@ -14,8 +14,13 @@ struct Fq2 {
 };
 
 // ---- uniform field interface (Fq and Fq2) ---------------------------------
-__device__ __forceinline__ Fq fmul(const Fq& a, const Fq& b) { return mul(a, b); }
-__device__ __forceinline__ Fq fsqr(const Fq& a) { return mul(a, a); }
+// The Fq multiplication is ~530 SASS instructions; curve formulas call it a
+// dozen times per point operation, so it is an out-of-line call here
+// (inlined, a bucket kernel's body exceeded 1 MB of code and thrashed the
+// instruction caches; see profiles/). NTT kernels keep the inline `mul`.
+static __device__ __noinline__ Fq fq_mul_call(const Fq a, const Fq b) { return mul(a, b); }
+__device__ __forceinline__ Fq fmul(const Fq& a, const Fq& b) { return fq_mul_call(a, b); }
+__device__ __forceinline__ Fq fsqr(const Fq& a) { return fq_mul_call(a, a); }
 __device__ __forceinline__ Fq fadd(const Fq& a, const Fq& b) { return add(a, b); }
 __device__ __forceinline__ Fq fsub(const Fq& a, const Fq& b) { return sub(a, b); }
 __device__ __forceinline__ bool fzero(const Fq& a) { return a.is_zero(); }
@@ -24,14 +29,14 @@ __device__ __forceinline__ void fset_zero(Fq& a) { a = Fq::zero(); }
 __device__ __forceinline__ bool feq(const Fq& a, const Fq& b) { return a == b; }
 
 __device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
-    Fq t0 = mul(a.c0, b.c0), t1 = mul(a.c1, b.c1);
-    Fq t2 = mul(add(a.c0, a.c1), add(b.c0, b.c1));
+    Fq t0 = fq_mul_call(a.c0, b.c0), t1 = fq_mul_call(a.c1, b.c1);
+    Fq t2 = fq_mul_call(add(a.c0, a.c1), add(b.c0, b.c1));
     return {sub(t0, t1), sub(sub(t2, t0), t1)};
 }
 __device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
     // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u
-    Fq t = mul(a.c0, a.c1);
-    return {mul(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
+    Fq t = fq_mul_call(a.c0, a.c1);
+    return {fq_mul_call(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
 }
 __device__ __forceinline__ Fq2 fadd(const Fq2& a, const Fq2& b) {
     return {add(a.c0, b.c0), add(a.c1, b.c1)};

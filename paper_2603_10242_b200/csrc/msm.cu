@@ -27,11 +27,11 @@ namespace bn {
 
 namespace {
 
-__device__ __forceinline__ Fq finv(const Fq& a) { return inv(a); }
+__device__ __forceinline__ Fq finv(const Fq& a) { return inv_fast(a); }
 __device__ __forceinline__ Fq2 finv(const Fq2& a) {
-    Fq n = add(mul(a.c0, a.c0), mul(a.c1, a.c1));
-    Fq ni = inv(n);
-    return {mul(a.c0, ni), neg(mul(a.c1, ni))};
+    Fq n = add(fmul(a.c0, a.c0), fmul(a.c1, a.c1));
+    Fq ni = inv_fast(n);
+    return {fmul(a.c0, ni), neg(fmul(a.c1, ni))};
 }
 __device__ __forceinline__ Fq fneg(const Fq& a) { return neg(a); }
 __device__ __forceinline__ Fq2 fneg(const Fq2& a) { return {neg(a.c0), neg(a.c1)}; }
@@ -140,33 +140,45 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
         if (d[w]) atomicAdd(&hist[abs(d[w]) - 1], 1u);
 }
 
-// Exclusive scan of kMsmBuckets counts in one CTA of 1024 threads.
+// Exclusive scans (one CTA of 1024 threads) of the bucket sizes -> entry
+// offsets, and of the per-bucket chunk counts ceil(size / kMsmSeg) -> chunk
+// offsets. Chunks never straddle buckets.
 __global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* hist, uint32_t* offs,
-                                                    uint32_t* cursor) {
-    __shared__ uint32_t part[1024];
+                                                    uint32_t* cursor, uint32_t* coffs) {
+    __shared__ uint32_t part[1024], cpart[1024];
     constexpr int per = kMsmBuckets / 1024;
     const int t = threadIdx.x;
-    uint32_t loc[per], sum = 0;
+    uint32_t loc[per], cloc[per], sum = 0, csum = 0;
 #pragma unroll
     for (int k = 0; k < per; ++k) {
+        const uint32_t h = hist[t * per + k];
         loc[k] = sum;
-        sum += hist[t * per + k];
+        cloc[k] = csum;
+        sum += h;
+        csum += (h + kMsmSeg - 1) / kMsmSeg;
     }
     part[t] = sum;
+    cpart[t] = csum;
     __syncthreads();
     for (int off = 1; off < 1024; off <<= 1) {
         uint32_t v = t >= off ? part[t - off] : 0;
+        uint32_t cv = t >= off ? cpart[t - off] : 0;
         __syncthreads();
         part[t] += v;
+        cpart[t] += cv;
         __syncthreads();
     }
-    const uint32_t base = t ? part[t - 1] : 0;
+    const uint32_t base = t ? part[t - 1] : 0, cbase = t ? cpart[t - 1] : 0;
 #pragma unroll
     for (int k = 0; k < per; ++k) {
         offs[t * per + k] = base + loc[k];
         cursor[t * per + k] = base + loc[k];
+        coffs[t * per + k] = cbase + cloc[k];
     }
-    if (t == 1023) offs[kMsmBuckets] = part[1023];
+    if (t == 1023) {
+        offs[kMsmBuckets] = part[1023];
+        coffs[kMsmBuckets] = cpart[1023];
+    }
 }
 
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
@@ -193,41 +205,46 @@ __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
     return lo;
 }
 
+// One thread per chunk (<= kMsmSeg entries of one bucket): mixed-add the
+// chunk's bases into one XYZZ partial.
 template <class F>
 __global__ void __launch_bounds__(128) accumulate_kernel(const uint8_t* table,
                                                          const uint32_t* sorted,
-                                                         const uint32_t* offs, uint8_t* buckets,
+                                                         const uint32_t* offs,
+                                                         const uint32_t* coffs,
                                                          uint8_t* partials) {
-    const uint32_t E = offs[kMsmBuckets];
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t p0 = t * kMsmSeg;
-    if (p0 >= E) return;
-    const uint32_t p1 = min(E, p0 + kMsmSeg);
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= coffs[kMsmBuckets]) return;
     constexpr int A = Lay<F>::AFF, X = Lay<F>::XZ;
-    int b = bucket_of(offs, p0);
-    uint32_t bstart = offs[b], bend = offs[b + 1];
+    const int b = bucket_of(coffs, c);
+    const uint32_t p0 = offs[b] + (c - coffs[b]) * kMsmSeg;
+    const uint32_t p1 = min(offs[b + 1], p0 + kMsmSeg);
     XYZZ<F> acc = XYZZ<F>::inf();
-    auto flush = [&]() {
-        const uint32_t s0 = bstart / kMsmSeg, s1 = (bend - 1) / kMsmSeg;
-        if (s0 == s1) store_xyzz(buckets + (uint64_t)X * b, acc);
-        else if (t == s0) store_xyzz(partials + (uint64_t)X * (2 * t + 1), acc);
-        else store_xyzz(partials + (uint64_t)X * (2 * t), acc);
-    };
+    uint32_t v = sorted[p0];
     for (uint32_t pos = p0; pos < p1; ++pos) {
-        while (pos >= bend) {
-            flush();
-            ++b;
-            bstart = offs[b];
-            bend = offs[b + 1];
-            acc = XYZZ<F>::inf();
-        }
-        const uint32_t v = sorted[pos];
+        const uint32_t nv = pos + 1 < p1 ? sorted[pos + 1] : 0u;  // prefetch the next index
         F x, y;
-        if (!load_affine<F>(table + (uint64_t)A * (v & 0x7FFFFFFFu), x, y)) continue;  // infinity
-        if (v >> 31) y = fneg(y);
-        acc = xyzz_madd(acc, x, y);
+        if (load_affine<F>(table + (uint64_t)A * (v & 0x7FFFFFFFu), x, y)) {  // skip infinity
+            if (v >> 31) y = fneg(y);
+            acc = xyzz_madd(acc, x, y);
+        }
+        v = nv;
     }
-    flush();
+    store_xyzz(partials + (uint64_t)X * c, acc);
+}
+
+// One thread per bucket: sum its chunk partials (infinity when empty).
+template <class F>
+__global__ void __launch_bounds__(128) bucket_sum_kernel(const uint32_t* coffs,
+                                                         const uint8_t* partials,
+                                                         uint8_t* buckets) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kMsmBuckets) return;
+    constexpr int X = Lay<F>::XZ;
+    XYZZ<F> acc = XYZZ<F>::inf();
+    for (uint32_t c = coffs[b]; c < coffs[b + 1]; ++c)
+        acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * c));
+    store_xyzz(buckets + (uint64_t)X * b, acc);
 }
 
 template <class F>
@@ -239,34 +256,6 @@ __device__ __forceinline__ XYZZ<F> shfl_xyzz(const XYZZ<F>& a, int src_lane_delt
     for (int k = 0; k < (int)(sizeof(XYZZ<F>) / 4); ++k)
         out[k] = __shfl_down_sync(0xffffffffu, in[k], src_lane_delta);
     return r;
-}
-
-// One warp per bucket: empty -> infinity; split -> sum of its partials.
-template <class F>
-__global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const uint8_t* partials,
-                                                    uint8_t* buckets) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= kMsmBuckets) return;
-    constexpr int X = Lay<F>::XZ;
-    const uint32_t bstart = offs[warp], bend = offs[warp + 1];
-    if (bstart == bend) {
-        if (lane == 0) store_xyzz(buckets + (uint64_t)X * warp, XYZZ<F>::inf());
-        return;
-    }
-    const uint32_t s0 = bstart / kMsmSeg, s1 = (bend - 1) / kMsmSeg;
-    if (s0 == s1) return;  // written directly by accumulate_kernel
-    XYZZ<F> acc = XYZZ<F>::inf();
-    for (uint32_t t = s0 + lane; t <= s1; t += 32) {
-        const uint32_t slot = t == s0 ? 2 * t + 1 : 2 * t;
-        acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * slot));
-    }
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        XYZZ<F> o = shfl_xyzz(acc, d);
-        if (lane < d) acc = xyzz_add(acc, o);
-    }
-    if (lane == 0) store_xyzz(buckets + (uint64_t)X * warp, acc);
 }
 
 constexpr int kRedSeg = 8;                           // buckets per reducing thread
@@ -334,10 +323,11 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
     const uint64_t cap = (uint64_t)kMsmWindows * n;
     if (sc.cap_entries < cap || !sc.hist) {
         sc.release();
-        const uint64_t segs = (cap + kMsmSeg - 1) / kMsmSeg;
+        const uint64_t chunks = (cap + kMsmSeg - 1) / kMsmSeg + kMsmBuckets;
         if (cudaMalloc(&sc.hist, 4 * (kMsmBuckets + 1)) || cudaMalloc(&sc.offs, 4 * (kMsmBuckets + 1)) ||
+            cudaMalloc(&sc.coffs, 4 * (kMsmBuckets + 1)) ||
             cudaMalloc(&sc.cursor, 4 * kMsmBuckets) || cudaMalloc(&sc.sorted, 4 * cap) ||
-            cudaMalloc(&sc.partials, (size_t)256 * 2 * segs) ||
+            cudaMalloc(&sc.partials, (size_t)256 * chunks) ||
             cudaMalloc(&sc.buckets, (size_t)256 * kMsmBuckets) ||
             cudaMalloc(&sc.segsum, (size_t)256 * kRedThreads))
             return -1;
@@ -346,12 +336,12 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
     cudaMemsetAsync(sc.hist, 0, 4 * (kMsmBuckets + 1), s);
     const unsigned gb = (unsigned)((n + 255) / 256);
     count_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.hist);
-    scan_kernel<<<1, 1024, 0, s>>>(sc.hist, sc.offs, sc.cursor);
+    scan_kernel<<<1, 1024, 0, s>>>(sc.hist, sc.offs, sc.cursor, sc.coffs);
     scatter_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
-    const uint64_t segs = (cap + kMsmSeg - 1) / kMsmSeg;
-    accumulate_kernel<F><<<(unsigned)((segs + 127) / 128), 128, 0, s>>>(table, sc.sorted, sc.offs,
-                                                                         sc.buckets, sc.partials);
-    fixup_kernel<F><<<kMsmBuckets * 32 / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets);
+    const uint64_t chunks = (cap + kMsmSeg - 1) / kMsmSeg + kMsmBuckets;  // upper bound
+    accumulate_kernel<F><<<(unsigned)((chunks + 127) / 128), 128, 0, s>>>(
+        table, sc.sorted, sc.offs, sc.coffs, sc.partials);
+    bucket_sum_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.coffs, sc.partials, sc.buckets);
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
     reduce_final_kernel<F><<<1, 256, 0, s>>>(sc.segsum, out);
     (void)X;
@@ -361,7 +351,8 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 }  // namespace
 
 void MsmScratch::release() {
-    void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum};
+    void* ps[] = {hist, offs, coffs, cursor, sorted, partials, buckets, segsum};
+    coffs = nullptr;
     for (void* p : ps)
         if (p) cudaFree(p);
     hist = offs = cursor = sorted = nullptr;

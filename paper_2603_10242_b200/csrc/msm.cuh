@@ -10,12 +10,13 @@ namespace bn {
 constexpr int kMsmC = 16;                      // window bits
 constexpr int kMsmWindows = 16;                // ceil(254 / 16), signed digits need no 17th
 constexpr int kMsmBuckets = 1 << (kMsmC - 1);  // |digit| in 1..2^15
-constexpr int kMsmSeg = 32;                    // sorted entries per accumulating thread
+constexpr int kMsmSeg = 64;                    // max entries per chunk (one accumulating thread)
 
 // Device scratch for one MSM size (grow-only, reused).
 struct MsmScratch {
     uint32_t* hist = nullptr;      // kMsmBuckets + 1
     uint32_t* offs = nullptr;      // kMsmBuckets + 1
+    uint32_t* coffs = nullptr;     // kMsmBuckets + 1 chunk offsets
     uint32_t* cursor = nullptr;    // kMsmBuckets
     uint32_t* sorted = nullptr;    // W * n entries
     uint8_t* partials = nullptr;   // 2 per segment, XYZZ records
