@@ -210,6 +210,31 @@ int acegpu_bn_msm_run(acegpu_ctx* ctx, const acegpu_msm_bases* bases, const uint
 /* Device version: d_scalars standard form, d_out affine Montgomery form. */
 int acegpu_bn_msm_run_dev(acegpu_ctx* ctx, void* stream, const acegpu_msm_bases* bases,
                           const uint8_t* d_scalars, uint8_t* d_out);
+/* ---- Groth16 per-chunk prover (north star; synthetic ZK-ACE stand-in
+ * circuit documented in oracle/bn254_oracle.h: T txs x K constraints per
+ * chunk, paper size T = 1024, K = 1400 -> 1,434,625 constraints, domain 2^21).
+ * setup: CRS from a trapdoor tau|alpha|beta|gamma|delta (5 x 32-B standard
+ * Fr), proving-key MSM tables resident on the device. prove: per-tx private
+ * witness w (n x 32-B LE, reduced mod r; the attest key, prover.cpp:181-188)
+ * and public input pub (LE(public_inputs_digest) mod r, prover.cpp:74-76);
+ * rs = r | s (standard form) or NULL to derive them deterministically
+ * (SHA-256 of the chunk's public inputs). Output: the 256-B proof
+ * A(64) | B(128) | C(64) big-endian (EIP-197, G2 as c1|c0), the raw affine
+ * points little-endian (A x,y | B x.c0,x.c1,y.c0,y.c1 | C x,y) and the chunk
+ * digest SHA-256("ace-g16-chunk-v1" | pub_0 | pub_{T-1} | T_be32). */
+typedef struct acegpu_g16 acegpu_g16;
+int acegpu_g16_setup(acegpu_ctx* ctx, uint32_t txs_per_chunk, uint32_t constraints_per_tx,
+                     const uint8_t* trapdoor5, acegpu_g16** out);
+void acegpu_g16_free(acegpu_g16* g);
+int acegpu_g16_shape(const acegpu_g16* g, uint64_t* variables, uint64_t* constraints,
+                     uint32_t* log_domain);
+int acegpu_g16_prove_chunk(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* w, const uint8_t* pub,
+                           const uint8_t* rs, uint8_t* proof256, uint8_t* raw256,
+                           uint8_t* digest32);
+int acegpu_g16_prove_chunk_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_w,
+                               const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
+                               uint8_t* d_raw256, uint8_t* d_digest32);
+
 /* Integer-pipe microbenchmarks (roofline denominators for MSM / NTT). */
 int acegpu_imad_peak(acegpu_ctx* ctx, double* imad_per_s);
 int acegpu_bn_mul_rate(acegpu_ctx* ctx, int field, double* muls_per_s);

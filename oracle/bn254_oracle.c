@@ -694,3 +694,175 @@ void bn_msm(int g, const uint8_t* pts, const uint8_t* sc, uint64_t n, uint8_t* o
     }
     store_aff(g, &acc, out);
 }
+
+/* ------------------------------------------------ Groth16 (known trapdoor) */
+void or_sha256(const uint8_t* m, uint64_t len, uint8_t out[32]); /* ace_oracle.c */
+
+static void fr_from_le_bytes(const uint8_t* b, fe* o) { to_mont(&FR, b, o); }
+
+void bn_g16_chain_const(uint32_t k, uint8_t out[32]) {
+    uint8_t m[20] = "ace-g16-chain-v1";
+    m[16] = (uint8_t)(k >> 24); m[17] = (uint8_t)(k >> 16); m[18] = (uint8_t)(k >> 8); m[19] = (uint8_t)k;
+    uint8_t d[32];
+    or_sha256(m, 20, d);
+    fe x;
+    fr_from_le_bytes(d, &x); /* reduces mod r */
+    from_mont(&FR, &x, out);
+}
+
+/* batch inversion (Montgomery trick) of n nonzero elements in place */
+static void batch_inv(fe* a, uint64_t n) {
+    fe* pre = (fe*)malloc(sizeof(fe) * (n ? n : 1));
+    fe acc;
+    memcpy(acc.v, FR.one, 32);
+    for (uint64_t i = 0; i < n; ++i) {
+        pre[i] = acc;
+        fmul(&FR, &acc, &a[i], &acc);
+    }
+    fe inv;
+    finv(&FR, &acc, &inv);
+    for (uint64_t i = n; i-- > 0;) {
+        fe t;
+        fmul(&FR, &inv, &pre[i], &t);
+        fmul(&FR, &inv, &a[i], &inv);
+        a[i] = t;
+    }
+    free(pre);
+}
+
+int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w_in, const uint8_t* pub_in,
+                    const uint8_t* trap, const uint8_t* rs2, uint8_t* out, int threads) {
+    (void)threads;
+    const uint64_t m = (uint64_t)T * K + T + 1;
+    uint32_t logn = 0;
+    while ((1ull << logn) < m) ++logn;
+    const uint64_t N = 1ull << logn;
+    fe tau, alpha, beta, delta, r, s;
+    fr_from_le_bytes(trap, &tau);
+    fr_from_le_bytes(trap + 32, &alpha);
+    fr_from_le_bytes(trap + 64, &beta);
+    fr_from_le_bytes(trap + 128, &delta);
+    fr_from_le_bytes(rs2, &r);
+    fr_from_le_bytes(rs2 + 32, &s);
+    fe one;
+    memcpy(one.v, FR.one, 32);
+    /* L_j(tau) = Z(tau)/N * w^j / (tau - w^j) for j < m */
+    fe w;
+    fr_root(logn, 0, &w);
+    uint64_t e[4] = {N, 0, 0, 0};
+    fe tN, Z, Ninv, nN, coef;
+    fpow(&FR, &tau, e, &tN);
+    fsub(&FR, &tN, &one, &Z);
+    uint8_t nb[32] = {0};
+    memcpy(nb, &N, 8);
+    to_mont(&FR, nb, &nN);
+    finv(&FR, &nN, &Ninv);
+    fmul(&FR, &Z, &Ninv, &coef);
+    fe* L = (fe*)malloc(sizeof(fe) * m);
+    fe* wj = (fe*)malloc(sizeof(fe) * m);
+    fe cur = one;
+    for (uint64_t j = 0; j < m; ++j) {
+        wj[j] = cur;
+        fsub(&FR, &tau, &cur, &L[j]);
+        fmul(&FR, &cur, &w, &cur);
+    }
+    batch_inv(L, m);
+    for (uint64_t j = 0; j < m; ++j) {
+        fmul(&FR, &L[j], &wj[j], &L[j]);
+        fmul(&FR, &L[j], &coef, &L[j]);
+    }
+    free(wj);
+    /* chain constants */
+    fe* c = (fe*)malloc(sizeof(fe) * K);
+    for (uint32_t k = 1; k < K; ++k) {
+        uint8_t b[32];
+        bn_g16_chain_const(k, b);
+        to_mont(&FR, b, &c[k]);
+    }
+    /* a(tau), b(tau), c(tau) over the rows, and the public polynomials */
+    fe at = {{0}}, bt = {{0}}, ct = {{0}}, u1 = {{0}}, v1 = {{0}}, pub_part = {{0}}, t1, t2;
+    fe zero = {{0}};
+    for (uint32_t t = 0; t < T; ++t) {
+        fe wt, pt, x;
+        fr_from_le_bytes(w_in + 32ull * t, &wt);
+        fr_from_le_bytes(pub_in + 32ull * t, &pt);
+        const uint64_t R = (uint64_t)t * K;
+        /* row R: a = w+pub, b = 1, c = x0 */
+        fadd(&FR, &wt, &pt, &x);
+        fmul(&FR, &x, &L[R], &t1); fadd(&FR, &at, &t1, &at);
+        fadd(&FR, &bt, &L[R], &bt);
+        fmul(&FR, &x, &L[R], &t1); fadd(&FR, &ct, &t1, &ct);
+        fadd(&FR, &v1, &L[R], &v1); /* ONE in B of row R */
+        /* pub_t: u = L[R] + L[P0+1+t] */
+        fe upub;
+        fadd(&FR, &L[R], &L[(uint64_t)T * K + 1 + t], &upub);
+        fmul(&FR, &beta, &upub, &t1);
+        fmul(&FR, &pt, &t1, &t2);
+        fadd(&FR, &pub_part, &t2, &pub_part);
+        for (uint32_t k = 1; k < K; ++k) {
+            fe y, y2;
+            fadd(&FR, &x, &c[k], &y);
+            fmul(&FR, &y, &y, &y2);
+            fmul(&FR, &y, &L[R + k], &t1);
+            fadd(&FR, &at, &t1, &at);
+            fadd(&FR, &bt, &t1, &bt);
+            fmul(&FR, &y2, &L[R + k], &t1);
+            fadd(&FR, &ct, &t1, &ct);
+            fmul(&FR, &c[k], &L[R + k], &t1);
+            fadd(&FR, &u1, &t1, &u1); /* ONE in A of chain rows */
+            fadd(&FR, &v1, &t1, &v1); /* and in B */
+            x = y2;
+        }
+        /* public row for pub_t: a = pub_t */
+        fmul(&FR, &pt, &L[(uint64_t)T * K + 1 + t], &t1);
+        fadd(&FR, &at, &t1, &at);
+    }
+    /* public row for ONE */
+    fadd(&FR, &at, &L[(uint64_t)T * K], &at);
+    fadd(&FR, &u1, &L[(uint64_t)T * K], &u1);
+    /* ONE's share of the public part: beta*u1 + alpha*v1 (w = 0) */
+    fmul(&FR, &beta, &u1, &t1);
+    fmul(&FR, &alpha, &v1, &t2);
+    fadd(&FR, &pub_part, &t1, &pub_part);
+    fadd(&FR, &pub_part, &t2, &pub_part);
+    /* h(tau) Z(tau) = a b - c */
+    fe hz, priv;
+    fmul(&FR, &at, &bt, &hz);
+    fsub(&FR, &hz, &ct, &hz);
+    fmul(&FR, &beta, &at, &t1);
+    fmul(&FR, &alpha, &bt, &t2);
+    fadd(&FR, &t1, &t2, &priv);
+    fadd(&FR, &priv, &ct, &priv);
+    fsub(&FR, &priv, &pub_part, &priv);
+    fe A, B, C, dinv, rs;
+    fmul(&FR, &r, &delta, &t1);
+    fadd(&FR, &alpha, &at, &A);
+    fadd(&FR, &A, &t1, &A);
+    fmul(&FR, &s, &delta, &t1);
+    fadd(&FR, &beta, &bt, &B);
+    fadd(&FR, &B, &t1, &B);
+    finv(&FR, &delta, &dinv);
+    fadd(&FR, &priv, &hz, &C);
+    fmul(&FR, &C, &dinv, &C);
+    fmul(&FR, &s, &A, &t1);
+    fadd(&FR, &C, &t1, &C);
+    fmul(&FR, &r, &B, &t1);
+    fadd(&FR, &C, &t1, &C);
+    fmul(&FR, &r, &s, &rs);
+    fmul(&FR, &rs, &delta, &t1);
+    fsub(&FR, &C, &t1, &C);
+    from_mont(&FR, &A, out);
+    from_mont(&FR, &B, out + 32);
+    from_mont(&FR, &C, out + 64);
+    /* verification identity */
+    fe lhs, rhs;
+    fmul(&FR, &A, &B, &lhs);
+    fmul(&FR, &alpha, &beta, &rhs);
+    fadd(&FR, &rhs, &pub_part, &rhs);
+    fmul(&FR, &C, &delta, &t1);
+    fadd(&FR, &rhs, &t1, &rhs);
+    (void)zero;
+    free(L);
+    free(c);
+    return feq(&lhs, &rhs);
+}

@@ -55,6 +55,22 @@ void bn_fixed_base_muls(int group, const uint8_t* base, const uint8_t* scalars, 
 void bn_msm(int group, const uint8_t* points, const uint8_t* scalars, uint64_t n, uint8_t* out,
             int threads);
 
+/* ---- Groth16 over the synthetic ZK-ACE stand-in circuit (known trapdoor) ----
+ * Shape: T txs, K >= 2 constraints per tx. Variables: 0 = ONE, 1..T = pub_t
+ * (public), then per tx t: w_t, x_{t,0}, ..., x_{t,K-1} (private).
+ * Rows: tx t, base R = t*K: row R: (w_t + pub_t) * 1 = x_{t,0};
+ * row R+k (k = 1..K-1): (x_{t,k-1} + c_k) * (x_{t,k-1} + c_k) = x_{t,k};
+ * rows T*K + i (i = 0..T): z_i * 0 = 0 for the public variables (ONE, pub).
+ * c_k = LE(SHA-256("ace-g16-chain-v1" | k_be32)) mod r.
+ * Given the trapdoor (tau, alpha, beta, gamma, delta) and r, s, returns the
+ * discrete logs of the proof (A, B, C) in Fr and whether the Groth16
+ * verification identity A*B = alpha*beta + sum_pub z_i(beta u_i + alpha v_i
+ * + w_i) + C*delta holds (1) — the pairing check, in exponents. */
+void bn_g16_chain_const(uint32_t k, uint8_t out32[32]);
+int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w, const uint8_t* pub,
+                    const uint8_t* trapdoor5, const uint8_t* rs2, uint8_t* out_abc3,
+                    int threads);
+
 #ifdef __cplusplus
 }
 #endif

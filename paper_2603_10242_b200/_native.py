@@ -69,6 +69,11 @@ _SIGS = {
     "acegpu_bn_msm_free": (None, [C.c_void_p]),
     "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),
     "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),
+    "acegpu_g16_setup": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_void_p)]),
+    "acegpu_g16_free": (None, [C.c_void_p]),
+    "acegpu_g16_shape": (C.c_int, [C.c_void_p, u64p, u64p, C.POINTER(C.c_uint32)]),
+    "acegpu_g16_prove_chunk": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
+    "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_imad_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
     "acegpu_bn_mul_rate": (C.c_int, [ctxp, C.c_int, C.POINTER(C.c_double)]),
 }

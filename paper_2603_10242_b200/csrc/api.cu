@@ -6,12 +6,14 @@
 #include <atomic>
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/acegpu.h"
 #include "bn_kernels.cuh"
+#include "g16_kernels.cuh"
 #include "mock_kernels.cuh"
 #include "msm.cuh"
 #include "ntt.cuh"
@@ -1150,5 +1152,245 @@ extern "C" int acegpu_bn_mul_rate(acegpu_ctx* c, int field, double* muls_per_s) 
     RET(bn_time(c, c->stream, mulrate_launch, &a, &ms));
     c->launches += 2;
     *muls_per_s = double(a.blocks) * a.threads * a.iters * 4 / (ms * 1e-3);
+    return ACEGPU_OK;
+}
+
+// ==================================================================== Groth16
+struct acegpu_g16 {
+    int device = 0;
+    bn::G16Dims d{};
+    uint32_t logn = 0;
+    uint64_t N = 0, Vp = 0;  // Vp: private variables
+    acegpu_msm_bases *qa = nullptr, *qb1 = nullptr, *qb2 = nullptr, *ql = nullptr, *qh = nullptr;
+    uint8_t *consts = nullptr, *cc = nullptr;
+    uint8_t *z = nullptr, *zb = nullptr, *zl = nullptr, *ea = nullptr, *eb = nullptr, *ec = nullptr;
+    uint8_t *pts = nullptr, *scaled = nullptr, *rs = nullptr, *digest = nullptr;
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_ab = nullptr, ev_scaled = nullptr;
+};
+
+namespace {
+
+int bases_from_device(int device, int group, const uint8_t* d_pts_mont, uint64_t n,
+                      cudaStream_t s, acegpu_msm_bases** out) {
+    auto* b = new acegpu_msm_bases();
+    b->device = device;
+    b->group = group;
+    b->n = n;
+    cudaError_t e = cudaMalloc(&b->table, 64ull * group * n * bn::kMsmWindows);
+    if (e != cudaSuccess) {
+        delete b;
+        return fail(ACEGPU_ECUDA, std::string("g16 table alloc: ") + cudaGetErrorString(e));
+    }
+    if (bn::msm_prepare(group, d_pts_mont, n, b->table, s)) {
+        acegpu_bn_msm_free(b);
+        return fail(ACEGPU_ECUDA, "g16 msm_prepare");
+    }
+    *out = b;
+    return ACEGPU_OK;
+}
+
+const char* kG2Gen[4] = {
+    "10857046999023057135944570762232829481370756359578518086990519993285655852781",
+    "11559732032986387107991004021392285783925812861821192530917403151452391805634",
+    "8495653923123431417604973247489272438418190587263600148770280649306958101930",
+    "4082367875863433681332203403145435568316851327593401208105741076214120093531"};
+
+void dec_to_le32(const char* s, uint8_t* out) {
+    uint32_t v[8] = {0};
+    for (; *s; ++s) {
+        uint64_t c = uint64_t(*s - '0');
+        for (int i = 0; i < 8; ++i) {
+            uint64_t x = uint64_t(v[i]) * 10 + c;
+            v[i] = uint32_t(x);
+            c = x >> 32;
+        }
+    }
+    std::memcpy(out, v, 32);
+}
+
+}  // namespace
+
+extern "C" void acegpu_g16_free(acegpu_g16* g) {
+    if (!g) return;
+    DeviceGuard guard(g->device);
+    cudaDeviceSynchronize();
+    for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh}) acegpu_bn_msm_free(b);
+    for (uint8_t* p : {g->consts, g->cc, g->z, g->zb, g->zl, g->ea, g->eb, g->ec, g->pts,
+                       g->scaled, g->rs, g->digest})
+        if (p) cudaFree(p);
+    if (g->side) cudaStreamDestroy(g->side);
+    if (g->ev_ab) cudaEventDestroy(g->ev_ab);
+    if (g->ev_scaled) cudaEventDestroy(g->ev_scaled);
+    delete g;
+}
+
+extern "C" int acegpu_g16_shape(const acegpu_g16* g, uint64_t* V, uint64_t* m, uint32_t* logn) {
+    if (V) *V = g->d.V;
+    if (m) *m = g->d.m;
+    if (logn) *logn = g->logn;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uint8_t* trapdoor5,
+                                acegpu_g16** out) {
+    if (T < 1 || K < 2) return fail(ACEGPU_EINVAL, "g16: need T >= 1 and K >= 2");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    auto* g = new acegpu_g16();
+    std::unique_ptr<acegpu_g16, void (*)(acegpu_g16*)> own(g, acegpu_g16_free);
+    g->device = c->device;
+    g->d.T = T;
+    g->d.K = K;
+    g->d.V = 1 + uint64_t(T) + uint64_t(T) * (K + 1);
+    g->d.m = uint64_t(T) * K + T + 1;
+    while ((1ull << g->logn) < g->d.m) ++g->logn;
+    if (g->logn > uint32_t(bn::kNttMaxLog)) return fail(ACEGPU_EINVAL, "g16: domain above 2^22");
+    g->N = 1ull << g->logn;
+    g->Vp = g->d.V - 1 - T;
+    const uint64_t V = g->d.V, N = g->N, m = g->d.m;
+    auto dm = [&](uint8_t** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 16); };
+    if (dm(&g->consts, 32 * 16) || dm(&g->cc, 32ull * K) || dm(&g->z, 32 * (V + 2)) ||
+        dm(&g->zb, 32 * (V + 2)) || dm(&g->zl, 32 * (g->Vp + 1)) || dm(&g->ea, 32 * N) ||
+        dm(&g->eb, 32 * N) || dm(&g->ec, 32 * N) || dm(&g->pts, 512) || dm(&g->scaled, 256) ||
+        dm(&g->rs, 64) || dm(&g->digest, 32))
+        return fail(ACEGPU_ECUDA, "g16 alloc");
+    CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g->ev_ab, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
+    // constants
+    CK(cudaMemcpyAsync(g->consts, trapdoor5, 160, cudaMemcpyHostToDevice, s));
+    bn::g16_setup_consts(g->consts, g->logn, s);
+    bn::g16_chain_consts(K, g->cc, s);
+    // query scalars
+    uint8_t *L, *su, *sv, *sl, *part, *hs, *gens, *ext, *pts;
+    if (dm(&L, 32 * m) || dm(&su, 32 * V) || dm(&sv, 32 * V) || dm(&sl, 32 * g->Vp) ||
+        dm(&part, 256 * 64) || dm(&hs, 32 * N) || dm(&gens, 256) || dm(&ext, 512) ||
+        dm(&pts, 128 * (std::max(V, N) + 2)))
+        return fail(ACEGPU_ECUDA, "g16 setup alloc");
+    bn::g16_lagrange(g->consts, m, L, s);
+    bn::g16_query_scalars(g->d, L, g->consts, g->cc, part, su, sv, sl, s);
+    bn::g16_h_scalars(g->consts, N - 1, hs, s);
+    // generators (Montgomery affine) and the extra bases alpha1 beta1 delta1 | beta2 delta2
+    uint8_t hgen[192] = {0};
+    hgen[0] = 1;
+    hgen[32] = 2;
+    for (int i = 0; i < 4; ++i) dec_to_le32(kG2Gen[i], hgen + 64 + 32 * i);
+    uint8_t hsc[96];
+    std::memcpy(hsc, trapdoor5 + 32, 32);      // alpha
+    std::memcpy(hsc + 32, trapdoor5 + 64, 32); // beta
+    std::memcpy(hsc + 64, trapdoor5 + 128, 32);// delta
+    CK(cudaMemcpyAsync(gens, hgen, 192, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(ext + 256, hsc, 96, cudaMemcpyHostToDevice, s));  // scalars at ext+256
+    bn::launch_points_convert(1, gens, 1, 1, s);
+    bn::launch_points_convert(2, gens + 64, 1, 1, s);
+    uint8_t* ex1 = ext;  // 3 G1 points: alpha1, beta1, delta1 (192 B) -> then G2 below
+    bn::launch_scalar_muls(1, gens, ext + 256, 3, ex1, s);
+    uint8_t* ex2;
+    if (dm(&ex2, 256)) return fail(ACEGPU_ECUDA, "g16 setup alloc");
+    bn::launch_scalar_muls(2, gens + 64, ext + 256 + 32, 2, ex2, s);  // beta2, delta2
+    CKL();
+    // A: [u]1 | alpha1 | delta1
+    bn::launch_scalar_muls(1, gens, su, V, pts, s);
+    CK(cudaMemcpyAsync(pts + 64 * V, ex1, 64, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(pts + 64 * (V + 1), ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
+    RET(bases_from_device(c->device, 1, pts, V + 2, s, &g->qa));
+    // B1: [v]1 | beta1 | delta1
+    bn::launch_scalar_muls(1, gens, sv, V, pts, s);
+    CK(cudaMemcpyAsync(pts + 64 * V, ex1 + 64, 64, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(pts + 64 * (V + 1), ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
+    RET(bases_from_device(c->device, 1, pts, V + 2, s, &g->qb1));
+    // B2: [v]2 | beta2 | delta2
+    bn::launch_scalar_muls(2, gens + 64, sv, V, pts, s);
+    CK(cudaMemcpyAsync(pts + 128 * V, ex2, 256, cudaMemcpyDeviceToDevice, s));
+    RET(bases_from_device(c->device, 2, pts, V + 2, s, &g->qb2));
+    // L: [l]1 (private) | delta1
+    bn::launch_scalar_muls(1, gens, sl, g->Vp, pts, s);
+    CK(cudaMemcpyAsync(pts + 64 * g->Vp, ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
+    RET(bases_from_device(c->device, 1, pts, g->Vp + 1, s, &g->ql));
+    // H: [tau^j Z(tau)/delta]1, j < N-1
+    bn::launch_scalar_muls(1, gens, hs, N - 1, pts, s);
+    RET(bases_from_device(c->device, 1, pts, N - 1, s, &g->qh));
+    CKL();
+    CK(cudaStreamSynchronize(s));
+    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2}) cudaFree(p);
+    if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s)) return fail(ACEGPU_ECUDA, "g16 NTT tables");
+    CK(cudaStreamSynchronize(s));
+    c->launches += 20;
+    *out = own.release();
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                          const uint8_t* d_w, const uint8_t* d_pub,
+                                          const uint8_t* d_rs, uint8_t* d_proof256,
+                                          uint8_t* d_raw256, uint8_t* d_digest32) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    const uint64_t V = g->d.V, N = g->N, m = g->d.m;
+    uint8_t* scratch;
+    RET(ws(c, kBnScratch, 32 * N, &scratch));
+    for (uint8_t* e : {g->ea, g->eb, g->ec})
+        if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), s));
+    bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, s);
+    bn::g16_derive_rs(d_pub, g->d.T, g->rs, g->digest, s);
+    if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, s));
+    if (d_digest32) CK(cudaMemcpyAsync(d_digest32, g->digest, 32, cudaMemcpyDeviceToDevice, s));
+    // H(x) = (a b - c) / Z on the coset, back to coefficients
+    const bn::NttTables& t = c->ntt[g->logn];
+    if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
+    for (uint8_t* e : {g->ea, g->eb, g->ec}) {
+        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, s)) return fail(ACEGPU_ECUDA, "g16 intt");
+        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, s)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
+    }
+    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, s);
+    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, s)) return fail(ACEGPU_ECUDA, "g16 coset intt");
+    bn::launch_fr_convert(g->ea, N, 0, s);  // h coefficients -> standard form scalars
+    // scalar vectors with their extras
+    CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, s));
+    bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, s);
+    CKL();
+    // MSMs: A and B1 first, then s*A and r*B1 on the side stream under B2/L/H
+    if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, s) ||
+        bn::msm_run(1, g->qb1->table, V + 2, g->zb, c->msm, g->pts + 64, s))
+        return fail(ACEGPU_ECUDA, "g16 msm A/B1");
+    CK(cudaEventRecord(g->ev_ab, s));
+    CK(cudaStreamWaitEvent(g->side, g->ev_ab, 0));
+    bn::g16_scale(g->pts, g->rs, g->scaled, g->side);
+    CK(cudaEventRecord(g->ev_scaled, g->side));
+    if (bn::msm_run(2, g->qb2->table, V + 2, g->zb, c->msm, g->pts + 128, s) ||
+        bn::msm_run(1, g->ql->table, g->Vp + 1, g->zl, c->msm, g->pts + 256, s) ||
+        bn::msm_run(1, g->qh->table, N - 1, g->ea, c->msm, g->pts + 320, s))
+        return fail(ACEGPU_ECUDA, "g16 msm B2/L/H");
+    CK(cudaStreamWaitEvent(s, g->ev_scaled, 0));
+    bn::g16_assemble(g->pts, g->scaled, d_proof256, d_raw256, s);
+    CKL();
+    c->launches += 16 + 5 * 7 + 6;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_prove_chunk(acegpu_ctx* c, acegpu_g16* g, const uint8_t* w,
+                                      const uint8_t* pub, const uint8_t* rs, uint8_t* proof256,
+                                      uint8_t* raw256, uint8_t* digest32) {
+    uint8_t *dw, *dp, *drs = nullptr, *dout;
+    const uint64_t T = g->d.T;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard guard(c->device);
+        RET(h2d_t(c, kBnA, w, 32 * T, c->stream, &dw));
+        RET(h2d_t(c, kBnB, pub, 32 * T, c->stream, &dp));
+        if (rs) RET(h2d_t(c, kIn2, rs, 64, c->stream, &drs));
+        RET(ws(c, kBnOut, 512 + 32, &dout));
+    }
+    RET(acegpu_g16_prove_chunk_dev(c, c->stream, g, dw, dp, drs, dout, dout + 256, dout + 512));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    if (proof256) CK(cudaMemcpyAsync(proof256, dout, 256, cudaMemcpyDeviceToHost, c->stream));
+    if (raw256) CK(cudaMemcpyAsync(raw256, dout + 256, 256, cudaMemcpyDeviceToHost, c->stream));
+    if (digest32) CK(cudaMemcpyAsync(digest32, dout + 512, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
     return ACEGPU_OK;
 }

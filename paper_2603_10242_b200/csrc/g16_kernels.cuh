@@ -1,0 +1,41 @@
+// Launchers for groth16.cu (synthetic ZK-ACE stand-in circuit, see
+// oracle/bn254_oracle.h for the constraint system).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace ace_gpu {
+namespace bn {
+
+struct G16Dims {
+    uint32_t T, K;  // txs per chunk, constraints per tx
+    uint64_t V;     // variables 1 + T + T*(K+1)
+    uint64_t m;     // constraints T*K + T + 1
+};
+
+// Setup (CRS from a trapdoor; all Fr in Montgomery form unless noted).
+void g16_chain_consts(uint32_t K, uint8_t* out, cudaStream_t s);
+// c[0..4] = tau, alpha, beta, gamma, delta in standard form -> converted;
+// fills c[5..10] (see groth16.cu).
+void g16_setup_consts(uint8_t* c, uint32_t logn, cudaStream_t s);
+void g16_lagrange(const uint8_t* c, uint64_t m, uint8_t* L, cudaStream_t s);
+// su, sv: V scalars; sl: V - T - 1 scalars (standard form); part: 256*64 B scratch
+void g16_query_scalars(const G16Dims& d, const uint8_t* L, const uint8_t* c, const uint8_t* cc,
+                       uint8_t* part, uint8_t* su, uint8_t* sv, uint8_t* sl, cudaStream_t s);
+void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s);
+
+// Prover.
+void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const uint8_t* cc,
+                 uint8_t* z, uint8_t* ea, uint8_t* eb, uint8_t* ec, cudaStream_t s);
+void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint8_t* c,
+                   uint64_t n, cudaStream_t s);
+void g16_derive_rs(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest, cudaStream_t s);
+void g16_extras(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp, const uint8_t* rs,
+                cudaStream_t s);
+void g16_scale(const uint8_t* pts, const uint8_t* rs, uint8_t* out, cudaStream_t s);
+void g16_assemble(const uint8_t* pts, const uint8_t* scaled, uint8_t* proof, uint8_t* raw,
+                  cudaStream_t s);
+
+}  // namespace bn
+}  // namespace ace_gpu

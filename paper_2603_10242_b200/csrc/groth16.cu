@@ -1,0 +1,411 @@
+// Groth16 over BN254 for the synthetic ZK-ACE stand-in circuit (north-star
+// K10 r1cs_eval + h_pointwise and K11 groth16_assemble of SURVEY §2b; the
+// reference has only a hash mock). The constraint system is
+// documented in oracle/bn254_oracle.h (the CPU checker of record).
+//
+// Per chunk of T txs with K constraints each (paper size T = 1024, K = 1400,
+// m = 1,434,625 constraints, domain 2^21):
+//   witness  : per tx the K-step chain x_k = (x_{k-1} + c_k)^2 seeded with
+//              w_t + pub_t; writes z and the row evaluations a, b, c
+//   H        : 3 iNTT + 3 coset NTT + pointwise (a b - c) / Z(g w^j) + coset iNTT
+//   MSMs     : A = [u](z) + alpha + r delta, B = [v](z) + beta + s delta (G2
+//              and G1), L = [l](z_priv) - rs delta, H = [h]
+//   assemble : C = L + H + s A + r B1
+#include <cuda_runtime.h>
+
+#include "curve.cuh"
+#include "g16_kernels.cuh"
+#include "sha256.cuh"
+
+namespace ace_gpu {
+namespace bn {
+
+namespace {
+
+__device__ __forceinline__ Fr ldr(const uint8_t* p) { return load<FrCfg>(p); }
+__device__ __forceinline__ void str(uint8_t* p, const Fr& x) { store<FrCfg>(p, x); }
+
+// LE(32 B) mod r for any 256-bit value (< 2^256 < 6r).
+__device__ __forceinline__ Fr reduce256(const uint32_t v[8]) {
+    uint32_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = v[i];
+    uint32_t m[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) m[i] = mod_limb<FrCfg>(i);
+    while (detail::limbs_geq(x, m)) detail::limbs_sub(x, m);
+    Fr r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.v[i] = x[i];
+    return r;
+}
+
+// Digest words (big-endian values) -> the 32 wire bytes read as a LE integer.
+__device__ __forceinline__ Fr digest_to_fr(const uint32_t d[8]) {
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = bswap32(d[i]);  // byte 4i is the low byte of limb i
+    return reduce256(v);
+}
+
+// c_k = LE(SHA-256("ace-g16-chain-v1" | k_be32)) mod r (Montgomery out).
+__global__ void chain_consts_kernel(uint32_t K, uint8_t* out) {
+    const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    __align__(16) uint8_t m[32];
+    const char tag[] = "ace-g16-chain-v1";
+    for (int i = 0; i < 16; ++i) m[i] = tag[i];
+    m[16] = k >> 24; m[17] = k >> 16; m[18] = k >> 8; m[19] = k;
+    uint32_t d[8];
+    sha256_bytes(m, 0, 20, d);
+    str(out + 32ull * k, k ? to_mont(digest_to_fr(d)) : Fr::zero());
+}
+
+// Scalars of the setup (Montgomery): [0] tau [1] alpha [2] beta [3] gamma
+// [4] delta (inputs, standard form, converted here) -> [5] omega_N,
+// [6] Z(tau)/N, [7] Z(tau)/delta, [8] 1/delta, [9] (g^N - 1)^-1, [10] Z(tau).
+__global__ void setup_consts_kernel(uint8_t* c, uint32_t logn) {
+    if (threadIdx.x || blockIdx.x) return;
+    for (int i = 0; i < 5; ++i) str(c + 32 * i, to_mont(ldr(c + 32 * i)));
+    const Fr tau = ldr(c), delta = ldr(c + 128);
+    uint32_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = mod_limb<FrCfg>(i);
+    e[0] -= 1;
+    for (uint32_t s = 0; s < logn; ++s)
+        for (int i = 0; i < 8; ++i) e[i] = (e[i] >> 1) | (i < 7 ? (e[i + 1] << 31) : 0u);
+    Fr five = Fr::zero();
+    five.v[0] = 5;
+    five = to_mont(five);
+    const Fr w = pow(five, e);
+    uint32_t en[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (logn < 32) en[0] = 1u << logn;
+    else en[1] = 1u << (logn - 32);
+    const Fr Z = sub(pow(tau, en), Fr::one());
+    Fr n = Fr::zero();
+    n.v[0] = en[0];
+    n.v[1] = en[1];
+    const Fr ninv = inv_fast(to_mont(n));
+    const Fr dinv = inv_fast(delta);
+    str(c + 32 * 5, w);
+    str(c + 32 * 6, mul(Z, ninv));
+    str(c + 32 * 7, mul(Z, dinv));
+    str(c + 32 * 8, dinv);
+    str(c + 32 * 9, inv_fast(sub(pow(five, en), Fr::one())));
+    str(c + 32 * 10, Z);
+}
+
+// L_j(tau) = Z(tau)/N * w^j / (tau - w^j), j < m (Montgomery).
+__global__ void lagrange_kernel(const uint8_t* c, uint64_t m, uint8_t* L) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= m) return;
+    const Fr tau = ldr(c), w = ldr(c + 32 * 5), coef = ldr(c + 32 * 6);
+    Fr wj = Fr::one(), b = w;
+    for (uint64_t e = j; e; e >>= 1) {
+        if (e & 1) wj = mul(wj, b);
+        b = sqr(b);
+    }
+    str(L + 32 * j, mul(mul(coef, wj), inv_fast(sub(tau, wj))));
+}
+
+// Partial sums for ONE's u and v over the chain rows (block per tx range).
+__global__ void one_partials_kernel(G16Dims d, const uint8_t* L, const uint8_t* cc,
+                                    uint8_t* part /* 2 per block */) {
+    __shared__ __align__(16) uint8_t su[256 * 32], sv[256 * 32];
+    Fr u = Fr::zero(), v = Fr::zero();
+    const uint64_t total = (uint64_t)d.T * d.K;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < total;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = idx % d.K;
+        const Fr l = ldr(L + 32 * idx);  // row idx = t*K + k
+        if (k == 0) {
+            v = add(v, l);  // B of row R_t holds ONE
+        } else {
+            const Fr t = mul(ldr(cc + 32ull * k), l);
+            u = add(u, t);
+            v = add(v, t);
+        }
+    }
+    str(su + 32 * threadIdx.x, u);
+    str(sv + 32 * threadIdx.x, v);
+    __syncthreads();
+    for (int s = blockDim.x / 2; s; s >>= 1) {
+        if (threadIdx.x < s) {
+            str(su + 32 * threadIdx.x, add(ldr(su + 32 * threadIdx.x), ldr(su + 32 * (threadIdx.x + s))));
+            str(sv + 32 * threadIdx.x, add(ldr(sv + 32 * threadIdx.x), ldr(sv + 32 * (threadIdx.x + s))));
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        str(part + 64ull * blockIdx.x, ldr(su));
+        str(part + 64ull * blockIdx.x + 32, ldr(sv));
+    }
+}
+
+// Query scalars (standard form) for every variable i:
+//   su[i] = u_i(tau), sv[i] = v_i(tau), sl[i - T - 1] = (beta u + alpha v + w)/delta (private)
+// ONE's u, v come from the block partials (summed by thread 0).
+__global__ void query_scalars_kernel(G16Dims d, const uint8_t* L, const uint8_t* c,
+                                     const uint8_t* part, uint32_t nparts, uint8_t* su,
+                                     uint8_t* sv, uint8_t* sl) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= d.V) return;
+    const uint64_t P0 = (uint64_t)d.T * d.K;
+    const Fr zero = Fr::zero();
+    Fr u = zero, v = zero, w = zero;
+    if (i == 0) {
+        for (uint32_t b = 0; b < nparts; ++b) {
+            u = add(u, ldr(part + 64ull * b));
+            v = add(v, ldr(part + 64ull * b + 32));
+        }
+        u = add(u, ldr(L + 32 * P0));
+    } else if (i <= d.T) {
+        const uint64_t t = i - 1;
+        u = add(ldr(L + 32 * (t * d.K)), ldr(L + 32 * (P0 + 1 + t)));
+    } else {
+        const uint64_t q = i - 1 - d.T, t = q / (d.K + 1), loc = q % (d.K + 1);
+        const uint64_t R = t * d.K;
+        if (loc == 0) {  // w_t: A of row R
+            u = ldr(L + 32 * R);
+        } else {  // x_{t,k}, k = loc - 1
+            const uint64_t k = loc - 1;
+            w = ldr(L + 32 * (R + k));
+            if (k + 1 < d.K) {
+                u = ldr(L + 32 * (R + k + 1));
+                v = u;
+            }
+        }
+    }
+    str(su + 32 * i, from_mont(u));
+    str(sv + 32 * i, from_mont(v));
+    if (i > d.T) {
+        const Fr alpha = ldr(c + 32), beta = ldr(c + 64), dinv = ldr(c + 32 * 8);
+        const Fr l = mul(add(add(mul(beta, u), mul(alpha, v)), w), dinv);
+        str(sl + 32 * (i - 1 - d.T), from_mont(l));
+    }
+}
+
+// H-query scalars: tau^j Z(tau)/delta for j < n (standard form).
+__global__ void h_scalars_kernel(const uint8_t* c, uint64_t n, uint8_t* out) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    Fr x = ldr(c + 32 * 7), b = ldr(c);
+    for (uint64_t e = j; e; e >>= 1) {
+        if (e & 1) x = mul(x, b);
+        b = sqr(b);
+    }
+    str(out + 32 * j, from_mont(x));
+}
+
+// Witness + row evaluations. One thread per tx: the chain is sequential.
+// z: standard form (MSM scalars); ea/eb/ec: Montgomery (NTT inputs, zeroed beyond m).
+__global__ void witness_kernel(G16Dims d, const uint8_t* w_in, const uint8_t* pub_in,
+                               const uint8_t* cc, uint8_t* z, uint8_t* ea, uint8_t* eb,
+                               uint8_t* ec) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= d.T) return;
+    const uint64_t P0 = (uint64_t)d.T * d.K;
+    const Fr one = Fr::one();
+    const Fr ws = reduce256(ldr(w_in + 32ull * t).v), ps = reduce256(ldr(pub_in + 32ull * t).v);
+    const Fr wt = to_mont(ws), pt = to_mont(ps);
+    if (t == 0) {
+        Fr o = Fr::zero();
+        o.v[0] = 1;
+        str(z, o);
+        str(ea + 32 * P0, one);  // public row of ONE: a = 1
+        str(eb + 32 * P0, Fr::zero());
+        str(ec + 32 * P0, Fr::zero());
+    }
+    str(z + 32 * (1 + t), ps);
+    str(ea + 32 * (P0 + 1 + t), pt);  // public row of pub_t
+    str(eb + 32 * (P0 + 1 + t), Fr::zero());
+    str(ec + 32 * (P0 + 1 + t), Fr::zero());
+    const uint64_t vb = 1 + d.T + (uint64_t)t * (d.K + 1);  // w_t, x_{t,0..K-1}
+    const uint64_t R = (uint64_t)t * d.K;
+    str(z + 32 * vb, ws);
+    Fr x = add(wt, pt);
+    str(ea + 32 * R, x);
+    str(eb + 32 * R, one);
+    str(ec + 32 * R, x);
+    str(z + 32 * (vb + 1), from_mont(x));
+    for (uint32_t k = 1; k < d.K; ++k) {
+        const Fr y = add(x, ldr(cc + 32ull * k));
+        const Fr y2 = sqr(y);
+        str(ea + 32 * (R + k), y);
+        str(eb + 32 * (R + k), y);
+        str(ec + 32 * (R + k), y2);
+        str(z + 32 * (vb + 1 + k), from_mont(y2));
+        x = y2;
+    }
+}
+
+// h_j = (a_j b_j - c_j) / (g^N - 1) on the coset (Montgomery, in place into ea).
+__global__ void pointwise_kernel(uint8_t* ea, const uint8_t* eb, const uint8_t* ec,
+                                 const uint8_t* c, uint64_t n) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const Fr zi = ldr(c + 32 * 9);
+    str(ea + 32 * j, mul(sub(mul(ldr(ea + 32 * j), ldr(eb + 32 * j)), ldr(ec + 32 * j)), zi));
+}
+
+// Deterministic r, s: LE(SHA-256(tag | pub_0 | pub_{T-1} | T_be32)) mod r,
+// tags "ace-g16-r-v1" / "ace-g16-s-v1"; also writes the chunk digest
+// SHA-256("ace-g16-chunk-v1" | pub_0 | pub_{T-1} | T_be32).
+__global__ void derive_rs_kernel(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest) {
+    const int which = threadIdx.x;  // 0: r, 1: s, 2: chunk digest
+    if (which > 2) return;
+    __align__(16) uint8_t m[96];
+    const char* tag = which == 0 ? "ace-g16-r-v1" : which == 1 ? "ace-g16-s-v1" : "ace-g16-chunk-v1";
+    const int tl = which == 2 ? 16 : 12;
+    for (int i = 0; i < tl; ++i) m[i] = tag[i];
+    for (int i = 0; i < 32; ++i) {
+        m[tl + i] = pub[i];
+        m[tl + 32 + i] = pub[32ull * (T - 1) + i];
+    }
+    m[tl + 64] = T >> 24; m[tl + 65] = T >> 16; m[tl + 66] = T >> 8; m[tl + 67] = T;
+    uint32_t d[8];
+    sha256_bytes(m, 0, tl + 68, d);
+    if (which == 2) store_digest(digest, d);
+    else str(rs + 32 * which, digest_to_fr(d));
+}
+
+// Scalar extras appended to the MSM scalar vectors (standard form):
+// zA[V..] = 1, r ; zB[V..] = 1, s ; zL[Vp] = -rs.
+__global__ void extras_kernel(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp,
+                              const uint8_t* rs) {
+    if (threadIdx.x || blockIdx.x) return;
+    Fr one = Fr::zero();
+    one.v[0] = 1;
+    const Fr r = ldr(rs), s = ldr(rs + 32);
+    str(za + 32 * V, one);
+    str(za + 32 * (V + 1), r);
+    str(zb + 32 * V, one);
+    str(zb + 32 * (V + 1), s);
+    str(zl + 32 * Vp, from_mont(neg(mul(to_mont(r), to_mont(s)))));
+}
+
+// s*A and r*B1 (two threads, double-and-add on XYZZ), written as XYZZ.
+__global__ void scale_kernel(const uint8_t* pts, const uint8_t* rs, uint8_t* out) {
+    const int which = threadIdx.x;
+    if (which > 1) return;
+    const uint8_t* p = pts + (which == 0 ? 0 : 64);  // A or B1 (affine Montgomery)
+    Fq x = load<FqCfg>(p), y = load<FqCfg>(p + 32);
+    const uint8_t* k = rs + (which == 0 ? 32 : 0);   // s for A, r for B1
+    XYZZ<Fq> acc = XYZZ<Fq>::inf();
+    if (!(x.is_zero() && y.is_zero())) {
+        for (int bit = 255; bit >= 0; --bit) {
+            acc = xyzz_dbl(acc);
+            if ((k[bit >> 3] >> (bit & 7)) & 1) acc = xyzz_madd(acc, x, y);
+        }
+    }
+    uint8_t* o = out + 128 * which;
+    store<FqCfg>(o, acc.X);
+    store<FqCfg>(o + 32, acc.Y);
+    store<FqCfg>(o + 64, acc.ZZ);
+    store<FqCfg>(o + 96, acc.ZZZ);
+}
+
+__device__ __forceinline__ void put_be(uint8_t* o, const Fq& a) {
+    const Fq s = from_mont(a);
+    for (int i = 0; i < 32; ++i) o[i] = (uint8_t)(s.v[7 - i / 4] >> (8 * (3 - i % 4)));
+}
+__device__ __forceinline__ void put_le(uint8_t* o, const Fq& a) { store<FqCfg>(o, from_mont(a)); }
+
+// C = L + H + sA + rB1; serialise A | B | C (EIP-197 big-endian, G2 as
+// x.c1 | x.c0 | y.c1 | y.c0) and the raw little-endian affine points.
+__global__ void assemble_kernel(const uint8_t* pts, const uint8_t* scaled, uint8_t* proof256,
+                                uint8_t* raw256) {
+    if (threadIdx.x || blockIdx.x) return;
+    const uint8_t* A = pts;
+    const uint8_t* B2 = pts + 128;
+    const uint8_t* Lp = pts + 256;
+    const uint8_t* Hp = pts + 320;
+    auto xyzz_at = [](const uint8_t* p) {
+        XYZZ<Fq> a;
+        a.X = load<FqCfg>(p);
+        a.Y = load<FqCfg>(p + 32);
+        a.ZZ = load<FqCfg>(p + 64);
+        a.ZZZ = load<FqCfg>(p + 96);
+        return a;
+    };
+    XYZZ<Fq> acc = xyzz_add(xyzz_at(scaled), xyzz_at(scaled + 128));
+    for (const uint8_t* q : {Lp, Hp}) {
+        Fq x = load<FqCfg>(q), y = load<FqCfg>(q + 32);
+        if (!(x.is_zero() && y.is_zero())) acc = xyzz_madd(acc, x, y);
+    }
+    Fq cx = Fq::zero(), cy = Fq::zero();
+    if (!acc.is_inf()) {
+        const Fq t = inv_fast(fmul(acc.ZZ, acc.ZZZ));
+        cx = fmul(acc.X, fmul(t, acc.ZZZ));
+        cy = fmul(acc.Y, fmul(t, acc.ZZ));
+    }
+    const Fq ax = load<FqCfg>(A), ay = load<FqCfg>(A + 32);
+    const Fq bx0 = load<FqCfg>(B2), bx1 = load<FqCfg>(B2 + 32), by0 = load<FqCfg>(B2 + 64),
+             by1 = load<FqCfg>(B2 + 96);
+    put_be(proof256, ax);
+    put_be(proof256 + 32, ay);
+    put_be(proof256 + 64, bx1);
+    put_be(proof256 + 96, bx0);
+    put_be(proof256 + 128, by1);
+    put_be(proof256 + 160, by0);
+    put_be(proof256 + 192, cx);
+    put_be(proof256 + 224, cy);
+    if (raw256) {
+        put_le(raw256, ax);
+        put_le(raw256 + 32, ay);
+        put_le(raw256 + 64, bx0);
+        put_le(raw256 + 96, bx1);
+        put_le(raw256 + 128, by0);
+        put_le(raw256 + 160, by1);
+        put_le(raw256 + 192, cx);
+        put_le(raw256 + 224, cy);
+    }
+}
+
+inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+void g16_chain_consts(uint32_t K, uint8_t* out, cudaStream_t s) {
+    chain_consts_kernel<<<grid(K, 128), 128, 0, s>>>(K, out);
+}
+void g16_setup_consts(uint8_t* c, uint32_t logn, cudaStream_t s) {
+    setup_consts_kernel<<<1, 1, 0, s>>>(c, logn);
+}
+void g16_lagrange(const uint8_t* c, uint64_t m, uint8_t* L, cudaStream_t s) {
+    lagrange_kernel<<<grid(m, 128), 128, 0, s>>>(c, m, L);
+}
+void g16_query_scalars(const G16Dims& d, const uint8_t* L, const uint8_t* c, const uint8_t* cc,
+                       uint8_t* part, uint8_t* su, uint8_t* sv, uint8_t* sl, cudaStream_t s) {
+    constexpr unsigned kParts = 256;
+    one_partials_kernel<<<kParts, 256, 0, s>>>(d, L, cc, part);
+    query_scalars_kernel<<<grid(d.V, 128), 128, 0, s>>>(d, L, c, part, kParts, su, sv, sl);
+}
+void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s) {
+    h_scalars_kernel<<<grid(n, 128), 128, 0, s>>>(c, n, out);
+}
+void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const uint8_t* cc,
+                 uint8_t* z, uint8_t* ea, uint8_t* eb, uint8_t* ec, cudaStream_t s) {
+    witness_kernel<<<grid(d.T, 64), 64, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+}
+void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint8_t* c,
+                   uint64_t n, cudaStream_t s) {
+    pointwise_kernel<<<grid(n, 256), 256, 0, s>>>(ea, eb, ec, c, n);
+}
+void g16_derive_rs(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest, cudaStream_t s) {
+    derive_rs_kernel<<<1, 32, 0, s>>>(pub, T, rs, digest);
+}
+void g16_extras(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp, const uint8_t* rs,
+                cudaStream_t s) {
+    extras_kernel<<<1, 1, 0, s>>>(za, zb, zl, V, Vp, rs);
+}
+void g16_scale(const uint8_t* pts, const uint8_t* rs, uint8_t* out, cudaStream_t s) {
+    scale_kernel<<<1, 32, 0, s>>>(pts, rs, out);
+}
+void g16_assemble(const uint8_t* pts, const uint8_t* scaled, uint8_t* proof, uint8_t* raw,
+                  cudaStream_t s) {
+    assemble_kernel<<<1, 1, 0, s>>>(pts, scaled, proof, raw);
+}
+
+}  // namespace bn
+}  // namespace ace_gpu

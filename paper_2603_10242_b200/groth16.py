@@ -1,0 +1,63 @@
+"""Groth16 per-chunk prover over BN254 (north star) — host API over libacegpu.
+
+Synthetic ZK-ACE stand-in circuit (constraint system in
+oracle/bn254_oracle.h): per tx a private witness w_t (the attest key,
+prover.cpp:181-188) and public input pub_t (the tx's public-inputs digest,
+prover.cpp:74-76), K constraints of a squaring chain. A proving key is built
+once per (T, K) from a trapdoor and stays resident on the device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .bn254 import R
+
+PAPER_T, PAPER_K = 1024, 1400  # 1,024-tx chunks x ~1,400 constraints/tx
+
+
+def deterministic_trapdoor(label: bytes = b"ace-g16-setup-v1", ctx=None) -> np.ndarray:
+    """tau, alpha, beta, gamma, delta = LE(SHA-256(label | i)) mod r (hashed on
+    the GPU) — a synthetic, reproducible ceremony stand-in, never for production."""
+    from .wire import sha256_many
+    digests = sha256_many([label + bytes([i]) for i in range(5)], ctx)
+    vals = [(int.from_bytes(d, "little") % R).to_bytes(32, "little") for d in digests]
+    return np.frombuffer(b"".join(vals), np.uint8).copy()
+
+
+class ProvingKey:
+    def __init__(self, T: int, K: int, trapdoor: np.ndarray | None = None, ctx=None):
+        self.ctx = ctx or N.context()
+        self.T, self.K = T, K
+        self.trapdoor = deterministic_trapdoor(ctx=self.ctx) if trapdoor is None else trapdoor
+        h = C.c_void_p()
+        self.ctx.call("acegpu_g16_setup", T, K, self.trapdoor, C.byref(h))
+        self.h = h
+        V, m, L = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        N.lib().acegpu_g16_shape(self.h, C.byref(V), C.byref(m), C.byref(L))
+        self.variables, self.constraints, self.log_domain = V.value, m.value, L.value
+
+    def prove(self, w: np.ndarray, pub: np.ndarray, rs: np.ndarray | None = None):
+        """-> (proof256 bytes, raw affine points bytes, chunk digest bytes)."""
+        proof = np.zeros(256, np.uint8)
+        raw = np.zeros(256, np.uint8)
+        dig = np.zeros(32, np.uint8)
+        self.ctx.call("acegpu_g16_prove_chunk", self.h, w, pub, rs, proof, raw, dig)
+        return proof.tobytes(), raw.tobytes(), dig.tobytes()
+
+    def prove_dev(self, d_w, d_pub, d_proof, d_raw=None, d_digest=None, d_rs=None, stream=None):
+        self.ctx.call("acegpu_g16_prove_chunk_dev", stream, self.h, d_w, d_pub, d_rs, d_proof,
+                      d_raw, d_digest)
+
+    def close(self):
+        if self.h:
+            N.lib().acegpu_g16_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
