@@ -235,6 +235,20 @@ int acegpu_g16_prove_chunk_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, con
                                const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                                uint8_t* d_raw256, uint8_t* d_digest32);
 
+/* Groth16-mode shard (north-star block path): like acegpu_shard_roots_dev,
+ * but each aligned chunk of T txs (T = txs_per_chunk, a power of two) is one
+ * Groth16 proof over the chunk's witnesses (d_witness256: n x 256-B
+ * build_witness records, prover.cpp:181-188; w = LE(first 32 B) mod r) and
+ * public-input digests; the last chunk of the block is zero-padded. Chunk
+ * roots (289 B: proof | chunk digest | kind Tx) combine with
+ * acegpu_combine_roots_dev under the reference's tree rule. */
+int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
+                               const uint8_t* d_payloads, const uint64_t* d_offs,
+                               const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                               const uint8_t* d_revs, const uint32_t* d_rev_index,
+                               uint8_t* d_codes, const uint8_t* d_witness256,
+                               uint8_t* d_roots289, uint8_t* d_merkle32);
+
 /* Integer-pipe microbenchmarks (roofline denominators for MSM / NTT). */
 int acegpu_imad_peak(acegpu_ctx* ctx, double* imad_per_s);
 int acegpu_bn_mul_rate(acegpu_ctx* ctx, int field, double* muls_per_s);

@@ -74,6 +74,8 @@ _SIGS = {
     "acegpu_g16_shape": (C.c_int, [C.c_void_p, u64p, u64p, C.POINTER(C.c_uint32)]),
     "acegpu_g16_prove_chunk": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
+    "acegpu_g16_shard_roots_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, u64, vp, vp,
+                                             vp, vp, vp, vp]),
     "acegpu_imad_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
     "acegpu_bn_mul_rate": (C.c_int, [ctxp, C.c_int, C.POINTER(C.c_double)]),
 }

@@ -1322,13 +1322,26 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     return ACEGPU_OK;
 }
 
+namespace {
+int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
+                     const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
+                     uint8_t* d_raw256, uint8_t* d_digest32);
+}
+
 extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
                                           const uint8_t* d_w, const uint8_t* d_pub,
                                           const uint8_t* d_rs, uint8_t* d_proof256,
                                           uint8_t* d_raw256, uint8_t* d_digest32) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
-    cudaStream_t s = pick(c, stream);
+    return g16_prove_locked(c, pick(c, stream), g, d_w, d_pub, d_rs, d_proof256, d_raw256,
+                            d_digest32);
+}
+
+namespace {
+int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
+                     const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
+                     uint8_t* d_raw256, uint8_t* d_digest32) {
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     uint8_t* scratch;
     RET(ws(c, kBnScratch, 32 * N, &scratch));
@@ -1369,6 +1382,68 @@ extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g1
     bn::g16_assemble(g->pts, g->scaled, d_proof256, d_raw256, s);
     CKL();
     c->launches += 16 + 5 * 7 + 6;
+    return ACEGPU_OK;
+}
+}  // namespace
+
+// Groth16-mode shard: attestation verdicts + per-tx public-input digests
+// (the leaf kernel), the id_com Merkle tree up to the chunk level (lifted
+// like the mock shard), and one Groth16 proof per chunk of T txs (the last
+// chunk of the block zero-padded). Chunk roots = chunk proofs as mock-tree
+// leaves (proof | chunk digest | kind Tx), so acegpu_combine_roots_dev
+// aggregates them with the reference's tree rule (prover.cpp:106-127).
+extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                          const uint8_t* d_payloads, const uint64_t* d_offs,
+                                          const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                                          const uint8_t* d_revs, const uint32_t* d_rev_index,
+                                          uint8_t* d_codes, const uint8_t* d_witness256,
+                                          uint8_t* d_roots289, uint8_t* d_merkle32) {
+    const uint32_t T = g->d.T;
+    if (T & (T - 1)) return fail(ACEGPU_EINVAL, "g16 shard: txs per chunk must be a power of two");
+    if (n == 0) return fail(ACEGPU_EINVAL, "g16 shard: empty shard");
+    RET(check_n(n));
+    uint32_t log2_chunk = 0;
+    while ((1u << log2_chunk) < T) ++log2_chunk;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    // leaves: verdicts, public-input digests (node records), Merkle leaves
+    TreeResult t;
+    RET(run_tree(c, s, d_payloads, d_offs, d_atts, uint32_t(n), nullptr, d_revs, d_rev_index,
+                 d_codes, true, 0, false, &t));
+    // Merkle levels up to the chunk level (lift the block's short last chunk)
+    const bool lift = n_total > T;
+    uint8_t* min_ = t.merkle;  // kMerkA after zero levels
+    uint8_t* mout = static_cast<uint8_t*>(c->bufs[kMerkB].p);
+    uint32_t cur = uint32_t(n), lv = 0;
+    while (lv < log2_chunk && (cur > 1 || (lift && cur == 1))) {
+        launch_level(nullptr, 0, nullptr, min_, cur, mout, lift, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        std::swap(min_, mout);
+        ++lv;
+    }
+    const uint64_t chunks = (n + T - 1) / T;
+    if (cur != chunks) return fail(ACEGPU_EINVAL, "g16 shard: chunk count mismatch");
+    CK(cudaMemcpyAsync(d_merkle32, min_, 32 * chunks, cudaMemcpyDeviceToDevice, s));
+    // chunk inputs: pub = LE(public_inputs_digest), w = LE(witness[0:32]), zero padded
+    uint8_t *pub, *w, *proof, *node;
+    RET(ws(c, kBnA, 32 * chunks * T, &pub));
+    RET(ws(c, kBnB, 32 * chunks * T, &w));
+    RET(ws(c, kIn2, 256 + 32 + 320, &proof));
+    node = proof + 288;
+    bn::g16_gather32(t.nodes + 256, kNodeBytes, n, chunks * T, pub, s);
+    bn::g16_gather32(d_witness256, 256, n, chunks * T, w, s);
+    CKL();
+    for (uint64_t k = 0; k < chunks; ++k) {
+        RET(g16_prove_locked(c, s, g, w + 32 * T * k, pub + 32 * T * k, nullptr, proof, nullptr,
+                             proof + 256));
+        bn::g16_chunk_node(proof, proof + 256, node, s);
+        launch_pack_nodes(node, 1, d_roots289 + 289 * k, s);
+        CKL();
+        c->launches += 2;
+    }
     return ACEGPU_OK;
 }
 

@@ -362,9 +362,41 @@ __global__ void assemble_kernel(const uint8_t* pts, const uint8_t* scaled, uint8
     }
 }
 
+// dst[i] = src[i*stride .. +32) for i < n; zero for n <= i < n_pad (chunk padding).
+__global__ void gather32_kernel(const uint8_t* src, uint64_t stride, uint64_t n, uint64_t n_pad,
+                                uint8_t* dst) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n_pad) return;
+    uint4* d = reinterpret_cast<uint4*>(dst + 32 * i);
+    if (i < n) {
+        const uint4* q = reinterpret_cast<const uint4*>(src + stride * i);
+        d[0] = q[0];
+        d[1] = q[1];
+    } else {
+        d[0] = d[1] = make_uint4(0, 0, 0, 0);
+    }
+}
+
+// Chunk node record (mock-tree leaf, 320 B): proof bytes | digest | kind = Tx.
+__global__ void chunk_node_kernel(const uint8_t* proof256, const uint8_t* digest32, uint8_t* node) {
+    const int t = threadIdx.x;
+    if (t < 256) node[t] = proof256[t];
+    else if (t < 288) node[t] = digest32[t - 256];
+    else if (t < 320) node[t] = 0;
+}
+
 inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 }  // namespace
+
+void g16_gather32(const uint8_t* src, uint64_t stride, uint64_t n, uint64_t n_pad, uint8_t* dst,
+                  cudaStream_t s) {
+    if (n_pad) gather32_kernel<<<grid(n_pad, 256), 256, 0, s>>>(src, stride, n, n_pad, dst);
+}
+void g16_chunk_node(const uint8_t* proof256, const uint8_t* digest32, uint8_t* node,
+                    cudaStream_t s) {
+    chunk_node_kernel<<<1, 320, 0, s>>>(proof256, digest32, node);
+}
 
 void g16_chain_consts(uint32_t K, uint8_t* out, cudaStream_t s) {
     chain_consts_kernel<<<grid(K, 128), 128, 0, s>>>(K, out);

@@ -51,6 +51,7 @@ class DeviceBlock:
     n: int
     revs: "object" = None       # torch.uint8 [32*users]
     rev_index: "object" = None  # torch.int32 [n]
+    witnesses: "object" = None  # torch.uint8 [n*256] (Groth16 mode)
 
     @staticmethod
     def upload(fb, start: int = 0, count: int | None = None, revs=None, rev_index=None,
@@ -115,6 +116,30 @@ class GpuBackend:
         return out[:289], out[304:304 + 328]
 
 
+class G16Backend(GpuBackend):
+    """Groth16 mode: each aligned chunk of T = pk.T txs is one Groth16 proof
+    (acegpu_g16_shard_roots_dev); the tree above the chunks and the FC are
+    the reference's rules (acegpu_combine_roots_dev). `witnesses` is the
+    rank's n x 256-B witness tensor (build_witness layout)."""
+
+    def __init__(self, pk, ctx: N.Context | None = None):
+        super().__init__(ctx or pk.ctx)
+        self.pk = pk
+
+    def shard_roots(self, db: DeviceBlock, n_total: int, log2_chunk: int, codes=None):
+        import torch
+        assert (1 << log2_chunk) == self.pk.T, "chunk size must equal the circuit's txs/chunk"
+        c = n_chunks(db.n, log2_chunk)
+        roots = torch.empty(max(c, 1) * 289, dtype=torch.uint8, device=db.atts.device)
+        merk = torch.empty(max(c, 1) * 32, dtype=torch.uint8, device=db.atts.device)
+        if db.n:
+            self.ctx.call("acegpu_g16_shard_roots_dev", _stream(), self.pk.h, _ptr(db.payloads),
+                          _ptr(db.offs), _ptr(db.atts), db.n, n_total, _ptr(db.revs),
+                          _ptr(db.rev_index), _ptr(codes), _ptr(db.witnesses), _ptr(roots),
+                          _ptr(merk))
+        return roots[:c * 289], merk[:c * 32]
+
+
 def gather_roots(roots, merk, counts: list[int], group=None):
     """All-gather each rank's chunk roots (padded to the largest rank) and
     return them concatenated in rank order."""
@@ -149,15 +174,20 @@ def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
     return backend.combine(roots, merk, sum(counts), n_total, local.header)
 
 
-def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None):
+def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None, pk=None,
+                                 witnesses=None):
     """Emulates `world` ranks one after another on one GPU (no collective):
-    used to check shard/combine bit-exactness with a single device."""
+    used to check shard/combine bit-exactness with a single device.
+    With a Groth16 proving key `pk`, chunks are Groth16 proofs."""
     import torch
-    be = GpuBackend(ctx)
+    be = G16Backend(pk, ctx) if pk is not None else GpuBackend(ctx)
     parts = partition(fb.n, world, log2_chunk)
     rs, ms = [], []
     for s, c in parts:
         db = DeviceBlock.upload(fb, s, c)
+        if witnesses is not None:
+            db.witnesses = torch.from_numpy(
+                np.ascontiguousarray(witnesses[256 * s:256 * (s + c)])).to(db.atts.device)
         r, m = be.shard_roots(db, fb.n, log2_chunk)
         rs.append(r)
         ms.append(m)

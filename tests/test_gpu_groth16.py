@@ -124,3 +124,62 @@ def test_groth16_paper_size_chunk(ctx):
         assert raw == A + B + Cc
     finally:
         pk.close()
+
+
+@pytest.mark.parametrize("n,world", [(1, 1), (11, 1), (11, 2), (16, 3), (37, 4)])
+def test_groth16_block_shards(ctx, n, world):
+    """Groth16 mode end to end: attestation + per-tx public-input digests ->
+    one Groth16 proof per aligned 4-tx chunk (last chunk zero-padded) ->
+    reference tree rule over chunk proofs -> FC; ranks emulated in sequence.
+    Each chunk proof is checked against the trapdoor oracle; the root and FC
+    against the oracle's aggregate_tree / merkle_root."""
+    from paper_2603_10242_b200 import groth16, shard, wire
+    T, K = 4, 3
+    rng = random.Random(n * 10 + world)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        fb = O.multi_user_block(n, 3)
+        # witnesses: build_witness(attest_key, tx_hash) (prover.cpp:181-188)
+        wit = b""
+        for i in range(n):
+            att = fb.att(i)
+            u = int(fb.rev_index[i])
+            key = O.derive_attest_key(fb.revs[32 * u:32 * u + 32].tobytes(), att[64:72])
+            out = O.buf(256)
+            O.oracle().or_build_witness(O.ptr(key), O.ptr(att[:32]), out)
+            wit += bytes(out)
+        witnesses = np.frombuffer(wit, np.uint8).copy()
+        wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+        proof, fc = shard.prove_sharded_single_process(wfb, world, 2, ctx, pk=pk, witnesses=witnesses)
+        # expected: per-chunk proofs from the chunk prover on the same inputs
+        digests = []
+        for i in range(n):
+            p = O.buf(289)
+            O.oracle().or_prove_tx(O.ptr(fb.payload(i)), C.c_uint64(len(fb.payload(i))),
+                                   O.ptr(fb.att(i)), p)
+            digests.append(bytes(p)[256:288])
+        nodes = b""
+        for c0 in range(0, n, T):
+            pubs = digests[c0:c0 + T] + [bytes(32)] * (T - len(digests[c0:c0 + T]))
+            ws = [wit[256 * i:256 * i + 32] for i in range(c0, min(n, c0 + T))]
+            ws += [bytes(32)] * (T - len(ws))
+            pa = np.frombuffer(b"".join(pubs), np.uint8).copy()
+            wa = np.frombuffer(b"".join(ws), np.uint8).copy()
+            pr, raw, dg = pk.prove(wa, pa)
+            # the chunk proof verifies (trapdoor oracle), with the derived r, s
+            tail = pubs[0] + pubs[-1] + T.to_bytes(4, "big")
+            r = int.from_bytes(hashlib.sha256(b"ace-g16-r-v1" + tail).digest(), "little") % R
+            s = int.from_bytes(hashlib.sha256(b"ace-g16-s-v1" + tail).digest(), "little") % R
+            wred = arr([int.from_bytes(x, "little") % R for x in ws])
+            pred = arr([int.from_bytes(x, "little") % R for x in pubs])
+            assert raw == b"".join(expected_points(T, K, wred, pred, trap, arr([r, s])))
+            nodes += pr + dg + b"\0"
+        out = O.buf(289)
+        lv, pp = C.c_uint64(), C.c_uint64()
+        O.oracle().or_aggregate_tree(O.ptr(nodes), C.c_uint64(len(nodes) // 289), out,
+                                     C.byref(lv), C.byref(pp))
+        assert proof == bytes(out)
+        assert fc == O.oracle_build_fc(fb, bytes(out))
+    finally:
+        pk.close()
