@@ -30,6 +30,7 @@ _SIGS = {
     "acegpu_launch_count": (C.c_uint64, [ctxp]),
     "acegpu_set_phase_timing": (C.c_int, [ctxp, C.c_int]),
     "acegpu_phase_times": (C.c_int, [ctxp, C.POINTER(C.c_float)]),
+    "acegpu_set_segmented": (C.c_int, [ctxp, C.c_int]),
     "acegpu_host_alloc": (C.c_void_p, [C.c_size_t]),
     "acegpu_host_free": (None, [C.c_void_p]),
     "acegpu_sha256_varlen": (C.c_int, [ctxp, vp, vp, u64, vp]),

@@ -55,7 +55,8 @@ int fail(int code, const std::string& msg) {
 
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
-    kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kNumSlots
+    kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kSegRoots, kSegMerk,
+    kNumSlots
 };
 
 struct DevBuf {
@@ -85,6 +86,10 @@ struct acegpu_ctx {
     // BN254: NTT twiddle tables per log-size, MSM scratch.
     ace_gpu::bn::NttTables ntt[ace_gpu::bn::kNttMaxLog + 1];
     ace_gpu::bn::MsmScratch msm;
+    // Segmented block pipeline: sub-contexts (own stream + workspace).
+    std::vector<acegpu_ctx*> subs;
+    cudaEvent_t seg_ev[9] = {};
+    bool force_single = false;  // acegpu_set_segmented(ctx, 0)
 };
 
 // A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
@@ -239,6 +244,19 @@ int block_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const
     return ACEGPU_OK;
 }
 
+struct HostBlock;
+int segmented_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
+                       const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                       const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
+                       uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock* host,
+                       const uint32_t* host_rix);
+
+// Large blocks take the segmented pipeline, except under phase timing (whose
+// leaves | levels | finalize split needs the single-pass pipeline).
+inline bool use_segments(const acegpu_ctx* c, uint64_t n) {
+    return !c->timing && !c->force_single && n >= (2ull << 13);
+}
+
 struct HostBlock {
     const uint8_t* payloads;
     const uint64_t* offs;
@@ -304,6 +322,9 @@ void acegpu_destroy(acegpu_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& t : c->ntt) t.release();
     c->msm.release();
+    for (auto* sub : c->subs) acegpu_destroy(sub);
+    for (auto& e : c->seg_ev)
+        if (e) cudaEventDestroy(e);
     for (auto& b : c->bufs)
         if (b.p) cudaFree(b.p);
     cudaStreamDestroy(c->stream);
@@ -311,6 +332,12 @@ void acegpu_destroy(acegpu_ctx* c) {
 }
 
 uint64_t acegpu_launch_count(const acegpu_ctx* c) { return c ? c->launches.load() : 0; }
+
+int acegpu_set_segmented(acegpu_ctx* c, int enable) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->force_single = !enable;
+    return ACEGPU_OK;
+}
 
 int acegpu_set_phase_timing(acegpu_ctx* c, int enable) {
     std::lock_guard<std::mutex> lk(c->mu);
@@ -527,15 +554,31 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
     uint8_t *dp, *da, *dh, *dout, *dr = nullptr, *dc = nullptr;
     uint64_t* doff;
     uint32_t* dri = nullptr;
-    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
     RET(h2d_t(c, kHeader, header, 256, s, &dh));
-    if (codes && n) {
-        RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
-        RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
-        RET(ws(c, kCodes, n, &dc));
-    }
     RET(ws(c, kOut, 289 + 328 + 16, &dout));
-    RET(block_pipeline(c, s, dp, doff, da, uint32_t(n), dh, dr, dri, dc, dout, dout + 304));
+    if (use_segments(c, n)) {
+        // offsets + REV table first; payload/attestation slices are copied per
+        // segment on the sub-streams, overlapping the compute of earlier ones
+        const HostBlock hb{payloads, offs, atts, n};
+        RET(ws(c, kPayloads, offs[n] + 16, &dp));
+        RET(ws(c, kAtts, 104 * n + 16, &da));
+        RET(h2d_t(c, kOffs, offs, 8 * (n + 1), s, &doff));
+        if (codes) {
+            RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+            RET(ws(c, kRevIdx, 4 * n, &dri));
+            RET(ws(c, kCodes, n, &dc));
+        }
+        RET(segmented_pipeline(c, s, dp, doff, da, n, dh, dr, dri, dc, dout, dout + 304, &hb,
+                               codes ? rev_index : nullptr));
+    } else {
+        RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+        if (codes && n) {
+            RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+            RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
+            RET(ws(c, kCodes, n, &dc));
+        }
+        RET(block_pipeline(c, s, dp, doff, da, uint32_t(n), dh, dr, dri, dc, dout, dout + 304));
+    }
     if (dc) CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
     if (out289) CK(cudaMemcpyAsync(out289, dout, 289, cudaMemcpyDeviceToHost, s));
     if (out328) CK(cudaMemcpyAsync(out328, dout + 304, 328, cudaMemcpyDeviceToHost, s));
@@ -553,6 +596,9 @@ int acegpu_attest_prove_certify_dev(acegpu_ctx* c, void* stream, const uint8_t* 
     RET(check_n(n));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
+    if (use_segments(c, n))
+        return segmented_pipeline(c, pick(c, stream), payloads, offs, atts, n, header, revs,
+                                  rev_index, codes, out289, out328, nullptr, nullptr);
     return block_pipeline(c, pick(c, stream), payloads, offs, atts, uint32_t(n), header, revs,
                           rev_index, n ? codes : nullptr, out289, out328);
 }
@@ -642,6 +688,20 @@ int acegpu_block_hash(acegpu_ctx* c, const uint8_t* header, uint8_t* out32) {
 }
 
 // ------------------------------------------------------------- sharding
+}  // extern "C"
+
+namespace {
+int shard_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
+               const uint8_t* atts, uint64_t n, uint64_t n_total, uint32_t log2_chunk,
+               const uint8_t* revs, const uint32_t* rev_index, uint8_t* codes, uint8_t* roots289,
+               uint8_t* merkle32);
+int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const uint8_t* merkle32,
+                 uint64_t n_chunks, uint64_t n_total, const uint8_t* header, uint8_t* out289,
+                 uint8_t* out328);
+}  // namespace
+
+extern "C" {
+
 int acegpu_shard_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
                            const uint64_t* offs, const uint8_t* atts, uint64_t n, uint64_t n_total,
                            uint32_t log2_chunk, const uint8_t* revs, const uint32_t* rev_index,
@@ -650,7 +710,27 @@ int acegpu_shard_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
     if (n == 0 || log2_chunk > 31) return fail(ACEGPU_EINVAL, "empty shard or chunk too large");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    cudaStream_t s = pick(c, stream);
+    return shard_impl(c, pick(c, stream), payloads, offs, atts, n, n_total, log2_chunk, revs,
+                      rev_index, codes, roots289, merkle32);
+}
+
+int acegpu_combine_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* roots289,
+                             const uint8_t* merkle32, uint64_t n_chunks, uint64_t n_total,
+                             const uint8_t* header, uint8_t* out289, uint8_t* out328) {
+    RET(check_n(n_chunks));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    return combine_impl(c, pick(c, stream), roots289, merkle32, n_chunks, n_total, header, out289,
+                        out328);
+}
+
+}  // extern "C"
+
+namespace {
+int shard_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
+               const uint8_t* atts, uint64_t n, uint64_t n_total, uint32_t log2_chunk,
+               const uint8_t* revs, const uint32_t* rev_index, uint8_t* codes, uint8_t* roots289,
+               uint8_t* merkle32) {
     const bool lift = n_total > (1ull << log2_chunk);
     TreeResult t;
     RET(run_tree(c, s, payloads, offs, atts, uint32_t(n), nullptr, revs, rev_index, codes, true,
@@ -664,13 +744,9 @@ int acegpu_shard_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
     return ACEGPU_OK;
 }
 
-int acegpu_combine_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* roots289,
-                             const uint8_t* merkle32, uint64_t n_chunks, uint64_t n_total,
-                             const uint8_t* header, uint8_t* out289, uint8_t* out328) {
-    RET(check_n(n_chunks));
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard g(c->device);
-    cudaStream_t s = pick(c, stream);
+int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const uint8_t* merkle32,
+                 uint64_t n_chunks, uint64_t n_total, const uint8_t* header, uint8_t* out289,
+                 uint8_t* out328) {
     uint8_t *na, *nb, *ma, *mb, *bh;
     RET(ws(c, kBlockHash, 32, &bh));
     launch_sha256_strided(header, 256, 256, 1, bh, s);
@@ -704,6 +780,69 @@ int acegpu_combine_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* roots28
     c->launches++;
     return ACEGPU_OK;
 }
+
+// Segmented single-GPU block pipeline: the block is cut into 2^kSegLog-tx
+// aligned segments (the shard rule of SURVEY §8e, within one GPU); each
+// segment's leaves + 13 lower levels run on one of kSubs sub-contexts
+// (own stream + workspace) so that the latency-bound narrow levels of
+// different segments overlap each other — and, for host inputs, the H2D copy
+// of later segments. The segment roots are combined on the caller's stream.
+constexpr uint32_t kSegLog = 13;
+constexpr int kSubs = 8;
+
+int ensure_subs(acegpu_ctx* c) {
+    while ((int)c->subs.size() < kSubs) {
+        acegpu_ctx* sub = nullptr;
+        RET(acegpu_create(c->device, &sub));
+        c->subs.push_back(sub);
+    }
+    if (!c->seg_ev[0])
+        for (auto& e : c->seg_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    return ACEGPU_OK;
+}
+
+int segmented_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
+                       const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                       const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
+                       uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock* host,
+                       const uint32_t* host_rix) {
+    RET(ensure_subs(c));
+    const uint64_t seg = 1ull << kSegLog, S = (n + seg - 1) / seg;
+    uint8_t *roots, *merk;
+    RET(ws(c, kSegRoots, 289 * S + 32, &roots));
+    RET(ws(c, kSegMerk, 32 * S + 32, &merk));
+    CK(cudaEventRecord(c->seg_ev[kSubs], s));
+    for (int k = 0; k < kSubs; ++k) CK(cudaStreamWaitEvent(c->subs[k]->stream, c->seg_ev[kSubs], 0));
+    for (uint64_t j = 0; j < S; ++j) {
+        acegpu_ctx* sub = c->subs[j % kSubs];
+        cudaStream_t ss = sub->stream;
+        const uint64_t a = j * seg, cnt = std::min(seg, n - a);
+        if (host) {  // this segment's slice host -> device on the sub stream
+            const uint64_t b0 = host->offs[a], b1 = host->offs[a + cnt];
+            CK(cudaMemcpyAsync(const_cast<uint8_t*>(payloads) + b0, host->payloads + b0, b1 - b0,
+                               cudaMemcpyHostToDevice, ss));
+            CK(cudaMemcpyAsync(const_cast<uint8_t*>(atts) + 104 * a, host->atts + 104 * a,
+                               104 * cnt, cudaMemcpyHostToDevice, ss));
+            if (host_rix)
+                CK(cudaMemcpyAsync(const_cast<uint32_t*>(rev_index) + a, host_rix + a, 4 * cnt,
+                                   cudaMemcpyHostToDevice, ss));
+        }
+        RET(shard_impl(sub, ss, payloads, offs + a, atts + 104 * a, cnt, n, kSegLog, revs,
+                       rev_index ? rev_index + a : nullptr, codes ? codes + a : nullptr,
+                       roots + 289 * j, merk + 32 * j));
+        c->launches += 1;
+    }
+    for (int k = 0; k < kSubs && k < (int)S; ++k) {
+        CK(cudaEventRecord(c->seg_ev[k], c->subs[k]->stream));
+        CK(cudaStreamWaitEvent(s, c->seg_ev[k], 0));
+    }
+    for (auto* sub : c->subs) c->launches += sub->launches.exchange(0);
+    return combine_impl(c, s, roots, merk, S, n, header, out289, out328);
+}
+
+}  // namespace
+
+extern "C" {
 
 // ------------------------------------------------------------ attestation
 int acegpu_attest_verify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
