@@ -87,8 +87,8 @@ struct acegpu_ctx {
     ace_gpu::bn::NttTables ntt[ace_gpu::bn::kNttMaxLog + 1];
     ace_gpu::bn::MsmScratch msm;
     // Segmented block pipeline: sub-contexts (own stream + workspace).
-    std::vector<acegpu_ctx*> subs;
-    cudaEvent_t seg_ev[9] = {};
+    cudaStream_t copy_stream = nullptr;  // overlapped host-input pipeline
+    std::vector<cudaEvent_t> seg_events;
     bool force_single = false;  // acegpu_set_segmented(ctx, 0)
 };
 
@@ -174,7 +174,7 @@ struct TreeResult {
 int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
              const uint8_t* atts, uint32_t n, const uint8_t* header, const uint8_t* revs,
              const uint32_t* rev_index, uint8_t* codes, bool prove, uint32_t max_levels,
-             bool lift, TreeResult* r) {
+             bool lift, TreeResult* r, bool skip_leaves = false) {
     uint8_t *na = nullptr, *nb = nullptr, *ma = nullptr, *mb = nullptr, *bh = nullptr;
     const size_t half = n / 2 + 1;
     if (prove) {
@@ -197,7 +197,7 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
     a.header = header;
     a.block_hash = bh;
     if (c->timing) CK(cudaEventRecord(c->ev[0], s));
-    if (n || header) {
+    if ((n || header) && !skip_leaves) {
         launch_leaves(a, s);
         CKL();
         c->launches++;
@@ -245,11 +245,11 @@ int block_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const
 }
 
 struct HostBlock;
-int segmented_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
-                       const uint64_t* offs, const uint8_t* atts, uint64_t n,
-                       const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
-                       uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock* host,
-                       const uint32_t* host_rix);
+int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
+                        const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                        const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
+                        uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock& host,
+                        const uint32_t* host_rix);
 
 // Large blocks take the segmented pipeline, except under phase timing (whose
 // leaves | levels | finalize split needs the single-pass pipeline).
@@ -322,9 +322,8 @@ void acegpu_destroy(acegpu_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& t : c->ntt) t.release();
     c->msm.release();
-    for (auto* sub : c->subs) acegpu_destroy(sub);
-    for (auto& e : c->seg_ev)
-        if (e) cudaEventDestroy(e);
+    for (auto& e : c->seg_events) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (auto& b : c->bufs)
         if (b.p) cudaFree(b.p);
     cudaStreamDestroy(c->stream);
@@ -568,8 +567,8 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
             RET(ws(c, kRevIdx, 4 * n, &dri));
             RET(ws(c, kCodes, n, &dc));
         }
-        RET(segmented_pipeline(c, s, dp, doff, da, n, dh, dr, dri, dc, dout, dout + 304, &hb,
-                               codes ? rev_index : nullptr));
+        RET(overlapped_pipeline(c, s, dp, doff, da, n, dh, dr, dri, dc, dout, dout + 304, hb,
+                                codes ? rev_index : nullptr));
     } else {
         RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
         if (codes && n) {
@@ -596,9 +595,6 @@ int acegpu_attest_prove_certify_dev(acegpu_ctx* c, void* stream, const uint8_t* 
     RET(check_n(n));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    if (use_segments(c, n))
-        return segmented_pipeline(c, pick(c, stream), payloads, offs, atts, n, header, revs,
-                                  rev_index, codes, out289, out328, nullptr, nullptr);
     return block_pipeline(c, pick(c, stream), payloads, offs, atts, uint32_t(n), header, revs,
                           rev_index, n ? codes : nullptr, out289, out328);
 }
@@ -781,63 +777,73 @@ int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const u
     return ACEGPU_OK;
 }
 
-// Segmented single-GPU block pipeline: the block is cut into 2^kSegLog-tx
-// aligned segments (the shard rule of SURVEY §8e, within one GPU); each
-// segment's leaves + 13 lower levels run on one of kSubs sub-contexts
-// (own stream + workspace) so that the latency-bound narrow levels of
-// different segments overlap each other — and, for host inputs, the H2D copy
-// of later segments. The segment roots are combined on the caller's stream.
+// Host-input block pipeline with the H2D copy overlapped: the payload,
+// attestation and REV-index slices of 2^kSegLog-tx segments are copied on a
+// copy stream while the leaf kernel of earlier segments runs on the compute
+// stream; the tree levels and the FC then follow as in block_pipeline.
 constexpr uint32_t kSegLog = 13;
-constexpr int kSubs = 8;
 
-int ensure_subs(acegpu_ctx* c) {
-    while ((int)c->subs.size() < kSubs) {
-        acegpu_ctx* sub = nullptr;
-        RET(acegpu_create(c->device, &sub));
-        c->subs.push_back(sub);
+int ensure_copy(acegpu_ctx* c, size_t nev) {
+    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    while (c->seg_events.size() < nev) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->seg_events.push_back(e);
     }
-    if (!c->seg_ev[0])
-        for (auto& e : c->seg_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     return ACEGPU_OK;
 }
 
-int segmented_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
-                       const uint64_t* offs, const uint8_t* atts, uint64_t n,
-                       const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
-                       uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock* host,
-                       const uint32_t* host_rix) {
-    RET(ensure_subs(c));
+int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
+                        const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                        const uint8_t* header, const uint8_t* revs, const uint32_t* rev_index,
+                        uint8_t* codes, uint8_t* out289, uint8_t* out328, const HostBlock& host,
+                        const uint32_t* host_rix) {
     const uint64_t seg = 1ull << kSegLog, S = (n + seg - 1) / seg;
-    uint8_t *roots, *merk;
-    RET(ws(c, kSegRoots, 289 * S + 32, &roots));
-    RET(ws(c, kSegMerk, 32 * S + 32, &merk));
-    CK(cudaEventRecord(c->seg_ev[kSubs], s));
-    for (int k = 0; k < kSubs; ++k) CK(cudaStreamWaitEvent(c->subs[k]->stream, c->seg_ev[kSubs], 0));
+    RET(ensure_copy(c, S + 1));
+    uint8_t *na, *nb, *ma, *mb, *bh;
+    RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &na));
+    RET(ws(c, kNodesB, size_t(kNodeBytes) * (n / 2 + 1), &nb));
+    RET(ws(c, kMerkA, 32ull * n, &ma));
+    RET(ws(c, kMerkB, 32ull * (n / 2 + 1), &mb));
+    RET(ws(c, kBlockHash, 32, &bh));
+    // the copy stream starts after what is already enqueued on s (offsets, REVs, header)
+    CK(cudaEventRecord(c->seg_events[S], s));
+    CK(cudaStreamWaitEvent(c->copy_stream, c->seg_events[S], 0));
     for (uint64_t j = 0; j < S; ++j) {
-        acegpu_ctx* sub = c->subs[j % kSubs];
-        cudaStream_t ss = sub->stream;
         const uint64_t a = j * seg, cnt = std::min(seg, n - a);
-        if (host) {  // this segment's slice host -> device on the sub stream
-            const uint64_t b0 = host->offs[a], b1 = host->offs[a + cnt];
-            CK(cudaMemcpyAsync(const_cast<uint8_t*>(payloads) + b0, host->payloads + b0, b1 - b0,
-                               cudaMemcpyHostToDevice, ss));
-            CK(cudaMemcpyAsync(const_cast<uint8_t*>(atts) + 104 * a, host->atts + 104 * a,
-                               104 * cnt, cudaMemcpyHostToDevice, ss));
-            if (host_rix)
-                CK(cudaMemcpyAsync(const_cast<uint32_t*>(rev_index) + a, host_rix + a, 4 * cnt,
-                                   cudaMemcpyHostToDevice, ss));
-        }
-        RET(shard_impl(sub, ss, payloads, offs + a, atts + 104 * a, cnt, n, kSegLog, revs,
-                       rev_index ? rev_index + a : nullptr, codes ? codes + a : nullptr,
-                       roots + 289 * j, merk + 32 * j));
-        c->launches += 1;
+        const uint64_t b0 = host.offs[a], b1 = host.offs[a + cnt];
+        CK(cudaMemcpyAsync(const_cast<uint8_t*>(payloads) + b0, host.payloads + b0, b1 - b0,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(const_cast<uint8_t*>(atts) + 104 * a, host.atts + 104 * a, 104 * cnt,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        if (host_rix)
+            CK(cudaMemcpyAsync(const_cast<uint32_t*>(rev_index) + a, host_rix + a, 4 * cnt,
+                               cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaEventRecord(c->seg_events[j], c->copy_stream));
+        CK(cudaStreamWaitEvent(s, c->seg_events[j], 0));
+        LeafArgs la{};
+        la.payloads = payloads;
+        la.offs = offs + a;
+        la.atts = atts + 104 * a;
+        la.n = uint32_t(cnt);
+        la.revs = revs;
+        la.rev_index = rev_index ? rev_index + a : nullptr;
+        la.codes = codes ? codes + a : nullptr;
+        la.nodes = na + size_t(kNodeBytes) * a;
+        la.merkle = ma + 32 * a;
+        la.header = j == 0 ? header : nullptr;
+        la.block_hash = bh;
+        launch_leaves(la, s);
+        CKL();
+        c->launches++;
     }
-    for (int k = 0; k < kSubs && k < (int)S; ++k) {
-        CK(cudaEventRecord(c->seg_ev[k], c->subs[k]->stream));
-        CK(cudaStreamWaitEvent(s, c->seg_ev[k], 0));
-    }
-    for (auto* sub : c->subs) c->launches += sub->launches.exchange(0);
-    return combine_impl(c, s, roots, merk, S, n, header, out289, out328);
+    TreeResult t;
+    RET(run_tree(c, s, payloads, offs, atts, uint32_t(n), header, revs, rev_index, codes, true, 64,
+                 false, &t, /*skip_leaves=*/true));
+    launch_finalize(t.nodes, t.merkle, header, t.bh, false, out289, out328, s);
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
 }
 
 }  // namespace
