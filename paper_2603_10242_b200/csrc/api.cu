@@ -89,7 +89,7 @@ struct acegpu_ctx {
     // Segmented block pipeline: sub-contexts (own stream + workspace).
     cudaStream_t copy_stream = nullptr;  // overlapped host-input pipeline
     std::vector<cudaEvent_t> seg_events;
-    bool force_single = false;  // acegpu_set_segmented(ctx, 0)
+    bool force_single = true;  // overlapped pipeline off unless acegpu_set_segmented(ctx, 1)
 };
 
 // A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
