@@ -195,6 +195,59 @@ __global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restri
         const uint32_t g = blockIdx.x * kThreads + threadIdx.x;
         const uint32_t t = g / G, lane = g % G;
         const uint32_t p = nn / 2;
+        if constexpr (G >= 8) {
+            // Latency path: the group's lanes precompute the W+K schedules of
+            // the 8 data blocks in parallel (smem), then every lane runs only
+            // the rounds of the 9-block chain; the padding block's schedule is
+            // a compile-time constant. Bank layout: block stride 65 words,
+            // group stride 520 (= 8 mod 32) -> conflict-free.
+            __shared__ uint32_t wk_sm[(kThreads / G) * 520];
+            uint32_t* wk = wk_sm + (threadIdx.x / G) * 520;
+            if (t < p) {
+                const uint8_t* a = nin + static_cast<uint64_t>(kNodeBytes) * (2 * t);
+#pragma unroll 1
+                for (uint32_t blk = lane; blk < 8; blk += G) {
+                    const uint4* q = reinterpret_cast<const uint4*>((blk < 4 ? a : a + kNodeBytes) + 64 * (blk & 3));
+                    uint32_t w[16];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint4 v = q[k];
+                        w[4 * k] = bswap32(v.x);
+                        w[4 * k + 1] = bswap32(v.y);
+                        w[4 * k + 2] = bswap32(v.z);
+                        w[4 * k + 3] = bswap32(v.w);
+                    }
+                    sha256_schedule_wk(w, wk + 65 * blk);
+                }
+            }
+            __syncwarp();
+            if (t < p) {
+                uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
+                uint32_t d[8], seed[8];
+                sha256_init(d);
+#pragma unroll 1
+                for (int blk = 0; blk < 8; ++blk) {
+                    const uint32_t* wb = wk + 65 * blk;
+                    sha256_rounds(d, [wb](int i) { return wb[i]; });
+                }
+                constexpr Wk64 kPad = pad_block_wk(512 * 8);
+                sha256_rounds(d, [](int i) { return kPad.v[i]; });
+                expand_seed(1, d, seed);
+#pragma unroll 1
+                for (uint32_t c = lane; c < 8; c += G) {
+                    uint32_t o[8];
+                    expand_block(seed, c, o);
+                    store_digest(out + 32 * c, o);
+                }
+                if (lane == 0) write_node_tail(out, d, 1);
+            } else if (t == p && (nn & 1) && lane == 0) {
+                const uint4* s = reinterpret_cast<const uint4*>(nin + static_cast<uint64_t>(kNodeBytes) * (nn - 1));
+                uint4* dd = reinterpret_cast<uint4*>(nout + static_cast<uint64_t>(kNodeBytes) * p);
+#pragma unroll
+                for (int k = 0; k < kNodeBytes / 16; ++k) dd[k] = s[k];
+            }
+            return;
+        }
         if (t < p) {
             const uint8_t* a = nin + static_cast<uint64_t>(kNodeBytes) * (2 * t);
             uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;

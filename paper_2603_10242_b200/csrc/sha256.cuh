@@ -69,6 +69,76 @@ __device__ __forceinline__ void sha256_compress(uint32_t s[8], uint32_t w[16]) {
     s[4] += e; s[5] += f; s[6] += g; s[7] += h;
 }
 
+// ---- split compression: message schedule (W[i] + K[i]) and rounds ---------
+// Used where a compression's latency, not its issue cost, matters: sibling
+// lanes precompute the schedules of independent blocks so that the serial
+// chain only runs the rounds.
+__device__ __forceinline__ void sha256_schedule_wk(const uint32_t w_in[16], uint32_t* wk,
+                                                   int stride = 1) {
+    constexpr uint32_t K[64] = ACE_K256;
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) w[i] = w_in[i];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        uint32_t wi;
+        if (i < 16) {
+            wi = w[i];
+        } else {
+            uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
+            uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+            uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+            wi = w[i & 15] = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
+        }
+        wk[i * stride] = wi + K[i];
+    }
+}
+
+// Rounds only, W[i] + K[i] supplied by `wk(i)`.
+template <class WK>
+__device__ __forceinline__ void sha256_rounds(uint32_t s[8], WK wk) {
+    uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+    for (int i = 0; i < 64; ++i) {
+        uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+        uint32_t ch = (e & f) ^ (~e & g);
+        uint32_t t1 = h + S1 + ch + wk(i);
+        uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+        uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        h = g;
+        g = f;
+        f = e;
+        e = d + t1;
+        d = c;
+        c = b;
+        b = a;
+        a = t1 + S0 + mj;
+    }
+    s[0] += a; s[1] += b; s[2] += c; s[3] += d;
+    s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+// Compile-time schedule (W + K) of the constant final padding block of a
+// message of `bitlen` bits that is a multiple of 512 (0x80, zeros, length).
+struct Wk64 {
+    uint32_t v[64];
+};
+__host__ __device__ constexpr uint32_t ror_c(uint32_t x, int n) { return (x >> n) | (x << (32 - n)); }
+__host__ __device__ constexpr Wk64 pad_block_wk(uint32_t bitlen) {
+    constexpr uint32_t K[64] = ACE_K256;
+    uint32_t w[64] = {};
+    w[0] = 0x80000000u;
+    w[15] = bitlen;
+    for (int i = 16; i < 64; ++i) {
+        const uint32_t s0 = ror_c(w[i - 15], 7) ^ ror_c(w[i - 15], 18) ^ (w[i - 15] >> 3);
+        const uint32_t s1 = ror_c(w[i - 2], 17) ^ ror_c(w[i - 2], 19) ^ (w[i - 2] >> 10);
+        w[i] = w[i - 16] + s0 + w[i - 7] + s1;
+    }
+    Wk64 r{};
+    for (int i = 0; i < 64; ++i) r.v[i] = w[i] + K[i];
+    return r;
+}
+
 // SHA-256 of `len` bytes starting at byte `start` of a 4-byte-aligned buffer
 // (global or shared; generic addressing). Reads only aligned words that hold
 // message bytes, so no padding of the buffer is required. Handles any length
