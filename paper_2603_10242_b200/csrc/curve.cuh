@@ -28,16 +28,30 @@ __device__ __forceinline__ void fset_one(Fq& a) { a = Fq::one(); }
 __device__ __forceinline__ void fset_zero(Fq& a) { a = Fq::zero(); }
 __device__ __forceinline__ bool feq(const Fq& a, const Fq& b) { return a == b; }
 
-__device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
-    Fq t0 = fq_mul_call(a.c0, b.c0), t1 = fq_mul_call(a.c1, b.c1);
-    Fq t2 = fq_mul_call(add(a.c0, a.c1), add(b.c0, b.c1));
+// Fq2 products as one out-of-line unit whose three (two) independent Fq
+// multiplications are inlined, so the scheduler can interleave them (ILP 3).
+static __device__ __noinline__ Fq2 fq2_mul_call(const Fq2 a, const Fq2 b) {
+    Fq t0 = mul(a.c0, b.c0), t1 = mul(a.c1, b.c1);
+    Fq t2 = mul(add(a.c0, a.c1), add(b.c0, b.c1));
     return {sub(t0, t1), sub(sub(t2, t0), t1)};
 }
-__device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
+static __device__ __noinline__ Fq2 fq2_sqr_call(const Fq2 a) {
     // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u
-    Fq t = fq_mul_call(a.c0, a.c1);
-    return {fq_mul_call(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
+    Fq t = mul(a.c0, a.c1);
+    return {mul(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
 }
+__device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) { return fq2_mul_call(a, b); }
+__device__ __forceinline__ Fq2 fsqr(const Fq2& a) { return fq2_sqr_call(a); }
+
+// Selectable inlining: the G1 bucket-accumulation loop inlines its Fq
+// multiplications (one madd body, ILP across independent products).
+template <bool INL>
+__device__ __forceinline__ Fq fmul_s(const Fq& a, const Fq& b) {
+    if constexpr (INL) return mul(a, b);
+    else return fq_mul_call(a, b);
+}
+template <bool INL>
+__device__ __forceinline__ Fq2 fmul_s(const Fq2& a, const Fq2& b) { return fmul(a, b); }
 __device__ __forceinline__ Fq2 fadd(const Fq2& a, const Fq2& b) {
     return {add(a.c0, b.c0), add(a.c1, b.c1)};
 }
@@ -104,8 +118,10 @@ __device__ __forceinline__ XYZZ<F> xyzz_mdbl(const F& x, const F& y) {
     return r;
 }
 
-// madd-2008-s: p + (x, y) with (x, y) affine, not infinity.
-template <class F>
+// madd-2008-s: p + (x, y) with (x, y) affine, not infinity. INL inlines the
+// ten Fq products (independent pairs interleave); the rare doubling path
+// stays out of line.
+template <class F, bool INL = false>
 __device__ __forceinline__ XYZZ<F> xyzz_madd(const XYZZ<F>& p, const F& x, const F& y) {
     if (p.is_inf()) {
         XYZZ<F> r;
@@ -115,22 +131,24 @@ __device__ __forceinline__ XYZZ<F> xyzz_madd(const XYZZ<F>& p, const F& x, const
         fset_one(r.ZZZ);
         return r;
     }
-    F U2 = fmul(x, p.ZZ);
-    F S2 = fmul(y, p.ZZZ);
+    F U2 = fmul_s<INL>(x, p.ZZ);
+    F S2 = fmul_s<INL>(y, p.ZZZ);
     F P = fsub(U2, p.X);
     F R = fsub(S2, p.Y);
     if (fzero(P)) {
         if (fzero(R)) return xyzz_mdbl(x, y);
         return XYZZ<F>::inf();
     }
-    F PP = fsqr(P);
-    F PPP = fmul(P, PP);
-    F Q = fmul(p.X, PP);
+    F PP = fmul_s<INL>(P, P);
+    F PPP = fmul_s<INL>(P, PP);
+    F Q = fmul_s<INL>(p.X, PP);
+    F R2 = fmul_s<INL>(R, R);
+    F YP = fmul_s<INL>(p.Y, PPP);
     XYZZ<F> r;
-    r.X = fsub(fsub(fsub(fsqr(R), PPP), Q), Q);
-    r.Y = fsub(fmul(R, fsub(Q, r.X)), fmul(p.Y, PPP));
-    r.ZZ = fmul(p.ZZ, PP);
-    r.ZZZ = fmul(p.ZZZ, PPP);
+    r.ZZ = fmul_s<INL>(p.ZZ, PP);
+    r.ZZZ = fmul_s<INL>(p.ZZZ, PPP);
+    r.X = fsub(fsub(fsub(R2, PPP), Q), Q);
+    r.Y = fsub(fmul_s<INL>(R, fsub(Q, r.X)), YP);
     return r;
 }
 
