@@ -28,20 +28,18 @@ __device__ __forceinline__ void fset_one(Fq& a) { a = Fq::one(); }
 __device__ __forceinline__ void fset_zero(Fq& a) { a = Fq::zero(); }
 __device__ __forceinline__ bool feq(const Fq& a, const Fq& b) { return a == b; }
 
-// Fq2 products as one out-of-line unit whose three (two) independent Fq
-// multiplications are inlined, so the scheduler can interleave them (ILP 3).
-static __device__ __noinline__ Fq2 fq2_mul_call(const Fq2 a, const Fq2 b) {
-    Fq t0 = mul(a.c0, b.c0), t1 = mul(a.c1, b.c1);
-    Fq t2 = mul(add(a.c0, a.c1), add(b.c0, b.c1));
+// Fq2 products: Karatsuba over out-of-line Fq products. (Inlining the three
+// Fq products into one out-of-line Fq2 unit measured 8 % slower.)
+__device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
+    Fq t0 = fq_mul_call(a.c0, b.c0), t1 = fq_mul_call(a.c1, b.c1);
+    Fq t2 = fq_mul_call(add(a.c0, a.c1), add(b.c0, b.c1));
     return {sub(t0, t1), sub(sub(t2, t0), t1)};
 }
-static __device__ __noinline__ Fq2 fq2_sqr_call(const Fq2 a) {
+__device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
     // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u
-    Fq t = mul(a.c0, a.c1);
-    return {mul(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
+    Fq t = fq_mul_call(a.c0, a.c1);
+    return {fq_mul_call(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
 }
-__device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) { return fq2_mul_call(a, b); }
-__device__ __forceinline__ Fq2 fsqr(const Fq2& a) { return fq2_sqr_call(a); }
 
 // Selectable inlining: the G1 bucket-accumulation loop inlines its Fq
 // multiplications (one madd body, ILP across independent products).

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(128) accumulate_kernel(const uint8_t* table,
         F x, y;
         if (load_affine<F>(table + (uint64_t)A * (v & 0x7FFFFFFFu), x, y)) {  // skip infinity
             if (v >> 31) y = fneg(y);
-            acc = xyzz_madd<F, true>(acc, x, y);
+            acc = xyzz_madd<F>(acc, x, y);  // out-of-line Fq products (inlining measured slower)
         }
         v = nv;
     }
