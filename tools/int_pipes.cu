@@ -8,7 +8,8 @@ template <int MODE>
 __global__ void k(uint32_t* sink, uint32_t iters) {
     uint32_t a[8];
     uint64_t w[8];
-    for (int j = 0; j < 8; ++j) { a[j] = threadIdx.x * 7 + j; w[j] = a[j]; }
+    double dd[8];
+    for (int j = 0; j < 8; ++j) { a[j] = threadIdx.x * 7 + j; w[j] = a[j]; dd[j] = a[j]; }
     const uint32_t m = blockIdx.x | 0x9E3779B1u;
     for (uint32_t it = 0; it < iters; ++it) {
 #pragma unroll
@@ -19,12 +20,13 @@ __global__ void k(uint32_t* sink, uint32_t iters) {
                 if (MODE == 1) asm volatile("mad.wide.u32 %0, %1, %2, %0;" : "+l"(w[j]) : "r"((uint32_t)(w[j] >> 7)), "r"(m));
                 if (MODE == 2) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(it));
                 if (MODE == 3) asm volatile("add.u32 %0, %0, %1;" : "+r"(a[j]) : "r"(m));
+                if (MODE == 5) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dd[j]) : "d"(1.0000001), "d"(1e-9));
                 if (MODE == 4) asm volatile("{.reg .u32 t; mad.lo.cc.u32 %0, %0, %1, %2; madc.hi.u32 t, %0, %1, 0; add.u32 %0, %0, t;}" : "+r"(a[j]) : "r"(m), "r"(it));
             }
         }
     }
     uint64_t x = 0;
-    for (int j = 0; j < 8; ++j) x ^= a[j] ^ w[j];
+    for (int j = 0; j < 8; ++j) x ^= a[j] ^ w[j] ^ (uint64_t)dd[j];
     if (x == 0x1234567ull) sink[0] = (uint32_t)x;
 }
 
@@ -55,5 +57,6 @@ int main() {
     printf("mad.hi.u32   %.3e /s\n", run<2>(sink));
     printf("add.u32      %.3e /s\n", run<3>(sink));
     printf("lo.cc+hi chain(3 ops) %.3e /s\n", run<4>(sink));
+    printf("fma.rn.f64   %.3e /s\n", run<5>(sink));
     return 0;
 }
