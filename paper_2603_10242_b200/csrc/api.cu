@@ -89,6 +89,8 @@ struct acegpu_ctx {
     // Segmented block pipeline: sub-contexts (own stream + workspace).
     cudaStream_t copy_stream = nullptr;  // overlapped host-input pipeline
     std::vector<cudaEvent_t> seg_events;
+    cudaStream_t leaf_streams[4] = {};
+    cudaEvent_t leaf_events[4] = {};
     bool force_single = true;  // overlapped pipeline off unless acegpu_set_segmented(ctx, 1)
 };
 
@@ -324,6 +326,10 @@ void acegpu_destroy(acegpu_ctx* c) {
     c->msm.release();
     for (auto& e : c->seg_events) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (int k = 0; k < 4; ++k) {
+        if (c->leaf_streams[k]) cudaStreamDestroy(c->leaf_streams[k]);
+        if (c->leaf_events[k]) cudaEventDestroy(c->leaf_events[k]);
+    }
     for (auto& b : c->bufs)
         if (b.p) cudaFree(b.p);
     cudaStreamDestroy(c->stream);
@@ -781,10 +787,17 @@ int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const u
 // attestation and REV-index slices of 2^kSegLog-tx segments are copied on a
 // copy stream while the leaf kernel of earlier segments runs on the compute
 // stream; the tree levels and the FC then follow as in block_pipeline.
-constexpr uint32_t kSegLog = 13;
+constexpr uint32_t kSegLog = 14;
+constexpr int kLeafStreams = 4;
 
 int ensure_copy(acegpu_ctx* c, size_t nev) {
-    if (!c->copy_stream) CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    if (!c->copy_stream) {
+        CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int k = 0; k < kLeafStreams; ++k) {
+            CK(cudaStreamCreateWithFlags(&c->leaf_streams[k], cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&c->leaf_events[k], cudaEventDisableTiming));
+        }
+    }
     while (c->seg_events.size() < nev) {
         cudaEvent_t e;
         CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -820,7 +833,10 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
             CK(cudaMemcpyAsync(const_cast<uint32_t*>(rev_index) + a, host_rix + a, 4 * cnt,
                                cudaMemcpyHostToDevice, c->copy_stream));
         CK(cudaEventRecord(c->seg_events[j], c->copy_stream));
-        CK(cudaStreamWaitEvent(s, c->seg_events[j], 0));
+        // each segment's leaf kernel on its own stream: a 2^kSegLog segment is
+        // about one wave, i.e. latency-bound alone, so segments must overlap
+        cudaStream_t ls = c->leaf_streams[j % kLeafStreams];
+        CK(cudaStreamWaitEvent(ls, c->seg_events[j], 0));
         LeafArgs la{};
         la.payloads = payloads;
         la.offs = offs + a;
@@ -833,9 +849,13 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
         la.merkle = ma + 32 * a;
         la.header = j == 0 ? header : nullptr;
         la.block_hash = bh;
-        launch_leaves(la, s);
+        launch_leaves(la, ls);
         CKL();
         c->launches++;
+    }
+    for (int k = 0; k < kLeafStreams; ++k) {
+        CK(cudaEventRecord(c->leaf_events[k], c->leaf_streams[k]));
+        CK(cudaStreamWaitEvent(s, c->leaf_events[k], 0));
     }
     TreeResult t;
     RET(run_tree(c, s, payloads, offs, atts, uint32_t(n), header, revs, rev_index, codes, true, 64,
