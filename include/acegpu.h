@@ -61,9 +61,9 @@ uint64_t acegpu_launch_count(const acegpu_ctx* ctx);
  * stream): ms3 = {leaves(+attestation), tree levels, finalize} of the most
  * recent attest_prove_certify call. */
 int acegpu_set_phase_timing(acegpu_ctx* ctx, int enable);
-/* Experimental (default off: measured slower in round 1): host-input calls
- * on blocks of >= 16,384 txs copy 8,192-tx segments on a copy stream
- * overlapped with the leaf kernels of earlier segments. Results identical. */
+/* Host-input calls on blocks of >= 16,384 txs copy 16,384-tx segments on a
+ * copy stream overlapped with the leaf kernels of earlier segments (on four
+ * streams). Default on (100k block e2e 1.23 vs 1.31 ms); results identical. */
 int acegpu_set_segmented(acegpu_ctx* ctx, int enable);
 int acegpu_phase_times(acegpu_ctx* ctx, float* ms3);
 /* Pinned host memory for fast host<->device copies. */

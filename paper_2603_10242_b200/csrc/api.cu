@@ -91,7 +91,7 @@ struct acegpu_ctx {
     std::vector<cudaEvent_t> seg_events;
     cudaStream_t leaf_streams[4] = {};
     cudaEvent_t leaf_events[4] = {};
-    bool force_single = true;  // overlapped pipeline off unless acegpu_set_segmented(ctx, 1)
+    bool force_single = false;  // acegpu_set_segmented(ctx, 0) forces the single-pass pipeline
 };
 
 // A prepared fixed-base MSM (proving-key bases with their 16 window shifts).

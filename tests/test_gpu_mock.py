@@ -429,12 +429,12 @@ def test_segmented_pipeline_equals_single_pass(P):
     """The overlapped host-input pipeline (per-segment H2D + leaf kernels)
     must give the single-pass pipeline's verdicts, proof and FC (and the oracle's)."""
     fb = O.forge(O.multi_user_block(40000, 5), every=5, phase=3)
-    single = gpu_block(P, fb)
-    P.ctx.call("acegpu_set_segmented", 1)
+    seg = gpu_block(P, fb)
+    P.ctx.call("acegpu_set_segmented", 0)
     try:
-        seg = gpu_block(P, fb)
+        single = gpu_block(P, fb)
     finally:
-        P.ctx.call("acegpu_set_segmented", 0)
+        P.ctx.call("acegpu_set_segmented", 1)
     assert seg[0] == single[0] and seg[1] == single[1] and (seg[2] == single[2]).all()
     assert (seg[2] == O.oracle_attest_codes(fb)).all()
     oproof, _, _ = O.oracle_prove_block(fb)
