@@ -244,8 +244,8 @@ def run_ours(args, rank: int, world: int) -> None:
         if world == 1:
             ctx.call("acegpu_attest_prove_certify_dev", sptr, db.payloads.data_ptr(),
                      db.offs.data_ptr(), db.atts.data_ptr(), n, db.header.data_ptr(),
-                     db.revs.data_ptr(), db.rev_index.data_ptr(), codes.data_ptr(),
-                     out.data_ptr(), out.data_ptr() + 304)
+                     db.revs.data_ptr(), db.revs.numel() // 32, db.rev_index.data_ptr(),
+                     codes.data_ptr(), out.data_ptr(), out.data_ptr() + 304)
             return out[:289], out[304:632]
         return shard.prove_sharded(db, n, rank, world, shard.LOG2_CHUNK, be, codes=codes)
 

@@ -119,8 +119,8 @@ int acegpu_attest_prove_certify(acegpu_ctx* ctx, const uint8_t* payloads, const 
 int acegpu_attest_prove_certify_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
                                     const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
                                     const uint8_t* d_header256, const uint8_t* d_revs,
-                                    const uint32_t* d_rev_index, uint8_t* d_codes,
-                                    uint8_t* d_out289, uint8_t* d_out_fc328);
+                                    uint64_t n_revs, const uint32_t* d_rev_index,
+                                    uint8_t* d_codes, uint8_t* d_out289, uint8_t* d_out_fc328);
 
 /* ---- multi-GPU sharding (power-of-two aligned chunks) -------- */
 /* Reduce one rank's shard (txs [start, start+n) of an n_total-tx block, start
@@ -132,8 +132,8 @@ int acegpu_attest_prove_certify_dev(acegpu_ctx* ctx, void* stream, const uint8_t
 int acegpu_shard_roots_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
                            const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
                            uint64_t n_total, uint32_t log2_chunk, const uint8_t* d_revs,
-                           const uint32_t* d_rev_index, uint8_t* d_codes, uint8_t* d_roots289,
-                           uint8_t* d_merkle32);
+                           uint64_t n_revs, const uint32_t* d_rev_index, uint8_t* d_codes,
+                           uint8_t* d_roots289, uint8_t* d_merkle32);
 /* Combine the ordered chunk roots of all ranks into the block proof + FC. */
 int acegpu_combine_roots_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_roots289,
                              const uint8_t* d_merkle32, uint64_t n_chunks, uint64_t n_total,

@@ -47,10 +47,10 @@ _SIGS = {
     "acegpu_block_hash": (C.c_int, [ctxp, vp, vp]),
     "acegpu_attest_prove_certify": (C.c_int, [ctxp, vp, vp, vp, u64, vp, vp, u64, vp, vp, vp, vp,
                                               u64p, u64p]),
-    "acegpu_attest_prove_certify_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, vp, vp, vp, vp,
-                                                  vp]),
-    "acegpu_shard_roots_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, u64, C.c_uint32, vp, vp, vp,
-                                         vp, vp]),
+    "acegpu_attest_prove_certify_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, vp, u64, vp, vp,
+                                                  vp, vp]),
+    "acegpu_shard_roots_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, u64, C.c_uint32, vp, u64, vp,
+                                         vp, vp, vp]),
     "acegpu_combine_roots_dev": (C.c_int, [ctxp, vp, vp, vp, u64, u64, vp, vp, vp]),
     "acegpu_attest_verify": (C.c_int, [ctxp, vp, vp, vp, u64, vp, u64, vp, vp]),
     "acegpu_attest_generate": (C.c_int, [ctxp, vp, vp, u64, vp, u64, vp, vp, vp, vp]),

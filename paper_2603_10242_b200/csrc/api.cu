@@ -56,7 +56,7 @@ int fail(int code, const std::string& msg) {
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
     kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kSegRoots, kSegMerk,
-    kNumSlots
+    kKeytab, kKeydom, kNumSlots
 };
 
 struct DevBuf {
@@ -92,6 +92,9 @@ struct acegpu_ctx {
     cudaStream_t leaf_streams[4] = {};
     cudaEvent_t leaf_events[4] = {};
     bool force_single = false;  // acegpu_set_segmented(ctx, 0) forces the single-pass pipeline
+    // attest-key cache of the call in flight (see LeafArgs::keytab)
+    const uint32_t* cur_keytab = nullptr;
+    const uint8_t* cur_keydom = nullptr;
 };
 
 // A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
@@ -198,6 +201,8 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
     a.merkle = ma;
     a.header = header;
     a.block_hash = bh;
+    a.keytab = codes ? c->cur_keytab : nullptr;
+    a.keydom = c->cur_keydom;
     if (c->timing) CK(cudaEventRecord(c->ev[0], s));
     if ((n || header) && !skip_leaves) {
         launch_leaves(a, s);
@@ -245,6 +250,28 @@ int block_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const
     }
     return ACEGPU_OK;
 }
+
+// Attest-key cache for one call: keytab for every REV under the domain at
+// d_dom8 (tx 0's), consumed by the leaf kernels through ctx->cur_keytab.
+struct KeytabScope {
+    acegpu_ctx* c;
+    explicit KeytabScope(acegpu_ctx* ctx) : c(ctx) {}
+    ~KeytabScope() {
+        c->cur_keytab = nullptr;
+        c->cur_keydom = nullptr;
+    }
+    int build(cudaStream_t s, const uint8_t* d_revs, uint64_t n_revs, const uint8_t* d_dom8) {
+        if (!d_revs || !n_revs || n_revs > 0xFFFFFFFFull) return ACEGPU_OK;
+        uint32_t* kt;
+        RET(ws(c, kKeytab, 64 * n_revs, &kt));
+        launch_keytab(d_revs, uint32_t(n_revs), d_dom8, kt, s);
+        CKL();
+        c->launches++;
+        c->cur_keytab = kt;
+        c->cur_keydom = d_dom8;
+        return ACEGPU_OK;
+    }
+};
 
 struct HostBlock;
 int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
@@ -561,6 +588,13 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
     uint32_t* dri = nullptr;
     RET(h2d_t(c, kHeader, header, 256, s, &dh));
     RET(ws(c, kOut, 289 + 328 + 16, &dout));
+    KeytabScope kts(c);
+    uint8_t* dkeydom = nullptr;
+    if (codes && n) {
+        RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
+        RET(h2d_t(c, kKeydom, atts + 64, 8, s, &dkeydom));  // tx 0's domain
+        RET(kts.build(s, dr, n_revs, dkeydom));
+    }
     if (use_segments(c, n)) {
         // offsets + REV table first; payload/attestation slices are copied per
         // segment on the sub-streams, overlapping the compute of earlier ones
@@ -569,7 +603,6 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
         RET(ws(c, kAtts, 104 * n + 16, &da));
         RET(h2d_t(c, kOffs, offs, 8 * (n + 1), s, &doff));
         if (codes) {
-            RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
             RET(ws(c, kRevIdx, 4 * n, &dri));
             RET(ws(c, kCodes, n, &dc));
         }
@@ -578,7 +611,6 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
     } else {
         RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
         if (codes && n) {
-            RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
             RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &dri));
             RET(ws(c, kCodes, n, &dc));
         }
@@ -595,14 +627,17 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
 
 int acegpu_attest_prove_certify_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
                                     const uint64_t* offs, const uint8_t* atts, uint64_t n,
-                                    const uint8_t* header, const uint8_t* revs,
+                                    const uint8_t* header, const uint8_t* revs, uint64_t n_revs,
                                     const uint32_t* rev_index, uint8_t* codes, uint8_t* out289,
                                     uint8_t* out328) {
     RET(check_n(n));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    return block_pipeline(c, pick(c, stream), payloads, offs, atts, uint32_t(n), header, revs,
-                          rev_index, n ? codes : nullptr, out289, out328);
+    cudaStream_t s = pick(c, stream);
+    KeytabScope kts(c);
+    if (codes && n) RET(kts.build(s, revs, n_revs, atts + 64));
+    return block_pipeline(c, s, payloads, offs, atts, uint32_t(n), header, revs, rev_index,
+                          n ? codes : nullptr, out289, out328);
 }
 
 int acegpu_prove_block(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
@@ -706,14 +741,18 @@ extern "C" {
 
 int acegpu_shard_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
                            const uint64_t* offs, const uint8_t* atts, uint64_t n, uint64_t n_total,
-                           uint32_t log2_chunk, const uint8_t* revs, const uint32_t* rev_index,
-                           uint8_t* codes, uint8_t* roots289, uint8_t* merkle32) {
+                           uint32_t log2_chunk, const uint8_t* revs, uint64_t n_revs,
+                           const uint32_t* rev_index, uint8_t* codes, uint8_t* roots289,
+                           uint8_t* merkle32) {
     RET(check_n(n));
     if (n == 0 || log2_chunk > 31) return fail(ACEGPU_EINVAL, "empty shard or chunk too large");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    return shard_impl(c, pick(c, stream), payloads, offs, atts, n, n_total, log2_chunk, revs,
-                      rev_index, codes, roots289, merkle32);
+    cudaStream_t s = pick(c, stream);
+    KeytabScope kts(c);
+    if (codes) RET(kts.build(s, revs, n_revs, atts + 64));
+    return shard_impl(c, s, payloads, offs, atts, n, n_total, log2_chunk, revs, rev_index, codes,
+                      roots289, merkle32);
 }
 
 int acegpu_combine_roots_dev(acegpu_ctx* c, void* stream, const uint8_t* roots289,
@@ -849,6 +888,8 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
         la.merkle = ma + 32 * a;
         la.header = j == 0 ? header : nullptr;
         la.block_hash = bh;
+        la.keytab = codes ? c->cur_keytab : nullptr;
+        la.keydom = c->cur_keydom;
         launch_leaves(la, ls);
         CKL();
         c->launches++;

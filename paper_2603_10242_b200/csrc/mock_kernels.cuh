@@ -23,9 +23,18 @@ struct LeafArgs {
     uint8_t* merkle;           // n x 32 merkle leaf hashes H(0x00|id_com), or nullptr
     const uint8_t* header;     // 256-B header; nullptr = no block hash
     uint8_t* block_hash;       // 32 B out when header != nullptr
+    // Optional attest-key cache: per REV u, the HMAC ipad/opad midstates of
+    // derive_attest_key(REV_u, D0) where D0 = the domain of tx 0. A tx whose
+    // domain equals D0 uses them (2 compressions for the credential instead
+    // of 12); any other domain takes the full path. Exact either way.
+// launch_keytab builds it from the domain at `dom8` (8 device bytes).
+    const uint32_t* keytab;    // n_revs x 16 words, or nullptr
+    const uint8_t* keydom;     // the 8-B domain D0 the keytab was built for
 };
 
 void launch_leaves(const LeafArgs& a, cudaStream_t s);
+void launch_keytab(const uint8_t* revs, uint32_t n_revs, const uint8_t* dom8, uint32_t* keytab,
+                   cudaStream_t s);
 
 // One tree level for the proof tree (pairs (2i,2i+1), odd node promoted,
 // prover.cpp:112-124) and/or the Merkle tree (odd node duplicated,

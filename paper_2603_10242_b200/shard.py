@@ -104,6 +104,7 @@ class GpuBackend:
         if db.n:
             self.ctx.call("acegpu_shard_roots_dev", _stream(), _ptr(db.payloads), _ptr(db.offs),
                           _ptr(db.atts), db.n, n_total, log2_chunk, _ptr(db.revs),
+                          0 if db.revs is None else db.revs.numel() // 32,
                           _ptr(db.rev_index), _ptr(codes), _ptr(roots), _ptr(merk))
         return roots[:c * 289], merk[:c * 32]
 
