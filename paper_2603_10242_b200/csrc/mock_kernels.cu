@@ -21,6 +21,9 @@ namespace {
 constexpr int kThreads = 128;
 constexpr uint32_t kStageBytes = 192 * kThreads;  // payload staging per CTA (24 KB)
 
+// W+K schedule of the constant padding block of a 512-B message (aggregate_pair).
+__device__ __constant__ const Wk64 kPadWk512 = pad_block_wk(512 * 8);
+
 __device__ __forceinline__ void load_be8(const uint8_t* p, uint32_t w[8]) { load_digest(p, w); }
 
 // 8 BE words from an 8-B aligned pointer.
@@ -246,18 +249,19 @@ __global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restri
                 uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
                 uint32_t d[8], seed[8];
                 sha256_init(d);
+                // compact (rolled) compressions: this chain runs once per
+                // launch, so its code size is I-cache-miss latency
 #pragma unroll 1
                 for (int blk = 0; blk < 8; ++blk) {
                     const uint32_t* wb = wk + 65 * blk;
-                    sha256_rounds(d, [wb](int i) { return wb[i]; });
+                    sha256_rounds_c(d, [wb](int i) { return wb[i]; });
                 }
-                constexpr Wk64 kPad = pad_block_wk(512 * 8);
-                sha256_rounds(d, [](int i) { return kPad.v[i]; });
-                expand_seed(1, d, seed);
+                sha256_rounds_c(d, [](int i) { return kPadWk512.v[i]; });
+                expand_seed<true>(1, d, seed);
 #pragma unroll 1
                 for (uint32_t c = lane; c < 8; c += G) {
                     uint32_t o[8];
-                    expand_block(seed, c, o);
+                    expand_block<true>(seed, c, o);
                     store_digest(out + 32 * c, o);
                 }
                 if (lane == 0) write_node_tail(out, d, 1);
@@ -459,10 +463,10 @@ __global__ void keytab_kernel(const uint8_t* revs, uint32_t n_revs, const uint8_
     const uint2 dv = *reinterpret_cast<const uint2*>(dom8);
     uint32_t rev[8], key[16], ist[8], ost[8];
     load_be8(revs + 32ull * u, rev);
-    derive_attest_key(rev, bswap32(dv.x), bswap32(dv.y), key);
+    derive_attest_key<true>(rev, bswap32(dv.x), bswap32(dv.y), key);  // compact: latency path
 #pragma unroll
     for (int k = 8; k < 16; ++k) key[k] = 0;
-    hmac_midstates(key, ist, ost);
+    hmac_midstates<true>(key, ist, ost);
     uint4* o = reinterpret_cast<uint4*>(keytab + 16ull * u);
     o[0] = make_uint4(ist[0], ist[1], ist[2], ist[3]);
     o[1] = make_uint4(ist[4], ist[5], ist[6], ist[7]);

@@ -69,6 +69,71 @@ __device__ __forceinline__ void sha256_compress(uint32_t s[8], uint32_t w[16]) {
     s[4] += e; s[5] += f; s[6] += g; s[7] += h;
 }
 
+// ---- compact compression for latency-bound code ----------------------------
+// The fully unrolled compression is ~1,400 SASS instructions (~22 KB). In a
+// kernel that runs a chain of compressions ONCE (the narrow tree levels, the
+// key cache), every instruction line is an I-cache miss on first touch, so
+// code size is latency. These variants keep 16 rounds per loop iteration
+// (register roles return to identity every 8 rounds, window index = j) and
+// read K from the constant bank: ~4x less code.
+__device__ __constant__ static const uint32_t kK256c[64] = ACE_K256;
+
+#define ACE_SHA_ROUND(i, wi)                                                 \
+    do {                                                                     \
+        uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);          \
+        uint32_t ch = (e & f) ^ (~e & g);                                    \
+        uint32_t t1 = h + S1 + ch + kK256c[i] + (wi);                        \
+        uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);          \
+        uint32_t mj = (a & b) ^ (a & c) ^ (b & c);                           \
+        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj; \
+    } while (0)
+
+__device__ __forceinline__ void sha256_compress_c(uint32_t s[8], uint32_t w[16]) {
+    uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) ACE_SHA_ROUND(j, w[j]);
+#pragma unroll 1
+    for (int i0 = 16; i0 < 64; i0 += 16) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            uint32_t w15 = w[(j + 1) & 15], w2 = w[(j + 14) & 15];
+            uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
+            uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
+            w[j] = w[j] + s0 + w[(j + 9) & 15] + s1;
+            ACE_SHA_ROUND(i0 + j, w[j]);
+        }
+    }
+    s[0] += a; s[1] += b; s[2] += c; s[3] += d;
+    s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+// Rounds only (W+K precomputed), compact.
+template <class WK>
+__device__ __forceinline__ void sha256_rounds_c(uint32_t s[8], WK wk) {
+    uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
+#pragma unroll 1
+    for (int i0 = 0; i0 < 64; i0 += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
+            uint32_t ch = (e & f) ^ (~e & g);
+            uint32_t t1 = h + S1 + ch + wk(i0 + j);
+            uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
+            uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+            h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+        }
+    }
+    s[0] += a; s[1] += b; s[2] += c; s[3] += d;
+    s[4] += e; s[5] += f; s[6] += g; s[7] += h;
+}
+
+// Compile-time dispatch: full unroll (throughput kernels) or compact.
+template <bool COMPACT>
+__device__ __forceinline__ void compress(uint32_t s[8], uint32_t w[16]) {
+    if constexpr (COMPACT) sha256_compress_c(s, w);
+    else sha256_compress(s, w);
+}
+
 // ---- split compression: message schedule (W[i] + K[i]) and rounds ---------
 // Used where a compression's latency, not its issue cost, matters: sibling
 // lanes precompute the schedules of independent blocks so that the serial
@@ -197,6 +262,7 @@ __device__ __forceinline__ void load_digest(const uint8_t* src, uint32_t s[8]) {
 // out[c] = SHA(seed | c_be32) for c = 0..7. Tags "zk-tx-proof-v1" (14 B) and
 // "zk-agg-proof-v1" (15 B) (prover.cpp:14-15) are folded into constants.
 // kind 0 = Tx, 1 = Aggregate.
+template <bool C = false>
 __device__ __forceinline__ void expand_seed(int kind, const uint32_t d[8], uint32_t seed[8]) {
     uint32_t w[16];
     if (kind == 0) {
@@ -217,10 +283,11 @@ __device__ __forceinline__ void expand_seed(int kind, const uint32_t d[8], uint3
         w[12] = 0; w[13] = 0; w[14] = 0; w[15] = 47 * 8;
     }
     sha256_init(seed);
-    sha256_compress(seed, w);
+    compress<C>(seed, w);
 }
 
 // One output block of expand256: SHA(seed | c_be32), a single 36-B message.
+template <bool C = false>
 __device__ __forceinline__ void expand_block(const uint32_t seed[8], uint32_t c, uint32_t o[8]) {
     uint32_t w[16];
 #pragma unroll
@@ -231,7 +298,7 @@ __device__ __forceinline__ void expand_block(const uint32_t seed[8], uint32_t c,
     for (int k = 10; k < 15; ++k) w[k] = 0;
     w[15] = 36 * 8;
     sha256_init(o);
-    sha256_compress(o, w);
+    compress<C>(o, w);
 }
 
 // Full expand256 written to 256 B of wire-order bytes (16-B aligned).
@@ -290,20 +357,22 @@ __device__ __forceinline__ void public_inputs_digest_full(const uint32_t pub[40]
 // ------------------------------------------------------------- HMAC-SHA256 --
 // HmacCtx (hkdf.cpp:12-39) for keys <= 64 B given as BE words (key zero-padded
 // to 64 B). Midstates after the ipad / opad blocks.
+template <bool C = false>
 __device__ __forceinline__ void hmac_midstates(const uint32_t key[16], uint32_t ist[8],
                                                uint32_t ost[8]) {
     uint32_t w[16];
 #pragma unroll
     for (int k = 0; k < 16; ++k) w[k] = key[k] ^ 0x36363636u;
     sha256_init(ist);
-    sha256_compress(ist, w);
+    compress<C>(ist, w);
 #pragma unroll
     for (int k = 0; k < 16; ++k) w[k] = key[k] ^ 0x5c5c5c5cu;
     sha256_init(ost);
-    sha256_compress(ost, w);
+    compress<C>(ost, w);
 }
 
 // Outer hash: SHA(opad | inner) from the opad midstate: one compression.
+template <bool C = false>
 __device__ __forceinline__ void hmac_outer(const uint32_t ost[8], const uint32_t inner[8],
                                            uint32_t out[8]) {
     uint32_t w[16];
@@ -313,22 +382,23 @@ __device__ __forceinline__ void hmac_outer(const uint32_t ost[8], const uint32_t
 #pragma unroll
     for (int k = 9; k < 15; ++k) w[k] = 0;
     w[15] = (64 + 32) * 8;
-    sha256_compress(out, w);
+    compress<C>(out, w);
 }
 
 // HMAC(key32, msg) for a one-block message tail `m` of mlen <= 55 bytes,
 // already laid out as BE words with the 0x80 terminator; the length word is
 // filled here. key32 is a 32-B key as 8 BE words.
+template <bool C = false>
 __device__ __forceinline__ void hmac32_short(const uint32_t key32[8], uint32_t m[16],
                                              uint32_t mlen, uint32_t out[8]) {
     uint32_t key[16], ist[8], ost[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) { key[k] = key32[k]; key[k + 8] = 0; }
-    hmac_midstates(key, ist, ost);
+    hmac_midstates<C>(key, ist, ost);
     m[14] = 0;
     m[15] = (64 + mlen) * 8;
-    sha256_compress(ist, m);
-    hmac_outer(ost, ist, out);
+    compress<C>(ist, m);
+    hmac_outer<C>(ost, ist, out);
 }
 
 // Credential HMAC(k, obj_hash | domain8) (crypto.cpp:129-139, :149-150;
@@ -347,6 +417,7 @@ __device__ __forceinline__ void credential_hmac(const uint32_t key[8], const uin
 // derive_attest_key (crypto.cpp:124-127 -> derive_key :78-89 -> hkdf_sha256):
 // prk = HMAC(salt = domain8, ikm = REV32); okm = HMAC(prk, info | 0x01) with
 // info = "ACEGF-V1-MEMPOOL-ATTEST" (23 B, crypto.hpp:19), L = 32.
+template <bool C = false>
 __device__ __forceinline__ void derive_attest_key(const uint32_t rev[8], uint32_t dom0,
                                                   uint32_t dom1, uint32_t out[8]) {
     uint32_t key[16], ist[8], ost[8], m[16], prk[8];
@@ -354,21 +425,21 @@ __device__ __forceinline__ void derive_attest_key(const uint32_t rev[8], uint32_
     for (int k = 0; k < 16; ++k) key[k] = 0;
     key[0] = dom0;
     key[1] = dom1;
-    hmac_midstates(key, ist, ost);
+    hmac_midstates<C>(key, ist, ost);
 #pragma unroll
     for (int k = 0; k < 8; ++k) m[k] = rev[k];
     m[8] = 0x80000000u;
 #pragma unroll
     for (int k = 9; k < 15; ++k) m[k] = 0;
     m[15] = (64 + 32) * 8;
-    sha256_compress(ist, m);
-    hmac_outer(ost, ist, prk);
+    compress<C>(ist, m);
+    hmac_outer<C>(ost, ist, prk);
     // "ACEGF-V1-MEMPOOL-ATTEST" | 0x01 | 0x80
     m[0] = 0x41434547u; m[1] = 0x462d5631u; m[2] = 0x2d4d454du; m[3] = 0x504f4f4cu;
     m[4] = 0x2d415454u; m[5] = 0x45535401u; m[6] = 0x80000000u;
 #pragma unroll
     for (int k = 7; k < 16; ++k) m[k] = 0;
-    hmac32_short(prk, m, 24, out);
+    hmac32_short<C>(prk, m, 24, out);
 }
 
 }  // namespace ace_gpu
