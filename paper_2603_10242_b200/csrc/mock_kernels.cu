@@ -611,7 +611,8 @@ void launch_level(const uint8_t* nin, uint32_t nn, uint8_t* nout, const uint8_t*
                   uint32_t nm, uint8_t* mout, bool lift, cudaStream_t s) {
     const uint32_t pt0 = nin ? nn / 2 + (nn & 1) : 0;
     // Lanes per pair: cost ~ max(latency (10 + 8/G) L, throughput P (10 + 8/G) G / 32).
-    const int G = pt0 >= 24576 ? 1 : pt0 >= 6144 ? 2 : pt0 >= 1536 ? 4 : 8;
+    // (measured: the 8-lane smem-schedule path runs a narrow level in ~19 us)
+    const int G = pt0 >= 24576 ? 1 : pt0 >= 8192 ? 2 : 8;
     const uint32_t pt = pt0 * G;
     const uint32_t pb = blocks_for(pt);
     const uint32_t mt = (!min_ || (nm == 1 && !lift)) ? 0 : (nm + 1) / 2;
