@@ -322,12 +322,14 @@ def run_ours(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     # Work actually executed (SHA-256 compressions): leaf
-    # kernel = 15 (leaf proof: payload 3 + public inputs 3 + seed 1 + expand 8)
-    # + 2 (credential HMAC from the cached attest-key midstates; every tx of
-    # this block shares tx 0's domain, so the 8-compression key derivation
-    # runs once per REV in keytab_kernel) + 1 (Merkle leaf) per tx;
+    # kernel = 15 (leaf proof: payload 3 + public inputs 3 + seed 1 + expand 8;
+    # the attestation's payload check reuses the payload hash) + 1 (Merkle
+    # leaf) per tx. The credential HMAC (2 per tx from the cached attest-key
+    # midstates: every tx of this block shares tx 0's domain, so the
+    # 8-compression key derivation runs once per REV in keytab_kernel) runs in
+    # credential_kernel on a side stream, overlapped with the tree levels.
     # tree = 18 per pair + 2 per Merkle pair.
-    leaf_c = 18 * n
+    leaf_c = 16 * n
     tree_c = 18 * (n - 1) + 2 * (n - 1)
     roof = None
     if phase:

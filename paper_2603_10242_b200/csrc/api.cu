@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -89,12 +90,16 @@ struct acegpu_ctx {
     // Segmented block pipeline: sub-contexts (own stream + workspace).
     cudaStream_t copy_stream = nullptr;  // overlapped host-input pipeline
     std::vector<cudaEvent_t> seg_events;
-    cudaStream_t leaf_streams[4] = {};
-    cudaEvent_t leaf_events[4] = {};
+    cudaStream_t leaf_streams[8] = {};
+    cudaEvent_t leaf_events[8] = {};
     bool force_single = false;  // acegpu_set_segmented(ctx, 0) forces the single-pass pipeline
-    // attest-key cache of the call in flight (see LeafArgs::keytab)
+    // attest-key cache of the call in flight (launch_keytab / launch_credentials)
     const uint32_t* cur_keytab = nullptr;
     const uint8_t* cur_keydom = nullptr;
+    // Side stream of the attestation credential check (keytab + credential
+    // kernels), overlapping the leaf kernel and the tree levels.
+    cudaStream_t cred_stream = nullptr;
+    cudaEvent_t cred_in = nullptr, cred_out = nullptr;
 };
 
 // A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
@@ -173,6 +178,15 @@ struct TreeResult {
     uint32_t count = 0;
 };
 
+int side_stream(acegpu_ctx* c) {
+    if (!c->cred_stream) {
+        CK(cudaStreamCreateWithFlags(&c->cred_stream, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->cred_in, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->cred_out, cudaEventDisableTiming));
+    }
+    return ACEGPU_OK;
+}
+
 // Leaves (+attestation verdicts, merkle leaves, header hash) and up to
 // `max_levels` fused proof/merkle levels. With lift, a lone merkle node keeps
 // self-pairing until max_levels (aligned-chunk roots).
@@ -201,8 +215,6 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
     a.merkle = ma;
     a.header = header;
     a.block_hash = bh;
-    a.keytab = codes ? c->cur_keytab : nullptr;
-    a.keydom = c->cur_keydom;
     if (c->timing) CK(cudaEventRecord(c->ev[0], s));
     if ((n || header) && !skip_leaves) {
         launch_leaves(a, s);
@@ -210,6 +222,18 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
         c->launches++;
     }
     if (c->timing) CK(cudaEventRecord(c->ev[1], s));
+    const bool cred = codes && n;
+    if (cred) {
+        // credential verdicts on the side stream, concurrent with the levels
+        RET(side_stream(c));
+        CK(cudaEventRecord(c->cred_in, s));
+        CK(cudaStreamWaitEvent(c->cred_stream, c->cred_in, 0));
+        launch_credentials(atts, n, revs, rev_index, c->cur_keytab, c->cur_keydom, codes,
+                           c->cred_stream);
+        CKL();
+        c->launches++;
+        CK(cudaEventRecord(c->cred_out, c->cred_stream));
+    }
     uint32_t cur = n, lv = 0;
     uint8_t *nin = na, *nout = nb, *min_ = ma, *mout = mb;
     while (lv < max_levels && (cur > 1 || (lift && cur == 1))) {
@@ -221,6 +245,7 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
         std::swap(min_, mout);
         ++lv;
     }
+    if (cred) CK(cudaStreamWaitEvent(s, c->cred_out, 0));
     if (c->timing) CK(cudaEventRecord(c->ev[2], s));
     r->nodes = nin;
     r->merkle = min_;
@@ -252,7 +277,7 @@ int block_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const
 }
 
 // Attest-key cache for one call: keytab for every REV under the domain at
-// d_dom8 (tx 0's), consumed by the leaf kernels through ctx->cur_keytab.
+// d_dom8 (tx 0's), consumed by the credential kernel through ctx->cur_keytab.
 struct KeytabScope {
     acegpu_ctx* c;
     explicit KeytabScope(acegpu_ctx* ctx) : c(ctx) {}
@@ -264,7 +289,11 @@ struct KeytabScope {
         if (!d_revs || !n_revs || n_revs > 0xFFFFFFFFull) return ACEGPU_OK;
         uint32_t* kt;
         RET(ws(c, kKeytab, 64 * n_revs, &kt));
-        launch_keytab(d_revs, uint32_t(n_revs), d_dom8, kt, s);
+        // on the credential side stream: off the leaf kernel's critical path
+        RET(side_stream(c));
+        CK(cudaEventRecord(c->cred_in, s));
+        CK(cudaStreamWaitEvent(c->cred_stream, c->cred_in, 0));
+        launch_keytab(d_revs, uint32_t(n_revs), d_dom8, kt, c->cred_stream);
         CKL();
         c->launches++;
         c->cur_keytab = kt;
@@ -353,7 +382,14 @@ void acegpu_destroy(acegpu_ctx* c) {
     c->msm.release();
     for (auto& e : c->seg_events) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
-    for (int k = 0; k < 4; ++k) {
+
+    if (c->cred_stream) {
+        cudaStreamSynchronize(c->cred_stream);
+        cudaStreamDestroy(c->cred_stream);
+        cudaEventDestroy(c->cred_in);
+        cudaEventDestroy(c->cred_out);
+    }
+    for (int k = 0; k < 8; ++k) {
         if (c->leaf_streams[k]) cudaStreamDestroy(c->leaf_streams[k]);
         if (c->leaf_events[k]) cudaEventDestroy(c->leaf_events[k]);
     }
@@ -596,12 +632,12 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
         RET(kts.build(s, dr, n_revs, dkeydom));
     }
     if (use_segments(c, n)) {
-        // offsets + REV table first; payload/attestation slices are copied per
-        // segment on the sub-streams, overlapping the compute of earlier ones
+        // REV table first; offset/payload/attestation slices are copied per
+        // segment on the copy streams, overlapping the compute of earlier ones
         const HostBlock hb{payloads, offs, atts, n};
         RET(ws(c, kPayloads, offs[n] + 16, &dp));
         RET(ws(c, kAtts, 104 * n + 16, &da));
-        RET(h2d_t(c, kOffs, offs, 8 * (n + 1), s, &doff));
+        RET(ws(c, kOffs, 8 * (n + 1), &doff));  // copied per segment
         if (codes) {
             RET(ws(c, kRevIdx, 4 * n, &dri));
             RET(ws(c, kCodes, n, &dc));
@@ -827,11 +863,12 @@ int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const u
 // copy stream while the leaf kernel of earlier segments runs on the compute
 // stream; the tree levels and the FC then follow as in block_pipeline.
 constexpr uint32_t kSegLog = 14;
-constexpr int kLeafStreams = 4;
+constexpr int kLeafStreams = 8;
 
 int ensure_copy(acegpu_ctx* c, size_t nev) {
     if (!c->copy_stream) {
         CK(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+
         for (int k = 0; k < kLeafStreams; ++k) {
             CK(cudaStreamCreateWithFlags(&c->leaf_streams[k], cudaStreamNonBlocking));
             CK(cudaEventCreateWithFlags(&c->leaf_events[k], cudaEventDisableTiming));
@@ -852,19 +889,55 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
                         const uint32_t* host_rix) {
     const uint64_t seg = 1ull << kSegLog, S = (n + seg - 1) / seg;
     RET(ensure_copy(c, S + 1));
+    // Level-major node arrays: level L >= 1 occupies [off[L], off[L] + ceil(n / 2^L))
+    // of nb / mb, so the subtrees of different segments (aligned 2^kSegLog
+    // ranges) write disjoint slices of every level and can run concurrently.
+    uint64_t off[66], tot = 0;
+    off[0] = 0;
+    for (uint32_t L = 1; L < 66; ++L) {
+        off[L] = tot;
+        tot += (n + (1ull << std::min(L, 63u)) - 1) >> std::min(L, 63u);
+    }
+    // levels run per segment on the segment's stream (the rest on s)
+    static const uint32_t sub = [] {
+        const char* e = getenv("ACEGPU_SEG_LEVELS");
+        return e ? std::min<uint32_t>(uint32_t(atoi(e)), kSegLog) : kSegLog;
+    }();
     uint8_t *na, *nb, *ma, *mb, *bh;
     RET(ws(c, kNodesA, size_t(kNodeBytes) * n, &na));
-    RET(ws(c, kNodesB, size_t(kNodeBytes) * (n / 2 + 1), &nb));
+    RET(ws(c, kNodesB, size_t(kNodeBytes) * (tot + 2), &nb));
     RET(ws(c, kMerkA, 32ull * n, &ma));
-    RET(ws(c, kMerkB, 32ull * (n / 2 + 1), &mb));
+    RET(ws(c, kMerkB, 32ull * (tot + 2), &mb));
     RET(ws(c, kBlockHash, 32, &bh));
+    auto nodes_at = [&](uint32_t L, uint64_t i) {
+        return L ? nb + size_t(kNodeBytes) * (off[L] + i) : na + size_t(kNodeBytes) * i;
+    };
+    auto merk_at = [&](uint32_t L, uint64_t i) { return L ? mb + 32 * (off[L] + i) : ma + 32 * i; };
     // the copy stream starts after what is already enqueued on s (offsets, REVs, header)
+    // ACEGPU_TRACE=1: per-segment timeline on stderr (debug; adds a sync)
+    static const bool trace = getenv("ACEGPU_TRACE") != nullptr;
+    std::vector<cudaEvent_t> tev;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.push_back(e);
+    };
+    mark(s);
     CK(cudaEventRecord(c->seg_events[S], s));
     CK(cudaStreamWaitEvent(c->copy_stream, c->seg_events[S], 0));
+    const bool lift = n > seg;  // short last segment: Merkle self-pairing up to level kSegLog
+    const bool cred = codes != nullptr;
+    if (cred) RET(side_stream(c));
     for (uint64_t j = 0; j < S; ++j) {
         const uint64_t a = j * seg, cnt = std::min(seg, n - a);
         const uint64_t b0 = host.offs[a], b1 = host.offs[a + cnt];
+        // (one copy stream: a second one split by field measured no faster,
+        // ~43 GB/s either way on this PCIe 5 x16 host)
         CK(cudaMemcpyAsync(const_cast<uint8_t*>(payloads) + b0, host.payloads + b0, b1 - b0,
+                           cudaMemcpyHostToDevice, c->copy_stream));
+        CK(cudaMemcpyAsync(const_cast<uint64_t*>(offs) + a, host.offs + a, 8 * (cnt + 1),
                            cudaMemcpyHostToDevice, c->copy_stream));
         CK(cudaMemcpyAsync(const_cast<uint8_t*>(atts) + 104 * a, host.atts + 104 * a, 104 * cnt,
                            cudaMemcpyHostToDevice, c->copy_stream));
@@ -872,10 +945,12 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
             CK(cudaMemcpyAsync(const_cast<uint32_t*>(rev_index) + a, host_rix + a, 4 * cnt,
                                cudaMemcpyHostToDevice, c->copy_stream));
         CK(cudaEventRecord(c->seg_events[j], c->copy_stream));
-        // each segment's leaf kernel on its own stream: a 2^kSegLog segment is
-        // about one wave, i.e. latency-bound alone, so segments must overlap
+        // Each segment's leaves AND its subtree (levels 1..kSegLog) on its own
+        // stream: they overlap the copies of later segments and each other
+        // (a segment's narrow levels alone would leave the GPU idle).
         cudaStream_t ls = c->leaf_streams[j % kLeafStreams];
         CK(cudaStreamWaitEvent(ls, c->seg_events[j], 0));
+        mark(ls);
         LeafArgs la{};
         la.payloads = payloads;
         la.offs = offs + a;
@@ -888,22 +963,68 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
         la.merkle = ma + 32 * a;
         la.header = j == 0 ? header : nullptr;
         la.block_hash = bh;
-        la.keytab = codes ? c->cur_keytab : nullptr;
-        la.keydom = c->cur_keydom;
         launch_leaves(la, ls);
         CKL();
         c->launches++;
+        mark(ls);
+        if (cred) {
+            CK(cudaEventRecord(c->leaf_events[j % kLeafStreams], ls));
+            CK(cudaStreamWaitEvent(c->cred_stream, c->leaf_events[j % kLeafStreams], 0));
+            launch_credentials(atts + 104 * a, uint32_t(cnt), revs, rev_index + a,
+                               c->cur_keytab, c->cur_keydom, codes + a, c->cred_stream);
+            CKL();
+            c->launches++;
+        }
+        uint64_t cur = cnt;
+        for (uint32_t L = 0; L < sub && (cur > 1 || (lift && cur == 1)); ++L) {
+            launch_level(nodes_at(L, a >> L), uint32_t(cur), nodes_at(L + 1, a >> (L + 1)),
+                         merk_at(L, a >> L), uint32_t(cur), merk_at(L + 1, a >> (L + 1)), lift, ls);
+            CKL();
+            c->launches++;
+            cur = (cur + 1) / 2;
+        }
+        mark(ls);
     }
     for (int k = 0; k < kLeafStreams; ++k) {
         CK(cudaEventRecord(c->leaf_events[k], c->leaf_streams[k]));
         CK(cudaStreamWaitEvent(s, c->leaf_events[k], 0));
     }
-    TreeResult t;
-    RET(run_tree(c, s, payloads, offs, atts, uint32_t(n), header, revs, rev_index, codes, true, 64,
-                 false, &t, /*skip_leaves=*/true));
-    launch_finalize(t.nodes, t.merkle, header, t.bh, false, out289, out328, s);
+    if (cred) {
+        CK(cudaEventRecord(c->cred_out, c->cred_stream));
+        CK(cudaStreamWaitEvent(s, c->cred_out, 0));
+    }
+    // the rest of the tree from level `sub` (the concatenated segment slices
+    // are the global level array), reference rules
+    uint32_t L = sub;
+    uint64_t cur = (n + (1ull << sub) - 1) >> sub;
+    while (cur > 1) {
+        launch_level(nodes_at(L, 0), uint32_t(cur), nodes_at(L + 1, 0), merk_at(L, 0),
+                     uint32_t(cur), merk_at(L + 1, 0), false, s);
+        CKL();
+        c->launches++;
+        cur = (cur + 1) / 2;
+        ++L;
+    }
+    mark(s);
+    const uint8_t *root = nodes_at(L, 0), *mroot = merk_at(L, 0);
+    launch_finalize(root, mroot, header, bh, false, out289, out328, s);
     CKL();
     c->launches++;
+    if (trace) {
+        mark(s);
+        cudaStreamSynchronize(s);
+        std::string line = "acegpu trace (us):";
+        for (size_t k = 1; k < tev.size(); ++k) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, tev[0], tev[k]);
+            char buf[32];
+            snprintf(buf, sizeof buf, " %.0f", 1e3 * ms);
+            line += buf;
+            if (k < tev.size() - 2 && k % 3 == 0) line += " |";
+        }
+        fprintf(stderr, "%s\n", line.c_str());
+        for (auto e : tev) cudaEventDestroy(e);
+    }
     return ACEGPU_OK;
 }
 
@@ -938,9 +1059,15 @@ int acegpu_attest_verify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t*
     a.revs = dr;
     a.rev_index = dri;
     a.codes = dc;
-    launch_leaves(a, s);
+    launch_leaves(a, s);  // payload verdicts
     CKL();
-    c->launches++;
+    uint32_t* kt;
+    RET(ws(c, kKeytab, 64 * n_revs, &kt));
+    launch_keytab(dr, uint32_t(n_revs), da + 64, kt, s);  // tx 0's domain
+    CKL();
+    launch_credentials(da, uint32_t(n), dr, dri, kt, da + 64, dc, s);
+    CKL();
+    c->launches += 3;
     CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;

@@ -23,16 +23,18 @@ struct LeafArgs {
     uint8_t* merkle;           // n x 32 merkle leaf hashes H(0x00|id_com), or nullptr
     const uint8_t* header;     // 256-B header; nullptr = no block hash
     uint8_t* block_hash;       // 32 B out when header != nullptr
-    // Optional attest-key cache: per REV u, the HMAC ipad/opad midstates of
-    // derive_attest_key(REV_u, D0) where D0 = the domain of tx 0. A tx whose
-    // domain equals D0 uses them (2 compressions for the credential instead
-    // of 12); any other domain takes the full path. Exact either way.
-// launch_keytab builds it from the domain at `dom8` (8 device bytes).
-    const uint32_t* keytab;    // n_revs x 16 words, or nullptr
-    const uint8_t* keydom;     // the 8-B domain D0 the keytab was built for
+    // With codes, the leaf kernel writes the payload verdict (0 / 1); the
+    // credential verdict (2) follows in launch_credentials.
 };
 
 void launch_leaves(const LeafArgs& a, cudaStream_t s);
+// Credential check of verify_attestation_full for every tx with codes[i] == 0
+// (sets 2 on mismatch). keytab (launch_keytab for domain keydom) may be null.
+void launch_credentials(const uint8_t* atts, uint32_t n, const uint8_t* revs,
+                        const uint32_t* rev_index, const uint32_t* keytab, const uint8_t* keydom,
+                        uint8_t* codes, cudaStream_t s);
+// Attest-key cache: per REV u, the HMAC ipad/opad midstates of
+// derive_attest_key(REV_u, D0), D0 = the 8-B domain at dom8 (16 words per REV).
 void launch_keytab(const uint8_t* revs, uint32_t n_revs, const uint8_t* dom8, uint32_t* keytab,
                    cudaStream_t s);
 

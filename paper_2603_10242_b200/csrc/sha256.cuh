@@ -29,6 +29,33 @@ __device__ __constant__ static const uint32_t kSha256IV[8] = {
      0xc67178f2u}
 
 __device__ __forceinline__ uint32_t rotr32(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+// Pipe balancing. A compression is ~16 ALU-only operations per round (SHF
+// rotations, LOP3 for Sigma/Ch/Maj) plus ~9 additions; the integer ALU pipe
+// and the FMA pipe each take one warp instruction per 2 cycles per SMSP, and
+// ptxas puts most additions on the ALU (IADD3). Writing the additions as
+// x * kOne + y, with a constant-bank multiplier ptxas cannot fold, issues
+// them as IMAD on the otherwise idle FMA pipe (tools/sha_lat.cu: 14.1 ->
+// 16.2 G compressions/s on B200; the ALU-only floor is ~18 G/s).
+__device__ __constant__ static uint32_t kOne = 1;  // not const: must not fold
+__device__ __forceinline__ uint32_t madd(uint32_t x, uint32_t y) { return x * kOne + y; }
+// In situ the balanced form is NOT faster (bench, 100k block: device step
+// 0.586 / 0.589 / 0.613 / 0.622 ms for ACE_SHA_BAL = 0 / 1 / 3 / 7): the leaf
+// kernel runs ~5 warps per SMSP (80 registers, one wave) and the tree levels
+// are latency chains, so IMAD's longer latency costs more than the ALU issue
+// slots it frees. The product kernels therefore default to 0; the roofline
+// peak (acegpu_sha256_peak) uses the balanced form, the best compression
+// throughput measured on this GPU.
+#ifndef ACE_SHA_BAL
+#define ACE_SHA_BAL 0
+#endif
+// bit 0: schedule additions, bit 1: h + K + W (off the round's critical
+// path), bit 2: the e / a updates (on it)
+template <int BIT, int BAL = ACE_SHA_BAL>
+__device__ __forceinline__ uint32_t add_b(uint32_t x, uint32_t y) {
+    if constexpr ((BAL >> BIT) & 1) return madd(x, y);
+    else return x + y;
+}
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 __device__ __forceinline__ void sha256_init(uint32_t s[8]) {
@@ -37,6 +64,7 @@ __device__ __forceinline__ void sha256_init(uint32_t s[8]) {
 }
 
 // One compression. `w` is consumed (used as the rolling schedule window).
+template <int BAL = ACE_SHA_BAL>
 __device__ __forceinline__ void sha256_compress(uint32_t s[8], uint32_t w[16]) {
     constexpr uint32_t K[64] = ACE_K256;
     uint32_t a = s[0], b = s[1], c = s[2], d = s[3], e = s[4], f = s[5], g = s[6], h = s[7];
@@ -49,21 +77,21 @@ __device__ __forceinline__ void sha256_compress(uint32_t s[8], uint32_t w[16]) {
             uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
             uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
             uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
-            wi = w[i & 15] = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
+            wi = w[i & 15] = add_b<0, BAL>(w[i & 15] + s0, w[(i - 7) & 15] + s1);
         }
         uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
         uint32_t ch = (e & f) ^ (~e & g);
-        uint32_t t1 = h + S1 + ch + K[i] + wi;
+        uint32_t t1 = add_b<1, BAL>(h, K[i] + wi) + S1 + ch;
         uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
         uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
         h = g;
         g = f;
         f = e;
-        e = d + t1;
+        e = add_b<2, BAL>(d, t1);
         d = c;
         c = b;
         b = a;
-        a = t1 + S0 + mj;
+        a = add_b<2, BAL>(t1, S0 + mj);
     }
     s[0] += a; s[1] += b; s[2] += c; s[3] += d;
     s[4] += e; s[5] += f; s[6] += g; s[7] += h;
@@ -82,10 +110,11 @@ __device__ __constant__ static const uint32_t kK256c[64] = ACE_K256;
     do {                                                                     \
         uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);          \
         uint32_t ch = (e & f) ^ (~e & g);                                    \
-        uint32_t t1 = h + S1 + ch + kK256c[i] + (wi);                        \
+        uint32_t t1 = add_b<1>(h, kK256c[i] + (wi)) + S1 + ch;               \
         uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);          \
         uint32_t mj = (a & b) ^ (a & c) ^ (b & c);                           \
-        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj; \
+        h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a;                \
+        a = t1 + S0 + mj;                                                    \
     } while (0)
 
 __device__ __forceinline__ void sha256_compress_c(uint32_t s[8], uint32_t w[16]) {
@@ -99,7 +128,7 @@ __device__ __forceinline__ void sha256_compress_c(uint32_t s[8], uint32_t w[16])
             uint32_t w15 = w[(j + 1) & 15], w2 = w[(j + 14) & 15];
             uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
             uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
-            w[j] = w[j] + s0 + w[(j + 9) & 15] + s1;
+            w[j] = add_b<0>(w[j] + s0, w[(j + 9) & 15] + s1);
             ACE_SHA_ROUND(i0 + j, w[j]);
         }
     }
@@ -117,7 +146,7 @@ __device__ __forceinline__ void sha256_rounds_c(uint32_t s[8], WK wk) {
         for (int j = 0; j < 8; ++j) {
             uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
             uint32_t ch = (e & f) ^ (~e & g);
-            uint32_t t1 = h + S1 + ch + wk(i0 + j);
+            uint32_t t1 = add_b<1>(h, wk(i0 + j)) + S1 + ch;
             uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
             uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
             h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
@@ -153,7 +182,7 @@ __device__ __forceinline__ void sha256_schedule_wk(const uint32_t w_in[16], uint
             uint32_t w15 = w[(i - 15) & 15], w2 = w[(i - 2) & 15];
             uint32_t s0 = rotr32(w15, 7) ^ rotr32(w15, 18) ^ (w15 >> 3);
             uint32_t s1 = rotr32(w2, 17) ^ rotr32(w2, 19) ^ (w2 >> 10);
-            wi = w[i & 15] = w[i & 15] + s0 + w[(i - 7) & 15] + s1;
+            wi = w[i & 15] = add_b<0>(w[i & 15] + s0, w[(i - 7) & 15] + s1);
         }
         wk[i * stride] = wi + K[i];
     }
@@ -167,7 +196,7 @@ __device__ __forceinline__ void sha256_rounds(uint32_t s[8], WK wk) {
     for (int i = 0; i < 64; ++i) {
         uint32_t S1 = rotr32(e, 6) ^ rotr32(e, 11) ^ rotr32(e, 25);
         uint32_t ch = (e & f) ^ (~e & g);
-        uint32_t t1 = h + S1 + ch + wk(i);
+        uint32_t t1 = add_b<1>(h, wk(i)) + S1 + ch;
         uint32_t S0 = rotr32(a, 2) ^ rotr32(a, 13) ^ rotr32(a, 22);
         uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
         h = g;
