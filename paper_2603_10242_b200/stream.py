@@ -1,0 +1,156 @@
+"""Pipelined block prover: the sustained-stream form of ProverService
+(prover.hpp:141-172, prover.cpp:301-359).
+
+The reference's worker proves one block at a time. Here blocks are spread
+over `lanes` independent libacegpu contexts, each with its own CUDA stream,
+device workspace and pinned staging buffers, so block n+1's host->device copy
+and attestation run while block n's proof tree is still being hashed (a
+12,800-tx block's upper tree levels are latency chains that leave most SMs
+idle). Everything is stream-ordered and asynchronous from the submitting
+thread; per-block latency is taken from CUDA events on the lane's stream
+(submission of the H2D copy -> FC and verdicts back in pinned host memory).
+
+Device work goes through acegpu_attest_prove_certify_dev (include/acegpu.h).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .wire import FlatBlock
+
+
+@dataclass
+class StreamResult:
+    ticket: int
+    codes: np.ndarray      # n verdicts (AttestationCheck)
+    proof289: bytes
+    fc328: bytes
+    latency_ms: float      # device timeline: H2D start -> results in host memory
+
+
+class _Lane:
+    def __init__(self, device: int, max_tx: int, max_payload: int, max_revs: int):
+        import torch
+        self.ctx = N.Context(device)
+        self.dev = torch.device("cuda", device)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        u8 = dict(dtype=torch.uint8, device=self.dev)
+        self.d_pay = torch.empty(max_payload + 16, **u8)
+        self.d_offs = torch.empty(max_tx + 1, dtype=torch.int64, device=self.dev)
+        self.d_atts = torch.empty(104 * max_tx + 8, **u8)
+        self.d_hdr = torch.empty(256, **u8)
+        self.d_revs = torch.empty(32 * max_revs, **u8)
+        self.d_rix = torch.empty(max(max_tx, 1), dtype=torch.int32, device=self.dev)
+        self.d_codes = torch.empty(max(max_tx, 1), **u8)
+        self.d_out = torch.empty(640, **u8)
+        self.h_codes = torch.empty(max(max_tx, 1), dtype=torch.uint8).pin_memory()
+        self.h_out = torch.empty(640, dtype=torch.uint8).pin_memory()
+        self.ev0 = torch.cuda.Event(enable_timing=True)
+        self.ev1 = torch.cuda.Event(enable_timing=True)
+        self.ticket = None
+        self.n = 0
+
+
+class PipelinedProver:
+    """submit() enqueues a block (host FlatBlock, ideally in pinned memory) and
+    returns a ticket; result(ticket) waits for it. A lane is reused only after
+    its previous block's results were collected (FIFO per lane)."""
+
+    def __init__(self, lanes: int = 4, max_tx: int = 16384, max_payload: int | None = None,
+                 max_revs: int = 64, device: int | None = None):
+        dev = N.default_device() if device is None else device
+        self.max_tx = max_tx
+        self.max_payload = max_payload or 256 * max_tx
+        self.max_revs = max_revs
+        self.lanes = [_Lane(dev, max_tx, self.max_payload, max_revs) for _ in range(lanes)]
+        self.next_ticket = 0
+        self.done: dict[int, StreamResult] = {}
+
+    def _collect(self, lane: _Lane) -> None:
+        if lane.ticket is None:
+            return
+        lane.ev1.synchronize()
+        n = lane.n
+        out = lane.h_out.numpy()
+        self.done[lane.ticket] = StreamResult(
+            lane.ticket, lane.h_codes.numpy()[:n].copy(), out[:289].tobytes(),
+            out[304:304 + 328].tobytes(), lane.ev0.elapsed_time(lane.ev1))
+        lane.ticket = None
+
+    def submit(self, fb: FlatBlock, revs: np.ndarray, rev_index: np.ndarray,
+               pinned: dict | None = None) -> int:
+        """pinned: optional dict of torch pinned CPU tensors with keys
+        payloads/offs/atts/header/revs/rev_index (skips staging copies)."""
+        import torch
+        n = fb.n
+        nb = int(fb.offs[n]) if n else 0
+        if n > self.max_tx or nb > self.max_payload or len(revs) > 32 * self.max_revs:
+            raise ValueError("block exceeds the PipelinedProver capacity")
+        t = self.next_ticket
+        self.next_ticket += 1
+        lane = self.lanes[t % len(self.lanes)]
+        self._collect(lane)
+        if pinned is None:
+            pinned = pin_block(fb, revs, rev_index)
+        with torch.cuda.stream(lane.stream):
+            lane.ev0.record(lane.stream)
+            if n:
+                lane.d_pay[:nb].copy_(pinned["payloads"][:nb], non_blocking=True)
+                lane.d_offs[:n + 1].copy_(pinned["offs"][:n + 1], non_blocking=True)
+                lane.d_atts[:104 * n].copy_(pinned["atts"][:104 * n], non_blocking=True)
+                lane.d_rix[:n].copy_(pinned["rev_index"][:n], non_blocking=True)
+            lane.d_hdr.copy_(pinned["header"], non_blocking=True)
+            nr = len(revs) // 32
+            lane.d_revs[:32 * nr].copy_(pinned["revs"][:32 * nr], non_blocking=True)
+            lane.ctx.call("acegpu_attest_prove_certify_dev", lane.stream.cuda_stream,
+                          lane.d_pay.data_ptr(), lane.d_offs.data_ptr(), lane.d_atts.data_ptr(),
+                          n, lane.d_hdr.data_ptr(), lane.d_revs.data_ptr(), nr,
+                          lane.d_rix.data_ptr(), lane.d_codes.data_ptr() if n else None,
+                          lane.d_out.data_ptr(), lane.d_out.data_ptr() + 304)
+            if n:
+                lane.h_codes[:n].copy_(lane.d_codes[:n], non_blocking=True)
+            lane.h_out.copy_(lane.d_out, non_blocking=True)
+            lane.ev1.record(lane.stream)
+        lane.ticket, lane.n = t, n
+        return t
+
+    def result(self, ticket: int) -> StreamResult:
+        if ticket not in self.done:
+            lane = self.lanes[ticket % len(self.lanes)]
+            if lane.ticket != ticket:
+                raise KeyError(f"ticket {ticket} unknown or already collected")
+            self._collect(lane)
+        return self.done.pop(ticket)
+
+    def drain(self) -> list[StreamResult]:
+        for lane in self.lanes:
+            self._collect(lane)
+        out = [self.done.pop(k) for k in sorted(self.done)]
+        return out
+
+    def close(self) -> None:
+        for lane in self.lanes:
+            lane.ctx.close()
+
+
+def pin_block(fb: FlatBlock, revs: np.ndarray, rev_index: np.ndarray) -> dict:
+    """Host block -> pinned torch tensors (done once per block, off the hot loop)."""
+    import torch
+
+    def pin(a, dtype=None):
+        t = torch.from_numpy(np.ascontiguousarray(a if dtype is None else a.view(dtype)))
+        return t.pin_memory()
+    n = fb.n
+    return {
+        "payloads": pin(fb.payloads),
+        "offs": pin(np.ascontiguousarray(fb.offs, np.uint64), np.int64),
+        "atts": pin(fb.atts),
+        "header": pin(fb.header if isinstance(fb.header, np.ndarray)
+                      else np.frombuffer(bytes(fb.header), np.uint8)),
+        "revs": pin(np.ascontiguousarray(revs, np.uint8)),
+        "rev_index": pin(np.ascontiguousarray(rev_index[:max(n, 1)] if n else np.zeros(1),
+                                              np.uint32), np.int32),
+    }

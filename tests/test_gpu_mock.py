@@ -439,3 +439,23 @@ def test_segmented_pipeline_equals_single_pass(P):
     assert (seg[2] == O.oracle_attest_codes(fb)).all()
     oproof, _, _ = O.oracle_prove_block(fb)
     assert seg[0] == oproof and seg[1] == O.oracle_build_fc(fb, oproof)
+
+
+def test_pipelined_prover_stream():
+    """Sustained-stream prover (stream.py): consecutive blocks over pipelined
+    lanes give the oracle's verdicts, proof and FC, in submission order."""
+    from paper_2603_10242_b200.stream import PipelinedProver
+    blocks = [O.forge(O.multi_user_block(n, 4), every=7, phase=2) for n in (1, 700, 1024, 3000, 333)]
+    pp = PipelinedProver(lanes=2, max_tx=4096, max_revs=8)
+    try:
+        tickets = [pp.submit(fb, fb.revs, fb.rev_index) for fb in blocks]
+        res = pp.drain()
+    finally:
+        pp.close()
+    assert [r.ticket for r in res] == tickets
+    for fb, r in zip(blocks, res):
+        assert (r.codes == O.oracle_attest_codes(fb)).all()
+        oproof, _, _ = O.oracle_prove_block(fb)
+        assert r.proof289 == oproof
+        assert r.fc328 == O.oracle_build_fc(fb, oproof)
+        assert r.latency_ms > 0
