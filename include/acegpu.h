@@ -253,6 +253,36 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                uint8_t* d_codes, const uint8_t* d_witness256,
                                uint8_t* d_roots289, uint8_t* d_merkle32);
 
+/* ---- Phase 1a on the GPU --------------------------------
+ * attest_check_light (pipeline.cpp:20-42; LightCheck, pipeline.hpp:32-37):
+ * codes[i] = 0 AcceptPendingProof, 1 PayloadBinding, 2 UnknownIdentity,
+ * 3 StaleDomain. The IdentityRegistry (pipeline.hpp:22-30, a std::set<Hash32>)
+ * is passed as n_registry 32-B commitments sorted ascending (bytewise), which
+ * is the set's iteration order; window = PipelineConfig::domain_window_slots.
+ * counters3 (host, optional): LightCheckCounters {sha256_ops, registry_probes,
+ * window_checks} summed over the batch (pipeline.hpp:41-52). */
+int acegpu_light_check(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
+                       const uint8_t* atts, uint64_t n, const uint8_t* registry32,
+                       uint64_t n_registry, uint64_t current_slot, uint64_t window_slots,
+                       uint8_t* codes, uint64_t* counters3);
+int acegpu_light_check_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
+                           const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
+                           const uint8_t* d_registry32, uint64_t n_registry,
+                           uint64_t current_slot, uint64_t window_slots, uint8_t* d_codes,
+                           uint8_t* d_tx_hashes /* n x 32 SHA-256(payload), or NULL */);
+/* Block build (process_slot, pipeline.cpp:132-145): order-preserving
+ * compaction of the txs with d_codes[i] == 0 (all txs when d_codes is NULL)
+ * into the out arrays (out_offs: n_accepted + 1 entries, rebased to 0), and the
+ * 256-B header = header_tmpl with tx_count, tx_merkle_root, attest_merkle_root
+ * set (wire.cpp:74-96, 257-273). The result is device-resident, ready for
+ * acegpu_attest_prove_certify_dev. *n_accepted is written to HOST memory (the
+ * call synchronises `stream` once to read it). */
+int acegpu_build_block_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
+                           const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
+                           const uint8_t* d_codes, const uint8_t* d_header_tmpl,
+                           uint8_t* d_out_payloads, uint64_t* d_out_offs, uint8_t* d_out_atts,
+                           uint8_t* d_out_header, uint64_t* n_accepted);
+
 /* Integer-pipe microbenchmarks (roofline denominators for MSM / NTT). */
 int acegpu_imad_peak(acegpu_ctx* ctx, double* imad_per_s);
 int acegpu_bn_mul_rate(acegpu_ctx* ctx, int field, double* muls_per_s);

@@ -338,6 +338,45 @@ void or_merkle_root(const uint8_t* leaves, uint64_t n, uint8_t out[32]) {
     free(lvl);
 }
 
+/* ------------------------------------------------------------- phase 1a --*/
+/* pipeline.cpp:20-42: payload binding first, then the registry probe
+ * (std::set<Hash32>::count == binary search over the sorted ids), then the
+ * domain window |slot - current| <= w, written without underflow. */
+int or_attest_check_light(const uint8_t* payload, uint64_t len, const uint8_t att[104],
+                          const uint8_t* registry, uint64_t n_reg, uint64_t current_slot,
+                          uint64_t window_slots) {
+    uint8_t h[32];
+    or_sha256(payload, len, h);
+    if (memcmp(h, att, 32) != 0) return 1;
+    uint64_t lo = 0, hi = n_reg;
+    int found = 0;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        int c = memcmp(registry + 32 * mid, att + 32, 32);
+        if (c == 0) {
+            found = 1;
+            break;
+        }
+        if (c < 0) lo = mid + 1;
+        else hi = mid;
+    }
+    if (!found) return 2;
+    uint64_t slot = 0;
+    for (int i = 0; i < 6; ++i) slot = (slot << 8) | att[66 + i];  /* Domain: u16 chain | u48 slot */
+    int fresh = slot <= current_slot + window_slots && current_slot <= slot + window_slots;
+    return fresh ? 0 : 3;
+}
+
+void or_block_roots(const uint8_t* payloads, const uint64_t* offs, const uint8_t* atts,
+                    uint64_t n, uint8_t tx_root[32], uint8_t att_root[32]) {
+    uint8_t* lv = (uint8_t*)calloc(n ? n : 1, 32);
+    for (uint64_t i = 0; i < n; ++i) or_sha256(payloads + offs[i], offs[i + 1] - offs[i], lv + 32 * i);
+    or_merkle_root(lv, n, tx_root);
+    for (uint64_t i = 0; i < n; ++i) or_sha256(atts + 104 * i, 104, lv + 32 * i);
+    or_merkle_root(lv, n, att_root);
+    free(lv);
+}
+
 /* ---------------------------------------------------------------- prover --*/
 static const char kTagTx[] = "zk-tx-proof-v1";       /* prover.cpp:14 */
 static const char kTagAgg[] = "zk-agg-proof-v1";     /* prover.cpp:15 */

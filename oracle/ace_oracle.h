@@ -62,6 +62,15 @@ void or_make_transfer_payload(const uint8_t from[32], const uint8_t to[32], uint
 void or_block_hash(const uint8_t header[256], uint8_t out[32]);
 void or_merkle_root(const uint8_t* leaves, uint64_t n, uint8_t out[32]);
 
+/* Phase 1a. attest_check_light (pipeline.cpp:20-42):
+ * 0 AcceptPendingProof, 1 PayloadBinding, 2 UnknownIdentity, 3 StaleDomain.
+ * registry = n_reg sorted 32-B id commitments (std::set<Hash32> order). */
+int or_attest_check_light(const uint8_t* payload, uint64_t len, const uint8_t att[104],
+                          const uint8_t* registry, uint64_t n_reg, uint64_t current_slot,
+                          uint64_t window_slots);
+/* tx_merkle_root / attest_merkle_root (wire.cpp:257-273). */
+void or_block_roots(const uint8_t* payloads, const uint64_t* offs, const uint8_t* atts,
+                    uint64_t n, uint8_t tx_root[32], uint8_t att_root[32]);
 void or_expand256(int kind, const uint8_t digest[32], uint8_t out[256]);
 void or_prove_public_inputs(const uint8_t pub160[160], uint8_t out289[289]);
 void or_prove_tx(const uint8_t* payload, uint64_t len, const uint8_t att[104], uint8_t out289[289]);

@@ -19,6 +19,7 @@
 #include "ace/bench.hpp"
 #include "ace/crypto.hpp"
 #include "ace/hkdf.hpp"
+#include "ace/pipeline.hpp"
 #include "ace/prover.hpp"
 #include "ace/sha256.hpp"
 #include "ace/thread_pool.hpp"
@@ -179,6 +180,31 @@ void ref_tx_merkle_root(const uint8_t* payloads, const uint64_t* offs, const uin
     Hash32 a = wire::attest_merkle_root(b.transactions);
     std::memcpy(tx_root, t.data(), 32);
     std::memcpy(att_root, a.data(), 32);
+}
+
+// pipeline::attest_check_light over a block, with the reference's own
+// IdentityRegistry; counters summed as process_slot does (pipeline.cpp:110-122).
+void ref_attest_check_light_batch(const uint8_t* payloads, const uint64_t* offs,
+                                  const uint8_t* atts, uint32_t n, const uint8_t* ids,
+                                  uint64_t n_ids, uint64_t current_slot, uint64_t window,
+                                  uint8_t* codes, uint64_t* counters3) {
+    uint8_t zero[256] = {0};
+    auto b = make_block(payloads, offs, atts, n, zero);
+    pipeline::IdentityRegistry reg;
+    for (uint64_t i = 0; i < n_ids; ++i) {
+        Hash32 h;
+        std::memcpy(h.data(), ids + 32 * i, 32);
+        reg.add(h);
+    }
+    pipeline::PipelineConfig cfg;
+    cfg.domain_window_slots = window;
+    pipeline::LightCheckCounters c;
+    for (uint32_t i = 0; i < n; ++i)
+        codes[i] = static_cast<uint8_t>(
+            pipeline::attest_check_light(b.transactions[i], reg, current_slot, cfg, &c));
+    counters3[0] = c.sha256_ops;
+    counters3[1] = c.registry_probes;
+    counters3[2] = c.window_checks;
 }
 
 void ref_prove_tx(const uint8_t* payload, uint64_t len, const uint8_t* att104, uint8_t* out289) {

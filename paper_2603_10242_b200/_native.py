@@ -77,6 +77,9 @@ _SIGS = {
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_shard_roots_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, u64, vp, vp,
                                              vp, vp, vp, vp]),
+    "acegpu_light_check": (C.c_int, [ctxp, vp, vp, vp, u64, vp, u64, u64, u64, vp, u64p]),
+    "acegpu_light_check_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, u64, u64, u64, vp, vp]),
+    "acegpu_build_block_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, vp, vp, vp, vp, vp, u64p]),
     "acegpu_imad_peak": (C.c_int, [ctxp, C.POINTER(C.c_double)]),
     "acegpu_bn_mul_rate": (C.c_int, [ctxp, C.c_int, C.POINTER(C.c_double)]),
 }

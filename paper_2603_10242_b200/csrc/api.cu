@@ -16,6 +16,7 @@
 #include "bn_kernels.cuh"
 #include "g16_kernels.cuh"
 #include "mock_kernels.cuh"
+#include "phase1.cuh"
 #include "msm.cuh"
 #include "ntt.cuh"
 
@@ -57,7 +58,7 @@ int fail(int code, const std::string& msg) {
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
     kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kSegRoots, kSegMerk,
-    kKeytab, kKeydom, kNumSlots
+    kKeytab, kKeydom, kP1Scratch, kP1Hash, kP1Reg, kNumSlots
 };
 
 struct DevBuf {
@@ -724,6 +725,111 @@ int acegpu_verify_fc(acegpu_ctx* c, const uint8_t* fc, const uint8_t* payloads,
     else if (std::memcmp(expect + 40, fc + 40, 256) != 0) *out_check = 3;
     else if (std::memcmp(expect + 296, fc + 296, 32) != 0) *out_check = 3;
     else *out_check = 0;
+    return ACEGPU_OK;
+}
+
+// ---- Phase 1a ----------------------------------------------------------
+int acegpu_light_check_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                           const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                           const uint8_t* registry, uint64_t n_registry, uint64_t current_slot,
+                           uint64_t window_slots, uint8_t* codes, uint8_t* tx_hashes) {
+    RET(check_n(n));
+    if (n == 0) return ACEGPU_OK;
+    if (!codes || (n_registry && !registry)) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    launch_light_check(payloads, offs, atts, uint32_t(n), registry, n_registry, current_slot,
+                       window_slots, codes, tx_hashes, pick(c, stream));
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
+}
+
+int acegpu_light_check(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                       const uint8_t* atts, uint64_t n, const uint8_t* registry,
+                       uint64_t n_registry, uint64_t current_slot, uint64_t window_slots,
+                       uint8_t* codes, uint64_t* counters3) {
+    RET(check_n(n));
+    if (counters3) counters3[0] = counters3[1] = counters3[2] = 0;
+    if (n == 0) return ACEGPU_OK;
+    if (!codes || (n_registry && !registry)) return fail(ACEGPU_EINVAL, "null argument");
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard g(c->device);
+        cudaStream_t s = c->stream;
+        uint8_t *dp, *da, *dr = nullptr, *dc;
+        uint64_t* doff;
+        RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+        if (n_registry) RET(h2d_t(c, kP1Reg, registry, 32 * n_registry, s, &dr));
+        RET(ws(c, kCodes, n, &dc));
+        launch_light_check(dp, doff, da, uint32_t(n), dr, n_registry, current_slot, window_slots,
+                           dc, nullptr, s);
+        CKL();
+        c->launches++;
+        CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
+    if (counters3) {  // every tx hashes its payload; later stages run only if reached
+        counters3[0] = n;
+        for (uint64_t i = 0; i < n; ++i) {
+            counters3[1] += codes[i] != 1;
+            counters3[2] += codes[i] == 0 || codes[i] == 3;
+        }
+    }
+    return ACEGPU_OK;
+}
+
+int acegpu_build_block_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                           const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                           const uint8_t* codes, const uint8_t* header_tmpl,
+                           uint8_t* out_payloads, uint64_t* out_offs, uint8_t* out_atts,
+                           uint8_t* out_header, uint64_t* n_accepted) {
+    RET(check_n(n));
+    if (!header_tmpl || !out_header || !out_offs || !n_accepted)
+        return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    uint8_t *scratch, *hash, *ma, *mb;
+    RET(ws(c, kP1Scratch, compact_scratch_bytes(uint32_t(n)), &scratch));
+    RET(ws(c, kP1Hash, 96ull * n + 64, &hash));
+    uint8_t *txh = hash, *ctxh = hash + 32ull * n, *cath = hash + 64ull * n,
+            *roots = hash + 96ull * n;
+    if (n) {
+        launch_sha256_varlen(payloads, offs, uint32_t(n), txh, s);  // tx Merkle leaves
+        CKL();
+        c->launches++;
+    }
+    uint32_t *d_count;
+    uint64_t* d_total;
+    CK(launch_compact(payloads, offs, atts, uint32_t(n), codes, txh, scratch, out_payloads,
+                      out_offs, out_atts, ctxh, cath, &d_count, &d_total, s));
+    c->launches += n ? 4 : 3;
+    uint32_t cnt = 0;
+    CK(cudaMemcpyAsync(&cnt, d_count, 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    // tx_merkle_root and attest_merkle_root over the accepted txs (wire.cpp:223-273)
+    if (cnt) {
+        RET(ws(c, kMerkA, 32ull * cnt, &ma));
+        RET(ws(c, kMerkB, 32ull * (cnt / 2 + 1), &mb));
+        for (int r = 0; r < 2; ++r) {
+            uint8_t *a = ma, *b = mb;
+            launch_merkle_leaves(r ? cath : ctxh, cnt, a, s);
+            CKL();
+            c->launches++;
+            for (uint32_t cur = cnt; cur > 1; cur = (cur + 1) / 2) {
+                launch_level(nullptr, 0, nullptr, a, cur, b, false, s);
+                CKL();
+                c->launches++;
+                std::swap(a, b);
+            }
+            CK(cudaMemcpyAsync(roots + 32 * r, a, 32, cudaMemcpyDeviceToDevice, s));
+        }
+    }
+    launch_header(header_tmpl, d_count, d_total, out_offs, roots, roots + 32, out_header, s);
+    CKL();
+    c->launches++;
+    *n_accepted = cnt;
     return ACEGPU_OK;
 }
 

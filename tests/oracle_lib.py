@@ -321,3 +321,78 @@ def forge(fb: FlatBlock, every: int = 8, phase: int = 7) -> FlatBlock:
             a[72:104] = hmac(key, bytes(a[0:32]) + bytes(a[64:72]))
         out.atts[104 * i:104 * (i + 1)] = np.frombuffer(bytes(a), np.uint8)
     return out
+
+
+# ------------------------------------------------------------- phase 1a
+def phase1_block(n: int, seed: int = 5, cur: int = 100, users: int = 6):
+    """Candidate txs for the light check (pipeline.cpp:20-42): honest txs of
+    `users` registered identities with domain slots in cur-4..cur+4, some
+    mutated payloads (PayloadBinding), some unregistered identities
+    (UnknownIdentity). Returns (FlatBlock, sorted registry ids (+ decoys), cur)."""
+    import random
+    rng = random.Random(seed)
+    revs = [rev_from_seed(0xB10C00 + u) for u in range(users + 2)]
+    a, b = b"\x01" * 32, b"\x02" * 32
+    payloads, atts = [], []
+    for i in range(n):
+        u = rng.randrange(users + 2)  # users, users+1: never registered
+        slot = cur + rng.randint(-4, 4)
+        dom = domain_encode(1, slot)
+        idc = id_commitment(revs[u], b"\0" * 32, 1, slot)
+        p = transfer_payload(a, b, 1 + i, i, b"\0" * 32)
+        att = generate_attestation(revs[u], p, dom, idc)
+        if rng.random() < 0.15:
+            p = bytearray(p)
+            p[rng.randrange(len(p))] ^= 1 << rng.randrange(8)
+            p = bytes(p)
+        payloads.append(p)
+        atts.append(att)
+    reg = set()
+    for u in range(users):
+        for slot in range(cur - 4, cur + 5):
+            reg.add(id_commitment(revs[u], b"\0" * 32, 1, slot))
+    for k in range(50):  # decoys
+        reg.add(sha256(b"decoy" + k.to_bytes(4, "big")))
+    fb = flat_from_lists(payloads, atts, encode_header(slot=cur), revs[:users], [0] * n)
+    return fb, sorted(reg), cur
+
+
+def oracle_light_check(fb: FlatBlock, reg: list[bytes], cur: int, window: int = 2) -> np.ndarray:
+    r = b"".join(reg) or b"\0" * 32
+    out = np.zeros(max(fb.n, 1), np.uint8)
+    for i in range(fb.n):
+        p = fb.payload(i)
+        out[i] = oracle().or_attest_check_light(
+            ptr(p), C.c_uint64(len(p)), ptr(fb.atts[104 * i:104 * i + 104].tobytes()), ptr(r),
+            C.c_uint64(len(reg)), C.c_uint64(cur), C.c_uint64(window))
+    return out[:fb.n]
+
+
+def ref_light_check(fb: FlatBlock, reg: list[bytes], cur: int, window: int = 2):
+    r = b"".join(reg) or b"\0" * 32
+    codes = np.zeros(max(fb.n, 1), np.uint8)
+    cnt = np.zeros(3, np.uint64)
+    ref().ref_attest_check_light_batch(*_blk_args(fb), ptr(r), C.c_uint64(len(reg)),
+                                       C.c_uint64(cur), C.c_uint64(window),
+                                       np_ptr(codes, C.c_uint8), np_ptr(cnt, C.c_uint64))
+    return codes[:fb.n], [int(x) for x in cnt]
+
+
+def oracle_block_roots(fb: FlatBlock) -> tuple[bytes, bytes]:
+    t, a = buf(32), buf(32)
+    oracle().or_block_roots(np_ptr(fb.payloads, C.c_uint8), np_ptr(fb.offs, C.c_uint64),
+                            np_ptr(fb.atts, C.c_uint8), C.c_uint64(fb.n), t, a)
+    return bytes(t), bytes(a)
+
+
+def ref_block_roots(fb: FlatBlock) -> tuple[bytes, bytes]:
+    t, a = buf(32), buf(32)
+    ref().ref_tx_merkle_root(*_blk_args(fb), t, a)
+    return bytes(t), bytes(a)
+
+
+def select(fb: FlatBlock, keep: np.ndarray, header: bytes) -> FlatBlock:
+    """The sub-block of the txs with keep[i] (order preserved)."""
+    idx = [i for i in range(fb.n) if keep[i]]
+    return flat_from_lists([fb.payload(i) for i in idx],
+                           [fb.atts[104 * i:104 * i + 104].tobytes() for i in idx], header)

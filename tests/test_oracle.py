@@ -203,3 +203,39 @@ def test_oracle_matches_reference_random():
         lib.or_merkle_root(O.ptr(leaves), C.c_uint64(n), a)
         R.ref_merkle_root(O.ptr(leaves), C.c_uint64(n), b)
         assert bytes(a) == bytes(b)
+
+
+# ---------------------------------------------------------------- phase 1a
+def test_light_check_oracle_vs_reference():
+    """attest_check_light (pipeline.cpp:20-42): the C restatement against the
+    reference's own function and IdentityRegistry, codes and counters."""
+    if not O.ref_available():
+        pytest.skip("reference build not available")
+    fb, reg, cur = O.phase1_block(600, seed=11)
+    for window in (0, 2, 3):
+        oc = O.oracle_light_check(fb, reg, cur, window)
+        rc, cnt = O.ref_light_check(fb, reg, cur, window)
+        assert (oc == rc).all()
+        assert set(np.unique(oc)) == {0, 1, 2, 3}
+        assert cnt == [fb.n, int((oc != 1).sum()), int(((oc == 0) | (oc == 3)).sum())]
+
+
+def test_light_check_window_edges():
+    """test_pipeline.cpp:72-81: slot +-2 accepted, +-3 stale (window 2)."""
+    fb, reg, cur = O.phase1_block(1, seed=3)
+    rev = O.rev_from_seed(0xB10C00)
+    dom = O.domain_encode(1, 50)
+    idc = O.id_commitment(rev, b"\0" * 32, 1, 50)
+    p = O.transfer_payload(b"\x01" * 32, b"\x02" * 32, 5, 0, b"\0" * 32)
+    one = O.flat_from_lists([p], [O.generate_attestation(rev, p, dom, idc)], O.encode_header())
+    for cur, want in ((50, 0), (52, 0), (53, 3), (48, 0), (47, 3)):
+        assert O.oracle_light_check(one, [idc], cur)[0] == want
+    assert O.oracle_light_check(one, [], 50)[0] == 2
+
+
+def test_block_roots_oracle_vs_reference():
+    if not O.ref_available():
+        pytest.skip("reference build not available")
+    for n in (0, 1, 2, 3, 17, 300):
+        fb, _, _ = O.phase1_block(n, seed=n)
+        assert O.oracle_block_roots(fb) == O.ref_block_roots(fb)
