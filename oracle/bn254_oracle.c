@@ -866,3 +866,429 @@ int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w_in, const uint8_t* 
     free(c);
     return feq(&lhs, &rhs);
 }
+
+/* ======================================================================
+ * Optimal ate pairing (TEST INFRASTRUCTURE: the CPU checker of record for
+ * the GPU verifier). Written for clarity, not speed:
+ *   tower  Fq2 = Fq[u]/(u^2+1), Fq6 = Fq2[v]/(v^3 - xi), xi = 9+u,
+ *          Fq12 = Fq6[w]/(w^2 - v)   (so w^6 = xi);
+ *   G2 on the D-type sextic twist y^2 = x^3 + 3/xi, untwisted by
+ *          (x, y) -> (x w^2, y w^3);
+ *   Miller loop over 6x+2 with AFFINE doubling/addition steps (one Fq2
+ *          inversion per step), lines  l(P) = yP - lambda xP w + (lambda xT - yT) w^3,
+ *          then the two Frobenius-twisted additions pi(Q), -pi^2(Q);
+ *   final exponentiation by (p^12-1)/r = (p^6-1)(p^2+1) * h, h = (p^4-p^2+1)/r,
+ *          as f^(p^6-1) = conj(f)/f, then plain square-and-multiply by p^2
+ *          and by h (exponents below are derived constants: p, r, x of
+ *          SURVEY Appendix C; tests/test_bn254_oracle.py re-derives them).
+ * ==================================================================== */
+typedef struct { fe2 c0, c1, c2; } fe6;
+typedef struct { fe6 c0, c1; } fe12;
+
+/* 6x+2, x = 4965661367192848881 (65 bits) */
+static const uint64_t ATE_LOOP[2] = {0x9d797039be763ba8ull, 0x1ull};
+/* p^2 (508 bits), little-endian 64-bit limbs */
+static uint64_t P2_EXP[8];
+/* h = (p^4 - p^2 + 1) / r (761 bits) */
+static const char* H_HEX =
+    "1baaa710b0759ad331ec15183177faf6c0eb522d5b122784e529a5861876f6b3b1b1355d189227d79581e16f3fd9"
+    "0c66b887d56d5095f23aaa441e3954bcf8adcc7b44c87cdbacff1154e7e1da014fd5abf5cc4f49c36d4e81bb482c"
+    "cdf42b1";
+static uint64_t H_EXP[12];
+static int pairing_ready = 0;
+static fe2 XI, G12, G13;  /* xi, xi^((p-1)/3), xi^((p-1)/2) (Montgomery) */
+
+static void f2zero(fe2* o) { memset(o, 0, sizeof *o); }
+static void f2one(fe2* o) { memset(o, 0, sizeof *o); memcpy(o->c0.v, FQ.one, 32); }
+static void f2neg(const fe2* a, fe2* o) { fe2 z; f2zero(&z); f2sub(&z, a, o); }
+static void f2conj(const fe2* a, fe2* o) { fe z = {{0}}; o->c0 = a->c0; fsub(&FQ, &z, &a->c1, &o->c1); }
+static void f2mul_fe(const fe2* a, const fe* s, fe2* o) {
+    fmul(&FQ, &a->c0, s, &o->c0);
+    fmul(&FQ, &a->c1, s, &o->c1);
+}
+
+static void f2pow(const fe2* a, const uint64_t* e, int limbs, fe2* o) {
+    fe2 r, b = *a;
+    f2one(&r);
+    for (int i = 0; i < 64 * limbs; ++i) {
+        if (e[i >> 6] >> (i & 63) & 1) f2mul(&r, &b, &r);
+        f2mul(&b, &b, &b);
+    }
+    *o = r;
+}
+
+static void f6add(const fe6* a, const fe6* b, fe6* o) {
+    f2add(&a->c0, &b->c0, &o->c0); f2add(&a->c1, &b->c1, &o->c1); f2add(&a->c2, &b->c2, &o->c2);
+}
+static void f6sub(const fe6* a, const fe6* b, fe6* o) {
+    f2sub(&a->c0, &b->c0, &o->c0); f2sub(&a->c1, &b->c1, &o->c1); f2sub(&a->c2, &b->c2, &o->c2);
+}
+static void f6mul(const fe6* a, const fe6* b, fe6* o) {
+    fe2 t, u, c0, c1, c2;
+    /* c0 = a0b0 + xi(a1b2 + a2b1) */
+    f2mul(&a->c1, &b->c2, &t); f2mul(&a->c2, &b->c1, &u); f2add(&t, &u, &t);
+    f2mul(&t, &XI, &t); f2mul(&a->c0, &b->c0, &u); f2add(&t, &u, &c0);
+    /* c1 = a0b1 + a1b0 + xi a2b2 */
+    f2mul(&a->c2, &b->c2, &t); f2mul(&t, &XI, &t);
+    f2mul(&a->c0, &b->c1, &u); f2add(&t, &u, &t);
+    f2mul(&a->c1, &b->c0, &u); f2add(&t, &u, &c1);
+    /* c2 = a0b2 + a1b1 + a2b0 */
+    f2mul(&a->c0, &b->c2, &t); f2mul(&a->c1, &b->c1, &u); f2add(&t, &u, &t);
+    f2mul(&a->c2, &b->c0, &u); f2add(&t, &u, &c2);
+    o->c0 = c0; o->c1 = c1; o->c2 = c2;
+}
+static void f6mul_v(const fe6* a, fe6* o) {  /* (a0 + a1 v + a2 v^2) v */
+    fe2 t;
+    f2mul(&a->c2, &XI, &t);
+    o->c2 = a->c1; o->c1 = a->c0; o->c0 = t;
+}
+static void f6inv(const fe6* a, fe6* o) {
+    fe2 t0, t1, t2, s, d, di;
+    f2mul(&a->c0, &a->c0, &t0); f2mul(&a->c1, &a->c2, &s); f2mul(&s, &XI, &s); f2sub(&t0, &s, &t0);
+    f2mul(&a->c2, &a->c2, &t1); f2mul(&t1, &XI, &t1); f2mul(&a->c0, &a->c1, &s); f2sub(&t1, &s, &t1);
+    f2mul(&a->c1, &a->c1, &t2); f2mul(&a->c0, &a->c2, &s); f2sub(&t2, &s, &t2);
+    f2mul(&a->c2, &t1, &d); f2mul(&a->c1, &t2, &s); f2add(&d, &s, &d); f2mul(&d, &XI, &d);
+    f2mul(&a->c0, &t0, &s); f2add(&d, &s, &d);
+    f2inv(&d, &di);
+    f2mul(&t0, &di, &o->c0); f2mul(&t1, &di, &o->c1); f2mul(&t2, &di, &o->c2);
+}
+static void f12one(fe12* o) { memset(o, 0, sizeof *o); f2one(&o->c0.c0); }
+static void f12mul(const fe12* a, const fe12* b, fe12* o) {
+    fe6 t0, t1, t2, t3;
+    f6mul(&a->c0, &b->c0, &t0);
+    f6mul(&a->c1, &b->c1, &t1);
+    f6mul_v(&t1, &t1);
+    f6mul(&a->c0, &b->c1, &t2);
+    f6mul(&a->c1, &b->c0, &t3);
+    f6add(&t0, &t1, &o->c0);
+    f6add(&t2, &t3, &o->c1);
+}
+static void f12conj(const fe12* a, fe12* o) {
+    fe6 z;
+    memset(&z, 0, sizeof z);
+    o->c0 = a->c0;
+    f6sub(&z, &a->c1, &o->c1);
+}
+static void f12inv(const fe12* a, fe12* o) {
+    fe6 t0, t1, d, di;
+    f6mul(&a->c0, &a->c0, &t0);
+    f6mul(&a->c1, &a->c1, &t1);
+    f6mul_v(&t1, &t1);
+    f6sub(&t0, &t1, &d);
+    f6inv(&d, &di);
+    fe12 c;
+    f12conj(a, &c);
+    f6mul(&c.c0, &di, &o->c0);
+    f6mul(&c.c1, &di, &o->c1);
+}
+static void f12pow(const fe12* a, const uint64_t* e, int limbs, fe12* o) {
+    fe12 r, b = *a;
+    f12one(&r);
+    int top = 64 * limbs - 1;
+    while (top >= 0 && !(e[top >> 6] >> (top & 63) & 1)) --top;
+    for (int i = top; i >= 0; --i) {
+        f12mul(&r, &r, &r);
+        if (e[i >> 6] >> (i & 63) & 1) f12mul(&r, &b, &r);
+    }
+    *o = r;
+}
+static int f12is_one(const fe12* a) {
+    fe12 one;
+    f12one(&one);
+    return !memcmp(a, &one, sizeof one);
+}
+
+static void hex_to_limbs(const char* h, uint64_t* out, int limbs) {
+    memset(out, 0, 8 * limbs);
+    int n = (int)strlen(h);
+    for (int i = 0; i < n; ++i) {
+        char ch = h[n - 1 - i];
+        uint64_t d = (ch >= '0' && ch <= '9') ? (uint64_t)(ch - '0') : (uint64_t)((ch | 32) - 'a' + 10);
+        out[i / 16] |= d << (4 * (i % 16));
+    }
+}
+
+static void pairing_init(void) {
+    if (pairing_ready) return;
+    uint8_t nine[32] = {9}, one[32] = {1};
+    to_mont(&FQ, nine, &XI.c0);
+    to_mont(&FQ, one, &XI.c1);
+    /* p^2 by schoolbook 4x4 limbs */
+    memset(P2_EXP, 0, sizeof P2_EXP);
+    for (int i = 0; i < 4; ++i) {
+        uint64_t c = 0;
+        for (int j = 0; j < 4; ++j) {
+            u128 x = (u128)FQ.m[i] * FQ.m[j] + P2_EXP[i + j] + c;
+            P2_EXP[i + j] = (uint64_t)x;
+            c = (uint64_t)(x >> 64);
+        }
+        P2_EXP[i + 4] = c;
+    }
+    hex_to_limbs(H_HEX, H_EXP, 12);
+    /* (p-1)/3 and (p-1)/2 by long division of the 256-bit p-1 */
+    uint64_t pm1[4];
+    memcpy(pm1, FQ.m, 32);
+    pm1[0] -= 1;
+    uint64_t q3[4], q2[4];
+    u128 rem = 0;
+    for (int i = 3; i >= 0; --i) {
+        u128 cur = (rem << 64) | pm1[i];
+        q3[i] = (uint64_t)(cur / 3);
+        rem = cur % 3;
+    }
+    for (int i = 0; i < 4; ++i) q2[i] = (pm1[i] >> 1) | (i < 3 ? pm1[i + 1] << 63 : 0);
+    f2pow(&XI, q3, 4, &G12);
+    f2pow(&XI, q2, 4, &G13);
+    pairing_ready = 1;
+}
+
+/* Line through T and (the untwisted) step point with slope lambda, at P:
+ * yP + (-lambda xP) w + (lambda xT - yT) w^3 -> Fq6 parts (w^3 = v w). */
+static void line_eval(const fe2* lambda, const fe2* xT, const fe2* yT, const fe* xP,
+                      const fe* yP, fe12* l) {
+    memset(l, 0, sizeof *l);
+    l->c0.c0.c0 = *yP;
+    fe2 t;
+    f2mul_fe(lambda, xP, &t);
+    f2neg(&t, &l->c1.c0);
+    f2mul(lambda, xT, &t);
+    f2sub(&t, yT, &l->c1.c1);
+}
+
+typedef struct { fe2 x, y; int inf; } aff2;
+
+static void step_dbl(aff2* T, const fe* xP, const fe* yP, fe12* l) {
+    fe2 num, den, lam, x2, t;
+    f2mul(&T->x, &T->x, &num);
+    f2add(&num, &num, &t);
+    f2add(&t, &num, &num);       /* 3x^2 */
+    f2add(&T->y, &T->y, &den);   /* 2y */
+    f2inv(&den, &den);
+    f2mul(&num, &den, &lam);
+    line_eval(&lam, &T->x, &T->y, xP, yP, l);
+    f2mul(&lam, &lam, &x2);
+    f2sub(&x2, &T->x, &x2);
+    f2sub(&x2, &T->x, &x2);
+    f2sub(&T->x, &x2, &t);
+    f2mul(&lam, &t, &t);
+    f2sub(&t, &T->y, &T->y);
+    T->x = x2;
+}
+
+static void step_add(aff2* T, const aff2* Q, const fe* xP, const fe* yP, fe12* l) {
+    fe2 num, den, lam, x3, t;
+    f2sub(&Q->y, &T->y, &num);
+    f2sub(&Q->x, &T->x, &den);
+    f2inv(&den, &den);
+    f2mul(&num, &den, &lam);
+    line_eval(&lam, &T->x, &T->y, xP, yP, l);
+    f2mul(&lam, &lam, &x3);
+    f2sub(&x3, &T->x, &x3);
+    f2sub(&x3, &Q->x, &x3);
+    f2sub(&T->x, &x3, &t);
+    f2mul(&lam, &t, &t);
+    f2sub(&t, &T->y, &T->y);
+    T->x = x3;
+}
+
+static void frob_twist(const aff2* Q, aff2* o) {  /* pi(Q) on the twist */
+    fe2 t;
+    f2conj(&Q->x, &t);
+    f2mul(&t, &G12, &o->x);
+    f2conj(&Q->y, &t);
+    f2mul(&t, &G13, &o->y);
+    o->inf = Q->inf;
+}
+
+static void miller(const uint8_t* g1, const uint8_t* g2, fe12* f) {
+    f12one(f);
+    if (bytes_zero(g1, 64) || bytes_zero(g2, 128)) return;
+    fe xP, yP;
+    to_mont(&FQ, g1, &xP);
+    to_mont(&FQ, g1 + 32, &yP);
+    aff2 Q, T;
+    to_mont(&FQ, g2, &Q.x.c0);
+    to_mont(&FQ, g2 + 32, &Q.x.c1);
+    to_mont(&FQ, g2 + 64, &Q.y.c0);
+    to_mont(&FQ, g2 + 96, &Q.y.c1);
+    Q.inf = 0;
+    T = Q;
+    fe12 l;
+    for (int i = 63; i >= 0; --i) {  /* bit 64 is the top bit of 6x+2 */
+        f12mul(f, f, f);
+        step_dbl(&T, &xP, &yP, &l);
+        f12mul(f, &l, f);
+        if (ATE_LOOP[i >> 6] >> (i & 63) & 1) {
+            step_add(&T, &Q, &xP, &yP, &l);
+            f12mul(f, &l, f);
+        }
+    }
+    aff2 Q1, Q2;
+    frob_twist(&Q, &Q1);
+    frob_twist(&Q1, &Q2);
+    f2neg(&Q2.y, &Q2.y);
+    step_add(&T, &Q1, &xP, &yP, &l);
+    f12mul(f, &l, f);
+    step_add(&T, &Q2, &xP, &yP, &l);
+    f12mul(f, &l, f);
+}
+
+static void final_exp(const fe12* f, fe12* o) {
+    fe12 a, b, c;
+    f12conj(f, &a);
+    f12inv(f, &b);
+    f12mul(&a, &b, &a);          /* f^(p^6 - 1) */
+    f12pow(&a, P2_EXP, 8, &c);
+    f12mul(&c, &a, &a);          /* ^(p^2 + 1) */
+    f12pow(&a, H_EXP, 12, o);    /* ^h */
+}
+
+static void store_f12(const fe12* f, uint8_t* out) {
+    const fe2* c[6] = {&f->c0.c0, &f->c0.c1, &f->c0.c2, &f->c1.c0, &f->c1.c1, &f->c1.c2};
+    for (int i = 0; i < 6; ++i) {
+        from_mont(&FQ, &c[i]->c0, out + 64 * i);
+        from_mont(&FQ, &c[i]->c1, out + 64 * i + 32);
+    }
+}
+
+void bn_pairing(uint64_t n, const uint8_t* g1s, const uint8_t* g2s, uint8_t* out384) {
+    pairing_init();
+    fe12 acc, f;
+    f12one(&acc);
+    for (uint64_t i = 0; i < n; ++i) {
+        miller(g1s + 64 * i, g2s + 128 * i, &f);
+        f12mul(&acc, &f, &acc);
+    }
+    final_exp(&acc, &f);
+    store_f12(&f, out384);
+}
+
+int bn_pairing_check(uint64_t n, const uint8_t* g1s, const uint8_t* g2s) {
+    pairing_init();
+    fe12 acc, f;
+    f12one(&acc);
+    for (uint64_t i = 0; i < n; ++i) {
+        miller(g1s + 64 * i, g2s + 128 * i, &f);
+        f12mul(&acc, &f, &acc);
+    }
+    final_exp(&acc, &f);
+    return f12is_one(&f);
+}
+
+void bn_f12_pow(const uint8_t* a384, const uint8_t* e32, uint8_t* out384) {
+    pairing_init();
+    fe12 a;
+    fe2* c[6] = {&a.c0.c0, &a.c0.c1, &a.c0.c2, &a.c1.c0, &a.c1.c1, &a.c1.c2};
+    for (int i = 0; i < 6; ++i) {
+        to_mont(&FQ, a384 + 64 * i, &c[i]->c0);
+        to_mont(&FQ, a384 + 64 * i + 32, &c[i]->c1);
+    }
+    uint64_t e[4];
+    memcpy(e, e32, 32);
+    fe12 r;
+    f12pow(&a, e, 4, &r);
+    store_f12(&r, out384);
+}
+
+/* ---- Groth16 verifying key and verifier for the synthetic circuit ----
+ * IC_0 (ONE) = ((beta u_1 + alpha v_1) / gamma) G1 and IC_{1+t} (pub_t) =
+ * (beta (L_{tK}(tau) + L_{TK+1+t}(tau)) / gamma) G1 (w = 0 for all public
+ * variables; u / v from the row layout in bn254_oracle.h). */
+int bn_g16_vk(uint32_t T, uint32_t K, const uint8_t* trap, uint8_t* out) {
+    const uint64_t m = (uint64_t)T * K + T + 1;
+    uint32_t logn = 0;
+    while ((1ull << logn) < m) ++logn;
+    const uint64_t N = 1ull << logn;
+    fe tau, alpha, beta, gamma, one, w, tN, Z, nN, Ninv, coef, t1, t2;
+    fr_from_le_bytes(trap, &tau);
+    fr_from_le_bytes(trap + 32, &alpha);
+    fr_from_le_bytes(trap + 64, &beta);
+    fr_from_le_bytes(trap + 96, &gamma);
+    memcpy(one.v, FR.one, 32);
+    fr_root(logn, 0, &w);
+    uint64_t e[4] = {N, 0, 0, 0};
+    fpow(&FR, &tau, e, &tN);
+    fsub(&FR, &tN, &one, &Z);
+    uint8_t nb[32] = {0};
+    memcpy(nb, &N, 8);
+    to_mont(&FR, nb, &nN);
+    finv(&FR, &nN, &Ninv);
+    fmul(&FR, &Z, &Ninv, &coef);
+    /* L_j(tau) on demand: coef * w^j / (tau - w^j) */
+    fe* wj = (fe*)malloc(sizeof(fe) * m);
+    fe cur = one;
+    for (uint64_t j = 0; j < m; ++j) { wj[j] = cur; fmul(&FR, &cur, &w, &cur); }
+    #define LJ(j, o) do { fe d_, di_; fsub(&FR, &tau, &wj[j], &d_); finv(&FR, &d_, &di_); \
+        fmul(&FR, &di_, &wj[j], o); fmul(&FR, o, &coef, o); } while (0)
+    fe* c = (fe*)malloc(sizeof(fe) * (K > 1 ? K : 2));
+    for (uint32_t k = 1; k < K; ++k) {
+        uint8_t b[32];
+        bn_g16_chain_const(k, b);
+        to_mont(&FR, b, &c[k]);
+    }
+    fe u1 = {{0}}, v1 = {{0}}, gi, L;
+    for (uint32_t t = 0; t < T; ++t) {
+        const uint64_t R = (uint64_t)t * K;
+        LJ(R, &L);
+        fadd(&FR, &v1, &L, &v1);
+        for (uint32_t k = 1; k < K; ++k) {
+            LJ(R + k, &L);
+            fmul(&FR, &c[k], &L, &t1);
+            fadd(&FR, &u1, &t1, &u1);
+            fadd(&FR, &v1, &t1, &v1);
+        }
+    }
+    LJ((uint64_t)T * K, &L);
+    fadd(&FR, &u1, &L, &u1);
+    finv(&FR, &gamma, &gi);
+    uint8_t* sc = (uint8_t*)malloc(32ull * (T + 1));
+    fmul(&FR, &beta, &u1, &t1);
+    fmul(&FR, &alpha, &v1, &t2);
+    fadd(&FR, &t1, &t2, &t1);
+    fmul(&FR, &t1, &gi, &t1);
+    from_mont(&FR, &t1, sc);
+    for (uint32_t t = 0; t < T; ++t) {
+        fe La, Lb;
+        LJ((uint64_t)t * K, &La);
+        LJ((uint64_t)T * K + 1 + t, &Lb);
+        fadd(&FR, &La, &Lb, &t1);
+        fmul(&FR, &t1, &beta, &t1);
+        fmul(&FR, &t1, &gi, &t1);
+        from_mont(&FR, &t1, sc + 32ull * (t + 1));
+    }
+    #undef LJ
+    uint8_t g1[64], g2[128];
+    bn_generator(1, g1);
+    bn_generator(2, g2);
+    bn_scalar_mul(1, g1, trap + 32, out);          /* alpha G1 */
+    bn_scalar_mul(2, g2, trap + 64, out + 64);     /* beta G2 */
+    bn_scalar_mul(2, g2, trap + 96, out + 192);    /* gamma G2 */
+    bn_scalar_mul(2, g2, trap + 128, out + 320);   /* delta G2 */
+    bn_fixed_base_muls(1, g1, sc, T + 1, out + 448, 8);
+    free(sc);
+    free(c);
+    free(wj);
+    return 0;
+}
+
+/* e(A, B) == e(alpha, beta) e(sum_i z_i IC_i, gamma) e(C, delta), z = (1, pub).
+ * vk layout of bn_g16_vk; abc = A (64) | B (128) | C (64), oracle encodings. */
+int bn_g16_verify(uint32_t T, const uint8_t* vk, const uint8_t* abc, const uint8_t* pubs) {
+    uint8_t* sc = (uint8_t*)malloc(32ull * (T + 1));
+    memset(sc, 0, 32);
+    sc[0] = 1;
+    memcpy(sc + 32, pubs, 32ull * T);
+    uint8_t Lp[64];
+    bn_msm(1, vk + 448, sc, T + 1, Lp, 8);
+    free(sc);
+    uint8_t g1[4 * 64], g2[4 * 128];
+    memcpy(g1, abc, 64);
+    memcpy(g2, abc + 64, 128);
+    bn_point_neg(1, vk, g1 + 64);          /* -alpha, beta */
+    memcpy(g2 + 128, vk + 64, 128);
+    bn_point_neg(1, Lp, g1 + 128);         /* -L, gamma */
+    memcpy(g2 + 256, vk + 192, 128);
+    bn_point_neg(1, abc + 192, g1 + 192);  /* -C, delta */
+    memcpy(g2 + 384, vk + 320, 128);
+    return bn_pairing_check(4, g1, g2);
+}

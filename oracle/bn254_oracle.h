@@ -71,6 +71,19 @@ int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w, const uint8_t* pub
                     const uint8_t* trapdoor5, const uint8_t* rs2, uint8_t* out_abc3,
                     int threads);
 
+/* ---- optimal ate pairing (tower Fq2/Fq6/Fq12 over xi = 9+u) ----
+ * Fq12 encoding: 12 x 32-B LE standard form, order c0.c0.c0, c0.c0.c1,
+ * c0.c1.c0, ..., c1.c2.c1 (Fq12 = Fq6 + Fq6 w, Fq6 = Fq2 + Fq2 v + Fq2 v^2).
+ * bn_pairing: prod_i e(P_i, Q_i) after the final exponentiation;
+ * bn_pairing_check: 1 iff that product is 1. */
+void bn_pairing(uint64_t n, const uint8_t* g1s, const uint8_t* g2s, uint8_t* out384);
+int bn_pairing_check(uint64_t n, const uint8_t* g1s, const uint8_t* g2s);
+void bn_f12_pow(const uint8_t* a384, const uint8_t* e32, uint8_t* out384);
+/* Verifying key: alpha G1 (64) | beta G2 (128) | gamma G2 (128) | delta G2 (128)
+ * | IC_0..IC_T (64 each) = 448 + 64 (T + 1) bytes. */
+int bn_g16_vk(uint32_t T, uint32_t K, const uint8_t* trapdoor5, uint8_t* out);
+int bn_g16_verify(uint32_t T, const uint8_t* vk, const uint8_t* abc, const uint8_t* pubs);
+
 #ifdef __cplusplus
 }
 #endif
