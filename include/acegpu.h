@@ -239,6 +239,20 @@ int acegpu_g16_prove_chunk_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, con
                                const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                                uint8_t* d_raw256, uint8_t* d_digest32);
 
+/* Verifying key in the oracle layout (32-B LE standard-form coordinates):
+ * alpha G1 (64) | beta G2 (128) | gamma G2 (128) | delta G2 (128) |
+ * IC_0..IC_T G1 (64 each) = 448 + 64 (T + 1) bytes (oracle: bn_g16_vk). */
+int acegpu_g16_vk(acegpu_ctx* ctx, const acegpu_g16* g, uint8_t* out);
+/* Batched pairing verification of n chunk proofs:
+ * proofs256 = n x 256-B EIP-197 proofs (acegpu_g16_prove_chunk's proof256),
+ * pubs = n x T x 32-B little-endian public inputs (the raw public-input
+ * digests; reduced mod r). *ok = 1 iff every proof satisfies
+ * e(A,B) = e(alpha,beta) e(sum z_j IC_j, gamma) e(C,delta) with its points on
+ * the curves and B in the order-r subgroup (one random-linear-combination
+ * check: n + 3 Miller loops, one final exponentiation, one MSM over IC). */
+int acegpu_g16_verify_batch(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* proofs256,
+                            const uint8_t* pubs, uint64_t n, int* ok);
+
 /* Groth16-mode shard (north-star block path): like acegpu_shard_roots_dev,
  * but each aligned chunk of T txs (T = txs_per_chunk, a power of two) is one
  * Groth16 proof over the chunk's witnesses (d_witness256: n x 256-B
@@ -252,6 +266,22 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                const uint8_t* d_revs, const uint32_t* d_rev_index,
                                uint8_t* d_codes, const uint8_t* d_witness256,
                                uint8_t* d_roots289, uint8_t* d_merkle32);
+
+/* Optimal ate pairing product prod_i e(P_i, Q_i) (final exponentiation
+ * included) over host buffers in the oracle encodings: G1 = x|y, G2 =
+ * x.c0|x.c1|y.c0|y.c1, 32-B little-endian standard form, all-zero = infinity.
+ * out384 (optional): Fq12 as 12 x 32 B (c0.c0.c0, c0.c0.c1, ..., c1.c2.c1);
+ * is_one (optional): 1 iff the product is the identity (a pairing check). */
+int acegpu_bn_pairing(acegpu_ctx* ctx, uint64_t n, const uint8_t* g1s, const uint8_t* g2s,
+                      uint8_t* out384, int* is_one);
+
+/* Fq12 unit operation for parity tests (one element, 384 B in/out in the
+ * encoding above): 0 final exponentiation, 1 easy part ^((p^6-1)(p^2+1)),
+ * 2 hard part ^((p^4-p^2+1)/r), 3/4/5 Frobenius p/p^2/p^3, 6 ^x (BN
+ * parameter), 7 inverse, 8 square, 9 Miller loop of the G1|G2 pair in the
+ * first 192 input bytes (defined up to subfield factors), 10 ^e with e the
+ * u64 (LE) at in384[384..392) (the input buffer is then 392 bytes). */
+int acegpu_bn_f12_op(acegpu_ctx* ctx, int op, const uint8_t* in384, uint8_t* out384);
 
 /* ---- Phase 1a on the GPU --------------------------------
  * attest_check_light (pipeline.cpp:20-42; LightCheck, pipeline.hpp:32-37):

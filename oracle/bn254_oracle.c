@@ -1292,3 +1292,47 @@ int bn_g16_verify(uint32_t T, const uint8_t* vk, const uint8_t* abc, const uint8
     memcpy(g2 + 384, vk + 320, 128);
     return bn_pairing_check(4, g1, g2);
 }
+
+/* Fq12 unit operations for GPU parity tests (same codes as acegpu_bn_f12_op):
+ * 0 final exponentiation, 1 easy part ^((p^6-1)(p^2+1)), 2 hard part ^h,
+ * 3/4/5 Frobenius ^p, ^p^2, ^p^3 (as plain exponentiations), 6 ^x,
+ * 7 inverse, 8 square, 9 Miller loop of (g1, g2) given in a384 (64 + 128 B). */
+static void load_f12(const uint8_t* in, fe12* a) {
+    fe2* c[6] = {&a->c0.c0, &a->c0.c1, &a->c0.c2, &a->c1.c0, &a->c1.c1, &a->c1.c2};
+    for (int i = 0; i < 6; ++i) {
+        to_mont(&FQ, in + 64 * i, &c[i]->c0);
+        to_mont(&FQ, in + 64 * i + 32, &c[i]->c1);
+    }
+}
+void bn_f12_op(int op, const uint8_t* in, uint8_t* out384) {
+    pairing_init();
+    fe12 a, r;
+    if (op == 9) {
+        miller(in, in + 64, &r);
+        store_f12(&r, out384);
+        return;
+    }
+    load_f12(in, &a);
+    uint64_t p1[4];
+    memcpy(p1, FQ.m, 32);
+    switch (op) {
+        case 0: final_exp(&a, &r); break;
+        case 1: {
+            fe12 b, c;
+            f12conj(&a, &b);
+            f12inv(&a, &c);
+            f12mul(&b, &c, &b);
+            f12pow(&b, P2_EXP, 8, &c);
+            f12mul(&c, &b, &r);
+            break;
+        }
+        case 2: f12pow(&a, H_EXP, 12, &r); break;
+        case 3: f12pow(&a, p1, 4, &r); break;
+        case 4: f12pow(&a, P2_EXP, 8, &r); break;
+        case 5: { fe12 t; f12pow(&a, P2_EXP, 8, &t); f12pow(&t, p1, 4, &r); break; }
+        case 6: { uint64_t x[1] = {4965661367192848881ull}; f12pow(&a, x, 1, &r); break; }
+        case 7: f12inv(&a, &r); break;
+        default: f12mul(&a, &a, &r); break;
+    }
+    store_f12(&r, out384);
+}

@@ -81,6 +81,11 @@ int bn_pairing_check(uint64_t n, const uint8_t* g1s, const uint8_t* g2s);
 void bn_f12_pow(const uint8_t* a384, const uint8_t* e32, uint8_t* out384);
 /* Verifying key: alpha G1 (64) | beta G2 (128) | gamma G2 (128) | delta G2 (128)
  * | IC_0..IC_T (64 each) = 448 + 64 (T + 1) bytes. */
+/* Fq12 unit ops for parity tests: 0 final exp, 1 easy part, 2 hard part,
+ * 3/4/5 Frobenius p/p^2/p^3, 6 ^x, 7 inverse, 8 square, 9 Miller loop of
+ * the (G1 | G2) pair in `in` (its value is only defined up to subfield
+ * factors: compare after op 1). */
+void bn_f12_op(int op, const uint8_t* in, uint8_t* out384);
 int bn_g16_vk(uint32_t T, uint32_t K, const uint8_t* trapdoor5, uint8_t* out);
 int bn_g16_verify(uint32_t T, const uint8_t* vk, const uint8_t* abc, const uint8_t* pubs);
 

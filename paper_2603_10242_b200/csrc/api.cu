@@ -17,6 +17,8 @@
 #include "g16_kernels.cuh"
 #include "mock_kernels.cuh"
 #include "phase1.cuh"
+#include "pairing_kernels.cuh"
+#include "g16_verify.cuh"
 #include "msm.cuh"
 #include "ntt.cuh"
 
@@ -725,6 +727,46 @@ int acegpu_verify_fc(acegpu_ctx* c, const uint8_t* fc, const uint8_t* payloads,
     else if (std::memcmp(expect + 40, fc + 40, 256) != 0) *out_check = 3;
     else if (std::memcmp(expect + 296, fc + 296, 32) != 0) *out_check = 3;
     else *out_check = 0;
+    return ACEGPU_OK;
+}
+
+int acegpu_bn_pairing(acegpu_ctx* c, uint64_t n, const uint8_t* g1s, const uint8_t* g2s,
+                      uint8_t* out384, int* is_one) {
+    if (n > (1u << 20)) return fail(ACEGPU_EINVAL, "too many pairs");
+    if (n && (!g1s || !g2s)) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *d1 = nullptr, *d2 = nullptr, *scratch, *out;
+    if (n) {
+        RET(h2d_t(c, kBnA, g1s, 64 * n, s, &d1));
+        RET(h2d_t(c, kBnB, g2s, 128 * n, s, &d2));
+    }
+    RET(ws(c, kBnScratch, bn::pairing_scratch_bytes(uint32_t(n)), &scratch));
+    RET(ws(c, kBnOut, 384 + 16, &out));
+    bn::launch_pairing_product(uint32_t(n), d1, d2, scratch, out,
+                               reinterpret_cast<int*>(out + 384), s);
+    CKL();
+    c->launches += n ? 2 : 1;
+    if (out384) CK(cudaMemcpyAsync(out384, out, 384, cudaMemcpyDeviceToHost, s));
+    if (is_one) CK(cudaMemcpyAsync(is_one, out + 384, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+int acegpu_bn_f12_op(acegpu_ctx* c, int op, const uint8_t* in384, uint8_t* out384) {
+    if (op < 0 || op > 10 || !in384 || !out384) return fail(ACEGPU_EINVAL, "bad f12 op");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *din, *dout;
+    RET(h2d_t(c, kBnA, in384, op >= 10 ? 392 : 384, s, &din));
+    RET(ws(c, kBnOut, 384, &dout));
+    bn::launch_f12_op(op, din, dout, s);
+    CKL();
+    c->launches++;
+    CK(cudaMemcpyAsync(out384, dout, 384, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;
 }
 
@@ -1601,6 +1643,10 @@ struct acegpu_g16 {
     uint32_t logn = 0;
     uint64_t N = 0, Vp = 0;  // Vp: private variables
     acegpu_msm_bases *qa = nullptr, *qb1 = nullptr, *qb2 = nullptr, *ql = nullptr, *qh = nullptr;
+    // verifying key: IC MSM table; alpha1 (Montgomery affine); beta2 | gamma2 |
+    // delta2 in the oracle encoding; IC_0..IC_T Montgomery affine (export)
+    acegpu_msm_bases* qic = nullptr;
+    uint8_t *vk_alpha1 = nullptr, *vk_g2_std = nullptr, *vk_ic = nullptr;
     uint8_t *consts = nullptr, *cc = nullptr;
     uint8_t *z = nullptr, *zb = nullptr, *zl = nullptr, *ea = nullptr, *eb = nullptr, *ec = nullptr;
     uint8_t *pts = nullptr, *scaled = nullptr, *rs = nullptr, *digest = nullptr;
@@ -1654,9 +1700,10 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     if (!g) return;
     DeviceGuard guard(g->device);
     cudaDeviceSynchronize();
-    for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh}) acegpu_bn_msm_free(b);
+    for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh, g->qic})
+        acegpu_bn_msm_free(b);
     for (uint8_t* p : {g->consts, g->cc, g->z, g->zb, g->zl, g->ea, g->eb, g->ec, g->pts,
-                       g->scaled, g->rs, g->digest})
+                       g->scaled, g->rs, g->digest, g->vk_alpha1, g->vk_g2_std, g->vk_ic})
         if (p) cudaFree(p);
     if (g->side) cudaStreamDestroy(g->side);
     if (g->ev_ab) cudaEventDestroy(g->ev_ab);
@@ -1751,6 +1798,18 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     // H: [tau^j Z(tau)/delta]1, j < N-1
     bn::launch_scalar_muls(1, gens, hs, N - 1, pts, s);
     RET(bases_from_device(c->device, 1, pts, N - 1, s, &g->qh));
+    // verifying key (the Groth16 verifier, g16_verify.cu)
+    if (dm(&g->vk_alpha1, 64) || dm(&g->vk_g2_std, 384) || dm(&g->vk_ic, 64ull * (T + 1)))
+        return fail(ACEGPU_ECUDA, "g16 vk alloc");
+    bn::g16_ic_scalars(T, g->consts, su, sv, hs, s);  // hs reused as scratch
+    bn::launch_scalar_muls(1, gens, hs, T + 1, g->vk_ic, s);
+    RET(bases_from_device(c->device, 1, g->vk_ic, T + 1, s, &g->qic));
+    CK(cudaMemcpyAsync(g->vk_alpha1, ex1, 64, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(ext + 256, trapdoor5 + 96, 32, cudaMemcpyHostToDevice, s));  // gamma
+    CK(cudaMemcpyAsync(g->vk_g2_std, ex2, 128, cudaMemcpyDeviceToDevice, s));        // beta2
+    bn::launch_scalar_muls(2, gens + 64, ext + 256, 1, g->vk_g2_std + 128, s);       // gamma2
+    CK(cudaMemcpyAsync(g->vk_g2_std + 256, ex2 + 128, 128, cudaMemcpyDeviceToDevice, s));
+    bn::launch_points_convert(2, g->vk_g2_std, 3, 0, s);
     CKL();
     CK(cudaStreamSynchronize(s));
     for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2}) cudaFree(p);
@@ -1883,6 +1942,61 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
         CKL();
         c->launches += 2;
     }
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_vk(acegpu_ctx* c, const acegpu_g16* g, uint8_t* out) {
+    if (!g || !out) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t T = g->d.T, bytes = 448 + 64 * (T + 1);
+    uint8_t* d;
+    RET(ws(c, kBnOut, bytes, &d));
+    CK(cudaMemcpyAsync(d, g->vk_alpha1, 64, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(d + 64, g->vk_g2_std, 384, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(d + 448, g->vk_ic, 64 * (T + 1), cudaMemcpyDeviceToDevice, s));
+    bn::launch_points_convert(1, d, 1, 0, s);
+    bn::launch_points_convert(1, d + 448, T + 1, 0, s);
+    CKL();
+    c->launches += 2;
+    CK(cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+
+namespace {
+int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_proofs,
+                      const uint8_t* d_pubs, uint64_t n, int* d_ok) {
+    if (n == 0 || n > (1u << 20)) return fail(ACEGPU_EINVAL, "g16 verify: bad proof count");
+    uint8_t* scratch;
+    RET(ws(c, kP1Scratch, bn::g16_verify_scratch_bytes(uint32_t(n), g->d.T), &scratch));
+    bn::G16VerifyKey vk;
+    vk.T = g->d.T;
+    vk.ic_table = g->qic->table;
+    vk.alpha1_mont = g->vk_alpha1;
+    vk.g2_std = g->vk_g2_std;
+    if (bn::g16_verify_batch(vk, d_proofs, d_pubs, uint32_t(n), scratch, c->msm, d_ok, s))
+        return fail(ACEGPU_ECUDA, "g16 verify launch");
+    CKL();
+    c->launches += 10;
+    return ACEGPU_OK;
+}
+}  // namespace
+
+extern "C" int acegpu_g16_verify_batch(acegpu_ctx* c, acegpu_g16* g, const uint8_t* proofs256,
+                                       const uint8_t* pubs, uint64_t n, int* ok) {
+    if (!g || !proofs256 || !pubs || !ok) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dp, *dq, *dok;
+    RET(h2d_t(c, kBnA, proofs256, 256 * n, s, &dp));
+    RET(h2d_t(c, kBnB, pubs, 32ull * g->d.T * n, s, &dq));
+    RET(ws(c, kBnOut, 16, &dok));
+    RET(g16_verify_locked(c, s, g, dp, dq, n, reinterpret_cast<int*>(dok)));
+    CK(cudaMemcpyAsync(ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;
 }
 

@@ -24,6 +24,9 @@ void g16_lagrange(const uint8_t* c, uint64_t m, uint8_t* L, cudaStream_t s);
 void g16_query_scalars(const G16Dims& d, const uint8_t* L, const uint8_t* c, const uint8_t* cc,
                        uint8_t* part, uint8_t* su, uint8_t* sv, uint8_t* sl, cudaStream_t s);
 void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s);
+// Verifying key: IC_j scalars (beta u_j + alpha v_j) / gamma, j = 0..T (standard form).
+void g16_ic_scalars(uint32_t T, const uint8_t* c, const uint8_t* su, const uint8_t* sv,
+                    uint8_t* out, cudaStream_t s);
 
 // Prover.
 void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const uint8_t* cc,

@@ -185,6 +185,17 @@ __global__ void query_scalars_kernel(G16Dims d, const uint8_t* L, const uint8_t*
     }
 }
 
+// Verifying-key IC scalars (beta u_j + alpha v_j + w_j) / gamma for the
+// public variables j = 0 (ONE) .. T (w_j = 0 for all of them), standard form.
+__global__ void ic_scalars_kernel(uint32_t T, const uint8_t* c, const uint8_t* su,
+                                  const uint8_t* sv, uint8_t* out) {
+    const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > T) return;
+    const Fr alpha = ldr(c + 32), beta = ldr(c + 64), gamma = ldr(c + 96);
+    const Fr u = to_mont(ldr(su + 32ull * j)), v = to_mont(ldr(sv + 32ull * j));
+    str(out + 32ull * j, from_mont(mul(add(mul(beta, u), mul(alpha, v)), inv_fast(gamma))));
+}
+
 // H-query scalars: tau^j Z(tau)/delta for j < n (standard form).
 __global__ void h_scalars_kernel(const uint8_t* c, uint64_t n, uint8_t* out) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -412,6 +423,10 @@ void g16_query_scalars(const G16Dims& d, const uint8_t* L, const uint8_t* c, con
     constexpr unsigned kParts = 256;
     one_partials_kernel<<<kParts, 256, 0, s>>>(d, L, cc, part);
     query_scalars_kernel<<<grid(d.V, 128), 128, 0, s>>>(d, L, c, part, kParts, su, sv, sl);
+}
+void g16_ic_scalars(uint32_t T, const uint8_t* c, const uint8_t* su, const uint8_t* sv,
+                    uint8_t* out, cudaStream_t s) {
+    ic_scalars_kernel<<<grid(T + 1, 128), 128, 0, s>>>(T, c, su, sv, out);
 }
 void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s) {
     h_scalars_kernel<<<grid(n, 128), 128, 0, s>>>(c, n, out);

@@ -183,3 +183,137 @@ def test_groth16_block_shards(ctx, n, world):
         assert fc == O.oracle_build_fc(fb, bytes(out))
     finally:
         pk.close()
+
+
+# ------------------------------------------------------------- verifier
+def _vk_oracle(T, K, trap):
+    vk = O.buf(448 + 64 * (T + 1))
+    O.oracle().bn_g16_vk(C.c_uint32(T), C.c_uint32(K), O.ptr(trap.tobytes()), vk)
+    return bytes(vk)
+
+
+@pytest.mark.parametrize("T,K", [(1, 2), (4, 3), (64, 20)])
+def test_verifying_key_matches_oracle(ctx, T, K):
+    from paper_2603_10242_b200 import _native as N, groth16
+    rng = random.Random(T + 7 * K)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        out = np.zeros(448 + 64 * (T + 1), np.uint8)
+        ctx.call("acegpu_g16_vk", pk.h, N.addr(out))
+        assert out.tobytes() == _vk_oracle(T, K, trap)
+    finally:
+        pk.close()
+
+
+def test_gpu_proofs_verify_under_oracle_pairing(ctx):
+    """The GPU prover's proofs pass the oracle's pairing verifier (bn_g16_verify,
+    a full e(A,B) = e(alpha,beta) e(L,gamma) e(C,delta) check)."""
+    from paper_2603_10242_b200 import groth16
+    T, K = 4, 3
+    rng = random.Random(5)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        vk = _vk_oracle(T, K, trap)
+        for _ in range(2):
+            w = arr([rng.randrange(R) for _ in range(T)])
+            pub = arr([rng.randrange(R) for _ in range(T)])
+            _, raw, _ = pk.prove(w, pub)
+            assert O.oracle().bn_g16_verify(C.c_uint32(T), O.ptr(vk), O.ptr(raw),
+                                            O.ptr(pub.tobytes())) == 1
+            bad = bytearray(pub.tobytes())
+            bad[3] ^= 4
+            assert O.oracle().bn_g16_verify(C.c_uint32(T), O.ptr(vk), O.ptr(raw),
+                                            O.ptr(bytes(bad))) == 0
+    finally:
+        pk.close()
+
+
+def _gpu_verify(ctx, pk, proofs, pubs):
+    from paper_2603_10242_b200 import _native as N
+    ok = C.c_int(-1)
+    p = np.frombuffer(b"".join(proofs), np.uint8).copy()
+    q = np.frombuffer(b"".join(pubs), np.uint8).copy()
+    ctx.call("acegpu_g16_verify_batch", pk.h, N.addr(p), N.addr(q), len(proofs), C.byref(ok))
+    return ok.value
+
+
+def test_gpu_batch_verifier(ctx):
+    """acegpu_g16_verify_batch accepts honest proofs and rejects a changed
+    public input, swapped proofs, an off-curve point and a B on the twist
+    outside the order-r subgroup."""
+    from paper_2603_10242_b200 import groth16
+    T, K = 8, 3
+    rng = random.Random(17)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        proofs, pubs = [], []
+        for _ in range(5):
+            w = arr([rng.randrange(R) for _ in range(T)])
+            pub = arr([rng.randrange(R) for _ in range(T)])
+            proof, _, _ = pk.prove(w, pub)
+            proofs.append(bytes(proof))
+            pubs.append(pub.tobytes())
+        assert _gpu_verify(ctx, pk, proofs, pubs) == 1
+        assert _gpu_verify(ctx, pk, proofs[:1], pubs[:1]) == 1
+        bad = bytearray(pubs[2])
+        bad[40] ^= 1
+        assert _gpu_verify(ctx, pk, proofs, pubs[:2] + [bytes(bad)] + pubs[3:]) == 0
+        assert _gpu_verify(ctx, pk, [proofs[1], proofs[0]] + proofs[2:], pubs) == 0
+        off = bytearray(proofs[3])
+        off[63] ^= 1  # A.y changed: off the curve
+        assert _gpu_verify(ctx, pk, proofs[:3] + [bytes(off)] + proofs[4:], pubs) == 0
+        nb = bytearray(proofs[4])
+        nb[64:192] = _twist_point_outside_g2(rng)
+        assert _gpu_verify(ctx, pk, proofs[:4] + [bytes(nb)], pubs) == 0
+        # raw digests >= r are reduced like the prover's
+        assert _gpu_verify(ctx, pk, proofs, pubs) == 1
+    finally:
+        pk.close()
+
+
+PQ = 0x30644E72E131A029B85045B68181585D97816A916871CA8D3C208C16D87CFD47
+
+
+def _f2mul(a, b):
+    return ((a[0] * b[0] - a[1] * b[1]) % PQ, (a[0] * b[1] + a[1] * b[0]) % PQ)
+
+
+def _f2pow(a, e):
+    r = (1, 0)
+    while e:
+        if e & 1:
+            r = _f2mul(r, a)
+        a = _f2mul(a, a)
+        e >>= 1
+    return r
+
+
+def _f2sqrt(a):
+    """Square root in Fq2 for p = 3 mod 4 (or None)."""
+    a1 = _f2pow(a, (PQ - 3) // 4)
+    alpha = _f2mul(_f2mul(a1, a1), a)
+    x0 = _f2mul(a1, a)
+    if alpha == (PQ - 1, 0):
+        x = _f2mul((0, 1), x0)
+    else:
+        x = _f2mul(_f2pow(((1 + alpha[0]) % PQ, alpha[1]), (PQ - 1) // 2), x0)
+    return x if _f2mul(x, x) == a else None
+
+
+def _twist_point_outside_g2(rng):
+    """A point of y^2 = x^3 + 3/(9+u) over Fq2 that is not in the order-r
+    subgroup (the twist's cofactor is 2p - r), EIP-197-encoded (128 B)."""
+    binv = _f2pow((9, 1), PQ * PQ - 2)
+    b = ((3 * binv[0]) % PQ, (3 * binv[1]) % PQ)
+    while True:
+        x = (rng.randrange(PQ), rng.randrange(PQ))
+        rhs = _f2mul(_f2mul(x, x), x)
+        rhs = ((rhs[0] + b[0]) % PQ, (rhs[1] + b[1]) % PQ)
+        y = _f2sqrt(rhs)
+        if y is not None:
+            break
+    be = lambda v: v.to_bytes(32, "big")  # noqa: E731
+    return be(x[1]) + be(x[0]) + be(y[1]) + be(y[0])
