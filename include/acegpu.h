@@ -253,6 +253,19 @@ int acegpu_g16_vk(acegpu_ctx* ctx, const acegpu_g16* g, uint8_t* out);
 int acegpu_g16_verify_batch(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* proofs256,
                             const uint8_t* pubs, uint64_t n, int* ok);
 
+/* verify_finality_certificate in Groth16 mode (prover.cpp:158-169 with real
+ * proofs): *result = 0 Valid, 1 SlotMismatch, 2
+ * HashMismatch, 3 ProofMismatch, checked in the reference's order. Instead
+ * of re-proving, the chunk proofs (n_chunks x 256 B, chunk k covering txs
+ * [kT, kT+T), as acegpu_g16_shard_roots_dev emits them) are checked with one
+ * batched pairing verification against the public inputs recomputed from the
+ * block, and the FC is recomputed from them with the reference's tree rule.
+ * cost_units (optional) += 1 as the reference does. */
+int acegpu_g16_verify_fc(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* fc328,
+                         const uint8_t* payloads, const uint64_t* offs, const uint8_t* atts,
+                         uint64_t n, const uint8_t* header256, const uint8_t* chunk_proofs256,
+                         uint64_t* cost_units, int* result);
+
 /* Groth16-mode shard (north-star block path): like acegpu_shard_roots_dev,
  * but each aligned chunk of T txs (T = txs_per_chunk, a power of two) is one
  * Groth16 proof over the chunk's witnesses (d_witness256: n x 256-B

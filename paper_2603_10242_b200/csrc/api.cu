@@ -1890,28 +1890,27 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
 // chunk of the block zero-padded). Chunk roots = chunk proofs as mock-tree
 // leaves (proof | chunk digest | kind Tx), so acegpu_combine_roots_dev
 // aggregates them with the reference's tree rule (prover.cpp:106-127).
-extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
-                                          const uint8_t* d_payloads, const uint64_t* d_offs,
-                                          const uint8_t* d_atts, uint64_t n, uint64_t n_total,
-                                          const uint8_t* d_revs, const uint32_t* d_rev_index,
-                                          uint8_t* d_codes, const uint8_t* d_witness256,
-                                          uint8_t* d_roots289, uint8_t* d_merkle32) {
+namespace {
+int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_proofs,
+                      const uint8_t* d_pubs, uint64_t n, int* d_ok);
+// Per-chunk inputs of a (shard of a) block in Groth16 mode: leaves (verdicts,
+// public-input digests, Merkle leaves), Merkle levels up to the chunk level
+// (the block's short last chunk lifted), the chunk Merkle roots, and the
+// zero-padded public inputs pub (chunks x T x 32 B raw digests).
+int g16_chunk_inputs(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_payloads,
+                     const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                     const uint8_t* d_revs, const uint32_t* d_rev_index, uint8_t* d_codes,
+                     uint8_t* d_merkle32, uint8_t** pub_out, TreeResult* t) {
     const uint32_t T = g->d.T;
-    if (T & (T - 1)) return fail(ACEGPU_EINVAL, "g16 shard: txs per chunk must be a power of two");
-    if (n == 0) return fail(ACEGPU_EINVAL, "g16 shard: empty shard");
+    if (T & (T - 1)) return fail(ACEGPU_EINVAL, "g16: txs per chunk must be a power of two");
+    if (n == 0) return fail(ACEGPU_EINVAL, "g16: empty block or shard");
     RET(check_n(n));
     uint32_t log2_chunk = 0;
     while ((1u << log2_chunk) < T) ++log2_chunk;
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard guard(c->device);
-    cudaStream_t s = pick(c, stream);
-    // leaves: verdicts, public-input digests (node records), Merkle leaves
-    TreeResult t;
     RET(run_tree(c, s, d_payloads, d_offs, d_atts, uint32_t(n), nullptr, d_revs, d_rev_index,
-                 d_codes, true, 0, false, &t));
-    // Merkle levels up to the chunk level (lift the block's short last chunk)
+                 d_codes, true, 0, false, t));
     const bool lift = n_total > T;
-    uint8_t* min_ = t.merkle;  // kMerkA after zero levels
+    uint8_t* min_ = t->merkle;  // kMerkA after zero levels
     uint8_t* mout = static_cast<uint8_t*>(c->bufs[kMerkB].p);
     uint32_t cur = uint32_t(n), lv = 0;
     while (lv < log2_chunk && (cur > 1 || (lift && cur == 1))) {
@@ -1923,15 +1922,36 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
         ++lv;
     }
     const uint64_t chunks = (n + T - 1) / T;
-    if (cur != chunks) return fail(ACEGPU_EINVAL, "g16 shard: chunk count mismatch");
+    if (cur != chunks) return fail(ACEGPU_EINVAL, "g16: chunk count mismatch");
     CK(cudaMemcpyAsync(d_merkle32, min_, 32 * chunks, cudaMemcpyDeviceToDevice, s));
-    // chunk inputs: pub = LE(public_inputs_digest), w = LE(witness[0:32]), zero padded
-    uint8_t *pub, *w, *proof, *node;
+    uint8_t* pub;
     RET(ws(c, kBnA, 32 * chunks * T, &pub));
+    bn::g16_gather32(t->nodes + 256, kNodeBytes, n, chunks * T, pub, s);
+    CKL();
+    *pub_out = pub;
+    return ACEGPU_OK;
+}
+}  // namespace
+
+extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                          const uint8_t* d_payloads, const uint64_t* d_offs,
+                                          const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                                          const uint8_t* d_revs, const uint32_t* d_rev_index,
+                                          uint8_t* d_codes, const uint8_t* d_witness256,
+                                          uint8_t* d_roots289, uint8_t* d_merkle32) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    const uint32_t T = g->d.T;
+    TreeResult t;
+    uint8_t *pub, *w, *proof, *node;
+    RET(g16_chunk_inputs(c, s, g, d_payloads, d_offs, d_atts, n, n_total, d_revs, d_rev_index,
+                         d_codes, d_merkle32, &pub, &t));
+    const uint64_t chunks = (n + T - 1) / T;
+    // w = LE(witness[0:32]), zero padded
     RET(ws(c, kBnB, 32 * chunks * T, &w));
     RET(ws(c, kIn2, 256 + 32 + 320, &proof));
     node = proof + 288;
-    bn::g16_gather32(t.nodes + 256, kNodeBytes, n, chunks * T, pub, s);
     bn::g16_gather32(d_witness256, 256, n, chunks * T, w, s);
     CKL();
     for (uint64_t k = 0; k < chunks; ++k) {
@@ -1942,6 +1962,64 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
         CKL();
         c->launches += 2;
     }
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_verify_fc(acegpu_ctx* c, acegpu_g16* g, const uint8_t* fc328,
+                                    const uint8_t* payloads, const uint64_t* offs,
+                                    const uint8_t* atts, uint64_t n, const uint8_t* header,
+                                    const uint8_t* chunk_proofs256, uint64_t* cost_units,
+                                    int* result) {
+    if (!g || !fc328 || !header || !result || (n && (!payloads || !offs || !atts)))
+        return fail(ACEGPU_EINVAL, "null argument");
+    if (cost_units) *cost_units += 1;  // K_FC_VERIFY_COST_UNITS (prover.hpp:77)
+    // slot first (prover.cpp:160-162): FC bytes 32..40 vs header bytes 0..8
+    if (std::memcmp(fc328 + 32, header, 8) != 0) {
+        *result = 1;
+        return ACEGPU_OK;
+    }
+    if (n == 0) return fail(ACEGPU_EINVAL, "g16 verify_fc: empty block");
+    if (!chunk_proofs256) return fail(ACEGPU_EINVAL, "g16 verify_fc: chunk proofs required");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    const uint32_t T = g->d.T;
+    const uint64_t chunks = (n + T - 1) / T;
+    uint8_t *dp, *da, *dh, *dproofs, *roots, *merk, *pub, *digest, *node, *out, *dok;
+    uint64_t* doff;
+    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+    RET(h2d_t(c, kHeader, header, 256, s, &dh));
+    RET(h2d_t(c, kSegRoots, chunk_proofs256, 256 * chunks, s, &dproofs));
+    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };  // 16-B vector stores
+    RET(ws(c, kSegMerk, al(32 * chunks) + al(289 * chunks) + al(32 * chunks) + al(320) + al(640) + 16,
+           &merk));
+    roots = merk + al(32 * chunks);
+    digest = roots + al(289 * chunks);
+    node = digest + al(32 * chunks);
+    out = node + al(320);
+    dok = out + al(640);
+    TreeResult t;
+    RET(g16_chunk_inputs(c, s, g, dp, doff, da, n, n, nullptr, nullptr, nullptr, merk, &pub, &t));
+    // chunk roots: proof | chunk digest | kind Tx, as the prover built them
+    uint8_t* rs;
+    RET(ws(c, kIn2, 64, &rs));
+    for (uint64_t k = 0; k < chunks; ++k) {
+        bn::g16_derive_rs(pub + 32 * T * k, T, rs, digest + 32 * k, s);
+        bn::g16_chunk_node(dproofs + 256 * k, digest + 32 * k, node, s);
+        launch_pack_nodes(node, 1, roots + 289 * k, s);
+        CKL();
+        c->launches += 3;
+    }
+    RET(combine_impl(c, s, roots, merk, chunks, n, dh, out, out + 304));
+    RET(g16_verify_locked(c, s, g, dproofs, pub, chunks, reinterpret_cast<int*>(dok)));
+    uint8_t fc[328];
+    int ok = 0;
+    CK(cudaMemcpyAsync(fc, out + 304, 328, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (std::memcmp(fc, fc328, 32) != 0) *result = 2;                       // HashMismatch
+    else if (!ok || std::memcmp(fc + 40, fc328 + 40, 288) != 0) *result = 3;  // ProofMismatch
+    else *result = 0;                                                        // Valid
     return ACEGPU_OK;
 }
 

@@ -51,6 +51,40 @@ class ProvingKey:
         self.ctx.call("acegpu_g16_prove_chunk_dev", stream, self.h, d_w, d_pub, d_rs, d_proof,
                       d_raw, d_digest)
 
+    def verifying_key(self) -> bytes:
+        """alpha G1 | beta G2 | gamma G2 | delta G2 | IC_0..IC_T (oracle encoding)."""
+        out = np.zeros(448 + 64 * (self.T + 1), np.uint8)
+        self.ctx.call("acegpu_g16_vk", self.h, out)
+        return out.tobytes()
+
+    def verify_batch(self, proofs: list[bytes], pubs: list[bytes]) -> bool:
+        """Batched pairing verification of chunk proofs (EIP-197 256 B each)
+        against their T x 32-B public inputs."""
+        if not proofs:
+            return True
+        ok = C.c_int(0)
+        p = np.frombuffer(b"".join(proofs), np.uint8).copy()
+        q = np.frombuffer(b"".join(pubs), np.uint8).copy()
+        self.ctx.call("acegpu_g16_verify_batch", self.h, p, q, len(proofs), C.byref(ok))
+        return ok.value == 1
+
+    def verify_finality_certificate(self, fc, block, chunk_proofs: bytes, cost_units=None):
+        """verify_finality_certificate (prover.cpp:158-169) in Groth16 mode:
+        slot, block hash, then the chunk proofs by one batched pairing check
+        and the FC recomputed from them -> prover.FcCheck."""
+        from .prover import FcCheck, _flat
+        fb = _flat(block)
+        fcb = np.frombuffer(fc.encode() if hasattr(fc, "encode") else bytes(fc), np.uint8).copy()
+        cu = C.c_uint64(0)
+        res = C.c_int(-1)
+        cp = np.frombuffer(bytes(chunk_proofs) or b"\0", np.uint8).copy()
+        hdr = np.ascontiguousarray(fb.header, np.uint8)
+        self.ctx.call("acegpu_g16_verify_fc", self.h, fcb, fb.payloads, fb.offs, fb.atts, fb.n,
+                      hdr, cp, C.byref(cu), C.byref(res))
+        if cost_units is not None:
+            cost_units.value += cu.value
+        return FcCheck(res.value)
+
     def close(self):
         if self.h:
             N.lib().acegpu_g16_free(self.h)

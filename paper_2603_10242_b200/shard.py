@@ -176,10 +176,11 @@ def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
 
 
 def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None, pk=None,
-                                 witnesses=None):
+                                 witnesses=None, return_roots: bool = False):
     """Emulates `world` ranks one after another on one GPU (no collective):
     used to check shard/combine bit-exactness with a single device.
-    With a Groth16 proving key `pk`, chunks are Groth16 proofs."""
+    With a Groth16 proving key `pk`, chunks are Groth16 proofs. return_roots
+    adds the chunk roots (n_chunks x 289 B: proof | digest | kind)."""
     import torch
     be = G16Backend(pk, ctx) if pk is not None else GpuBackend(ctx)
     parts = partition(fb.n, world, log2_chunk)
@@ -196,4 +197,5 @@ def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None, pk=N
     roots, merk = torch.cat(rs), torch.cat(ms)
     proof, fc = be.combine(roots, merk, sum(n_chunks(c, log2_chunk) for _, c in parts), fb.n, hdr)
     torch.cuda.synchronize()
-    return proof.cpu().numpy().tobytes(), fc.cpu().numpy().tobytes()
+    out = (proof.cpu().numpy().tobytes(), fc.cpu().numpy().tobytes())
+    return out + (roots.cpu().numpy().tobytes(),) if return_roots else out

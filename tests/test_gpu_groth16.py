@@ -317,3 +317,56 @@ def _twist_point_outside_g2(rng):
             break
     be = lambda v: v.to_bytes(32, "big")  # noqa: E731
     return be(x[1]) + be(x[0]) + be(y[1]) + be(y[0])
+
+
+def _witnesses(fb, n):
+    wit = b""
+    for i in range(n):
+        att = fb.att(i)
+        u = int(fb.rev_index[i])
+        key = O.derive_attest_key(fb.revs[32 * u:32 * u + 32].tobytes(), att[64:72])
+        out = O.buf(256)
+        O.oracle().or_build_witness(O.ptr(key), O.ptr(att[:32]), out)
+        wit += bytes(out)
+    return np.frombuffer(wit, np.uint8).copy()
+
+
+@pytest.mark.parametrize("n", [4, 11, 37])
+def test_groth16_verify_finality_certificate(ctx, n):
+    """verify_finality_certificate in Groth16 mode: the
+    prover's FC + chunk proofs verify by pairings; slot, header, payload and
+    proof tampering give SlotMismatch / HashMismatch / ProofMismatch."""
+    from paper_2603_10242_b200 import groth16, prover, shard, wire
+    T, K = 4, 3
+    rng = random.Random(n)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        fb = O.multi_user_block(n, 3)
+        wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts,
+                             np.frombuffer(fb.header, np.uint8).copy())
+        _, fc, roots = shard.prove_sharded_single_process(
+            wfb, 2, 2, ctx, pk=pk, witnesses=_witnesses(fb, n), return_roots=True)
+        chunks = (n + T - 1) // T
+        proofs = b"".join(roots[289 * k:289 * k + 256] for k in range(chunks))
+        cu = prover.CostUnits()
+        V = prover.FcCheck
+        assert pk.verify_finality_certificate(fc, wfb, proofs, cu) == V.Valid
+        assert cu.value == 1
+        bad_slot = bytearray(fc)
+        bad_slot[39] ^= 1
+        assert pk.verify_finality_certificate(bytes(bad_slot), wfb, proofs) == V.SlotMismatch
+        hdr = bytearray(fb.header)
+        hdr[100] ^= 1  # a root byte: same slot, different block hash
+        wfb2 = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(bytes(hdr), np.uint8).copy())
+        assert pk.verify_finality_certificate(fc, wfb2, proofs) == V.HashMismatch
+        pay = fb.payloads.copy()
+        pay[int(fb.offs[n - 1]) + 20] ^= 1  # last tx's payload -> its public input
+        wfb3 = wire.FlatBlock(pay, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+        assert pk.verify_finality_certificate(fc, wfb3, proofs) == V.ProofMismatch
+        pr = bytearray(proofs)
+        pr[0:256], pr[-256:] = pr[-256:], pr[0:256]
+        if chunks > 1:
+            assert pk.verify_finality_certificate(fc, wfb, bytes(pr)) == V.ProofMismatch
+    finally:
+        pk.close()
