@@ -659,6 +659,27 @@ def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup,
            "vs_400ms_interval": ms / 400.0, "steps": steps,
            "accepted": int((codes[:count] == 0).sum().item()),
            "fc_sha256": hashlib_sha256(fc.cpu().numpy().tobytes())}
+    if world == 1:
+        # verify_finality_certificate in Groth16 mode: the
+        # host API (block H2D, public inputs recomputed, one batched pairing
+        # check of the chunk proofs, FC recomputed) vs the reference's O(N)
+        # re-prove
+        _, fc2, roots = shard.prove_sharded(db, n, 0, 1, shard.LOG2_CHUNK, be, codes=codes,
+                                            return_roots=True)
+        chunks = -(-n // 1024)
+        r = roots.cpu().numpy().tobytes()
+        proofs = b"".join(r[289 * k:289 * k + 256] for k in range(chunks))
+        fcb = fc2.cpu().numpy().tobytes()
+        pk.verify_finality_certificate(fcb, fb, proofs)  # warm-up
+        vt = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            verdict = pk.verify_finality_certificate(fcb, fb, proofs)
+            vt.append((time.perf_counter() - t0) * 1e3)
+        out["verify_fc"] = {"ms": statistics.median(vt), "verdict": verdict.name,
+                            "method": "batched pairing check of %d chunk proofs (%d Miller loops, "
+                                      "1 final exponentiation) + FC recompute, host buffers"
+                                      % (chunks, chunks + 3)}
     if own:
         pk.close()
     return out

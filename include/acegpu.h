@@ -293,7 +293,8 @@ int acegpu_bn_pairing(acegpu_ctx* ctx, uint64_t n, const uint8_t* g1s, const uin
  * 2 hard part ^((p^4-p^2+1)/r), 3/4/5 Frobenius p/p^2/p^3, 6 ^x (BN
  * parameter), 7 inverse, 8 square, 9 Miller loop of the G1|G2 pair in the
  * first 192 input bytes (defined up to subfield factors), 10 ^e with e the
- * u64 (LE) at in384[384..392) (the input buffer is then 392 bytes). */
+ * u64 (LE) at in384[384..392) (the input buffer is then 392 bytes),
+ * 11 square of an element of the cyclotomic subgroup (Granger-Scott). */
 int acegpu_bn_f12_op(acegpu_ctx* ctx, int op, const uint8_t* in384, uint8_t* out384);
 
 /* ---- Phase 1a on the GPU --------------------------------

@@ -755,7 +755,7 @@ int acegpu_bn_pairing(acegpu_ctx* c, uint64_t n, const uint8_t* g1s, const uint8
 }
 
 int acegpu_bn_f12_op(acegpu_ctx* c, int op, const uint8_t* in384, uint8_t* out384) {
-    if (op < 0 || op > 10 || !in384 || !out384) return fail(ACEGPU_EINVAL, "bad f12 op");
+    if (op < 0 || op > 11 || !in384 || !out384) return fail(ACEGPU_EINVAL, "bad f12 op");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     cudaStream_t s = c->stream;

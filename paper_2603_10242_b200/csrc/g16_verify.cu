@@ -10,7 +10,8 @@
 //
 // i.e. n + 3 Miller loops and ONE final exponentiation, plus one MSM over the
 // T + 1 IC points with combined scalars. Every proof point is checked to be
-// on its curve and B_i to be in the order-r subgroup of the twist.
+// on its curve and B_i to be in the order-r subgroup of the twist
+// (psi(B) = [6x^2] B).
 #include <cuda_runtime.h>
 
 #include "g16_verify.cuh"
@@ -150,11 +151,16 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
     const Fq ax = ld_be(p), ay = ld_be(p + 32), cx = ld_be(p + 192), cy = ld_be(p + 224);
     const Fq2 bx = {ld_be(p + 96), ld_be(p + 64)}, by = {ld_be(p + 160), ld_be(p + 128)};
     bool ok = on_curve(ax, ay, g1_b()) && on_curve(cx, cy, g1_b()) && on_curve(bx, by, g2_b());
-    // order-r subgroup of the twist: r B = O
-    uint32_t rr[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) rr[k] = mod_limb<FrCfg>(k);
-    if (ok && !mul_bits(bx, by, rr, 254).is_inf()) ok = false;
+    // order-r subgroup of the twist: psi(B) == [6x^2] B (El Housni-Guillevic-
+    // Piellard 2022 for BN254; psi = the untwist-Frobenius-twist map, the
+    // Miller loop's frob_twist) -- a 127-bit scalar instead of r's 254 bits
+    if (ok) {
+        const uint32_t k6x2[4] = {0xe87cfd46u, 0xf83e9682u, 0xeeb859fbu, 0x6f4d8248u};
+        const XYZZ<Fq2> m = mul_bits(bx, by, k6x2, 127);
+        Fq2 px = bx, py = by;
+        frob_twist(px, py);
+        if (m.is_inf() || !feq(fmul(px, m.ZZ), m.X) || !feq(fmul(py, m.ZZZ), m.Y)) ok = false;
+    }
     if (!ok) atomicExch(bad, 1);
     uint32_t k[4];
     for (int w = 0; w < 4; ++w) {

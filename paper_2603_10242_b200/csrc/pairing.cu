@@ -112,6 +112,7 @@ __global__ void f12_op_kernel(int op, const uint8_t* in, uint8_t* out) {
                 }
                 break;
             }
+            case 11: r = f12_cyc_sqr(a); break;  // input in the cyclotomic subgroup
             default: r = f12_sqr(a); break;
         }
     }

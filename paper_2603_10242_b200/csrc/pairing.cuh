@@ -148,6 +148,48 @@ static __device__ __noinline__ Fq12 f12_sqr(const Fq12 a) {
     return {c0, f6_add(ab, ab)};
 }
 __device__ __forceinline__ Fq12 f12_conj(const Fq12& a) { return {a.c0, f6_neg(a.c1)}; }
+
+// a * (b0 + b1 v): 5 Fq2 products (Karatsuba on the two non-zero terms).
+static __device__ __noinline__ Fq6 f6_mul_01(const Fq6 a, const Fq2 b0, const Fq2 b1) {
+    const Fq2 v0 = fmul(a.c0, b0), v1 = fmul(a.c1, b1);
+    const Fq2 c1 = fsub(fsub(fmul(fadd(a.c0, a.c1), fadd(b0, b1)), v0), v1);
+    return {fadd(v0, f2_mul_xi(fmul(a.c2, b1))), c1, fadd(v1, fmul(a.c2, b0))};
+}
+// f * line, line = l0 + (l1 + l2 v) w (the Miller-loop line shape): 13 Fq2
+// products instead of the dense 18.
+static __device__ __noinline__ Fq12 f12_mul_line(const Fq12 f, const Fq2 l0, const Fq2 l1,
+                                                 const Fq2 l2) {
+    const Fq6 t0 = {fmul(f.c0.c0, l0), fmul(f.c0.c1, l0), fmul(f.c0.c2, l0)};
+    const Fq6 t1 = f6_mul_01(f.c1, l1, l2);
+    const Fq6 t2 = f6_mul_01(f6_add(f.c0, f.c1), fadd(l0, l1), l2);
+    return {f6_add(t0, f6_mul_v(t1)), f6_sub(f6_sub(t2, t0), t1)};
+}
+// Squaring in the cyclotomic subgroup (Granger-Scott): the three Fq4
+// squarings (z0,z1) = (c0.c0, c1.c1), (z2,z3) = (c1.c0, c0.c2),
+// (z4,z5) = (c0.c1, c1.c2) over y^2 = xi; 6 Fq2 products instead of 12.
+static __device__ __noinline__ Fq12 f12_cyc_sqr(const Fq12 a) {
+    auto fq4 = [](const Fq2& x, const Fq2& y, Fq2& s0, Fq2& s1) {  // (x + y t)^2, t^2 = xi
+        const Fq2 xy = fmul(x, y);
+        s0 = fsub(fsub(fmul(fadd(x, y), fadd(x, f2_mul_xi(y))), xy), f2_mul_xi(xy));
+        s1 = fadd(xy, xy);
+    };
+    Fq2 t0, t1, t2, t3, t4, t5;
+    fq4(a.c0.c0, a.c1.c1, t0, t1);
+    fq4(a.c1.c0, a.c0.c2, t2, t3);
+    fq4(a.c0.c1, a.c1.c2, t4, t5);
+    auto tw = [](const Fq2& t, const Fq2& z, bool plus) {  // 3t -+ 2z
+        const Fq2 d = plus ? fadd(t, z) : fsub(t, z);
+        return fadd(fadd(d, d), t);
+    };
+    Fq12 r;
+    r.c0.c0 = tw(t0, a.c0.c0, false);
+    r.c1.c1 = tw(t1, a.c1.c1, true);
+    r.c1.c0 = tw(f2_mul_xi(t5), a.c1.c0, true);
+    r.c0.c2 = tw(t4, a.c0.c2, false);
+    r.c0.c1 = tw(t2, a.c0.c1, false);
+    r.c1.c2 = tw(t3, a.c1.c2, true);
+    return r;
+}
 static __device__ __noinline__ Fq12 f12_inv(const Fq12 a) {
     const Fq6 d = f6_sub(f6_mul(a.c0, a.c0), f6_mul_v(f6_mul(a.c1, a.c1)));
     const Fq6 di = f6_inv(d);
@@ -172,12 +214,12 @@ __device__ __forceinline__ bool f12_is_one(const Fq12& a) {
            fzero(a.c1.c1) && fzero(a.c1.c2);
 }
 
-// a^x, x = 4965661367192848881 (63 bits), square-and-multiply.
+// a^x, x = 4965661367192848881 (63 bits); a in the cyclotomic subgroup.
 __device__ __forceinline__ Fq12 f12_pow_x(const Fq12& a) {
     const uint64_t x = 4965661367192848881ull;
     Fq12 r = f12_one();
     for (int i = 62; i >= 0; --i) {
-        r = f12_sqr(r);
+        r = f12_cyc_sqr(r);
         if ((x >> i) & 1) r = f12_mul(r, a);
     }
     return r;
@@ -188,20 +230,19 @@ struct G2Proj {
     Fq2 X, Y, Z;
 };
 
-// Line coefficients (cy * yP) + (cx * xP) w + c3 w^3 as an Fq12 (dense).
-__device__ __forceinline__ Fq12 line_to_f12(const Fq2& cy, const Fq2& cx, const Fq2& c3,
-                                            const Fq& xP, const Fq& yP) {
-    Fq12 l;
-    l.c0.c0 = f2_mul_fq(cy, yP);
-    fset_zero(l.c0.c1);
-    fset_zero(l.c0.c2);
-    l.c1.c0 = f2_mul_fq(cx, xP);
-    l.c1.c1 = c3;
-    fset_zero(l.c1.c2);
-    return l;
+// Line (cy * yP) + (cx * xP) w + c3 w^3 = l0 + (l1 + l2 v) w.
+struct Line {
+    Fq2 l0, l1, l2;
+};
+__device__ __forceinline__ Line make_line(const Fq2& cy, const Fq2& cx, const Fq2& c3,
+                                          const Fq& xP, const Fq& yP) {
+    return {f2_mul_fq(cy, yP), f2_mul_fq(cx, xP), c3};
+}
+__device__ __forceinline__ Fq12 f12_mul_line(const Fq12& f, const Line& l) {
+    return f12_mul_line(f, l.l0, l.l1, l.l2);
 }
 
-static __device__ __noinline__ Fq12 dbl_step(G2Proj& T, const Fq xP, const Fq yP) {
+static __device__ __noinline__ Line dbl_step(G2Proj& T, const Fq xP, const Fq yP) {
     const Fq2 X2 = fsqr(T.X), Y2 = fsqr(T.Y);
     const Fq2 W = fadd(fadd(X2, X2), X2);
     const Fq2 S = fmul(T.Y, T.Z);
@@ -224,11 +265,11 @@ static __device__ __noinline__ Fq12 dbl_step(G2Proj& T, const Fq xP, const Fq yP
     T.X = fadd(HS, HS);
     T.Y = fsub(fmul(W, fsub(B4, H)), Y2S2x8);
     T.Z = fadd(S3x4, S3x4);
-    return line_to_f12(cy, cx, c3, xP, yP);
+    return make_line(cy, cx, c3, xP, yP);
 }
 
-static __device__ __noinline__ Fq12 add_step(G2Proj& T, const Fq2 x2, const Fq2 y2, const Fq xP,
-                                             const Fq yP) {
+static __device__ __noinline__ Line add_step(G2Proj& T, const Fq2 x2, const Fq2 y2, const Fq xP,
+                                            const Fq yP) {
     const Fq2 N = fsub(fmul(y2, T.Z), T.Y);
     const Fq2 D = fsub(fmul(x2, T.Z), T.X);
     const Fq2 cy = D;
@@ -243,7 +284,7 @@ static __device__ __noinline__ Fq12 add_step(G2Proj& T, const Fq2 x2, const Fq2 
     T.X = X3;
     T.Y = Y3;
     T.Z = Z3;
-    return line_to_f12(cy, cx, c3, xP, yP);
+    return make_line(cy, cx, c3, xP, yP);
 }
 
 // pi(Q) on the twist: (conj(x) gamma_{1,2}, conj(y) gamma_{1,3}).
@@ -263,15 +304,15 @@ static __device__ __noinline__ Fq12 miller_loop(const Fq xP, const Fq yP, const 
     fset_one(T.Z);
     for (int i = 63; i >= 0; --i) {
         f = f12_sqr(f);
-        f = f12_mul(f, dbl_step(T, xP, yP));
-        if ((loop_lo >> i) & 1) f = f12_mul(f, add_step(T, xQ, yQ, xP, yP));
+        f = f12_mul_line(f, dbl_step(T, xP, yP));
+        if ((loop_lo >> i) & 1) f = f12_mul_line(f, add_step(T, xQ, yQ, xP, yP));
     }
     Fq2 x1 = xQ, y1 = yQ;
     frob_twist(x1, y1);
     Fq2 x2 = x1, y2 = y1;
     frob_twist(x2, y2);
-    f = f12_mul(f, add_step(T, x1, y1, xP, yP));
-    f = f12_mul(f, add_step(T, x2, f2_neg(y2), xP, yP));
+    f = f12_mul_line(f, add_step(T, x1, y1, xP, yP));
+    f = f12_mul_line(f, add_step(T, x2, f2_neg(y2), xP, yP));
     return f;
 }
 
@@ -287,13 +328,13 @@ static __device__ __noinline__ Fq12 final_exp_hard(const Fq12 t1) {
     y3 = f12_conj(y3);
     const Fq12 y4 = f12_conj(f12_mul(fu, fu2p));
     const Fq12 y6 = f12_conj(f12_mul(fu3, fu3p));
-    Fq12 t0 = f12_mul(f12_mul(f12_sqr(y6), y4), y5);
+    Fq12 t0 = f12_mul(f12_mul(f12_cyc_sqr(y6), y4), y5);
     Fq12 u1 = f12_mul(f12_mul(y3, y5), t0);
     t0 = f12_mul(t0, y2);
-    u1 = f12_sqr(f12_mul(f12_sqr(u1), t0));
+    u1 = f12_cyc_sqr(f12_mul(f12_cyc_sqr(u1), t0));
     t0 = f12_mul(u1, y1);
     u1 = f12_mul(u1, y0);
-    t0 = f12_mul(f12_sqr(t0), u1);
+    t0 = f12_mul(f12_cyc_sqr(t0), u1);
     return t0;
 }
 

@@ -162,9 +162,11 @@ def gather_roots(roots, merk, counts: list[int], group=None):
 
 
 def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
-                  log2_chunk: int = LOG2_CHUNK, backend=None, group=None, codes=None):
+                  log2_chunk: int = LOG2_CHUNK, backend=None, group=None, codes=None,
+                  return_roots: bool = False):
     """One rank's part of a sharded block proof; every rank returns the same
-    (proof289, fc328) device tensors."""
+    (proof289, fc328) device tensors (+ all chunk roots, n_chunks x 289 B,
+    with return_roots: their first 256 B are the chunk proofs)."""
     backend = backend or GpuBackend()
     parts = partition(n_total, world, log2_chunk)
     counts = [n_chunks(c, log2_chunk) for _, c in parts]
@@ -172,7 +174,8 @@ def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
     roots, merk = backend.shard_roots(local, n_total, log2_chunk, codes)
     if world > 1:
         roots, merk = gather_roots(roots, merk, counts, group)
-    return backend.combine(roots, merk, sum(counts), n_total, local.header)
+    out = backend.combine(roots, merk, sum(counts), n_total, local.header)
+    return out + (roots,) if return_roots else out
 
 
 def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None, pk=None,

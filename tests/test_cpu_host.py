@@ -166,3 +166,32 @@ def test_sharded_gloo_world2_matches_global(n, k):
     fc = O.oracle_build_fc(fb, root)
     for _, proof, got_fc in res:
         assert proof == root and got_fc == fc
+
+
+def test_identity_registry_is_the_sorted_set():
+    """IdentityRegistry (pipeline.hpp:22-30): set semantics, and the device
+    layout is the std::set<Hash32> iteration order (bytewise ascending)."""
+    import random
+
+    from paper_2603_10242_b200 import pipeline
+    rng = random.Random(4)
+    ids = [bytes(rng.getrandbits(8) for _ in range(32)) for _ in range(200)]
+    reg = pipeline.IdentityRegistry()
+    for i in ids + ids[:50]:
+        reg.add(i)
+    assert reg.size() == len(set(ids))
+    arr = reg.array().reshape(-1, 32)
+    got = [bytes(r) for r in arr]
+    assert got == sorted(set(ids))
+    assert all(reg.contains(i) for i in ids)
+    assert not reg.contains(b"\xff" * 32)
+    assert pipeline.IdentityRegistry().array().shape == (32,)  # empty: one dummy row, size 0
+
+
+def test_light_check_counters_accumulate():
+    from paper_2603_10242_b200 import pipeline
+    c = pipeline.LightCheckCounters()
+    c += pipeline.LightCheckCounters(3, 2, 1)
+    c += pipeline.LightCheckCounters(1, 1, 1)
+    assert (c.sha256_ops, c.registry_probes, c.window_checks) == (4, 3, 2)
+    assert pipeline.to_string(pipeline.LightCheck.StaleDomain) == "StaleDomain"

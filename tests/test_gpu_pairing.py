@@ -101,10 +101,13 @@ def cpu_op(op, x):
 
 @pytest.mark.parametrize("op", [8, 7, 3, 4, 5, 6])
 def test_f12_unit_ops(M, op):
-    """Square, inverse, Frobenius^1,2,3 (vs plain ^p powers) and ^x."""
+    """Square, inverse, Frobenius^1,2,3 (vs plain ^p powers) and ^x (on
+    cyclotomic-subgroup elements, where the GPU uses Granger-Scott squarings)."""
     rng = random.Random(op)
     for _ in range(2):
         x = rand_f12(rng)
+        if op == 6:
+            x = cpu_op(1, x)
         assert gpu_op(M, op, x) == cpu_op(op, x)
 
 
@@ -122,3 +125,19 @@ def test_miller_loop_up_to_subfield_factors(M):
     mg = gpu_op(M, 9, p + q)
     mc = cpu_op(9, p + q)
     assert gpu_op(M, 1, mg) == cpu_op(1, mc)
+
+
+def test_cyclotomic_square(M):
+    """Granger-Scott squaring on elements after the easy part (cyclotomic
+    subgroup) equals the plain square."""
+    rng = random.Random(21)
+    for _ in range(3):
+        c = gpu_op(M, 1, rand_f12(rng))
+        assert gpu_op(M, 11, c) == cpu_op(8, c)
+
+
+def test_pairing_g2_generator_multiples(M):
+    g1, g2 = gens()
+    ps = [smul(1, g1, k) for k in (2, 3, 11)]
+    qs = [smul(2, g2, k) for k in (5, 7, 13)]
+    assert gpu_pair(M, ps, qs)[0] == cpu_pair(ps, qs)
