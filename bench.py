@@ -342,7 +342,9 @@ def run_ours(args, rank: int, world: int) -> None:
         ach = leaf_c / (phase[0] * 1e-3)
         roof = {"bound": "int_alu", "kernel": "leaf_kernel (K1+K4 fused)",
                 "achieved": ach / 1e9, "peak": peak_cps / 1e9, "unit": "G SHA-256 compressions/s",
-                "frac": ach / peak_cps, "traffic": None,
+                "frac": ach / peak_cps, "traffic": leaf_traffic_bytes(),
+                "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
+                                  "leaf_kernel, profiles/r01_ncu_full_leaf_credential_keytab.csv",
                 "algorithmic_bytes_per_launch": int(fb.offs[n]) + 104 * n + 4 * n + 320 * n + 32 * n,
                 "hbm_gbs_achieved": (int(fb.offs[n]) + 104 * n + 352 * n) / (phase[0] * 1e-3) / 1e9,
                 "phase_ms": {"leaves": phase[0], "tree_levels": phase[1], "finalize": phase[2]},
@@ -683,6 +685,26 @@ def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup,
     if own:
         pk.close()
     return out
+
+
+def leaf_traffic_bytes() -> float | None:
+    """DRAM bytes per leaf_kernel launch from the committed ncu capture."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01_ncu_full_leaf_credential_keytab.csv")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    try:
+        rows = list(csv.reader(open(path)))
+        hdr, units = rows[0], rows[1]
+        for r in rows[2:]:
+            d = dict(zip(hdr, r))
+            if "leaf_kernel" in d.get("Kernel Name", ""):
+                tot = 0.0
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    tot += float(d[k].replace(",", "")) * scale[units[hdr.index(k)]]
+                return tot
+    except (OSError, KeyError, ValueError, IndexError):
+        pass
+    return None
 
 
 def hashlib_sha256(b: bytes) -> str:
