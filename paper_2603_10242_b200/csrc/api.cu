@@ -1652,6 +1652,12 @@ struct acegpu_g16 {
     uint8_t *pts = nullptr, *scaled = nullptr, *rs = nullptr, *digest = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_ab = nullptr, ev_scaled = nullptr;
+    // concurrent MSM streams: B2 + L on s_bl, NTTs + H on s_h, each with its
+    // own MSM scratch, so one MSM's latency-bound sort/reduction phases
+    // overlap another's throughput-bound bucket accumulation
+    cudaStream_t s_bl = nullptr, s_h = nullptr;
+    cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
+    bn::MsmScratch msm_bl, msm_h;
 };
 
 namespace {
@@ -1708,6 +1714,12 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     if (g->side) cudaStreamDestroy(g->side);
     if (g->ev_ab) cudaEventDestroy(g->ev_ab);
     if (g->ev_scaled) cudaEventDestroy(g->ev_scaled);
+    for (cudaStream_t t : {g->s_bl, g->s_h})
+        if (t) cudaStreamDestroy(t);
+    for (cudaEvent_t e : {g->ev_z, g->ev_bl, g->ev_h})
+        if (e) cudaEventDestroy(e);
+    g->msm_bl.release();
+    g->msm_h.release();
     delete g;
 }
 
@@ -1745,6 +1757,10 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->ev_ab, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&g->s_bl, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&g->s_h, cudaStreamNonBlocking));
+    for (cudaEvent_t* e : {&g->ev_z, &g->ev_bl, &g->ev_h})
+        CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // constants
     CK(cudaMemcpyAsync(g->consts, trapdoor5, 160, cudaMemcpyHostToDevice, s));
     bn::g16_setup_consts(g->consts, g->logn, s);
@@ -1849,22 +1865,35 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     bn::g16_derive_rs(d_pub, g->d.T, g->rs, g->digest, s);
     if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, s));
     if (d_digest32) CK(cudaMemcpyAsync(d_digest32, g->digest, 32, cudaMemcpyDeviceToDevice, s));
-    // H(x) = (a b - c) / Z on the coset, back to coefficients
-    const bn::NttTables& t = c->ntt[g->logn];
-    if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
-    for (uint8_t* e : {g->ea, g->eb, g->ec}) {
-        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, s)) return fail(ACEGPU_ECUDA, "g16 intt");
-        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, s)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
-    }
-    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, s);
-    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, s)) return fail(ACEGPU_ECUDA, "g16 coset intt");
-    bn::launch_fr_convert(g->ea, N, 0, s);  // h coefficients -> standard form scalars
     // scalar vectors with their extras
     CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, s));
     bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, s);
     CKL();
-    // MSMs: A and B1 first, then s*A and r*B1 on the side stream under B2/L/H
+    CK(cudaEventRecord(g->ev_z, s));
+    // s_h: H(x) = (a b - c) / Z on the coset, back to coefficients, then [h]
+    const bn::NttTables& t = c->ntt[g->logn];
+    if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
+    cudaStream_t sh = g->s_h;
+    CK(cudaStreamWaitEvent(sh, g->ev_z, 0));
+    for (uint8_t* e : {g->ea, g->eb, g->ec}) {
+        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sh)) return fail(ACEGPU_ECUDA, "g16 intt");
+        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sh)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
+    }
+    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sh);
+    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, sh)) return fail(ACEGPU_ECUDA, "g16 coset intt");
+    bn::launch_fr_convert(g->ea, N, 0, sh);  // h coefficients -> standard form scalars
+    CKL();
+    if (bn::msm_run(1, g->qh->table, N - 1, g->ea, g->msm_h, g->pts + 320, sh))
+        return fail(ACEGPU_ECUDA, "g16 msm H");
+    CK(cudaEventRecord(g->ev_h, sh));
+    // s_bl: [v]2 (B2) and [l] (L)
+    CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
+    if (bn::msm_run(2, g->qb2->table, V + 2, g->zb, g->msm_bl, g->pts + 128, g->s_bl) ||
+        bn::msm_run(1, g->ql->table, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
+        return fail(ACEGPU_ECUDA, "g16 msm B2/L");
+    CK(cudaEventRecord(g->ev_bl, g->s_bl));
+    // s: A and B1, then s*A and r*B1 on the side stream
     if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, s) ||
         bn::msm_run(1, g->qb1->table, V + 2, g->zb, c->msm, g->pts + 64, s))
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
@@ -1872,11 +1901,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CK(cudaStreamWaitEvent(g->side, g->ev_ab, 0));
     bn::g16_scale(g->pts, g->rs, g->scaled, g->side);
     CK(cudaEventRecord(g->ev_scaled, g->side));
-    if (bn::msm_run(2, g->qb2->table, V + 2, g->zb, c->msm, g->pts + 128, s) ||
-        bn::msm_run(1, g->ql->table, g->Vp + 1, g->zl, c->msm, g->pts + 256, s) ||
-        bn::msm_run(1, g->qh->table, N - 1, g->ea, c->msm, g->pts + 320, s))
-        return fail(ACEGPU_ECUDA, "g16 msm B2/L/H");
-    CK(cudaStreamWaitEvent(s, g->ev_scaled, 0));
+    for (cudaEvent_t e : {g->ev_scaled, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
     bn::g16_assemble(g->pts, g->scaled, d_proof256, d_raw256, s);
     CKL();
     c->launches += 16 + 5 * 7 + 6;
