@@ -38,6 +38,10 @@ N_TX = 100_000
 SLOT = 40
 
 
+def bench_device() -> int:
+    return int(os.environ.get("ACE_BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+
+
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
@@ -223,7 +227,7 @@ def run_ours(args, rank: int, world: int) -> None:
     import torch.distributed as dist
     from paper_2603_10242_b200 import _native as N, shard
 
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = bench_device()
     torch.cuda.set_device(dev)
     ctx = N.context(dev)
     n = args.n_tx
@@ -264,7 +268,11 @@ def run_ours(args, rank: int, world: int) -> None:
     torch.cuda.synchronize()
     g = golden_fc(n)
     fc_hex = fc.cpu().numpy().tobytes().hex()
-    acc = int((codes[:count] == 0).sum().item())
+    acc_t = (codes[:count] == 0).sum().to(torch.int64).reshape(1)
+    if world > 1:  # verdicts of the whole block
+        import torch.distributed as dist
+        dist.all_reduce(acc_t)
+    acc = int(acc_t.item())
     parity = {"fc_matches_golden": (fc_hex == g) if g else None, "accepted": acc,
               "fc_sha256_prefix": None}
 
@@ -861,7 +869,7 @@ def run_groth16_mode(args, rank: int, world: int) -> None:
     (BASELINE configs[3]); latency vs the 400 ms block interval."""
     import torch
     from paper_2603_10242_b200 import _native as N
-    dev = int(os.environ.get("LOCAL_RANK", 0))
+    dev = bench_device()
     torch.cuda.set_device(dev)
     ctx = N.context(dev)
     fb, revs, rix = canonical_block_host(args.n_tx, ctx)
@@ -905,8 +913,10 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(bench_device())
+        # ACE_DIST_BACKEND / ACE_BENCH_DEVICE: functional multi-rank runs on a
+        # one-GPU box (gloo, every rank on cuda:0) -- never a measurement
+        dist.init_process_group(os.environ.get("ACE_DIST_BACKEND", "nccl"))
     try:
         if args.mode == "groth16":
             run_groth16_mode(args, rank, world)
