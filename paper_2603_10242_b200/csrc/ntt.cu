@@ -15,6 +15,8 @@
 // IMAD-pipe bound (NTT at 2^21-2^22 is ~8x above the HBM ridge).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "bn254.cuh"
 #include "ntt.cuh"
 
@@ -61,6 +63,9 @@ struct PassArgs {
     const Fr* w_sub;     // roots of the sub-DFT (size 2^(m-1))
     const Fr* tw_lo;     // pass A: w^e for e < n2 ; pass C: unused
     const Fr* tw_hi;     // pass A: w^(n2*e) for e < n1
+    const Fr* tw_full;   // pass A: w^e for e < n (replaces tw_lo * tw_hi when present)
+    const Fr* pre_full;  // pass A coset: g^idx (replaces pre_lo * pre_hi)
+    const Fr* post_full; // pass C coset: n^-1 g^-idx (replaces post_lo * post_hi)
     const Fr* pre_lo;    // pass A coset: g^i1 (n1) ; single: g^i (n)
     const Fr* pre_hi;    // pass A coset: g^(n1*i2) (n2)
     const Fr* post_lo;   // pass C: scale_k2 (n2), e.g. n^-1 g^-k2
@@ -79,7 +84,8 @@ __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
         const int i1 = i1_0 + r;
         const uint64_t idx = i1 + (uint64_t)n1 * i2;
         Fr x = load<FrCfg>(a.in + 32 * idx);
-        if (a.pre_lo) x = mul(x, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[i2])));
+        if (a.pre_full) x = mul(x, ld(&a.pre_full[idx]));
+        else if (a.pre_lo) x = mul(x, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[i2])));
         st(&s[bitrev(i2, a.L2) * R + r], x);
     }
     __syncthreads();
@@ -90,8 +96,12 @@ __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
         Fr x = ld(&s[k2 * R + r]);
         // twiddle w^(i1*k2), exponent < n, split as lo (L2 bits) + hi
         const uint64_t ex = (uint64_t)i1 * k2;
-        const uint32_t lo = ex & (n2 - 1), hi = ex >> a.L2;
-        if (ex) x = mul(x, mul(ld(&a.tw_lo[lo]), ld(&a.tw_hi[hi])));
+        if (a.tw_full) {
+            if (ex) x = mul(x, ld(&a.tw_full[ex]));
+        } else {
+            const uint32_t lo = ex & (n2 - 1), hi = ex >> a.L2;
+            if (ex) x = mul(x, mul(ld(&a.tw_lo[lo]), ld(&a.tw_hi[hi])));
+        }
         store<FrCfg>(a.out + 32 * (i1 + (uint64_t)n1 * k2), x);
     }
 }
@@ -113,7 +123,8 @@ __global__ void __launch_bounds__(512) ntt_pass_c(PassArgs a) {
         const int r = e % R, k1 = e / R;
         const int k2 = k2_0 + r;
         Fr x = ld(&s[k1 * R + r]);
-        if (a.post_lo) x = mul(x, mul(ld(&a.post_lo[k2]), ld(&a.post_hi[k1])));
+        if (a.post_full) x = mul(x, ld(&a.post_full[k2 + (uint64_t)n2 * k1]));
+        else if (a.post_lo) x = mul(x, mul(ld(&a.post_lo[k2]), ld(&a.post_hi[k1])));
         else if (a.scale) x = mul(x, ld(a.scale));
         store<FrCfg>(a.out + 32 * (k2 + (uint64_t)n2 * k1), x);
     }
@@ -225,14 +236,17 @@ int ntt_tables(NttTables& t, int L, cudaStream_t s) {
         pw(&t.tw_lo, w, 1, n2, nullptr) || pw(&t.tw_hi, w, n2, n1, nullptr) ||
         pw(&t.twi_lo, wi, 1, n2, nullptr) || pw(&t.twi_hi, wi, n2, n1, nullptr) ||
         pw(&t.g_lo, g, 1, n1, nullptr) || pw(&t.g_hi, g, n1, n2, nullptr) ||
-        pw(&t.gi_post_lo, gi, 1, n2, ninv) || pw(&t.gi_post_hi, gi, n2, n1, nullptr))
+        pw(&t.gi_post_lo, gi, 1, n2, ninv) || pw(&t.gi_post_hi, gi, n2, n1, nullptr) ||
+        pw(&t.tw_full, w, 1, n, nullptr) || pw(&t.twi_full, wi, 1, n, nullptr) ||
+        pw(&t.g_full, g, 1, n, nullptr) || pw(&t.gi_post_full, gi, 1, n, ninv))
         return -1;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
 void NttTables::release() {
     Fr** all[] = {&consts, &w_a, &wi_a, &w_c, &wi_c, &tw_lo, &tw_hi, &twi_lo, &twi_hi,
-                  &g_lo, &g_hi, &gi_post_lo, &gi_post_hi};
+                  &g_lo, &g_hi, &gi_post_lo, &gi_post_hi, &tw_full, &twi_full, &g_full,
+                  &gi_post_full};
     for (Fr** p : all) {
         if (*p) cudaFree(*p);
         *p = nullptr;
@@ -269,8 +283,11 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
     a.w_sub = inverse ? t.wi_a : t.w_a;
     a.tw_lo = inverse ? t.twi_lo : t.tw_lo;
     a.tw_hi = inverse ? t.twi_hi : t.tw_hi;
+    static const bool full = !getenv("ACEGPU_NTT_SPLIT_TW");
+    a.tw_full = full ? (inverse ? t.twi_full : t.tw_full) : nullptr;
     a.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
     a.pre_hi = (coset && !inverse) ? t.g_hi : nullptr;
+    a.pre_full = (full && coset && !inverse) ? t.g_full : nullptr;
     size_t smem = sizeof(Fr) * (size_t)n2 * kNttR;
     cudaFuncSetAttribute(ntt_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     ntt_pass_a<<<n1 / kNttR, 512, smem, s>>>(a);
@@ -282,6 +299,8 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
     c.pre_lo = c.pre_hi = nullptr;
     c.post_lo = (coset && inverse) ? t.gi_post_lo : nullptr;
     c.post_hi = (coset && inverse) ? t.gi_post_hi : nullptr;
+    c.pre_full = nullptr;
+    c.post_full = (full && coset && inverse) ? t.gi_post_full : nullptr;
  if (inverse && !coset) c.scale = t.consts + 4;
     smem = sizeof(Fr) * (size_t)n1 * kNttR;
     cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
