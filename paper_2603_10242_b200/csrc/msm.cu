@@ -36,11 +36,18 @@ __device__ __forceinline__ Fq2 finv(const Fq2& a) {
 __device__ __forceinline__ Fq fneg(const Fq& a) { return neg(a); }
 __device__ __forceinline__ Fq2 fneg(const Fq2& a) { return {neg(a.c0), neg(a.c1)}; }
 
+#ifndef ACEGPU_G2_ACC_MINB
+#define ACEGPU_G2_ACC_MINB 1  // measured (paper-size chunk): 1 -> 60.1 ms, 3 -> 61.4, 4 -> 61.1
+#endif
 template <class F>
 struct Lay {
     static constexpr int EB = felem_bytes<F>();
     static constexpr int AFF = 2 * EB;
     static constexpr int XZ = 4 * EB;
+    // accumulate_kernel min CTAs/SM (register cap): G2's Fq2 temporaries
+    // take 216 registers -> 2 CTAs (8 warps) per SM; capping them spills
+    // and measured slower
+    static constexpr int ACC_MIN_CTAS = EB == 32 ? 1 : ACEGPU_G2_ACC_MINB;
 };
 
 template <class F>
@@ -208,7 +215,7 @@ __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
 // One thread per chunk (<= kMsmSeg entries of one bucket): mixed-add the
 // chunk's bases into one XYZZ partial.
 template <class F>
-__global__ void __launch_bounds__(128) accumulate_kernel(const uint8_t* table,
+__global__ void __launch_bounds__(128, Lay<F>::ACC_MIN_CTAS) accumulate_kernel(const uint8_t* table,
                                                          const uint32_t* sorted,
                                                          const uint32_t* offs,
                                                          const uint32_t* coffs,
