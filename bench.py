@@ -531,7 +531,7 @@ def bench_bn254(ctx, dev: int, reps: int = 5) -> dict:
     return out
 
 
-def bench_stream(ctx, dev: int, blocks: int = 30, n: int = 12800, lanes: int = 4) -> dict:
+def bench_stream(ctx, dev: int, blocks: int = 30, n: int = 12800, lanes: int = 8) -> dict:
     """32,000 TPS x 0.4 s = 12,800-tx blocks, >= 30
     consecutive blocks through the pipelined prover (block n+1's H2D copy and
     attestation overlap block n's tree). Host inputs are pinned once before

@@ -116,6 +116,19 @@ int acegpu_attest_prove_certify(acegpu_ctx* ctx, const uint8_t* payloads, const 
                                 const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,
                                 uint8_t* codes, uint8_t* out289, uint8_t* out_fc328,
                                 uint64_t* levels, uint64_t* pair_ops);
+/* As acegpu_attest_prove_certify, enqueued on `stream` without waiting: the
+ * H2D copies, the pipeline and the D2H of codes / proof / FC are
+ * stream-ordered; the caller synchronises (event / stream) before reading
+ * the outputs. Host buffers should be pinned (acegpu_host_alloc) for the
+ * copies to be asynchronous, and must stay untouched until completion.
+ * Successive async calls on one context must use the same stream (the
+ * context's device workspace is reused in stream order). This is the
+ * sustained-stream entry point (one call per block, ~20 launches). */
+int acegpu_attest_prove_certify_async(acegpu_ctx* ctx, void* stream, const uint8_t* payloads,
+                                      const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                                      const uint8_t* header, const uint8_t* revs,
+                                      uint64_t n_revs, const uint32_t* rev_index, uint8_t* codes,
+                                      uint8_t* out289, uint8_t* out328);
 int acegpu_attest_prove_certify_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
                                     const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
                                     const uint8_t* d_header256, const uint8_t* d_revs,

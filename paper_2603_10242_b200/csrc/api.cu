@@ -607,11 +607,14 @@ int acegpu_aggregate_tree(acegpu_ctx* c, const uint8_t* proofs, uint64_t n, uint
     return ACEGPU_OK;
 }
 
-int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
-                                const uint8_t* atts, uint64_t n, const uint8_t* header,
-                                const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,
-                                uint8_t* codes, uint8_t* out289, uint8_t* out328,
-                                uint64_t* levels, uint64_t* pair_ops) {
+}  // extern "C"
+
+namespace {
+// Host-buffer attest+prove+certify on stream s; sync = wait for completion.
+int apc_host(acegpu_ctx* c, cudaStream_t s, bool sync, const uint8_t* payloads,
+             const uint64_t* offs, const uint8_t* atts, uint64_t n, const uint8_t* header,
+             const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index, uint8_t* codes,
+             uint8_t* out289, uint8_t* out328) {
     RET(check_n(n));
     if (codes && n && (!revs || !rev_index || n_revs == 0))
         return fail(ACEGPU_EINVAL, "attestation needs a REV table and index");
@@ -621,7 +624,6 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
     }
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
-    cudaStream_t s = c->stream;
     uint8_t *dp, *da, *dh, *dout, *dr = nullptr, *dc = nullptr;
     uint64_t* doff;
     uint32_t* dri = nullptr;
@@ -658,10 +660,32 @@ int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const ui
     if (dc) CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
     if (out289) CK(cudaMemcpyAsync(out289, dout, 289, cudaMemcpyDeviceToHost, s));
     if (out328) CK(cudaMemcpyAsync(out328, dout + 304, 328, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    if (sync) CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int acegpu_attest_prove_certify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t* offs,
+                                const uint8_t* atts, uint64_t n, const uint8_t* header,
+                                const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,
+                                uint8_t* codes, uint8_t* out289, uint8_t* out328,
+                                uint64_t* levels, uint64_t* pair_ops) {
+    RET(apc_host(c, c->stream, true, payloads, offs, atts, n, header, revs, n_revs, rev_index,
+                 codes, out289, out328));
     if (levels) *levels = n ? ceil_log2(n) : 0;
     if (pair_ops) *pair_ops = n ? n - 1 : 0;
     return ACEGPU_OK;
+}
+
+int acegpu_attest_prove_certify_async(acegpu_ctx* c, void* stream, const uint8_t* payloads,
+                                      const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                                      const uint8_t* header, const uint8_t* revs,
+                                      uint64_t n_revs, const uint32_t* rev_index,
+                                      uint8_t* codes, uint8_t* out289, uint8_t* out328) {
+    return apc_host(c, pick(c, stream), false, payloads, offs, atts, n, header, revs, n_revs,
+                    rev_index, codes, out289, out328);
 }
 
 int acegpu_attest_prove_certify_dev(acegpu_ctx* c, void* stream, const uint8_t* payloads,

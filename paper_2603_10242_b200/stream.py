@@ -3,14 +3,14 @@
 
 The reference's worker proves one block at a time. Here blocks are spread
 over `lanes` independent libacegpu contexts, each with its own CUDA stream,
-device workspace and pinned staging buffers, so block n+1's host->device copy
+device workspace and pinned output buffers, so block n+1's host->device copy
 and attestation run while block n's proof tree is still being hashed (a
 12,800-tx block's upper tree levels are latency chains that leave most SMs
 idle). Everything is stream-ordered and asynchronous from the submitting
-thread; per-block latency is taken from CUDA events on the lane's stream
-(submission of the H2D copy -> FC and verdicts back in pinned host memory).
-
-Device work goes through acegpu_attest_prove_certify_dev (include/acegpu.h).
+thread, one C-ABI call per block (acegpu_attest_prove_certify_async: H2D of
+the pinned inputs, the pipeline, D2H of verdicts / proof / FC); per-block
+latency is taken from CUDA events on the lane's stream (H2D start -> FC and
+verdicts back in pinned host memory).
 """
 from __future__ import annotations
 
@@ -37,21 +37,13 @@ class _Lane:
         self.ctx = N.Context(device)
         self.dev = torch.device("cuda", device)
         self.stream = torch.cuda.Stream(device=self.dev)
-        u8 = dict(dtype=torch.uint8, device=self.dev)
-        self.d_pay = torch.empty(max_payload + 16, **u8)
-        self.d_offs = torch.empty(max_tx + 1, dtype=torch.int64, device=self.dev)
-        self.d_atts = torch.empty(104 * max_tx + 8, **u8)
-        self.d_hdr = torch.empty(256, **u8)
-        self.d_revs = torch.empty(32 * max_revs, **u8)
-        self.d_rix = torch.empty(max(max_tx, 1), dtype=torch.int32, device=self.dev)
-        self.d_codes = torch.empty(max(max_tx, 1), **u8)
-        self.d_out = torch.empty(640, **u8)
         self.h_codes = torch.empty(max(max_tx, 1), dtype=torch.uint8).pin_memory()
         self.h_out = torch.empty(640, dtype=torch.uint8).pin_memory()
         self.ev0 = torch.cuda.Event(enable_timing=True)
         self.ev1 = torch.cuda.Event(enable_timing=True)
         self.ticket = None
         self.n = 0
+        self.pinned = None
 
 
 class PipelinedProver:
@@ -79,6 +71,7 @@ class PipelinedProver:
             lane.ticket, lane.h_codes.numpy()[:n].copy(), out[:289].tobytes(),
             out[304:304 + 328].tobytes(), lane.ev0.elapsed_time(lane.ev1))
         lane.ticket = None
+        lane.pinned = None
 
     def submit(self, fb: FlatBlock, revs: np.ndarray, rev_index: np.ndarray,
                pinned: dict | None = None) -> int:
@@ -95,25 +88,19 @@ class PipelinedProver:
         self._collect(lane)
         if pinned is None:
             pinned = pin_block(fb, revs, rev_index)
-        with torch.cuda.stream(lane.stream):
-            lane.ev0.record(lane.stream)
-            if n:
-                lane.d_pay[:nb].copy_(pinned["payloads"][:nb], non_blocking=True)
-                lane.d_offs[:n + 1].copy_(pinned["offs"][:n + 1], non_blocking=True)
-                lane.d_atts[:104 * n].copy_(pinned["atts"][:104 * n], non_blocking=True)
-                lane.d_rix[:n].copy_(pinned["rev_index"][:n], non_blocking=True)
-            lane.d_hdr.copy_(pinned["header"], non_blocking=True)
-            nr = len(revs) // 32
-            lane.d_revs[:32 * nr].copy_(pinned["revs"][:32 * nr], non_blocking=True)
-            lane.ctx.call("acegpu_attest_prove_certify_dev", lane.stream.cuda_stream,
-                          lane.d_pay.data_ptr(), lane.d_offs.data_ptr(), lane.d_atts.data_ptr(),
-                          n, lane.d_hdr.data_ptr(), lane.d_revs.data_ptr(), nr,
-                          lane.d_rix.data_ptr(), lane.d_codes.data_ptr() if n else None,
-                          lane.d_out.data_ptr(), lane.d_out.data_ptr() + 304)
-            if n:
-                lane.h_codes[:n].copy_(lane.d_codes[:n], non_blocking=True)
-            lane.h_out.copy_(lane.d_out, non_blocking=True)
-            lane.ev1.record(lane.stream)
+        nr = len(revs) // 32
+        lane.ev0.record(lane.stream)
+        # one C-ABI call per block: H2D (pinned), attestation + proof + FC,
+        # D2H of verdicts / proof / FC, all stream-ordered on the lane's stream
+        lane.ctx.call("acegpu_attest_prove_certify_async", lane.stream.cuda_stream,
+                      pinned["payloads"].data_ptr(), pinned["offs"].data_ptr(),
+                      pinned["atts"].data_ptr(), n, pinned["header"].data_ptr(),
+                      pinned["revs"].data_ptr() if n else None, nr if n else 0,
+                      pinned["rev_index"].data_ptr() if n else None,
+                      lane.h_codes.data_ptr() if n else None, lane.h_out.data_ptr(),
+                      lane.h_out.data_ptr() + 304)
+        lane.ev1.record(lane.stream)
+        lane.pinned = pinned  # inputs must outlive the asynchronous copies
         lane.ticket, lane.n = t, n
         return t
 
