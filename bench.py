@@ -498,7 +498,9 @@ def bench_bn254(ctx, dev: int, reps: int = 5) -> dict:
     f_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, x.data_ptr(), y.data_ptr(), L, 0, 0))
     i_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, y.data_ptr(), y.data_ptr(), L, 1, 0))
     c_ms = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, x.data_ptr(), y.data_ptr(), L, 0, 1))
-    muls = (n // 2) * L + 2 * n  # butterflies + pass-A twiddles
+    # butterflies + one pass-A twiddle product per element (full-size tables);
+    # the j = 0 butterflies skip their product but are counted, as usual
+    muls = (n // 2) * L + n
     bytes_moved = 2 * 2 * n * 32  # two passes, read + write
     out["ntt_2^22"] = {
         "forward_ms": f_ms, "inverse_ms": i_ms, "coset_forward_ms": c_ms,
@@ -617,7 +619,7 @@ def bench_groth16(ctx, dev: int, fq_rate: float, chunks: int = 16, reps: int = 3
     Vp = V - 1 - T
     madds = 16 * ((V + 2) * 2 + Vp + 1 + (Np - 1))  # G1 MSMs: A, B1, L, H
     fq_muls = madds * 10 + 16 * (V + 2) * 10 * 3     # + G2 (Fq2 mul = 3 Fq muls)
-    fr_muls = 7 * ((Np // 2) * pk.log_domain + 2 * Np)
+    fr_muls = 7 * ((Np // 2) * pk.log_domain + Np)
     pk.close()
     return {"txs_per_chunk": T, "constraints_per_tx": K, "constraints": pk.constraints,
             "domain": Np, "setup_s_once": setup_s, "chunk_prove_ms": chunk_ms,
