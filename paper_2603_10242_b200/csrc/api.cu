@@ -60,7 +60,7 @@ int fail(int code, const std::string& msg) {
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
     kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kSegRoots, kSegMerk,
-    kKeytab, kKeydom, kP1Scratch, kP1Hash, kP1Reg, kNumSlots
+    kKeytab, kKeydom, kP1Scratch, kP1Hash, kP1Reg, kErr, kNumSlots
 };
 
 struct DevBuf {
@@ -99,6 +99,8 @@ struct acegpu_ctx {
     // attest-key cache of the call in flight (launch_keytab / launch_credentials)
     const uint32_t* cur_keytab = nullptr;
     const uint8_t* cur_keydom = nullptr;
+    uint32_t cur_n_revs = 0;  // REV table size of the call in flight (index guard)
+    int* cur_err = nullptr;   // device flag: an out-of-range rev_index was seen
     // Side stream of the attestation credential check (keytab + credential
     // kernels), overlapping the leaf kernel and the tree levels.
     cudaStream_t cred_stream = nullptr;
@@ -232,7 +234,7 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
         CK(cudaEventRecord(c->cred_in, s));
         CK(cudaStreamWaitEvent(c->cred_stream, c->cred_in, 0));
         launch_credentials(atts, n, revs, rev_index, c->cur_keytab, c->cur_keydom, codes,
-                           c->cred_stream);
+                           c->cur_n_revs, c->cur_err, c->cred_stream);
         CKL();
         c->launches++;
         CK(cudaEventRecord(c->cred_out, c->cred_stream));
@@ -287,8 +289,11 @@ struct KeytabScope {
     ~KeytabScope() {
         c->cur_keytab = nullptr;
         c->cur_keydom = nullptr;
+        c->cur_n_revs = 0;
+        c->cur_err = nullptr;
     }
     int build(cudaStream_t s, const uint8_t* d_revs, uint64_t n_revs, const uint8_t* d_dom8) {
+        c->cur_n_revs = uint32_t(std::min<uint64_t>(n_revs, 0xFFFFFFFFull));
         if (!d_revs || !n_revs || n_revs > 0xFFFFFFFFull) return ACEGPU_OK;
         uint32_t* kt;
         RET(ws(c, kKeytab, 64 * n_revs, &kt));
@@ -618,23 +623,28 @@ int apc_host(acegpu_ctx* c, cudaStream_t s, bool sync, const uint8_t* payloads,
     RET(check_n(n));
     if (codes && n && (!revs || !rev_index || n_revs == 0))
         return fail(ACEGPU_EINVAL, "attestation needs a REV table and index");
-    if (codes && n) {
-        for (uint64_t i = 0; i < n; ++i)
-            if (rev_index[i] >= n_revs) return fail(ACEGPU_EINVAL, "rev_index out of range");
-    }
+    if (n_revs > 0xFFFFFFFFull) return fail(ACEGPU_EINVAL, "REV table too large");
+    // rev_index bounds are checked on the device (credential_kernel), not in an
+    // O(n) host loop ahead of the copies (measured ~45 us of the 100k e2e)
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     uint8_t *dp, *da, *dh, *dout, *dr = nullptr, *dc = nullptr;
     uint64_t* doff;
     uint32_t* dri = nullptr;
+    int* derr = nullptr;
     RET(h2d_t(c, kHeader, header, 256, s, &dh));
     RET(ws(c, kOut, 289 + 328 + 16, &dout));
     KeytabScope kts(c);
+    if (codes && n) {
+        RET(ws(c, kErr, 16, &derr));
+        CK(cudaMemsetAsync(derr, 0, sizeof(int), s));
+    }
     uint8_t* dkeydom = nullptr;
     if (codes && n) {
         RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &dr));
         RET(h2d_t(c, kKeydom, atts + 64, 8, s, &dkeydom));  // tx 0's domain
         RET(kts.build(s, dr, n_revs, dkeydom));
+        c->cur_err = derr;
     }
     if (use_segments(c, n)) {
         // REV table first; offset/payload/attestation slices are copied per
@@ -660,7 +670,10 @@ int apc_host(acegpu_ctx* c, cudaStream_t s, bool sync, const uint8_t* payloads,
     if (dc) CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));
     if (out289) CK(cudaMemcpyAsync(out289, dout, 289, cudaMemcpyDeviceToHost, s));
     if (out328) CK(cudaMemcpyAsync(out328, dout + 304, 328, cudaMemcpyDeviceToHost, s));
+    int herr = 0;
+    if (derr && sync) CK(cudaMemcpyAsync(&herr, derr, sizeof(int), cudaMemcpyDeviceToHost, s));
     if (sync) CK(cudaStreamSynchronize(s));
+    if (herr) return fail(ACEGPU_EINVAL, "rev_index out of range");
     return ACEGPU_OK;
 }
 }  // namespace
@@ -1143,7 +1156,8 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
             CK(cudaEventRecord(c->leaf_events[j % kLeafStreams], ls));
             CK(cudaStreamWaitEvent(c->cred_stream, c->leaf_events[j % kLeafStreams], 0));
             launch_credentials(atts + 104 * a, uint32_t(cnt), revs, rev_index + a,
-                               c->cur_keytab, c->cur_keydom, codes + a, c->cred_stream);
+                               c->cur_keytab, c->cur_keydom, codes + a, c->cur_n_revs,
+                               c->cur_err, c->cred_stream);
             CKL();
             c->launches++;
         }
@@ -1237,7 +1251,7 @@ int acegpu_attest_verify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t*
     RET(ws(c, kKeytab, 64 * n_revs, &kt));
     launch_keytab(dr, uint32_t(n_revs), da + 64, kt, s);  // tx 0's domain
     CKL();
-    launch_credentials(da, uint32_t(n), dr, dri, kt, da + 64, dc, s);
+    launch_credentials(da, uint32_t(n), dr, dri, kt, da + 64, dc, uint32_t(n_revs), nullptr, s);
     CKL();
     c->launches += 3;
     CK(cudaMemcpyAsync(codes, dc, n, cudaMemcpyDeviceToHost, s));

@@ -469,9 +469,14 @@ __global__ void keytab_kernel(const uint8_t* revs, uint32_t n_revs, const uint8_
 // cached midstates (2 compressions), any other domain the full derivation.
 __global__ void __launch_bounds__(kThreads) credential_kernel(
     const uint8_t* atts, uint32_t n, const uint8_t* revs, const uint32_t* rev_index,
-    const uint32_t* keytab, const uint8_t* keydom, uint8_t* codes) {
+    const uint32_t* keytab, const uint8_t* keydom, uint8_t* codes, uint32_t n_revs, int* err) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n || codes[i]) return;
+    if (rev_index[i] >= n_revs) {  // API misuse: flagged (host API -> EINVAL), never read
+        if (err) atomicOr(err, 1);
+        codes[i] = 2;
+        return;
+    }
     const uint8_t* att = atts + 104ull * i;
     const uint2 dv = *reinterpret_cast<const uint2*>(att + 64);
     const uint32_t dom0 = bswap32(dv.x), dom1 = bswap32(dv.y);
@@ -744,10 +749,10 @@ void launch_keytab(const uint8_t* revs, uint32_t n_revs, const uint8_t* dom8, ui
 
 void launch_credentials(const uint8_t* atts, uint32_t n, const uint8_t* revs,
                         const uint32_t* rev_index, const uint32_t* keytab, const uint8_t* keydom,
-                        uint8_t* codes, cudaStream_t s) {
+                        uint8_t* codes, uint32_t n_revs, int* err, cudaStream_t s) {
     if (n)
         credential_kernel<<<blocks_for(n), kThreads, 0, s>>>(atts, n, revs, rev_index, keytab,
-                                                             keydom, codes);
+                                                             keydom, codes, n_revs, err);
 }
 
 void launch_derive_attest_keys(const uint8_t* revs, const uint8_t* doms8, uint32_t n,

@@ -30,9 +30,10 @@ struct LeafArgs {
 void launch_leaves(const LeafArgs& a, cudaStream_t s);
 // Credential check of verify_attestation_full for every tx with codes[i] == 0
 // (sets 2 on mismatch). keytab (launch_keytab for domain keydom) may be null.
+// rev_index[i] >= n_revs sets *err (if given) and code 2 without reading.
 void launch_credentials(const uint8_t* atts, uint32_t n, const uint8_t* revs,
                         const uint32_t* rev_index, const uint32_t* keytab, const uint8_t* keydom,
-                        uint8_t* codes, cudaStream_t s);
+                        uint8_t* codes, uint32_t n_revs, int* err, cudaStream_t s);
 // Attest-key cache: per REV u, the HMAC ipad/opad midstates of
 // derive_attest_key(REV_u, D0), D0 = the 8-B domain at dom8 (16 words per REV).
 void launch_keytab(const uint8_t* revs, uint32_t n_revs, const uint8_t* dom8, uint32_t* keytab,

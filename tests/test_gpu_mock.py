@@ -459,3 +459,20 @@ def test_pipelined_prover_stream():
         assert r.proof289 == oproof
         assert r.fc328 == O.oracle_build_fc(fb, oproof)
         assert r.latency_ms > 0
+
+
+def test_rev_index_out_of_range_is_einval_after_the_run(P):
+    """An out-of-range REV index is caught on the device (no O(n) host scan
+    ahead of the copies): the host API still raises (EINVAL), for both the
+    single-pass and the segmented pipeline, and the context stays usable."""
+    for n in (1000, 20000):
+        fb = O.multi_user_block(n, 3)
+        bad = fb.rev_index.copy()
+        bad[n // 2] = 7  # 3 REVs
+        fb2 = O.FlatBlock(fb.payloads, fb.offs, fb.atts, fb.header, fb.revs, bad)
+        with pytest.raises(ValueError):
+            gpu_block(P, fb2)
+        proof, fc, codes, _, _ = gpu_block(P, fb)
+        assert (codes == 0).all()
+        oproof, _, _ = O.oracle_prove_block(fb)
+        assert proof == oproof
