@@ -188,6 +188,78 @@ __global__ void __launch_bounds__(kThreads) leaf_kernel(LeafArgs a) {
     }
 }
 
+// One proof pair of a narrow level with 8 lanes per pair (t = pair index,
+// lane = 0..7, wk = this group's 520-word shared-memory schedule area):
+// the lanes precompute the W+K schedules of the 8 data blocks of
+// SHA(a | b) in parallel, then every lane runs only the rounds of the 9-block
+// digest chain (padding block's schedule is a compile-time constant), the
+// seed, and its own expand block. Odd last node promoted (prover.cpp:119-121).
+// Bank layout: block stride 65 words, group stride 520 (= 8 mod 32).
+__device__ __forceinline__ void pair8(const uint8_t* __restrict__ nin, uint32_t nn,
+                                      uint8_t* __restrict__ nout, uint32_t t, uint32_t lane,
+                                      uint32_t* wk) {
+    const uint32_t p = nn / 2;
+    if (t < p) {
+        const uint8_t* a = nin + static_cast<uint64_t>(kNodeBytes) * (2 * t);
+        {
+            const uint32_t blk = lane;
+            const uint4* q = reinterpret_cast<const uint4*>((blk < 4 ? a : a + kNodeBytes) + 64 * (blk & 3));
+            uint32_t w[16];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint4 v = q[k];
+                w[4 * k] = bswap32(v.x);
+                w[4 * k + 1] = bswap32(v.y);
+                w[4 * k + 2] = bswap32(v.z);
+                w[4 * k + 3] = bswap32(v.w);
+            }
+            sha256_schedule_wk(w, wk + 65 * blk);
+        }
+    }
+    __syncwarp();
+    if (t < p) {
+        uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
+        uint32_t d[8], seed[8];
+        sha256_init(d);
+        // compact (rolled) compressions: this chain runs once per level, so
+        // its code size is I-cache-miss latency
+#pragma unroll 1
+        for (int blk = 0; blk < 8; ++blk) {
+            const uint32_t* wb = wk + 65 * blk;
+            sha256_rounds_c(d, [wb](int i) { return wb[i]; });
+        }
+        sha256_rounds_c(d, [](int i) { return kPadWk512.v[i]; });
+        expand_seed<true>(1, d, seed);
+        uint32_t o[8];
+        expand_block<true>(seed, lane, o);
+        store_digest(out + 32 * lane, o);
+        if (lane == 0) write_node_tail(out, d, 1);
+    } else if (t == p && (nn & 1) && lane == 0) {
+        const uint4* src = reinterpret_cast<const uint4*>(nin + static_cast<uint64_t>(kNodeBytes) * (nn - 1));
+        uint4* dd = reinterpret_cast<uint4*>(nout + static_cast<uint64_t>(kNodeBytes) * p);
+#pragma unroll
+        for (int k = 0; k < kNodeBytes / 16; ++k) dd[k] = src[k];
+    }
+}
+
+// One Merkle pair (wire.cpp:236-250): inner H(0x01 | l | r), an odd last node
+// paired with itself; with lift a lone node keeps self-pairing.
+__device__ __forceinline__ void merkle_pair(const uint8_t* __restrict__ min_, uint32_t nm,
+                                            uint8_t* __restrict__ mout, uint32_t u, int lift) {
+    const uint32_t mp = (nm == 1 && !lift) ? 0 : (nm + 1) / 2;
+    if (u < mp) {
+        uint32_t l[8], r[8], h[8];
+        load_be8(min_ + 64ull * u, l);
+        if (2 * u + 1 < nm) load_be8(min_ + 64ull * u + 32, r);
+        else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) r[k] = l[k];  // duplicate last (wire.cpp:240)
+        }
+        merkle_inner(l, r, h);
+        store_digest(mout + 32ull * u, h);
+    }
+}
+
 // ------------------------------------------------------------------ levels
 // G lanes per pair. Every lane of a group runs the 9-block digest chain and
 // the seed in lock-step (SIMT: no extra issue slots, no shuffles) and then
@@ -208,57 +280,8 @@ __global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restri
         const uint32_t t = g / G, lane = g % G;
         const uint32_t p = nn / 2;
         if constexpr (G >= 8) {
-            // Latency path: the group's lanes precompute the W+K schedules of
-            // the 8 data blocks in parallel (smem), then every lane runs only
-            // the rounds of the 9-block chain; the padding block's schedule is
-            // a compile-time constant. Bank layout: block stride 65 words,
-            // group stride 520 (= 8 mod 32) -> conflict-free.
             __shared__ uint32_t wk_sm[(kThreads / G) * 520];
-            uint32_t* wk = wk_sm + (threadIdx.x / G) * 520;
-            if (t < p) {
-                const uint8_t* a = nin + static_cast<uint64_t>(kNodeBytes) * (2 * t);
-#pragma unroll 1
-                for (uint32_t blk = lane; blk < 8; blk += G) {
-                    const uint4* q = reinterpret_cast<const uint4*>((blk < 4 ? a : a + kNodeBytes) + 64 * (blk & 3));
-                    uint32_t w[16];
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        uint4 v = q[k];
-                        w[4 * k] = bswap32(v.x);
-                        w[4 * k + 1] = bswap32(v.y);
-                        w[4 * k + 2] = bswap32(v.z);
-                        w[4 * k + 3] = bswap32(v.w);
-                    }
-                    sha256_schedule_wk(w, wk + 65 * blk);
-                }
-            }
-            __syncwarp();
-            if (t < p) {
-                uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
-                uint32_t d[8], seed[8];
-                sha256_init(d);
-                // compact (rolled) compressions: this chain runs once per
-                // launch, so its code size is I-cache-miss latency
-#pragma unroll 1
-                for (int blk = 0; blk < 8; ++blk) {
-                    const uint32_t* wb = wk + 65 * blk;
-                    sha256_rounds_c(d, [wb](int i) { return wb[i]; });
-                }
-                sha256_rounds_c(d, [](int i) { return kPadWk512.v[i]; });
-                expand_seed<true>(1, d, seed);
-#pragma unroll 1
-                for (uint32_t c = lane; c < 8; c += G) {
-                    uint32_t o[8];
-                    expand_block<true>(seed, c, o);
-                    store_digest(out + 32 * c, o);
-                }
-                if (lane == 0) write_node_tail(out, d, 1);
-            } else if (t == p && (nn & 1) && lane == 0) {
-                const uint4* s = reinterpret_cast<const uint4*>(nin + static_cast<uint64_t>(kNodeBytes) * (nn - 1));
-                uint4* dd = reinterpret_cast<uint4*>(nout + static_cast<uint64_t>(kNodeBytes) * p);
-#pragma unroll
-                for (int k = 0; k < kNodeBytes / 16; ++k) dd[k] = s[k];
-            }
+            pair8(nin, nn, nout, t, lane, wk_sm + (threadIdx.x / G) * 520);
             return;
         }
         if (t < p) {
@@ -284,18 +307,7 @@ __global__ void __launch_bounds__(kThreads) level_kernel(const uint8_t* __restri
         return;
     }
     const uint32_t u = (blockIdx.x - proof_blocks) * kThreads + threadIdx.x;
-    const uint32_t mp = (nm == 1 && !lift) ? 0 : (nm + 1) / 2;
-    if (u < mp) {
-        uint32_t l[8], r[8], h[8];
-        load_be8(min_ + 64ull * u, l);
-        if (2 * u + 1 < nm) load_be8(min_ + 64ull * u + 32, r);
-        else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) r[k] = l[k];  // duplicate last (wire.cpp:240)
-        }
-        merkle_inner(l, r, h);
-        store_digest(mout + 32ull * u, h);
-    }
+    merkle_pair(min_, nm, mout, u, lift);
 }
 
 __global__ void merkle_leaves_kernel(const uint8_t* leaves, uint32_t n, uint8_t* out) {
