@@ -19,6 +19,9 @@ namespace ace_gpu {
 namespace {
 
 constexpr int kThreads = 128;
+#ifndef ACEGPU_CHAIN_UNROLLED
+#define ACEGPU_CHAIN_UNROLLED 1
+#endif
 constexpr uint32_t kStageBytes = 192 * kThreads;  // payload staging per CTA (24 KB)
 
 // W+K schedule of the constant padding block of a 512-B message (aggregate_pair).
@@ -221,12 +224,16 @@ __device__ __forceinline__ void pair8(const uint8_t* __restrict__ nin, uint32_t 
         uint8_t* out = nout + static_cast<uint64_t>(kNodeBytes) * t;
         uint32_t d[8], seed[8];
         sha256_init(d);
-        // compact (rolled) compressions: this chain runs once per level, so
-        // its code size is I-cache-miss latency
+        // the 8 data blocks reuse one unrolled rounds body (I-cache warm after
+        // the first block); the single-use compressions below stay compact
 #pragma unroll 1
         for (int blk = 0; blk < 8; ++blk) {
             const uint32_t* wb = wk + 65 * blk;
+#if ACEGPU_CHAIN_UNROLLED
+            sha256_rounds(d, [wb](int i) { return wb[i]; });
+#else
             sha256_rounds_c(d, [wb](int i) { return wb[i]; });
+#endif
         }
         sha256_rounds_c(d, [](int i) { return kPadWk512.v[i]; });
         expand_seed<true>(1, d, seed);
