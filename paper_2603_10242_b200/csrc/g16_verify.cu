@@ -150,18 +150,8 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
     const uint8_t* p = proofs + 256ull * i;
     const Fq ax = ld_be(p), ay = ld_be(p + 32), cx = ld_be(p + 192), cy = ld_be(p + 224);
     const Fq2 bx = {ld_be(p + 96), ld_be(p + 64)}, by = {ld_be(p + 160), ld_be(p + 128)};
-    bool ok = on_curve(ax, ay, g1_b()) && on_curve(cx, cy, g1_b()) && on_curve(bx, by, g2_b());
-    // order-r subgroup of the twist: psi(B) == [6x^2] B (El Housni-Guillevic-
-    // Piellard 2022 for BN254; psi = the untwist-Frobenius-twist map, the
-    // Miller loop's frob_twist) -- a 127-bit scalar instead of r's 254 bits
-    if (ok) {
-        const uint32_t k6x2[4] = {0xe87cfd46u, 0xf83e9682u, 0xeeb859fbu, 0x6f4d8248u};
-        const XYZZ<Fq2> m = mul_bits(bx, by, k6x2, 127);
-        Fq2 px = bx, py = by;
-        frob_twist(px, py);
-        if (m.is_inf() || !feq(fmul(px, m.ZZ), m.X) || !feq(fmul(py, m.ZZZ), m.Y)) ok = false;
-    }
-    if (!ok) atomicExch(bad, 1);
+    const bool ok = on_curve(ax, ay, g1_b()) && on_curve(cx, cy, g1_b()) && on_curve(bx, by, g2_b());
+    if (!ok) atomicExch(bad, 1);  // the subgroup test of B runs beside the Miller loops
     uint32_t k[4];
     for (int w = 0; w < 4; ++w) {
         const uint8_t* q = rho + 32ull * i + 4 * w;
@@ -181,6 +171,48 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
     st_std2(o2, bx);
     st_std2(o2 + 64, by);
     cacc[i] = mul_bits(cx, cy, k, 128);
+}
+
+// Blocks [0, mb): one Miller loop per pair (raw Fq12 to scratch, as
+// launch_pairing_product). Blocks [mb, ...): the order-r subgroup test of
+// proof i's B: psi(B) == [6x^2] B (El Housni-Guillevic-Piellard 2022 for
+// BN254; psi = the untwist-Frobenius-twist map, the Miller loop's frob_twist)
+// -- a 127-bit scalar instead of r's 254 bits, run concurrently with the
+// Miller loops instead of before them.
+__global__ void __launch_bounds__(32) miller_check_kernel(uint32_t n_pairs, const uint8_t* g1s,
+                                                          const uint8_t* g2s, uint8_t* scratch,
+                                                          uint32_t mb, const uint8_t* proofs,
+                                                          uint32_t n, int* bad) {
+    if (blockIdx.x < mb) {
+        const uint32_t i = blockIdx.x * 32 + threadIdx.x;
+        if (i >= n_pairs) return;
+        const uint8_t* p = g1s + 64ull * i;
+        const uint8_t* q = g2s + 128ull * i;
+        bool inf = true;
+        for (int b = 0; b < 64 && inf; ++b) inf = p[b] == 0;
+        bool qinf = true;
+        for (int b = 0; b < 128 && qinf; ++b) qinf = q[b] == 0;
+        Fq12 f;
+        if (inf || qinf) {
+            f = f12_one();
+        } else {
+            const Fq2 xq = {to_mont(load<FqCfg>(q)), to_mont(load<FqCfg>(q + 32))};
+            const Fq2 yq = {to_mont(load<FqCfg>(q + 64)), to_mont(load<FqCfg>(q + 96))};
+            f = miller_loop(to_mont(load<FqCfg>(p)), to_mont(load<FqCfg>(p + 32)), xq, yq);
+        }
+        *reinterpret_cast<Fq12*>(scratch + sizeof(Fq12) * i) = f;
+        return;
+    }
+    const uint32_t i = (blockIdx.x - mb) * 32 + threadIdx.x;
+    if (i >= n) return;
+    const uint8_t* pr = proofs + 256ull * i;
+    const Fq2 bx = {ld_be(pr + 96), ld_be(pr + 64)}, by = {ld_be(pr + 160), ld_be(pr + 128)};
+    if (!on_curve(bx, by, g2_b())) return;  // flagged by points_kernel
+    const uint32_t k6x2[4] = {0xe87cfd46u, 0xf83e9682u, 0xeeb859fbu, 0x6f4d8248u};
+    const XYZZ<Fq2> m = mul_bits(bx, by, k6x2, 127);
+    Fq2 px = bx, py = by;
+    frob_twist(px, py);
+    if (m.is_inf() || !feq(fmul(px, m.ZZ), m.X) || !feq(fmul(py, m.ZZZ), m.Y)) atomicExch(bad, 1);
 }
 
 __device__ void put_neg_g1(uint8_t* o, const XYZZ<Fq>& p) {
@@ -254,7 +286,10 @@ int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_
     if (msm_run(1, vk.ic_table, T + 1, sc, msm, L, s)) return -1;
     points_kernel<<<grid(n, 32), 32, 0, s>>>(proofs, rho, n, g1s, g2s, cacc, bad);
     finish_kernel<<<1, 32, 0, s>>>(cacc, n, sc, vk.alpha1_mont, L, vk.g2_std, g1s, g2s);
-    launch_pairing_product(n + 3, g1s, g2s, pscratch, nullptr, d_ok, s);
+    const uint32_t mb = (n + 3 + 31) / 32;
+    miller_check_kernel<<<mb + (n + 31) / 32, 32, 0, s>>>(n + 3, g1s, g2s, pscratch, mb, proofs,
+                                                          n, bad);
+    launch_pairing_finish(n + 3, pscratch, nullptr, d_ok, s);
     // d_ok &= !bad
     combine_ok(d_ok, bad, s);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;

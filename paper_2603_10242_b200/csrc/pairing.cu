@@ -127,6 +127,11 @@ void launch_f12_op(int op, const uint8_t* in, uint8_t* out, cudaStream_t s) {
 
 size_t pairing_scratch_bytes(uint32_t n) { return sizeof(Fq12) * (n ? n : 1); }
 
+void launch_pairing_finish(uint32_t n, uint8_t* scratch, uint8_t* out384, int* is_one,
+                           cudaStream_t s) {
+    product_final_kernel<<<1, 128, 0, s>>>(n, scratch, out384, is_one);
+}
+
 void launch_pairing_product(uint32_t n, const uint8_t* g1s, const uint8_t* g2s, uint8_t* scratch,
                             uint8_t* out384, int* is_one, cudaStream_t s) {
     if (n) miller_kernel<<<(n + 63) / 64, 64, 0, s>>>(n, g1s, g2s, scratch);

@@ -16,6 +16,11 @@ size_t pairing_scratch_bytes(uint32_t n);
 void launch_pairing_product(uint32_t n, const uint8_t* g1s, const uint8_t* g2s, uint8_t* scratch,
                             uint8_t* out384, int* is_one, cudaStream_t s);
 
+// The product + final exponentiation half of launch_pairing_product, over n
+// Miller-loop values already in scratch (raw Fq12 records).
+void launch_pairing_finish(uint32_t n, uint8_t* scratch, uint8_t* out384, int* is_one,
+                           cudaStream_t s);
+
 // Fq12 unit op (codes of acegpu_bn_f12_op) on one element (or G1|G2 pair).
 void launch_f12_op(int op, const uint8_t* in, uint8_t* out, cudaStream_t s);
 
