@@ -108,14 +108,14 @@ __device__ __forceinline__ Fq6 f6_neg(const Fq6& a) { return {f2_neg(a.c0), f2_n
 __device__ __forceinline__ Fq6 f6_mul_v(const Fq6& a) { return {f2_mul_xi(a.c2), a.c0, a.c1}; }
 
 // Karatsuba-style (6 Fq2 products).
-static __device__ __noinline__ Fq6 f6_mul(const Fq6 a, const Fq6 b) {
+static __device__ __noinline__ Fq6 f6_mul(const Fq6& a, const Fq6& b) {
     const Fq2 t0 = fmul(a.c0, b.c0), t1 = fmul(a.c1, b.c1), t2 = fmul(a.c2, b.c2);
     const Fq2 c0 = fadd(t0, f2_mul_xi(fsub(fsub(fmul(fadd(a.c1, a.c2), fadd(b.c1, b.c2)), t1), t2)));
     const Fq2 c1 = fadd(fsub(fsub(fmul(fadd(a.c0, a.c1), fadd(b.c0, b.c1)), t0), t1), f2_mul_xi(t2));
     const Fq2 c2 = fadd(fsub(fsub(fmul(fadd(a.c0, a.c2), fadd(b.c0, b.c2)), t0), t2), t1);
     return {c0, c1, c2};
 }
-static __device__ __noinline__ Fq6 f6_inv(const Fq6 a) {
+static __device__ __noinline__ Fq6 f6_inv(const Fq6& a) {
     const Fq2 t0 = fsub(fsqr(a.c0), f2_mul_xi(fmul(a.c1, a.c2)));
     const Fq2 t1 = fsub(f2_mul_xi(fsqr(a.c2)), fmul(a.c0, a.c1));
     const Fq2 t2 = fsub(fsqr(a.c1), fmul(a.c0, a.c2));
@@ -135,13 +135,13 @@ __device__ __forceinline__ Fq12 f12_one() {
     fset_zero(r.c1.c2);
     return r;
 }
-static __device__ __noinline__ Fq12 f12_mul(const Fq12 a, const Fq12 b) {
+static __device__ __noinline__ Fq12 f12_mul(const Fq12& a, const Fq12& b) {
     const Fq6 t0 = f6_mul(a.c0, b.c0), t1 = f6_mul(a.c1, b.c1);
     const Fq6 c1 = f6_sub(f6_sub(f6_mul(f6_add(a.c0, a.c1), f6_add(b.c0, b.c1)), t0), t1);
     return {f6_add(t0, f6_mul_v(t1)), c1};
 }
 // (a0 + a1 w)^2 = a0^2 + a1^2 v + 2 a0 a1 w, via (a0 + a1)(a0 + a1 v).
-static __device__ __noinline__ Fq12 f12_sqr(const Fq12 a) {
+static __device__ __noinline__ Fq12 f12_sqr(const Fq12& a) {
     const Fq6 ab = f6_mul(a.c0, a.c1);
     const Fq6 t = f6_mul(f6_add(a.c0, a.c1), f6_add(a.c0, f6_mul_v(a.c1)));
     const Fq6 c0 = f6_sub(f6_sub(t, ab), f6_mul_v(ab));
@@ -150,15 +150,15 @@ static __device__ __noinline__ Fq12 f12_sqr(const Fq12 a) {
 __device__ __forceinline__ Fq12 f12_conj(const Fq12& a) { return {a.c0, f6_neg(a.c1)}; }
 
 // a * (b0 + b1 v): 5 Fq2 products (Karatsuba on the two non-zero terms).
-static __device__ __noinline__ Fq6 f6_mul_01(const Fq6 a, const Fq2 b0, const Fq2 b1) {
+static __device__ __noinline__ Fq6 f6_mul_01(const Fq6& a, const Fq2& b0, const Fq2& b1) {
     const Fq2 v0 = fmul(a.c0, b0), v1 = fmul(a.c1, b1);
     const Fq2 c1 = fsub(fsub(fmul(fadd(a.c0, a.c1), fadd(b0, b1)), v0), v1);
     return {fadd(v0, f2_mul_xi(fmul(a.c2, b1))), c1, fadd(v1, fmul(a.c2, b0))};
 }
 // f * line, line = l0 + (l1 + l2 v) w (the Miller-loop line shape): 13 Fq2
 // products instead of the dense 18.
-static __device__ __noinline__ Fq12 f12_mul_line(const Fq12 f, const Fq2 l0, const Fq2 l1,
-                                                 const Fq2 l2) {
+static __device__ __noinline__ Fq12 f12_mul_line(const Fq12& f, const Fq2& l0, const Fq2& l1,
+                                                 const Fq2& l2) {
     const Fq6 t0 = {fmul(f.c0.c0, l0), fmul(f.c0.c1, l0), fmul(f.c0.c2, l0)};
     const Fq6 t1 = f6_mul_01(f.c1, l1, l2);
     const Fq6 t2 = f6_mul_01(f6_add(f.c0, f.c1), fadd(l0, l1), l2);
@@ -167,7 +167,7 @@ static __device__ __noinline__ Fq12 f12_mul_line(const Fq12 f, const Fq2 l0, con
 // Squaring in the cyclotomic subgroup (Granger-Scott): the three Fq4
 // squarings (z0,z1) = (c0.c0, c1.c1), (z2,z3) = (c1.c0, c0.c2),
 // (z4,z5) = (c0.c1, c1.c2) over y^2 = xi; 6 Fq2 products instead of 12.
-static __device__ __noinline__ Fq12 f12_cyc_sqr(const Fq12 a) {
+static __device__ __noinline__ Fq12 f12_cyc_sqr(const Fq12& a) {
     auto fq4 = [](const Fq2& x, const Fq2& y, Fq2& s0, Fq2& s1) {  // (x + y t)^2, t^2 = xi
         const Fq2 xy = fmul(x, y);
         s0 = fsub(fsub(fmul(fadd(x, y), fadd(x, f2_mul_xi(y))), xy), f2_mul_xi(xy));
@@ -190,14 +190,14 @@ static __device__ __noinline__ Fq12 f12_cyc_sqr(const Fq12 a) {
     r.c1.c2 = tw(t3, a.c1.c2, true);
     return r;
 }
-static __device__ __noinline__ Fq12 f12_inv(const Fq12 a) {
+static __device__ __noinline__ Fq12 f12_inv(const Fq12& a) {
     const Fq6 d = f6_sub(f6_mul(a.c0, a.c0), f6_mul_v(f6_mul(a.c1, a.c1)));
     const Fq6 di = f6_inv(d);
     return {f6_mul(a.c0, di), f6_neg(f6_mul(a.c1, di))};
 }
 // Frobenius^k: coefficient of w^i -> conj^k(c_i) * gamma[k][i]; w^i order
 // (a0, b0, a1, b1, a2, b2) for a + b w, a = a0 + a1 v + a2 v^2.
-static __device__ __noinline__ Fq12 f12_frob(const Fq12 a, int k) {
+static __device__ __noinline__ Fq12 f12_frob(const Fq12& a, int k) {
     auto cj = [k](const Fq2& x) { return (k & 1) ? f2_conj(x) : x; };
     Fq12 r;
     r.c0.c0 = cj(a.c0.c0);
@@ -242,7 +242,7 @@ __device__ __forceinline__ Fq12 f12_mul_line(const Fq12& f, const Line& l) {
     return f12_mul_line(f, l.l0, l.l1, l.l2);
 }
 
-static __device__ __noinline__ Line dbl_step(G2Proj& T, const Fq xP, const Fq yP) {
+static __device__ __noinline__ Line dbl_step(G2Proj& T, const Fq& xP, const Fq& yP) {
     const Fq2 X2 = fsqr(T.X), Y2 = fsqr(T.Y);
     const Fq2 W = fadd(fadd(X2, X2), X2);
     const Fq2 S = fmul(T.Y, T.Z);
@@ -268,8 +268,8 @@ static __device__ __noinline__ Line dbl_step(G2Proj& T, const Fq xP, const Fq yP
     return make_line(cy, cx, c3, xP, yP);
 }
 
-static __device__ __noinline__ Line add_step(G2Proj& T, const Fq2 x2, const Fq2 y2, const Fq xP,
-                                            const Fq yP) {
+static __device__ __noinline__ Line add_step(G2Proj& T, const Fq2& x2, const Fq2& y2, const Fq& xP,
+                                            const Fq& yP) {
     const Fq2 N = fsub(fmul(y2, T.Z), T.Y);
     const Fq2 D = fsub(fmul(x2, T.Z), T.X);
     const Fq2 cy = D;
@@ -294,8 +294,8 @@ __device__ __forceinline__ void frob_twist(Fq2& x, Fq2& y) {
 }
 
 // f_{6x+2,Q}(P) * l_{T,pi(Q)}(P) * l_{T',-pi^2(Q)}(P); Q, P affine, not infinity.
-static __device__ __noinline__ Fq12 miller_loop(const Fq xP, const Fq yP, const Fq2 xQ,
-                                                const Fq2 yQ) {
+static __device__ __noinline__ Fq12 miller_loop(const Fq& xP, const Fq& yP, const Fq2& xQ,
+                                                const Fq2& yQ) {
     const uint64_t loop_lo = 0x9d797039be763ba8ull;  // 6x+2 = 2^64 + loop_lo
     Fq12 f = f12_one();
     G2Proj T;
@@ -317,7 +317,7 @@ static __device__ __noinline__ Fq12 miller_loop(const Fq xP, const Fq yP, const 
 }
 
 // Hard part ^((p^4 - p^2 + 1) / r) of an element of the cyclotomic subgroup.
-static __device__ __noinline__ Fq12 final_exp_hard(const Fq12 t1) {
+static __device__ __noinline__ Fq12 final_exp_hard(const Fq12& t1) {
     const Fq12 fp = f12_frob(t1, 1), fp2 = f12_frob(t1, 2), fp3 = f12_frob(fp2, 1);
     const Fq12 fu = f12_pow_x(t1), fu2 = f12_pow_x(fu), fu3 = f12_pow_x(fu2);
     Fq12 y3 = f12_frob(fu, 1);
@@ -339,7 +339,7 @@ static __device__ __noinline__ Fq12 final_exp_hard(const Fq12 t1) {
 }
 
 // f^((p^12 - 1) / r).
-static __device__ __noinline__ Fq12 final_exp(const Fq12 in) {
+static __device__ __noinline__ Fq12 final_exp(const Fq12& in) {
     Fq12 t1 = f12_mul(f12_conj(in), f12_inv(in));  // ^(p^6 - 1)
     t1 = f12_mul(t1, f12_frob(t1, 2));             // ^(p^2 + 1)
     return final_exp_hard(t1);
