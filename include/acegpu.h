@@ -129,6 +129,17 @@ int acegpu_attest_prove_certify_async(acegpu_ctx* ctx, void* stream, const uint8
                                       const uint8_t* header, const uint8_t* revs,
                                       uint64_t n_revs, const uint32_t* rev_index, uint8_t* codes,
                                       uint8_t* out289, uint8_t* out328);
+/* As acegpu_attest_prove_certify_async, replayed as a CUDA graph: the first
+ * block of a shape (n, payload bytes, REV count, stream, outputs) runs with
+ * plain launches and the same call is captured; later blocks of that shape
+ * re-point the graph's copy nodes at their host buffers and launch it (one
+ * graph launch instead of ~20 kernel launches + copies + events). `stream`
+ * must not be NULL. Same buffer rules as the async call. */
+int acegpu_attest_prove_certify_graph(acegpu_ctx* ctx, void* stream, const uint8_t* payloads,
+                                      const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                                      const uint8_t* header, const uint8_t* revs,
+                                      uint64_t n_revs, const uint32_t* rev_index, uint8_t* codes,
+                                      uint8_t* out289, uint8_t* out328);
 int acegpu_attest_prove_certify_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_payloads,
                                     const uint64_t* d_offs, const uint8_t* d_atts, uint64_t n,
                                     const uint8_t* d_header256, const uint8_t* d_revs,

@@ -51,6 +51,8 @@ _SIGS = {
                                                   vp, vp]),
     "acegpu_attest_prove_certify_async": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, vp, u64, vp,
                                                     vp, vp, vp]),
+    "acegpu_attest_prove_certify_graph": (C.c_int, [ctxp, vp, vp, vp, vp, u64, vp, vp, u64, vp,
+                                                    vp, vp, vp]),
     "acegpu_shard_roots_dev": (C.c_int, [ctxp, vp, vp, vp, vp, u64, u64, C.c_uint32, vp, u64, vp,
                                          vp, vp, vp]),
     "acegpu_combine_roots_dev": (C.c_int, [ctxp, vp, vp, vp, u64, u64, vp, vp, vp]),

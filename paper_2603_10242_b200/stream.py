@@ -52,13 +52,16 @@ class PipelinedProver:
     its previous block's results were collected (FIFO per lane)."""
 
     def __init__(self, lanes: int = 4, max_tx: int = 16384, max_payload: int | None = None,
-                 max_revs: int = 64, device: int | None = None):
+                 max_revs: int = 64, device: int | None = None, graphs: bool = True):
         dev = N.default_device() if device is None else device
         self.max_tx = max_tx
         self.max_payload = max_payload or 256 * max_tx
         self.max_revs = max_revs
         self.lanes = [_Lane(dev, max_tx, self.max_payload, max_revs) for _ in range(lanes)]
         self.next_ticket = 0
+        # CUDA-graph replay per lane for consecutive blocks of one shape
+        self.entry = ("acegpu_attest_prove_certify_graph" if graphs
+                      else "acegpu_attest_prove_certify_async")
         self.done: dict[int, StreamResult] = {}
 
     def _collect(self, lane: _Lane) -> None:
@@ -92,7 +95,7 @@ class PipelinedProver:
         lane.ev0.record(lane.stream)
         # one C-ABI call per block: H2D (pinned), attestation + proof + FC,
         # D2H of verdicts / proof / FC, all stream-ordered on the lane's stream
-        lane.ctx.call("acegpu_attest_prove_certify_async", lane.stream.cuda_stream,
+        lane.ctx.call(self.entry, lane.stream.cuda_stream,
                       pinned["payloads"].data_ptr(), pinned["offs"].data_ptr(),
                       pinned["atts"].data_ptr(), n, pinned["header"].data_ptr(),
                       pinned["revs"].data_ptr() if n else None, nr if n else 0,

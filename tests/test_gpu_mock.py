@@ -476,3 +476,26 @@ def test_rev_index_out_of_range_is_einval_after_the_run(P):
         assert (codes == 0).all()
         oproof, _, _ = O.oracle_prove_block(fb)
         assert proof == oproof
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_pipelined_prover_graph_replay(graphs):
+    """Consecutive same-shape blocks through the CUDA-graph replay path (and
+    the plain async path): each block's verdicts / proof / FC equal the
+    oracle's, i.e. the replayed copy nodes really read the new block."""
+    from paper_2603_10242_b200.stream import PipelinedProver
+    base = O.multi_user_block(1500, 4)
+    blocks = [O.forge(base, every=e, phase=p) for e, p in ((3, 0), (5, 1), (7, 2), (4, 3), (9, 4),
+                                                          (6, 5), (11, 0))]
+    pp = PipelinedProver(lanes=2, max_tx=2048, max_revs=8, graphs=graphs)
+    try:
+        tickets = [pp.submit(fb, fb.revs, fb.rev_index) for fb in blocks]
+        res = pp.drain()
+    finally:
+        pp.close()
+    assert [r.ticket for r in res] == tickets
+    for fb, r in zip(blocks, res):
+        assert (r.codes == O.oracle_attest_codes(fb)).all()
+        oproof, _, _ = O.oracle_prove_block(fb)
+        assert r.proof289 == oproof
+        assert r.fc328 == O.oracle_build_fc(fb, oproof)
