@@ -1344,7 +1344,7 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
         }
         mark(ls);
     }
-    for (int k = 0; k < kLeafStreams; ++k) {
+    for (int k = 0; k < int(std::min<uint64_t>(S, kLeafStreams)); ++k) {  // the streams used
         CK(cudaEventRecord(c->leaf_events[k], c->leaf_streams[k]));
         CK(cudaStreamWaitEvent(s, c->leaf_events[k], 0));
     }

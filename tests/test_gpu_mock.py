@@ -499,3 +499,22 @@ def test_pipelined_prover_graph_replay(graphs):
         oproof, _, _ = O.oracle_prove_block(fb)
         assert r.proof289 == oproof
         assert r.fc328 == O.oracle_build_fc(fb, oproof)
+
+
+def test_graph_replay_segmented_pipeline():
+    """Graph capture / replay of the segmented host pipeline (n >= 16,384:
+    copy stream, per-segment leaf + subtree streams, side stream)."""
+    from paper_2603_10242_b200.stream import PipelinedProver
+    base = O.multi_user_block(20000, 3)
+    blocks = [O.forge(base, every=e, phase=p) for e, p in ((3, 0), (5, 1), (7, 2))]
+    pp = PipelinedProver(lanes=1, max_tx=20000, max_revs=4, graphs=True)
+    try:
+        for fb in blocks:
+            pp.submit(fb, fb.revs, fb.rev_index)
+        res = pp.drain()
+    finally:
+        pp.close()
+    for fb, r in zip(blocks, res):
+        assert (r.codes == O.oracle_attest_codes(fb)).all()
+        oproof, _, _ = O.oracle_prove_block(fb)
+        assert r.fc328 == O.oracle_build_fc(fb, oproof)
