@@ -799,8 +799,31 @@ def cpu_baseline(args, n: int) -> dict | None:
                 cb = d["cpu_baseline"]
                 cb["ms_per_block"] = d["ms_per_step"]
                 cb["fc_matches_golden"] = d.get("parity", {}).get("fc_matches_golden")
+                cb["one_core"] = cpu_baseline_one_core(n)
                 return cb
     return {"unavailable": (r.stderr or "")[-300:]}
+
+
+def cpu_baseline_one_core(n: int) -> dict | None:
+    """SURVEY 8d: the same reference path pinned to ONE host core (taskset;
+    its ThreadPool still starts hardware_concurrency() threads, time-sliced on
+    that core), one timed block."""
+    import shutil
+    if not shutil.which("taskset"):
+        return None
+    try:
+        r = subprocess.run(["taskset", "-c", "0", sys.executable, os.path.abspath(__file__),
+                            "--impl", "reference", "--steps", "1", "--warmup", "0",
+                            "--n-tx", str(n)], capture_output=True, text=True, timeout=600)
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    for ln in r.stdout.splitlines():
+        if ln.startswith("{"):
+            d = json.loads(ln)
+            if "ms_per_step" in d:
+                return {"ms_per_block": d["ms_per_step"], "tx_per_s": d["value"], "cores": 1,
+                        "sample": "1 timed block, taskset -c 0"}
+    return None
 
 
 def bench_phase1a_and_verify(ctx, dev, fb, revs, rev_index, with_cpu: bool) -> dict:
