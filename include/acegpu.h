@@ -110,7 +110,10 @@ int acegpu_block_hash(acegpu_ctx* ctx, const uint8_t* header256, uint8_t* out32)
 /* The Phase-2 step (ProverService::run body, prover.cpp:350-351) with the
  * batched full attestation check fused in (crypto.cpp:141-154): per tx
  * verdict into codes (NULL = skip attestation), the block's root proof and
- * its finality certificate. Either output may be NULL. */
+ * its finality certificate. Either output may be NULL. With codes, the REV
+ * table (n_revs x 32 B) and the per-tx rev_index are required; an index
+ * >= n_revs is detected on the device and the call returns ACEGPU_EINVAL
+ * after the run (outputs undefined). */
 int acegpu_attest_prove_certify(acegpu_ctx* ctx, const uint8_t* payloads, const uint64_t* offs,
                                 const uint8_t* atts, uint64_t n, const uint8_t* header256,
                                 const uint8_t* revs, uint64_t n_revs, const uint32_t* rev_index,

@@ -203,7 +203,7 @@ int side_stream(acegpu_ctx* c) {
 int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint64_t* offs,
              const uint8_t* atts, uint32_t n, const uint8_t* header, const uint8_t* revs,
              const uint32_t* rev_index, uint8_t* codes, bool prove, uint32_t max_levels,
-             bool lift, TreeResult* r, bool skip_leaves = false) {
+             bool lift, TreeResult* r) {
     uint8_t *na = nullptr, *nb = nullptr, *ma = nullptr, *mb = nullptr, *bh = nullptr;
     const size_t half = n / 2 + 1;
     if (prove) {
@@ -218,15 +218,13 @@ int run_tree(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads, const uint6
     a.offs = offs;
     a.atts = atts;
     a.n = n;
-    a.revs = revs;
-    a.rev_index = rev_index;
     a.codes = codes;
     a.nodes = prove ? na : nullptr;
     a.merkle = ma;
     a.header = header;
     a.block_hash = bh;
     if (c->timing) CK(cudaEventRecord(c->ev[0], s));
-    if ((n || header) && !skip_leaves) {
+    if (n || header) {
         launch_leaves(a, s);
         CKL();
         c->launches++;
@@ -1314,8 +1312,6 @@ int overlapped_pipeline(acegpu_ctx* c, cudaStream_t s, const uint8_t* payloads,
         la.offs = offs + a;
         la.atts = atts + 104 * a;
         la.n = uint32_t(cnt);
-        la.revs = revs;
-        la.rev_index = rev_index ? rev_index + a : nullptr;
         la.codes = codes ? codes + a : nullptr;
         la.nodes = na + size_t(kNodeBytes) * a;
         la.merkle = ma + 32 * a;
@@ -1415,8 +1411,6 @@ int acegpu_attest_verify(acegpu_ctx* c, const uint8_t* payloads, const uint64_t*
     a.offs = doff;
     a.atts = da;
     a.n = uint32_t(n);
-    a.revs = dr;
-    a.rev_index = dri;
     a.codes = dc;
     launch_leaves(a, s);  // payload verdicts
     CKL();

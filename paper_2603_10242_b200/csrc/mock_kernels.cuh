@@ -16,8 +16,6 @@ struct LeafArgs {
     const uint64_t* offs;      // n+1 offsets into payloads
     const uint8_t* atts;       // n x 104 attestation records (8-B aligned)
     uint32_t n;
-    const uint8_t* revs;       // REV table (32 B each) — attestation only
-    const uint32_t* rev_index; // n entries — attestation only
     uint8_t* codes;            // n verdicts, or nullptr to skip attestation
     uint8_t* nodes;            // n x 320 leaf proof records, or nullptr (attest-only)
     uint8_t* merkle;           // n x 32 merkle leaf hashes H(0x00|id_com), or nullptr
