@@ -39,6 +39,9 @@ __device__ __forceinline__ Fq2 fneg(const Fq2& a) { return {neg(a.c0), neg(a.c1)
 #ifndef ACEGPU_G2_ACC_MINB
 #define ACEGPU_G2_ACC_MINB 1  // measured (paper-size chunk): 1 -> 60.1 ms, 3 -> 61.4, 4 -> 61.1
 #endif
+#ifndef ACEGPU_RED_SEG
+#define ACEGPU_RED_SEG 4
+#endif
 template <class F>
 struct Lay {
     static constexpr int EB = felem_bytes<F>();
@@ -265,7 +268,7 @@ __device__ __forceinline__ XYZZ<F> shfl_xyzz(const XYZZ<F>& a, int src_lane_delt
     return r;
 }
 
-constexpr int kRedSeg = 8;                           // buckets per reducing thread
+constexpr int kRedSeg = ACEGPU_RED_SEG;              // buckets per reducing thread
 constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // 4096
 
 // Segment j covers bucket indices [a, a+kRedSeg), weights a+1 .. a+kRedSeg:
@@ -273,26 +276,44 @@ constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // 4096
 template <class F>
 __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets, uint8_t* segsum) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= kRedThreads) return;
     constexpr int X = Lay<F>::XZ;
-    const int a = j * kRedSeg;
-    XYZZ<F> run = XYZZ<F>::inf(), tot = XYZZ<F>::inf();
-    for (int k = a + kRedSeg - 1; k >= a; --k) {
-        run = xyzz_add(run, load_xyzz<F>(buckets + (uint64_t)X * k));
-        tot = xyzz_add(tot, run);
+    XYZZ<F> tot = XYZZ<F>::inf();
+    if (j < kRedThreads) {
+        const int a = j * kRedSeg;
+        XYZZ<F> run = XYZZ<F>::inf();
+        for (int k = a + kRedSeg - 1; k >= a; --k) {
+            run = xyzz_add(run, load_xyzz<F>(buckets + (uint64_t)X * k));
+            tot = xyzz_add(tot, run);
+        }
+        if (a) tot = xyzz_add(tot, xyzz_mul_small(run, (uint32_t)a));
     }
-    if (a) tot = xyzz_add(tot, xyzz_mul_small(run, (uint32_t)a));
-    store_xyzz(segsum + (uint64_t)X * j, tot);
+    // one partial per CTA: warp shuffles, then the 4 warp sums
+    __shared__ __align__(16) uint8_t sm[4 * sizeof(XYZZ<F>)];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        XYZZ<F> o = shfl_xyzz(tot, d);
+        if (lane < d) tot = xyzz_add(tot, o);
+    }
+    if (lane == 0) store_xyzz(sm + X * warp, tot);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        XYZZ<F> r = load_xyzz<F>(sm);
+        for (int w = 1; w < 4; ++w) r = xyzz_add(r, load_xyzz<F>(sm + X * w));
+        store_xyzz(segsum + (uint64_t)X * blockIdx.x, r);
+    }
 }
 
 // Sum the kRedThreads segment sums in one CTA and write the affine result.
 template <class F>
-__global__ void __launch_bounds__(256) reduce_final_kernel(const uint8_t* segsum, uint8_t* out) {
+// Sum the per-CTA partials of reduce_seg (kRedThreads / 128 <= 64) and
+// write the affine result.
+__global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum, uint8_t* out) {
     constexpr int X = Lay<F>::XZ;
-    __shared__ __align__(16) uint8_t sm[8 * sizeof(XYZZ<F>)];
-    XYZZ<F> acc = XYZZ<F>::inf();
-    for (int j = threadIdx.x; j < kRedThreads; j += 256)
-        acc = xyzz_add(acc, load_xyzz<F>(segsum + (uint64_t)X * j));
+    constexpr int kParts = kRedThreads / 128;
+    __shared__ __align__(16) uint8_t sm[2 * sizeof(XYZZ<F>)];
+    XYZZ<F> acc = threadIdx.x < kParts ? load_xyzz<F>(segsum + (uint64_t)X * threadIdx.x)
+                                       : XYZZ<F>::inf();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
@@ -302,8 +323,7 @@ __global__ void __launch_bounds__(256) reduce_final_kernel(const uint8_t* segsum
     if (lane == 0) store_xyzz(sm + X * warp, acc);
     __syncthreads();
     if (threadIdx.x == 0) {
-        XYZZ<F> r = load_xyzz<F>(sm);
-        for (int w = 1; w < 8; ++w) r = xyzz_add(r, load_xyzz<F>(sm + X * w));
+        XYZZ<F> r = xyzz_add(load_xyzz<F>(sm), load_xyzz<F>(sm + X));
         F x, y;
         to_affine(r, x, y);
         store_affine(out, x, y);
@@ -350,7 +370,8 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
         table, sc.sorted, sc.offs, sc.coffs, sc.partials);
     bucket_sum_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.coffs, sc.partials, sc.buckets);
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
-    reduce_final_kernel<F><<<1, 256, 0, s>>>(sc.segsum, out);
+    static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
+    reduce_final_kernel<F><<<1, 64, 0, s>>>(sc.segsum, out);
     (void)X;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
