@@ -117,3 +117,16 @@ def test_light_check_rejects_null_codes(M):
         M.ctx.call("acegpu_light_check", M.N.addr(fb.payloads), M.N.addr(fb.offs),
                    M.N.addr(fb.atts), fb.n, None, 0, cur, 2, None, None)
     _ = C
+
+
+def test_phase1_does_no_proof_work(M):
+    """test_pipeline.cpp:169-190: Phase 1 (light check + block build) leaves
+    the prover's work counters unchanged."""
+    from paper_2603_10242_b200 import prover
+    fb, reg, cur = O.phase1_block(500, seed=9)
+    wc = prover.work_counters()
+    before = (wc.tx_proofs, wc.aggregations)
+    M.pl.attest_check_light_batch(wire_flat(M, fb), registry(M, reg), cur, ctx=M.ctx)
+    M.pl.build_block_device(wire_flat(M, fb), registry(M, reg),
+                            M.wire.BlockHeader(slot_number=cur), ctx=M.ctx)
+    assert (wc.tx_proofs, wc.aggregations) == before
