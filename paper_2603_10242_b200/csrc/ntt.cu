@@ -28,13 +28,46 @@ namespace {
 __device__ __forceinline__ Fr ld(const Fr* p) { return load<FrCfg>(p); }
 __device__ __forceinline__ void st(Fr* p, const Fr& x) { store<FrCfg>(p, x); }
 
+// Shared-memory sub-DFT arrays are planar: the low and high 16 B of element
+// i live at plane 0 / plane 1 index i, so a warp's 16-B accesses to
+// consecutive elements are contiguous (4 wavefronts, no bank conflicts)
+// instead of 32-B strided (8 wavefronts; ncu: 61 % of the shared wavefronts
+// were conflicts with the interleaved layout).
+#ifndef ACEGPU_NTT_PLANAR
+#define ACEGPU_NTT_PLANAR 1
+#endif
+struct SmemFr {
+    uint4* base;
+    uint32_t n;  // elements
+    __device__ __forceinline__ Fr get(uint32_t i) const {
+        if constexpr (ACEGPU_NTT_PLANAR) {
+            const uint4 lo = base[i], hi = base[n + i];
+            Fr r;
+            r.v[0] = lo.x; r.v[1] = lo.y; r.v[2] = lo.z; r.v[3] = lo.w;
+            r.v[4] = hi.x; r.v[5] = hi.y; r.v[6] = hi.z; r.v[7] = hi.w;
+            return r;
+        } else {
+            return ld(reinterpret_cast<const Fr*>(base) + i);
+        }
+    }
+    __device__ __forceinline__ void put(uint32_t i, const Fr& x) const {
+        if constexpr (ACEGPU_NTT_PLANAR) {
+            base[i] = make_uint4(x.v[0], x.v[1], x.v[2], x.v[3]);
+            base[n + i] = make_uint4(x.v[4], x.v[5], x.v[6], x.v[7]);
+        } else {
+            st(reinterpret_cast<Fr*>(base) + i, x);
+        }
+    }
+};
+
 __device__ __forceinline__ uint32_t bitrev(uint32_t x, int bits) {
     return __brev(x) >> (32 - bits);
 }
 
 // Shared-memory sub-DFT of size 2^m over R interleaved batches:
 // element (r, j) lives at s[j * R + r]. In: bit-reversed; out: natural.
-__device__ __forceinline__ void smem_dit(Fr* s, int m, int R, const Fr* __restrict__ w) {
+template <int R>  // compile-time: the index arithmetic divides by it
+__device__ __forceinline__ void smem_dit(const SmemFr& s, int m, const Fr* __restrict__ w) {
     const int half_n = 1 << (m - 1);
     const int total = half_n * R;
     for (int stage = 0; stage < m; ++stage) {
@@ -45,12 +78,11 @@ __device__ __forceinline__ void smem_dit(Fr* s, int m, int R, const Fr* __restri
             const int bf = b / R;
             const int j = bf & (half - 1);
             const int base = ((bf >> stage) << (stage + 1)) + j;
-            Fr* pu = &s[base * R + r];
-            Fr* pv = &s[(base + half) * R + r];
-            Fr u = ld(pu), v = ld(pv);
+            const uint32_t iu = base * R + r, iv = (base + half) * R + r;
+            Fr u = s.get(iu), v = s.get(iv);
             if (j) v = mul(v, ld(&w[j << tw_shift]));
-            st(pu, add(u, v));
-            st(pv, sub(u, v));
+            s.put(iu, add(u, v));
+            s.put(iv, sub(u, v));
         }
         __syncthreads();
     }
@@ -76,8 +108,9 @@ struct PassArgs {
 // Pass A: columns i1 in [cb*R, cb*R+R), DFT length n2 over i2.
 __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
-    Fr* s = reinterpret_cast<Fr*>(smem_raw);
-    const int n1 = 1 << a.L1, n2 = 1 << a.L2, R = a.R;
+    const int n1 = 1 << a.L1, n2 = 1 << a.L2;
+    constexpr int R = kNttR;
+    const SmemFr s{smem_raw, uint32_t(n2 * R)};
     const int i1_0 = blockIdx.x * R;
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
         const int r = e % R, i2 = e / R;
@@ -86,14 +119,14 @@ __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
         Fr x = load<FrCfg>(a.in + 32 * idx);
         if (a.pre_full) x = mul(x, ld(&a.pre_full[idx]));
         else if (a.pre_lo) x = mul(x, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[i2])));
-        st(&s[bitrev(i2, a.L2) * R + r], x);
+        s.put(bitrev(i2, a.L2) * R + r, x);
     }
     __syncthreads();
-    smem_dit(s, a.L2, R, a.w_sub);
+    smem_dit<R>(s, a.L2, a.w_sub);
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
         const int r = e % R, k2 = e / R;
         const int i1 = i1_0 + r;
-        Fr x = ld(&s[k2 * R + r]);
+        Fr x = s.get(k2 * R + r);
         // twiddle w^(i1*k2), exponent < n, split as lo (L2 bits) + hi
         const uint64_t ex = (uint64_t)i1 * k2;
         if (a.tw_full) {
@@ -109,20 +142,21 @@ __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
 // Pass C: rows k2 in [rb*R, rb*R+R), DFT length n1 over i1; natural output.
 __global__ void __launch_bounds__(512) ntt_pass_c(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
-    Fr* s = reinterpret_cast<Fr*>(smem_raw);
-    const int n1 = 1 << a.L1, n2 = 1 << a.L2, R = a.R;
+    const int n1 = 1 << a.L1, n2 = 1 << a.L2;
+    constexpr int R = kNttR;
+    const SmemFr s{smem_raw, uint32_t(n1 * R)};
     const int k2_0 = blockIdx.x * R;
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
         const int r = e % R, i1 = e / R;
         const uint64_t idx = i1 + (uint64_t)n1 * (k2_0 + r);
-        st(&s[bitrev(i1, a.L1) * R + r], load<FrCfg>(a.in + 32 * idx));
+        s.put(bitrev(i1, a.L1) * R + r, load<FrCfg>(a.in + 32 * idx));
     }
     __syncthreads();
-    smem_dit(s, a.L1, R, a.w_sub);
+    smem_dit<R>(s, a.L1, a.w_sub);
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
         const int r = e % R, k1 = e / R;
         const int k2 = k2_0 + r;
-        Fr x = ld(&s[k1 * R + r]);
+        Fr x = s.get(k1 * R + r);
         if (a.post_full) x = mul(x, ld(&a.post_full[k2 + (uint64_t)n2 * k1]));
         else if (a.post_lo) x = mul(x, mul(ld(&a.post_lo[k2]), ld(&a.post_hi[k1])));
         else if (a.scale) x = mul(x, ld(a.scale));
@@ -134,18 +168,18 @@ __global__ void __launch_bounds__(512) ntt_pass_c(PassArgs a) {
 // scale*g^-k (n) or uniform scale.
 __global__ void __launch_bounds__(512) ntt_single(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
-    Fr* s = reinterpret_cast<Fr*>(smem_raw);
     const int n = 1 << a.L;
+    const SmemFr s{smem_raw, uint32_t(n)};
     const uint64_t off = (uint64_t)blockIdx.x * n;  // batch of independent transforms
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         Fr x = load<FrCfg>(a.in + 32 * (off + i));
         if (a.pre_lo) x = mul(x, ld(&a.pre_lo[i]));
-        st(&s[a.L ? bitrev(i, a.L) : 0], x);
+        s.put(a.L ? bitrev(i, a.L) : 0, x);
     }
     __syncthreads();
-    if (a.L) smem_dit(s, a.L, 1, a.w_sub);
+    if (a.L) smem_dit<1>(s, a.L, a.w_sub);
     for (int k = threadIdx.x; k < n; k += blockDim.x) {
-        Fr x = ld(&s[k]);
+        Fr x = s.get(k);
         if (a.post_lo) x = mul(x, ld(&a.post_lo[k]));
         else if (a.scale) x = mul(x, ld(a.scale));
         store<FrCfg>(a.out + 32 * (off + k), x);
