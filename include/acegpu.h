@@ -238,6 +238,9 @@ int acegpu_bn_msm_prepare(acegpu_ctx* ctx, int group, const uint8_t* points, uin
 void acegpu_bn_msm_free(acegpu_msm_bases* bases);
 int acegpu_bn_msm_run(acegpu_ctx* ctx, const acegpu_msm_bases* bases, const uint8_t* scalars,
                       uint8_t* out_affine);
+/* The compiled window width c and window count ceil(255 / c) (each scalar
+ * contributes up to that many bucket entries). */
+int acegpu_bn_msm_params(acegpu_ctx* ctx, int* window_bits, int* windows);
 /* Device version: d_scalars standard form, d_out affine Montgomery form. */
 int acegpu_bn_msm_run_dev(acegpu_ctx* ctx, void* stream, const acegpu_msm_bases* bases,
                           const uint8_t* d_scalars, uint8_t* d_out);

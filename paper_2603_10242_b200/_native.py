@@ -70,6 +70,7 @@ _SIGS = {
     "acegpu_bn_ntt": (C.c_int, [ctxp, vp, C.c_uint32, C.c_int, C.c_int]),
     "acegpu_bn_ntt_dev": (C.c_int, [ctxp, vp, vp, vp, C.c_uint32, C.c_int, C.c_int]),
     "acegpu_bn_scalar_muls": (C.c_int, [ctxp, C.c_int, vp, vp, u64, vp]),
+    "acegpu_bn_msm_params": (C.c_int, [ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "acegpu_bn_msm_prepare": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, C.POINTER(C.c_void_p)]),
     "acegpu_bn_msm_free": (None, [C.c_void_p]),
     "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),

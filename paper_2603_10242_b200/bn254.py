@@ -104,6 +104,14 @@ class MsmBases:
             pass
 
 
+def msm_params(ctx=None) -> tuple[int, int]:
+    """(window bits c, windows per scalar) of the compiled Pippenger MSM."""
+    ctx = ctx or N.context()
+    c, w = C.c_int(), C.c_int()
+    ctx.call("acegpu_bn_msm_params", C.byref(c), C.byref(w))
+    return c.value, w.value
+
+
 def imad_peak(ctx=None) -> float:
     ctx = ctx or N.context()
     v = C.c_double()

@@ -1722,6 +1722,14 @@ extern "C" int acegpu_bn_scalar_muls(acegpu_ctx* c, int group, const uint8_t* ba
     return ACEGPU_OK;
 }
 
+extern "C" int acegpu_bn_msm_params(acegpu_ctx* c, int* window_bits, int* windows) {
+    if (!window_bits || !windows) return fail(ACEGPU_EINVAL, "null output");
+    (void)c;
+    *window_bits = bn::kMsmC;
+    *windows = bn::kMsmWindows;
+    return ACEGPU_OK;
+}
+
 extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* points,
                                      uint64_t n, int on_device, acegpu_msm_bases** out) {
     if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");

@@ -178,6 +178,182 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
 template <class C>
 __device__ __forceinline__ Fp<C> sqr(const Fp<C>& a) { return mul(a, a); }
 
+// ---- lazy reduction: 512-bit products, one Montgomery reduction per sum ----
+// A Montgomery product is half schoolbook product (128 IMAD) and half
+// reduction (136). Sums/differences of products (Karatsuba Fq2, x*y - z*w)
+// are formed on the 512-bit products and reduced once.
+
+// w = a * b (16 limbs). a, b < 2^256 (unreduced sums of two elements are fine).
+template <class C>
+__device__ __forceinline__ void mul_wide(const Fp<C>& a, const Fp<C>& b, uint32_t w[16]) {
+    uint32_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0, t7 = 0, t8 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t bi = b.v[i];
+        asm("mad.lo.cc.u32  %0, %9,  %17, %0;\n\t"
+            "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"
+            "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"
+            "madc.lo.cc.u32 %3, %12, %17, %3;\n\t"
+            "madc.lo.cc.u32 %4, %13, %17, %4;\n\t"
+            "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"
+            "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"
+            "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"
+            "addc.u32       %8, %8, 0;"
+            : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7),
+              "+r"(t8)
+            : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+              "r"(a.v[6]), "r"(a.v[7]), "r"(bi));
+        asm("mad.hi.cc.u32  %0, %8,  %16, %0;\n\t"
+            "madc.hi.cc.u32 %1, %9,  %16, %1;\n\t"
+            "madc.hi.cc.u32 %2, %10, %16, %2;\n\t"
+            "madc.hi.cc.u32 %3, %11, %16, %3;\n\t"
+            "madc.hi.cc.u32 %4, %12, %16, %4;\n\t"
+            "madc.hi.cc.u32 %5, %13, %16, %5;\n\t"
+            "madc.hi.cc.u32 %6, %14, %16, %6;\n\t"
+            "madc.hi.u32    %7, %15, %16, %7;"
+            : "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7), "+r"(t8)
+            : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+              "r"(a.v[6]), "r"(a.v[7]), "r"(bi));
+        w[i] = t0;  // final: later rows start one limb higher
+        t0 = t1; t1 = t2; t2 = t3; t3 = t4; t4 = t5; t5 = t6; t6 = t7; t7 = t8; t8 = 0;
+    }
+    w[8] = t0; w[9] = t1; w[10] = t2; w[11] = t3;
+    w[12] = t4; w[13] = t5; w[14] = t6; w[15] = t7;
+}
+
+// w -= x (16 limbs); returns the borrow mask (0xffffffff when w < x).
+__device__ __forceinline__ uint32_t sub_wide(uint32_t w[16], const uint32_t x[16]) {
+    uint32_t br;
+    asm("sub.cc.u32  %0, %0, %17;\n\t"
+        "subc.cc.u32 %1, %1, %18;\n\t"
+        "subc.cc.u32 %2, %2, %19;\n\t"
+        "subc.cc.u32 %3, %3, %20;\n\t"
+        "subc.cc.u32 %4, %4, %21;\n\t"
+        "subc.cc.u32 %5, %5, %22;\n\t"
+        "subc.cc.u32 %6, %6, %23;\n\t"
+        "subc.cc.u32 %7, %7, %24;\n\t"
+        "subc.cc.u32 %8, %8, %25;\n\t"
+        "subc.cc.u32 %9, %9, %26;\n\t"
+        "subc.cc.u32 %10, %10, %27;\n\t"
+        "subc.cc.u32 %11, %11, %28;\n\t"
+        "subc.cc.u32 %12, %12, %29;\n\t"
+        "subc.cc.u32 %13, %13, %30;\n\t"
+        "subc.cc.u32 %14, %14, %31;\n\t"
+        "subc.cc.u32 %15, %15, %32;\n\t"
+        "subc.u32    %16, 0, 0;"
+        : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]), "+r"(w[4]), "+r"(w[5]), "+r"(w[6]),
+          "+r"(w[7]), "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]),
+          "+r"(w[13]), "+r"(w[14]), "+r"(w[15]), "=r"(br)
+        : "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]),
+          "r"(x[7]), "r"(x[8]), "r"(x[9]), "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]),
+          "r"(x[14]), "r"(x[15]));
+    return br;
+}
+
+// w += m * 2^256 where mask is all-ones (mod 2^512): brings a negative
+// difference of two products back into [0, m * 2^256).
+template <class C>
+__device__ __forceinline__ void add_mR_masked(uint32_t w[16], uint32_t mask) {
+    asm("add.cc.u32  %0, %0, %8;\n\t"
+        "addc.cc.u32 %1, %1, %9;\n\t"
+        "addc.cc.u32 %2, %2, %10;\n\t"
+        "addc.cc.u32 %3, %3, %11;\n\t"
+        "addc.cc.u32 %4, %4, %12;\n\t"
+        "addc.cc.u32 %5, %5, %13;\n\t"
+        "addc.cc.u32 %6, %6, %14;\n\t"
+        "addc.u32    %7, %7, %15;"
+        : "+r"(w[8]), "+r"(w[9]), "+r"(w[10]), "+r"(w[11]), "+r"(w[12]), "+r"(w[13]),
+          "+r"(w[14]), "+r"(w[15])
+        : "r"(C::M[0] & mask), "r"(C::M[1] & mask), "r"(C::M[2] & mask), "r"(C::M[3] & mask),
+          "r"(C::M[4] & mask), "r"(C::M[5] & mask), "r"(C::M[6] & mask), "r"(C::M[7] & mask));
+}
+
+// Montgomery reduction of a 512-bit w < m * 2^256: returns w * 2^-256 mod m,
+// fully reduced. Reduces the low half (u = (w_lo + q m) / 2^256 <= m), then
+// u + w_hi < 2m takes one conditional subtraction.
+template <class C>
+__device__ __forceinline__ Fp<C> redc_wide(const uint32_t w[16]) {
+    uint32_t t0 = w[0], t1 = w[1], t2 = w[2], t3 = w[3], t4 = w[4], t5 = w[5], t6 = w[6],
+             t7 = w[7], t8 = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const uint32_t m = t0 * C::N0;
+        asm("mad.lo.cc.u32  %0, %9,  %10, %0;\n\t"
+            "madc.lo.cc.u32 %1, %9,  %11, %1;\n\t"
+            "madc.lo.cc.u32 %2, %9,  %12, %2;\n\t"
+            "madc.lo.cc.u32 %3, %9,  %13, %3;\n\t"
+            "madc.lo.cc.u32 %4, %9,  %14, %4;\n\t"
+            "madc.lo.cc.u32 %5, %9,  %15, %5;\n\t"
+            "madc.lo.cc.u32 %6, %9,  %16, %6;\n\t"
+            "madc.lo.cc.u32 %7, %9,  %17, %7;\n\t"
+            "addc.u32       %8, %8, 0;"
+            : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7),
+              "+r"(t8)
+            : "r"(m), "n"(C::M[0]), "n"(C::M[1]), "n"(C::M[2]), "n"(C::M[3]), "n"(C::M[4]),
+              "n"(C::M[5]), "n"(C::M[6]), "n"(C::M[7]));
+        asm("mad.hi.cc.u32  %0, %8,  %9,  %0;\n\t"
+            "madc.hi.cc.u32 %1, %8,  %10, %1;\n\t"
+            "madc.hi.cc.u32 %2, %8,  %11, %2;\n\t"
+            "madc.hi.cc.u32 %3, %8,  %12, %3;\n\t"
+            "madc.hi.cc.u32 %4, %8,  %13, %4;\n\t"
+            "madc.hi.cc.u32 %5, %8,  %14, %5;\n\t"
+            "madc.hi.cc.u32 %6, %8,  %15, %6;\n\t"
+            "madc.hi.u32    %7, %8,  %16, %7;"
+            : "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7), "+r"(t8)
+            : "r"(m), "n"(C::M[0]), "n"(C::M[1]), "n"(C::M[2]), "n"(C::M[3]), "n"(C::M[4]),
+              "n"(C::M[5]), "n"(C::M[6]), "n"(C::M[7]));
+        t0 = t1; t1 = t2; t2 = t3; t3 = t4; t4 = t5; t5 = t6; t6 = t7; t7 = t8; t8 = 0;
+    }
+    uint32_t t[9];
+    asm("add.cc.u32  %0, %9,  %17;\n\t"
+        "addc.cc.u32 %1, %10, %18;\n\t"
+        "addc.cc.u32 %2, %11, %19;\n\t"
+        "addc.cc.u32 %3, %12, %20;\n\t"
+        "addc.cc.u32 %4, %13, %21;\n\t"
+        "addc.cc.u32 %5, %14, %22;\n\t"
+        "addc.cc.u32 %6, %15, %23;\n\t"
+        "addc.cc.u32 %7, %16, %24;\n\t"
+        "addc.u32    %8, 0, 0;"
+        : "=r"(t[0]), "=r"(t[1]), "=r"(t[2]), "=r"(t[3]), "=r"(t[4]), "=r"(t[5]), "=r"(t[6]),
+          "=r"(t[7]), "=r"(t[8])
+        : "r"(t0), "r"(t1), "r"(t2), "r"(t3), "r"(t4), "r"(t5), "r"(t6), "r"(t7), "r"(w[8]),
+          "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15]));
+    Fp<C> r;
+    final_sub<C>(t, r.v);
+    return r;
+}
+
+// a + b without reduction (a, b < m < 2^254: the sum fits 8 limbs).
+template <class C>
+__device__ __forceinline__ Fp<C> add_raw(const Fp<C>& a, const Fp<C>& b) {
+    Fp<C> r;
+    asm("add.cc.u32  %0, %8,  %16;\n\t"
+        "addc.cc.u32 %1, %9,  %17;\n\t"
+        "addc.cc.u32 %2, %10, %18;\n\t"
+        "addc.cc.u32 %3, %11, %19;\n\t"
+        "addc.cc.u32 %4, %12, %20;\n\t"
+        "addc.cc.u32 %5, %13, %21;\n\t"
+        "addc.cc.u32 %6, %14, %22;\n\t"
+        "addc.u32    %7, %15, %23;"
+        : "=r"(r.v[0]), "=r"(r.v[1]), "=r"(r.v[2]), "=r"(r.v[3]), "=r"(r.v[4]), "=r"(r.v[5]),
+          "=r"(r.v[6]), "=r"(r.v[7])
+        : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
+          "r"(a.v[6]), "r"(a.v[7]), "r"(b.v[0]), "r"(b.v[1]), "r"(b.v[2]), "r"(b.v[3]),
+          "r"(b.v[4]), "r"(b.v[5]), "r"(b.v[6]), "r"(b.v[7]));
+    return r;
+}
+
+// a * b - c * d (a..d reduced): two products, one reduction.
+template <class C>
+__device__ __forceinline__ Fp<C> mul_sub_mul(const Fp<C>& a, const Fp<C>& b, const Fp<C>& c,
+                                             const Fp<C>& d) {
+    uint32_t w[16], x[16];
+    mul_wide(a, b, w);
+    mul_wide(c, d, x);
+    add_mR_masked<C>(w, sub_wide(w, x));  // (-m^2, m^2) -> [0, m * 2^256)
+    return redc_wide<C>(w);
+}
+
 template <class C>
 __device__ __forceinline__ Fp<C> add(const Fp<C>& a, const Fp<C>& b) {
     uint32_t t[9];

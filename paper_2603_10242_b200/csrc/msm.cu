@@ -2,22 +2,27 @@
 // (north-star row a21: K8/K9 of SURVEY §2b; the reference has none).
 //
 // Fixed-base form: the proving key's bases are fixed, so `msm_prepare`
-// stores table[w][i] = 2^(16 w) P_i once (affine). A run then needs no
-// doublings between windows: every (window, point) pair with a non-zero
-// signed 16-bit digit d lands in one of 2^15 buckets |d| of a single bucket
-// set, and the result is sum_k k * B_k.
+// stores table[w][i] = 2^(c w) P_i once (affine, c = kMsmC = 17 -> 15
+// windows). A run then needs no doublings between windows: every
+// (window, point) pair with a non-zero signed c-bit digit d lands in one of
+// 2^(c-1) buckets |d| of a single bucket set, and the result is
+// sum_k k * B_k.
 //
-//   1. count    : signed digits of each scalar -> bucket histogram (atomics)
-//   2. scan     : exclusive prefix sum -> bucket offsets
-//   3. scatter  : (window*n + i | sign) into bucket order
-//   4. accumulate: each thread adds kMsmSeg sorted entries (mixed XYZZ adds,
-//                 8M + 2S each), finished buckets written directly, the
-//                 first/last (split) buckets of a segment as partials
-//   5. fixup    : one warp per split bucket sums its partials (shuffles)
-//   6. reduce   : sum_k k*B_k by per-segment running sums + small scalar
-//                 multiples, then a block reduction, then affine.
+//   1. count     : signed digits of each scalar -> bucket histogram (atomics)
+//   2. scan      : exclusive prefix sum -> bucket offsets
+//   3. scatter   : (window*n + i | sign) into bucket order
+//   4. accumulate: each thread mixed-adds kMsmSeg consecutive sorted entries
+//                  (XYZZ, 8M + 2S, lazy-reduced Y); a bucket wholly inside
+//                  the segment is written directly, the first/last runs that
+//                  cross a segment edge go to two partial slots
+//   5. fixup     : one thread per bucket crossing segments sums its partials
+//                  (and writes infinity for empty buckets)
+//   6. reduce    : sum_k k*B_k by per-segment running sums + small scalar
+//                  multiples, per-CTA trees, then one CTA and affine.
 // Bound: IMAD pipe (Fq mul = CIOS carry chains). Work ~ (W*n) mixed adds.
 #include <cuda_runtime.h>
+
+#include <cub/device/device_scan.cuh>
 
 #include "curve.cuh"
 #include "msm.cuh"
@@ -38,9 +43,6 @@ __device__ __forceinline__ Fq2 fneg(const Fq2& a) { return {neg(a.c0), neg(a.c1)
 
 #ifndef ACEGPU_G2_ACC_MINB
 #define ACEGPU_G2_ACC_MINB 1  // measured (paper-size chunk): 1 -> 60.1 ms, 3 -> 61.4, 4 -> 61.1
-#endif
-#ifndef ACEGPU_RED_SEG
-#define ACEGPU_RED_SEG 4
 #endif
 template <class F>
 struct Lay {
@@ -98,7 +100,7 @@ __device__ __forceinline__ void to_affine(const XYZZ<F>& a, F& x, F& y) {
     y = fmul(a.Y, fmul(t, a.ZZ));   // Y / ZZZ
 }
 
-// ---- prepare: table[w*n + i] = 2^(16w) P_i ----------------------------------
+// ---- prepare: table[w*n + i] = 2^(c w) P_i ----------------------------------
 template <class F>
 __global__ void prepare_kernel(const uint8_t* bases, uint64_t n, uint8_t* table) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -121,20 +123,26 @@ __global__ void prepare_kernel(const uint8_t* bases, uint64_t n, uint8_t* table)
     }
 }
 
-// Signed base-2^16 digits of a canonical scalar < r < 2^254 (16 windows).
-__device__ __forceinline__ void digits16(const uint8_t* s, int32_t d[kMsmWindows]) {
+// Signed base-2^c digits of a canonical scalar < r < 2^254: window w reads
+// bits [c w, c w + c) (a 64-bit window over two limbs); raw values above
+// 2^(c-1) become raw - 2^c with a carry into the next window. The top window
+// holds < 2^(254 - c (W-1)) <= 2^(c-1), so no carry leaves it.
+__device__ __forceinline__ void digits(const uint8_t* s, int32_t d[kMsmWindows]) {
     const uint4* q = reinterpret_cast<const uint4*>(s);
     uint4 a = q[0], b = q[1];
-    const uint32_t limb[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const uint32_t limb[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, 0u};
     uint32_t carry = 0;
 #pragma unroll
     for (int w = 0; w < kMsmWindows; ++w) {
-        uint32_t raw = ((limb[w >> 1] >> (16 * (w & 1))) & 0xFFFFu) + carry;
-        if (raw > (1u << (kMsmC - 1))) {
-            d[w] = (int32_t)raw - (1 << kMsmC);
+        const int bit = w * kMsmC, lo = bit >> 5, sh = bit & 31;
+        const uint64_t v = ((uint64_t)limb[lo + 1] << 32) | limb[lo];
+        const uint32_t raw = (uint32_t)(v >> sh) & ((1u << kMsmC) - 1u);
+        const uint32_t t = raw + carry;
+        if (t > (1u << (kMsmC - 1))) {
+            d[w] = (int32_t)t - (1 << kMsmC);
             carry = 1;
         } else {
-            d[w] = (int32_t)raw;
+            d[w] = (int32_t)t;
             carry = 0;
         }
     }
@@ -144,51 +152,10 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t d[kMsmWindows];
-    digits16(scalars + 32 * i, d);
+    digits(scalars + 32 * i, d);
 #pragma unroll
     for (int w = 0; w < kMsmWindows; ++w)
         if (d[w]) atomicAdd(&hist[abs(d[w]) - 1], 1u);
-}
-
-// Exclusive scans (one CTA of 1024 threads) of the bucket sizes -> entry
-// offsets, and of the per-bucket chunk counts ceil(size / kMsmSeg) -> chunk
-// offsets. Chunks never straddle buckets.
-__global__ void __launch_bounds__(1024) scan_kernel(const uint32_t* hist, uint32_t* offs,
-                                                    uint32_t* cursor, uint32_t* coffs) {
-    __shared__ uint32_t part[1024], cpart[1024];
-    constexpr int per = kMsmBuckets / 1024;
-    const int t = threadIdx.x;
-    uint32_t loc[per], cloc[per], sum = 0, csum = 0;
-#pragma unroll
-    for (int k = 0; k < per; ++k) {
-        const uint32_t h = hist[t * per + k];
-        loc[k] = sum;
-        cloc[k] = csum;
-        sum += h;
-        csum += (h + kMsmSeg - 1) / kMsmSeg;
-    }
-    part[t] = sum;
-    cpart[t] = csum;
-    __syncthreads();
-    for (int off = 1; off < 1024; off <<= 1) {
-        uint32_t v = t >= off ? part[t - off] : 0;
-        uint32_t cv = t >= off ? cpart[t - off] : 0;
-        __syncthreads();
-        part[t] += v;
-        cpart[t] += cv;
-        __syncthreads();
-    }
-    const uint32_t base = t ? part[t - 1] : 0, cbase = t ? cpart[t - 1] : 0;
-#pragma unroll
-    for (int k = 0; k < per; ++k) {
-        offs[t * per + k] = base + loc[k];
-        cursor[t * per + k] = base + loc[k];
-        coffs[t * per + k] = cbase + cloc[k];
-    }
-    if (t == 1023) {
-        offs[kMsmBuckets] = part[1023];
-        coffs[kMsmBuckets] = cpart[1023];
-    }
 }
 
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
@@ -196,7 +163,7 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t d[kMsmWindows];
-    digits16(scalars + 32 * i, d);
+    digits(scalars + 32 * i, d);
 #pragma unroll
     for (int w = 0; w < kMsmWindows; ++w) {
         if (!d[w]) continue;
@@ -205,8 +172,9 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
     }
 }
 
+// The non-empty bucket b with offs[b] <= pos < offs[b + 1].
 __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
-    int lo = 0, hi = kMsmBuckets;  // offs[lo] <= pos < offs[hi]
+    int lo = 0, hi = kMsmBuckets;
     while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
         if (offs[mid] <= pos) lo = mid;
@@ -215,20 +183,30 @@ __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
     return lo;
 }
 
-// One thread per chunk (<= kMsmSeg entries of one bucket): mixed-add the
-// chunk's bases into one XYZZ partial.
+template <class F>
+__device__ __forceinline__ void store_inf(uint8_t* p) {
+    store_xyzz(p, XYZZ<F>::inf());
+}
+
+// One thread per segment of kMsmSeg consecutive sorted entries. Runs of one
+// bucket: a run that is the whole bucket is stored to buckets[b]; a run cut
+// by the segment edge is stored to partials[2 seg] (first run of the
+// segment) or partials[2 seg + 1] (a later run).
 template <class F>
 __global__ void __launch_bounds__(128, Lay<F>::ACC_MIN_CTAS) accumulate_kernel(const uint8_t* table,
                                                          const uint32_t* sorted,
                                                          const uint32_t* offs,
-                                                         const uint32_t* coffs,
+                                                         uint8_t* buckets,
                                                          uint8_t* partials) {
-    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= coffs[kMsmBuckets]) return;
+    const uint32_t seg = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t total = offs[kMsmBuckets];
+    const uint32_t p0 = seg * kMsmSeg;
+    if (p0 >= total) return;
     constexpr int A = Lay<F>::AFF, X = Lay<F>::XZ;
-    const int b = bucket_of(coffs, c);
-    const uint32_t p0 = offs[b] + (c - coffs[b]) * kMsmSeg;
-    const uint32_t p1 = min(offs[b + 1], p0 + kMsmSeg);
+    const uint32_t p1 = min(total, p0 + kMsmSeg);
+    int b = bucket_of(offs, p0);
+    uint32_t bs = offs[b], be = offs[b + 1];
+    int slot = 0;
     XYZZ<F> acc = XYZZ<F>::inf();
     uint32_t v = sorted[p0];
     for (uint32_t pos = p0; pos < p1; ++pos) {
@@ -239,22 +217,20 @@ __global__ void __launch_bounds__(128, Lay<F>::ACC_MIN_CTAS) accumulate_kernel(c
             acc = xyzz_madd<F>(acc, x, y);  // out-of-line Fq products (inlining measured slower)
         }
         v = nv;
+        if (pos + 1 == be || pos + 1 == p1) {  // the run of bucket b ends here
+            if (bs >= p0 && be <= p1) store_xyzz(buckets + (uint64_t)X * b, acc);
+            else store_xyzz(partials + (uint64_t)X * (2ull * seg + slot), acc);
+            slot = 1;
+            acc = XYZZ<F>::inf();
+            if (pos + 1 < p1) {
+                do {  // next non-empty bucket
+                    ++b;
+                    bs = be;
+                    be = offs[b + 1];
+                } while (be == bs);
+            }
+        }
     }
-    store_xyzz(partials + (uint64_t)X * c, acc);
-}
-
-// One thread per bucket: sum its chunk partials (infinity when empty).
-template <class F>
-__global__ void __launch_bounds__(128) bucket_sum_kernel(const uint32_t* coffs,
-                                                         const uint8_t* partials,
-                                                         uint8_t* buckets) {
-    const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= kMsmBuckets) return;
-    constexpr int X = Lay<F>::XZ;
-    XYZZ<F> acc = XYZZ<F>::inf();
-    for (uint32_t c = coffs[b]; c < coffs[b + 1]; ++c)
-        acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * c));
-    store_xyzz(buckets + (uint64_t)X * b, acc);
 }
 
 template <class F>
@@ -268,11 +244,82 @@ __device__ __forceinline__ XYZZ<F> shfl_xyzz(const XYZZ<F>& a, int src_lane_delt
     return r;
 }
 
-constexpr int kRedSeg = ACEGPU_RED_SEG;              // buckets per reducing thread
-constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // 4096
+// Sum of a 128-thread CTA's values (result valid in thread 0).
+template <class F>
+__device__ __forceinline__ XYZZ<F> cta_sum128(XYZZ<F> v) {
+    __shared__ __align__(16) uint8_t sm[4 * sizeof(XYZZ<F>)];
+    constexpr int X = Lay<F>::XZ;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        XYZZ<F> o = shfl_xyzz(v, d);
+        if (lane < d) v = xyzz_add(v, o);
+    }
+    if (lane == 0) store_xyzz(sm + X * warp, v);
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int w = 1; w < 4; ++w) v = xyzz_add(v, load_xyzz<F>(sm + X * w));
+    return v;
+}
+
+constexpr uint32_t kHeavySpan = 64;  // segments; longer buckets go to heavy_kernel
+
+// One thread per bucket: empty -> infinity; a bucket spanning segments
+// s0 < s1 sums its run partials (slot 0 or 1 in s0, slot 0 after). Buckets
+// spanning more than kHeavySpan segments (skewed digits, e.g. a witness of
+// 0/1 values) are queued for heavy_kernel instead of one serial thread.
+template <class F>
+__global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const uint8_t* partials,
+                                                    uint8_t* buckets, uint32_t* heavy) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kMsmBuckets) return;
+    constexpr int X = Lay<F>::XZ;
+    const uint32_t s = offs[b], e = offs[b + 1];
+    if (s == e) {
+        store_inf<F>(buckets + (uint64_t)X * b);
+        return;
+    }
+    const uint32_t s0 = s / kMsmSeg, s1 = (e - 1) / kMsmSeg;
+    if (s0 == s1) return;
+    if (s1 - s0 > kHeavySpan) {
+        heavy[1 + atomicAdd(&heavy[0], 1u)] = b;
+        return;
+    }
+    XYZZ<F> acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * kMsmSeg ? 0 : 1)));
+    for (uint32_t sg = s0 + 1; sg <= s1; ++sg)
+        acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg)));
+    store_xyzz(buckets + (uint64_t)X * b, acc);
+}
+
+// One CTA per queued heavy bucket (grid-stride): threads stride over its
+// segment partials, then a CTA tree.
+template <class F>
+__global__ void __launch_bounds__(128) heavy_kernel(const uint32_t* offs, const uint8_t* partials,
+                                                    uint8_t* buckets, const uint32_t* heavy) {
+    constexpr int X = Lay<F>::XZ;
+    const uint32_t nh = heavy[0];
+    for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int b = heavy[1 + h];
+        const uint32_t s = offs[b], e = offs[b + 1];
+        const uint32_t s0 = s / kMsmSeg, s1 = (e - 1) / kMsmSeg;
+        XYZZ<F> acc = XYZZ<F>::inf();
+        if (threadIdx.x == 0)
+            acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * kMsmSeg ? 0 : 1)));
+        for (uint32_t sg = s0 + 1 + threadIdx.x; sg <= s1; sg += blockDim.x)
+            acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg)));
+        acc = cta_sum128(acc);
+        if (threadIdx.x == 0) store_xyzz(buckets + (uint64_t)X * b, acc);
+        __syncthreads();
+    }
+}
+
+constexpr int kRedSeg = kMsmBuckets / 8192 > 4 ? kMsmBuckets / 8192 : 4;  // buckets per thread
+constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // <= 8192 -> <= 64 CTA partials
 
 // Segment j covers bucket indices [a, a+kRedSeg), weights a+1 .. a+kRedSeg:
-// sum = tot + a*run with running sums from the top.
+// sum = tot + a*run with running sums from the top; one partial per CTA.
+// (A work-efficient multi-level recursion on the run_j measured 2.7x slower
+// here: every level pays a serial chain of point additions.)
 template <class F>
 __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets, uint8_t* segsum) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -287,27 +334,13 @@ __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets,
         }
         if (a) tot = xyzz_add(tot, xyzz_mul_small(run, (uint32_t)a));
     }
-    // one partial per CTA: warp shuffles, then the 4 warp sums
-    __shared__ __align__(16) uint8_t sm[4 * sizeof(XYZZ<F>)];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int d = 16; d >= 1; d >>= 1) {
-        XYZZ<F> o = shfl_xyzz(tot, d);
-        if (lane < d) tot = xyzz_add(tot, o);
-    }
-    if (lane == 0) store_xyzz(sm + X * warp, tot);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        XYZZ<F> r = load_xyzz<F>(sm);
-        for (int w = 1; w < 4; ++w) r = xyzz_add(r, load_xyzz<F>(sm + X * w));
-        store_xyzz(segsum + (uint64_t)X * blockIdx.x, r);
-    }
+    tot = cta_sum128(tot);
+    if (threadIdx.x == 0) store_xyzz(segsum + (uint64_t)X * blockIdx.x, tot);
 }
 
-// Sum the kRedThreads segment sums in one CTA and write the affine result.
-template <class F>
 // Sum the per-CTA partials of reduce_seg (kRedThreads / 128 <= 64) and
 // write the affine result.
+template <class F>
 __global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum, uint8_t* out) {
     constexpr int X = Lay<F>::XZ;
     constexpr int kParts = kRedThreads / 128;
@@ -348,27 +381,34 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
           cudaStream_t s) {
     constexpr int X = Lay<F>::XZ;
     const uint64_t cap = (uint64_t)kMsmWindows * n;
+    const uint64_t nseg = (cap + kMsmSeg - 1) / kMsmSeg;
     if (sc.cap_entries < cap || !sc.hist) {
         sc.release();
-        const uint64_t chunks = (cap + kMsmSeg - 1) / kMsmSeg + kMsmBuckets;
         if (cudaMalloc(&sc.hist, 4 * (kMsmBuckets + 1)) || cudaMalloc(&sc.offs, 4 * (kMsmBuckets + 1)) ||
-            cudaMalloc(&sc.coffs, 4 * (kMsmBuckets + 1)) ||
             cudaMalloc(&sc.cursor, 4 * kMsmBuckets) || cudaMalloc(&sc.sorted, 4 * cap) ||
-            cudaMalloc(&sc.partials, (size_t)256 * chunks) ||
+            cudaMalloc(&sc.partials, (size_t)256 * 2 * nseg) ||
             cudaMalloc(&sc.buckets, (size_t)256 * kMsmBuckets) ||
-            cudaMalloc(&sc.segsum, (size_t)256 * kRedThreads))
+            cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128)) ||
+            cudaMalloc(&sc.heavy, 4 * (kMsmBuckets + 1)))
             return -1;
+        cub::DeviceScan::ExclusiveSum(nullptr, sc.scan_bytes, sc.hist, sc.offs, kMsmBuckets + 1, s);
+        if (cudaMalloc(&sc.scan_tmp, sc.scan_bytes)) return -1;
         sc.cap_entries = cap;
     }
     cudaMemsetAsync(sc.hist, 0, 4 * (kMsmBuckets + 1), s);
+    cudaMemsetAsync(sc.heavy, 0, 4, s);
     const unsigned gb = (unsigned)((n + 255) / 256);
     count_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.hist);
-    scan_kernel<<<1, 1024, 0, s>>>(sc.hist, sc.offs, sc.cursor, sc.coffs);
+    // offs = exclusive scan of hist[0..NB] (hist[NB] = 0 -> offs[NB] = total)
+    if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, sc.scan_bytes, sc.hist, sc.offs,
+                                      kMsmBuckets + 1, s) != cudaSuccess)
+        return -1;
+    cudaMemcpyAsync(sc.cursor, sc.offs, 4 * kMsmBuckets, cudaMemcpyDeviceToDevice, s);
     scatter_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
-    const uint64_t chunks = (cap + kMsmSeg - 1) / kMsmSeg + kMsmBuckets;  // upper bound
-    accumulate_kernel<F><<<(unsigned)((chunks + 127) / 128), 128, 0, s>>>(
-        table, sc.sorted, sc.offs, sc.coffs, sc.partials);
-    bucket_sum_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.coffs, sc.partials, sc.buckets);
+    accumulate_kernel<F><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
+        table, sc.sorted, sc.offs, sc.buckets, sc.partials);
+    fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
+    heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
     static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
     reduce_final_kernel<F><<<1, 64, 0, s>>>(sc.segsum, out);
@@ -379,12 +419,13 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 }  // namespace
 
 void MsmScratch::release() {
-    void* ps[] = {hist, offs, coffs, cursor, sorted, partials, buckets, segsum};
-    coffs = nullptr;
+    void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum, scan_tmp, heavy};
     for (void* p : ps)
         if (p) cudaFree(p);
-    hist = offs = cursor = sorted = nullptr;
+    hist = offs = cursor = sorted = heavy = nullptr;
     partials = buckets = segsum = nullptr;
+    scan_tmp = nullptr;
+    scan_bytes = 0;
     cap_entries = 0;
 }
 

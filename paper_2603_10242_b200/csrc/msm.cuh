@@ -7,28 +7,34 @@
 namespace ace_gpu {
 namespace bn {
 
-constexpr int kMsmC = 16;                      // window bits
-constexpr int kMsmWindows = 16;                // ceil(254 / 16), signed digits need no 17th
-constexpr int kMsmBuckets = 1 << (kMsmC - 1);  // |digit| in 1..2^15
-constexpr int kMsmSeg = 64;                    // max entries per chunk (one accumulating thread)
+#ifndef ACEGPU_MSM_C
+#define ACEGPU_MSM_C 17  // 15 windows x 17 = 255 bits exactly; c = 16/18/20 measured
+#endif
+constexpr int kMsmC = ACEGPU_MSM_C;                   // window bits
+constexpr int kMsmWindows = (255 + kMsmC - 1) / kMsmC;  // 254-bit scalars + the signed-digit carry
+constexpr int kMsmBuckets = 1 << (kMsmC - 1);         // |digit| in 1..2^(c-1)
+constexpr int kMsmSeg = 64;                           // sorted entries per accumulating thread
+static_assert(kMsmC >= 12 && kMsmC <= 24, "window bits");
 
 // Device scratch for one MSM size (grow-only, reused).
 struct MsmScratch {
     uint32_t* hist = nullptr;      // kMsmBuckets + 1
     uint32_t* offs = nullptr;      // kMsmBuckets + 1
-    uint32_t* coffs = nullptr;     // kMsmBuckets + 1 chunk offsets
     uint32_t* cursor = nullptr;    // kMsmBuckets
     uint32_t* sorted = nullptr;    // W * n entries
-    uint8_t* partials = nullptr;   // 2 per segment, XYZZ records
+    uint8_t* partials = nullptr;   // 2 per accumulation segment, XYZZ records
     uint8_t* buckets = nullptr;    // kMsmBuckets XYZZ
-    uint8_t* segsum = nullptr;     // reduction partials
+    uint8_t* segsum = nullptr;     // reduction partials (one per CTA)
+    uint32_t* heavy = nullptr;     // [count, bucket ids] of buckets spanning many segments
+    void* scan_tmp = nullptr;      // CUB scan temporary storage
+    size_t scan_bytes = 0;
     size_t cap_entries = 0;
     void release();
 };
 
 // group = 1 (G1, 64-B affine / 128-B XYZZ) or 2 (G2, 128-B affine / 256-B XYZZ).
 // Bases: affine, Montgomery form, infinity = all-zero record.
-// prepare: table[w*n + i] = 2^(16 w) * base[i] for w < 16 (affine, Montgomery).
+// prepare: table[w*n + i] = 2^(c w) * base[i] for w < kMsmWindows (affine, Montgomery).
 int msm_prepare(int group, const uint8_t* bases, uint64_t n, uint8_t* table, cudaStream_t s);
 // scalars: n x 32-B canonical little-endian (standard form). out: affine,
 // Montgomery form (64 / 128 B).

@@ -176,7 +176,8 @@ def test_msm_degenerate_scalars(ctx):
     ctx.call("acegpu_bn_scalar_muls", 1, G, arr(ks), n, pts)
     pts[64 * 5:64 * 6] = 0  # infinity base
     for sc, label in [([1] * n, "ones"), ([0] * n, "zeros"), ([R - 1] * n, "minus ones"),
-                      ([(1 << 16) + 3] * n, "two windows")]:
+                      ([(1 << 16) + 3] * n, "two windows"), ([(1 << 17) + 5] * n, "c=17 edge"),
+                      ([i & 1 for i in range(n)], "0/1 witness")]:
         got = msm_gpu(ctx, 1, pts, arr(sc), n)
         e = sum(s * (k if i != 5 else 0) for i, (s, k) in enumerate(zip(sc, ks))) % R
         dl = O.buf(64)
