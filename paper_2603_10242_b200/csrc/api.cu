@@ -1777,7 +1777,7 @@ extern "C" int acegpu_bn_msm_run_dev(acegpu_ctx* c, void* stream, const acegpu_m
     cudaStream_t s = pick(c, stream);
     if (bn::msm_run(b->group, b->table, b->n, d_scalars, c->msm, d_out, s))
         return fail(ACEGPU_ECUDA, std::string("msm_run: ") + cudaGetErrorString(cudaGetLastError()));
-    c->launches += 7;
+    c->launches += bn::kMsmKernels;
     return ACEGPU_OK;
 }
 
@@ -1869,6 +1869,7 @@ struct acegpu_g16 {
     // own MSM scratch, so one MSM's latency-bound sort/reduction phases
     // overlap another's throughput-bound bucket accumulation
     cudaStream_t s_bl = nullptr, s_h = nullptr;
+    cudaStream_t s_ab = nullptr;  // highest priority: A, B1 finish first so s*A, r*B1 overlap
     cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
     bn::MsmScratch msm_bl, msm_h;
 };
@@ -1927,7 +1928,7 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     if (g->side) cudaStreamDestroy(g->side);
     if (g->ev_ab) cudaEventDestroy(g->ev_ab);
     if (g->ev_scaled) cudaEventDestroy(g->ev_scaled);
-    for (cudaStream_t t : {g->s_bl, g->s_h})
+    for (cudaStream_t t : {g->s_bl, g->s_h, g->s_ab})
         if (t) cudaStreamDestroy(t);
     for (cudaEvent_t e : {g->ev_z, g->ev_bl, g->ev_h})
         if (e) cudaEventDestroy(e);
@@ -1972,6 +1973,11 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&g->s_bl, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&g->s_h, cudaStreamNonBlocking));
+    {
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        CK(cudaStreamCreateWithPriority(&g->s_ab, cudaStreamNonBlocking, greatest));
+    }
     for (cudaEvent_t* e : {&g->ev_z, &g->ev_bl, &g->ev_h})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // constants
@@ -2066,12 +2072,40 @@ extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g1
 }
 
 namespace {
+// ACEGPU_G16_TRACE=1: per-stream stage completion times of one chunk proof
+// (events, printed to stderr after a synchronize) — a timeline without nsys.
+struct G16Trace {
+    bool on = std::getenv("ACEGPU_G16_TRACE") != nullptr;
+    cudaEvent_t ev[16] = {};
+    const char* name[16] = {};
+    int n = 0;
+    void mark(const char* what, cudaStream_t st) {
+        if (!on || n >= 16) return;
+        if (!ev[n]) cudaEventCreate(&ev[n]);
+        name[n] = what;
+        cudaEventRecord(ev[n++], st);
+    }
+    void dump() {
+        if (!on || !n) return;
+        cudaEventSynchronize(ev[n - 1]);
+        cudaDeviceSynchronize();
+        for (int i = 1; i < n; ++i) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[0], ev[i]);
+            std::fprintf(stderr, "[g16] %-10s %8.3f ms\n", name[i], ms);
+        }
+        n = 0;
+    }
+};
+G16Trace g_g16_trace;
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32) {
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     uint8_t* scratch;
     RET(ws(c, kBnScratch, 32 * N, &scratch));
+    G16Trace& tr = g_g16_trace;
+    tr.mark("start", s);
     for (uint8_t* e : {g->ea, g->eb, g->ec})
         if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), s));
     bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, s);
@@ -2084,6 +2118,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, s);
     CKL();
     CK(cudaEventRecord(g->ev_z, s));
+    tr.mark("witness", s);
     // s_h: H(x) = (a b - c) / Z on the coset, back to coefficients, then [h]
     const bn::NttTables& t = c->ntt[g->logn];
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
@@ -2096,28 +2131,39 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sh);
     if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, sh)) return fail(ACEGPU_ECUDA, "g16 coset intt");
     bn::launch_fr_convert(g->ea, N, 0, sh);  // h coefficients -> standard form scalars
+    tr.mark("ntt", sh);
     CKL();
     if (bn::msm_run(1, g->qh->table, N - 1, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
+    tr.mark("msm_h", sh);
     // s_bl: [v]2 (B2) and [l] (L)
     CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
     if (bn::msm_run(2, g->qb2->table, V + 2, g->zb, g->msm_bl, g->pts + 128, g->s_bl) ||
+        (tr.mark("msm_b2", g->s_bl), false) ||
         bn::msm_run(1, g->ql->table, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
         return fail(ACEGPU_ECUDA, "g16 msm B2/L");
     CK(cudaEventRecord(g->ev_bl, g->s_bl));
-    // s: A and B1, then s*A and r*B1 on the side stream
-    if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, s) ||
-        bn::msm_run(1, g->qb1->table, V + 2, g->zb, c->msm, g->pts + 64, s))
+    tr.mark("msm_l", g->s_bl);
+    // s_ab (high priority): A and B1, then s*A and r*B1 (one serial
+    // scalar multiplication each) on the side stream while the others finish
+    CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
+    if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, g->s_ab) ||
+        (tr.mark("msm_a", g->s_ab), false) ||
+        bn::msm_run(1, g->qb1->table, V + 2, g->zb, c->msm, g->pts + 64, g->s_ab))
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
-    CK(cudaEventRecord(g->ev_ab, s));
+    CK(cudaEventRecord(g->ev_ab, g->s_ab));
+    tr.mark("msm_b1", g->s_ab);
     CK(cudaStreamWaitEvent(g->side, g->ev_ab, 0));
     bn::g16_scale(g->pts, g->rs, g->scaled, g->side);
     CK(cudaEventRecord(g->ev_scaled, g->side));
+    tr.mark("scale", g->side);
     for (cudaEvent_t e : {g->ev_scaled, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
     bn::g16_assemble(g->pts, g->scaled, d_proof256, d_raw256, s);
     CKL();
-    c->launches += 16 + 5 * 7 + 6;
+    tr.mark("assemble", s);
+    tr.dump();
+    c->launches += 17 + 5 * bn::kMsmKernels + 6;
     return ACEGPU_OK;
 }
 }  // namespace
@@ -2295,7 +2341,7 @@ int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_
     if (bn::g16_verify_batch(vk, d_proofs, d_pubs, uint32_t(n), scratch, c->msm, d_ok, s))
         return fail(ACEGPU_ECUDA, "g16 verify launch");
     CKL();
-    c->launches += 10;
+    c->launches += 3 + bn::kMsmKernels;
     return ACEGPU_OK;
 }
 }  // namespace

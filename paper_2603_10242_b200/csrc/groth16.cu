@@ -238,16 +238,22 @@ __global__ void witness_kernel(G16Dims d, const uint8_t* w_in, const uint8_t* pu
     str(ea + 32 * R, x);
     str(eb + 32 * R, one);
     str(ec + 32 * R, x);
-    str(z + 32 * (vb + 1), from_mont(x));
-    for (uint32_t k = 1; k < d.K; ++k) {
+    for (uint32_t k = 1; k < d.K; ++k) {  // the serial chain; z_{t,k} = c_{t,k} follow in parallel
         const Fr y = add(x, ldr(cc + 32ull * k));
         const Fr y2 = sqr(y);
         str(ea + 32 * (R + k), y);
         str(eb + 32 * (R + k), y);
         str(ec + 32 * (R + k), y2);
-        str(z + 32 * (vb + 1 + k), from_mont(y2));
         x = y2;
     }
+}
+
+// z_{t,k} (standard form) = c row t*K + k (Montgomery): x_{t,0} = x, x_{t,k} = y_k^2.
+__global__ void witness_z_kernel(G16Dims d, const uint8_t* ec, uint8_t* z) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= (uint64_t)d.T * d.K) return;
+    const uint64_t t = j / d.K, k = j - t * d.K;
+    str(z + 32 * (1 + d.T + t * (d.K + 1) + 1 + k), from_mont(ldr(ec + 32 * j)));
 }
 
 // h_j = (a_j b_j - c_j) / (g^N - 1) on the coset (Montgomery, in place into ea).
@@ -433,7 +439,8 @@ void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s) {
 }
 void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const uint8_t* cc,
                  uint8_t* z, uint8_t* ea, uint8_t* eb, uint8_t* ec, cudaStream_t s) {
-    witness_kernel<<<grid(d.T, 64), 64, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+    witness_kernel<<<grid(d.T, 32), 32, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+    witness_z_kernel<<<grid((uint64_t)d.T * d.K, 256), 256, 0, s>>>(d, ec, z);
 }
 void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint8_t* c,
                    uint64_t n, cudaStream_t s) {
