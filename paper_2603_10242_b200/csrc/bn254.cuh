@@ -175,9 +175,6 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
     return r;
 }
 
-template <class C>
-__device__ __forceinline__ Fp<C> sqr(const Fp<C>& a) { return mul(a, a); }
-
 // ---- lazy reduction: 512-bit products, one Montgomery reduction per sum ----
 // A Montgomery product is half schoolbook product (128 IMAD) and half
 // reduction (136). Sums/differences of products (Karatsuba Fq2, x*y - z*w)
@@ -220,6 +217,128 @@ __device__ __forceinline__ void mul_wide(const Fp<C>& a, const Fp<C>& b, uint32_
     w[8] = t0; w[9] = t1; w[10] = t2; w[11] = t3;
     w[12] = t4; w[13] = t5; w[14] = t6; w[15] = t7;
 }
+
+// w = a^2 (16 limbs): 28 off-diagonal products (lo + hi), doubled by a
+// funnel shift, plus the 8 diagonal squares: 72 IMAD instead of 128.
+template <class C>
+__device__ __forceinline__ void sqr_wide(const Fp<C>& x, uint32_t t[16]) {
+    const uint32_t* a = x.v;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) t[k] = 0;
+    asm("mad.lo.cc.u32  %0, %8, %9, %0;\n\t"
+        "madc.lo.cc.u32 %1, %8, %10, %1;\n\t"
+        "madc.lo.cc.u32 %2, %8, %11, %2;\n\t"
+        "madc.lo.cc.u32 %3, %8, %12, %3;\n\t"
+        "madc.lo.cc.u32 %4, %8, %13, %4;\n\t"
+        "madc.lo.cc.u32 %5, %8, %14, %5;\n\t"
+        "madc.lo.cc.u32 %6, %8, %15, %6;\n\t"
+        "addc.u32       %7, %7, 0;"
+        : "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %7, %8, %0;\n\t"
+        "madc.hi.cc.u32 %1, %7, %9, %1;\n\t"
+        "madc.hi.cc.u32 %2, %7, %10, %2;\n\t"
+        "madc.hi.cc.u32 %3, %7, %11, %3;\n\t"
+        "madc.hi.cc.u32 %4, %7, %12, %4;\n\t"
+        "madc.hi.cc.u32 %5, %7, %13, %5;\n\t"
+        "madc.hi.u32    %6, %7, %14, %6;"
+        : "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %7, %8, %0;\n\t"
+        "madc.lo.cc.u32 %1, %7, %9, %1;\n\t"
+        "madc.lo.cc.u32 %2, %7, %10, %2;\n\t"
+        "madc.lo.cc.u32 %3, %7, %11, %3;\n\t"
+        "madc.lo.cc.u32 %4, %7, %12, %4;\n\t"
+        "madc.lo.cc.u32 %5, %7, %13, %5;\n\t"
+        "addc.u32       %6, %6, 0;"
+        : "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %6, %7, %0;\n\t"
+        "madc.hi.cc.u32 %1, %6, %8, %1;\n\t"
+        "madc.hi.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.hi.cc.u32 %3, %6, %10, %3;\n\t"
+        "madc.hi.cc.u32 %4, %6, %11, %4;\n\t"
+        "madc.hi.u32    %5, %6, %12, %5;"
+        : "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9])
+        : "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %6, %7, %0;\n\t"
+        "madc.lo.cc.u32 %1, %6, %8, %1;\n\t"
+        "madc.lo.cc.u32 %2, %6, %9, %2;\n\t"
+        "madc.lo.cc.u32 %3, %6, %10, %3;\n\t"
+        "madc.lo.cc.u32 %4, %6, %11, %4;\n\t"
+        "addc.u32       %5, %5, 0;"
+        : "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9]), "+r"(t[10])
+        : "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %5, %6, %0;\n\t"
+        "madc.hi.cc.u32 %1, %5, %7, %1;\n\t"
+        "madc.hi.cc.u32 %2, %5, %8, %2;\n\t"
+        "madc.hi.cc.u32 %3, %5, %9, %3;\n\t"
+        "madc.hi.u32    %4, %5, %10, %4;"
+        : "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9]), "+r"(t[10])
+        : "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %5, %6, %0;\n\t"
+        "madc.lo.cc.u32 %1, %5, %7, %1;\n\t"
+        "madc.lo.cc.u32 %2, %5, %8, %2;\n\t"
+        "madc.lo.cc.u32 %3, %5, %9, %3;\n\t"
+        "addc.u32       %4, %4, 0;"
+        : "+r"(t[7]), "+r"(t[8]), "+r"(t[9]), "+r"(t[10]), "+r"(t[11])
+        : "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %4, %5, %0;\n\t"
+        "madc.hi.cc.u32 %1, %4, %6, %1;\n\t"
+        "madc.hi.cc.u32 %2, %4, %7, %2;\n\t"
+        "madc.hi.u32    %3, %4, %8, %3;"
+        : "+r"(t[8]), "+r"(t[9]), "+r"(t[10]), "+r"(t[11])
+        : "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %4, %5, %0;\n\t"
+        "madc.lo.cc.u32 %1, %4, %6, %1;\n\t"
+        "madc.lo.cc.u32 %2, %4, %7, %2;\n\t"
+        "addc.u32       %3, %3, 0;"
+        : "+r"(t[9]), "+r"(t[10]), "+r"(t[11]), "+r"(t[12])
+        : "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %3, %4, %0;\n\t"
+        "madc.hi.cc.u32 %1, %3, %5, %1;\n\t"
+        "madc.hi.u32    %2, %3, %6, %2;"
+        : "+r"(t[10]), "+r"(t[11]), "+r"(t[12])
+        : "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %3, %4, %0;\n\t"
+        "madc.lo.cc.u32 %1, %3, %5, %1;\n\t"
+        "addc.u32       %2, %2, 0;"
+        : "+r"(t[11]), "+r"(t[12]), "+r"(t[13])
+        : "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.cc.u32  %0, %2, %3, %0;\n\t"
+        "madc.hi.u32    %1, %2, %4, %1;"
+        : "+r"(t[12]), "+r"(t[13])
+        : "r"(a[5]), "r"(a[6]), "r"(a[7]));
+    asm("mad.lo.cc.u32  %0, %2, %3, %0;\n\t"
+        "addc.u32       %1, %1, 0;"
+        : "+r"(t[13]), "+r"(t[14])
+        : "r"(a[6]), "r"(a[7]));
+    asm("mad.hi.u32     %0, %1, %2, %0;"
+        : "+r"(t[14])
+        : "r"(a[6]), "r"(a[7]));
+#pragma unroll
+    for (int k = 15; k > 0; --k) t[k] = __funnelshift_l(t[k - 1], t[k], 1);
+    t[0] <<= 1;
+    asm("mad.lo.cc.u32  %0, %16, %16, %0;\n\t"
+        "madc.hi.cc.u32 %1, %16, %16, %1;\n\t"
+        "madc.lo.cc.u32 %2, %17, %17, %2;\n\t"
+        "madc.hi.cc.u32 %3, %17, %17, %3;\n\t"
+        "madc.lo.cc.u32 %4, %18, %18, %4;\n\t"
+        "madc.hi.cc.u32 %5, %18, %18, %5;\n\t"
+        "madc.lo.cc.u32 %6, %19, %19, %6;\n\t"
+        "madc.hi.cc.u32 %7, %19, %19, %7;\n\t"
+        "madc.lo.cc.u32 %8, %20, %20, %8;\n\t"
+        "madc.hi.cc.u32 %9, %20, %20, %9;\n\t"
+        "madc.lo.cc.u32 %10, %21, %21, %10;\n\t"
+        "madc.hi.cc.u32 %11, %21, %21, %11;\n\t"
+        "madc.lo.cc.u32 %12, %22, %22, %12;\n\t"
+        "madc.hi.cc.u32 %13, %22, %22, %13;\n\t"
+        "madc.lo.cc.u32 %14, %23, %23, %14;\n\t"
+        "madc.hi.u32    %15, %23, %23, %15;"
+        : "+r"(t[0]), "+r"(t[1]), "+r"(t[2]), "+r"(t[3]), "+r"(t[4]), "+r"(t[5]), "+r"(t[6]), "+r"(t[7]), "+r"(t[8]), "+r"(t[9]), "+r"(t[10]), "+r"(t[11]), "+r"(t[12]), "+r"(t[13]), "+r"(t[14]), "+r"(t[15])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]));
+}
+
 
 // w -= x (16 limbs); returns the borrow mask (0xffffffff when w < x).
 __device__ __forceinline__ uint32_t sub_wide(uint32_t w[16], const uint32_t x[16]) {
@@ -321,6 +440,14 @@ __device__ __forceinline__ Fp<C> redc_wide(const uint32_t w[16]) {
     Fp<C> r;
     final_sub<C>(t, r.v);
     return r;
+}
+
+// Montgomery squaring: sqr_wide + one reduction (208 IMAD vs 264).
+template <class C>
+__device__ __forceinline__ Fp<C> sqr(const Fp<C>& a) {
+    uint32_t w[16];
+    sqr_wide(a, w);
+    return redc_wide<C>(w);
 }
 
 // a + b without reduction (a, b < m < 2^254: the sum fits 8 limbs).
