@@ -18,7 +18,40 @@ struct Fq2 {
 // dozen times per point operation, so it is an out-of-line call here
 // (inlined, a bucket kernel's body exceeded 1 MB of code and thrashed the
 // instruction caches; see profiles/). NTT kernels keep the inline `mul`.
+#ifndef ACEGPU_FQ2_SHARED
+#define ACEGPU_FQ2_SHARED 1  // Fq2 units call one shared 512-bit product / reduction body
+#endif
+struct W16 {
+    uint32_t v[16];
+};
+#if ACEGPU_FQ2_SHARED
+// The G2 bucket loop was instruction-fetch bound with the products inlined
+// into each Fq2 unit (ncu: stalled_no_instruction ~1 per issue); one
+// out-of-line body each keeps the loop's code small.
+static __device__ __noinline__ W16 fq_mul_wide_call(const Fq a, const Fq b) {
+    W16 w;
+    mul_wide(a, b, w.v);
+    return w;
+}
+static __device__ __noinline__ Fq fq_redc_call(const W16 w) { return redc_wide<FqCfg>(w.v); }
+#else
+__device__ __forceinline__ W16 fq_mul_wide_call(const Fq& a, const Fq& b) {
+    W16 w;
+    mul_wide(a, b, w.v);
+    return w;
+}
+__device__ __forceinline__ Fq fq_redc_call(const W16& w) { return redc_wide<FqCfg>(w.v); }
+#endif
+#ifndef ACEGPU_ONE_BODY
+#define ACEGPU_ONE_BODY 0  // 1: G1 products through the G2 bodies too (measured 51.0 vs 50.7 ms chunk)
+#endif
+#if ACEGPU_ONE_BODY && ACEGPU_FQ2_SHARED
+static __device__ __noinline__ Fq fq_mul_call(const Fq a, const Fq b) {
+    return fq_redc_call(fq_mul_wide_call(a, b));
+}
+#else
 static __device__ __noinline__ Fq fq_mul_call(const Fq a, const Fq b) { return mul(a, b); }
+#endif
 __device__ __forceinline__ Fq fmul(const Fq& a, const Fq& b) { return fq_mul_call(a, b); }
 // (A dedicated out-of-line squaring, 208 IMAD, measured slower in the bucket
 // loop than reusing the one product routine: a second 500-instruction body.)
@@ -39,34 +72,41 @@ __device__ __forceinline__ bool feq(const Fq& a, const Fq& b) { return a == b; }
 // Karatsuba on 512-bit products: c0 = a0 b0 - a1 b1 in [0, p 2^256),
 // c1 = (a0 + a1)(b0 + b1) - a0 b0 - a1 b1 = a0 b1 + a1 b0 in [0, 2p^2):
 // three products, two reductions (656 IMAD vs 792).
-__device__ __forceinline__ void fq2_mul_wide(const Fq2& a, const Fq2& b, uint32_t c0[16],
-                                             uint32_t c1[16]) {
-    uint32_t w1[16];
-    mul_wide(a.c0, b.c0, c0);
-    mul_wide(a.c1, b.c1, w1);
-    mul_wide(add_raw(a.c0, a.c1), add_raw(b.c0, b.c1), c1);
-    sub_wide(c1, c0);
-    sub_wide(c1, w1);
-    add_mR_masked<FqCfg>(c0, sub_wide(c0, w1));
+__device__ __forceinline__ void fq2_mul_wide(const Fq2& a, const Fq2& b, W16& c0, W16& c1) {
+    c0 = fq_mul_wide_call(a.c0, b.c0);
+    const W16 w1 = fq_mul_wide_call(a.c1, b.c1);
+    c1 = fq_mul_wide_call(add_raw(a.c0, a.c1), add_raw(b.c0, b.c1));
+    sub_wide(c1.v, c0.v);
+    sub_wide(c1.v, w1.v);
+    add_mR_masked<FqCfg>(c0.v, sub_wide(c0.v, w1.v));
 }
 static __device__ __noinline__ Fq2 fq2_mul_call(const Fq2 a, const Fq2 b) {
-    uint32_t c0[16], c1[16];
+    W16 c0, c1;
     fq2_mul_wide(a, b, c0, c1);
-    return {redc_wide<FqCfg>(c0), redc_wide<FqCfg>(c1)};
+    return {fq_redc_call(c0), fq_redc_call(c1)};
 }
 // a b - c d over Fq2: six products, two reductions.
 static __device__ __noinline__ Fq2 fq2_mul_sub_call(const Fq2 a, const Fq2 b, const Fq2 c,
                                                     const Fq2 d) {
-    uint32_t x0[16], x1[16], y0[16], y1[16];
+    W16 x0, x1, y0, y1;
     fq2_mul_wide(a, b, x0, x1);
     fq2_mul_wide(c, d, y0, y1);
-    add_mR_masked<FqCfg>(x0, sub_wide(x0, y0));
-    add_mR_masked<FqCfg>(x1, sub_wide(x1, y1));
-    return {redc_wide<FqCfg>(x0), redc_wide<FqCfg>(x1)};
+    add_mR_masked<FqCfg>(x0.v, sub_wide(x0.v, y0.v));
+    add_mR_masked<FqCfg>(x1.v, sub_wide(x1.v, y1.v));
+    return {fq_redc_call(x0), fq_redc_call(x1)};
 }
+#if ACEGPU_ONE_BODY && ACEGPU_FQ2_SHARED
+__device__ __forceinline__ Fq fq_mul_sub_call(const Fq& a, const Fq& b, const Fq& c, const Fq& d) {
+    W16 w = fq_mul_wide_call(a, b);
+    const W16 x = fq_mul_wide_call(c, d);
+    add_mR_masked<FqCfg>(w.v, sub_wide(w.v, x.v));
+    return fq_redc_call(w);
+}
+#else
 static __device__ __noinline__ Fq fq_mul_sub_call(const Fq a, const Fq b, const Fq c, const Fq d) {
     return mul_sub_mul(a, b, c, d);
 }
+#endif
 __device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) { return fq2_mul_call(a, b); }
 __device__ __forceinline__ Fq fmul_sub(const Fq& a, const Fq& b, const Fq& c, const Fq& d) {
     return fq_mul_sub_call(a, b, c, d);
