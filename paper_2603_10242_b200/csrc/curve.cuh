@@ -121,11 +121,25 @@ __device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
     return {sub(t0, t1), sub(sub(t2, t0), t1)};
 }
 #endif
+#if ACEGPU_LAZY && ACEGPU_FQ2_SHARED
+// (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u through the shared wide
+// bodies: (c0 + c1) unreduced times (c0 - c1) mod p < 2p^2, and 2 c0 c1 <
+// 2p^2 (a one-bit shift of the 512-bit product), both below p 2^256.
+__device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
+    W16 t = fq_mul_wide_call(a.c0, a.c1);
+#pragma unroll
+    for (int k = 15; k > 0; --k) t.v[k] = __funnelshift_l(t.v[k - 1], t.v[k], 1);
+    t.v[0] <<= 1;
+    const W16 u = fq_mul_wide_call(add_raw(a.c0, a.c1), sub(a.c0, a.c1));
+    return {fq_redc_call(u), fq_redc_call(t)};
+}
+#else
 __device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
     // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u
     Fq t = fq_mul_call(a.c0, a.c1);
     return {fq_mul_call(add(a.c0, a.c1), sub(a.c0, a.c1)), add(t, t)};
 }
+#endif
 
 // Selectable inlining: the G1 bucket-accumulation loop inlines its Fq
 // multiplications (one madd body, ILP across independent products).
