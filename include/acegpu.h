@@ -306,9 +306,10 @@ int acegpu_g16_verify_fc(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* fc328,
 int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                const uint8_t* d_payloads, const uint64_t* d_offs,
                                const uint8_t* d_atts, uint64_t n, uint64_t n_total,
-                               const uint8_t* d_revs, const uint32_t* d_rev_index,
-                               uint8_t* d_codes, const uint8_t* d_witness256,
-                               uint8_t* d_roots289, uint8_t* d_merkle32);
+                               const uint8_t* d_revs, uint64_t n_revs,
+                               const uint32_t* d_rev_index, uint8_t* d_codes,
+                               const uint8_t* d_witness256, uint8_t* d_roots289,
+                               uint8_t* d_merkle32);
 
 /* Optimal ate pairing product prod_i e(P_i, Q_i) (final exponentiation
  * included) over host buffers in the oracle encodings: G1 = x|y, G2 =

@@ -84,8 +84,8 @@ _SIGS = {
     "acegpu_g16_verify_batch": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int)]),
     "acegpu_g16_verify_fc": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, u64, vp, vp, u64p,
                                        C.POINTER(C.c_int)]),
-    "acegpu_g16_shard_roots_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, u64, vp, vp,
-                                             vp, vp, vp, vp]),
+    "acegpu_g16_shard_roots_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, u64, vp, u64,
+                                             vp, vp, vp, vp, vp]),
     "acegpu_bn_pairing": (C.c_int, [ctxp, u64, vp, vp, vp, C.POINTER(C.c_int)]),
     "acegpu_bn_f12_op": (C.c_int, [ctxp, C.c_int, vp, vp]),
     "acegpu_light_check": (C.c_int, [ctxp, vp, vp, vp, u64, vp, u64, u64, u64, vp, u64p]),

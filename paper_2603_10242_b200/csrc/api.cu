@@ -2220,12 +2220,15 @@ int g16_chunk_inputs(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
 extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
                                           const uint8_t* d_payloads, const uint64_t* d_offs,
                                           const uint8_t* d_atts, uint64_t n, uint64_t n_total,
-                                          const uint8_t* d_revs, const uint32_t* d_rev_index,
-                                          uint8_t* d_codes, const uint8_t* d_witness256,
-                                          uint8_t* d_roots289, uint8_t* d_merkle32) {
+                                          const uint8_t* d_revs, uint64_t n_revs,
+                                          const uint32_t* d_rev_index, uint8_t* d_codes,
+                                          const uint8_t* d_witness256, uint8_t* d_roots289,
+                                          uint8_t* d_merkle32) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     cudaStream_t s = pick(c, stream);
+    KeytabScope kts(c);  // attest keys for the credential verdicts (as the mock shard)
+    if (d_codes && n) RET(kts.build(s, d_revs, n_revs, d_atts + 64));
     const uint32_t T = g->d.T;
     TreeResult t;
     uint8_t *pub, *w, *proof, *node;

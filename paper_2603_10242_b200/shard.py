@@ -136,6 +136,7 @@ class G16Backend(GpuBackend):
         if db.n:
             self.ctx.call("acegpu_g16_shard_roots_dev", _stream(), self.pk.h, _ptr(db.payloads),
                           _ptr(db.offs), _ptr(db.atts), db.n, n_total, _ptr(db.revs),
+                          0 if db.revs is None else db.revs.numel() // 32,
                           _ptr(db.rev_index), _ptr(codes), _ptr(db.witnesses), _ptr(roots),
                           _ptr(merk))
         return roots[:c * 289], merk[:c * 32]

@@ -370,3 +370,36 @@ def test_groth16_verify_finality_certificate(ctx, n):
             assert pk.verify_finality_certificate(fc, wfb, bytes(pr)) == V.ProofMismatch
     finally:
         pk.close()
+
+
+def test_groth16_mode_attestation_verdicts(ctx):
+    """Groth16 mode runs the same batched HKDF/HMAC attestation check as the
+    hash-proof path: per-tx verdicts are identical to the mock shard's (and
+    all-accept on an honest block), including forged credentials."""
+    import torch
+    from paper_2603_10242_b200 import groth16, shard, wire
+    T, K, n = 4, 3, 23
+    pk = groth16.ProvingKey(T, K, arr([3, 5, 7, 11, 13]), ctx)
+    try:
+        fb = O.multi_user_block(n, 3)
+        atts = fb.atts.copy()
+        atts[104 * 5 + 100] ^= 1   # tx 5: credential bytes corrupted
+        atts[104 * 17 + 90] ^= 4   # tx 17
+        for forged in (False, True):
+            a = atts if forged else fb.atts
+            wfb = wire.FlatBlock(fb.payloads, fb.offs, a, np.frombuffer(fb.header, np.uint8).copy())
+            revs = np.frombuffer(fb.revs, np.uint8).copy()
+            rix = np.asarray(fb.rev_index, np.uint32)
+            db = shard.DeviceBlock.upload(wfb, 0, n, revs, rix, device=0)
+            db.witnesses = torch.zeros(256 * n, dtype=torch.uint8, device="cuda")
+            got = {}
+            for name, be in (("g16", shard.G16Backend(pk, ctx)), ("mock", shard.GpuBackend(ctx))):
+                codes = torch.full((n,), 0xEE, dtype=torch.uint8, device="cuda")
+                be.shard_roots(db, n, 2, codes=codes)
+                torch.cuda.synchronize()
+                got[name] = codes.cpu().numpy().copy()
+            assert (got["g16"] == got["mock"]).all()
+            bad = np.nonzero(got["g16"])[0].tolist()
+            assert bad == ([5, 17] if forged else [])
+    finally:
+        pk.close()
