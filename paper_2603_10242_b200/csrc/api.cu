@@ -1861,8 +1861,19 @@ struct acegpu_g16 {
     acegpu_msm_bases* qic = nullptr;
     uint8_t *vk_alpha1 = nullptr, *vk_g2_std = nullptr, *vk_ic = nullptr;
     uint8_t *consts = nullptr, *cc = nullptr;
+    // per-proof buffers of the current slot (pointers into slot[cur])
     uint8_t *z = nullptr, *zb = nullptr, *zl = nullptr, *ea = nullptr, *eb = nullptr, *ec = nullptr;
     uint8_t *pts = nullptr, *scaled = nullptr, *rs = nullptr, *digest = nullptr;
+    // two buffer slots: chunk k+1's witness chain (stream s_w) runs while
+    // chunk k's NTTs / MSMs still read the other slot; `done` = the slot's
+    // proof assembled (its buffers free again)
+    struct Slot {
+        uint8_t *z, *zb, *zl, *ea, *eb, *ec, *pts, *scaled, *rs, *digest;
+        cudaEvent_t done;
+    } slot[2] = {};
+    int cur = 1;
+    cudaStream_t s_w = nullptr;
+    cudaEvent_t ev_in = nullptr;
     cudaStream_t side = nullptr;
     cudaEvent_t ev_ab = nullptr, ev_scaled = nullptr;
     // concurrent MSM streams: B2 + L on s_bl, NTTs + H on s_h, each with its
@@ -1922,9 +1933,16 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     cudaDeviceSynchronize();
     for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh, g->qic})
         acegpu_bn_msm_free(b);
-    for (uint8_t* p : {g->consts, g->cc, g->z, g->zb, g->zl, g->ea, g->eb, g->ec, g->pts,
-                       g->scaled, g->rs, g->digest, g->vk_alpha1, g->vk_g2_std, g->vk_ic})
+    for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic})
         if (p) cudaFree(p);
+    for (auto& sl : g->slot) {
+        for (uint8_t* p : {sl.z, sl.zb, sl.zl, sl.ea, sl.eb, sl.ec, sl.pts, sl.scaled, sl.rs,
+                           sl.digest})
+            if (p) cudaFree(p);
+        if (sl.done) cudaEventDestroy(sl.done);
+    }
+    if (g->s_w) cudaStreamDestroy(g->s_w);
+    if (g->ev_in) cudaEventDestroy(g->ev_in);
     if (g->side) cudaStreamDestroy(g->side);
     if (g->ev_ab) cudaEventDestroy(g->ev_ab);
     if (g->ev_scaled) cudaEventDestroy(g->ev_scaled);
@@ -1963,11 +1981,17 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     g->Vp = g->d.V - 1 - T;
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     auto dm = [&](uint8_t** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 16); };
-    if (dm(&g->consts, 32 * 16) || dm(&g->cc, 32ull * K) || dm(&g->z, 32 * (V + 2)) ||
-        dm(&g->zb, 32 * (V + 2)) || dm(&g->zl, 32 * (g->Vp + 1)) || dm(&g->ea, 32 * N) ||
-        dm(&g->eb, 32 * N) || dm(&g->ec, 32 * N) || dm(&g->pts, 512) || dm(&g->scaled, 256) ||
-        dm(&g->rs, 64) || dm(&g->digest, 32))
+    if (dm(&g->consts, 32 * 16) || dm(&g->cc, 32ull * K))
         return fail(ACEGPU_ECUDA, "g16 alloc");
+    for (auto& sl : g->slot) {
+        if (dm(&sl.z, 32 * (V + 2)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
+            dm(&sl.ea, 32 * N) || dm(&sl.eb, 32 * N) || dm(&sl.ec, 32 * N) || dm(&sl.pts, 512) ||
+            dm(&sl.scaled, 256) || dm(&sl.rs, 64) || dm(&sl.digest, 32))
+            return fail(ACEGPU_ECUDA, "g16 alloc");
+        CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+    }
+    CK(cudaStreamCreateWithFlags(&g->s_w, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->ev_ab, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
@@ -2058,7 +2082,7 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
 namespace {
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
-                     uint8_t* d_raw256, uint8_t* d_digest32);
+                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr);
 }
 
 extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
@@ -2100,25 +2124,36 @@ struct G16Trace {
 G16Trace g_g16_trace;
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
-                     uint8_t* d_raw256, uint8_t* d_digest32) {
+                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready) {
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     uint8_t* scratch;
     RET(ws(c, kBnScratch, 32 * N, &scratch));
+    // next buffer slot; its previous proof must be assembled before reuse
+    g->cur ^= 1;
+    acegpu_g16::Slot& sl = g->slot[g->cur];
+    g->z = sl.z, g->zb = sl.zb, g->zl = sl.zl, g->ea = sl.ea, g->eb = sl.eb, g->ec = sl.ec;
+    g->pts = sl.pts, g->scaled = sl.scaled, g->rs = sl.rs, g->digest = sl.digest;
+    cudaStream_t sw = g->s_w;
+    if (!inputs_ready) {  // inputs produced on s up to now
+        CK(cudaEventRecord(g->ev_in, s));
+        inputs_ready = g->ev_in;
+    }
+    CK(cudaStreamWaitEvent(sw, inputs_ready, 0));
+    CK(cudaStreamWaitEvent(sw, sl.done, 0));
     G16Trace& tr = g_g16_trace;
-    tr.mark("start", s);
+    tr.mark("start", sw);
     for (uint8_t* e : {g->ea, g->eb, g->ec})
-        if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), s));
-    bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, s);
-    bn::g16_derive_rs(d_pub, g->d.T, g->rs, g->digest, s);
-    if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, s));
-    if (d_digest32) CK(cudaMemcpyAsync(d_digest32, g->digest, 32, cudaMemcpyDeviceToDevice, s));
+        if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), sw));
+    bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, sw);
+    bn::g16_derive_rs(d_pub, g->d.T, g->rs, g->digest, sw);
+    if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, sw));
     // scalar vectors with their extras
-    CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, s));
-    bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, s);
+    CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, sw));
+    CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, sw));
+    bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, sw);
     CKL();
-    CK(cudaEventRecord(g->ev_z, s));
-    tr.mark("witness", s);
+    CK(cudaEventRecord(g->ev_z, sw));
+    tr.mark("witness", sw);
     // s_h: H(x) = (a b - c) / Z on the coset, back to coefficients, then [h]
     const bn::NttTables& t = c->ntt[g->logn];
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
@@ -2159,8 +2194,12 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CK(cudaEventRecord(g->ev_scaled, g->side));
     tr.mark("scale", g->side);
     for (cudaEvent_t e : {g->ev_scaled, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
+    // outputs on s (the caller's order): the slot's digest was written on s_w
+    // before ev_z, which every wait above follows
+    if (d_digest32) CK(cudaMemcpyAsync(d_digest32, g->digest, 32, cudaMemcpyDeviceToDevice, s));
     bn::g16_assemble(g->pts, g->scaled, d_proof256, d_raw256, s);
     CKL();
+    CK(cudaEventRecord(sl.done, s));
     tr.mark("assemble", s);
     tr.dump();
     c->launches += 17 + 5 * bn::kMsmKernels + 6;
@@ -2241,9 +2280,13 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
     node = proof + 288;
     bn::g16_gather32(d_witness256, 256, n, chunks * T, w, s);
     CKL();
+    // every chunk's inputs are ready now: chunk k+1's witness chain may start
+    // while chunk k's MSMs run (two buffer slots)
+    cudaEvent_t ready = g->ev_in;
+    CK(cudaEventRecord(ready, s));
     for (uint64_t k = 0; k < chunks; ++k) {
         RET(g16_prove_locked(c, s, g, w + 32 * T * k, pub + 32 * T * k, nullptr, proof, nullptr,
-                             proof + 256));
+                             proof + 256, ready));
         bn::g16_chunk_node(proof, proof + 256, node, s);
         launch_pack_nodes(node, 1, d_roots289 + 289 * k, s);
         CKL();
