@@ -692,8 +692,12 @@ def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup,
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    out = {"n_tx": n, "chunks": -(-n // 1024), "latency_ms": ms, "proven_tx_per_s": n / (ms * 1e-3),
+    chunks_total = -(-n // 1024)
+    out = {"n_tx": n, "chunks": chunks_total, "latency_ms": ms, "proven_tx_per_s": n / (ms * 1e-3),
            "vs_400ms_interval": ms / 400.0, "steps": steps,
+           "per_chunk_ms": ms / -(-chunks_total // world),
+           # the 100k block has 98 chunks -> 13 on the busiest of 8 ranks
+           "extrapolated_100k_block_ms_8gpu": 13 * ms / -(-chunks_total // world),
            "accepted": accepted_total(codes[:count], world),
            "fc_sha256": hashlib_sha256(fc.cpu().numpy().tobytes())}
     if world == 1:
