@@ -185,6 +185,24 @@ def test_msm_degenerate_scalars(ctx):
         assert got == bytes(dl), label
 
 
+@pytest.mark.parametrize("group,n", [(2, 3000), (1, 1 << 18)])
+def test_msm_heavy_buckets(ctx, group, n):
+    """A 0/1-valued witness (one bucket holds every window-0 entry: it spans
+    thousands of accumulation segments and goes through the heavy-bucket
+    queue) on G2 and at 2^18 points on G1, checked by discrete logs."""
+    G = np.frombuffer(g_gen(group), np.uint8).copy()
+    ks = [(i * 2654435761) % (1 << 40) + 1 for i in range(n)]
+    pts = np.zeros(64 * group * n, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", group, G, arr(ks), n, pts)
+    sc = [(i % 3) & 1 for i in range(n)]
+    sc[-1] = R - 1
+    got = msm_gpu(ctx, group, pts, arr(sc), n)
+    e = sum(s * k for s, k in zip(sc, ks)) % R
+    dl = O.buf(64 * group)
+    O.oracle().bn_scalar_mul(C.c_int(group), O.ptr(bytes(G)), O.ptr(le(e)), dl)
+    assert got == bytes(dl)
+
+
 def test_msm_2_20_discrete_log(ctx):
     """BASELINE configs[1]: G1 MSM of 2^20 points, checked exactly through
     known discrete logs (bases k_i * G)."""
