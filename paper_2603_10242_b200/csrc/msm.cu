@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <cstdlib>
 
 #include "curve.cuh"
 #include "msm.cuh"
@@ -363,6 +364,198 @@ __global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum,
     }
 }
 
+// ---- batch-affine bucket levels (G1) ---------------------------------------
+// Alternative to accumulate/fixup: each level adds the entries of every
+// bucket pairwise in AFFINE coordinates, (x1,y1) + (x2,y2) with
+// lambda = num / den (den = x2 - x1, or 2y for a doubling), 3 products + one
+// shared inversion. The inversions of a warp's 32 x kAffK additions are
+// batched (Montgomery's trick: prefix products per lane, a product scan
+// across lanes, ONE binary-EEA inversion on lane 0 — ALU work, off the
+// saturated IMAD pipe), so an addition costs ~6 products + 12/kAffK
+// instead of the mixed XYZZ add's 8 products + a lazy difference. After
+// ~log2(entries / buckets) levels the few points left per bucket are summed
+// in XYZZ. EXPERIMENTAL, off by default (-DACEGPU_MSM_AFFINE=1 builds it in;
+// ACEGPU_MSM_AFFINE=0 in the environment then selects XYZZ at run time):
+// correct (the MSM tests pass on it) but G1 2^20 takes 8.6 ms vs 5.0 ms —
+// each level re-gathers its input pairs in the back-substitution pass (DRAM
+// 3.9 GB at level 0), 168 registers leave 12 warps/SM for random gathers,
+// and the per-warp inversion puts a ~130 us latency floor under each level.
+// A version staging the pairs in shared memory with a larger batch is the
+// round-2 candidate (DESIGN.md round log).
+#ifndef ACEGPU_MSM_AFFINE
+#define ACEGPU_MSM_AFFINE 0
+#endif
+#ifndef ACEGPU_AFF_K
+#define ACEGPU_AFF_K 8
+#endif
+constexpr int kAffK = ACEGPU_AFF_K;
+inline bool affine_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("ACEGPU_MSM_AFFINE");
+        return !e || e[0] != '0';
+    }();
+    return on;
+}
+
+// out[b] = ceil(size_b / 2), out[NB] = 0 (for the exclusive scan)
+__global__ void halve_counts_kernel(const uint32_t* in_offs, uint32_t* cnt) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b > kMsmBuckets) return;
+    cnt[b] = b < kMsmBuckets ? (in_offs[b + 1] - in_offs[b] + 1) / 2 : 0u;
+}
+
+__device__ __forceinline__ Fq shfl_fq(const Fq& a, int lane_or_delta, int mode) {
+    Fq r;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        r.v[k] = mode == 0 ? __shfl_sync(0xffffffffu, a.v[k], lane_or_delta)
+                 : mode == 1 ? __shfl_up_sync(0xffffffffu, a.v[k], lane_or_delta)
+                             : __shfl_down_sync(0xffffffffu, a.v[k], lane_or_delta);
+    return r;
+}
+
+template <bool FIRST>
+__device__ __forceinline__ bool aff_load(const uint8_t* table, const uint32_t* sorted,
+                                         const uint8_t* pts, uint32_t i, Fq& x, Fq& y) {
+    if (FIRST) {
+        const uint32_t v = sorted[i];
+        const bool fin = load_affine<Fq>(table + 64ull * (v & 0x7FFFFFFFu), x, y);
+        if (fin && (v >> 31)) y = neg(y);
+        return fin;
+    }
+    return load_affine<Fq>(pts + 64ull * i, x, y);
+}
+
+// Slot j of bucket b: its input pair, the case and (num, den).
+// kind: 0 = copy P1, 1 = copy P2, 2 = infinity, 3 = add (num / den)
+template <bool FIRST>
+__device__ __forceinline__ int aff_pair(const uint8_t* table, const uint32_t* sorted,
+                                        const uint8_t* pts, const uint32_t* in_offs,
+                                        const uint32_t* out_offs, int b, uint32_t j, Fq& x1,
+                                        Fq& y1, Fq& x2, Fq& y2, Fq& num, Fq& den) {
+    const uint32_t i0 = in_offs[b] + 2 * (j - out_offs[b]);
+    const bool f1 = aff_load<FIRST>(table, sorted, pts, i0, x1, y1);
+    const bool f2 = i0 + 1 < in_offs[b + 1] && aff_load<FIRST>(table, sorted, pts, i0 + 1, x2, y2);
+    den = Fq::one();
+    if (!f2) return f1 ? 0 : 2;
+    if (!f1) return 1;
+    if (x1 == x2) {
+        if (!(y1 == y2)) return 2;  // P + (-P)
+        const Fq xx = fsqr(x1);
+        num = add(add(xx, xx), xx);  // doubling: 3x^2 / 2y (no 2-torsion in G1)
+        den = add(y1, y1);
+        return 3;
+    }
+    num = sub(y2, y1);
+    den = sub(x2, x1);
+    return 3;
+}
+
+// One level: output slot j = pair (2(j - out_offs[b]), +1) of bucket b's
+// input run. Every lane of a warp takes part in the scans (no early exit).
+template <bool FIRST>
+__global__ void __launch_bounds__(128) affine_level_kernel(const uint8_t* table,
+                                                           const uint32_t* sorted,
+                                                           const uint8_t* in_pts,
+                                                           const uint32_t* in_offs,
+                                                           const uint32_t* out_offs,
+                                                           uint8_t* out_pts) {
+    const uint32_t total = out_offs[kMsmBuckets];
+    const uint32_t j0 = (blockIdx.x * blockDim.x + threadIdx.x) * kAffK;
+    const int lane = threadIdx.x & 31;
+    int bs[kAffK];
+    Fq pre[kAffK];
+    Fq run = Fq::one();
+    int b = j0 < total ? bucket_of(out_offs, j0) : 0;
+#pragma unroll
+    for (int s = 0; s < kAffK; ++s) {
+        const uint32_t j = j0 + s;
+        Fq den = Fq::one();
+        if (j < total) {
+            while (out_offs[b + 1] <= j) ++b;
+            Fq x1, y1, x2, y2, num;
+            aff_pair<FIRST>(table, sorted, in_pts, in_offs, out_offs, b, j, x1, y1, x2, y2, num,
+                            den);
+        }
+        bs[s] = b;
+        run = fmul(run, den);
+        pre[s] = run;
+    }
+    // inclusive prefix and suffix products of the lane totals across the warp
+    Fq q = run, sx = run;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const Fq o = shfl_fq(q, d, 1), u = shfl_fq(sx, d, 2);
+        if (lane >= d) q = fmul(q, o);
+        if (lane + d < 32) sx = fmul(sx, u);
+    }
+    Fq inv = shfl_fq(q, 31, 0);
+    if (lane == 0) inv = finv(inv);
+    inv = shfl_fq(inv, 0, 0);
+    Fq pe = shfl_fq(q, 1, 1), se = shfl_fq(sx, 1, 2);
+    if (lane == 0) pe = Fq::one();
+    if (lane == 31) se = Fq::one();
+    Fq inv_run = fmul(fmul(inv, pe), se);  // 1 / (this lane's product)
+#pragma unroll
+    for (int s = kAffK - 1; s >= 0; --s) {
+        const uint32_t j = j0 + s;
+        if (j >= total) continue;
+        Fq x1, y1, x2, y2, num, den;
+        const int kind = aff_pair<FIRST>(table, sorted, in_pts, in_offs, out_offs, bs[s], j, x1, y1,
+                                         x2, y2, num, den);
+        const Fq inv_den = s > 0 ? fmul(inv_run, pre[s - 1]) : inv_run;
+        inv_run = fmul(inv_run, den);
+        uint8_t* o = out_pts + 64ull * j;
+        if (kind == 3) {
+            const Fq lam = fmul(num, inv_den);
+            const Fq x3 = sub(sub(fsqr(lam), x1), x2);
+            store_affine(o, x3, sub(fmul(lam, sub(x1, x3)), y1));
+        } else if (kind == 0) {
+            store_affine(o, x1, y1);
+        } else if (kind == 1) {
+            store_affine(o, x2, y2);
+        } else {
+            store_affine(o, Fq::zero(), Fq::zero());
+        }
+    }
+}
+
+// After the levels: one thread per bucket sums its (few) remaining affine
+// points into XYZZ; long runs (skewed digits) go to the heavy queue.
+__global__ void __launch_bounds__(128) affine_finish_kernel(const uint8_t* pts,
+                                                            const uint32_t* offs,
+                                                            uint8_t* buckets, uint32_t* heavy) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= kMsmBuckets) return;
+    const uint32_t s = offs[b], e = offs[b + 1];
+    if (e - s > 64) {
+        heavy[1 + atomicAdd(&heavy[0], 1u)] = b;
+        return;
+    }
+    XYZZ<Fq> acc = XYZZ<Fq>::inf();
+    for (uint32_t i = s; i < e; ++i) {
+        Fq x, y;
+        if (load_affine<Fq>(pts + 64ull * i, x, y)) acc = xyzz_madd<Fq>(acc, x, y);
+    }
+    store_xyzz(buckets + 128ull * b, acc);
+}
+
+__global__ void __launch_bounds__(128) affine_heavy_kernel(const uint8_t* pts, const uint32_t* offs,
+                                                           uint8_t* buckets, const uint32_t* heavy) {
+    const uint32_t nh = heavy[0];
+    for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int b = heavy[1 + h];
+        XYZZ<Fq> acc = XYZZ<Fq>::inf();
+        for (uint32_t i = offs[b] + threadIdx.x; i < offs[b + 1]; i += blockDim.x) {
+            Fq x, y;
+            if (load_affine<Fq>(pts + 64ull * i, x, y)) acc = xyzz_madd<Fq>(acc, x, y);
+        }
+        acc = cta_sum128(acc);
+        if (threadIdx.x == 0) store_xyzz(buckets + 128ull * b, acc);
+        __syncthreads();
+    }
+}
+
 __global__ void points_convert_kernel(uint8_t* pts, uint64_t n_elems, int to) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n_elems) return;
@@ -405,10 +598,59 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
         return -1;
     cudaMemcpyAsync(sc.cursor, sc.offs, 4 * kMsmBuckets, cudaMemcpyDeviceToDevice, s);
     scatter_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
-    accumulate_kernel<F><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
-        table, sc.sorted, sc.offs, sc.buckets, sc.partials);
-    fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
-    heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
+    bool affine = false;
+    if constexpr (sizeof(F) == sizeof(Fq)) affine = ACEGPU_MSM_AFFINE && affine_enabled();
+    if (affine) {
+        // levels until ~1 point per bucket remains for uniform digits (the
+        // finish kernel sums what is left); output-slot upper bounds size the
+        // grids without a host sync
+        uint64_t U = cap, ub[24];
+        int L = 0;
+        do {
+            U = U / 2 + kMsmBuckets;
+            ub[L++] = U;
+        } while ((cap >> L) > (uint64_t)kMsmBuckets && L < 20);
+        if (sc.aff_cap < ub[0]) {
+            for (void* p : {(void*)sc.aff_pts[0], (void*)sc.aff_pts[1]})
+                if (p) cudaFree(p);
+            if (cudaMalloc(&sc.aff_pts[0], 64 * ub[0]) || cudaMalloc(&sc.aff_pts[1], 64 * ub[0]))
+                return -1;
+            sc.aff_cap = ub[0];
+        }
+        if (!sc.aff_offs[0] &&
+            (cudaMalloc(&sc.aff_offs[0], 4 * (kMsmBuckets + 1)) ||
+             cudaMalloc(&sc.aff_offs[1], 4 * (kMsmBuckets + 1)) ||
+             cudaMalloc(&sc.aff_cnt, 4 * (kMsmBuckets + 1))))
+            return -1;
+        const uint32_t* in_offs = sc.offs;
+        const uint8_t* in_pts = nullptr;
+        for (int l = 0; l < L; ++l) {
+            uint32_t* out_offs = sc.aff_offs[l & 1];
+            uint8_t* out_pts = sc.aff_pts[l & 1];
+            halve_counts_kernel<<<kMsmBuckets / 128 + 1, 128, 0, s>>>(in_offs, sc.aff_cnt);
+            if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, sc.scan_bytes, sc.aff_cnt, out_offs,
+                                              kMsmBuckets + 1, s) != cudaSuccess)
+                return -1;
+            const unsigned grid = (unsigned)((ub[l] + 128ull * kAffK - 1) / (128ull * kAffK));
+            if (l == 0)
+                affine_level_kernel<true><<<grid, 128, 0, s>>>(table, sc.sorted, nullptr, in_offs,
+                                                               out_offs, out_pts);
+            else
+                affine_level_kernel<false><<<grid, 128, 0, s>>>(nullptr, nullptr, in_pts, in_offs,
+                                                                out_offs, out_pts);
+            in_offs = out_offs;
+            in_pts = out_pts;
+        }
+        affine_finish_kernel<<<kMsmBuckets / 128, 128, 0, s>>>(in_pts, in_offs, sc.buckets,
+                                                               sc.heavy);
+        affine_heavy_kernel<<<148, 128, 0, s>>>(in_pts, in_offs, sc.buckets, sc.heavy);
+    } else {
+        accumulate_kernel<F><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
+            table, sc.sorted, sc.offs, sc.buckets, sc.partials);
+        fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets,
+                                                          sc.heavy);
+        heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
+    }
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
     static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
     reduce_final_kernel<F><<<1, 64, 0, s>>>(sc.segsum, out);
@@ -419,9 +661,13 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 }  // namespace
 
 void MsmScratch::release() {
-    void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum, scan_tmp, heavy};
+    void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum, scan_tmp, heavy,
+                  aff_pts[0], aff_pts[1], aff_offs[0], aff_offs[1], aff_cnt};
     for (void* p : ps)
         if (p) cudaFree(p);
+    aff_pts[0] = aff_pts[1] = nullptr;
+    aff_offs[0] = aff_offs[1] = aff_cnt = nullptr;
+    aff_cap = 0;
     hist = offs = cursor = sorted = heavy = nullptr;
     partials = buckets = segsum = nullptr;
     scan_tmp = nullptr;

@@ -28,6 +28,10 @@ struct MsmScratch {
     uint8_t* segsum = nullptr;     // reduction partials (one per CTA)
     uint32_t* heavy = nullptr;     // [count, bucket ids] of buckets spanning many segments
     void* scan_tmp = nullptr;      // CUB scan temporary storage
+    uint8_t* aff_pts[2] = {nullptr, nullptr};     // batch-affine levels (G1): points
+    uint32_t* aff_offs[2] = {nullptr, nullptr};   // and bucket offsets, ping-pong
+    uint32_t* aff_cnt = nullptr;
+    uint64_t aff_cap = 0;
     size_t scan_bytes = 0;
     size_t cap_entries = 0;
     void release();
