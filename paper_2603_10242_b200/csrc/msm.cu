@@ -248,8 +248,24 @@ __device__ __forceinline__ XYZZ<F> shfl_xyzz(const XYZZ<F>& a, int src_lane_delt
 // Sum of a 128-thread CTA's values (result valid in thread 0).
 template <class F>
 __device__ __forceinline__ XYZZ<F> cta_sum128(XYZZ<F> v) {
-    __shared__ __align__(16) uint8_t sm[4 * sizeof(XYZZ<F>)];
     constexpr int X = Lay<F>::XZ;
+    if constexpr (sizeof(F) > sizeof(Fq)) {
+        // G2: a shared-memory tree (shuffling 64-word XYZZ values spilled)
+        __shared__ __align__(16) uint8_t buf[128 * sizeof(XYZZ<F>)];
+        const int t = threadIdx.x;
+        store_xyzz(buf + X * t, v);
+        __syncthreads();
+#pragma unroll 1
+        for (int st = 64; st >= 1; st >>= 1) {
+            if (t < st) {
+                v = xyzz_add(v, load_xyzz<F>(buf + X * (t + st)));
+                store_xyzz(buf + X * t, v);
+            }
+            __syncthreads();
+        }
+        return v;
+    }
+    __shared__ __align__(16) uint8_t sm[4 * sizeof(XYZZ<F>)];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
