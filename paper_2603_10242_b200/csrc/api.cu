@@ -1880,7 +1880,9 @@ struct acegpu_g16 {
     // own MSM scratch, so one MSM's latency-bound sort/reduction phases
     // overlap another's throughput-bound bucket accumulation
     cudaStream_t s_bl = nullptr, s_h = nullptr;
-    cudaStream_t s_ab = nullptr;  // highest priority: A, B1 finish first so s*A, r*B1 overlap
+    cudaStream_t s_ab = nullptr;  // A, B1, then s*A, r*B1 on `side` overlapping the others
+    cudaStream_t s_n = nullptr;   // the H-polynomial NTTs (then ev_n -> the H MSM on s_h)
+    cudaEvent_t ev_n = nullptr;
     cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
     bn::MsmScratch msm_bl, msm_h;
 };
@@ -1946,8 +1948,9 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     if (g->side) cudaStreamDestroy(g->side);
     if (g->ev_ab) cudaEventDestroy(g->ev_ab);
     if (g->ev_scaled) cudaEventDestroy(g->ev_scaled);
-    for (cudaStream_t t : {g->s_bl, g->s_h, g->s_ab})
+    for (cudaStream_t t : {g->s_bl, g->s_h, g->s_ab, g->s_n})
         if (t) cudaStreamDestroy(t);
+    if (g->ev_n) cudaEventDestroy(g->ev_n);
     for (cudaEvent_t e : {g->ev_z, g->ev_bl, g->ev_h})
         if (e) cudaEventDestroy(e);
     g->msm_bl.release();
@@ -1995,12 +1998,25 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->ev_ab, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
-    CK(cudaStreamCreateWithFlags(&g->s_bl, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&g->s_h, cudaStreamNonBlocking));
     {
+        // stream priorities (ACEGPU_G16_PRIO: which of ab / h / bl run at the
+        // highest priority; "none" = all equal). Measured (chunk, ms): bl 49.75,
+        // none 49.7-50.1, ab 50.3, ab+bl 50.5, ab+h 52.1, h 52.9, NTTs on top
+        // ("n", "nbl", "nab") 51.5-52.7 -> the longest MSM (G2, B2) first.
         int least = 0, greatest = 0;
         CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        CK(cudaStreamCreateWithPriority(&g->s_ab, cudaStreamNonBlocking, greatest));
+        const char* e = std::getenv("ACEGPU_G16_PRIO");
+        const std::string pr = e ? e : "bl";
+        auto prio = [&](const char* k) { return pr.find(k) != std::string::npos ? greatest : least; };
+        // "n": the H-polynomial NTTs on their own top-priority stream (the H
+        // MSM then waits for them on s_h) with the others one level below
+        const bool n_top = pr.find('n') != std::string::npos && greatest < least;
+        auto lvl = [&](const char* k) { return n_top && prio(k) == greatest ? greatest + 1 : prio(k); };
+        CK(cudaStreamCreateWithPriority(&g->s_bl, cudaStreamNonBlocking, lvl("bl")));
+        CK(cudaStreamCreateWithPriority(&g->s_h, cudaStreamNonBlocking, lvl("h")));
+        CK(cudaStreamCreateWithPriority(&g->s_ab, cudaStreamNonBlocking, lvl("ab")));
+        CK(cudaStreamCreateWithPriority(&g->s_n, cudaStreamNonBlocking, n_top ? greatest : lvl("h")));
+        CK(cudaEventCreateWithFlags(&g->ev_n, cudaEventDisableTiming));
     }
     for (cudaEvent_t* e : {&g->ev_z, &g->ev_bl, &g->ev_h})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -2157,17 +2173,19 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     // s_h: H(x) = (a b - c) / Z on the coset, back to coefficients, then [h]
     const bn::NttTables& t = c->ntt[g->logn];
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
-    cudaStream_t sh = g->s_h;
-    CK(cudaStreamWaitEvent(sh, g->ev_z, 0));
+    cudaStream_t sh = g->s_h, sn = g->s_n;
+    CK(cudaStreamWaitEvent(sn, g->ev_z, 0));
     for (uint8_t* e : {g->ea, g->eb, g->ec}) {
-        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sh)) return fail(ACEGPU_ECUDA, "g16 intt");
-        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sh)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
+        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn)) return fail(ACEGPU_ECUDA, "g16 intt");
+        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
     }
-    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sh);
-    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, sh)) return fail(ACEGPU_ECUDA, "g16 coset intt");
-    bn::launch_fr_convert(g->ea, N, 0, sh);  // h coefficients -> standard form scalars
-    tr.mark("ntt", sh);
+    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
+    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset intt");
+    bn::launch_fr_convert(g->ea, N, 0, sn);  // h coefficients -> standard form scalars
+    tr.mark("ntt", sn);
     CKL();
+    CK(cudaEventRecord(g->ev_n, sn));
+    CK(cudaStreamWaitEvent(sh, g->ev_n, 0));
     if (bn::msm_run(1, g->qh->table, N - 1, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
@@ -2180,8 +2198,8 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm B2/L");
     CK(cudaEventRecord(g->ev_bl, g->s_bl));
     tr.mark("msm_l", g->s_bl);
-    // s_ab (high priority): A and B1, then s*A and r*B1 (one serial
-    // scalar multiplication each) on the side stream while the others finish
+    // s_ab: A and B1, then s*A and r*B1 (one serial scalar multiplication
+    // each) on the side stream while the others finish
     CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
     if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, g->s_ab) ||
         (tr.mark("msm_a", g->s_ab), false) ||

@@ -116,7 +116,7 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const uint32_t bi = b.v[i];
-        // t += a * b_i : low halves into t0..t7 (carry into t8), high halves into t1..t8.
+        // t += a * b_i : low halves into t0..t7 (carry into t8 = 0), high halves into t1..t8.
         asm("mad.lo.cc.u32  %0, %9,  %17, %0;\n\t"
             "madc.lo.cc.u32 %1, %10, %17, %1;\n\t"
             "madc.lo.cc.u32 %2, %11, %17, %2;\n\t"
@@ -125,9 +125,9 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
             "madc.lo.cc.u32 %5, %14, %17, %5;\n\t"
             "madc.lo.cc.u32 %6, %15, %17, %6;\n\t"
             "madc.lo.cc.u32 %7, %16, %17, %7;\n\t"
-            "addc.u32       %8, %8, 0;"
+            "addc.u32       %8, 0, 0;"
             : "+r"(t0), "+r"(t1), "+r"(t2), "+r"(t3), "+r"(t4), "+r"(t5), "+r"(t6), "+r"(t7),
-              "+r"(t8)
+              "=r"(t8)
             : "r"(a.v[0]), "r"(a.v[1]), "r"(a.v[2]), "r"(a.v[3]), "r"(a.v[4]), "r"(a.v[5]),
               "r"(a.v[6]), "r"(a.v[7]), "r"(bi));
         asm("mad.hi.cc.u32  %0, %8,  %16, %0;\n\t"
