@@ -179,31 +179,37 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
 // BN254; psi = the untwist-Frobenius-twist map, the Miller loop's frob_twist)
 // -- a 127-bit scalar instead of r's 254 bits, run concurrently with the
 // Miller loops instead of before them.
-__global__ void __launch_bounds__(32) miller_check_kernel(uint32_t n_pairs, const uint8_t* g1s,
+// Blocks [0, mb): 32 pairs per 64-thread CTA, Miller loops split over two
+// warps (miller_loop_2w). Blocks >= mb: the psi(B) = [6x^2]B subgroup checks.
+__global__ void __launch_bounds__(64) miller_check_kernel(uint32_t n_pairs, const uint8_t* g1s,
                                                           const uint8_t* g2s, uint8_t* scratch,
                                                           uint32_t mb, const uint8_t* proofs,
                                                           uint32_t n, int* bad) {
     if (blockIdx.x < mb) {
-        const uint32_t i = blockIdx.x * 32 + threadIdx.x;
-        if (i >= n_pairs) return;
-        const uint8_t* p = g1s + 64ull * i;
-        const uint8_t* q = g2s + 128ull * i;
-        bool inf = true;
-        for (int b = 0; b < 64 && inf; ++b) inf = p[b] == 0;
-        bool qinf = true;
-        for (int b = 0; b < 128 && qinf; ++b) qinf = q[b] == 0;
-        Fq12 f;
-        if (inf || qinf) {
-            f = f12_one();
-        } else {
-            const Fq2 xq = {to_mont(load<FqCfg>(q)), to_mont(load<FqCfg>(q + 32))};
-            const Fq2 yq = {to_mont(load<FqCfg>(q + 64)), to_mont(load<FqCfg>(q + 96))};
-            f = miller_loop(to_mont(load<FqCfg>(p)), to_mont(load<FqCfg>(p + 32)), xq, yq);
+        __shared__ LinePair buf[2][32];
+        const uint32_t i = blockIdx.x * 32 + (threadIdx.x & 31);
+        bool active = i < n_pairs;
+        Fq xp = Fq::zero(), yp = Fq::zero();
+        Fq2 xq = {xp, xp}, yq = {xp, xp};
+        if (active) {
+            const uint8_t* p = g1s + 64ull * i;
+            const uint8_t* q = g2s + 128ull * i;
+            bool inf = true;
+            for (int b = 0; b < 64 && inf; ++b) inf = p[b] == 0;
+            bool qinf = true;
+            for (int b = 0; b < 128 && qinf; ++b) qinf = q[b] == 0;
+            active = !(inf || qinf);
+            xp = to_mont(load<FqCfg>(p));
+            yp = to_mont(load<FqCfg>(p + 32));
+            xq = {to_mont(load<FqCfg>(q)), to_mont(load<FqCfg>(q + 32))};
+            yq = {to_mont(load<FqCfg>(q + 64)), to_mont(load<FqCfg>(q + 96))};
         }
-        *reinterpret_cast<Fq12*>(scratch + sizeof(Fq12) * i) = f;
+        const Fq12 f = miller_loop_2w(xp, yp, xq, yq, active, buf);
+        if (threadIdx.x < 32 && i < n_pairs)  // degenerate pairs: f = 1
+            *reinterpret_cast<Fq12*>(scratch + sizeof(Fq12) * i) = active ? f : f12_one();
         return;
     }
-    const uint32_t i = (blockIdx.x - mb) * 32 + threadIdx.x;
+    const uint32_t i = (blockIdx.x - mb) * 64 + threadIdx.x;
     if (i >= n) return;
     const uint8_t* pr = proofs + 256ull * i;
     const Fq2 bx = {ld_be(pr + 96), ld_be(pr + 64)}, by = {ld_be(pr + 160), ld_be(pr + 128)};
@@ -287,7 +293,7 @@ int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_
     points_kernel<<<grid(n, 32), 32, 0, s>>>(proofs, rho, n, g1s, g2s, cacc, bad);
     finish_kernel<<<1, 32, 0, s>>>(cacc, n, sc, vk.alpha1_mont, L, vk.g2_std, g1s, g2s);
     const uint32_t mb = (n + 3 + 31) / 32;
-    miller_check_kernel<<<mb + (n + 31) / 32, 32, 0, s>>>(n + 3, g1s, g2s, pscratch, mb, proofs,
+    miller_check_kernel<<<mb + (n + 63) / 64, 64, 0, s>>>(n + 3, g1s, g2s, pscratch, mb, proofs,
                                                           n, bad);
     launch_pairing_finish(n + 3, pscratch, nullptr, d_ok, s);
     // d_ok &= !bad

@@ -13,7 +13,10 @@ namespace bn {
 constexpr int kMsmC = ACEGPU_MSM_C;                   // window bits
 constexpr int kMsmWindows = (255 + kMsmC - 1) / kMsmC;  // 254-bit scalars + the signed-digit carry
 constexpr int kMsmBuckets = 1 << (kMsmC - 1);         // |digit| in 1..2^(c-1)
-constexpr int kMsmSeg = 64;                           // sorted entries per accumulating thread
+#ifndef ACEGPU_MSM_SEG
+#define ACEGPU_MSM_SEG 64
+#endif
+constexpr int kMsmSeg = ACEGPU_MSM_SEG;               // sorted entries per accumulating thread
 constexpr int kMsmKernels = 9;  // kernel launches per msm_run (2 of them in the CUB scan)
 static_assert(kMsmC >= 12 && kMsmC <= 24, "window bits");
 

@@ -316,6 +316,60 @@ static __device__ __noinline__ Fq12 miller_loop(const Fq& xP, const Fq& yP, cons
     return f;
 }
 
+// The same Miller loop split over two warps of one CTA for up to 32 pairs:
+// warp 0 keeps f (squaring, then the sparse line products), warp 1 walks T
+// and produces the lines (dbl_step, add_step), handing them over in shared
+// memory double-buffered by iteration parity with one __syncthreads per
+// iteration — f's squaring overlaps T's doubling. Identical operations in
+// identical order as miller_loop, so f is bit-identical. All 64 threads must
+// call it (`active` = this lane holds a non-degenerate pair); the result is
+// valid in warp 0.
+struct LinePair {
+    Line d, a;
+};
+__device__ __forceinline__ Fq12 miller_loop_2w(const Fq& xP, const Fq& yP, const Fq2& xQ,
+                                               const Fq2& yQ, bool active, LinePair (*buf)[32]) {
+    const uint64_t loop_lo = 0x9d797039be763ba8ull;  // 6x+2 = 2^64 + loop_lo
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    Fq12 f = f12_one();
+    G2Proj T;
+    T.X = xQ;
+    T.Y = yQ;
+    fset_one(T.Z);
+    for (int i = 63; i >= 0; --i) {
+        const int par = i & 1;
+        const bool bit = (loop_lo >> i) & 1;
+        if (active) {
+            if (w == 1) {
+                buf[par][lane].d = dbl_step(T, xP, yP);
+                if (bit) buf[par][lane].a = add_step(T, xQ, yQ, xP, yP);
+            } else {
+                f = f12_sqr(f);
+            }
+        }
+        __syncthreads();
+        if (active && w == 0) {
+            f = f12_mul_line(f, buf[par][lane].d);
+            if (bit) f = f12_mul_line(f, buf[par][lane].a);
+        }
+    }
+    // buf[1] was last read before the i = 0 barrier: free for the tail
+    if (active && w == 1) {
+        Fq2 x1 = xQ, y1 = yQ;
+        frob_twist(x1, y1);
+        Fq2 x2 = x1, y2 = y1;
+        frob_twist(x2, y2);
+        buf[1][lane].d = add_step(T, x1, y1, xP, yP);
+        buf[1][lane].a = add_step(T, x2, f2_neg(y2), xP, yP);
+    }
+    __syncthreads();
+    if (active && w == 0) {
+        f = f12_mul_line(f, buf[1][lane].d);
+        f = f12_mul_line(f, buf[1][lane].a);
+    }
+    return f;
+}
+
 // Hard part ^((p^4 - p^2 + 1) / r) of an element of the cyclotomic subgroup.
 static __device__ __noinline__ Fq12 final_exp_hard(const Fq12& t1) {
     const Fq12 fp = f12_frob(t1, 1), fp2 = f12_frob(t1, 2), fp3 = f12_frob(fp2, 1);
