@@ -142,21 +142,50 @@ __global__ void combine_kernel(const uint8_t* pubs, const uint8_t* rho, uint32_t
     store<FrCfg>(out + 32ull * j, from_mont(acc));
 }
 
-// Per proof: validate, rho_i A_i (pair i), B_i, rho_i C_i (XYZZ, Montgomery).
+__device__ void put_neg_g1(uint8_t* o, const XYZZ<Fq>& p) {
+    if (p.is_inf()) {
+        for (int b = 0; b < 64; ++b) o[b] = 0;
+        return;
+    }
+    Fq x, y;
+    to_affine(p, x, y);
+    st_std(o, x);
+    st_std(o + 32, neg(y));
+}
+
+// Two threads per proof: thread 2i validates proof i and writes rho_i A_i
+// (pair i) and B_i; thread 2i+1 computes rho_i C_i (XYZZ, Montgomery).
+// Thread 2n computes s0 * alpha (pair n, negated), s0 = sum_i rho_i, so the
+// three serial scalar multiplications run side by side.
 __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_t n,
-                              uint8_t* g1s, uint8_t* g2s, XYZZ<Fq>* cacc, int* bad) {
-    const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+                              uint8_t* g1s, uint8_t* g2s, XYZZ<Fq>* cacc, int* bad,
+                              const uint8_t* s0_std, const uint8_t* vk_mont) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t i = t >> 1;
+    if (t == 2 * n) {
+        const Fq alx = load<FqCfg>(vk_mont), aly = load<FqCfg>(vk_mont + 32);
+        const uint4* sq = reinterpret_cast<const uint4*>(s0_std);
+        const uint4 lo = sq[0], hi = sq[1];
+        const uint32_t s0[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+        put_neg_g1(g1s + 64ull * n, mul_bits(alx, aly, s0, 256));
+        return;
+    }
     if (i >= n) return;
     const uint8_t* p = proofs + 256ull * i;
-    const Fq ax = ld_be(p), ay = ld_be(p + 32), cx = ld_be(p + 192), cy = ld_be(p + 224);
-    const Fq2 bx = {ld_be(p + 96), ld_be(p + 64)}, by = {ld_be(p + 160), ld_be(p + 128)};
-    const bool ok = on_curve(ax, ay, g1_b()) && on_curve(cx, cy, g1_b()) && on_curve(bx, by, g2_b());
-    if (!ok) atomicExch(bad, 1);  // the subgroup test of B runs beside the Miller loops
     uint32_t k[4];
     for (int w = 0; w < 4; ++w) {
         const uint8_t* q = rho + 32ull * i + 4 * w;
         k[w] = uint32_t(q[0]) | (uint32_t(q[1]) << 8) | (uint32_t(q[2]) << 16) | (uint32_t(q[3]) << 24);
     }
+    if (t & 1) {
+        const Fq cx = ld_be(p + 192), cy = ld_be(p + 224);
+        cacc[i] = mul_bits(cx, cy, k, 128);
+        return;
+    }
+    const Fq ax = ld_be(p), ay = ld_be(p + 32), cx = ld_be(p + 192), cy = ld_be(p + 224);
+    const Fq2 bx = {ld_be(p + 96), ld_be(p + 64)}, by = {ld_be(p + 160), ld_be(p + 128)};
+    const bool ok = on_curve(ax, ay, g1_b()) && on_curve(cx, cy, g1_b()) && on_curve(bx, by, g2_b());
+    if (!ok) atomicExch(bad, 1);  // the subgroup test of B runs beside the Miller loops
     const XYZZ<Fq> ra = mul_bits(ax, ay, k, 128);
     uint8_t* o1 = g1s + 64ull * i;
     if (ra.is_inf()) {
@@ -170,7 +199,6 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
     uint8_t* o2 = g2s + 128ull * i;
     st_std2(o2, bx);
     st_std2(o2 + 64, by);
-    cacc[i] = mul_bits(cx, cy, k, 128);
 }
 
 // Blocks [0, mb): one Miller loop per pair (raw Fq12 to scratch, as
@@ -221,16 +249,6 @@ __global__ void __launch_bounds__(64) miller_check_kernel(uint32_t n_pairs, cons
     if (m.is_inf() || !feq(fmul(px, m.ZZ), m.X) || !feq(fmul(py, m.ZZZ), m.Y)) atomicExch(bad, 1);
 }
 
-__device__ void put_neg_g1(uint8_t* o, const XYZZ<Fq>& p) {
-    if (p.is_inf()) {
-        for (int b = 0; b < 64; ++b) o[b] = 0;
-        return;
-    }
-    Fq x, y;
-    to_affine(p, x, y);
-    st_std(o, x);
-    st_std(o + 32, neg(y));
-}
 
 // Pairs n, n+1, n+2: (-(s_0) alpha, beta), (-L, gamma), (-sum rho_i C_i, delta).
 __global__ void finish_kernel(const XYZZ<Fq>* cacc, uint32_t n, const uint8_t* s0_std,
@@ -239,11 +257,8 @@ __global__ void finish_kernel(const XYZZ<Fq>* cacc, uint32_t n, const uint8_t* s
     if (threadIdx.x || blockIdx.x) return;
     XYZZ<Fq> cs = XYZZ<Fq>::inf();
     for (uint32_t i = 0; i < n; ++i) cs = xyzz_add(cs, cacc[i]);
-    const Fq alx = load<FqCfg>(vk_mont), aly = load<FqCfg>(vk_mont + 32);
-    const uint4* sq = reinterpret_cast<const uint4*>(s0_std);
-    const uint4 lo = sq[0], hi = sq[1];
-    const uint32_t s0[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
-    put_neg_g1(g1s + 64ull * n, mul_bits(alx, aly, s0, 256));
+    (void)s0_std;
+    (void)vk_mont;  // s0 * alpha (pair n) is written by points_kernel
     const Fq lx = load<FqCfg>(L_mont), ly = load<FqCfg>(L_mont + 32);
     uint8_t* ol = g1s + 64ull * (n + 1);
     if (lx.is_zero() && ly.is_zero()) {
@@ -290,7 +305,8 @@ int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_
     rho_kernel<<<grid(n, 64), 64, 0, s>>>(seed, n, rho);
     combine_kernel<<<grid(T + 1, 64), 64, 0, s>>>(pubs, rho, n, T, sc);
     if (msm_run(1, vk.ic_table, T + 1, sc, msm, L, s)) return -1;
-    points_kernel<<<grid(n, 32), 32, 0, s>>>(proofs, rho, n, g1s, g2s, cacc, bad);
+    points_kernel<<<grid(2ull * n + 1, 32), 32, 0, s>>>(proofs, rho, n, g1s, g2s, cacc, bad, sc,
+                                                        vk.alpha1_mont);
     finish_kernel<<<1, 32, 0, s>>>(cacc, n, sc, vk.alpha1_mont, L, vk.g2_std, g1s, g2s);
     const uint32_t mb = (n + 3 + 31) / 32;
     miller_check_kernel<<<mb + (n + 63) / 64, 64, 0, s>>>(n + 3, g1s, g2s, pscratch, mb, proofs,
