@@ -207,14 +207,14 @@ __global__ void points_kernel(const uint8_t* proofs, const uint8_t* rho, uint32_
 // BN254; psi = the untwist-Frobenius-twist map, the Miller loop's frob_twist)
 // -- a 127-bit scalar instead of r's 254 bits, run concurrently with the
 // Miller loops instead of before them.
-// Blocks [0, mb): 32 pairs per 64-thread CTA, Miller loops split over two
-// warps (miller_loop_2w). Blocks >= mb: the psi(B) = [6x^2]B subgroup checks.
-__global__ void __launch_bounds__(64) miller_check_kernel(uint32_t n_pairs, const uint8_t* g1s,
+// Blocks [0, mb): 32 pairs per 128-thread CTA, Miller loops split over four
+// warps (miller_loop_4w). Blocks >= mb: the psi(B) = [6x^2]B subgroup checks.
+__global__ void __launch_bounds__(128) miller_check_kernel(uint32_t n_pairs, const uint8_t* g1s,
                                                           const uint8_t* g2s, uint8_t* scratch,
                                                           uint32_t mb, const uint8_t* proofs,
                                                           uint32_t n, int* bad) {
     if (blockIdx.x < mb) {
-        __shared__ LinePair buf[2][32];
+        __shared__ MillerSmem sm;
         const uint32_t i = blockIdx.x * 32 + (threadIdx.x & 31);
         bool active = i < n_pairs;
         Fq xp = Fq::zero(), yp = Fq::zero();
@@ -232,12 +232,12 @@ __global__ void __launch_bounds__(64) miller_check_kernel(uint32_t n_pairs, cons
             xq = {to_mont(load<FqCfg>(q)), to_mont(load<FqCfg>(q + 32))};
             yq = {to_mont(load<FqCfg>(q + 64)), to_mont(load<FqCfg>(q + 96))};
         }
-        const Fq12 f = miller_loop_2w(xp, yp, xq, yq, active, buf);
+        const Fq12 f = miller_loop_4w(xp, yp, xq, yq, active, sm);
         if (threadIdx.x < 32 && i < n_pairs)  // degenerate pairs: f = 1
             *reinterpret_cast<Fq12*>(scratch + sizeof(Fq12) * i) = active ? f : f12_one();
         return;
     }
-    const uint32_t i = (blockIdx.x - mb) * 64 + threadIdx.x;
+    const uint32_t i = (blockIdx.x - mb) * 128 + threadIdx.x;
     if (i >= n) return;
     const uint8_t* pr = proofs + 256ull * i;
     const Fq2 bx = {ld_be(pr + 96), ld_be(pr + 64)}, by = {ld_be(pr + 160), ld_be(pr + 128)};
@@ -309,8 +309,8 @@ int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_
                                                         vk.alpha1_mont);
     finish_kernel<<<1, 32, 0, s>>>(cacc, n, sc, vk.alpha1_mont, L, vk.g2_std, g1s, g2s);
     const uint32_t mb = (n + 3 + 31) / 32;
-    miller_check_kernel<<<mb + (n + 63) / 64, 64, 0, s>>>(n + 3, g1s, g2s, pscratch, mb, proofs,
-                                                          n, bad);
+    miller_check_kernel<<<mb + (n + 127) / 128, 128, 0, s>>>(n + 3, g1s, g2s, pscratch, mb,
+                                                            proofs, n, bad);
     launch_pairing_finish(n + 3, pscratch, nullptr, d_ok, s);
     // d_ok &= !bad
     combine_ok(d_ok, bad, s);

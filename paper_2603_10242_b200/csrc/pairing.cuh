@@ -316,19 +316,47 @@ static __device__ __noinline__ Fq12 miller_loop(const Fq& xP, const Fq& yP, cons
     return f;
 }
 
-// The same Miller loop split over two warps of one CTA for up to 32 pairs:
-// warp 0 keeps f (squaring, then the sparse line products), warp 1 walks T
-// and produces the lines (dbl_step, add_step), handing them over in shared
-// memory double-buffered by iteration parity with one __syncthreads per
-// iteration — f's squaring overlaps T's doubling. Identical operations in
-// identical order as miller_loop, so f is bit-identical. All 64 threads must
-// call it (`active` = this lane holds a non-degenerate pair); the result is
-// valid in warp 0.
+// The Miller loop split over four warps of one CTA for up to 32 pairs (one
+// per lane): warp 3 walks T and produces the lines (dbl_step, add_step),
+// handing them over in shared memory double-buffered by iteration parity with
+// one __syncthreads per iteration, so T's doubling overlaps f's squaring;
+// warps 0-2 share f's squaring (two Fq6 products) and each line product (the
+// three parts of f12_mul_line) through shared memory and a named barrier
+// (bar.sync 1, 96). Same operations in the same order as miller_loop, so f
+// is bit-identical. All 128 threads call it; f is valid in warps 0-2.
 struct LinePair {
     Line d, a;
 };
-__device__ __forceinline__ Fq12 miller_loop_2w(const Fq& xP, const Fq& yP, const Fq2& xQ,
-                                               const Fq2& yQ, bool active, LinePair (*buf)[32]) {
+
+struct MillerSmem {
+    LinePair lines[2][32];
+    Fq6 xs[3][32];
+};
+__device__ __forceinline__ void f_bar() { asm volatile("bar.sync 1, 96;" ::: "memory"); }
+__device__ __forceinline__ Fq12 f12_sqr_3w(const Fq12& a, Fq6 (*xs)[32], int w, int lane,
+                                           bool active) {
+    if (active && w < 2)
+        xs[w][lane] = w == 0 ? f6_mul(a.c0, a.c1)
+                             : f6_mul(f6_add(a.c0, a.c1), f6_add(a.c0, f6_mul_v(a.c1)));
+    f_bar();
+    const Fq6 ab = xs[0][lane], t = xs[1][lane];
+    f_bar();
+    return {f6_sub(f6_sub(t, ab), f6_mul_v(ab)), f6_add(ab, ab)};
+}
+__device__ __forceinline__ Fq12 f12_mul_line_3w(const Fq12& f, const Line& l, Fq6 (*xs)[32], int w,
+                                                int lane, bool active) {
+    if (active) {
+        if (w == 0) xs[0][lane] = {fmul(f.c0.c0, l.l0), fmul(f.c0.c1, l.l0), fmul(f.c0.c2, l.l0)};
+        else if (w == 1) xs[1][lane] = f6_mul_01(f.c1, l.l1, l.l2);
+        else xs[2][lane] = f6_mul_01(f6_add(f.c0, f.c1), fadd(l.l0, l.l1), l.l2);
+    }
+    f_bar();
+    const Fq6 t0 = xs[0][lane], t1 = xs[1][lane], t2 = xs[2][lane];
+    f_bar();
+    return {f6_add(t0, f6_mul_v(t1)), f6_sub(f6_sub(t2, t0), t1)};
+}
+__device__ __forceinline__ Fq12 miller_loop_4w(const Fq& xP, const Fq& yP, const Fq2& xQ,
+                                               const Fq2& yQ, bool active, MillerSmem& sm) {
     const uint64_t loop_lo = 0x9d797039be763ba8ull;  // 6x+2 = 2^64 + loop_lo
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     Fq12 f = f12_one();
@@ -339,33 +367,32 @@ __device__ __forceinline__ Fq12 miller_loop_2w(const Fq& xP, const Fq& yP, const
     for (int i = 63; i >= 0; --i) {
         const int par = i & 1;
         const bool bit = (loop_lo >> i) & 1;
-        if (active) {
-            if (w == 1) {
-                buf[par][lane].d = dbl_step(T, xP, yP);
-                if (bit) buf[par][lane].a = add_step(T, xQ, yQ, xP, yP);
-            } else {
-                f = f12_sqr(f);
+        if (w == 3) {
+            if (active) {
+                sm.lines[par][lane].d = dbl_step(T, xP, yP);
+                if (bit) sm.lines[par][lane].a = add_step(T, xQ, yQ, xP, yP);
             }
+        } else {
+            f = f12_sqr_3w(f, sm.xs, w, lane, active);
         }
         __syncthreads();
-        if (active && w == 0) {
-            f = f12_mul_line(f, buf[par][lane].d);
-            if (bit) f = f12_mul_line(f, buf[par][lane].a);
+        if (w < 3) {
+            f = f12_mul_line_3w(f, sm.lines[par][lane].d, sm.xs, w, lane, active);
+            if (bit) f = f12_mul_line_3w(f, sm.lines[par][lane].a, sm.xs, w, lane, active);
         }
     }
-    // buf[1] was last read before the i = 0 barrier: free for the tail
-    if (active && w == 1) {
+    if (w == 3 && active) {  // lines[1] was last read before the i = 0 barrier
         Fq2 x1 = xQ, y1 = yQ;
         frob_twist(x1, y1);
         Fq2 x2 = x1, y2 = y1;
         frob_twist(x2, y2);
-        buf[1][lane].d = add_step(T, x1, y1, xP, yP);
-        buf[1][lane].a = add_step(T, x2, f2_neg(y2), xP, yP);
+        sm.lines[1][lane].d = add_step(T, x1, y1, xP, yP);
+        sm.lines[1][lane].a = add_step(T, x2, f2_neg(y2), xP, yP);
     }
     __syncthreads();
-    if (active && w == 0) {
-        f = f12_mul_line(f, buf[1][lane].d);
-        f = f12_mul_line(f, buf[1][lane].a);
+    if (w < 3) {
+        f = f12_mul_line_3w(f, sm.lines[1][lane].d, sm.xs, w, lane, active);
+        f = f12_mul_line_3w(f, sm.lines[1][lane].a, sm.xs, w, lane, active);
     }
     return f;
 }
