@@ -11,7 +11,8 @@
 //   1. count     : signed digits of each scalar -> bucket histogram (atomics)
 //   2. scan      : exclusive prefix sum -> bucket offsets
 //   3. scatter   : (window*n + i | sign) into bucket order
-//   4. accumulate: each thread mixed-adds kMsmSeg consecutive sorted entries
+//   4. accumulate: each thread mixed-adds kMsmSeg (fewer for small MSMs)
+//                  consecutive sorted entries
 //                  (XYZZ, 8M + 2S, lazy-reduced Y); a bucket wholly inside
 //                  the segment is written directly, the first/last runs that
 //                  cross a segment edge go to two partial slots
@@ -23,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cub/device/device_scan.cuh>
+#include <algorithm>
 #include <cstdlib>
 
 #include "curve.cuh"
@@ -189,7 +191,7 @@ __device__ __forceinline__ void store_inf(uint8_t* p) {
     store_xyzz(p, XYZZ<F>::inf());
 }
 
-// One thread per segment of kMsmSeg consecutive sorted entries. Runs of one
+// One thread per segment of segsz consecutive sorted entries. Runs of one
 // bucket: a run that is the whole bucket is stored to buckets[b]; a run cut
 // by the segment edge is stored to partials[2 seg] (first run of the
 // segment) or partials[2 seg + 1] (a later run).
@@ -198,13 +200,13 @@ __global__ void __launch_bounds__(128, Lay<F>::ACC_MIN_CTAS) accumulate_kernel(c
                                                          const uint32_t* sorted,
                                                          const uint32_t* offs,
                                                          uint8_t* buckets,
-                                                         uint8_t* partials) {
+                                                         uint8_t* partials, uint32_t segsz) {
     const uint32_t seg = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t total = offs[kMsmBuckets];
-    const uint32_t p0 = seg * kMsmSeg;
+    const uint32_t p0 = seg * segsz;
     if (p0 >= total) return;
     constexpr int A = Lay<F>::AFF, X = Lay<F>::XZ;
-    const uint32_t p1 = min(total, p0 + kMsmSeg);
+    const uint32_t p1 = min(total, p0 + segsz);
     int b = bucket_of(offs, p0);
     uint32_t bs = offs[b], be = offs[b + 1];
     int slot = 0;
@@ -287,7 +289,8 @@ constexpr uint32_t kHeavySpan = 64;  // segments; longer buckets go to heavy_ker
 // 0/1 values) are queued for heavy_kernel instead of one serial thread.
 template <class F>
 __global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const uint8_t* partials,
-                                                    uint8_t* buckets, uint32_t* heavy) {
+                                                    uint8_t* buckets, uint32_t* heavy,
+                                                    uint32_t segsz) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= kMsmBuckets) return;
     constexpr int X = Lay<F>::XZ;
@@ -296,13 +299,13 @@ __global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const 
         store_inf<F>(buckets + (uint64_t)X * b);
         return;
     }
-    const uint32_t s0 = s / kMsmSeg, s1 = (e - 1) / kMsmSeg;
+    const uint32_t s0 = s / segsz, s1 = (e - 1) / segsz;
     if (s0 == s1) return;
     if (s1 - s0 > kHeavySpan) {
         heavy[1 + atomicAdd(&heavy[0], 1u)] = b;
         return;
     }
-    XYZZ<F> acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * kMsmSeg ? 0 : 1)));
+    XYZZ<F> acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * segsz ? 0 : 1)));
     for (uint32_t sg = s0 + 1; sg <= s1; ++sg)
         acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg)));
     store_xyzz(buckets + (uint64_t)X * b, acc);
@@ -312,16 +315,17 @@ __global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const 
 // segment partials, then a CTA tree.
 template <class F>
 __global__ void __launch_bounds__(128) heavy_kernel(const uint32_t* offs, const uint8_t* partials,
-                                                    uint8_t* buckets, const uint32_t* heavy) {
+                                                    uint8_t* buckets, const uint32_t* heavy,
+                                                    uint32_t segsz) {
     constexpr int X = Lay<F>::XZ;
     const uint32_t nh = heavy[0];
     for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
         const int b = heavy[1 + h];
         const uint32_t s = offs[b], e = offs[b + 1];
-        const uint32_t s0 = s / kMsmSeg, s1 = (e - 1) / kMsmSeg;
+        const uint32_t s0 = s / segsz, s1 = (e - 1) / segsz;
         XYZZ<F> acc = XYZZ<F>::inf();
         if (threadIdx.x == 0)
-            acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * kMsmSeg ? 0 : 1)));
+            acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * segsz ? 0 : 1)));
         for (uint32_t sg = s0 + 1 + threadIdx.x; sg <= s1; sg += blockDim.x)
             acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg)));
         acc = cta_sum128(acc);
@@ -590,19 +594,26 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
           cudaStream_t s) {
     constexpr int X = Lay<F>::XZ;
     const uint64_t cap = (uint64_t)kMsmWindows * n;
-    const uint64_t nseg = (cap + kMsmSeg - 1) / kMsmSeg;
-    if (sc.cap_entries < cap || !sc.hist) {
+    // segment length: kMsmSeg, shorter for small MSMs (>= ~19k threads, so a
+    // verifier-size MSM is not a few hundred threads of 64 serial adds)
+    uint32_t segsz = kMsmSeg;
+    while (segsz > 4 && cap / segsz < 148ull * 128) segsz >>= 1;
+    const uint64_t nseg = (cap + segsz - 1) / segsz;
+    if (sc.cap_entries < cap || sc.cap_segs < nseg || !sc.hist) {
+        const uint64_t keep = std::max<uint64_t>(cap, sc.cap_entries);
+        const uint64_t keep_segs = std::max<uint64_t>(nseg, sc.cap_segs);
         sc.release();
         if (cudaMalloc(&sc.hist, 4 * (kMsmBuckets + 1)) || cudaMalloc(&sc.offs, 4 * (kMsmBuckets + 1)) ||
-            cudaMalloc(&sc.cursor, 4 * kMsmBuckets) || cudaMalloc(&sc.sorted, 4 * cap) ||
-            cudaMalloc(&sc.partials, (size_t)256 * 2 * nseg) ||
+            cudaMalloc(&sc.cursor, 4 * kMsmBuckets) || cudaMalloc(&sc.sorted, 4 * keep) ||
+            cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||
             cudaMalloc(&sc.buckets, (size_t)256 * kMsmBuckets) ||
             cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128)) ||
             cudaMalloc(&sc.heavy, 4 * (kMsmBuckets + 1)))
             return -1;
         cub::DeviceScan::ExclusiveSum(nullptr, sc.scan_bytes, sc.hist, sc.offs, kMsmBuckets + 1, s);
         if (cudaMalloc(&sc.scan_tmp, sc.scan_bytes)) return -1;
-        sc.cap_entries = cap;
+        sc.cap_entries = keep;
+        sc.cap_segs = keep_segs;
     }
     cudaMemsetAsync(sc.hist, 0, 4 * (kMsmBuckets + 1), s);
     cudaMemsetAsync(sc.heavy, 0, 4, s);
@@ -662,10 +673,10 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
         affine_heavy_kernel<<<148, 128, 0, s>>>(in_pts, in_offs, sc.buckets, sc.heavy);
     } else {
         accumulate_kernel<F><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
-            table, sc.sorted, sc.offs, sc.buckets, sc.partials);
+            table, sc.sorted, sc.offs, sc.buckets, sc.partials, segsz);
         fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets,
-                                                          sc.heavy);
-        heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy);
+                                                          sc.heavy, segsz);
+        heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy, segsz);
     }
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
     static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
@@ -684,6 +695,7 @@ void MsmScratch::release() {
     aff_pts[0] = aff_pts[1] = nullptr;
     aff_offs[0] = aff_offs[1] = aff_cnt = nullptr;
     aff_cap = 0;
+    cap_segs = 0;
     hist = offs = cursor = sorted = heavy = nullptr;
     partials = buckets = segsum = nullptr;
     scan_tmp = nullptr;

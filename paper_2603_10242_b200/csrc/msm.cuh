@@ -37,6 +37,7 @@ struct MsmScratch {
     uint64_t aff_cap = 0;
     size_t scan_bytes = 0;
     size_t cap_entries = 0;
+    uint64_t cap_segs = 0;         // accumulation segments the partials hold
     void release();
 };
 
