@@ -64,9 +64,10 @@ __global__ void product_final_kernel(uint32_t n, uint8_t* scratch, uint8_t* out3
         }
         __syncthreads();
     }
-    // all threads: the final exponentiation runs on three warps
-    __shared__ Fq6 sm[3];
-    const Fq12 f = final_exp_3w(n ? get_raw(scratch) : f12_one(), sm);
+    // the final exponentiation on warp 0, lane-parallel products
+    if (threadIdx.x >= 32) return;
+    __shared__ WarpProducts ws;
+    const Fq12 f = final_exp_warp(n ? get_raw(scratch) : f12_one(), ws);
     if (threadIdx.x) return;
     if (out384) store_f12(out384, f);
     if (is_one) *is_one = f12_is_one(f) ? 1 : 0;

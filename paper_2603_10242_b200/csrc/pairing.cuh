@@ -427,79 +427,108 @@ static __device__ __noinline__ Fq12 final_exp(const Fq12& in) {
 }
 
 
-// ---- the final exponentiation on three warps --------------------------------
-// Lane 0 of warps 0-2 each take one of the three independent Fq6 products of
-// an Fq12 product (Karatsuba) or one of the three Fq4 squarings of a
-// cyclotomic squaring; partial results meet in shared memory. Every thread of
-// the CTA (>= 96) calls these; the results are replicated in all threads.
-// Same operations as the one-thread versions -> bit-identical.
-__device__ __forceinline__ Fq12 f12_mul_3w(const Fq12& a, const Fq12& b, Fq6* sm) {
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0 && w < 3) {
-        const Fq6 x = w == 0 ? a.c0 : w == 1 ? a.c1 : f6_add(a.c0, a.c1);
-        const Fq6 y = w == 0 ? b.c0 : w == 1 ? b.c1 : f6_add(b.c0, b.c1);
-        sm[w] = f6_mul(x, y);
+// ---- the final exponentiation on one warp, lane-parallel --------------------
+// All 32 lanes hold the operands; lanes 0-17 each compute ONE of the 18 Fq2
+// products of an Fq12 product (3 Karatsuba Fq6 products x 6 Fq2 products),
+// or lanes 0-5 the 6 products of a cyclotomic squaring — the same product
+// code on different data, so an Fq12 product costs one Fq2 product of
+// latency. Products meet in a per-warp shared buffer; every lane then forms
+// the (exact, order-independent) sums. Bit-identical to the serial forms.
+struct WarpProducts {
+    Fq2 p[32];
+};
+__device__ __forceinline__ Fq6 f6_from_products(const Fq2* p) {
+    const Fq2 t0 = p[0], t1 = p[1], t2 = p[2];
+    return {fadd(t0, f2_mul_xi(fsub(fsub(p[3], t1), t2))), fadd(fsub(fsub(p[4], t0), t1), f2_mul_xi(t2)),
+            fadd(fsub(fsub(p[5], t0), t2), t1)};
+}
+static __device__ __noinline__ Fq12 f12_mul_warp(const Fq12& a, const Fq12& b, WarpProducts& ws) {
+    const int lane = threadIdx.x & 31;
+    const int which = lane < 18 ? lane / 6 : 0, j = lane % 6;
+    const Fq6 x6 = which == 0 ? a.c0 : which == 1 ? a.c1 : f6_add(a.c0, a.c1);
+    const Fq6 y6 = which == 0 ? b.c0 : which == 1 ? b.c1 : f6_add(b.c0, b.c1);
+    Fq2 x, y;
+    if (j < 3) {
+        x = j == 0 ? x6.c0 : j == 1 ? x6.c1 : x6.c2;
+        y = j == 0 ? y6.c0 : j == 1 ? y6.c1 : y6.c2;
+    } else if (j == 3) {
+        x = fadd(x6.c1, x6.c2);
+        y = fadd(y6.c1, y6.c2);
+    } else if (j == 4) {
+        x = fadd(x6.c0, x6.c1);
+        y = fadd(y6.c0, y6.c1);
+    } else {
+        x = fadd(x6.c0, x6.c2);
+        y = fadd(y6.c0, y6.c2);
     }
-    __syncthreads();
-    const Fq6 t0 = sm[0], t1 = sm[1], t2 = sm[2];
-    __syncthreads();
+    const Fq2 pr = fmul(x, y);
+    if (lane < 18) ws.p[lane] = pr;
+    __syncwarp();
+    const Fq6 t0 = f6_from_products(ws.p), t1 = f6_from_products(ws.p + 6),
+              t2 = f6_from_products(ws.p + 12);
+    __syncwarp();
     return {f6_add(t0, f6_mul_v(t1)), f6_sub(f6_sub(t2, t0), t1)};
 }
-__device__ __forceinline__ Fq12 f12_cyc_sqr_3w(const Fq12& a, Fq6* sm6) {
-    Fq2* sm = reinterpret_cast<Fq2*>(sm6);
-    const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0 && w < 3) {
-        const Fq2 x = w == 0 ? a.c0.c0 : w == 1 ? a.c1.c0 : a.c0.c1;
-        const Fq2 y = w == 0 ? a.c1.c1 : w == 1 ? a.c0.c2 : a.c1.c2;
-        const Fq2 xy = fmul(x, y);  // (x + y t)^2, t^2 = xi
-        sm[2 * w] = fsub(fsub(fmul(fadd(x, y), fadd(x, f2_mul_xi(y))), xy), f2_mul_xi(xy));
-        sm[2 * w + 1] = fadd(xy, xy);
+static __device__ __noinline__ Fq12 f12_cyc_sqr_warp(const Fq12& a, WarpProducts& ws) {
+    const int lane = threadIdx.x & 31;
+    const int w = lane < 6 ? lane >> 1 : 0;
+    const Fq2 x = w == 0 ? a.c0.c0 : w == 1 ? a.c1.c0 : a.c0.c1;
+    const Fq2 y = w == 0 ? a.c1.c1 : w == 1 ? a.c0.c2 : a.c1.c2;
+    const Fq2 pr = (lane & 1) ? fmul(fadd(x, y), fadd(x, f2_mul_xi(y))) : fmul(x, y);
+    if (lane < 6) ws.p[lane] = pr;
+    __syncwarp();
+    Fq2 t[6];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {  // (x + y t)^2 = ((x+y)(x+xi y) - xy - xi xy) + 2xy t
+        const Fq2 xy = ws.p[2 * k];
+        t[2 * k] = fsub(fsub(ws.p[2 * k + 1], xy), f2_mul_xi(xy));
+        t[2 * k + 1] = fadd(xy, xy);
     }
-    __syncthreads();
-    const Fq2 t0 = sm[0], t1 = sm[1], t2 = sm[2], t3 = sm[3], t4 = sm[4], t5 = sm[5];
-    __syncthreads();
-    auto tw = [](const Fq2& t, const Fq2& z, bool plus) {  // 3t -+ 2z
-        const Fq2 d = plus ? fadd(t, z) : fsub(t, z);
-        return fadd(fadd(d, d), t);
+    __syncwarp();
+    auto tw = [](const Fq2& tt, const Fq2& z, bool plus) {  // 3t -+ 2z
+        const Fq2 d = plus ? fadd(tt, z) : fsub(tt, z);
+        return fadd(fadd(d, d), tt);
     };
     Fq12 r;
-    r.c0.c0 = tw(t0, a.c0.c0, false);
-    r.c1.c1 = tw(t1, a.c1.c1, true);
-    r.c1.c0 = tw(f2_mul_xi(t5), a.c1.c0, true);
-    r.c0.c2 = tw(t4, a.c0.c2, false);
-    r.c0.c1 = tw(t2, a.c0.c1, false);
-    r.c1.c2 = tw(t3, a.c1.c2, true);
+    r.c0.c0 = tw(t[0], a.c0.c0, false);
+    r.c1.c1 = tw(t[1], a.c1.c1, true);
+    r.c1.c0 = tw(f2_mul_xi(t[5]), a.c1.c0, true);
+    r.c0.c2 = tw(t[4], a.c0.c2, false);
+    r.c0.c1 = tw(t[2], a.c0.c1, false);
+    r.c1.c2 = tw(t[3], a.c1.c2, true);
     return r;
 }
-__device__ __forceinline__ Fq12 f12_pow_x_3w(const Fq12& a, Fq6* sm) {
+__device__ __forceinline__ Fq12 f12_pow_x_warp(const Fq12& a, WarpProducts& ws) {
     const uint64_t x = 4965661367192848881ull;
     Fq12 r = f12_one();
     for (int i = 62; i >= 0; --i) {
-        r = f12_cyc_sqr_3w(r, sm);
-        if ((x >> i) & 1) r = f12_mul_3w(r, a, sm);
+        r = f12_cyc_sqr_warp(r, ws);
+        if ((x >> i) & 1) r = f12_mul_warp(r, a, ws);
     }
     return r;
 }
-static __device__ __noinline__ Fq12 final_exp_3w(const Fq12& in, Fq6* sm) {
-    Fq12 t1 = f12_mul_3w(f12_conj(in), f12_inv(in), sm);  // ^(p^6 - 1)
-    t1 = f12_mul_3w(t1, f12_frob(t1, 2), sm);             // ^(p^2 + 1)
+// Every lane of ONE warp calls it; the result is replicated in all lanes.
+static __device__ __noinline__ Fq12 final_exp_warp(const Fq12& in, WarpProducts& ws) {
+    Fq12 t1 = f12_mul_warp(f12_conj(in), f12_inv(in), ws);  // ^(p^6 - 1)
+    t1 = f12_mul_warp(t1, f12_frob(t1, 2), ws);             // ^(p^2 + 1)
     const Fq12 fp = f12_frob(t1, 1), fp2 = f12_frob(t1, 2), fp3 = f12_frob(fp2, 1);
-    const Fq12 fu = f12_pow_x_3w(t1, sm), fu2 = f12_pow_x_3w(fu, sm), fu3 = f12_pow_x_3w(fu2, sm);
+    const Fq12 fu = f12_pow_x_warp(t1, ws), fu2 = f12_pow_x_warp(fu, ws),
+               fu3 = f12_pow_x_warp(fu2, ws);
     Fq12 y3 = f12_frob(fu, 1);
     const Fq12 fu2p = f12_frob(fu2, 1), fu3p = f12_frob(fu3, 1), y2 = f12_frob(fu2, 2);
-    const Fq12 y0 = f12_mul_3w(f12_mul_3w(fp, fp2, sm), fp3, sm);
+    const Fq12 y0 = f12_mul_warp(f12_mul_warp(fp, fp2, ws), fp3, ws);
     const Fq12 y1 = f12_conj(t1);
     const Fq12 y5 = f12_conj(fu2);
     y3 = f12_conj(y3);
-    const Fq12 y4 = f12_conj(f12_mul_3w(fu, fu2p, sm));
-    const Fq12 y6 = f12_conj(f12_mul_3w(fu3, fu3p, sm));
-    Fq12 t0 = f12_mul_3w(f12_mul_3w(f12_cyc_sqr_3w(y6, sm), y4, sm), y5, sm);
-    Fq12 u1 = f12_mul_3w(f12_mul_3w(y3, y5, sm), t0, sm);
-    t0 = f12_mul_3w(t0, y2, sm);
-    u1 = f12_cyc_sqr_3w(f12_mul_3w(f12_cyc_sqr_3w(u1, sm), t0, sm), sm);
-    t0 = f12_mul_3w(u1, y1, sm);
-    u1 = f12_mul_3w(u1, y0, sm);
-    return f12_mul_3w(f12_cyc_sqr_3w(t0, sm), u1, sm);
+    const Fq12 y4 = f12_conj(f12_mul_warp(fu, fu2p, ws));
+    const Fq12 y6 = f12_conj(f12_mul_warp(fu3, fu3p, ws));
+    Fq12 t0 = f12_mul_warp(f12_mul_warp(f12_cyc_sqr_warp(y6, ws), y4, ws), y5, ws);
+    Fq12 u1 = f12_mul_warp(f12_mul_warp(y3, y5, ws), t0, ws);
+    t0 = f12_mul_warp(t0, y2, ws);
+    u1 = f12_cyc_sqr_warp(f12_mul_warp(f12_cyc_sqr_warp(u1, ws), t0, ws), ws);
+    t0 = f12_mul_warp(u1, y1, ws);
+    u1 = f12_mul_warp(u1, y0, ws);
+    return f12_mul_warp(f12_cyc_sqr_warp(t0, ws), u1, ws);
 }
 
 }  // namespace bn
