@@ -1214,7 +1214,10 @@ int combine_impl(acegpu_ctx* c, cudaStream_t s, const uint8_t* roots289, const u
 // attestation and REV-index slices of 2^kSegLog-tx segments are copied on a
 // copy stream while the leaf kernel of earlier segments runs on the compute
 // stream; the tree levels and the FC then follow as in block_pipeline.
-constexpr uint32_t kSegLog = 14;
+#ifndef ACEGPU_SEG_LOG
+#define ACEGPU_SEG_LOG 14  // 100k e2e (tools/e2e_probe.py): 2^13 1.20 ms, 2^14 1.08, 2^15 1.12
+#endif
+constexpr uint32_t kSegLog = ACEGPU_SEG_LOG;
 constexpr int kLeafStreams = 8;
 
 int ensure_copy(acegpu_ctx* c, size_t nev) {
