@@ -621,9 +621,9 @@ def bench_groth16(ctx, dev: int, fq_rate: float, chunks: int = 16, reps: int = 3
     V, Np = pk.variables, 1 << pk.log_domain
     Vp = V - 1 - T
     W = bn254.msm_params(ctx)[1]
-    madds = W * ((V + 2) * 2 + Vp + 1 + (Np - 1))  # G1 MSMs: A, B1, L, H
+    madds = W * ((V + 2) * 2 + Vp + 1 + Np)  # G1 MSMs: A, B1, L, H (coset-Lagrange, N points)
     fq_muls = madds * 10 + W * (V + 2) * 10 * 3     # + G2 (Fq2 mul = 3 Fq muls)
-    fr_muls = 7 * ((Np // 2) * pk.log_domain + Np)
+    fr_muls = 6 * ((Np // 2) * pk.log_domain + Np)  # 3 iNTT + 3 coset NTT
     pk.close()
     return {"txs_per_chunk": T, "constraints_per_tx": K, "constraints": pk.constraints,
             "domain": Np, "setup_s_once": setup_s, "chunk_prove_ms": chunk_ms,

@@ -2003,13 +2003,14 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     CK(cudaEventCreateWithFlags(&g->ev_scaled, cudaEventDisableTiming));
     {
         // stream priorities (ACEGPU_G16_PRIO: which of ab / h / bl run at the
-        // highest priority; "none" = all equal). Measured (chunk, ms): bl 49.75,
-        // none 49.7-50.1, ab 50.3, ab+bl 50.5, ab+h 52.1, h 52.9, NTTs on top
-        // ("n", "nbl", "nab") 51.5-52.7 -> the longest MSM (G2, B2) first.
+        // highest priority; "none" = all equal). Measured (chunk, ms) with
+        // the coset-Lagrange H (6 NTTs): ab 49.35, ab+bl 49.56, bl 50.1,
+        // none 51.6; with 7 NTTs bl had led (49.75 vs ab 50.3): the stream
+        // balance shifts with the H stream's length.
         int least = 0, greatest = 0;
         CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         const char* e = std::getenv("ACEGPU_G16_PRIO");
-        const std::string pr = e ? e : "bl";
+        const std::string pr = e ? e : "ab";
         auto prio = [&](const char* k) { return pr.find(k) != std::string::npos ? greatest : least; };
         // "n": the H-polynomial NTTs on their own top-priority stream (the H
         // MSM then waits for them on s_h) with the others one level below
@@ -2035,7 +2036,7 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
         return fail(ACEGPU_ECUDA, "g16 setup alloc");
     bn::g16_lagrange(g->consts, m, L, s);
     bn::g16_query_scalars(g->d, L, g->consts, g->cc, part, su, sv, sl, s);
-    bn::g16_h_scalars(g->consts, N - 1, hs, s);
+    bn::g16_h_scalars(g->consts, N, hs, s);  // coset-Lagrange H bases (groth16.cu)
     // generators (Montgomery affine) and the extra bases alpha1 beta1 delta1 | beta2 delta2
     uint8_t hgen[192] = {0};
     hgen[0] = 1;
@@ -2074,8 +2075,8 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     CK(cudaMemcpyAsync(pts + 64 * g->Vp, ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
     RET(bases_from_device(c->device, 1, pts, g->Vp + 1, s, &g->ql));
     // H: [tau^j Z(tau)/delta]1, j < N-1
-    bn::launch_scalar_muls(1, gens, hs, N - 1, pts, s);
-    RET(bases_from_device(c->device, 1, pts, N - 1, s, &g->qh));
+    bn::launch_scalar_muls(1, gens, hs, N, pts, s);
+    RET(bases_from_device(c->device, 1, pts, N, s, &g->qh));
     // verifying key (the Groth16 verifier, g16_verify.cu)
     if (dm(&g->vk_alpha1, 64) || dm(&g->vk_g2_std, 384) || dm(&g->vk_ic, 64ull * (T + 1)))
         return fail(ACEGPU_ECUDA, "g16 vk alloc");
@@ -2183,13 +2184,14 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
     }
     bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
-    if (bn::ntt_run(t, g->ea, g->ea, scratch, 1, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset intt");
-    bn::launch_fr_convert(g->ea, N, 0, sn);  // h coefficients -> standard form scalars
+    // H(g w^j) are the MSM scalars as they stand (Lagrange-coset H bases): no
+    // coset iNTT back to coefficients
+    bn::launch_fr_convert(g->ea, N, 0, sn);  // -> standard form scalars
     tr.mark("ntt", sn);
     CKL();
     CK(cudaEventRecord(g->ev_n, sn));
     CK(cudaStreamWaitEvent(sh, g->ev_n, 0));
-    if (bn::msm_run(1, g->qh->table, N - 1, g->ea, g->msm_h, g->pts + 320, sh))
+    if (bn::msm_run(1, g->qh->table, N, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
@@ -2223,7 +2225,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CK(cudaEventRecord(sl.done, s));
     tr.mark("assemble", s);
     tr.dump();
-    c->launches += 17 + 5 * bn::kMsmKernels + 6;
+    c->launches += 15 + 5 * bn::kMsmKernels + 6;
     return ACEGPU_OK;
 }
 }  // namespace

@@ -63,7 +63,8 @@ __global__ void chain_consts_kernel(uint32_t K, uint8_t* out) {
 
 // Scalars of the setup (Montgomery): [0] tau [1] alpha [2] beta [3] gamma
 // [4] delta (inputs, standard form, converted here) -> [5] omega_N,
-// [6] Z(tau)/N, [7] Z(tau)/delta, [8] 1/delta, [9] (g^N - 1)^-1, [10] Z(tau).
+// [6] Z(tau)/N, [7] Z(tau)/delta, [8] 1/delta, [9] (g^N - 1)^-1, [10] Z(tau),
+// [11] (tau^N - g^N) / (N g^N) * Z(tau)/delta (the coset-Lagrange H bases).
 __global__ void setup_consts_kernel(uint8_t* c, uint32_t logn) {
     if (threadIdx.x || blockIdx.x) return;
     for (int i = 0; i < 5; ++i) str(c + 32 * i, to_mont(ldr(c + 32 * i)));
@@ -91,8 +92,11 @@ __global__ void setup_consts_kernel(uint8_t* c, uint32_t logn) {
     str(c + 32 * 6, mul(Z, ninv));
     str(c + 32 * 7, mul(Z, dinv));
     str(c + 32 * 8, dinv);
-    str(c + 32 * 9, inv_fast(sub(pow(five, en), Fr::one())));
+    const Fr gN = pow(five, en);
+    str(c + 32 * 9, inv_fast(sub(gN, Fr::one())));
     str(c + 32 * 10, Z);
+    const Fr tauN = add(Z, Fr::one());
+    str(c + 32 * 11, mul(mul(sub(tauN, gN), inv_fast(mul(to_mont(n), gN))), mul(Z, dinv)));
 }
 
 // L_j(tau) = Z(tau)/N * w^j / (tau - w^j), j < m (Montgomery).
@@ -197,15 +201,24 @@ __global__ void ic_scalars_kernel(uint32_t T, const uint8_t* c, const uint8_t* s
 }
 
 // H-query scalars: tau^j Z(tau)/delta for j < n (standard form).
+// H bases in the Lagrange basis of the coset g<omega> (g = 5), so the MSM
+// takes the coset evaluations H(g w^j) straight from the pointwise division
+// (no coset iNTT): [H(tau) Z(tau)/delta] = sum_j H(g w^j) L^g_j(tau) Z(tau)/delta,
+// L^g_j(tau) = (tau^N - g^N) g w^j / (N g^N (tau - g w^j)). Scalar j (j < N,
+// standard form) = c[11] * x_j / (tau - x_j), x_j = g w^j.
 __global__ void h_scalars_kernel(const uint8_t* c, uint64_t n, uint8_t* out) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= n) return;
-    Fr x = ldr(c + 32 * 7), b = ldr(c);
+    const Fr tau = ldr(c), w = ldr(c + 32 * 5), k = ldr(c + 32 * 11);
+    Fr xj = Fr::one(), b = w;
     for (uint64_t e = j; e; e >>= 1) {
-        if (e & 1) x = mul(x, b);
+        if (e & 1) xj = mul(xj, b);
         b = sqr(b);
     }
-    str(out + 32 * j, from_mont(x));
+    Fr five = Fr::zero();
+    five.v[0] = 5;
+    xj = mul(xj, to_mont(five));
+    str(out + 32 * j, from_mont(mul(mul(k, xj), inv_fast(sub(tau, xj)))));
 }
 
 // Witness + row evaluations. One thread per tx: the chain is sequential.
