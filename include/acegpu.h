@@ -251,11 +251,18 @@ int acegpu_bn_msm_run_dev(acegpu_ctx* ctx, void* stream, const acegpu_msm_bases*
  * Fr), proving-key MSM tables resident on the device. prove: per-tx private
  * witness w (n x 32-B LE, reduced mod r; the attest key, prover.cpp:181-188)
  * and public input pub (LE(public_inputs_digest) mod r, prover.cpp:74-76);
- * rs = r | s (standard form) or NULL to derive them deterministically
- * (SHA-256 of the chunk's public inputs). Output: the 256-B proof
- * A(64) | B(128) | C(64) big-endian (EIP-197, G2 as c1|c0), the raw affine
- * points little-endian (A x,y | B x.c0,x.c1,y.c0,y.c1 | C x,y) and the chunk
- * digest SHA-256("ace-g16-chunk-v1" | pub_0 | pub_{T-1} | T_be32). */
+ * rs = r | s (standard form) or NULL to derive them deterministically from
+ * the witnesses and the public inputs (binding v2, groth16.cu):
+ *   D(x) = SHA-256(tag16 | SHA-256(x_0..x_31) | SHA-256(x_32..x_63) | ... | T_be32)
+ *   (32-input blocks of the T 32-B inputs, the last block short; tag16 =
+ *   "ace-g16-pubs-v2:" / "ace-g16-wits-v2:"),
+ *   r = LE(SHA-256("ace-g16-r-v2" | D(w) | D(pub))) mod r, s likewise with
+ *   "ace-g16-s-v2" (RFC 6979 style: secret, yet reproducible by a backup
+ *   prover holding the witnesses).
+ * Output: the 256-B proof A(64) | B(128) | C(64) big-endian (EIP-197, G2 as
+ * c1|c0), the raw affine points little-endian (A x,y | B x.c0,x.c1,y.c0,y.c1 |
+ * C x,y) and the chunk digest SHA-256("ace-g16-chunk-v2" | D(pub)), which
+ * commits to every public input of the chunk. */
 typedef struct acegpu_g16 acegpu_g16;
 int acegpu_g16_setup(acegpu_ctx* ctx, uint32_t txs_per_chunk, uint32_t constraints_per_tx,
                      const uint8_t* trapdoor5, acegpu_g16** out);
@@ -279,9 +286,16 @@ int acegpu_g16_vk(acegpu_ctx* ctx, const acegpu_g16* g, uint8_t* out);
  * digests; reduced mod r). *ok = 1 iff every proof satisfies
  * e(A,B) = e(alpha,beta) e(sum z_j IC_j, gamma) e(C,delta) with its points on
  * the curves and B in the order-r subgroup (one random-linear-combination
- * check: n + 3 Miller loops, one final exponentiation, one MSM over IC). */
+ * check: n + 3 Miller loops, one final exponentiation, one MSM over IC).
+ * The 128-bit weights rho_i = LE(SHA-256("ace-g16-batch-v2" | seed | i_be32))[0:16]
+ * come from seed = SHA-256("ace-g16-seed-v2:" | SHA-256(acegpu_g16_vk export) |
+ * SHA-256(proof_0) | D(pub_0) | ... | SHA-256(proof_{n-1}) | D(pub_{n-1})): they
+ * commit to the key, every proof and every public input, so no input can be
+ * adjusted after the weights are known. _seed also returns the seed (32 B). */
 int acegpu_g16_verify_batch(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* proofs256,
                             const uint8_t* pubs, uint64_t n, int* ok);
+int acegpu_g16_verify_batch_seed(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* proofs256,
+                                 const uint8_t* pubs, uint64_t n, int* ok, uint8_t* seed32);
 
 /* verify_finality_certificate in Groth16 mode (prover.cpp:158-169 with real
  * proofs): *result = 0 Valid, 1 SlotMismatch, 2

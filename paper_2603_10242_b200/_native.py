@@ -11,7 +11,8 @@ import threading
 
 import numpy as np
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libacegpu.so")
+LIB_PATH = os.environ.get("ACEGPU_LIB") or os.path.join(
+    os.path.dirname(os.path.abspath(__file__)), "lib", "libacegpu.so")  # ACEGPU_LIB: A/B probes
 
 OK, EINVAL, ECUDA, ENODEV = 0, -1, -2, -3
 
@@ -82,6 +83,8 @@ _SIGS = {
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_vk": (C.c_int, [ctxp, C.c_void_p, vp]),
     "acegpu_g16_verify_batch": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int)]),
+    "acegpu_g16_verify_batch_seed": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int),
+                                               vp]),
     "acegpu_g16_verify_fc": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, u64, vp, vp, u64p,
                                        C.POINTER(C.c_int)]),
     "acegpu_g16_shard_roots_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, u64, vp, u64,

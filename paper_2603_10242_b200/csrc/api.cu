@@ -1741,28 +1741,25 @@ extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* po
     DeviceGuard g(c->device);
     cudaStream_t s = c->stream;
     const uint64_t pb = 64ull * group;
-    auto* b = new acegpu_msm_bases();
+    // owned until success: every error path frees the table and the staging copy
+    std::unique_ptr<acegpu_msm_bases, void (*)(acegpu_msm_bases*)> b(new acegpu_msm_bases(),
+                                                                      acegpu_bn_msm_free);
     b->device = c->device;
     b->group = group;
     b->n = n;
-    uint8_t* tmp = nullptr;
+    std::unique_ptr<uint8_t, cudaError_t (*)(void*)> tmp(nullptr, cudaFree);
     cudaError_t e = cudaMalloc(&b->table, pb * n * bn::kMsmWindows);
-    if (e == cudaSuccess) e = cudaMalloc(&tmp, pb * n);
-    if (e != cudaSuccess) {
-        if (b->table) cudaFree(b->table);
-        delete b;
+    uint8_t* t = nullptr;
+    if (e == cudaSuccess) e = cudaMalloc(&t, pb * n);
+    tmp.reset(t);
+    if (e != cudaSuccess)
         return fail(ACEGPU_ECUDA, std::string("msm_prepare alloc: ") + cudaGetErrorString(e));
-    }
-    CK(cudaMemcpyAsync(tmp, points, pb * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    bn::launch_points_convert(group, tmp, n, 1, s);
-    if (bn::msm_prepare(group, tmp, n, b->table, s)) {
-        cudaFree(tmp);
-        return fail(ACEGPU_ECUDA, "msm_prepare launch");
-    }
+    CK(cudaMemcpyAsync(t, points, pb * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    bn::launch_points_convert(group, t, n, 1, s);
+    if (bn::msm_prepare(group, t, n, b->table, s)) return fail(ACEGPU_ECUDA, "msm_prepare launch");
     CK(cudaStreamSynchronize(s));
-    cudaFree(tmp);
     c->launches += 2;
-    *out = b;
+    *out = b.release();
     return ACEGPU_OK;
 }
 
@@ -1863,6 +1860,7 @@ struct acegpu_g16 {
     // delta2 in the oracle encoding; IC_0..IC_T Montgomery affine (export)
     acegpu_msm_bases* qic = nullptr;
     uint8_t *vk_alpha1 = nullptr, *vk_g2_std = nullptr, *vk_ic = nullptr;
+    uint8_t* vk_digest = nullptr;  // SHA-256 of the acegpu_g16_vk export (verifier seed)
     uint8_t *consts = nullptr, *cc = nullptr;
     // per-proof buffers of the current slot (pointers into slot[cur])
     uint8_t *z = nullptr, *zb = nullptr, *zl = nullptr, *ea = nullptr, *eb = nullptr, *ec = nullptr;
@@ -1871,7 +1869,7 @@ struct acegpu_g16 {
     // chunk k's NTTs / MSMs still read the other slot; `done` = the slot's
     // proof assembled (its buffers free again)
     struct Slot {
-        uint8_t *z, *zb, *zl, *ea, *eb, *ec, *pts, *scaled, *rs, *digest;
+        uint8_t *z, *zb, *zl, *ea, *eb, *ec, *pts, *scaled, *rs, *digest, *dsc;
         cudaEvent_t done;
     } slot[2] = {};
     int cur = 1;
@@ -1887,10 +1885,24 @@ struct acegpu_g16 {
     cudaStream_t s_n = nullptr;   // the H-polynomial NTTs (then ev_n -> the H MSM on s_h)
     cudaEvent_t ev_n = nullptr;
     cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
-    bn::MsmScratch msm_bl, msm_h;
+    bn::MsmScratch msm_bl, msm_h, msm_ab;  // one per MSM stream (no cross-stream scratch)
 };
 
 namespace {
+
+// The verifying key's export encoding (acegpu_g16_vk) into device memory d
+// (448 + 64 (T + 1) bytes): alpha1 | beta2 | gamma2 | delta2 | IC_0..IC_T.
+int vk_export_dev(acegpu_ctx* c, const acegpu_g16* g, uint8_t* d, cudaStream_t s) {
+    const uint64_t T = g->d.T;
+    CK(cudaMemcpyAsync(d, g->vk_alpha1, 64, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(d + 64, g->vk_g2_std, 384, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(d + 448, g->vk_ic, 64 * (T + 1), cudaMemcpyDeviceToDevice, s));
+    bn::launch_points_convert(1, d, 1, 0, s);
+    bn::launch_points_convert(1, d + 448, T + 1, 0, s);
+    CKL();
+    c->launches += 2;
+    return ACEGPU_OK;
+}
 
 int bases_from_device(int device, int group, const uint8_t* d_pts_mont, uint64_t n,
                       cudaStream_t s, acegpu_msm_bases** out) {
@@ -1938,11 +1950,11 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     cudaDeviceSynchronize();
     for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh, g->qic})
         acegpu_bn_msm_free(b);
-    for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic})
+    for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic, g->vk_digest})
         if (p) cudaFree(p);
     for (auto& sl : g->slot) {
         for (uint8_t* p : {sl.z, sl.zb, sl.zl, sl.ea, sl.eb, sl.ec, sl.pts, sl.scaled, sl.rs,
-                           sl.digest})
+                           sl.digest, sl.dsc})
             if (p) cudaFree(p);
         if (sl.done) cudaEventDestroy(sl.done);
     }
@@ -1958,6 +1970,7 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
         if (e) cudaEventDestroy(e);
     g->msm_bl.release();
     g->msm_h.release();
+    g->msm_ab.release();
     delete g;
 }
 
@@ -1992,7 +2005,8 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     for (auto& sl : g->slot) {
         if (dm(&sl.z, 32 * (V + 2)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
             dm(&sl.ea, 32 * N) || dm(&sl.eb, 32 * N) || dm(&sl.ec, 32 * N) || dm(&sl.pts, 512) ||
-            dm(&sl.scaled, 256) || dm(&sl.rs, 64) || dm(&sl.digest, 32))
+            dm(&sl.scaled, 256) || dm(&sl.rs, 64) || dm(&sl.digest, 32) ||
+            dm(&sl.dsc, bn::g16_digest_scratch_bytes(T, 1) + 32))
             return fail(ACEGPU_ECUDA, "g16 alloc");
         CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
     }
@@ -2074,7 +2088,7 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     bn::launch_scalar_muls(1, gens, sl, g->Vp, pts, s);
     CK(cudaMemcpyAsync(pts + 64 * g->Vp, ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
     RET(bases_from_device(c->device, 1, pts, g->Vp + 1, s, &g->ql));
-    // H: [tau^j Z(tau)/delta]1, j < N-1
+    // H: [L^g_j(tau) Z(tau)/delta]1, j < N (coset-Lagrange basis, N points)
     bn::launch_scalar_muls(1, gens, hs, N, pts, s);
     RET(bases_from_device(c->device, 1, pts, N, s, &g->qh));
     // verifying key (the Groth16 verifier, g16_verify.cu)
@@ -2089,6 +2103,11 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     bn::launch_scalar_muls(2, gens + 64, ext + 256, 1, g->vk_g2_std + 128, s);       // gamma2
     CK(cudaMemcpyAsync(g->vk_g2_std + 256, ex2 + 128, 128, cudaMemcpyDeviceToDevice, s));
     bn::launch_points_convert(2, g->vk_g2_std, 3, 0, s);
+    CKL();
+    // the verifier's Fiat-Shamir seed commits to the verifying key
+    if (dm(&g->vk_digest, 32)) return fail(ACEGPU_ECUDA, "g16 vk alloc");
+    RET(vk_export_dev(c, g, pts, s));  // pts: free scratch by now
+    bn::g16_vk_digest(pts, uint32_t(448 + 64 * (T + 1)), g->vk_digest, s);
     CKL();
     CK(cudaStreamSynchronize(s));
     for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2}) cudaFree(p);
@@ -2165,7 +2184,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     for (uint8_t* e : {g->ea, g->eb, g->ec})
         if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), sw));
     bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, sw);
-    bn::g16_derive_rs(d_pub, g->d.T, g->rs, g->digest, sw);
+    bn::g16_derive_rs(d_w, d_pub, g->d.T, sl.dsc, g->rs, g->digest, sw);
     if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, sw));
     // scalar vectors with their extras
     CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, sw));
@@ -2174,7 +2193,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CKL();
     CK(cudaEventRecord(g->ev_z, sw));
     tr.mark("witness", sw);
-    // s_h: H(x) = (a b - c) / Z on the coset, back to coefficients, then [h]
+    // s_h: H(g w^j) = (a b - c) / Z on the coset, then [h] over those evaluations
     const bn::NttTables& t = c->ntt[g->logn];
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
     cudaStream_t sh = g->s_h, sn = g->s_n;
@@ -2206,9 +2225,9 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     // s_ab: A and B1, then s*A and r*B1 (one serial scalar multiplication
     // each) on the side stream while the others finish
     CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
-    if (bn::msm_run(1, g->qa->table, V + 2, g->z, c->msm, g->pts, g->s_ab) ||
+    if (bn::msm_run(1, g->qa->table, V + 2, g->z, g->msm_ab, g->pts, g->s_ab) ||
         (tr.mark("msm_a", g->s_ab), false) ||
-        bn::msm_run(1, g->qb1->table, V + 2, g->zb, c->msm, g->pts + 64, g->s_ab))
+        bn::msm_run(1, g->qb1->table, V + 2, g->zb, g->msm_ab, g->pts + 64, g->s_ab))
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
@@ -2238,7 +2257,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
 // aggregates them with the reference's tree rule (prover.cpp:106-127).
 namespace {
 int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_proofs,
-                      const uint8_t* d_pubs, uint64_t n, int* d_ok);
+                      const uint8_t* d_pubs, uint64_t n, int* d_ok, uint8_t* d_seed = nullptr);
 // Per-chunk inputs of a (shard of a) block in Groth16 mode: leaves (verdicts,
 // public-input digests, Merkle leaves), Merkle levels up to the chunk level
 // (the block's short last chunk lifted), the chunk Merkle roots, and the
@@ -2344,20 +2363,20 @@ extern "C" int acegpu_g16_verify_fc(acegpu_ctx* c, acegpu_g16* g, const uint8_t*
     RET(h2d_t(c, kHeader, header, 256, s, &dh));
     RET(h2d_t(c, kSegRoots, chunk_proofs256, 256 * chunks, s, &dproofs));
     auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };  // 16-B vector stores
-    RET(ws(c, kSegMerk, al(32 * chunks) + al(289 * chunks) + al(32 * chunks) + al(320) + al(640) + 16,
-           &merk));
+    const uint64_t dsc_bytes = bn::g16_digest_scratch_bytes(T, uint32_t(chunks));
+    RET(ws(c, kSegMerk, al(32 * chunks) + al(289 * chunks) + al(32 * chunks) + al(320) + al(640) +
+                            al(16) + dsc_bytes, &merk));
     roots = merk + al(32 * chunks);
     digest = roots + al(289 * chunks);
     node = digest + al(32 * chunks);
     out = node + al(320);
     dok = out + al(640);
+    uint8_t* dsc = dok + al(16);
     TreeResult t;
     RET(g16_chunk_inputs(c, s, g, dp, doff, da, n, n, nullptr, nullptr, nullptr, merk, &pub, &t));
     // chunk roots: proof | chunk digest | kind Tx, as the prover built them
-    uint8_t* rs;
-    RET(ws(c, kIn2, 64, &rs));
+    bn::g16_chunk_digests(pub, T, uint32_t(chunks), dsc, digest, s);
     for (uint64_t k = 0; k < chunks; ++k) {
-        bn::g16_derive_rs(pub + 32 * T * k, T, rs, digest + 32 * k, s);
         bn::g16_chunk_node(dproofs + 256 * k, digest + 32 * k, node, s);
         launch_pack_nodes(node, 1, roots + 289 * k, s);
         CKL();
@@ -2381,16 +2400,10 @@ extern "C" int acegpu_g16_vk(acegpu_ctx* c, const acegpu_g16* g, uint8_t* out) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     cudaStream_t s = c->stream;
-    const uint64_t T = g->d.T, bytes = 448 + 64 * (T + 1);
+    const uint64_t bytes = 448 + 64 * (uint64_t(g->d.T) + 1);
     uint8_t* d;
     RET(ws(c, kBnOut, bytes, &d));
-    CK(cudaMemcpyAsync(d, g->vk_alpha1, 64, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(d + 64, g->vk_g2_std, 384, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(d + 448, g->vk_ic, 64 * (T + 1), cudaMemcpyDeviceToDevice, s));
-    bn::launch_points_convert(1, d, 1, 0, s);
-    bn::launch_points_convert(1, d + 448, T + 1, 0, s);
-    CKL();
-    c->launches += 2;
+    RET(vk_export_dev(c, g, d, s));
     CK(cudaMemcpyAsync(out, d, bytes, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;
@@ -2398,7 +2411,7 @@ extern "C" int acegpu_g16_vk(acegpu_ctx* c, const acegpu_g16* g, uint8_t* out) {
 
 namespace {
 int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_proofs,
-                      const uint8_t* d_pubs, uint64_t n, int* d_ok) {
+                      const uint8_t* d_pubs, uint64_t n, int* d_ok, uint8_t* d_seed) {
     if (n == 0 || n > (1u << 20)) return fail(ACEGPU_EINVAL, "g16 verify: bad proof count");
     uint8_t* scratch;
     RET(ws(c, kP1Scratch, bn::g16_verify_scratch_bytes(uint32_t(n), g->d.T), &scratch));
@@ -2407,7 +2420,8 @@ int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_
     vk.ic_table = g->qic->table;
     vk.alpha1_mont = g->vk_alpha1;
     vk.g2_std = g->vk_g2_std;
-    if (bn::g16_verify_batch(vk, d_proofs, d_pubs, uint32_t(n), scratch, c->msm, d_ok, s))
+    vk.vk_digest = g->vk_digest;
+    if (bn::g16_verify_batch(vk, d_proofs, d_pubs, uint32_t(n), scratch, c->msm, d_ok, s, d_seed))
         return fail(ACEGPU_ECUDA, "g16 verify launch");
     CKL();
     c->launches += 3 + bn::kMsmKernels;
@@ -2415,8 +2429,9 @@ int g16_verify_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_
 }
 }  // namespace
 
-extern "C" int acegpu_g16_verify_batch(acegpu_ctx* c, acegpu_g16* g, const uint8_t* proofs256,
-                                       const uint8_t* pubs, uint64_t n, int* ok) {
+extern "C" int acegpu_g16_verify_batch_seed(acegpu_ctx* c, acegpu_g16* g,
+                                            const uint8_t* proofs256, const uint8_t* pubs,
+                                            uint64_t n, int* ok, uint8_t* seed32) {
     if (!g || !proofs256 || !pubs || !ok) return fail(ACEGPU_EINVAL, "null argument");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
@@ -2424,11 +2439,17 @@ extern "C" int acegpu_g16_verify_batch(acegpu_ctx* c, acegpu_g16* g, const uint8
     uint8_t *dp, *dq, *dok;
     RET(h2d_t(c, kBnA, proofs256, 256 * n, s, &dp));
     RET(h2d_t(c, kBnB, pubs, 32ull * g->d.T * n, s, &dq));
-    RET(ws(c, kBnOut, 16, &dok));
-    RET(g16_verify_locked(c, s, g, dp, dq, n, reinterpret_cast<int*>(dok)));
+    RET(ws(c, kBnOut, 64, &dok));
+    RET(g16_verify_locked(c, s, g, dp, dq, n, reinterpret_cast<int*>(dok), dok + 32));
     CK(cudaMemcpyAsync(ok, dok, sizeof(int), cudaMemcpyDeviceToHost, s));
+    if (seed32) CK(cudaMemcpyAsync(seed32, dok + 32, 32, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;
+}
+
+extern "C" int acegpu_g16_verify_batch(acegpu_ctx* c, acegpu_g16* g, const uint8_t* proofs256,
+                                       const uint8_t* pubs, uint64_t n, int* ok) {
+    return acegpu_g16_verify_batch_seed(c, g, proofs256, pubs, n, ok, nullptr);
 }
 
 extern "C" int acegpu_g16_prove_chunk(acegpu_ctx* c, acegpu_g16* g, const uint8_t* w,

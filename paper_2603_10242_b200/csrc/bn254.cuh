@@ -111,7 +111,7 @@ __device__ __forceinline__ void final_sub(uint32_t t[9], uint32_t r[8]) {
 
 // CIOS Montgomery multiplication: r = a * b * 2^-256 mod m.
 template <class C>
-__device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
+__device__ __forceinline__ Fp<C> mul_cios(const Fp<C>& a, const Fp<C>& b) {
     uint32_t t0 = 0, t1 = 0, t2 = 0, t3 = 0, t4 = 0, t5 = 0, t6 = 0, t7 = 0, t8 = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
@@ -173,6 +173,132 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
     Fp<C> r;
     final_sub<C>(t, r.v);
     return r;
+}
+
+// ---- FP64 (DFMA) Montgomery product ----------------------------------------
+// On sm_100a IMAD, IMAD.HI and DFMA share one issue pipe: IMAD costs 2
+// cycles per warp, IMAD.HI 4, IMAD.WIDE 6, DFMA 2 (tools/int_pipes.cu). A
+// 32x32-bit product (lo + hi) therefore costs 6 pipe cycles for 1,024 bits^2
+// while a 52x52-bit DFMA split (3 FP64 ops) costs 6 for 2,704: the product
+// below does the multiplications in FP64 and the column sums on the integer
+// ALU pipe. Radix 2^52, 5 limbs, R' = 2^260, used as a drop-in for the
+// R = 2^256 product: MM'(16a, b) = a b 2^-256 mod m, bit-identical results.
+// Split of x*y (x, y < 2^52): t = fma_rz(x, y, 2^104) = 2^104 + hi 2^52,
+// s = (2^104 + 2^52) - t (exact), l = fma(x, y, s) = 2^52 + lo; hi and lo
+// are the low mantissa bits of t and l, accumulated as raw bit patterns in
+// 64-bit columns that start from minus the exponent bits they will collect.
+namespace f64 {
+constexpr uint64_t kM52 = (1ull << 52) - 1;
+constexpr uint64_t kB52 = 0x4330000000000000ull;   // bits(2^52)
+constexpr uint64_t kB104 = 0x4670000000000000ull;  // bits(2^104)
+constexpr double kC1 = 20282409603651670423947251286016.0;                       // 2^104
+constexpr double kC2 = 20282409603651670423947251286016.0 + 4503599627370496.0;  // + 2^52
+constexpr double kT52 = 4503599627370496.0;                                      // 2^52
+template <class C>
+constexpr uint64_t limb52(int k) {  // bits [52k, 52k + 52) of the modulus
+    uint64_t r = 0;
+    for (int b = 0; b < 52; ++b) {
+        const int i = 52 * k + b;
+        if (i < 256 && ((C::M[i >> 5] >> (i & 31)) & 1)) r |= 1ull << b;
+    }
+    return r;
+}
+template <class C>
+constexpr uint64_t nprime52() {  // -m^-1 mod 2^52 (Newton)
+    const uint64_t m0 = (uint64_t)C::M[0] | ((uint64_t)C::M[1] << 32);
+    uint64_t x = m0;  // correct to 3 bits
+    for (int i = 0; i < 5; ++i) x *= 2 - m0 * x;
+    return (0ull - x) & kM52;
+}
+// column bias: minus the exponent bits of the lo / hi patterns column k collects
+constexpr uint64_t bias(int k) {
+    uint64_t s = 0;
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+            if (i + j == k) s += kB52;      // a_i b_j lo
+            if (i + j + 1 == k) s += kB104;  // a_i b_j hi
+            if (j > 0 && i + j == k) s += kB52;  // m_i p_j lo (j = 0: carried, not added)
+            if (i + j + 1 == k) s += kB104;      // m_i p_j hi
+        }
+    return 0ull - s;
+}
+__device__ __forceinline__ uint64_t bits(double x) { return (uint64_t)__double_as_longlong(x); }
+__device__ __forceinline__ double to_d(uint64_t x52) {  // exact for x < 2^52
+    return __dsub_rn(__longlong_as_double((long long)(x52 | kB52)), kT52);
+}
+__device__ __forceinline__ void split_acc(double x, double y, uint64_t& clo, uint64_t& chi) {
+    const double t = __fma_rz(x, y, kC1);
+    const double l = __fma_rn(x, y, __dsub_rn(kC2, t));
+    clo += bits(l);
+    chi += bits(t);
+}
+// 8 x 32-bit limbs -> 5 x 52-bit doubles of (a << SH); a << SH < 2^260
+template <int SH>
+__device__ __forceinline__ void to52(const uint32_t v[8], double d[5]) {
+    const uint64_t w0 = ((uint64_t)v[1] << 32) | v[0], w1 = ((uint64_t)v[3] << 32) | v[2],
+                   w2 = ((uint64_t)v[5] << 32) | v[4], w3 = ((uint64_t)v[7] << 32) | v[6];
+    d[0] = to_d((w0 << SH) & kM52);
+    d[1] = to_d(((w0 >> (52 - SH)) | (w1 << (12 + SH))) & kM52);
+    d[2] = to_d(((w1 >> (40 - SH)) | (w2 << (24 + SH))) & kM52);
+    d[3] = to_d(((w2 >> (28 - SH)) | (w3 << (36 + SH))) & kM52);
+    d[4] = to_d((w3 >> (16 - SH)) & kM52);
+}
+}  // namespace f64
+
+// r = a b 2^-256 mod m (a, b < m), fully reduced: identical to mul().
+template <class C>
+__device__ __forceinline__ Fp<C> mul_f64(const Fp<C>& a, const Fp<C>& b) {
+    using namespace f64;
+    double x[5], y[5];
+    to52<4>(a.v, x);
+    to52<0>(b.v, y);
+    uint64_t c[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) c[k] = bias(k);
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) split_acc(x[i], y[j], c[i + j], c[i + j + 1]);
+    constexpr double NP = (double)nprime52<C>();
+    constexpr double P[5] = {(double)limb52<C>(0), (double)limb52<C>(1), (double)limb52<C>(2),
+                             (double)limb52<C>(3), (double)limb52<C>(4)};
+    uint64_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const uint64_t s = c[i] + carry;
+        const uint64_t v = s & kM52;
+        carry = (s >> 52) + (v != 0);  // v + lo(m p_0) is 0 or 2^52
+        const double vd = to_d(v);
+        const double t = __fma_rz(vd, NP, kC1);
+        const double md = __dsub_rn(__fma_rn(vd, NP, __dsub_rn(kC2, t)), kT52);  // lo52(v n')
+        c[i + 1] += bits(__fma_rz(md, P[0], kC1));
+#pragma unroll
+        for (int j = 1; j < 5; ++j) split_acc(md, P[j], c[i + j], c[i + j + 1]);
+    }
+    uint64_t r[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const uint64_t s = c[5 + k] + carry;
+        r[k] = s & kM52;
+        carry = s >> 52;
+    }
+    // result < 2^255: r[4] < 2^47, no carry out
+    const uint64_t w0 = r[0] | (r[1] << 52), w1 = (r[1] >> 12) | (r[2] << 40),
+                   w2 = (r[2] >> 24) | (r[3] << 28), w3 = (r[3] >> 36) | (r[4] << 16);
+    uint32_t t9[9] = {(uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32),
+                      (uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32), 0u};
+    Fp<C> out;
+    final_sub<C>(t9, out.v);
+    return out;
+}
+
+#ifndef ACEGPU_F64MUL
+#define ACEGPU_F64MUL 0  // 1: every mul() through the FP64 product
+#endif
+template <class C>
+__device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
+    if constexpr (ACEGPU_F64MUL) return mul_f64(a, b);
+    else return mul_cios(a, b);
 }
 
 // ---- lazy reduction: 512-bit products, one Montgomery reduction per sum ----

@@ -33,7 +33,17 @@ void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const u
                  uint8_t* z, uint8_t* ea, uint8_t* eb, uint8_t* ec, cudaStream_t s);
 void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint8_t* c,
                    uint64_t n, cudaStream_t s);
-void g16_derive_rs(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest, cudaStream_t s);
+// Binding v2 (groth16.cu): D(x) digests of T-input chunks, chunk digests
+// SHA-256("ace-g16-chunk-v2" | D(pub)), and r, s from D(w) | D(pub).
+size_t g16_digest_scratch_bytes(uint32_t T, uint32_t chunks);
+void g16_input_digests(const uint8_t* x, uint32_t T, uint32_t chunks, int wits, uint8_t* scratch,
+                       uint8_t* out, cudaStream_t s);
+// scratch: g16_digest_scratch_bytes(T, chunks); D(pub_k) left at scratch + stride * chunks
+void g16_chunk_digests(const uint8_t* pub, uint32_t T, uint32_t chunks, uint8_t* scratch,
+                       uint8_t* digests, cudaStream_t s);
+// scratch: g16_digest_scratch_bytes(T, 1) + 32
+void g16_derive_rs(const uint8_t* w, const uint8_t* pub, uint32_t T, uint8_t* scratch,
+                   uint8_t* rs, uint8_t* digest, cudaStream_t s);
 void g16_extras(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp, const uint8_t* rs,
                 cudaStream_t s);
 void g16_scale(const uint8_t* pts, const uint8_t* rs, uint8_t* out, cudaStream_t s);

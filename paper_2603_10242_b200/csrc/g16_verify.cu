@@ -2,8 +2,11 @@
 //
 // For n proofs (A_i, B_i, C_i) with public inputs z_i = (1, pub_i) the
 // verifier checks, with 128-bit weights rho_i derived Fiat-Shamir style from
-// the proofs themselves (rho_i = LE(SHA-256("ace-g16-batch-v1" | seed | i))[0:16],
-// seed = SHA-256(SHA-256(proof_0) | ... | SHA-256(proof_{n-1}))):
+// the whole statement (rho_i = LE(SHA-256("ace-g16-batch-v2" | seed | i))[0:16],
+// seed = SHA-256("ace-g16-seed-v2:" | SHA-256(VK) | SHA-256(proof_0) | D(pub_0) |
+// ... | SHA-256(proof_{n-1}) | D(pub_{n-1})), VK = the acegpu_g16_vk export and
+// D(pub_i) the input digest of proof i's T public inputs, groth16.cu), so no
+// public input can be changed after the weights are known:
 //
 //   prod_i e(rho_i A_i, B_i) * e(-(sum rho_i) alpha, beta)
 //       * e(-sum_j (sum_i rho_i z_ij) IC_j, gamma) * e(-sum_i rho_i C_i, delta) == 1
@@ -14,6 +17,7 @@
 // (psi(B) = [6x^2] B).
 #include <cuda_runtime.h>
 
+#include "g16_kernels.cuh"
 #include "g16_verify.cuh"
 #include "pairing.cuh"
 #include "pairing_kernels.cuh"
@@ -93,26 +97,42 @@ __device__ void to_affine<Fq>(const XYZZ<Fq>& p, Fq& x, Fq& y) {
     y = fmul(p.Y, fmul(t, p.ZZ));
 }
 
-__global__ void proof_hash_kernel(const uint8_t* proofs, uint32_t n, uint8_t* hashes) {
+// msg = "ace-g16-seed-v2:" | vk_digest | (SHA-256(proof_i) | D(pub_i))_i
+__global__ void proof_hash_kernel(const uint8_t* proofs, const uint8_t* pd, uint32_t n,
+                                  const uint8_t* vk_digest, uint8_t* msg) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {
+        const char tag[] = "ace-g16-seed-v2:";
+        for (int k = 0; k < 16; ++k) msg[k] = tag[k];
+        for (int k = 0; k < 32; ++k) msg[16 + k] = vk_digest[k];
+    }
     if (i >= n) return;
     uint32_t d[8];
     sha256_bytes(proofs, 256ull * i, 256, d);
-    store_digest(hashes + 32ull * i, d);
+    uint8_t* o = msg + 48 + 64ull * i;
+    store_digest(o, d);
+    for (int k = 0; k < 32; ++k) o[32 + k] = pd[32ull * i + k];
 }
 
-__global__ void seed_kernel(const uint8_t* hashes, uint32_t n, uint8_t* seed) {
+__global__ void seed_kernel(const uint8_t* msg, uint32_t n, uint8_t* seed) {
     if (threadIdx.x || blockIdx.x) return;
     uint32_t d[8];
-    sha256_bytes(hashes, 0, 32 * n, d);
+    sha256_bytes(msg, 0, 48 + 64 * n, d);
     store_digest(seed, d);
+}
+
+__global__ void hash_kernel(const uint8_t* x, uint32_t len, uint8_t* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    uint32_t d[8];
+    sha256_bytes(x, 0, len, d);
+    store_digest(out, d);
 }
 
 __global__ void rho_kernel(const uint8_t* seed, uint32_t n, uint8_t* rho) {
     const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     __align__(16) uint8_t m[52];
-    const char tag[] = "ace-g16-batch-v1";
+    const char tag[] = "ace-g16-batch-v2";
     for (int k = 0; k < 16; ++k) m[k] = tag[k];
     for (int k = 0; k < 32; ++k) m[16 + k] = seed[k];
     m[48] = i >> 24; m[49] = i >> 16; m[50] = i >> 8; m[51] = i;
@@ -276,22 +296,30 @@ inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 size_t g16_verify_scratch_bytes(uint32_t n, uint32_t T) {
-    const size_t a = 32ull * n * 2 + 32 + 32ull * (T + 1) + 64 + 64ull * (n + 3) +
-                     128ull * (n + 3) + sizeof(XYZZ<Fq>) * (n ? n : 1) + 16 * 8;
-    return a + pairing_scratch_bytes(n + 3) + 256;
+    const size_t a = (48 + 64ull * n) + 32ull * n + 32 + 32ull * (T + 1) + 64 + 64ull * (n + 3) +
+                     128ull * (n + 3) + sizeof(XYZZ<Fq>) * (n ? n : 1) + 16 * 8 +
+                     g16_digest_scratch_bytes(T, n) + 32ull * n;
+    return a + pairing_scratch_bytes(n + 3) + 256 + 128 * 4;
+}
+
+void g16_vk_digest(const uint8_t* vk_bytes, uint32_t len, uint8_t* out, cudaStream_t s) {
+    hash_kernel<<<1, 32, 0, s>>>(vk_bytes, len, out);
 }
 
 int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_t* pubs,
-                     uint32_t n, uint8_t* scratch, MsmScratch& msm, int* d_ok, cudaStream_t s) {
+                     uint32_t n, uint8_t* scratch, MsmScratch& msm, int* d_ok, cudaStream_t s,
+                     uint8_t* seed_out) {
     const uint32_t T = vk.T;
     auto take = [&scratch](size_t bytes) {
         uint8_t* p = scratch;
         scratch += (bytes + 127) & ~size_t(127);
         return p;
     };
-    uint8_t* hashes = take(32ull * n);
+    uint8_t* hashes = take(48 + 64ull * n);
     uint8_t* rho = take(32ull * n);
     uint8_t* seed = take(32);
+    uint8_t* dsc = take(g16_digest_scratch_bytes(T, n));
+    uint8_t* pd = take(32ull * n);
     uint8_t* sc = take(32ull * (T + 1));
     uint8_t* L = take(64);
     uint8_t* g1s = take(64ull * (n + 3));
@@ -300,8 +328,10 @@ int g16_verify_batch(const G16VerifyKey& vk, const uint8_t* proofs, const uint8_
     int* bad = reinterpret_cast<int*>(take(16));
     uint8_t* pscratch = take(pairing_scratch_bytes(n + 3));
     cudaMemsetAsync(bad, 0, sizeof(int), s);
-    proof_hash_kernel<<<grid(n, 64), 64, 0, s>>>(proofs, n, hashes);
+    g16_input_digests(pubs, T, n, 0, dsc, pd, s);
+    proof_hash_kernel<<<grid(n, 64), 64, 0, s>>>(proofs, pd, n, vk.vk_digest, hashes);
     seed_kernel<<<1, 32, 0, s>>>(hashes, n, seed);
+    if (seed_out) cudaMemcpyAsync(seed_out, seed, 32, cudaMemcpyDeviceToDevice, s);
     rho_kernel<<<grid(n, 64), 64, 0, s>>>(seed, n, rho);
     combine_kernel<<<grid(T + 1, 64), 64, 0, s>>>(pubs, rho, n, T, sc);
     if (msm_run(1, vk.ic_table, T + 1, sc, msm, L, s)) return -1;

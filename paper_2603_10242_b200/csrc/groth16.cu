@@ -7,7 +7,8 @@
 // m = 1,434,625 constraints, domain 2^21):
 //   witness  : per tx the K-step chain x_k = (x_{k-1} + c_k)^2 seeded with
 //              w_t + pub_t; writes z and the row evaluations a, b, c
-//   H        : 3 iNTT + 3 coset NTT + pointwise (a b - c) / Z(g w^j) + coset iNTT
+//   H        : 3 iNTT + 3 coset NTT + pointwise (a b - c) / Z(g w^j): the coset
+//              evaluations are the H-MSM scalars (H bases in the coset's Lagrange basis)
 //   MSMs     : A = [u](z) + alpha + r delta, B = [v](z) + beta + s delta (G2
 //              and G1), L = [l](z_priv) - rs delta, H = [h]
 //   assemble : C = L + H + s A + r B1
@@ -200,7 +201,7 @@ __global__ void ic_scalars_kernel(uint32_t T, const uint8_t* c, const uint8_t* s
     str(out + 32ull * j, from_mont(mul(add(mul(beta, u), mul(alpha, v)), inv_fast(gamma))));
 }
 
-// H-query scalars: tau^j Z(tau)/delta for j < n (standard form).
+// H-query scalars: the N coset-Lagrange values L^g_j(tau) Z(tau)/delta, j < N.
 // H bases in the Lagrange basis of the coset g<omega> (g = 5), so the MSM
 // takes the coset evaluations H(g w^j) straight from the pointwise division
 // (no coset iNTT): [H(tau) Z(tau)/delta] = sum_j H(g w^j) L^g_j(tau) Z(tau)/delta,
@@ -278,25 +279,70 @@ __global__ void pointwise_kernel(uint8_t* ea, const uint8_t* eb, const uint8_t* 
     str(ea + 32 * j, mul(sub(mul(ldr(ea + 32 * j), ldr(eb + 32 * j)), ldr(ec + 32 * j)), zi));
 }
 
-// Deterministic r, s: LE(SHA-256(tag | pub_0 | pub_{T-1} | T_be32)) mod r,
-// tags "ace-g16-r-v1" / "ace-g16-s-v1"; also writes the chunk digest
-// SHA-256("ace-g16-chunk-v1" | pub_0 | pub_{T-1} | T_be32).
-__global__ void derive_rs_kernel(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest) {
-    const int which = threadIdx.x;  // 0: r, 1: s, 2: chunk digest
-    if (which > 2) return;
-    __align__(16) uint8_t m[96];
-    const char* tag = which == 0 ? "ace-g16-r-v1" : which == 1 ? "ace-g16-s-v1" : "ace-g16-chunk-v1";
-    const int tl = which == 2 ? 16 : 12;
-    for (int i = 0; i < tl; ++i) m[i] = tag[i];
-    for (int i = 0; i < 32; ++i) {
-        m[tl + i] = pub[i];
-        m[tl + 32 + i] = pub[32ull * (T - 1) + i];
-    }
-    m[tl + 64] = T >> 24; m[tl + 65] = T >> 16; m[tl + 66] = T >> 8; m[tl + 67] = T;
+// Input digests (binding v2). For a chunk of T 32-B inputs x_0..x_{T-1}:
+//   D(x) = SHA-256(tag16 | SHA-256(x_0..x_31) | SHA-256(x_32..x_63) | ... | T_be32)
+// (blocks of 32 inputs, the last one short), tag16 = "ace-g16-pubs-v2:" for
+// public inputs, "ace-g16-wits-v2:" for witnesses. Thread per (chunk, block)
+// writes its block digest into the chunk's message; one thread per chunk
+// then hashes the message.
+__global__ void input_blocks_kernel(const uint8_t* x, uint32_t T, uint32_t chunks, int wits,
+                                    uint8_t* msg, uint32_t stride) {
+    const uint32_t nb = (T + 31) / 32;
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= (uint64_t)chunks * nb) return;
+    const uint32_t c = uint32_t(j / nb), b = uint32_t(j - (uint64_t)c * nb);
+    uint8_t* m = msg + (uint64_t)stride * c;
+    const uint32_t cnt = min(32u, T - 32 * b);
     uint32_t d[8];
-    sha256_bytes(m, 0, tl + 68, d);
-    if (which == 2) store_digest(digest, d);
-    else str(rs + 32 * which, digest_to_fr(d));
+    sha256_bytes(x, 32ull * ((uint64_t)c * T + 32ull * b), 32 * cnt, d);
+    store_digest(m + 16 + 32 * b, d);
+    if (b == 0) {
+        const char* tag = wits ? "ace-g16-wits-v2:" : "ace-g16-pubs-v2:";
+        for (int i = 0; i < 16; ++i) m[i] = tag[i];
+        uint8_t* e = m + 16 + 32 * nb;
+        e[0] = T >> 24; e[1] = T >> 16; e[2] = T >> 8; e[3] = T;
+    }
+}
+__global__ void input_top_kernel(const uint8_t* msg, uint32_t stride, uint32_t len,
+                                 uint32_t chunks, uint8_t* out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= chunks) return;
+    uint32_t d[8];
+    sha256_bytes(msg, (uint64_t)stride * c, len, d);
+    store_digest(out + 32ull * c, d);
+}
+
+// Chunk digest (the tree leaf's public-inputs digest) from D(pub):
+// SHA-256("ace-g16-chunk-v2" | D(pub)).
+__global__ void chunk_digest_kernel(const uint8_t* pd, uint32_t chunks, uint8_t* digest) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= chunks) return;
+    __align__(16) uint8_t m[48];
+    const char tag[] = "ace-g16-chunk-v2";
+    for (int i = 0; i < 16; ++i) m[i] = tag[i];
+    for (int i = 0; i < 32; ++i) m[16 + i] = pd[32ull * c + i];
+    uint32_t d[8];
+    sha256_bytes(m, 0, 48, d);
+    store_digest(digest + 32ull * c, d);
+}
+
+// Deterministic r, s (RFC 6979 style: a function of the
+// secret witness, so the blinding is not public, and of the statement):
+// LE(SHA-256(tag | D(w) | D(pub))) mod r, tags "ace-g16-r-v2" / "ace-g16-s-v2";
+// a backup prover holding the same witnesses reproduces the proof bytes.
+__global__ void derive_rs_kernel(const uint8_t* wd, const uint8_t* pd, uint8_t* rs) {
+    const int which = threadIdx.x;  // 0: r, 1: s
+    if (which > 1) return;
+    __align__(16) uint8_t m[76];
+    const char* tag = which == 0 ? "ace-g16-r-v2" : "ace-g16-s-v2";
+    for (int i = 0; i < 12; ++i) m[i] = tag[i];
+    for (int i = 0; i < 32; ++i) {
+        m[12 + i] = wd[i];
+        m[44 + i] = pd[i];
+    }
+    uint32_t d[8];
+    sha256_bytes(m, 0, 76, d);
+    str(rs + 32 * which, digest_to_fr(d));
 }
 
 // Scalar extras appended to the MSM scalar vectors (standard form):
@@ -416,6 +462,8 @@ __global__ void chunk_node_kernel(const uint8_t* proof256, const uint8_t* digest
 }
 
 inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+// bytes per chunk of the input-digest message: tag16 | block digests | T_be32, 16-B aligned
+inline uint32_t digest_msg_stride(uint32_t T) { return (16 + 32 * ((T + 31) / 32) + 4 + 15) & ~15u; }
 
 }  // namespace
 
@@ -459,8 +507,30 @@ void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint
                    uint64_t n, cudaStream_t s) {
     pointwise_kernel<<<grid(n, 256), 256, 0, s>>>(ea, eb, ec, c, n);
 }
-void g16_derive_rs(const uint8_t* pub, uint32_t T, uint8_t* rs, uint8_t* digest, cudaStream_t s) {
-    derive_rs_kernel<<<1, 32, 0, s>>>(pub, T, rs, digest);
+size_t g16_digest_scratch_bytes(uint32_t T, uint32_t chunks) {
+    return (size_t)digest_msg_stride(T) * chunks + 32ull * chunks;
+}
+void g16_input_digests(const uint8_t* x, uint32_t T, uint32_t chunks, int wits, uint8_t* scratch,
+                       uint8_t* out, cudaStream_t s) {
+    const uint32_t nb = (T + 31) / 32, stride = digest_msg_stride(T);
+    input_blocks_kernel<<<grid((uint64_t)chunks * nb, 64), 64, 0, s>>>(x, T, chunks, wits,
+                                                                      scratch, stride);
+    input_top_kernel<<<grid(chunks, 64), 64, 0, s>>>(scratch, stride, 16 + 32 * nb + 4, chunks,
+                                                     out);
+}
+void g16_chunk_digests(const uint8_t* pub, uint32_t T, uint32_t chunks, uint8_t* scratch,
+                       uint8_t* digests, cudaStream_t s) {
+    uint8_t* pd = scratch + (size_t)digest_msg_stride(T) * chunks;
+    g16_input_digests(pub, T, chunks, 0, scratch, pd, s);
+    chunk_digest_kernel<<<grid(chunks, 64), 64, 0, s>>>(pd, chunks, digests);
+}
+void g16_derive_rs(const uint8_t* w, const uint8_t* pub, uint32_t T, uint8_t* scratch,
+                   uint8_t* rs, uint8_t* digest, cudaStream_t s) {
+    // scratch: g16_digest_scratch_bytes(T, 1) + 32
+    uint8_t* wd = scratch + g16_digest_scratch_bytes(T, 1);
+    g16_input_digests(w, T, 1, 1, scratch, wd, s);
+    g16_chunk_digests(pub, T, 1, scratch, digest, s);  // leaves D(pub) at its scratch tail
+    derive_rs_kernel<<<1, 32, 0, s>>>(wd, scratch + digest_msg_stride(T), rs);
 }
 void g16_extras(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp, const uint8_t* rs,
                 cudaStream_t s) {

@@ -57,16 +57,19 @@ class ProvingKey:
         self.ctx.call("acegpu_g16_vk", self.h, out)
         return out.tobytes()
 
-    def verify_batch(self, proofs: list[bytes], pubs: list[bytes]) -> bool:
+    def verify_batch(self, proofs: list[bytes], pubs: list[bytes], return_seed: bool = False):
         """Batched pairing verification of chunk proofs (EIP-197 256 B each)
-        against their T x 32-B public inputs."""
+        against their T x 32-B public inputs. return_seed: also return the
+        32-B Fiat-Shamir seed of the batch weights (include/acegpu.h)."""
         if not proofs:
-            return True
+            return (True, None) if return_seed else True
         ok = C.c_int(0)
         p = np.frombuffer(b"".join(proofs), np.uint8).copy()
         q = np.frombuffer(b"".join(pubs), np.uint8).copy()
-        self.ctx.call("acegpu_g16_verify_batch", self.h, p, q, len(proofs), C.byref(ok))
-        return ok.value == 1
+        seed = np.zeros(32, np.uint8)
+        self.ctx.call("acegpu_g16_verify_batch_seed", self.h, p, q, len(proofs), C.byref(ok),
+                      seed)
+        return (ok.value == 1, seed.tobytes()) if return_seed else ok.value == 1
 
     def verify_finality_certificate(self, fc, block, chunk_proofs: bytes, cost_units=None):
         """verify_finality_certificate (prover.cpp:158-169) in Groth16 mode:

@@ -5,12 +5,12 @@ derives from the trapdoor, and those satisfy the Groth16 verification
 identity (the pairing check in exponents). Parity unpinned by the reference
 (it has no Groth16)."""
 import ctypes as C
-import hashlib
 import random
 
 import numpy as np
 import pytest
 
+import g16_spec as SP
 import oracle_lib as O
 
 pytestmark = pytest.mark.gpu
@@ -78,8 +78,8 @@ def test_groth16_chunk_matches_trapdoor_oracle(ctx, T, K):
 
 
 def test_groth16_deterministic_rs(ctx):
-    """r, s = LE(SHA-256(tag | pub_0 | pub_{T-1} | T_be32)) mod r:
-    same inputs -> identical proof bytes; matches explicit r, s."""
+    """r, s = LE(SHA-256(tag | D(w) | D(pub))) mod r (binding v2):
+    same inputs -> identical proof bytes; matches explicit r, s (tests/g16_spec.py)."""
     from paper_2603_10242_b200 import groth16
     T, K = 5, 3
     rng = random.Random(5)
@@ -91,15 +91,89 @@ def test_groth16_deterministic_rs(ctx):
         p1, raw1, d1 = pk.prove(w, pub)
         p2, _, _ = pk.prove(w, pub)
         assert p1 == p2
-        pb = pub.tobytes()
-        tail = pb[:32] + pb[32 * (T - 1):32 * T] + T.to_bytes(4, "big")
-        r = int.from_bytes(hashlib.sha256(b"ace-g16-r-v1" + tail).digest(), "little") % R
-        s = int.from_bytes(hashlib.sha256(b"ace-g16-s-v1" + tail).digest(), "little") % R
+        r, s = SP.derive_rs(w.tobytes(), pub.tobytes(), T)
         p3, _, _ = pk.prove(w, pub, arr([r, s]))
         assert p3 == p1
-        assert d1 == hashlib.sha256(b"ace-g16-chunk-v1" + tail).digest()
+        assert d1 == SP.chunk_digest(pub.tobytes(), T)
         A, B, Cc = expected_points(T, K, w, pub, trap, arr([r, s]))
         assert raw1 == A + B + Cc
+    finally:
+        pk.close()
+
+
+@pytest.mark.parametrize("T", [5, 33, 64])
+def test_groth16_binding_covers_every_input(ctx, T):
+    """Binding v2: flipping one MIDDLE public input changes r, s,
+    the chunk digest and the verifier's weight seed; flipping a middle
+    witness changes r and s but not the chunk digest. The GPU's values equal
+    the Python statement of the rules (tests/g16_spec.py)."""
+    from paper_2603_10242_b200 import groth16
+    K = 3
+    rng = random.Random(T)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        vk = pk.verifying_key()
+        w = arr([rng.randrange(R) for _ in range(T)])
+        pub = arr([rng.randrange(R) for _ in range(T)])
+        p0, raw0, d0 = pk.prove(w, pub)
+        r0, s0 = SP.derive_rs(w.tobytes(), pub.tobytes(), T)
+        assert raw0 == b"".join(expected_points(T, K, w, pub, trap, arr([r0, s0])))
+        assert d0 == SP.chunk_digest(pub.tobytes(), T)
+        ok, seed0 = pk.verify_batch([p0], [pub.tobytes()], return_seed=True)
+        assert ok and seed0 == SP.batch_seed(vk, [p0], [pub.tobytes()], T)
+        mid = T // 2
+        pub1 = pub.copy()
+        pub1[32 * mid + 5] ^= 1
+        p1, raw1, d1 = pk.prove(w, pub1)
+        r1, s1 = SP.derive_rs(w.tobytes(), pub1.tobytes(), T)
+        assert (r1, s1) != (r0, s0) and r1 != r0 and s1 != s0
+        assert raw1 == b"".join(expected_points(T, K, w, pub1, trap, arr([r1, s1])))
+        assert d1 != d0 and d1 == SP.chunk_digest(pub1.tobytes(), T)
+        ok1, seed1 = pk.verify_batch([p0], [pub1.tobytes()], return_seed=True)
+        assert not ok1 and seed1 != seed0
+        assert seed1 == SP.batch_seed(vk, [p0], [pub1.tobytes()], T)
+        w2 = w.copy()
+        w2[32 * mid + 1] ^= 2
+        _, raw2, d2 = pk.prove(w2, pub)
+        r2, s2 = SP.derive_rs(w2.tobytes(), pub.tobytes(), T)
+        assert r2 != r0 and s2 != s0 and d2 == d0
+        assert raw2 == b"".join(expected_points(T, K, w2, pub, trap, arr([r2, s2])))
+    finally:
+        pk.close()
+
+
+def test_batch_verifier_rejects_compensated_inputs(ctx):
+    """with weights that did not commit to the public
+    inputs, pub_0[j] += d and pub_1[j] -= (rho_0 / rho_1) d would leave
+    sum_i rho_i z_ij unchanged and pass. The weights now hash every public
+    input, so the compensated pair (built from the honest weights) fails."""
+    from paper_2603_10242_b200 import groth16
+    T, K = 8, 3
+    rng = random.Random(99)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        vk = pk.verifying_key()
+        proofs, pubs = [], []
+        for _ in range(2):
+            w = arr([rng.randrange(R) for _ in range(T)])
+            pub = arr([rng.randrange(R) for _ in range(T)])
+            proofs.append(pk.prove(w, pub)[0])
+            pubs.append(pub.tobytes())
+        ok, seed = pk.verify_batch(proofs, pubs, return_seed=True)
+        assert ok and seed == SP.batch_seed(vk, proofs, pubs, T)
+        rho0, rho1 = SP.batch_rho(seed, 0), SP.batch_rho(seed, 1)
+        j, d = 3, 12345
+        q0 = int.from_bytes(pubs[0][32 * j:32 * j + 32], "little") % R
+        q1 = int.from_bytes(pubs[1][32 * j:32 * j + 32], "little") % R
+        n0 = (q0 + d) % R
+        n1 = (q1 - rho0 * pow(rho1, -1, R) * d) % R
+        assert (rho0 * n0 + rho1 * n1) % R == (rho0 * q0 + rho1 * q1) % R  # the old attack
+        e0 = bytearray(pubs[0]); e0[32 * j:32 * j + 32] = le(n0)
+        e1 = bytearray(pubs[1]); e1[32 * j:32 * j + 32] = le(n1)
+        ok2, seed2 = pk.verify_batch(proofs, [bytes(e0), bytes(e1)], return_seed=True)
+        assert seed2 != seed and not ok2
     finally:
         pk.close()
 
@@ -168,9 +242,7 @@ def test_groth16_block_shards(ctx, n, world):
             wa = np.frombuffer(b"".join(ws), np.uint8).copy()
             pr, raw, dg = pk.prove(wa, pa)
             # the chunk proof verifies (trapdoor oracle), with the derived r, s
-            tail = pubs[0] + pubs[-1] + T.to_bytes(4, "big")
-            r = int.from_bytes(hashlib.sha256(b"ace-g16-r-v1" + tail).digest(), "little") % R
-            s = int.from_bytes(hashlib.sha256(b"ace-g16-s-v1" + tail).digest(), "little") % R
+            r, s = SP.derive_rs(b"".join(ws), b"".join(pubs), T)
             wred = arr([int.from_bytes(x, "little") % R for x in ws])
             pred = arr([int.from_bytes(x, "little") % R for x in pubs])
             assert raw == b"".join(expected_points(T, K, wred, pred, trap, arr([r, s])))

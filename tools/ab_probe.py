@@ -40,9 +40,20 @@ def msm_ms(ctx, group, n):
     return ms, out
 
 
+def ntt_ms(ctx, L=22):
+    sp = torch.cuda.current_stream().cuda_stream
+    n = 1 << L
+    x = torch.from_numpy(bn254.random_scalars(n, 22)).cuda()
+    ctx.call("acegpu_bn_convert_dev", sp, 1, x.data_ptr(), n, 1)
+    y = torch.empty_like(x)
+    f = timed(lambda: ctx.call("acegpu_bn_ntt_dev", sp, x.data_ptr(), y.data_ptr(), L, 0, 0))
+    return f, y[:16].cpu().numpy().tobytes().hex()
+
+
 def main():
     ctx = N.context(0)
     r = {"tag": os.environ.get("AB_TAG", "")}
+    r["ntt_2^22_ms"], r["ntt_digest"] = ntt_ms(ctx)
     r["g1_2^20_ms"], r["g1_digest"] = msm_ms(ctx, 1, 1 << 20)
     r["g2_2^18_ms"], r["g2_digest"] = msm_ms(ctx, 2, 1 << 18)
     g = bench.bench_groth16(ctx, 0, bn254.mul_rate(0, ctx), chunks=2, reps=3)

@@ -21,6 +21,19 @@ __global__ void k(uint32_t* sink, uint32_t iters) {
                 if (MODE == 2) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(it));
                 if (MODE == 3) asm volatile("add.u32 %0, %0, %1;" : "+r"(a[j]) : "r"(m));
                 if (MODE == 5) asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dd[j]) : "d"(1.0000001), "d"(1e-9));
+                if (MODE == 6) {  // even warps DFMA, odd warps IMAD
+                    if ((threadIdx.x >> 5) & 1) asm volatile("mad.lo.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(it));
+                    else asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dd[j]) : "d"(1.0000001), "d"(1e-9));
+                }
+                if (MODE == 7) {  // even warps DFMA, odd warps IMAD.HI
+                    if ((threadIdx.x >> 5) & 1) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(it));
+                    else asm volatile("fma.rn.f64 %0, %0, %1, %2;" : "+d"(dd[j]) : "d"(1.0000001), "d"(1e-9));
+                }
+                if (MODE == 8) {  // even warps FFMA, odd warps IMAD.HI
+                    if ((threadIdx.x >> 5) & 1) asm volatile("mad.hi.u32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(m), "r"(it));
+                    else asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(0x3f800001u), "r"(0x3000000u));
+                }
+                if (MODE == 9) asm volatile("fma.rn.f32 %0, %0, %1, %2;" : "+r"(a[j]) : "r"(0x3f800001u), "r"(0x3000000u));
                 if (MODE == 4) asm volatile("{.reg .u32 t; mad.lo.cc.u32 %0, %0, %1, %2; madc.hi.u32 t, %0, %1, 0; add.u32 %0, %0, t;}" : "+r"(a[j]) : "r"(m), "r"(it));
             }
         }
@@ -58,5 +71,9 @@ int main() {
     printf("add.u32      %.3e /s\n", run<3>(sink));
     printf("lo.cc+hi chain(3 ops) %.3e /s\n", run<4>(sink));
     printf("fma.rn.f64   %.3e /s\n", run<5>(sink));
+    printf("DFMA|IMAD warps %.3e /s (sum of both)\n", run<6>(sink));
+    printf("DFMA|IMAD.HI warps %.3e /s (sum of both)\n", run<7>(sink));
+    printf("FFMA|IMAD.HI warps %.3e /s (sum of both)\n", run<8>(sink));
+    printf("fma.rn.f32   %.3e /s\n", run<9>(sink));
     return 0;
 }
