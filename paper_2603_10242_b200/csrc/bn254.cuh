@@ -293,7 +293,7 @@ __device__ __forceinline__ Fp<C> mul_f64(const Fp<C>& a, const Fp<C>& b) {
 }
 
 #ifndef ACEGPU_F64MUL
-#define ACEGPU_F64MUL 0  // 1: every mul() through the FP64 product
+#define ACEGPU_F64MUL 1  // 0: every mul() through the IMAD CIOS product (mul_cios)
 #endif
 template <class C>
 __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
