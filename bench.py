@@ -320,14 +320,41 @@ def run_ours(args, rank: int, world: int) -> None:
     ctx.call("acegpu_sha256_probe", 1, 32, 512, C.byref(lat))
     lat_us = lat.value / 512 * 1e6  # one warp's chained compression latency
     bn = None
-    if world == 1 and not args.no_bn254:
-        bn = bench_bn254(ctx, dev)
-        bn["groth16"] = bench_groth16(ctx, dev, bn["peaks"]["fq_mul_per_s"])
+    g16 = {}
+    g16_roof = None
+    if not args.no_bn254:
+        # north star: the Groth16 block path at every N (BASELINE configs[2], [3]),
+        # one proving key (9 GB, resident) for all of it
+        from paper_2603_10242_b200 import bn254, groth16
+        msm_in = {}
+        if world == 1:
+            bn = bench_bn254(ctx, dev, keep=msm_in)
+        fq_rate = bn["peaks"]["fq_mul_per_s"] if bn else bn254.mul_rate(0, ctx)
+        t0 = time.perf_counter()
+        pk = groth16.ProvingKey(groth16.PAPER_T, groth16.PAPER_K, ctx=ctx)
+        setup_s = time.perf_counter() - t0
+        chunk = bench_groth16(ctx, dev, fq_rate, pk)
+        chunk["setup_s_once"] = setup_s
+        if bn is not None:
+            bn["groth16"] = chunk
         fb16, revs16, rix16 = canonical_block_host(16384, ctx)
-        bn["groth16_block_16384"] = run_groth16_block(ctx, dev, fb16, revs16, rix16, 0, 1,
-                                                      steps=1, warmup=1)
-        if not args.no_cpu_baseline:
-            bn["cpu_oracle"] = bn254_cpu_baseline()
+        g16["16384"] = run_groth16_block(ctx, dev, fb16, revs16, rix16, rank, world, steps=3,
+                                         warmup=1, pk=pk)
+        g16["100000"] = run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps=3,
+                                          warmup=1, pk=pk, e2e=True, verify=True)
+        g16["100000"]["chunk_prove_ms_alone"] = chunk["chunk_prove_ms"]
+        wk = chunk["work"]
+        ach = wk["fq_mul_equivalents"] / (chunk["chunk_prove_ms"] * 1e-3)
+        g16_roof = {"bound": "fmaheavy issue pipe (IMAD / IMAD.HI / DFMA share it)",
+                    "kernel": "Groth16 chunk (bucket accumulations dominate: G1 + G2)",
+                    "achieved": ach / 1e9, "peak": fq_rate / 1e9, "unit": "G Fq-mul-equivalents/s",
+                    "frac": ach / fq_rate, "work_per_chunk": wk,
+                    "peak_source": "acegpu_bn_mul_rate: a chain of the library's own Fq product "
+                                   "(FP64 split), same run",
+                    "ncu": g16_ncu_summary()}
+        pk.close()
+        if world == 1 and not args.no_cpu_baseline:
+            bn["cpu_oracle"] = bn254_cpu_baseline(msm_in)
 
     stream = None
     if not args.no_stream:
@@ -367,18 +394,29 @@ def run_ours(args, rank: int, world: int) -> None:
     tree_c = 18 * (n - 1) + 2 * (n - 1)
     roof = None
     if phase:
-        ach = leaf_c / (phase[0] * 1e-3)
-        roof = {"bound": "int_alu", "kernel": "leaf_kernel (K1+K4 fused)",
-                "achieved": ach / 1e9, "peak": peak_cps / 1e9, "unit": "G SHA-256 compressions/s",
-                "frac": ach / peak_cps, "traffic": leaf_traffic_bytes(),
-                "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of "
-                                  "leaf_kernel, profiles/r01_ncu_full_leaf_credential_keytab.csv",
-                "algorithmic_bytes_per_launch": int(fb.offs[n]) + 104 * n + 4 * n + 320 * n + 32 * n,
-                "hbm_gbs_achieved": (int(fb.offs[n]) + 104 * n + 352 * n) / (phase[0] * 1e-3) / 1e9,
+        leaf_ach = leaf_c / (phase[0] * 1e-3)
+        tree_ach = tree_c / (phase[1] * 1e-3)
+        # dominant kernel BY TIME: the tree levels (level_kernel, 17 launches)
+        roof = {"bound": "int_alu (wide levels) / one 11-compression dependent chain per "
+                         "narrow level (latency)",
+                "kernel": "level_kernel (K2+K3 fused: proof tree + id_com Merkle), all levels",
+                "achieved": tree_ach / 1e9, "peak": peak_cps / 1e9,
+                "unit": "G SHA-256 compressions/s", "frac": tree_ach / peak_cps,
+                "traffic": level_traffic_bytes(),
+                "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum "
+                                  "summed over one step's level_kernel launches, "
+                                  "profiles/r01_ncu_full_levels.csv",
+                "algorithmic_compressions_per_step": tree_c,
                 "phase_ms": {"leaves": phase[0], "tree_levels": phase[1], "finalize": phase[2]},
-                "tree_frac_of_peak": tree_c / (phase[1] * 1e-3) / peak_cps,
                 "single_warp_compression_latency_us": lat_us,
-                "peak_source": "acegpu_sha256_peak register-resident microkernel, same run"}
+                "peak_source": "acegpu_sha256_peak register-resident microkernel, same run",
+                "secondary": {
+                    "kernel": "leaf_kernel (K1+K4 fused)", "achieved": leaf_ach / 1e9,
+                    "frac": leaf_ach / peak_cps, "traffic": leaf_traffic_bytes(),
+                    "traffic_source": "profiles/r01_ncu_full_leaf_credential_keytab.csv",
+                    "algorithmic_bytes_per_launch":
+                        int(fb.offs[n]) + 104 * n + 4 * n + 320 * n + 32 * n,
+                    "hbm_gbs_achieved": (int(fb.offs[n]) + 104 * n + 352 * n) / (phase[0] * 1e-3) / 1e9}}
     cpu = cpu_baseline(args, n)
     cl = clocks.summary()
     line = {
@@ -392,8 +430,13 @@ def run_ours(args, rank: int, world: int) -> None:
                 "d2h_bytes_per_step": d2h},
         "clocks": cl, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "parity": parity, "impl": "ours", "stream": stream, "phase1a_and_verify": phase1a,
-        "bn254": bn,
+        "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
+        "groth16_roofline": g16_roof, "bn254": bn,
     }
+    if world > 1 and os.environ.get("ACE_BENCH_SHARED_GPU"):
+        line["config"]["ranks_share_one_gpu"] = True
+        line["config"]["note"] = ("functional multi-rank run (gloo, every rank on cuda:0): "
+                                  "not a scaling measurement")
     print(json.dumps(line), flush=True)
 
 
@@ -463,7 +506,7 @@ def run_e2e(args, ctx, fb, revs, rev_index, rank, world, start, count, be, dev):
     return ms, h2d, d2h
 
 
-def bench_bn254(ctx, dev: int, reps: int = 5) -> dict:
+def bench_bn254(ctx, dev: int, reps: int = 5, keep: dict | None = None) -> dict:
     """BASELINE configs[1]: Fr NTT/iNTT 2^22 and G1 MSM 2^20 (device-resident,
     CUDA events on the launching stream), with the integer-pipe roofline."""
     import torch
@@ -520,6 +563,13 @@ def bench_bn254(ctx, dev: int, reps: int = 5) -> dict:
     res = torch.zeros(64, dtype=torch.uint8, device=f"cuda:{dev}")
     m_ms = timed(lambda: bases.run_dev(sc.data_ptr(), res.data_ptr(), sp), k=3)
     c_bits, windows = bn254.msm_params(ctx)
+    if keep is not None:  # the same bases / scalars for the CPU oracle's cross-check
+        keep["pts"], keep["scalars"] = pts, bn254.random_scalars(n, 2)
+        keep["gpu_result"] = bases.run(keep["scalars"])
+        keep["ntt_in"] = bn254.random_scalars(1 << L, 22)
+        d = keep["ntt_in"].copy()
+        ctx.call("acegpu_bn_ntt", d, L, 0, 0)
+        keep["ntt_gpu"] = d
     entries = windows * n  # nonzero signed digits (uniform scalars)
     fq_muls = entries * 10  # mixed XYZZ add = 8M + 2S (Fq-mul equivalents)
     out["msm_g1_2^20"] = {
@@ -580,59 +630,52 @@ def bench_stream(ctx, dev: int, blocks: int = 30, n: int = 12800, lanes: int = 8
         pp.close()
 
 
-def bench_groth16(ctx, dev: int, fq_rate: float, chunks: int = 16, reps: int = 3) -> dict:
-    """BASELINE configs[2] shape: 1,024-tx chunks x 1,400 constraints/tx
+def chunk_work(pk, ctx) -> dict:
+    """Algorithmic work of one chunk proof (Fq-mul equivalents: 10 per G1
+    mixed add, 30 per G2 mixed add (3 Fq muls per Fq2 product); Fr muls of
+    the 6 NTTs)."""
+    from paper_2603_10242_b200 import bn254
+    T = pk.T
+    V, Np = pk.variables, 1 << pk.log_domain
+    Vp = V - 1 - T
+    W = bn254.msm_params(ctx)[1]
+    g1_adds = W * ((V + 2) * 2 + Vp + 1 + Np)  # A, B1, L, H (coset-Lagrange, N points)
+    g2_adds = W * (V + 2)                       # B2
+    fr_muls = 6 * ((Np // 2) * pk.log_domain + Np)  # 3 iNTT + 3 coset NTT
+    return {"g1_mixed_adds": g1_adds, "g2_mixed_adds": g2_adds, "ntt_fr_muls": fr_muls,
+            "fq_mul_equivalents": g1_adds * 10 + g2_adds * 30 + fr_muls}
+
+
+def bench_groth16(ctx, dev: int, fq_rate: float, pk, reps: int = 5) -> dict:
+    """BASELINE configs[2] shape: one 1,024-tx chunk x 1,400 constraints
     (1,434,625 constraints, domain 2^21) of the synthetic ZK-ACE stand-in
-    circuit; per-chunk Groth16 on one GPU, then `chunks` back-to-back chunk
-    proofs (16 = a 16,384-tx block)."""
+    circuit, proven alone (device-resident inputs, CUDA events, median of
+    `reps` after one warm-up)."""
     import torch
-    from paper_2603_10242_b200 import bn254, groth16
-    T, K = groth16.PAPER_T, groth16.PAPER_K
-    t0 = time.perf_counter()
-    pk = groth16.ProvingKey(T, K, ctx=ctx)
-    torch.cuda.synchronize()
-    setup_s = time.perf_counter() - t0
+    from paper_2603_10242_b200 import bn254
+    T = pk.T
     s = torch.cuda.current_stream()
     sp = s.cuda_stream
-    w = torch.from_numpy(bn254.random_scalars(T * chunks, 31)).to(f"cuda:{dev}")
-    pub = torch.from_numpy(bn254.random_scalars(T * chunks, 32)).to(f"cuda:{dev}")
-    out = torch.zeros(chunks * 256, dtype=torch.uint8, device=f"cuda:{dev}")
+    w = torch.from_numpy(bn254.random_scalars(T, 31)).to(f"cuda:{dev}")
+    pub = torch.from_numpy(bn254.random_scalars(T, 32)).to(f"cuda:{dev}")
+    out = torch.zeros(256, dtype=torch.uint8, device=f"cuda:{dev}")
 
-    def one(i):
-        pk.prove_dev(w.data_ptr() + 32 * T * i, pub.data_ptr() + 32 * T * i,
-                     out.data_ptr() + 256 * i, stream=sp)
-    one(0)
+    def one():
+        pk.prove_dev(w.data_ptr(), pub.data_ptr(), out.data_ptr(), stream=sp)
+    one()
     torch.cuda.synchronize()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(reps)]
     for a, b in evs:
         a.record(s)
-        one(0)
+        one()
         b.record(s)
     torch.cuda.synchronize()
     chunk_ms = statistics.median(a.elapsed_time(b) for a, b in evs)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(s)
-    for i in range(chunks):
-        one(i)
-    b.record(s)
-    torch.cuda.synchronize()
-    block_ms = a.elapsed_time(b)
-    V, Np = pk.variables, 1 << pk.log_domain
-    Vp = V - 1 - T
-    W = bn254.msm_params(ctx)[1]
-    madds = W * ((V + 2) * 2 + Vp + 1 + Np)  # G1 MSMs: A, B1, L, H (coset-Lagrange, N points)
-    fq_muls = madds * 10 + W * (V + 2) * 10 * 3     # + G2 (Fq2 mul = 3 Fq muls)
-    fr_muls = 6 * ((Np // 2) * pk.log_domain + Np)  # 3 iNTT + 3 coset NTT
-    pk.close()
-    return {"txs_per_chunk": T, "constraints_per_tx": K, "constraints": pk.constraints,
-            "domain": Np, "setup_s_once": setup_s, "chunk_prove_ms": chunk_ms,
-            f"block_{T * chunks}_tx_ms": block_ms,
-            "proven_tx_per_s": T * chunks / (block_ms * 1e-3),
-            "field_muls_per_chunk": fq_muls + fr_muls,
-            "frac_of_fq_mul_peak": (fq_muls + fr_muls) / (chunk_ms * 1e-3) / fq_rate,
-            "extrapolated_100k_block_ms_1gpu": 98 * chunk_ms,
-            "extrapolated_100k_block_ms_8gpu": 13 * chunk_ms,
+    wk = chunk_work(pk, ctx)
+    return {"txs_per_chunk": T, "constraints_per_tx": pk.K, "constraints": pk.constraints,
+            "domain": 1 << pk.log_domain, "chunk_prove_ms": chunk_ms, "reps": reps,
+            "work": wk, "frac_of_fq_mul_peak": wk["fq_mul_equivalents"] / (chunk_ms * 1e-3) / fq_rate,
             "note": "synthetic stand-in circuit (oracle/bn254_oracle.h); proofs checked "
                     "bit-exact vs the known-trapdoor oracle in tests/test_gpu_groth16.py"}
 
@@ -652,16 +695,29 @@ def make_witnesses(fb, revs, rev_index, ctx) -> np.ndarray:
     return wit
 
 
-def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup, pk=None):
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """A page-locked host copy (acegpu_host_alloc) of a byte array."""
+    from paper_2603_10242_b200 import _native as N
+    nb = max(a.nbytes, 1)
+    p = N.lib().acegpu_host_alloc(nb)
+    arr = np.ctypeslib.as_array((C.c_uint8 * nb).from_address(p))
+    arr[:a.nbytes] = np.ascontiguousarray(a).view(np.uint8).reshape(-1)
+    return arr
+
+
+def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup, pk,
+                      e2e: bool = False, verify: bool = False):
     """The north-star block path: attestation + one Groth16 proof per aligned
     1,024-tx chunk (synthetic stand-in circuit, 1,400 constraints/tx) + the
-    reference's tree rule over chunk proofs + FC; sharded over `world` ranks."""
+    reference's tree rule over chunk proofs + FC, sharded over `world` ranks
+    (one all-gather of chunk roots). Device-resident inputs, CUDA events on
+    the launching stream, max over ranks. e2e: the same block through the
+    host-buffer C-ABI call acegpu_g16_prove_block (1 rank) / the rank's host
+    slice copied in + prove_sharded (N ranks), pinned buffers, every copy
+    inside the timed region."""
     import torch
     import torch.distributed as dist
-    from paper_2603_10242_b200 import groth16, shard
-    own = pk is None
-    if own:
-        pk = groth16.ProvingKey(groth16.PAPER_T, groth16.PAPER_K, ctx=ctx)
+    from paper_2603_10242_b200 import shard
     n = fb.n
     wit = make_witnesses(fb, revs, rev_index, ctx)
     parts = shard.partition(n, world, shard.LOG2_CHUNK) if world > 1 else [(0, n)]
@@ -674,76 +730,188 @@ def run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps, warmup,
 
     def step():
         return shard.prove_sharded(db, n, rank, world, shard.LOG2_CHUNK, be, codes=codes)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def maxed(ms):
+        if world > 1:
+            t = torch.tensor([ms], device=f"cuda:{dev}")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+        return ms
     for _ in range(warmup):
         step()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    barrier()
     times = []
-    for _ in range(steps):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(s)
-        proof, fc = step()
-        b.record(s)
+    with ClockSampler(dev) as clocks:
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            a.record(s)
+            proof, fc = step()
+            b.record(s)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b))
+    ms = maxed(statistics.mean(times))
+    chunks_total = -(-n // pk.T)
+    my_chunks = -(-count // pk.T)
+    fcb = fc.cpu().numpy().tobytes()
+    out = {"n_tx": n, "chunks": chunks_total, "chunks_on_busiest_rank": -(-chunks_total // world),
+           "latency_ms": ms, "latency_ms_per_step": times, "steps": steps, "warmup": warmup,
+           "proven_tx_per_s": n / (ms * 1e-3), "vs_400ms_interval": ms / 400.0,
+           "pipelined_ms_per_chunk_on_rank": statistics.mean(times) / max(my_chunks, 1),
+           "accepted": accepted_total(codes[:count], world),
+           "fc_sha256": hashlib_sha256(fcb), "clocks": clocks.summary(),
+           "timing": "CUDA events on the launching stream, device-resident inputs, max over ranks"}
+    if e2e:
+        out["e2e"] = groth16_block_e2e(ctx, dev, fb, revs, rev_index, wit, rank, world, start,
+                                       count, pk, be, fcb, steps, warmup)
+    if verify and world == 1:
+        # verify_finality_certificate in Groth16 mode (SURVEY 8f row 1): the
+        # host API (block H2D, public inputs recomputed, one batched pairing
+        # check of all chunk proofs, FC recomputed) vs the reference's O(N)
+        # re-prove
+        _, fc2, roots = shard.prove_sharded(db, n, 0, 1, shard.LOG2_CHUNK, be, codes=codes,
+                                            return_roots=True)
+        r = roots.cpu().numpy().tobytes()
+        proofs = b"".join(r[289 * k:289 * k + 256] for k in range(chunks_total))
+        fcb2 = fc2.cpu().numpy().tobytes()
+        pk.verify_finality_certificate(fcb2, fb, proofs)  # warm-up
+        vt = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            verdict = pk.verify_finality_certificate(fcb2, fb, proofs)
+            vt.append((time.perf_counter() - t0) * 1e3)
+        out["verify_fc"] = {"ms": statistics.median(vt), "verdict": verdict.name, "reps": 3,
+                            "chunk_proofs": chunks_total, "chunk_proof_bytes": 256 * chunks_total,
+                            "method": "batched pairing check of %d chunk proofs (%d Miller loops, "
+                                      "1 final exponentiation) + FC recompute, host buffers, "
+                                      "wall clock around the host call" % (chunks_total,
+                                                                          chunks_total + 3)}
+    return out
+
+
+def groth16_block_e2e(ctx, dev, fb, revs, rev_index, wit, rank, world, start, count, pk, be,
+                      fc_expect, steps, warmup):
+    """e2e of the Groth16 block: pinned host inputs -> device -> codes, root
+    proof and FC back in host memory, wall clock around each step (max over
+    ranks). 1 rank: ONE C-ABI call (acegpu_g16_prove_block)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2603_10242_b200 import shard
+    n = fb.n
+    b0, b1 = int(fb.offs[start]), int(fb.offs[start + count])
+    h_pay = pinned_copy(np.concatenate([fb.payloads[b0:b1], np.zeros(16, np.uint8)]))
+    h_offs = pinned_copy((fb.offs[start:start + count + 1] - b0).astype(np.uint64))
+    h_atts = pinned_copy(fb.atts[104 * start:104 * (start + count)])
+    h_hdr = pinned_copy(np.ascontiguousarray(fb.header, np.uint8))
+    h_revs = pinned_copy(revs)
+    h_rix = pinned_copy(np.ascontiguousarray(rev_index[start:start + count], np.uint32))
+    h_wit = pinned_copy(wit[256 * start:256 * (start + count)])
+    h_codes = pinned_copy(np.zeros(count, np.uint8))
+    h_out = pinned_copy(np.zeros(640, np.uint8))
+    h2d = (b1 - b0) + 8 * (count + 1) + 104 * count + 256 + revs.nbytes + 4 * count + 256 * count
+    d2h = count + 289 + 328
+    a = lambda x: x.ctypes.data  # noqa: E731
+    times = []
+    for k in range(warmup + steps):
         torch.cuda.synchronize()
-        times.append(a.elapsed_time(b))
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        if world == 1:
+            ctx.call("acegpu_g16_prove_block", pk.h, a(h_pay), a(h_offs), a(h_atts), n, a(h_hdr),
+                     a(h_revs), len(revs) // 32, a(h_rix), a(h_wit), a(h_codes), a(h_out),
+                     a(h_out) + 304, None)
+        else:
+            d = f"cuda:{dev}"
+            to = lambda x: torch.from_numpy(x).to(d, non_blocking=True)  # noqa: E731
+            db = shard.DeviceBlock(to(h_pay), to(h_offs.view(np.int64)), to(h_atts), to(h_hdr),
+                                   count, to(h_revs), to(h_rix.view(np.int32)))
+            db.witnesses = to(h_wit)
+            codes = torch.empty(max(count, 1), dtype=torch.uint8, device=d)
+            proof, fc = shard.prove_sharded(db, n, rank, world, shard.LOG2_CHUNK, be, codes=codes)
+            h_codes[:count] = codes[:count].cpu().numpy()
+            h_out[:289] = proof.cpu().numpy()
+            h_out[304:632] = fc.cpu().numpy()
+        dt = (time.perf_counter() - t0) * 1e3
+        if k >= warmup:
+            times.append(dt)
     ms = statistics.mean(times)
     if world > 1:
         t = torch.tensor([ms], device=f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    chunks_total = -(-n // 1024)
-    out = {"n_tx": n, "chunks": chunks_total, "latency_ms": ms, "proven_tx_per_s": n / (ms * 1e-3),
-           "vs_400ms_interval": ms / 400.0, "steps": steps,
-           "per_chunk_ms": ms / -(-chunks_total // world),
-           # the 100k block has 98 chunks -> 13 on the busiest of 8 ranks
-           "extrapolated_100k_block_ms_8gpu": 13 * ms / -(-chunks_total // world),
-           "accepted": accepted_total(codes[:count], world),
-           "fc_sha256": hashlib_sha256(fc.cpu().numpy().tobytes())}
-    if world == 1:
-        # verify_finality_certificate in Groth16 mode (SURVEY 8f row 1): the
-        # host API (block H2D, public inputs recomputed, one batched pairing
-        # check of the chunk proofs, FC recomputed) vs the reference's O(N)
-        # re-prove
-        _, fc2, roots = shard.prove_sharded(db, n, 0, 1, shard.LOG2_CHUNK, be, codes=codes,
-                                            return_roots=True)
-        chunks = -(-n // 1024)
-        r = roots.cpu().numpy().tobytes()
-        proofs = b"".join(r[289 * k:289 * k + 256] for k in range(chunks))
-        fcb = fc2.cpu().numpy().tobytes()
-        pk.verify_finality_certificate(fcb, fb, proofs)  # warm-up
-        vt = []
-        for _ in range(3):
-            t0 = time.perf_counter()
-            verdict = pk.verify_finality_certificate(fcb, fb, proofs)
-            vt.append((time.perf_counter() - t0) * 1e3)
-        out["verify_fc"] = {"ms": statistics.median(vt), "verdict": verdict.name,
-                            "method": "batched pairing check of %d chunk proofs (%d Miller loops, "
-                                      "1 final exponentiation) + FC recompute, host buffers"
-                                      % (chunks, chunks + 3)}
-    if own:
-        pk.close()
-    return out
+    return {"latency_ms": ms, "proven_tx_per_s": n / (ms * 1e-3), "steps": steps,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "fc_matches_device_path": h_out[304:632].tobytes() == fc_expect,
+            "accepted": int((h_codes[:count] == 0).sum()),
+            "api": "acegpu_g16_prove_block (one host-buffer C-ABI call)" if world == 1 else
+                   "rank slice H2D from pinned buffers + prove_sharded (all-gather) + D2H"}
 
 
-def leaf_traffic_bytes() -> float | None:
-    """DRAM bytes per leaf_kernel launch from the committed ncu capture."""
+def ncu_dram_bytes(name: str, kernel: str) -> tuple[float, int] | None:
+    """(sum of dram__bytes_read.sum + dram__bytes_write.sum, launches) over the
+    launches of `kernel` in the committed ncu capture profiles/<name>."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01_ncu_full_leaf_credential_keytab.csv")
+    path = os.path.join(ROOT, "profiles", name)
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     try:
         rows = list(csv.reader(open(path)))
         hdr, units = rows[0], rows[1]
+        tot, cnt = 0.0, 0
         for r in rows[2:]:
             d = dict(zip(hdr, r))
-            if "leaf_kernel" in d.get("Kernel Name", ""):
-                tot = 0.0
+            if kernel in d.get("Kernel Name", ""):
                 for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     tot += float(d[k].replace(",", "")) * scale[units[hdr.index(k)]]
-                return tot
+                cnt += 1
+        return (tot, cnt) if cnt else None
     except (OSError, KeyError, ValueError, IndexError):
-        pass
-    return None
+        return None
+
+
+def leaf_traffic_bytes() -> float | None:
+    """DRAM bytes per leaf_kernel launch from the committed ncu capture."""
+    r = ncu_dram_bytes("r01_ncu_full_leaf_credential_keytab.csv", "leaf_kernel")
+    return r[0] / r[1] if r else None
+
+
+def level_traffic_bytes() -> float | None:
+    """DRAM bytes of one step's level_kernel launches (all levels), from the
+    committed ncu capture of a full step (profiles/r02_ncu_levels_step.csv)."""
+    r = ncu_dram_bytes("r02_ncu_levels_step.csv", "level_kernel")
+    return r[0] if r else None
+
+
+def g16_ncu_summary() -> dict | None:
+    """fmaheavy-pipe utilisation and DRAM bytes of the Groth16 chunk's bucket
+    accumulation kernels from the committed ncu capture (one chunk)."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r02_ncu_g16_accumulate.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+    except OSError:
+        return None
+    hdr = rows[0]
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        if "accumulate" not in d.get("Kernel Name", ""):
+            continue
+        pick = {k: d.get(k) for k in hdr if k in (
+            "gpu__time_duration.sum", "sm__inst_executed_pipe_fmaheavy.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+            "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread")}
+        pick["kernel"] = d["Kernel Name"][:80]
+        out.append(pick)
+    return {"source": "profiles/r02_ncu_g16_accumulate.csv", "launches": out} if out else None
 
 
 def accepted_total(codes, world: int) -> int:
@@ -761,35 +929,56 @@ def hashlib_sha256(b: bytes) -> str:
     return hashlib.sha256(b).hexdigest()
 
 
-def bn254_cpu_baseline(dev_unused=None) -> dict | None:
-    """Framework CPU oracle (NOT the reference: it has no BN254 code) on a
-    bounded sample: NTT 2^20 and G1 MSM 2^14, all host threads."""
+def bn254_cpu_baseline(msm_in: dict) -> dict | None:
+    """Framework CPU oracle (NOT the reference: it has no BN254 code) at the
+    benched sizes, all host threads: Fr NTT 2^22 and G1 MSM 2^20 on the very
+    inputs the GPU ran (outputs cross-checked), plus the Groth16 chunk's CPU
+    cost from the measured component rates (bounded sample: one G2 MSM 2^16
+    and one NTT 2^21 are timed; the chunk's 5 MSMs and 6 NTTs are summed)."""
     so = os.path.join(ROOT, "oracle", "liboracle.so")
-    if not os.path.exists(so):
+    if not os.path.exists(so) or "pts" not in msm_in:
         return None
     L = C.CDLL(so)
     thr = os.cpu_count() or 1
-    from paper_2603_10242_b200 import bn254
-    logn = 20
-    data = bn254.random_scalars(1 << logn, 5)
+    from paper_2603_10242_b200 import bn254, groth16
+    vp = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    out = {"kind": "framework CPU oracle, not reference", "cores": thr,
+           "oracle": "oracle/bn254_oracle.c (plain C, 4 x 64-bit Montgomery, radix-2 NTT, "
+                     "window-8 bucket MSM)"}
+    d = msm_in["ntt_in"].copy()
     t0 = time.perf_counter()
-    L.bn_ntt(data.ctypes.data_as(C.c_void_p), C.c_uint32(logn), 0, 0, thr)
-    ntt_ms = (time.perf_counter() - t0) * 1e3
-    n = 1 << 14
-    ks = bn254.random_scalars(n, 6)
-    g = bn254.generator(1)
-    pts = np.zeros(64 * n, np.uint8)
-    L.bn_fixed_base_muls(1, g.ctypes.data_as(C.c_void_p), ks.ctypes.data_as(C.c_void_p),
-                         C.c_uint64(n), pts.ctypes.data_as(C.c_void_p), thr)
-    sc = bn254.random_scalars(n, 7)
+    L.bn_ntt(vp(d), C.c_uint32(22), 0, 0, thr)
+    out["ntt_2^22_ms"] = (time.perf_counter() - t0) * 1e3
+    out["ntt_2^22_matches_gpu"] = bool(np.array_equal(d, msm_in["ntt_gpu"]))
+    n = len(msm_in["scalars"]) // 32
     res = np.zeros(64, np.uint8)
     t0 = time.perf_counter()
-    L.bn_msm(1, pts.ctypes.data_as(C.c_void_p), sc.ctypes.data_as(C.c_void_p), C.c_uint64(n),
-             res.ctypes.data_as(C.c_void_p), thr)
-    msm_ms = (time.perf_counter() - t0) * 1e3
-    return {"kind": "framework CPU oracle, not reference", "cores": thr,
-            "ntt_2^20_ms": ntt_ms, "msm_g1_2^14_ms": msm_ms,
-            "sample": "one NTT 2^20 + one G1 MSM 2^14 (window-8 buckets)"}
+    L.bn_msm(1, vp(msm_in["pts"]), vp(msm_in["scalars"]), C.c_uint64(n), vp(res), thr)
+    out["msm_g1_2^20_ms"] = (time.perf_counter() - t0) * 1e3
+    out["msm_g1_2^20_matches_gpu"] = bool(np.array_equal(res, msm_in["gpu_result"]))
+    # chunk components: G2 MSM 2^16 and NTT 2^21, scaled to the chunk's sizes
+    n2 = 1 << 16
+    p2 = bn254.scalar_muls(2, bn254.generator(2), bn254.random_scalars(n2, 41))
+    s2 = bn254.random_scalars(n2, 42)
+    r2 = np.zeros(128, np.uint8)
+    t0 = time.perf_counter()
+    L.bn_msm(2, vp(p2), vp(s2), C.c_uint64(n2), vp(r2), thr)
+    g2_ms = (time.perf_counter() - t0) * 1e3
+    d21 = bn254.random_scalars(1 << 21, 43)
+    t0 = time.perf_counter()
+    L.bn_ntt(vp(d21), C.c_uint32(21), 0, 0, thr)
+    ntt21_ms = (time.perf_counter() - t0) * 1e3
+    T, K = groth16.PAPER_T, groth16.PAPER_K
+    V = 1 + T + T * (K + 1)
+    Vp = V - 1 - T
+    g1_pts = 2 * (V + 2) + (Vp + 1) + (1 << 21)
+    chunk_ms = (out["msm_g1_2^20_ms"] * g1_pts / n + g2_ms * (V + 2) / n2 + 6 * ntt21_ms)
+    out["groth16_chunk"] = {
+        "ms_estimate": chunk_ms, "g1_msm_points": g1_pts, "g2_msm_points": V + 2,
+        "ntt_2^21_count": 6, "g2_msm_2^16_ms": g2_ms, "ntt_2^21_ms": ntt21_ms,
+        "sample": "timed: G1 MSM 2^20 (above), G2 MSM 2^16, NTT 2^21; the paper-size chunk's "
+                  "CPU time = those rates x its MSM sizes + 6 NTTs (linear in points)"}
+    return out
 
 
 def cpu_baseline(args, n: int) -> dict | None:
@@ -927,14 +1116,17 @@ def run_groth16_mode(args, rank: int, world: int) -> None:
     """`--mode groth16`: the 100k-tx block with Groth16 chunk proofs at N GPUs
     (BASELINE configs[3]); latency vs the 400 ms block interval."""
     import torch
-    from paper_2603_10242_b200 import _native as N
+    from paper_2603_10242_b200 import _native as N, groth16
     dev = bench_device()
     torch.cuda.set_device(dev)
     ctx = N.context(dev)
     fb, revs, rix = canonical_block_host(args.n_tx, ctx)
-    steps, warmup = min(args.steps, 3), min(args.warmup, 1)
+    steps, warmup = max(min(args.steps, 5), 3), 1
+    pk = groth16.ProvingKey(groth16.PAPER_T, groth16.PAPER_K, ctx=ctx)
     with ClockSampler(dev) as clocks:
-        r = run_groth16_block(ctx, dev, fb, revs, rix, rank, world, steps, warmup)
+        r = run_groth16_block(ctx, dev, fb, revs, rix, rank, world, steps, warmup, pk,
+                              e2e=True, verify=True)
+    pk.close()
     if rank != 0:
         return
     print(json.dumps({
@@ -947,6 +1139,29 @@ def run_groth16_mode(args, rank: int, world: int) -> None:
                                                     "x 1,400 constraints (synthetic stand-in circuit)",
                                         "parallelism": f"chunk-sharded x{world}"},
         "groth16": r, "clocks": clocks.summary(), "impl": "ours", "mode": "groth16"}), flush=True)
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` without a launcher: re-exec this command under
+    torch.distributed.run with N ranks (127.0.0.1). With fewer GPUs than ranks
+    (a functional run), every rank uses cuda:0 over gloo and the line says so."""
+    import socket
+    env = dict(os.environ)
+    try:
+        import torch
+        ngpu = torch.cuda.device_count()
+    except Exception:
+        ngpu = 0
+    if ngpu < n:
+        env.update({"ACE_BENCH_DEVICE": "0", "ACE_DIST_BACKEND": "gloo",
+                    "ACE_BENCH_SHARED_GPU": "1"})
+        log(f"bench.py: {n} ranks on {ngpu} GPU(s): functional run, gloo, all ranks on cuda:0")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)]
+    return subprocess.call(cmd + sys.argv[1:], env=env)
 
 
 def main():
@@ -965,8 +1180,12 @@ def main():
                          "groth16: the north-star chunk-Groth16 block path")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

@@ -325,6 +325,21 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                const uint8_t* d_witness256, uint8_t* d_roots289,
                                uint8_t* d_merkle32);
 
+/* The north-star block path through ONE host-buffer call (the Groth16-mode
+ * prove_block + build_finality_certificate, prover.cpp:129-156): the block's
+ * H2D, batched attestation verdicts (revs / rev_index as
+ * acegpu_attest_prove_certify; n_revs = 0 skips them), one Groth16 proof per
+ * aligned chunk of T txs over the n x 256-B build_witness records
+ * (prover.cpp:181-188), the reference's tree rule over the chunk proofs
+ * (prover.cpp:106-127) and the FC; D2H of codes (n), the root proof (289 B:
+ * bytes | digest | kind), the FC (328 B) and, if chunk_proofs256 is not NULL,
+ * the ceil(n / T) chunk proofs (256 B each, acegpu_g16_verify_fc's input). */
+int acegpu_g16_prove_block(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* payloads,
+                           const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                           const uint8_t* header256, const uint8_t* revs, uint64_t n_revs,
+                           const uint32_t* rev_index, const uint8_t* witness256, uint8_t* codes,
+                           uint8_t* proof289, uint8_t* fc328, uint8_t* chunk_proofs256);
+
 /* Optimal ate pairing product prod_i e(P_i, Q_i) (final exponentiation
  * included) over host buffers in the oracle encodings: G1 = x|y, G2 =
  * x.c0|x.c1|y.c0|y.c1, 32-B little-endian standard form, all-zero = infinity.

@@ -83,6 +83,8 @@ _SIGS = {
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_vk": (C.c_int, [ctxp, C.c_void_p, vp]),
     "acegpu_g16_verify_batch": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int)]),
+    "acegpu_g16_prove_block": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, u64, vp, vp, u64, vp, vp,
+                                         vp, vp, vp, vp]),
     "acegpu_g16_verify_batch_seed": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int),
                                                vp]),
     "acegpu_g16_verify_fc": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, u64, vp, vp, u64p,

@@ -60,7 +60,7 @@ int fail(int code, const std::string& msg) {
 enum Slot {
     kPayloads, kOffs, kAtts, kHeader, kRevs, kRevIdx, kCodes, kNodesA, kNodesB, kMerkA, kMerkB,
     kBlockHash, kOut, kIn2, kMisc, kBnA, kBnB, kBnOut, kBnScratch, kSegRoots, kSegMerk,
-    kKeytab, kKeydom, kP1Scratch, kP1Hash, kP1Reg, kErr, kNumSlots
+    kKeytab, kKeydom, kP1Scratch, kP1Hash, kP1Reg, kErr, kG16Wit, kG16Roots, kNumSlots
 };
 
 struct DevBuf {
@@ -2298,16 +2298,13 @@ int g16_chunk_inputs(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
 }
 }  // namespace
 
-extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
-                                          const uint8_t* d_payloads, const uint64_t* d_offs,
-                                          const uint8_t* d_atts, uint64_t n, uint64_t n_total,
-                                          const uint8_t* d_revs, uint64_t n_revs,
-                                          const uint32_t* d_rev_index, uint8_t* d_codes,
-                                          const uint8_t* d_witness256, uint8_t* d_roots289,
-                                          uint8_t* d_merkle32) {
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard guard(c->device);
-    cudaStream_t s = pick(c, stream);
+namespace {
+int g16_shard_roots_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g,
+                           const uint8_t* d_payloads, const uint64_t* d_offs,
+                           const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                           const uint8_t* d_revs, uint64_t n_revs, const uint32_t* d_rev_index,
+                           uint8_t* d_codes, const uint8_t* d_witness256, uint8_t* d_roots289,
+                           uint8_t* d_merkle32) {
     KeytabScope kts(c);  // attest keys for the credential verdicts (as the mock shard)
     if (d_codes && n) RET(kts.build(s, d_revs, n_revs, d_atts + 64));
     const uint32_t T = g->d.T;
@@ -2334,6 +2331,64 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
         CKL();
         c->launches += 2;
     }
+    return ACEGPU_OK;
+}
+}  // namespace
+
+extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                          const uint8_t* d_payloads, const uint64_t* d_offs,
+                                          const uint8_t* d_atts, uint64_t n, uint64_t n_total,
+                                          const uint8_t* d_revs, uint64_t n_revs,
+                                          const uint32_t* d_rev_index, uint8_t* d_codes,
+                                          const uint8_t* d_witness256, uint8_t* d_roots289,
+                                          uint8_t* d_merkle32) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_shard_roots_locked(c, pick(c, stream), g, d_payloads, d_offs, d_atts, n, n_total,
+                                  d_revs, n_revs, d_rev_index, d_codes, d_witness256, d_roots289,
+                                  d_merkle32);
+}
+
+extern "C" int acegpu_g16_prove_block(acegpu_ctx* c, acegpu_g16* g, const uint8_t* payloads,
+                                      const uint64_t* offs, const uint8_t* atts, uint64_t n,
+                                      const uint8_t* header256, const uint8_t* revs,
+                                      uint64_t n_revs, const uint32_t* rev_index,
+                                      const uint8_t* witness256, uint8_t* codes,
+                                      uint8_t* proof289, uint8_t* fc328,
+                                      uint8_t* chunk_proofs256) {
+    if (!g || !header256 || !witness256) return fail(ACEGPU_EINVAL, "null argument");
+    if (n == 0) return fail(ACEGPU_EINVAL, "g16 prove_block: empty block");
+    if (n_revs && (!revs || !rev_index)) return fail(ACEGPU_EINVAL, "revs without rev_index");
+    RET(check_n(n));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    const uint64_t T = g->d.T, chunks = (n + T - 1) / T;
+    uint8_t *dp, *da, *dh, *dw, *dcodes = nullptr, *drevs = nullptr, *roots;
+    uint64_t* doff;
+    uint32_t* drix = nullptr;
+    RET(upload_block(c, s, {payloads, offs, atts, n}, &dp, &doff, &da));
+    RET(h2d_t(c, kHeader, header256, 256, s, &dh));
+    RET(h2d_t(c, kG16Wit, witness256, 256 * n, s, &dw));
+    if (n_revs) {
+        RET(h2d_t(c, kRevs, revs, 32 * n_revs, s, &drevs));
+        RET(h2d_t(c, kRevIdx, rev_index, 4 * n, s, &drix));
+        RET(ws(c, kCodes, n, &dcodes));
+    }
+    auto al = [](uint64_t b) { return (b + 255) & ~uint64_t(255); };
+    RET(ws(c, kG16Roots, al(289 * chunks) + al(32 * chunks) + 640, &roots));
+    uint8_t* merk = roots + al(289 * chunks);
+    uint8_t* out = merk + al(32 * chunks);
+    RET(g16_shard_roots_locked(c, s, g, dp, doff, da, n, n, drevs, n_revs, drix, dcodes, dw,
+                               roots, merk));
+    RET(combine_impl(c, s, roots, merk, chunks, n, dh, out, out + 304));
+    if (codes && dcodes) CK(cudaMemcpyAsync(codes, dcodes, n, cudaMemcpyDeviceToHost, s));
+    if (proof289) CK(cudaMemcpyAsync(proof289, out, 289, cudaMemcpyDeviceToHost, s));
+    if (fc328) CK(cudaMemcpyAsync(fc328, out + 304, 328, cudaMemcpyDeviceToHost, s));
+    if (chunk_proofs256)
+        CK(cudaMemcpy2DAsync(chunk_proofs256, 256, roots, 289, 256, chunks, cudaMemcpyDeviceToHost,
+                             s));
+    CK(cudaStreamSynchronize(s));
     return ACEGPU_OK;
 }
 

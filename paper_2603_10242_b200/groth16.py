@@ -51,6 +51,25 @@ class ProvingKey:
         self.ctx.call("acegpu_g16_prove_chunk_dev", stream, self.h, d_w, d_pub, d_rs, d_proof,
                       d_raw, d_digest)
 
+    def prove_block(self, block, witnesses: np.ndarray, revs=None, rev_index=None):
+        """The Groth16-mode prove_block + FC through one host-buffer call
+        (acegpu_g16_prove_block): -> (codes, proof289, fc328, chunk proofs
+        (ceil(n/T) x 256 B)). witnesses: n x 256-B build_witness records."""
+        from .prover import _flat
+        fb = _flat(block)
+        n = fb.n
+        chunks = -(-n // self.T)
+        codes = np.zeros(max(n, 1), np.uint8)
+        proof = np.zeros(289, np.uint8)
+        fc = np.zeros(328, np.uint8)
+        cps = np.zeros(256 * max(chunks, 1), np.uint8)
+        nrev = 0 if revs is None else len(revs) // 32
+        rix = None if rev_index is None else np.ascontiguousarray(rev_index, np.uint32)
+        self.ctx.call("acegpu_g16_prove_block", self.h, fb.payloads, fb.offs, fb.atts, n,
+                      np.ascontiguousarray(fb.header, np.uint8), revs, nrev, rix,
+                      np.ascontiguousarray(witnesses, np.uint8), codes, proof, fc, cps)
+        return codes[:n], proof.tobytes(), fc.tobytes(), cps[:256 * chunks].tobytes()
+
     def verifying_key(self) -> bytes:
         """alpha G1 | beta G2 | gamma G2 | delta G2 | IC_0..IC_T (oracle encoding)."""
         out = np.zeros(448 + 64 * (self.T + 1), np.uint8)

@@ -153,12 +153,17 @@ def gather_roots(roots, merk, counts: list[int], group=None):
     pm = torch.zeros(mx * 32, dtype=torch.uint8, device=merk.device)
     pr[:roots.numel()] = roots
     pm[:merk.numel()] = merk
+    dev = pr.device
+    if dist.get_backend(group) == "gloo" and dev.type == "cuda":
+        # gloo (the CPU-side functional runs: ranks sharing one GPU) gathers
+        # host tensors; NCCL gathers the device tensors directly
+        pr, pm = pr.cpu(), pm.cpu()
     gr = [torch.empty_like(pr) for _ in range(world)]
     gm = [torch.empty_like(pm) for _ in range(world)]
     dist.all_gather(gr, pr, group=group)
     dist.all_gather(gm, pm, group=group)
-    allr = torch.cat([g[:c * 289] for g, c in zip(gr, counts)])
-    allm = torch.cat([g[:c * 32] for g, c in zip(gm, counts)])
+    allr = torch.cat([g[:c * 289] for g, c in zip(gr, counts)]).to(dev)
+    allm = torch.cat([g[:c * 32] for g, c in zip(gm, counts)]).to(dev)
     return allr, allm
 
 

@@ -88,7 +88,7 @@ def main() -> None:
 
     # --- canonical blocks: root digest, SHA(root proof), SHA(FC)
     blocks = {}
-    for n in (0, 1, 2, 3, 5, 7, 100, 1024, 1025, 4097, 16384, 100000):
+    for n in (0, 1, 2, 3, 5, 7, 100, 1000, 1024, 1025, 4097, 6250, 16384, 100000):
         fb = O.canonical_block(n)
         root, lv, pr = O.ref_prove_block(fb)
         fc = O.ref_prove_and_certify(fb)

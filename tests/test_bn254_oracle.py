@@ -212,3 +212,35 @@ def test_groth16_pairing_verify_known_trapdoor():
     assert L.bn_g16_verify(T, vk, O.ptr(proof), O.ptr(bytes(bad))) == 0
     forged = _smul(1, g1, a + 1) + proof[64:]
     assert L.bn_g16_verify(T, vk, O.ptr(forged), O.ptr(pub)) == 0
+
+
+def test_eip196_197_vectors_pin_the_oracle():
+    """External pin: the published EIP-196 ecAdd / ecMul and
+    EIP-197 ecPairing vectors (tests/golden/eip196_197.json) hold on the
+    oracle — encodings, generators, the twist and the pairing all agree with
+    Ethereum's BN254."""
+    import eip_vectors as E
+    L = O.oracle()
+    d = E.load()
+    for v in d["ecadd"]:
+        a, b, exp = E.ecadd(v)
+        o = O.buf(64)
+        L.bn_point_add(1, O.ptr(a), O.ptr(b), o)
+        assert bytes(o) == exp, v["name"]
+    for v in d["ecmul"]:
+        p, k, exp = E.ecmul(v)
+        o = O.buf(64)
+        L.bn_scalar_mul(1, O.ptr(p), O.ptr(k), o)
+        assert bytes(o) == exp, v["name"]
+    for v in d["ecpairing"]:
+        n, a, b, exp = E.ecpairing(v)
+        assert L.bn_pairing_check(C.c_uint64(n), O.ptr(a), O.ptr(b)) == exp, v["name"]
+        # a changed statement fails: the first G1 point doubled
+        d1 = O.buf(64)
+        L.bn_point_double(1, O.ptr(a[:64]), d1)
+        assert L.bn_pairing_check(C.c_uint64(n), O.ptr(bytes(d1) + a[64:]), O.ptr(b)) == 0
+    # jeff1's second G2 point is the EIP-197 generator: the oracle's generator
+    n, a, b, _ = E.ecpairing(d["ecpairing"][0])
+    g2 = O.buf(128)
+    L.bn_generator(2, g2)
+    assert b[128:256] == bytes(g2)

@@ -90,26 +90,37 @@ def test_ntt_small_vs_naive_dft(ctx):
 
 @pytest.mark.parametrize("logn", [20, 22])
 def test_ntt_large_roundtrip_and_oracle(ctx, logn):
-    """2^22 (BASELINE configs[1]) and 2^20: iNTT(NTT(x)) = x, coset round trip,
-    linearity, and (2^20) bit-exact vs the oracle."""
+    """2^22 (BASELINE configs[1]) and 2^20: forward, inverse and coset-forward
+    transforms each bit-exact vs the oracle's radix-2 NTT (multi-threaded,
+    ~1 s at 2^22), plus iNTT(NTT(x)) = x and the coset round trip."""
+    import os
+    thr = C.c_int(os.cpu_count() or 8)
     rng = np.random.default_rng(logn)
     n = 1 << logn
     raw = rng.integers(0, 2**63, size=(n, 4), dtype=np.uint64)
     raw[:, 3] &= (1 << 61) - 1  # < 2^253 < r: canonical
-    data = raw.view(np.uint8).reshape(-1).copy()
-    orig = data.copy()
+    orig = raw.view(np.uint8).reshape(-1).copy()
+
+    def oracle(x, inverse, coset):
+        y = x.copy()
+        O.oracle().bn_ntt((C.c_uint8 * (32 * n)).from_buffer(y), C.c_uint32(logn),
+                          C.c_int(inverse), C.c_int(coset), thr)
+        return y
+    data = orig.copy()
     ctx.call("acegpu_bn_ntt", data, logn, 0, 0)
     fwd = data.copy()
     assert not np.array_equal(fwd, orig)
+    assert np.array_equal(fwd, oracle(orig, 0, 0)), "forward"
+    inv = orig.copy()
+    ctx.call("acegpu_bn_ntt", inv, logn, 1, 0)
+    assert np.array_equal(inv, oracle(orig, 1, 0)), "inverse"
+    cos = orig.copy()
+    ctx.call("acegpu_bn_ntt", cos, logn, 0, 1)
+    assert np.array_equal(cos, oracle(orig, 0, 1)), "coset forward"
     ctx.call("acegpu_bn_ntt", data, logn, 1, 0)
     assert np.array_equal(data, orig)
-    ctx.call("acegpu_bn_ntt", data, logn, 0, 1)
-    ctx.call("acegpu_bn_ntt", data, logn, 1, 1)
-    assert np.array_equal(data, orig)
-    if logn == 20:
-        buf = (C.c_uint8 * (32 * n)).from_buffer(orig)
-        O.oracle().bn_ntt(buf, C.c_uint32(logn), C.c_int(0), C.c_int(0), C.c_int(8))
-        assert np.array_equal(orig, fwd)
+    ctx.call("acegpu_bn_ntt", cos, logn, 1, 1)
+    assert np.array_equal(cos, orig)
 
 
 def g_gen(group):
@@ -237,3 +248,28 @@ def test_integer_peaks_positive(ctx):
     for f in (0, 1):
         ctx.call("acegpu_bn_mul_rate", f, C.byref(v))
         assert v.value > 1e9
+
+
+def test_eip196_vectors_on_gpu(ctx):
+    """EIP-196 ecMul / ecAdd vectors (tests/golden/eip196_197.json) through the
+    GPU: scalar multiplication (acegpu_bn_scalar_muls) and a 2-point MSM with
+    unit scalars (the bucket additions)."""
+    import eip_vectors as E
+    from paper_2603_10242_b200 import bn254
+    d = E.load()
+    for v in d["ecmul"]:
+        p, k, exp = E.ecmul(v)
+        out = bn254.scalar_muls(1, np.frombuffer(p, np.uint8).copy(),
+                                np.frombuffer(k, np.uint8).copy(), ctx)
+        assert out.tobytes() == exp, v["name"]
+    one = np.frombuffer((1).to_bytes(32, "little") * 2, np.uint8).copy()
+    for v in d["ecadd"]:
+        a, b, exp = E.ecadd(v)
+        if a == b:  # the doubling vector: MSM of one point with scalar 2
+            bases = bn254.MsmBases(1, np.frombuffer(a, np.uint8).copy(), 1, ctx=ctx)
+            got = bases.run(np.frombuffer((2).to_bytes(32, "little"), np.uint8).copy())
+        else:
+            bases = bn254.MsmBases(1, np.frombuffer(a + b, np.uint8).copy(), 2, ctx=ctx)
+            got = bases.run(one)
+        bases.close()
+        assert got.tobytes() == exp, v["name"]

@@ -444,6 +444,35 @@ def test_groth16_verify_finality_certificate(ctx, n):
         pk.close()
 
 
+@pytest.mark.parametrize("n", [1, 11, 37])
+def test_groth16_prove_block_host_call(ctx, n):
+    """acegpu_g16_prove_block (one host-buffer call: H2D, verdicts, chunk
+    proofs, tree, FC, D2H) == the device-resident shard path, and its chunk
+    proofs verify the FC (verify_finality_certificate in Groth16 mode)."""
+    from paper_2603_10242_b200 import groth16, prover, shard, wire
+    T, K = 4, 3
+    rng = random.Random(3 * n)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        fb = O.multi_user_block(n, 3)
+        wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+        wit = _witnesses(fb, n)
+        proof, fc, roots = shard.prove_sharded_single_process(wfb, 1, 2, ctx, pk=pk, witnesses=wit,
+                                                              return_roots=True)
+        codes, p2, fc2, cps = pk.prove_block(wfb, wit, np.frombuffer(fb.revs, np.uint8).copy(),
+                                             np.asarray(fb.rev_index, np.uint32))
+        assert p2 == proof and fc2 == fc
+        assert (codes == 0).all()
+        chunks = (n + T - 1) // T
+        assert cps == b"".join(roots[289 * k:289 * k + 256] for k in range(chunks))
+        assert pk.verify_finality_certificate(fc2, wfb, cps) == prover.FcCheck.Valid
+        c3, p3, fc3, _ = pk.prove_block(wfb, wit)  # no REVs: verdicts skipped, proof unchanged
+        assert p3 == proof and fc3 == fc
+    finally:
+        pk.close()
+
+
 def test_groth16_mode_attestation_verdicts(ctx):
     """Groth16 mode runs the same batched HKDF/HMAC attestation check as the
     hash-proof path: per-tx verdicts are identical to the mock shard's (and

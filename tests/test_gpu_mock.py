@@ -416,13 +416,16 @@ def test_prover_service_and_counters(P):
                                  (4097, 10), (6250, 8), (100000, 10)])
 def test_shards_combine_to_global(P, kats, n, k):
     """aligned 2^k chunks proven shard-by-shard combine to the
-    single-GPU root and FC bit-exactly (ranks emulated one after another)."""
+    single-GPU root and FC bit-exactly (ranks emulated one after another), and
+    both equal the FC the reference itself printed for this block (kats)."""
     from paper_2603_10242_b200 import shard
     fb = O.canonical_block(n)
     world = 4
     proof, fc = shard.prove_sharded_single_process(to_wire_flat(P, fb), world, k, P.ctx)
     gproof, gfc, _, _, _ = gpu_block(P, fb, codes=False)
     assert proof == gproof and fc == gfc
+    g = kats["canonical_blocks"][str(n)]
+    assert fc.hex() == g["fc"] and proof[256:288].hex() == g["root_digest"]
 
 
 def test_segmented_pipeline_equals_single_pass(P):

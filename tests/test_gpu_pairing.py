@@ -141,3 +141,18 @@ def test_pairing_g2_generator_multiples(M):
     ps = [smul(1, g1, k) for k in (2, 3, 11)]
     qs = [smul(2, g2, k) for k in (5, 7, 13)]
     assert gpu_pair(M, ps, qs)[0] == cpu_pair(ps, qs)
+
+
+def test_eip197_vector_on_gpu(M):
+    """The EIP-197 ecPairing vector (tests/golden/eip196_197.json, jeff1)
+    checks to 1 on the GPU pairing, and a changed statement does not."""
+    import eip_vectors as E
+    for v in E.load()["ecpairing"]:
+        n, a, b, exp = E.ecpairing(v)
+        ps = [a[64 * k:64 * k + 64] for k in range(n)]
+        qs = [b[128 * k:128 * k + 128] for k in range(n)]
+        f, one = gpu_pair(M, ps, qs)
+        assert one == exp and f == cpu_pair(ps, qs)
+        d1 = O.buf(64)
+        O.oracle().bn_point_double(1, O.ptr(ps[0]), d1)
+        assert gpu_pair(M, [bytes(d1)] + ps[1:], qs)[1] == 0
