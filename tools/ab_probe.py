@@ -56,8 +56,11 @@ def main():
     r["ntt_2^22_ms"], r["ntt_digest"] = ntt_ms(ctx)
     r["g1_2^20_ms"], r["g1_digest"] = msm_ms(ctx, 1, 1 << 20)
     r["g2_2^18_ms"], r["g2_digest"] = msm_ms(ctx, 2, 1 << 18)
-    g = bench.bench_groth16(ctx, 0, bn254.mul_rate(0, ctx), chunks=2, reps=3)
+    from paper_2603_10242_b200 import groth16
+    pk = groth16.ProvingKey(groth16.PAPER_T, groth16.PAPER_K, ctx=ctx)
+    g = bench.bench_groth16(ctx, 0, bn254.mul_rate(0, ctx), pk, reps=3)
     r["chunk_ms"] = g["chunk_prove_ms"]
+    pk.close()
     print(json.dumps(r))
 
 

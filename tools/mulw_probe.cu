@@ -248,7 +248,9 @@ void run(const Fq* a, const Fq* b, uint32_t n, uint32_t* bad, uint32_t* sink, in
 
 }  // namespace
 
-int main() {
+int main2();
+int main(int argc, char**) {
+    if (argc > 1) return main2();
     int sms;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const uint32_t n = 1 << 16;
@@ -272,5 +274,59 @@ int main() {
     run<2>(a, b, n, bad, sink, sms);
     run<3>(a, b, n, bad, sink, sms);
     run<4>(a, b, n, bad, sink, sms);
+    return 0;
+}
+
+// ---- call-shape probe: the MSM calls its products out of line, one at a time
+namespace callshape {
+__device__ __noinline__ Fq mul1_call(const Fq a, const Fq b) { return f64m::mul_f64(a, b); }
+struct Fq2v { Fq a, b; };
+__device__ __noinline__ Fq2v mul2_call(const Fq a, const Fq b, const Fq c, const Fq d) {
+    return {f64m::mul_f64(a, b), f64m::mul_f64(c, d)};
+}
+__device__ __noinline__ Fq cios1_call(const Fq a, const Fq b) { return mul(a, b); }
+
+template <int MODE>  // 0: f64 1 chain/call, 1: f64 2 chains/call, 2: cios 1 chain/call
+__global__ void __launch_bounds__(128) k(uint32_t* sink, uint32_t iters) {
+    Fq x = Fq::one(), z = Fq::one(), y = Fq::one();
+    y.v[0] ^= blockIdx.x;
+    x.v[1] ^= threadIdx.x;
+    z.v[2] ^= threadIdx.x;
+    for (uint32_t it = 0; it < iters; ++it) {
+        if (MODE == 0) { x = mul1_call(x, y); z = mul1_call(z, y); }
+        if (MODE == 1) { Fq2v r = mul2_call(x, y, z, y); x = r.a; z = r.b; }
+        if (MODE == 2) { x = cios1_call(x, y); z = cios1_call(z, y); }
+    }
+    if ((x.v[0] ^ z.v[0]) == 0x1234567u) sink[0] = 1;
+}
+template <int MODE>
+void run(uint32_t* sink, int sms) {
+    for (int per_sm : {2, 4, 8, 16}) {
+        const int blocks = sms * per_sm;
+        const uint32_t iters = 256;
+        k<MODE><<<blocks, 128>>>(sink, 4);
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        k<MODE><<<blocks, 128>>>(sink, iters);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("callshape %d ctas/sm=%2d (128 thr): %.2f G mul/s\n", MODE, per_sm,
+               double(blocks) * 128 * iters * 2 / (ms * 1e-3) / 1e9);
+    }
+}
+}  // namespace callshape
+
+int main2() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    uint32_t* sink;
+    cudaMalloc(&sink, 4);
+    callshape::run<0>(sink, sms);
+    callshape::run<1>(sink, sms);
+    callshape::run<2>(sink, sms);
     return 0;
 }
