@@ -907,6 +907,8 @@ def g16_ncu_summary() -> dict | None:
             "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
             "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+            "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
             "sm__inst_executed.avg.per_cycle_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread")}
         pick["kernel"] = d["Kernel Name"][:80]
