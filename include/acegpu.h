@@ -276,6 +276,38 @@ int acegpu_g16_prove_chunk_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, con
                                const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                                uint8_t* d_raw256, uint8_t* d_digest32);
 
+/* ---- general rank-1 constraint systems (north-star witness / constraint
+ * evaluation; r1cs.cu). m rows <A_j, z> * <B_j, z> = <C_j, z> over `vars`
+ * variables, z_0 = ONE, z_1..z_{n_pub} the public inputs. Each matrix k
+ * (0 = A, 1 = B, 2 = C) in CSR: rowptr[k] (m + 1 u64, rowptr[k][0] = 0),
+ * cols[k] (u32 < vars), vals[k] (32-B little-endian integers, reduced mod r
+ * on load). The library appends one z_i * 0 = 0 row per public variable
+ * i = 0..n_pub (Groth16 needs the public u_i independent): rows = m + n_pub + 1.
+ * eval: a, b, c = A z, B z, C z over all rows (standard form; any of them
+ * may be NULL) — the satisfiability check is a_j b_j = c_j. */
+typedef struct acegpu_r1cs acegpu_r1cs;
+int acegpu_r1cs_create(acegpu_ctx* ctx, uint64_t m, uint64_t vars, uint64_t n_pub,
+                       const uint64_t* const rowptr[3], const uint32_t* const cols[3],
+                       const uint8_t* const vals[3], acegpu_r1cs** out);
+void acegpu_r1cs_free(acegpu_r1cs* r);
+int acegpu_r1cs_shape(const acegpu_r1cs* r, uint64_t* rows, uint64_t* vars, uint64_t* n_pub);
+int acegpu_r1cs_eval(acegpu_ctx* ctx, const acegpu_r1cs* r, const uint8_t* z, uint8_t* a,
+                     uint8_t* b, uint8_t* c);
+/* Groth16 keys for a general R1CS (r must outlive the key): the query
+ * polynomials are the column sums A^T L(tau), B^T L(tau), C^T L(tau) of the
+ * Lagrange basis; the verifying key has n_pub + 1 IC points. prove_z takes the
+ * full assignment z (vars x 32-B standard form); rs = NULL derives r, s as
+ * r = LE(SHA-256("ace-g16-r-v2" | D(z_{n_pub+1..}) | D(z_1..z_{n_pub}))) mod r
+ * (D as above, extended to any count by levels of 1-KB blocks until at most
+ * 32 digests remain); digest = SHA-256("ace-g16-chunk-v2" | D(public inputs)). */
+int acegpu_g16_setup_r1cs(acegpu_ctx* ctx, const acegpu_r1cs* r, const uint8_t* trapdoor5,
+                          acegpu_g16** out);
+int acegpu_g16_prove_z(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* z, const uint8_t* rs,
+                       uint8_t* proof256, uint8_t* raw256, uint8_t* digest32);
+int acegpu_g16_prove_z_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_z,
+                           const uint8_t* d_rs, uint8_t* d_proof256, uint8_t* d_raw256,
+                           uint8_t* d_digest32);
+
 /* Verifying key in the oracle layout (32-B LE standard-form coordinates):
  * alpha G1 (64) | beta G2 (128) | gamma G2 (128) | delta G2 (128) |
  * IC_0..IC_T G1 (64 each) = 448 + 64 (T + 1) bytes (oracle: bn_g16_vk). */

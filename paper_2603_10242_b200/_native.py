@@ -78,11 +78,18 @@ _SIGS = {
     "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),
     "acegpu_g16_setup": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_void_p)]),
     "acegpu_g16_free": (None, [C.c_void_p]),
+    "acegpu_r1cs_free": (None, [C.c_void_p]),
+    "acegpu_r1cs_shape": (C.c_int, [C.c_void_p, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "acegpu_g16_shape": (C.c_int, [C.c_void_p, u64p, u64p, C.POINTER(C.c_uint32)]),
     "acegpu_g16_prove_chunk": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_vk": (C.c_int, [ctxp, C.c_void_p, vp]),
     "acegpu_g16_verify_batch": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int)]),
+    "acegpu_r1cs_create": (C.c_int, [ctxp, u64, u64, u64, vp, vp, vp, C.POINTER(C.c_void_p)]),
+    "acegpu_r1cs_eval": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp]),
+    "acegpu_g16_setup_r1cs": (C.c_int, [ctxp, C.c_void_p, vp, C.POINTER(C.c_void_p)]),
+    "acegpu_g16_prove_z": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp]),
+    "acegpu_g16_prove_z_dev": (C.c_int, [ctxp, C.c_void_p, C.c_void_p, vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_block": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, u64, vp, vp, u64, vp, vp,
                                          vp, vp, vp, vp]),
     "acegpu_g16_verify_batch_seed": (C.c_int, [ctxp, C.c_void_p, vp, vp, u64, C.POINTER(C.c_int),

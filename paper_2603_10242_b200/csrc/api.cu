@@ -21,6 +21,7 @@
 #include "g16_verify.cuh"
 #include "msm.cuh"
 #include "ntt.cuh"
+#include "r1cs.cuh"
 
 #ifndef ACEGPU_GIT
 #define ACEGPU_GIT "dev"
@@ -1850,6 +1851,22 @@ extern "C" int acegpu_bn_mul_rate(acegpu_ctx* c, int field, double* muls_per_s) 
 }
 
 // ==================================================================== Groth16
+// A general constraint system (r1cs.cu): the caller's rows, then one
+// z_i * 0 = 0 row per public variable i = 0..n_pub (ONE and the public
+// inputs), which makes the public u_i linearly independent (as Groth16 needs).
+struct acegpu_r1cs {
+    int device = 0;
+    uint64_t m_user = 0, rows = 0, vars = 0, n_pub = 0;
+    bn::R1csMat mat[3];
+    ~acegpu_r1cs() {
+        DeviceGuard g(device);
+        for (auto& M : mat)
+            for (void* p : {(void*)M.rowptr, (void*)M.col, (void*)M.val, (void*)M.colptr,
+                            (void*)M.crow, (void*)M.cval})
+                if (p) cudaFree(p);
+    }
+};
+
 struct acegpu_g16 {
     int device = 0;
     bn::G16Dims d{};
@@ -1886,6 +1903,8 @@ struct acegpu_g16 {
     cudaEvent_t ev_n = nullptr;
     cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
     bn::MsmScratch msm_bl, msm_h, msm_ab;  // one per MSM stream (no cross-stream scratch)
+    const acegpu_r1cs* r1cs = nullptr;  // general circuit (setup_r1cs), else the synthetic chain
+    uint8_t* zsc = nullptr;             // general path: r, s digest scratch
 };
 
 namespace {
@@ -1950,7 +1969,8 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     cudaDeviceSynchronize();
     for (acegpu_msm_bases* b : {g->qa, g->qb1, g->qb2, g->ql, g->qh, g->qic})
         acegpu_bn_msm_free(b);
-    for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic, g->vk_digest})
+    for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic, g->vk_digest,
+                       g->zsc})
         if (p) cudaFree(p);
     for (auto& sl : g->slot) {
         for (uint8_t* p : {sl.z, sl.zb, sl.zl, sl.ea, sl.eb, sl.ec, sl.pts, sl.scaled, sl.rs,
@@ -1981,19 +2001,20 @@ extern "C" int acegpu_g16_shape(const acegpu_g16* g, uint64_t* V, uint64_t* m, u
     return ACEGPU_OK;
 }
 
-extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uint8_t* trapdoor5,
-                                acegpu_g16** out) {
-    if (T < 1 || K < 2) return fail(ACEGPU_EINVAL, "g16: need T >= 1 and K >= 2");
-    std::lock_guard<std::mutex> lk(c->mu);
-    DeviceGuard guard(c->device);
+namespace {
+// Proving + verifying key: the synthetic chain circuit (r == nullptr: T txs
+// x K constraints) or a general R1CS r (T = its public inputs, K = 0).
+int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
+                   const uint8_t* trapdoor5, acegpu_g16** out) {
     cudaStream_t s = c->stream;
     auto* g = new acegpu_g16();
     std::unique_ptr<acegpu_g16, void (*)(acegpu_g16*)> own(g, acegpu_g16_free);
     g->device = c->device;
+    g->r1cs = r;
     g->d.T = T;
     g->d.K = K;
-    g->d.V = 1 + uint64_t(T) + uint64_t(T) * (K + 1);
-    g->d.m = uint64_t(T) * K + T + 1;
+    g->d.V = r ? r->vars : 1 + uint64_t(T) + uint64_t(T) * (K + 1);
+    g->d.m = r ? r->rows : uint64_t(T) * K + T + 1;
     while ((1ull << g->logn) < g->d.m) ++g->logn;
     if (g->logn > uint32_t(bn::kNttMaxLog)) return fail(ACEGPU_EINVAL, "g16: domain above 2^22");
     g->N = 1ull << g->logn;
@@ -2001,6 +2022,8 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     auto dm = [&](uint8_t** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 16); };
     if (dm(&g->consts, 32 * 16) || dm(&g->cc, 32ull * K))
+        return fail(ACEGPU_ECUDA, "g16 alloc");
+    if (r && dm(&g->zsc, bn::g16_long_digest_scratch_bytes(std::max<uint64_t>(g->d.V, T)) + 64))
         return fail(ACEGPU_ECUDA, "g16 alloc");
     for (auto& sl : g->slot) {
         if (dm(&sl.z, 32 * (V + 2)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
@@ -2041,15 +2064,24 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     // constants
     CK(cudaMemcpyAsync(g->consts, trapdoor5, 160, cudaMemcpyHostToDevice, s));
     bn::g16_setup_consts(g->consts, g->logn, s);
-    bn::g16_chain_consts(K, g->cc, s);
+    if (K) bn::g16_chain_consts(K, g->cc, s);
     // query scalars
-    uint8_t *L, *su, *sv, *sl, *part, *hs, *gens, *ext, *pts;
+    uint8_t *L, *su, *sv, *sl, *part, *hs, *gens, *ext, *pts, *icsc;
     if (dm(&L, 32 * m) || dm(&su, 32 * V) || dm(&sv, 32 * V) || dm(&sl, 32 * g->Vp) ||
         dm(&part, 256 * 64) || dm(&hs, 32 * N) || dm(&gens, 256) || dm(&ext, 512) ||
-        dm(&pts, 128 * (std::max(V, N) + 2)))
+        dm(&pts, 128 * (std::max(V, N) + 2)) || dm(&icsc, 32ull * (T + 1)))
         return fail(ACEGPU_ECUDA, "g16 setup alloc");
     bn::g16_lagrange(g->consts, m, L, s);
-    bn::g16_query_scalars(g->d, L, g->consts, g->cc, part, su, sv, sl, s);
+    if (r) {
+        // u, v, w = A^T L(tau), B^T L(tau), C^T L(tau) (pts as scratch: 3 V x 32 B)
+        uint8_t* uvw = pts;
+        for (int k = 0; k < 3; ++k) bn::r1cs_colsum(r->mat[k], L, V, uvw + 32 * V * k, s);
+        bn::r1cs_query_scalars(g->consts, uvw, uvw + 32 * V, uvw + 64 * V, V, T, su, sv, sl,
+                               icsc, s);
+    } else {
+        bn::g16_query_scalars(g->d, L, g->consts, g->cc, part, su, sv, sl, s);
+        bn::g16_ic_scalars(T, g->consts, su, sv, icsc, s);
+    }
     bn::g16_h_scalars(g->consts, N, hs, s);  // coset-Lagrange H bases (groth16.cu)
     // generators (Montgomery affine) and the extra bases alpha1 beta1 delta1 | beta2 delta2
     uint8_t hgen[192] = {0};
@@ -2094,8 +2126,7 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     // verifying key (the Groth16 verifier, g16_verify.cu)
     if (dm(&g->vk_alpha1, 64) || dm(&g->vk_g2_std, 384) || dm(&g->vk_ic, 64ull * (T + 1)))
         return fail(ACEGPU_ECUDA, "g16 vk alloc");
-    bn::g16_ic_scalars(T, g->consts, su, sv, hs, s);  // hs reused as scratch
-    bn::launch_scalar_muls(1, gens, hs, T + 1, g->vk_ic, s);
+    bn::launch_scalar_muls(1, gens, icsc, T + 1, g->vk_ic, s);
     RET(bases_from_device(c->device, 1, g->vk_ic, T + 1, s, &g->qic));
     CK(cudaMemcpyAsync(g->vk_alpha1, ex1, 64, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ext + 256, trapdoor5 + 96, 32, cudaMemcpyHostToDevice, s));  // gamma
@@ -2110,18 +2141,196 @@ extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uin
     bn::g16_vk_digest(pts, uint32_t(448 + 64 * (T + 1)), g->vk_digest, s);
     CKL();
     CK(cudaStreamSynchronize(s));
-    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2}) cudaFree(p);
+    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2, icsc}) cudaFree(p);
     if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s)) return fail(ACEGPU_ECUDA, "g16 NTT tables");
     CK(cudaStreamSynchronize(s));
     c->launches += 20;
     *out = own.release();
     return ACEGPU_OK;
 }
+}  // namespace
+
+extern "C" int acegpu_g16_setup(acegpu_ctx* c, uint32_t T, uint32_t K, const uint8_t* trapdoor5,
+                                acegpu_g16** out) {
+    if (T < 1 || K < 2) return fail(ACEGPU_EINVAL, "g16: need T >= 1 and K >= 2");
+    if (!trapdoor5 || !out) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_setup_impl(c, T, K, nullptr, trapdoor5, out);
+}
+
+extern "C" int acegpu_g16_setup_r1cs(acegpu_ctx* c, const acegpu_r1cs* r, const uint8_t* trapdoor5,
+                                     acegpu_g16** out) {
+    if (!r || !trapdoor5 || !out) return fail(ACEGPU_EINVAL, "null argument");
+    if (r->device != c->device) return fail(ACEGPU_EINVAL, "r1cs on another device");
+    if (r->n_pub < 1 || r->n_pub > 0xFFFFFFFFull) return fail(ACEGPU_EINVAL, "g16: need >= 1 public input");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_setup_impl(c, uint32_t(r->n_pub), 0, r, trapdoor5, out);
+}
+
+// ---- general R1CS ------------------------------------------------------------
+extern "C" void acegpu_r1cs_free(acegpu_r1cs* r) { delete r; }
+
+extern "C" int acegpu_r1cs_create(acegpu_ctx* c, uint64_t m, uint64_t vars, uint64_t n_pub,
+                                  const uint64_t* const rowptr[3], const uint32_t* const cols[3],
+                                  const uint8_t* const vals[3], acegpu_r1cs** out) {
+    if (!out || !rowptr || !cols || !vals) return fail(ACEGPU_EINVAL, "null argument");
+    if (m == 0 || vars < 2 || n_pub + 1 >= vars || vars > 0xFFFFFFFFull)
+        return fail(ACEGPU_EINVAL, "r1cs: need m >= 1 and 1 + n_pub < vars < 2^32");
+    const uint64_t rows = m + n_pub + 1;
+    // host-side validation + the public rows + the CSC transposes
+    struct Host {
+        std::vector<uint64_t> rp, cp;
+        std::vector<uint32_t> col, crow;
+        std::vector<uint8_t> val, cval;
+    } h[3];
+    for (int k = 0; k < 3; ++k) {
+        if (!rowptr[k] || rowptr[k][0] != 0) return fail(ACEGPU_EINVAL, "r1cs: rowptr[0] != 0");
+        for (uint64_t j = 0; j < m; ++j)
+            if (rowptr[k][j + 1] < rowptr[k][j]) return fail(ACEGPU_EINVAL, "r1cs: rowptr not monotone");
+        const uint64_t nnz_u = rowptr[k][m];
+        if (nnz_u && (!cols[k] || !vals[k])) return fail(ACEGPU_EINVAL, "r1cs: null cols / vals");
+        for (uint64_t e = 0; e < nnz_u; ++e)
+            if (cols[k][e] >= vars) return fail(ACEGPU_EINVAL, "r1cs: column out of range");
+        Host& H = h[k];
+        const uint64_t nnz = nnz_u + (k == 0 ? n_pub + 1 : 0);  // A gets z_i * 0 = 0 rows
+        H.rp.assign(rowptr[k], rowptr[k] + m + 1);
+        H.col.assign(cols[k], cols[k] + nnz_u);
+        H.val.assign(vals[k], vals[k] + 32 * nnz_u);
+        for (uint64_t i = 0; i <= n_pub; ++i) {
+            if (k == 0) {
+                H.col.push_back(uint32_t(i));
+                uint8_t one[32] = {1};
+                H.val.insert(H.val.end(), one, one + 32);
+            }
+            H.rp.push_back(H.col.size());
+        }
+        // CSC (counting sort by column, stable in row order)
+        H.cp.assign(vars + 1, 0);
+        for (uint64_t e = 0; e < nnz; ++e) ++H.cp[H.col[e] + 1];
+        for (uint64_t i = 0; i < vars; ++i) H.cp[i + 1] += H.cp[i];
+        std::vector<uint64_t> cur(H.cp.begin(), H.cp.end() - 1);
+        H.crow.resize(nnz);
+        H.cval.resize(32 * nnz);
+        for (uint64_t j = 0; j < rows; ++j)
+            for (uint64_t e = H.rp[j]; e < H.rp[j + 1]; ++e) {
+                const uint64_t d = cur[H.col[e]]++;
+                H.crow[d] = uint32_t(j);
+                std::memcpy(&H.cval[32 * d], &H.val[32 * e], 32);
+            }
+    }
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    std::unique_ptr<acegpu_r1cs> r(new acegpu_r1cs());
+    r->device = c->device;
+    r->m_user = m;
+    r->rows = rows;
+    r->vars = vars;
+    r->n_pub = n_pub;
+    auto up = [&](auto** dst, const auto& v) -> int {
+        const size_t bytes = v.size() * sizeof(v[0]);
+        if (cudaMalloc(reinterpret_cast<void**>(dst), bytes ? bytes : 16) != cudaSuccess)
+            return fail(ACEGPU_ECUDA, "r1cs alloc");
+        if (bytes) CK(cudaMemcpyAsync(*dst, v.data(), bytes, cudaMemcpyHostToDevice, s));
+        return ACEGPU_OK;
+    };
+    for (int k = 0; k < 3; ++k) {
+        bn::R1csMat& M = r->mat[k];
+        M.nnz = h[k].col.size();
+        RET(up(&M.rowptr, h[k].rp));
+        RET(up(&M.col, h[k].col));
+        RET(up(&M.val, h[k].val));
+        RET(up(&M.colptr, h[k].cp));
+        RET(up(&M.crow, h[k].crow));
+        RET(up(&M.cval, h[k].cval));
+        // values: 32-B LE integers -> Montgomery (to_mont reduces any value < 2^256)
+        bn::launch_fr_convert(M.val, M.nnz, 1, s);
+        bn::launch_fr_convert(M.cval, M.nnz, 1, s);
+        CKL();
+    }
+    CK(cudaStreamSynchronize(s));
+    c->launches += 12;
+    *out = r.release();
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_r1cs_shape(const acegpu_r1cs* r, uint64_t* rows, uint64_t* vars,
+                                 uint64_t* n_pub) {
+    if (!r) return fail(ACEGPU_EINVAL, "null argument");
+    if (rows) *rows = r->rows;
+    if (vars) *vars = r->vars;
+    if (n_pub) *n_pub = r->n_pub;
+    return ACEGPU_OK;
+}
+
+// a = A z, b = B z, c = C z (rows entries, incl. the public rows), host buffers.
+extern "C" int acegpu_r1cs_eval(acegpu_ctx* c, const acegpu_r1cs* r, const uint8_t* z,
+                                uint8_t* a, uint8_t* b, uint8_t* cc) {
+    if (!r || !z) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    uint8_t *dz, *out;
+    RET(h2d_t(c, kBnA, z, 32 * r->vars, s, &dz));
+    RET(ws(c, kBnOut, 96 * r->rows, &out));
+    bn::launch_fr_convert(dz, r->vars, 1, s);
+    for (int k = 0; k < 3; ++k) {
+        bn::r1cs_spmv(r->mat[k], dz, r->rows, r->rows, out + 32 * r->rows * k, s);
+        bn::launch_fr_convert(out + 32 * r->rows * k, r->rows, 0, s);
+    }
+    CKL();
+    c->launches += 8;
+    uint8_t* dst[3] = {a, b, cc};
+    for (int k = 0; k < 3; ++k)
+        if (dst[k]) CK(cudaMemcpyAsync(dst[k], out + 32 * r->rows * k, 32 * r->rows,
+                                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return ACEGPU_OK;
+}
 
 namespace {
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
-                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr);
+                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr,
+                     const uint8_t* d_z = nullptr);
+}
+
+// General R1CS: prove from the full assignment z (vars x 32-B standard form,
+// z[0] = 1, z[1..n_pub] the public inputs).
+extern "C" int acegpu_g16_prove_z_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                      const uint8_t* d_z, const uint8_t* d_rs,
+                                      uint8_t* d_proof256, uint8_t* d_raw256,
+                                      uint8_t* d_digest32) {
+    if (!g || !d_z) return fail(ACEGPU_EINVAL, "null argument");
+    if (!g->r1cs) return fail(ACEGPU_EINVAL, "g16: key not built from an R1CS (acegpu_g16_setup_r1cs)");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_prove_locked(c, pick(c, stream), g, nullptr, nullptr, d_rs, d_proof256, d_raw256,
+                            d_digest32, nullptr, d_z);
+}
+
+extern "C" int acegpu_g16_prove_z(acegpu_ctx* c, acegpu_g16* g, const uint8_t* z,
+                                  const uint8_t* rs, uint8_t* proof256, uint8_t* raw256,
+                                  uint8_t* digest32) {
+    if (!g || !z) return fail(ACEGPU_EINVAL, "null argument");
+    uint8_t *dz, *drs = nullptr, *dout;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard guard(c->device);
+        RET(h2d_t(c, kBnB, z, 32 * g->d.V, c->stream, &dz));
+        if (rs) RET(h2d_t(c, kIn2, rs, 64, c->stream, &drs));
+        RET(ws(c, kBnOut, 512 + 32, &dout));
+    }
+    RET(acegpu_g16_prove_z_dev(c, c->stream, g, dz, drs, dout, dout + 256, dout + 512));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    if (proof256) CK(cudaMemcpyAsync(proof256, dout, 256, cudaMemcpyDeviceToHost, c->stream));
+    if (raw256) CK(cudaMemcpyAsync(raw256, dout + 256, 256, cudaMemcpyDeviceToHost, c->stream));
+    if (digest32) CK(cudaMemcpyAsync(digest32, dout + 512, 32, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ACEGPU_OK;
 }
 
 extern "C" int acegpu_g16_prove_chunk_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
@@ -2163,7 +2372,12 @@ struct G16Trace {
 G16Trace g_g16_trace;
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
-                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready) {
+                     uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready,
+                     const uint8_t* d_z) {
+    if (!g->r1cs != !d_z)
+        return fail(ACEGPU_EINVAL, g->r1cs ? "g16: an R1CS key proves full assignments "
+                                             "(acegpu_g16_prove_z)"
+                                           : "g16: full assignments need an R1CS key");
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     uint8_t* scratch;
     RET(ws(c, kBnScratch, 32 * N, &scratch));
@@ -2183,8 +2397,24 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     tr.mark("start", sw);
     for (uint8_t* e : {g->ea, g->eb, g->ec})
         if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), sw));
-    bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, sw);
-    bn::g16_derive_rs(d_w, d_pub, g->d.T, sl.dsc, g->rs, g->digest, sw);
+    if (g->r1cs) {
+        // general R1CS: the caller's full assignment z (standard form); the
+        // row evaluations a, b, c = A z, B z, C z by SpMV (zb holds z in
+        // Montgomery form meanwhile), zero-padded to the domain
+        const acegpu_r1cs* r = g->r1cs;
+        CK(cudaMemcpyAsync(g->zb, d_z, 32 * V, cudaMemcpyDeviceToDevice, sw));
+        bn::launch_fr_convert(g->zb, V, 1, sw);
+        uint8_t* e3[3] = {g->ea, g->eb, g->ec};
+        for (int k = 0; k < 3; ++k) bn::r1cs_spmv(r->mat[k], g->zb, r->rows, N, e3[k], sw);
+        // z canonical for the MSM scalars and the digests
+        bn::launch_fr_convert(g->zb, V, 0, sw);
+        CK(cudaMemcpyAsync(g->z, g->zb, 32 * V, cudaMemcpyDeviceToDevice, sw));
+        bn::g16_derive_rs_long(g->z + 32 * (1 + g->d.T), V - 1 - g->d.T, g->z + 32, g->d.T,
+                               g->zsc, g->rs, g->digest, sw);
+    } else {
+        bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, sw);
+        bn::g16_derive_rs(d_w, d_pub, g->d.T, sl.dsc, g->rs, g->digest, sw);
+    }
     if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, sw));
     // scalar vectors with their extras
     CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, sw));

@@ -41,6 +41,14 @@ void g16_input_digests(const uint8_t* x, uint32_t T, uint32_t chunks, int wits, 
 // scratch: g16_digest_scratch_bytes(T, chunks); D(pub_k) left at scratch + stride * chunks
 void g16_chunk_digests(const uint8_t* pub, uint32_t T, uint32_t chunks, uint8_t* scratch,
                        uint8_t* digests, cudaStream_t s);
+// D(x) for any count (levels of 1-KB blocks until <= 32 digests; == the
+// chunk rule for count <= 1024); r, s and the chunk digest of a general
+// R1CS assignment (w = its private part, n_w values)
+size_t g16_long_digest_scratch_bytes(uint64_t count);
+void g16_long_digest(const uint8_t* x, uint64_t count, int wits, uint8_t* scratch, uint8_t* out,
+                     cudaStream_t s);
+void g16_derive_rs_long(const uint8_t* w, uint64_t n_w, const uint8_t* pub, uint32_t T,
+                        uint8_t* scratch, uint8_t* rs, uint8_t* digest, cudaStream_t s);
 // scratch: g16_digest_scratch_bytes(T, 1) + 32
 void g16_derive_rs(const uint8_t* w, const uint8_t* pub, uint32_t T, uint8_t* scratch,
                    uint8_t* rs, uint8_t* digest, cudaStream_t s);

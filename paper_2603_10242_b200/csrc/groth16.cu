@@ -14,6 +14,8 @@
 //   assemble : C = L + H + s A + r B1
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "curve.cuh"
 #include "g16_kernels.cuh"
 #include "sha256.cuh"
@@ -312,6 +314,33 @@ __global__ void input_top_kernel(const uint8_t* msg, uint32_t stride, uint32_t l
     store_digest(out + 32ull * c, d);
 }
 
+// Digests of consecutive 1-KB blocks (32 items of 32 B; the last short):
+// out[b] = SHA-256(x[32 b .. min(32 b + 32, count))).
+__global__ void block_digest_kernel(const uint8_t* x, uint64_t count, uint8_t* out) {
+    const uint64_t b = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    const uint64_t nb = (count + 31) / 32;
+    if (b >= nb) return;
+    const uint64_t left = count - 32 * b;
+    const uint32_t cnt = left < 32 ? (uint32_t)left : 32u;
+    uint32_t d[8];
+    sha256_bytes(x, 1024ull * b, 32 * cnt, d);
+    store_digest(out + 32 * b, d);
+}
+// top: SHA-256(tag16 | digests (n x 32 B) | count_be32), one thread
+__global__ void long_top_kernel(const uint8_t* dig, uint32_t n, uint64_t count, int wits,
+                                uint8_t* msg, uint8_t* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    const char* tag = wits ? "ace-g16-wits-v2:" : "ace-g16-pubs-v2:";
+    for (int i = 0; i < 16; ++i) msg[i] = tag[i];
+    for (uint32_t i = 0; i < 32 * n; ++i) msg[16 + i] = dig[i];
+    uint8_t* e = msg + 16 + 32 * n;
+    const uint32_t c = (uint32_t)count;
+    e[0] = c >> 24; e[1] = c >> 16; e[2] = c >> 8; e[3] = c;
+    uint32_t d[8];
+    sha256_bytes(msg, 0, 16 + 32 * n + 4, d);
+    store_digest(out, d);
+}
+
 // Chunk digest (the tree leaf's public-inputs digest) from D(pub):
 // SHA-256("ace-g16-chunk-v2" | D(pub)).
 __global__ void chunk_digest_kernel(const uint8_t* pd, uint32_t chunks, uint8_t* digest) {
@@ -523,6 +552,42 @@ void g16_chunk_digests(const uint8_t* pub, uint32_t T, uint32_t chunks, uint8_t*
     uint8_t* pd = scratch + (size_t)digest_msg_stride(T) * chunks;
     g16_input_digests(pub, T, chunks, 0, scratch, pd, s);
     chunk_digest_kernel<<<grid(chunks, 64), 64, 0, s>>>(pd, chunks, digests);
+}
+size_t g16_long_digest_scratch_bytes(uint64_t count) {
+    return ((count + 31) / 32) * 32 * 2 + 2048 + g16_digest_scratch_bytes(1024, 1);
+}
+void g16_long_digest(const uint8_t* x, uint64_t count, int wits, uint8_t* scratch, uint8_t* out,
+                     cudaStream_t s) {
+    if (count <= 1024) {
+        g16_input_digests(x, uint32_t(count), 1, wits, scratch, out, s);
+        return;
+    }
+    // levels of 1-KB blocks until at most 32 digests remain, then the top
+    // message: identical to D for count <= 1024 (one level)
+    uint64_t nb = (count + 31) / 32;
+    uint8_t* a = scratch;
+    uint8_t* b = scratch + nb * 32;
+    block_digest_kernel<<<grid(nb, 64), 64, 0, s>>>(x, count, a);
+    while (nb > 32) {
+        const uint64_t n2 = (nb + 31) / 32;
+        block_digest_kernel<<<grid(n2, 64), 64, 0, s>>>(a, nb, b);
+        uint8_t* t = a;
+        a = b;
+        b = t;
+        nb = n2;
+    }
+    uint8_t* msg = scratch + ((count + 31) / 32) * 32 * 2;
+    long_top_kernel<<<1, 32, 0, s>>>(a, uint32_t(nb), count, wits, msg, out);
+}
+void g16_derive_rs_long(const uint8_t* w, uint64_t n_w, const uint8_t* pub, uint32_t T,
+                        uint8_t* scratch, uint8_t* rs, uint8_t* digest, cudaStream_t s) {
+    // scratch: g16_long_digest_scratch_bytes(max(n_w, T)) + 64
+    uint8_t* wd = scratch + g16_long_digest_scratch_bytes(std::max<uint64_t>(n_w, T));
+    uint8_t* pd = wd + 32;
+    g16_long_digest(w, n_w, 1, scratch, wd, s);
+    g16_long_digest(pub, T, 0, scratch, pd, s);
+    chunk_digest_kernel<<<1, 32, 0, s>>>(pd, 1, digest);
+    derive_rs_kernel<<<1, 32, 0, s>>>(wd, pd, rs);
 }
 void g16_derive_rs(const uint8_t* w, const uint8_t* pub, uint32_t T, uint8_t* scratch,
                    uint8_t* rs, uint8_t* digest, cudaStream_t s) {

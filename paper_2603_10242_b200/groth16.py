@@ -39,6 +39,32 @@ class ProvingKey:
         N.lib().acegpu_g16_shape(self.h, C.byref(V), C.byref(m), C.byref(L))
         self.variables, self.constraints, self.log_domain = V.value, m.value, L.value
 
+    @classmethod
+    def from_r1cs(cls, r1cs, trapdoor: np.ndarray | None = None, ctx=None) -> "ProvingKey":
+        """Keys for a general constraint system (r1cs.R1CS; it must outlive
+        the key): prove with prove_z(z) on the full assignment."""
+        self = cls.__new__(cls)
+        self.ctx = ctx or r1cs.ctx
+        self.T, self.K, self.r1cs = r1cs.n_pub, 0, r1cs
+        self.trapdoor = deterministic_trapdoor(ctx=self.ctx) if trapdoor is None else trapdoor
+        h = C.c_void_p()
+        self.ctx.call("acegpu_g16_setup_r1cs", r1cs.h, self.trapdoor, C.byref(h))
+        self.h = h
+        V, m, L = C.c_uint64(), C.c_uint64(), C.c_uint32()
+        N.lib().acegpu_g16_shape(self.h, C.byref(V), C.byref(m), C.byref(L))
+        self.variables, self.constraints, self.log_domain = V.value, m.value, L.value
+        return self
+
+    def prove_z(self, z: np.ndarray, rs: np.ndarray | None = None):
+        """General R1CS key: the full assignment z (vars x 32-B) ->
+        (proof256, raw affine points, public-inputs digest)."""
+        proof = np.zeros(256, np.uint8)
+        raw = np.zeros(256, np.uint8)
+        dig = np.zeros(32, np.uint8)
+        self.ctx.call("acegpu_g16_prove_z", self.h, np.ascontiguousarray(z, np.uint8), rs, proof,
+                      raw, dig)
+        return proof.tobytes(), raw.tobytes(), dig.tobytes()
+
     def prove(self, w: np.ndarray, pub: np.ndarray, rs: np.ndarray | None = None):
         """-> (proof256 bytes, raw affine points bytes, chunk digest bytes)."""
         proof = np.zeros(256, np.uint8)

@@ -19,10 +19,16 @@ def sha(b: bytes) -> bytes:
 
 
 def input_digest(x: bytes, T: int, wits: bool = False) -> bytes:
+    """D(x): 1-KB blocks (32 inputs) hashed, then (for more than 32 blocks)
+    the digests again in 1-KB blocks until at most 32 remain; the top hashes
+    tag16 | digests | T_be32."""
     assert len(x) == 32 * T
     tag = b"ace-g16-wits-v2:" if wits else b"ace-g16-pubs-v2:"
-    blocks = b"".join(sha(x[32 * 32 * b:32 * min(T, 32 * b + 32)]) for b in range((T + 31) // 32))
-    return sha(tag + blocks + T.to_bytes(4, "big"))
+    level = [sha(x[1024 * b:1024 * b + 1024]) for b in range((T + 31) // 32)]
+    while len(level) > 32:
+        cat = b"".join(level)
+        level = [sha(cat[1024 * b:1024 * b + 1024]) for b in range((len(level) + 31) // 32)]
+    return sha(tag + b"".join(level) + T.to_bytes(4, "big"))
 
 
 def derive_rs(w: bytes, pub: bytes, T: int) -> tuple[int, int]:

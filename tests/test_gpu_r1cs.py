@@ -1,0 +1,182 @@
+"""General R1CS path (north-star witness / constraint evaluation, csrc/r1cs.cu):
+CSR SpMV row evaluations vs Python big integers; the stand-in circuit run
+through the general path gives the bespoke prover's verifying key and proof
+bytes; a non-synthetic circuit proves, verifies (GPU batch verifier and the
+oracle's pairing verifier) and binds its public inputs."""
+import ctypes as C
+import random
+
+import numpy as np
+import pytest
+
+import g16_spec as SP
+import oracle_lib as O
+
+pytestmark = pytest.mark.gpu
+
+R = 0x30644E72E131A029B85045B68181585D2833E84879B9709143E1F593F0000001
+
+
+def le(x):
+    return (x % R).to_bytes(32, "little")
+
+
+def arr(vals):
+    return np.frombuffer(b"".join(le(v) for v in vals), np.uint8).copy()
+
+
+def ints(a):
+    b = a.tobytes()
+    return [int.from_bytes(b[i:i + 32], "little") for i in range(0, len(b), 32)]
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_2603_10242_b200 import _native as N
+    return N.context(0)
+
+
+def test_r1cs_eval_matches_python(ctx):
+    from paper_2603_10242_b200 import r1cs
+    rng = random.Random(1)
+    m, V, npub = 200, 60, 4
+    mats = []
+    for _ in range(3):
+        rows = []
+        for _ in range(m):
+            rows.append({rng.randrange(V): rng.choice([1, 2, R - 1, rng.randrange(R), 2**256 - 1])
+                         for _ in range(rng.randrange(0, 5))})
+        mats.append(rows)
+    z = [1] + [rng.randrange(R) for _ in range(V - 1)]
+    r = r1cs.R1CS(m, V, npub, *[r1cs.Csr.from_rows(x) for x in mats], ctx=ctx)
+    try:
+        a, b, c = r.eval(arr(z))
+        for k, (got, rows) in enumerate(zip((a, b, c), mats)):
+            exp = [sum(v * z[i] for i, v in row.items()) % R for row in rows]
+            # appended public rows: A_{m+i} = z_i, B = C = 0
+            exp += [z[i] if k == 0 else 0 for i in range(npub + 1)]
+            assert ints(got) == exp
+    finally:
+        r.close()
+
+
+def test_r1cs_rejects_malformed(ctx):
+    from paper_2603_10242_b200 import r1cs
+    good = r1cs.Csr.from_rows([{0: 1}, {1: 1}])
+    bad_col = r1cs.Csr.from_rows([{0: 1}, {7: 1}])
+    with pytest.raises(ValueError):
+        r1cs.R1CS(2, 5, 1, good, good, bad_col, ctx=ctx)
+    with pytest.raises(ValueError):
+        r1cs.R1CS(2, 5, 4, good, good, good, ctx=ctx)  # n_pub + 1 >= vars
+
+
+@pytest.mark.parametrize("T,K", [(4, 3), (64, 20)])
+def test_synthetic_circuit_through_the_general_path(ctx, T, K):
+    """The stand-in circuit as CSR matrices: same verifying key, same proof
+    bytes and digest as the bespoke chunk prover."""
+    from paper_2603_10242_b200 import groth16, r1cs
+    rng = random.Random(T * 7 + K)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    m, V, npub, A, B, Cm = r1cs.synthetic_chunk(T, K, ctx)
+    rc = r1cs.R1CS(m, V, npub, A, B, Cm, ctx=ctx)
+    pk1 = groth16.ProvingKey(T, K, trap, ctx)
+    pk2 = groth16.ProvingKey.from_r1cs(rc, trap, ctx)
+    try:
+        assert (pk2.variables, pk2.constraints, pk2.log_domain) == \
+               (pk1.variables, pk1.constraints, pk1.log_domain)
+        assert pk2.verifying_key() == pk1.verifying_key()
+        w = arr([rng.randrange(R) for _ in range(T)])
+        pub = arr([rng.randrange(R) for _ in range(T)])
+        z = r1cs.synthetic_assignment(T, K, w, pub, r1cs.chain_constants(K, ctx))
+        a, b, c = rc.eval(z)
+        assert all(x * y % R == v for x, y, v in zip(ints(a), ints(b), ints(c)))  # satisfied
+        rs = arr(SP.derive_rs(w.tobytes(), pub.tobytes(), T))
+        p1, raw1, d1 = pk1.prove(w, pub, rs)
+        p2, raw2, d2 = pk2.prove_z(z, rs)
+        assert p2 == p1 and raw2 == raw1 and d2 == d1
+        # derived r, s of the general path: D(private assignment) | D(public inputs)
+        p3, raw3, d3 = pk2.prove_z(z)
+        zb = z.tobytes()
+        wd = SP.input_digest(zb[32 * (1 + T):], V - 1 - T, True)
+        pd = SP.input_digest(zb[32:32 * (1 + T)], T)
+        r_ = int.from_bytes(SP.sha(b"ace-g16-r-v2" + wd + pd), "little") % R
+        s_ = int.from_bytes(SP.sha(b"ace-g16-s-v2" + wd + pd), "little") % R
+        assert pk2.prove_z(z, arr([r_, s_]))[0] == p3 and d3 == d1
+        with pytest.raises(ValueError):
+            pk1.prove_z(z)  # a synthetic key takes (w, pub), not an assignment
+    finally:
+        pk1.close()
+        pk2.close()
+        rc.close()
+
+
+def _cubic_circuit(n_inst, rng):
+    """n_inst instances of x^3 + a x + 5 = y (y public), 3 rows each:
+    s1 = x * x, s2 = s1 * x, (s2 + a x + 5) * 1 = y. Not the stand-in chain."""
+    npub = n_inst
+    V = 1 + npub + 3 * n_inst  # ONE, y_i, then x_i, s1_i, s2_i
+    A, B, Cm, z = [], [], [], [1] + [0] * (V - 1)
+    for i in range(n_inst):
+        y, x, s1, s2 = 1 + i, 1 + npub + 3 * i, 2 + npub + 3 * i, 3 + npub + 3 * i
+        a = rng.randrange(R)
+        xv = rng.randrange(R)
+        z[x], z[s1] = xv, xv * xv % R
+        z[s2] = z[s1] * xv % R
+        z[y] = (z[s2] + a * xv + 5) % R
+        A += [{x: 1}, {s1: 1}, {s2: 1, x: a, 0: 5}]
+        B += [{x: 1}, {x: 1}, {0: 1}]
+        Cm += [{s1: 1}, {s2: 1}, {y: 1}]
+    return 3 * n_inst, V, npub, A, B, Cm, z
+
+
+def test_general_circuit_proves_and_verifies(ctx):
+    from paper_2603_10242_b200 import groth16, r1cs
+    rng = random.Random(42)
+    m, V, npub, A, B, Cm, z = _cubic_circuit(6, rng)
+    rc = r1cs.R1CS(m, V, npub, *[r1cs.Csr.from_rows(x) for x in (A, B, Cm)], ctx=ctx)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    pk = groth16.ProvingKey.from_r1cs(rc, trap, ctx)
+    try:
+        za = arr(z)
+        proof, raw, dig = pk.prove_z(za)
+        pubs = za.tobytes()[32:32 * (1 + npub)]
+        assert dig == SP.chunk_digest(pubs, npub)
+        assert pk.verify_batch([proof], [pubs])
+        vk = pk.verifying_key()
+        assert O.oracle().bn_g16_verify(C.c_uint32(npub), O.ptr(vk), O.ptr(raw), O.ptr(pubs)) == 1
+        bad = bytearray(pubs)
+        bad[0] ^= 1
+        assert not pk.verify_batch([proof], [bytes(bad)])
+        assert O.oracle().bn_g16_verify(C.c_uint32(npub), O.ptr(vk), O.ptr(raw), O.ptr(bytes(bad))) == 0
+        # an unsatisfying assignment does not verify
+        z2 = list(z)
+        z2[1 + npub] = (z2[1 + npub] + 1) % R
+        p2, _, _ = pk.prove_z(arr(z2))
+        assert not pk.verify_batch([p2], [pubs])
+    finally:
+        pk.close()
+        rc.close()
+
+
+def test_paper_size_chunk_through_the_general_path(ctx):
+    """1,024 txs x 1,400 constraints (1,434,625 rows, domain 2^21) as CSR:
+    proof bytes equal the bespoke prover's."""
+    from paper_2603_10242_b200 import bn254, groth16, r1cs
+    T, K = groth16.PAPER_T, groth16.PAPER_K
+    m, V, npub, A, B, Cm = r1cs.synthetic_chunk(T, K, ctx)
+    rc = r1cs.R1CS(m, V, npub, A, B, Cm, ctx=ctx)
+    w, pub = bn254.random_scalars(T, 5), bn254.random_scalars(T, 6)
+    z = r1cs.synthetic_assignment(T, K, w, pub, r1cs.chain_constants(K, ctx))
+    trap = groth16.deterministic_trapdoor(ctx=ctx)
+    rs = arr(SP.derive_rs(w.tobytes(), pub.tobytes(), T))
+    pk1 = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        p1 = pk1.prove(w, pub, rs)
+    finally:
+        pk1.close()
+    pk2 = groth16.ProvingKey.from_r1cs(rc, trap, ctx)
+    try:
+        assert pk2.prove_z(z, rs) == p1
+    finally:
+        pk2.close()
+        rc.close()
