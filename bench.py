@@ -353,6 +353,8 @@ def run_ours(args, rank: int, world: int) -> None:
                                    "(FP64 split), same run",
                     "ncu": g16_ncu_summary()}
         pk.close()
+        if world == 1:
+            g16["zkace_hmac"] = bench_zkace_hmac_chunk(ctx, dev, fb, revs, rev_index)
         if world == 1 and not args.no_cpu_baseline:
             bn["cpu_oracle"] = bn254_cpu_baseline(msm_in)
 
@@ -431,6 +433,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "clocks": cl, "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "parity": parity, "impl": "ours", "stream": stream, "phase1a_and_verify": phase1a,
         "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
+        "zkace_hmac_chunk": g16.get("zkace_hmac"),
         "groth16_roofline": g16_roof, "bn254": bn,
     }
     if world > 1 and os.environ.get("ACE_BENCH_SHARED_GPU"):
@@ -678,6 +681,65 @@ def bench_groth16(ctx, dev: int, fq_rate: float, pk, reps: int = 5) -> dict:
             "work": wk, "frac_of_fq_mul_peak": wk["fq_mul_equivalents"] / (chunk_ms * 1e-3) / fq_rate,
             "note": "synthetic stand-in circuit (oracle/bn254_oracle.h); proofs checked "
                     "bit-exact vs the known-trapdoor oracle in tests/test_gpu_groth16.py"}
+
+
+def bench_zkace_hmac_chunk(ctx, dev: int, fb, revs, rev_index, reps: int = 3) -> dict:
+    """The ZK-ACE credential relation as a real circuit (zkace_circuit.py:
+    HMAC-SHA256(attest key, obj_hash || domain) == credential, ~103k
+    constraints per tx) through the general R1CS Groth16 path: as many txs of
+    the 100k block as fit a 2^21 domain, proven on the device (CUDA events,
+    the assignment resident), verified by the batch verifier. The host-side
+    witness generation (Python circuit evaluation) is timed separately."""
+    import torch
+    from paper_2603_10242_b200 import groth16, r1cs, zkace_circuit as Z
+    per_tx = Z.constraints_per_tx()
+    T = ((1 << 21) - 1) // (per_tx + Z.N_PUB_PER_TX)
+    n = T
+    keys_all = np.zeros(32 * n, np.uint8)
+    doms = fb.atts[:104 * n].reshape(n, 104)[:, 64:72].copy()
+    rv = revs.reshape(-1, 32)[rev_index[:n]].copy()
+    ctx.call("acegpu_derive_attest_keys", rv, doms, n, keys_all)
+    keys = [keys_all[32 * i:32 * i + 32].tobytes() for i in range(n)]
+    atts = [fb.atts[104 * i:104 * i + 104].tobytes() for i in range(n)]
+    t0 = time.perf_counter()
+    m, V, npub, A, B, Cm, z = Z.chunk(keys, atts)
+    wgen_s = time.perf_counter() - t0
+    rc = r1cs.R1CS(m, V, npub, A, B, Cm, ctx=ctx)
+    t0 = time.perf_counter()
+    pk = groth16.ProvingKey.from_r1cs(rc, ctx=ctx)
+    setup_s = time.perf_counter() - t0
+    try:
+        s = torch.cuda.current_stream()
+        dz = torch.from_numpy(z).to(f"cuda:{dev}")
+        out = torch.zeros(256 + 256 + 32, dtype=torch.uint8, device=f"cuda:{dev}")
+
+        def one():
+            ctx.call("acegpu_g16_prove_z_dev", s.cuda_stream, pk.h, dz.data_ptr(), None,
+                     out.data_ptr(), out.data_ptr() + 256, out.data_ptr() + 512)
+        one()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(reps)]
+        for a, b in evs:
+            a.record(s)
+            one()
+            b.record(s)
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in evs)
+        proof = out[:256].cpu().numpy().tobytes()
+        ok = pk.verify_batch([proof], [z.tobytes()[32:32 * (1 + npub)]])
+        return {"txs": T, "constraints_per_tx": per_tx, "constraints": pk.constraints,
+                "variables": V, "domain": 1 << pk.log_domain, "public_inputs": npub,
+                "prove_ms": ms, "reps": reps, "proven_tx_per_s": T / (ms * 1e-3),
+                "verifies": bool(ok), "setup_s_once": setup_s,
+                "host_witness_generation_s": wgen_s,
+                "100k_block_chunks": -(-100_000 // T),
+                "note": "relation witness_matches_tx (prover.cpp:190-197) as R1CS: 4 SHA-256 "
+                        "compressions per tx; the witness is mostly bits, so the MSM scalars "
+                        "are mostly 0/1"}
+    finally:
+        pk.close()
+        rc.close()
 
 
 def make_witnesses(fb, revs, rev_index, ctx) -> np.ndarray:

@@ -180,3 +180,41 @@ def test_paper_size_chunk_through_the_general_path(ctx):
     finally:
         pk2.close()
         rc.close()
+
+
+def test_zkace_hmac_circuit_proves_on_gpu(ctx):
+    """The ZK-ACE credential relation (zkace_circuit.py: HMAC-SHA256(attest key,
+    obj_hash || domain) == credential, ~103k constraints per tx) for 2 txs of a
+    multi-user block: satisfied on the GPU (A z o B z == C z), proven and
+    verified by the GPU batch verifier and the oracle's pairing check; a
+    forged credential makes the system unsatisfiable and its proof fails."""
+    from paper_2603_10242_b200 import groth16, r1cs, zkace_circuit as Z
+    fb = O.multi_user_block(2, 2)
+    keys, atts = [], []
+    for i in range(2):
+        att = fb.att(i)
+        u = int(fb.rev_index[i])
+        keys.append(bytes(O.derive_attest_key(fb.revs[32 * u:32 * u + 32].tobytes(), att[64:72])))
+        atts.append(bytes(att))
+    m, V, npub, A, B, Cm, z = Z.chunk(keys, atts)
+    rc = r1cs.R1CS(m, V, npub, A, B, Cm, ctx=ctx)
+    rng = random.Random(9)
+    pk = groth16.ProvingKey.from_r1cs(rc, arr([rng.randrange(1, R) for _ in range(5)]), ctx)
+    try:
+        a, b, c = rc.eval(z)
+        assert all(x * y % R == v for x, y, v in zip(ints(a), ints(b), ints(c)))
+        proof, raw, _ = pk.prove_z(z)
+        pubs = z.tobytes()[32:32 * (1 + npub)]
+        assert pk.verify_batch([proof], [pubs])
+        vk = pk.verifying_key()
+        assert O.oracle().bn_g16_verify(C.c_uint32(npub), O.ptr(vk), O.ptr(raw), O.ptr(pubs)) == 1
+        bad = list(atts)
+        bad[1] = bad[1][:80] + bytes([bad[1][80] ^ 4]) + bad[1][81:]
+        _, _, _, _, _, _, zf = Z.chunk(keys, bad)
+        a, b, c = rc.eval(zf)
+        assert any(x * y % R != v for x, y, v in zip(ints(a), ints(b), ints(c)))
+        pf, _, _ = pk.prove_z(zf)
+        assert not pk.verify_batch([pf], [zf.tobytes()[32:32 * (1 + npub)]])
+    finally:
+        pk.close()
+        rc.close()
