@@ -301,6 +301,123 @@ __device__ __forceinline__ Fp<C> mul(const Fp<C>& a, const Fp<C>& b) {
     else return mul_cios(a, b);
 }
 
+// ---- lazy reduction in the FP64 domain ------------------------------------
+// W10: a 520-bit value X = sum_k c[k] 2^(52 k) as ten SIGNED 64-bit columns
+// (not normalised), holding 16 a b of the product (the R' = 2^260 scaling of
+// mul_f64), so sums and differences of products are column-wise integer adds
+// and one redc10 per output does the Montgomery reduction: X 2^-260 mod m =
+// (a b + ...) 2^-256, the R = 2^256 Montgomery form of the rest of the code.
+// Column magnitudes stay below 2^60 (sums of at most a few dozen 52-bit parts).
+struct W10 {
+    int64_t c[10];
+};
+namespace f64 {
+constexpr uint64_t bias_ab(int k) {  // exponent bits the 25 products leave in column k
+    uint64_t s = 0;
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+            if (i + j == k) s += kB52;
+            if (i + j + 1 == k) s += kB104;
+        }
+    return 0ull - s;
+}
+constexpr uint64_t bias_red(int k) {  // ... and the reduction's 5 x (1 + 4 x 2) parts
+    uint64_t s = 0;
+    for (int i = 0; i < 5; ++i)
+        for (int j = 0; j < 5; ++j) {
+            if (j > 0 && i + j == k) s += kB52;
+            if (i + j + 1 == k) s += kB104;
+        }
+    return 0ull - s;
+}
+}  // namespace f64
+
+// w = 16 a b as true column values (a < 2^256, b < 2^256).
+template <class C>
+__device__ __forceinline__ void mul_wide10(const Fp<C>& a, const Fp<C>& b, W10& w) {
+    using namespace f64;
+    double x[5], y[5];
+    to52<4>(a.v, x);
+    to52<0>(b.v, y);
+    uint64_t c[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) c[k] = bias_ab(k);
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) split_acc(x[i], y[j], c[i + j], c[i + j + 1]);
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w.c[k] = (int64_t)c[k];
+}
+__device__ __forceinline__ void w10_sub(W10& w, const W10& o) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w.c[k] -= o.c[k];
+}
+__device__ __forceinline__ void w10_add(W10& w, const W10& o) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w.c[k] += o.c[k];
+}
+__device__ __forceinline__ void w10_shl1(W10& w) {
+#pragma unroll
+    for (int k = 0; k < 10; ++k) w.c[k] *= 2;
+}
+// w += m 2^260 (m's 52-bit limbs in columns 5..9): lifts a difference of
+// products |X| < m 2^260 into [0, 2 m 2^260)
+template <class C>
+__device__ __forceinline__ void w10_add_m260(W10& w) {
+    // compile-time limbs (C::M may not be read on the device at run time)
+    constexpr int64_t L[5] = {(int64_t)f64::limb52<C>(0), (int64_t)f64::limb52<C>(1),
+                              (int64_t)f64::limb52<C>(2), (int64_t)f64::limb52<C>(3),
+                              (int64_t)f64::limb52<C>(4)};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) w.c[5 + k] += L[k];
+}
+// X 2^-260 mod m for 0 <= X < 2 m 2^260, fully reduced (result < 3m before
+// the two conditional subtractions).
+template <class C>
+__device__ __forceinline__ Fp<C> redc10(const W10& w) {
+    using namespace f64;
+    constexpr double NP = (double)nprime52<C>();
+    constexpr double P[5] = {(double)limb52<C>(0), (double)limb52<C>(1), (double)limb52<C>(2),
+                             (double)limb52<C>(3), (double)limb52<C>(4)};
+    uint64_t c[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) c[k] = (uint64_t)w.c[k] + bias_red(k);
+    int64_t carry = 0;
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const int64_t s = (int64_t)c[i] + carry;  // column i is complete (true value)
+        const uint64_t v = (uint64_t)s & kM52;
+        carry = (s >> 52) + (v != 0);
+        const double vd = to_d(v);
+        const double t = __fma_rz(vd, NP, kC1);
+        const double md = __dsub_rn(__fma_rn(vd, NP, __dsub_rn(kC2, t)), kT52);
+        c[i + 1] += bits(__fma_rz(md, P[0], kC1));
+#pragma unroll
+        for (int j = 1; j < 5; ++j) split_acc(md, P[j], c[i + j], c[i + j + 1]);
+    }
+    uint64_t r[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const int64_t s = (int64_t)c[5 + k] + carry;
+        r[k] = (uint64_t)s & kM52;
+        carry = s >> 52;
+    }
+    // value < 3 m < 2^256: r[4] < 2^48
+    const uint64_t w0 = r[0] | (r[1] << 52), w1 = (r[1] >> 12) | (r[2] << 40),
+                   w2 = (r[2] >> 24) | (r[3] << 28), w3 = (r[3] >> 36) | (r[4] << 16);
+    uint32_t t9[9] = {(uint32_t)w0, (uint32_t)(w0 >> 32), (uint32_t)w1, (uint32_t)(w1 >> 32),
+                      (uint32_t)w2, (uint32_t)(w2 >> 32), (uint32_t)w3, (uint32_t)(w3 >> 32), 0u};
+    Fp<C> o1, out;
+    final_sub<C>(t9, o1.v);  // < 2m
+    uint32_t u9[9];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u9[i] = o1.v[i];
+    u9[8] = 0;
+    final_sub<C>(u9, out.v);  // < m
+    return out;
+}
+
 // ---- lazy reduction: 512-bit products, one Montgomery reduction per sum ----
 // A Montgomery product is half schoolbook product (128 IMAD) and half
 // reduction (136). Sums/differences of products (Karatsuba Fq2, x*y - z*w)

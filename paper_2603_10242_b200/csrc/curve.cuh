@@ -115,6 +115,50 @@ __device__ __forceinline__ void fq2_mul_wide(const Fq2& a, const Fq2& b, W16& c0
     sub_wide(c1.v, w1.v);
     add_mR_masked<FqCfg>(c0.v, sub_wide(c0.v, w1.v));
 }
+#ifndef ACEGPU_G2_F64
+#define ACEGPU_G2_F64 1  // Fq2 products through the FP64 wide product (W10) + one redc10 each
+#endif
+#if ACEGPU_G2_F64
+// FP64-domain Karatsuba: three 16 a b column products, sums / differences
+// column-wise, two reductions (bn254.cuh W10 / redc10).
+static __device__ __noinline__ W10 fq_mulw10_call(const Fq a, const Fq b) {
+    W10 w;
+    mul_wide10(a, b, w);
+    return w;
+}
+static __device__ __noinline__ Fq2Pair fq_redc10x2_call(const W10 x, const W10 y) {
+    return {redc10<FqCfg>(x), redc10<FqCfg>(y)};
+}
+// c0 = 16 (a0 b0 - a1 b1) (signed), c1 = 16 (a0 b1 + a1 b0) >= 0
+__device__ __forceinline__ void fq2_mul_wide10(const Fq2& a, const Fq2& b, W10& c0, W10& c1) {
+    c0 = fq_mulw10_call(a.c0, b.c0);
+    const W10 t1 = fq_mulw10_call(a.c1, b.c1);
+    c1 = fq_mulw10_call(add_raw(a.c0, a.c1), add_raw(b.c0, b.c1));
+    w10_sub(c1, c0);
+    w10_sub(c1, t1);
+    w10_sub(c0, t1);
+}
+static __device__ __noinline__ Fq2 fq2_mul_call(const Fq2 a, const Fq2 b) {
+    W10 c0, c1;
+    fq2_mul_wide10(a, b, c0, c1);
+    w10_add_m260<FqCfg>(c0);
+    const Fq2Pair r = fq_redc10x2_call(c0, c1);
+    return {r.a, r.b};
+}
+// a b - c d over Fq2: six products, two reductions.
+static __device__ __noinline__ Fq2 fq2_mul_sub_call(const Fq2 a, const Fq2 b, const Fq2 c,
+                                                    const Fq2 d) {
+    W10 x0, x1, y0, y1;
+    fq2_mul_wide10(a, b, x0, x1);
+    fq2_mul_wide10(c, d, y0, y1);
+    w10_sub(x0, y0);
+    w10_sub(x1, y1);
+    w10_add_m260<FqCfg>(x0);
+    w10_add_m260<FqCfg>(x1);
+    const Fq2Pair r = fq_redc10x2_call(x0, x1);
+    return {r.a, r.b};
+}
+#else
 static __device__ __noinline__ Fq2 fq2_mul_call(const Fq2 a, const Fq2 b) {
     W16 c0, c1;
     fq2_mul_wide(a, b, c0, c1);
@@ -130,6 +174,7 @@ static __device__ __noinline__ Fq2 fq2_mul_sub_call(const Fq2 a, const Fq2 b, co
     add_mR_masked<FqCfg>(x1.v, sub_wide(x1.v, y1.v));
     return ACE_REDC2(x0, x1);
 }
+#endif
 #if ACEGPU_ONE_BODY && ACEGPU_FQ2_SHARED
 __device__ __forceinline__ Fq fq_mul_sub_call(const Fq& a, const Fq& b, const Fq& c, const Fq& d) {
     W16 w = fq_mul_wide_call(a, b);
@@ -156,7 +201,17 @@ __device__ __forceinline__ Fq2 fmul(const Fq2& a, const Fq2& b) {
     return {sub(t0, t1), sub(sub(t2, t0), t1)};
 }
 #endif
-#if ACEGPU_LAZY && ACEGPU_FQ2_SHARED
+#if ACEGPU_G2_F64
+// (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u: two FP64 wide products
+// (both non-negative, below 32 p^2), two reductions.
+__device__ __forceinline__ Fq2 fsqr(const Fq2& a) {
+    W10 t = fq_mulw10_call(a.c0, a.c1);
+    const W10 u = fq_mulw10_call(add_raw(a.c0, a.c1), sub(a.c0, a.c1));
+    w10_shl1(t);
+    const Fq2Pair r = fq_redc10x2_call(u, t);
+    return {r.a, r.b};
+}
+#elif ACEGPU_LAZY && ACEGPU_FQ2_SHARED
 // (c0 + c1 u)^2 = (c0 + c1)(c0 - c1) + 2 c0 c1 u through the shared wide
 // bodies: (c0 + c1) unreduced times (c0 - c1) mod p < 2p^2, and 2 c0 c1 <
 // 2p^2 (a one-bit shift of the 512-bit product), both below p 2^256.
