@@ -182,6 +182,16 @@ __device__ __forceinline__ Fq fq_mul_sub_call(const Fq& a, const Fq& b, const Fq
     add_mR_masked<FqCfg>(w.v, sub_wide(w.v, x.v));
     return fq_redc_call(w);
 }
+#elif ACEGPU_G2_F64 && !ACEGPU_G1_MULSUB_CIOS
+// a b - c d: two FP64 wide products, one reduction (|16 (ab - cd)| < p 2^260)
+static __device__ __noinline__ Fq fq_mul_sub_call(const Fq a, const Fq b, const Fq c, const Fq d) {
+    W10 w, x;
+    mul_wide10(a, b, w);
+    mul_wide10(c, d, x);
+    w10_sub(w, x);
+    w10_add_m260<FqCfg>(w);
+    return redc10<FqCfg>(w);
+}
 #else
 static __device__ __noinline__ Fq fq_mul_sub_call(const Fq a, const Fq b, const Fq c, const Fq d) {
     return mul_sub_mul(a, b, c, d);
