@@ -1401,7 +1401,7 @@ def spawn_ranks(n: int) -> int:
     except Exception:
         ngpu = 0
     if ngpu < n:
-        env.update({"ACE_BENCH_DEVICE": "0", "ACE_DIST_BACKEND": "gloo",
+        env.update({"ACE_BENCH_DEVICE": "0", "ACEGPU_DEVICE": "0", "ACE_DIST_BACKEND": "gloo",
                     "ACE_BENCH_SHARED_GPU": "1"})
         log(f"bench.py: {n} ranks on {ngpu} GPU(s): functional run, gloo, all ranks on cuda:0")
     with socket.socket() as so:
