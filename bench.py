@@ -1137,7 +1137,7 @@ def g16_ncu_summary() -> dict | None:
     """fmaheavy-pipe utilisation and DRAM bytes of the Groth16 chunk's bucket
     accumulation kernels from the committed ncu capture (one chunk)."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r02_ncu_g16_accumulate.csv")
+    path = os.path.join(ROOT, "profiles", "r02_ncu_g16_accumulate_final.csv")
     try:
         rows = list(csv.reader(open(path)))
     except OSError:
@@ -1159,7 +1159,7 @@ def g16_ncu_summary() -> dict | None:
             "dram__bytes_read.sum", "dram__bytes_write.sum", "launch__registers_per_thread")}
         pick["kernel"] = d["Kernel Name"][:80]
         out.append(pick)
-    return {"source": "profiles/r02_ncu_g16_accumulate.csv", "launches": out} if out else None
+    return {"source": "profiles/r02_ncu_g16_accumulate_final.csv", "launches": out} if out else None
 
 
 def accepted_total(codes, world: int) -> int:
