@@ -1862,7 +1862,7 @@ struct acegpu_r1cs {
         DeviceGuard g(device);
         for (auto& M : mat)
             for (void* p : {(void*)M.rowptr, (void*)M.col, (void*)M.val, (void*)M.colptr,
-                            (void*)M.crow, (void*)M.cval})
+                            (void*)M.crow, (void*)M.cval, (void*)M.long_rows})
                 if (p) cudaFree(p);
     }
 };
@@ -2182,7 +2182,7 @@ extern "C" int acegpu_r1cs_create(acegpu_ctx* c, uint64_t m, uint64_t vars, uint
     // host-side validation + the public rows + the CSC transposes
     struct Host {
         std::vector<uint64_t> rp, cp;
-        std::vector<uint32_t> col, crow;
+        std::vector<uint32_t> col, crow, longr;
         std::vector<uint8_t> val, cval;
     } h[3];
     for (int k = 0; k < 3; ++k) {
@@ -2206,6 +2206,8 @@ extern "C" int acegpu_r1cs_create(acegpu_ctx* c, uint64_t m, uint64_t vars, uint
             }
             H.rp.push_back(H.col.size());
         }
+        for (uint64_t j = 0; j < rows; ++j)
+            if (H.rp[j + 1] - H.rp[j] > bn::kR1csLongRow) H.longr.push_back(uint32_t(j));
         // CSC (counting sort by column, stable in row order)
         H.cp.assign(vars + 1, 0);
         for (uint64_t e = 0; e < nnz; ++e) ++H.cp[H.col[e] + 1];
@@ -2245,6 +2247,8 @@ extern "C" int acegpu_r1cs_create(acegpu_ctx* c, uint64_t m, uint64_t vars, uint
         RET(up(&M.colptr, h[k].cp));
         RET(up(&M.crow, h[k].crow));
         RET(up(&M.cval, h[k].cval));
+        M.n_long = h[k].longr.size();
+        RET(up(&M.long_rows, h[k].longr));
         // values: 32-B LE integers -> Montgomery (to_mont reduces any value < 2^256)
         bn::launch_fr_convert(M.val, M.nnz, 1, s);
         bn::launch_fr_convert(M.cval, M.nnz, 1, s);

@@ -154,6 +154,15 @@ __device__ __forceinline__ void digits(const uint8_t* s, int32_t d[kMsmWindows])
     }
 }
 
+// Histogram / scatter with warp-aggregated atomics: lanes whose digit lands
+// in the same bucket elect one lane for the atomic (__match_any_sync), so a
+// hot bucket (a 0/1 witness sends every point to bucket 1) costs one atomic
+// per warp instead of 32 serialised ones. Lanes past n take part with a
+// bucket no real digit uses.
+#ifndef ACEGPU_SORT_AGG
+#define ACEGPU_SORT_AGG 1
+#endif
+#if !ACEGPU_SORT_AGG
 __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
@@ -163,7 +172,6 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
     for (int w = 0; w < kMsmWindows; ++w)
         if (d[w]) atomicAdd(&hist[abs(d[w]) - 1], 1u);
 }
-
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
                                uint32_t* sorted) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -177,6 +185,41 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
         sorted[pos] = (uint32_t)(w * n + i) | (d[w] < 0 ? 0x80000000u : 0u);
     }
 }
+#else
+__global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    int32_t d[kMsmWindows];
+    if (i < n) digits(scalars + 32 * i, d);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int w = 0; w < kMsmWindows; ++w) {
+        const uint32_t key = (i < n && d[w]) ? (uint32_t)(abs(d[w]) - 1) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
+    }
+}
+
+__global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
+                               uint32_t* sorted) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    int32_t d[kMsmWindows];
+    if (i < n) digits(scalars + 32 * i, d);
+    const int lane = threadIdx.x & 31;
+    const uint32_t below = (1u << lane) - 1u;
+#pragma unroll
+    for (int w = 0; w < kMsmWindows; ++w) {
+        const uint32_t key = (i < n && d[w]) ? (uint32_t)(abs(d[w]) - 1) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (key != 0xFFFFFFFFu && lane == leader) base = atomicAdd(&cursor[key], __popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        if (key != 0xFFFFFFFFu)
+            sorted[base + __popc(peers & below)] =
+                (uint32_t)(w * n + i) | (d[w] < 0 ? 0x80000000u : 0u);
+    }
+}
+#endif
 
 // The non-empty bucket b with offs[b] <= pos < offs[b + 1].
 __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
@@ -314,25 +357,67 @@ __global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const 
     store_xyzz(buckets + (uint64_t)X * b, acc);
 }
 
-// One CTA per queued heavy bucket (grid-stride): threads stride over its
-// segment partials, then a CTA tree.
+// Heavy buckets in two passes: the segment partials of every queued bucket
+// are cut into slices of kHeavySlice segments, one CTA per slice (grid-
+// stride over all slices of all heavy buckets) sums its slice into
+// heavy_part; then one CTA per heavy bucket sums its slice sums. A 0/1
+// witness sends ~a million entries (16k segments) to one bucket: one CTA
+// walking them was the longest kernel of such a proof.
+constexpr uint32_t kHeavySlice = 256;  // segments per slice (2 per thread)
+// slices of heavy bucket h, and the first slice index of h (nh is small)
+__device__ __forceinline__ uint32_t heavy_slices(const uint32_t* offs, const uint32_t* heavy,
+                                                 uint32_t h, uint32_t segsz) {
+    const int b = heavy[1 + h];
+    const uint32_t s0 = offs[b] / segsz, s1 = (offs[b + 1] - 1) / segsz;
+    return (s1 - s0 + kHeavySlice) / kHeavySlice;  // segments s0..s1
+}
 template <class F>
-__global__ void __launch_bounds__(128) heavy_kernel(const uint32_t* offs, const uint8_t* partials,
-                                                    uint8_t* buckets, const uint32_t* heavy,
-                                                    uint32_t segsz) {
+__global__ void __launch_bounds__(128) heavy_slice_kernel(const uint32_t* offs,
+                                                          const uint8_t* partials,
+                                                          const uint32_t* heavy, uint32_t segsz,
+                                                          uint8_t* heavy_part) {
     constexpr int X = Lay<F>::XZ;
     const uint32_t nh = heavy[0];
-    for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+    uint32_t h = 0, first = 0;  // the bucket of the current item and its first slice
+    for (uint32_t it = blockIdx.x;; it += gridDim.x) {
+        while (h < nh && it >= first + heavy_slices(offs, heavy, h, segsz)) {
+            first += heavy_slices(offs, heavy, h, segsz);
+            ++h;
+        }
+        if (h >= nh) return;
         const int b = heavy[1 + h];
-        const uint32_t s = offs[b], e = offs[b + 1];
-        const uint32_t s0 = s / segsz, s1 = (e - 1) / segsz;
+        const uint32_t s = offs[b];
+        const uint32_t s0 = s / segsz, s1 = (offs[b + 1] - 1) / segsz;
+        const uint32_t lo = s0 + (it - first) * kHeavySlice;
+        const uint32_t hi = min(s1, lo + kHeavySlice - 1);
         XYZZ<F> acc = XYZZ<F>::inf();
-        if (threadIdx.x == 0)
-            acc = load_xyzz<F>(partials + (uint64_t)X * (2ull * s0 + (s == s0 * segsz ? 0 : 1)));
-        for (uint32_t sg = s0 + 1 + threadIdx.x; sg <= s1; sg += blockDim.x)
-            acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg)));
+        for (uint32_t sg = lo + threadIdx.x; sg <= hi; sg += blockDim.x) {
+            // the bucket's first segment holds its run in slot 0 only if the
+            // bucket starts the segment, else in slot 1
+            const uint32_t slot = (sg == s0 && s != s0 * segsz) ? 1 : 0;
+            acc = xyzz_add(acc, load_xyzz<F>(partials + (uint64_t)X * (2ull * sg + slot)));
+        }
         acc = cta_sum128(acc);
-        if (threadIdx.x == 0) store_xyzz(buckets + (uint64_t)X * b, acc);
+        if (threadIdx.x == 0) store_xyzz(heavy_part + (uint64_t)X * it, acc);
+        __syncthreads();
+    }
+}
+template <class F>
+__global__ void __launch_bounds__(128) heavy_final_kernel(const uint32_t* offs,
+                                                          const uint32_t* heavy, uint32_t segsz,
+                                                          const uint8_t* heavy_part,
+                                                          uint8_t* buckets) {
+    constexpr int X = Lay<F>::XZ;
+    const uint32_t nh = heavy[0];
+    uint32_t first = 0, h0 = 0;
+    for (uint32_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        for (; h0 < h; ++h0) first += heavy_slices(offs, heavy, h0, segsz);
+        const uint32_t ns = heavy_slices(offs, heavy, h, segsz);
+        XYZZ<F> acc = XYZZ<F>::inf();
+        for (uint32_t k = threadIdx.x; k < ns; k += blockDim.x)
+            acc = xyzz_add(acc, load_xyzz<F>(heavy_part + (uint64_t)X * (first + k)));
+        acc = cta_sum128(acc);
+        if (threadIdx.x == 0) store_xyzz(buckets + (uint64_t)X * heavy[1 + h], acc);
         __syncthreads();
     }
 }
@@ -611,7 +696,11 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
             cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||
             cudaMalloc(&sc.buckets, (size_t)256 * kMsmBuckets) ||
             cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128)) ||
-            cudaMalloc(&sc.heavy, 4 * (kMsmBuckets + 1)))
+            cudaMalloc(&sc.heavy, 4 * (kMsmBuckets + 1)) ||
+            // slices: <= nseg / kHeavySlice + one partial slice per heavy bucket
+            // (each spans > kHeavySpan segments)
+            cudaMalloc(&sc.heavy_part,
+                       (size_t)256 * (keep_segs / kHeavySlice + keep_segs / kHeavySpan + 16)))
             return -1;
         cub::DeviceScan::ExclusiveSum(nullptr, sc.scan_bytes, sc.hist, sc.offs, kMsmBuckets + 1, s);
         if (cudaMalloc(&sc.scan_tmp, sc.scan_bytes)) return -1;
@@ -679,7 +768,10 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
             table, sc.sorted, sc.offs, sc.buckets, sc.partials, segsz);
         fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets,
                                                           sc.heavy, segsz);
-        heavy_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy, segsz);
+        heavy_slice_kernel<F><<<4 * 148, 128, 0, s>>>(sc.offs, sc.partials, sc.heavy, segsz,
+                                                        sc.heavy_part);
+        heavy_final_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.heavy, segsz, sc.heavy_part,
+                                                  sc.buckets);
     }
     reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
     static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
@@ -700,6 +792,8 @@ void MsmScratch::release() {
     aff_cap = 0;
     cap_segs = 0;
     hist = offs = cursor = sorted = heavy = nullptr;
+    if (heavy_part) cudaFree(heavy_part);
+    heavy_part = nullptr;
     partials = buckets = segsum = nullptr;
     scan_tmp = nullptr;
     scan_bytes = 0;

@@ -30,6 +30,7 @@ struct MsmScratch {
     uint8_t* buckets = nullptr;    // kMsmBuckets XYZZ
     uint8_t* segsum = nullptr;     // reduction partials (one per CTA)
     uint32_t* heavy = nullptr;     // [count, bucket ids] of buckets spanning many segments
+    uint8_t* heavy_part = nullptr; // per-slice sums of the heavy buckets (XYZZ records)
     void* scan_tmp = nullptr;      // CUB scan temporary storage
     uint8_t* aff_pts[2] = {nullptr, nullptr};     // batch-affine levels (G1): points
     uint32_t* aff_offs[2] = {nullptr, nullptr};   // and bucket offsets, ping-pong

@@ -14,11 +14,19 @@ namespace {
 __device__ __forceinline__ Fr ld(const uint8_t* p) { return load<FrCfg>(p); }
 __device__ __forceinline__ void st(uint8_t* p, const Fr& x) { store<FrCfg>(p, x); }
 
+__device__ __forceinline__ Fr shfl_down(const Fr& a, int d) {
+    Fr r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], d);
+    return r;
+}
+
 __global__ void spmv_kernel(const uint64_t* rowptr, const uint32_t* col, const uint8_t* val,
                             const uint8_t* zm, uint64_t rows, uint64_t pad, uint8_t* out) {
     const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (j >= pad) return;
     Fr acc = Fr::zero();
+    if (j < rows && rowptr[j + 1] - rowptr[j] > kR1csLongRow) return;  // long_rows_kernel
     if (j < rows) {
         const Fr one = Fr::one();
         for (uint64_t k = rowptr[j], e = rowptr[j + 1]; k < e; ++k) {
@@ -29,11 +37,23 @@ __global__ void spmv_kernel(const uint64_t* rowptr, const uint32_t* col, const u
     st(out + 32 * j, acc);
 }
 
-__device__ __forceinline__ Fr shfl_down(const Fr& a, int d) {
-    Fr r;
+// one warp per long row: lanes stride over the entries, then a shuffle tree
+__global__ void long_rows_kernel(const uint64_t* rowptr, const uint32_t* col, const uint8_t* val,
+                                 const uint32_t* long_rows, uint64_t n_long, const uint8_t* zm,
+                                 uint8_t* out) {
+    const uint64_t w = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= n_long) return;  // whole warps exit together
+    const uint32_t j = long_rows[w];
+    const Fr one = Fr::one();
+    Fr acc = Fr::zero();
+    for (uint64_t k = rowptr[j] + lane, e = rowptr[j + 1]; k < e; k += 32) {
+        const Fr v = ld(val + 32 * k), x = ld(zm + 32ull * col[k]);
+        acc = add(acc, v == one ? x : mul(v, x));
+    }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.v[i] = __shfl_down_sync(0xffffffffu, a.v[i], d);
-    return r;
+    for (int d = 16; d >= 1; d >>= 1) acc = add(acc, shfl_down(acc, d));
+    if (lane == 0) st(out + 32ull * j, acc);
 }
 
 __global__ void colsum_kernel(const uint64_t* colptr, const uint32_t* crow, const uint8_t* cval,
@@ -73,6 +93,9 @@ inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 void r1cs_spmv(const R1csMat& M, const uint8_t* zm, uint64_t rows, uint64_t pad, uint8_t* out,
                cudaStream_t s) {
     if (pad) spmv_kernel<<<grid(pad, 128), 128, 0, s>>>(M.rowptr, M.col, M.val, zm, rows, pad, out);
+    if (M.n_long)
+        long_rows_kernel<<<grid(32 * M.n_long, 128), 128, 0, s>>>(M.rowptr, M.col, M.val,
+                                                                 M.long_rows, M.n_long, zm, out);
 }
 
 void r1cs_colsum(const R1csMat& M, const uint8_t* L, uint64_t vars, uint8_t* out,

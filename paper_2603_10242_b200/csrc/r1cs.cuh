@@ -17,10 +17,16 @@ struct R1csMat {
     uint64_t* rowptr = nullptr;  // rows + 1
     uint32_t* col = nullptr;     // nnz
     uint8_t* val = nullptr;      // nnz x 32
+    uint32_t* long_rows = nullptr;  // rows with more than kR1csLongRow entries (a warp each)
+    uint64_t n_long = 0;
     uint64_t* colptr = nullptr;  // vars + 1 (CSC transpose, setup only)
     uint32_t* crow = nullptr;    // nnz
     uint8_t* cval = nullptr;     // nnz x 32
 };
+
+// Rows longer than this (the packing / 32-bit addition rows of a SHA-256
+// circuit hold ~200 entries) are evaluated by a warp each.
+constexpr uint64_t kR1csLongRow = 16;
 
 // a[j] = sum_k val[k] zm[col[k]] over row j's entries (zm, out: Montgomery),
 // rows [0, rows); rows < pad are written as zero up to pad.
