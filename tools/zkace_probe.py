@@ -10,7 +10,7 @@ import bench  # noqa: E402
 from paper_2603_10242_b200 import _native as N, groth16, r1cs, zkace_circuit as Z  # noqa: E402
 
 ctx = N.context(0)
-fb, revs, rix = bench.canonical_block_host(32, ctx)
+fb, revs, rix = bench.canonical_block_host(64, ctx)
 import numpy as np  # noqa: E402
 T = int(os.environ.get("ZK_T", "20"))
 keys_all = np.zeros(32 * T, np.uint8)
