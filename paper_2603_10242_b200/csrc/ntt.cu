@@ -28,6 +28,21 @@ namespace {
 __device__ __forceinline__ Fr ld(const Fr* p) { return load<FrCfg>(p); }
 __device__ __forceinline__ void st(Fr* p, const Fr& x) { store<FrCfg>(p, x); }
 
+// Pass kernels' occupancy: 512-thread CTAs with 64 KB of shared memory; the
+// FP64 product needs ~84 registers, which allows only one CTA per SM, so the
+// passes are capped at 64 registers for two (loads of one CTA overlap the
+// other's butterflies). ACEGPU_NTT_CIOS=1 uses the IMAD product (fewer
+// registers) inside the NTT instead.
+#ifndef ACEGPU_NTT_MINB
+#define ACEGPU_NTT_MINB 2
+#endif
+#ifndef ACEGPU_NTT_CIOS
+#define ACEGPU_NTT_CIOS 0
+#endif
+#if ACEGPU_NTT_CIOS
+__device__ __forceinline__ Fr mul(const Fr& a, const Fr& b) { return mul_cios(a, b); }
+#endif
+
 // Shared-memory sub-DFT arrays are planar: the low and high 16 B of element
 // i live at plane 0 / plane 1 index i, so a warp's 16-B accesses to
 // consecutive elements are contiguous (4 wavefronts, no bank conflicts)
@@ -106,7 +121,7 @@ struct PassArgs {
 };
 
 // Pass A: columns i1 in [cb*R, cb*R+R), DFT length n2 over i2.
-__global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
+__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_a(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
     const int n1 = 1 << a.L1, n2 = 1 << a.L2;
     constexpr int R = kNttR;
@@ -140,7 +155,7 @@ __global__ void __launch_bounds__(512) ntt_pass_a(PassArgs a) {
 }
 
 // Pass C: rows k2 in [rb*R, rb*R+R), DFT length n1 over i1; natural output.
-__global__ void __launch_bounds__(512) ntt_pass_c(PassArgs a) {
+__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_c(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
     const int n1 = 1 << a.L1, n2 = 1 << a.L2;
     constexpr int R = kNttR;
