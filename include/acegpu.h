@@ -293,6 +293,26 @@ void acegpu_r1cs_free(acegpu_r1cs* r);
 int acegpu_r1cs_shape(const acegpu_r1cs* r, uint64_t* rows, uint64_t* vars, uint64_t* n_pub);
 int acegpu_r1cs_eval(acegpu_ctx* ctx, const acegpu_r1cs* r, const uint8_t* z, uint8_t* a,
                      uint8_t* b, uint8_t* c);
+/* GPU witness generation for bit-level circuits (witprog.cu): a straight-
+ * line program compiled once by the host circuit builder (zkace_circuit.py:
+ * 4 x u32 per op, opcode << 24 | dst then operands; ADD operand lists in
+ * addtab; var_slot = the slot of each private variable in order) and run by
+ * every transaction on the device. run / run_dev write the full assignment
+ * z = ONE | 5T public inputs (obj_hash, domain, credential packed big-endian
+ * from the 104-B attestations) | T x n_vars private values (32-B LE). */
+typedef struct acegpu_witprog acegpu_witprog;
+int acegpu_witprog_create(acegpu_ctx* ctx, const uint32_t* ops4, uint64_t n_ops,
+                          const uint32_t* addtab, uint64_t n_addtab, uint32_t n_adds,
+                          const uint32_t* var_slot, uint32_t n_vars, uint32_t n_slots,
+                          acegpu_witprog** out);
+void acegpu_witprog_free(acegpu_witprog* w);
+int acegpu_witprog_run(acegpu_ctx* ctx, const acegpu_witprog* w, const uint8_t* keys,
+                       const uint8_t* atts, uint32_t T, uint8_t* z);
+/* run_dev: T transactions in chunks of Tc (0 = one chunk), the chunks'
+ * assignments (each 1 + 5 Tc + Tc n_vars elements) back to back in d_z. */
+int acegpu_witprog_run_dev(acegpu_ctx* ctx, void* stream, const acegpu_witprog* w,
+                           const uint8_t* d_keys, uint64_t key_stride, const uint8_t* d_atts,
+                           uint32_t T, uint32_t Tc, uint8_t* d_z);
 /* Groth16 keys for a general R1CS (r must outlive the key): the query
  * polynomials are the column sums A^T L(tau), B^T L(tau), C^T L(tau) of the
  * Lagrange basis; the verifying key has n_pub + 1 IC points. prove_z takes the

@@ -79,6 +79,12 @@ _SIGS = {
     "acegpu_g16_setup": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_void_p)]),
     "acegpu_g16_free": (None, [C.c_void_p]),
     "acegpu_r1cs_free": (None, [C.c_void_p]),
+    "acegpu_witprog_free": (None, [C.c_void_p]),
+    "acegpu_witprog_create": (C.c_int, [ctxp, vp, u64, vp, u64, C.c_uint32, vp, C.c_uint32,
+                                        C.c_uint32, C.POINTER(C.c_void_p)]),
+    "acegpu_witprog_run": (C.c_int, [ctxp, C.c_void_p, vp, vp, C.c_uint32, vp]),
+    "acegpu_witprog_run_dev": (C.c_int, [ctxp, C.c_void_p, C.c_void_p, vp, u64, vp, C.c_uint32,
+                                         C.c_uint32, vp]),
     "acegpu_r1cs_shape": (C.c_int, [C.c_void_p, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "acegpu_g16_shape": (C.c_int, [C.c_void_p, u64p, u64p, C.POINTER(C.c_uint32)]),
     "acegpu_g16_prove_chunk": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp, vp]),

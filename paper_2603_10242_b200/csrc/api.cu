@@ -22,6 +22,7 @@
 #include "msm.cuh"
 #include "ntt.cuh"
 #include "r1cs.cuh"
+#include "witprog.cuh"
 
 #ifndef ACEGPU_GIT
 #define ACEGPU_GIT "dev"
@@ -2167,6 +2168,93 @@ extern "C" int acegpu_g16_setup_r1cs(acegpu_ctx* c, const acegpu_r1cs* r, const 
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     return g16_setup_impl(c, uint32_t(r->n_pub), 0, r, trapdoor5, out);
+}
+
+// ---- witness programs (GPU witness generation for bit circuits) ---------------
+struct acegpu_witprog {
+    int device = 0;
+    bn::WitProg p;
+    uint4* ops = nullptr;
+    uint32_t *addtab = nullptr, *var_slot = nullptr;
+    ~acegpu_witprog() {
+        DeviceGuard g(device);
+        for (void* q : {(void*)ops, (void*)addtab, (void*)var_slot})
+            if (q) cudaFree(q);
+    }
+};
+
+extern "C" void acegpu_witprog_free(acegpu_witprog* w) { delete w; }
+
+extern "C" int acegpu_witprog_create(acegpu_ctx* c, const uint32_t* ops4, uint64_t n_ops,
+                                     const uint32_t* addtab, uint64_t n_addtab, uint32_t n_adds,
+                                     const uint32_t* var_slot, uint32_t n_vars, uint32_t n_slots,
+                                     acegpu_witprog** out) {
+    if (!ops4 || !var_slot || !out || !n_ops || !n_slots) return fail(ACEGPU_EINVAL, "null argument");
+    if (n_slots >= (1u << 24)) return fail(ACEGPU_EINVAL, "witprog: too many slots");
+    for (uint64_t i = 0; i < n_ops; ++i)
+        if ((ops4[4 * i] & 0xFFFFFFu) >= (ops4[4 * i] >> 24 == 9 ? n_adds : n_slots))
+            return fail(ACEGPU_EINVAL, "witprog: destination out of range");
+    for (uint32_t i = 0; i < n_vars; ++i)
+        if (var_slot[i] >= n_slots) return fail(ACEGPU_EINVAL, "witprog: var slot out of range");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = c->stream;
+    std::unique_ptr<acegpu_witprog> w(new acegpu_witprog());
+    w->device = c->device;
+    if (cudaMalloc(&w->ops, 16 * n_ops) || cudaMalloc(&w->addtab, 4 * (n_addtab ? n_addtab : 1)) ||
+        cudaMalloc(&w->var_slot, 4 * (n_vars ? n_vars : 1)))
+        return fail(ACEGPU_ECUDA, "witprog alloc");
+    CK(cudaMemcpyAsync(w->ops, ops4, 16 * n_ops, cudaMemcpyHostToDevice, s));
+    if (n_addtab) CK(cudaMemcpyAsync(w->addtab, addtab, 4 * n_addtab, cudaMemcpyHostToDevice, s));
+    if (n_vars) CK(cudaMemcpyAsync(w->var_slot, var_slot, 4 * n_vars, cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    w->p = {w->ops, n_ops, w->addtab, w->var_slot, n_slots, n_adds, n_vars};
+    *out = w.release();
+    return ACEGPU_OK;
+}
+
+// z (device) for T transactions in chunks of Tc (0: one chunk of T), each
+// chunk's assignment (1 + 5 Tc + Tc n_vars) x 32 B, back to back: attest
+// keys (32 B each, key_stride apart: 256 for build_witness records) and their
+// 104-B attestations, all on the device.
+extern "C" int acegpu_witprog_run_dev(acegpu_ctx* c, void* stream, const acegpu_witprog* w,
+                                      const uint8_t* d_keys, uint64_t key_stride,
+                                      const uint8_t* d_atts, uint32_t T, uint32_t Tc,
+                                      uint8_t* d_z) {
+    if (!w || !d_keys || !d_atts || !d_z) return fail(ACEGPU_EINVAL, "null argument");
+    if (Tc == 0) Tc = T;
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    uint8_t* scratch;
+    const size_t sb = (size_t)T * w->p.n_slots, ab = 8ull * T * (w->p.n_adds ? w->p.n_adds : 1);
+    RET(ws(c, kG16Wit, ((sb + 255) & ~size_t(255)) + ab, &scratch));
+    bn::witprog_run(w->p, d_keys, key_stride, d_atts, T, Tc, reinterpret_cast<int8_t*>(scratch),
+                    reinterpret_cast<int64_t*>(scratch + ((sb + 255) & ~size_t(255))), d_z,
+                    pick(c, stream));
+    CKL();
+    c->launches += 3;
+    return ACEGPU_OK;
+}
+
+// host-buffer form: keys T x 32 B, atts T x 104 B -> z
+extern "C" int acegpu_witprog_run(acegpu_ctx* c, const acegpu_witprog* w, const uint8_t* keys,
+                                  const uint8_t* atts, uint32_t T, uint8_t* z) {
+    if (!w || !keys || !atts || !z) return fail(ACEGPU_EINVAL, "null argument");
+    uint8_t *dk, *da, *dz;
+    const uint64_t zb = 32ull * (1 + 5ull * T + (uint64_t)T * w->p.n_vars);
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard guard(c->device);
+        RET(h2d_t(c, kBnA, keys, 32ull * T, c->stream, &dk));
+        RET(h2d_t(c, kBnB, atts, 104ull * T, c->stream, &da));
+        RET(ws(c, kBnOut, zb, &dz));
+    }
+    RET(acegpu_witprog_run_dev(c, c->stream, w, dk, 32, da, T, T, dz));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    CK(cudaMemcpyAsync(z, dz, zb, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ACEGPU_OK;
 }
 
 // ---- general R1CS ------------------------------------------------------------

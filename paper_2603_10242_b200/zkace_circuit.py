@@ -43,11 +43,14 @@ N_PUB_PER_TX = 5  # obj_hash (2), domain (1), credential (2)
 
 
 class Bit:
-    """A boolean value as a linear combination {var: coef} (var 0 = ONE)."""
-    __slots__ = ("lc", "v")
+    """A boolean value as a linear combination {var: coef} (var 0 = ONE) and,
+    for the witness program, the slot that holds its value (slots 0 / 1 are
+    the constants)."""
+    __slots__ = ("lc", "v", "s")
 
-    def __init__(self, lc: dict, v: int):
+    def __init__(self, lc: dict, v: int, s: int | None = None):
         self.lc, self.v = lc, v
+        self.s = v if s is None else s  # constants live in slots 0 / 1
 
 
 def _const(b: int) -> Bit:
@@ -63,9 +66,21 @@ class Builder:
         self.A: list[dict] = []
         self.B: list[dict] = []
         self.C: list[dict] = []
+        # witness program (zkace_witness.py): ops computing every slot from
+        # earlier ones, and the slot of each private variable in creation order
+        self.prog: list[tuple] = []
+        self.nslot = 2
+        self.var_slot: list[int] = []
 
-    def var(self, value: int) -> int:
+    def slot(self, op: tuple) -> int:
+        s = self.nslot
+        self.nslot += 1
+        self.prog.append((op[0], s) + op[1:])
+        return s
+
+    def var(self, value: int, slot: int | None = None) -> int:
         self.vals.append(value % R)
+        self.var_slot.append(slot)
         return len(self.vals) - 1
 
     def row(self, a: dict, b: dict, c: dict) -> None:
@@ -74,10 +89,13 @@ class Builder:
         self.C.append(c)
 
     # ---- bits
-    def bit(self, v: int) -> Bit:
-        x = self.var(v)
+    def bit(self, v: int, src: tuple) -> Bit:
+        """A new boolean variable whose value the witness program computes
+        with `src` (("KEY", i) / ("MSG", i) / ("SUMBIT", add, k))."""
+        s = self.slot(src)
+        x = self.var(v, s)
         self.row({x: 1}, {x: 1}, {x: 1})  # x * x = x
-        return Bit({x: 1}, v)
+        return Bit({x: 1}, v, s)
 
     @staticmethod
     def _is_const(lc: dict) -> bool:
@@ -95,37 +113,49 @@ class Builder:
                     out.pop(k, None)
         return out
 
-    def prod(self, a: dict, av: int, b: dict, bv: int) -> dict:
+    def prod(self, a: dict, av: int, b: dict, bv: int, op: tuple = ()) -> dict:
         """a * b: a constant factor scales the other (no constraint), else one
-        multiplication row with a fresh variable."""
+        multiplication row with a fresh variable (its value computed by the
+        witness program op `op`)."""
         if self._is_const(a):
             return self.lin((av, b))
         if self._is_const(b):
             return self.lin((bv, a))
-        t = self.var(av * bv)
+        t = self.var(av * bv, self.slot(op))
         self.row(a, b, {t: 1})
         return {t: 1}
 
+    def _bit(self, lc: dict, v: int, op: tuple) -> Bit:
+        """A result bit: a constant, or a slot the program computes."""
+        if self._is_const(lc):
+            return Bit(lc, v)
+        return Bit(lc, v, self.slot(op))
+
     def xor(self, a: Bit, b: Bit) -> Bit:  # a + b - 2ab
-        t = self.prod(a.lc, a.v, b.lc, b.v)
-        return Bit(self.lin((1, a.lc), (1, b.lc), (-2, t)), a.v ^ b.v)
+        t = self.prod(a.lc, a.v, b.lc, b.v, ("AND", a.s, b.s))
+        return self._bit(self.lin((1, a.lc), (1, b.lc), (-2, t)), a.v ^ b.v, ("XOR", a.s, b.s))
 
     def ch(self, e: Bit, f: Bit, g: Bit) -> Bit:  # e (f - g) + g
-        t = self.prod(e.lc, e.v, self.lin((1, f.lc), (-1, g.lc)), f.v - g.v)
-        return Bit(self.lin((1, t), (1, g.lc)), (e.v & f.v) ^ ((1 - e.v) & g.v))
+        t = self.prod(e.lc, e.v, self.lin((1, f.lc), (-1, g.lc)), f.v - g.v,
+                      ("CHP", e.s, f.s, g.s))
+        return self._bit(self.lin((1, t), (1, g.lc)), (e.v & f.v) ^ ((1 - e.v) & g.v),
+                         ("CH", e.s, f.s, g.s))
 
     def maj(self, a: Bit, b: Bit, c: Bit) -> Bit:  # a (b + c - 2bc) + bc
-        bc = self.prod(b.lc, b.v, c.lc, c.v)
+        bc = self.prod(b.lc, b.v, c.lc, c.v, ("AND", b.s, c.s))
         inner = self.lin((1, b.lc), (1, c.lc), (-2, bc))
-        t = self.prod(a.lc, a.v, inner, b.v ^ c.v)
-        return Bit(self.lin((1, t), (1, bc)), (a.v & b.v) ^ (a.v & c.v) ^ (b.v & c.v))
+        t = self.prod(a.lc, a.v, inner, b.v ^ c.v, ("MAJP", a.s, b.s, c.s))
+        return self._bit(self.lin((1, t), (1, bc)), (a.v & b.v) ^ (a.v & c.v) ^ (b.v & c.v),
+                         ("MAJ", a.s, b.s, c.s))
 
     # ---- 32-bit words: lists of 32 Bits, LSB first
     def add(self, words: list, k: int = 0) -> list:
         s = sum(sum(b.v << i for i, b in enumerate(w)) for w in words) + k
         nc = max(1, (len(words) + (1 if k else 0) - 1).bit_length())
-        r = [self.bit((s >> i) & 1) for i in range(32)]
-        cr = [self.bit((s >> (32 + j)) & 1) for j in range(nc)]
+        # the sum itself: an "ADD" op over the words' bit slots (+ k)
+        add = self.slot(("ADD", tuple(b.s for w in words for b in w), k))
+        r = [self.bit((s >> i) & 1, ("SUMBIT", add, i)) for i in range(32)]
+        cr = [self.bit((s >> (32 + j)) & 1, ("SUMBIT", add, 32 + j)) for j in range(nc)]
         terms = [(1 << i, b.lc) for w in words for i, b in enumerate(w)]
         terms += [(-(1 << i), b.lc) for i, b in enumerate(r)]
         terms += [(-(1 << (32 + j)), b.lc) for j, b in enumerate(cr)]
@@ -187,9 +217,11 @@ def hmac_tx(B: Builder, key: bytes, obj_hash: bytes, domain: bytes, credential: 
             pub_vars: list[int]) -> None:
     """HMAC-SHA256(key, obj_hash || domain) == credential for one tx; the five
     public variables pub_vars get their packed values."""
-    kb = [[B.bit((byte >> (7 - i)) & 1) for i in range(8)] for byte in key]  # private key bits
+    kb = [[B.bit((byte >> (7 - i)) & 1, ("KEY", 8 * j + i)) for i in range(8)]
+          for j, byte in enumerate(key)]  # private key bits
     msg = obj_hash + domain
-    mb = [[B.bit((byte >> (7 - i)) & 1) for i in range(8)] for byte in msg]
+    mb = [[B.bit((byte >> (7 - i)) & 1, ("MSG", 8 * j + i)) for i in range(8)]
+          for j, byte in enumerate(msg)]
     # public packing: obj_hash halves, domain, credential halves (big-endian integers)
     def pack(byte_bits, pv):
         flat = [b for byte in byte_bits for b in byte]  # MSB first
@@ -247,13 +279,10 @@ def constraints_per_tx() -> int:
     return len(build_tx(bytes(32), bytes(104)).A)
 
 
-def chunk(keys: list[bytes], atts: list[bytes]):
-    """T transactions -> (m, vars, n_pub, A, B, C as r1cs.Csr, z) with
-    variables ONE | 5T public inputs | T x (the tx's private variables)."""
+def _structure(b0: Builder, T: int):
+    """CSR matrices of T copies of one tx's circuit, with variables ONE | 5T
+    public inputs | T x (the tx's private variables)."""
     from .r1cs import Csr
-    T = len(keys)
-    builders = [build_tx(k, a) for k, a in zip(keys, atts)]
-    b0 = builders[0]
     P = len(b0.vals) - 1 - N_PUB_PER_TX  # private variables per tx
     npub = N_PUB_PER_TX * T
     vars_ = 1 + npub + T * P
@@ -283,9 +312,88 @@ def chunk(keys: list[bytes], atts: list[bytes]):
             allr.append(rp[1:] + nnz * t)
         out.append(Csr(np.concatenate(allr).astype(np.uint64),
                        np.concatenate(allc).astype(np.uint32), np.concatenate(allv)))
+    return m0 * T, vars_, npub, out[0], out[1], out[2], P
+
+
+def chunk(keys: list[bytes], atts: list[bytes]):
+    """T transactions -> (m, vars, n_pub, A, B, C as r1cs.Csr, z) with
+    variables ONE | 5T public inputs | T x (the tx's private variables); z is
+    evaluated here on the host (the checker for the GPU witness program)."""
+    T = len(keys)
+    builders = [build_tx(k, a) for k, a in zip(keys, atts)]
+    m, vars_, npub, A, B, Cm, P = _structure(builders[0], T)
     z = [1] + [0] * npub + [0] * (T * P)
     for t, b in enumerate(builders):
         z[1 + N_PUB_PER_TX * t:1 + N_PUB_PER_TX * (t + 1)] = b.vals[1:1 + N_PUB_PER_TX]
         z[1 + npub + P * t:1 + npub + P * (t + 1)] = b.vals[1 + N_PUB_PER_TX:]
     za = np.frombuffer(b"".join(v.to_bytes(32, "little") for v in z), np.uint8).copy()
-    return m0 * T, vars_, npub, out[0], out[1], out[2], za
+    return m, vars_, npub, A, B, Cm, za
+
+
+def chunk_r1cs(T: int):
+    """The constraint system of a T-tx chunk alone (-> m, vars, n_pub, A, B, C):
+    the circuit's shape does not depend on the transactions."""
+    return _structure(build_tx(bytes(32), bytes(104)), T)[:6]
+
+
+_OPS = {"KEY": 1, "MSG": 2, "AND": 3, "XOR": 4, "CHP": 5, "CH": 6, "MAJP": 7, "MAJ": 8,
+        "ADD": 9, "SUMBIT": 10}
+
+
+class WitnessProgram:
+    """The circuit compiled to a GPU witness program (csrc/witprog.cu): the
+    builder's value ops in creation order, uploaded once; `run_dev` writes a
+    chunk's full assignment z from its attest keys and attestations."""
+
+    def __init__(self, ctx=None):
+        import ctypes as C
+        from . import _native as N
+        self.ctx = ctx or N.context()
+        b = build_tx(bytes(32), bytes(104))
+        add_ord: dict[int, int] = {}
+        ops = np.zeros((len(b.prog), 4), np.uint32)
+        addtab: list[int] = []
+        for i, op in enumerate(b.prog):
+            code, dst = _OPS[op[0]], op[1]
+            if op[0] == "ADD":
+                add_ord[dst] = len(add_ord)
+                ops[i] = (code << 24 | add_ord[dst], len(addtab), len(op[2]), op[3])
+                addtab.extend(op[2])
+            elif op[0] == "SUMBIT":
+                ops[i] = (code << 24 | dst, add_ord[op[2]], op[3], 0)
+            else:
+                ops[i] = [code << 24 | dst] + list(op[2:]) + [0] * (3 - len(op[2:]))
+        self.n_vars = len(b.var_slot)
+        self.n_slots = b.nslot
+        at = np.array(addtab or [0], np.uint32)
+        vs = np.array(b.var_slot, np.uint32)
+        h = C.c_void_p()
+        self.ctx.call("acegpu_witprog_create", ops.reshape(-1), len(b.prog), at, len(addtab),
+                      len(add_ord), vs, self.n_vars, self.n_slots, C.byref(h))
+        self.h = h
+        self.n_ops = len(b.prog)
+
+    def run(self, keys: list[bytes], atts: list[bytes]) -> np.ndarray:
+        T = len(keys)
+        z = np.zeros(32 * (1 + N_PUB_PER_TX * T + T * self.n_vars), np.uint8)
+        k = np.frombuffer(b"".join(keys), np.uint8).copy()
+        a = np.frombuffer(b"".join(atts), np.uint8).copy()
+        self.ctx.call("acegpu_witprog_run", self.h, k, a, T, z)
+        return z
+
+    def run_dev(self, d_keys, key_stride: int, d_atts, T: int, d_z, stream=None, Tc: int = 0):
+        """T transactions in chunks of Tc (0: one chunk), assignments back to back."""
+        self.ctx.call("acegpu_witprog_run_dev", stream, self.h, d_keys, key_stride, d_atts, T, Tc,
+                      d_z)
+
+    def close(self):
+        from . import _native as N
+        if self.h:
+            N.lib().acegpu_witprog_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -218,3 +218,84 @@ def test_zkace_hmac_circuit_proves_on_gpu(ctx):
     finally:
         pk.close()
         rc.close()
+
+
+def test_zkace_gpu_witness_program(ctx):
+    """GPU witness generation (csrc/witprog.cu): the circuit compiled to a
+    straight-line program and run per tx on the device gives exactly the
+    host builder's assignment — honest and forged transactions — and the
+    chunk proves and verifies from the GPU-made assignment."""
+    from paper_2603_10242_b200 import groth16, r1cs, zkace_circuit as Z
+    fb = O.multi_user_block(3, 2)
+    keys, atts = [], []
+    for i in range(3):
+        att = fb.att(i)
+        u = int(fb.rev_index[i])
+        keys.append(bytes(O.derive_attest_key(fb.revs[32 * u:32 * u + 32].tobytes(), att[64:72])))
+        atts.append(bytes(att))
+    atts[2] = atts[2][:90] + bytes([atts[2][90] ^ 1]) + atts[2][91:]  # tx 2 forged
+    prog = Z.WitnessProgram(ctx)
+    try:
+        _, _, _, _, _, _, z_host = Z.chunk(keys, atts)
+        z_gpu = prog.run(keys, atts)
+        assert z_gpu.tobytes() == z_host.tobytes()
+        m, V, npub, A, B, Cm = Z.chunk_r1cs(2)
+        rc = r1cs.R1CS(m, V, npub, A, B, Cm, ctx=ctx)
+        pk = groth16.ProvingKey.from_r1cs(rc, arr([3, 5, 7, 11, 13]), ctx)
+        try:
+            z2 = prog.run(keys[:2], atts[:2])
+            proof, _, _ = pk.prove_z(z2)
+            assert pk.verify_batch([proof], [z2.tobytes()[32:32 * (1 + npub)]])
+        finally:
+            pk.close()
+            rc.close()
+    finally:
+        prog.close()
+
+
+@pytest.mark.parametrize("n", [16, 37])
+def test_zkace_block_prover(ctx, n):
+    """The block path over the REAL credential relation (zkace.py): 16-tx
+    chunks, GPU witness generation, one Groth16 proof per chunk, the
+    reference's tree over the chunk proofs and the FC. The FC equals the
+    oracle's tree / FC over nodes (chunk proof | chunk digest | Tx) built from
+    the chunk proofs; the chunk proofs verify against the public inputs
+    recomputed from the block; a forged credential fails verification."""
+    from paper_2603_10242_b200 import shard, wire, zkace
+    fb = O.multi_user_block(n, 3)
+    wit = b""
+    for i in range(n):
+        att = fb.att(i)
+        u = int(fb.rev_index[i])
+        key = O.derive_attest_key(fb.revs[32 * u:32 * u + 32].tobytes(), att[64:72])
+        out = O.buf(256)
+        O.oracle().or_build_witness(O.ptr(key), O.ptr(att[:32]), out)
+        wit += bytes(out)
+    zp = zkace.ZkAceProver(16, arr([3, 5, 7, 11, 13]), ctx)
+    try:
+        for forged in (False, True):
+            atts = fb.atts.copy()
+            if forged:
+                atts[104 * (n - 1) + 80] ^= 2
+            wfb = wire.FlatBlock(fb.payloads, fb.offs, atts, np.frombuffer(fb.header, np.uint8).copy())
+            db = shard.DeviceBlock.upload(wfb, 0, n, np.frombuffer(fb.revs, np.uint8).copy(),
+                                          np.asarray(fb.rev_index, np.uint32), device=0)
+            import torch
+            db.witnesses = torch.from_numpy(np.frombuffer(wit, np.uint8).copy()).cuda()
+            codes = torch.full((n,), 0xEE, dtype=torch.uint8, device="cuda")
+            proof, fc, cps = zp.prove_block(db, n, codes=codes, return_chunk_proofs=True)
+            proofs = [bytes(x) for x in cps.cpu().numpy()]
+            pubs = zp.public_inputs(atts, n)
+            ok = zp.verify_chunk_proofs(proofs, atts, n)
+            assert ok == (not forged)
+            assert int((codes.cpu().numpy() != 0).sum()) == (1 if forged else 0)
+            nodes = b"".join(p + SP.chunk_digest(q, 16 * 5) + b"\0" for p, q in zip(proofs, pubs))
+            outp = O.buf(289)
+            lv, pr = C.c_uint64(), C.c_uint64()
+            O.oracle().or_aggregate_tree(O.ptr(nodes), C.c_uint64(len(proofs)), outp,
+                                         C.byref(lv), C.byref(pr))
+            assert proof.cpu().numpy().tobytes() == bytes(outp)
+            ofb = O.FlatBlock(fb.payloads, fb.offs, atts, fb.header, fb.revs, fb.rev_index)
+            assert fc.cpu().numpy().tobytes() == O.oracle_build_fc(ofb, bytes(outp))
+    finally:
+        zp.close()
