@@ -73,6 +73,8 @@ _SIGS = {
     "acegpu_bn_scalar_muls": (C.c_int, [ctxp, C.c_int, vp, vp, u64, vp]),
     "acegpu_bn_msm_params": (C.c_int, [ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "acegpu_bn_msm_prepare": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, C.POINTER(C.c_void_p)]),
+    "acegpu_bn_msm_prepare_vb": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, u64,
+                                           C.POINTER(C.c_void_p)]),
     "acegpu_bn_msm_free": (None, [C.c_void_p]),
     "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),
     "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),

@@ -114,12 +114,15 @@ struct acegpu_ctx {
     cudaEvent_t cred_in = nullptr, cred_out = nullptr;
 };
 
-// A prepared fixed-base MSM (proving-key bases with their 16 window shifts).
+// A prepared MSM: fixed base (proving-key bases with their window shifts)
+// or variable base (the bases alone; vb_sub = sub-range size, 0 = default).
 struct acegpu_msm_bases {
     int device = 0;
     int group = 1;
     uint64_t n = 0;
-    uint8_t* table = nullptr;  // kMsmWindows * n affine points, Montgomery form
+    uint8_t* table = nullptr;  // kMsmWindows * n (vb: n) affine points, Montgomery form
+    int vb = 0;
+    uint64_t vb_sub = 0;
 };
 
 namespace {
@@ -1669,7 +1672,7 @@ extern "C" int acegpu_bn_convert_dev(acegpu_ctx* c, void* stream, int field, uin
 
 extern "C" int acegpu_bn_ntt_dev(acegpu_ctx* c, void* stream, const uint8_t* d_in, uint8_t* d_out,
                                  uint32_t logn, int inverse, int coset) {
-    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^22");
+    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^28");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     cudaStream_t s = pick(c, stream);
@@ -1678,13 +1681,13 @@ extern "C" int acegpu_bn_ntt_dev(acegpu_ctx* c, void* stream, const uint8_t* d_i
     if ((int)logn > bn::kNttSingleMax) RET(ws(c, kBnScratch, 32ull << logn, &scratch));
     if (bn::ntt_run(c->ntt[logn], d_in, d_out, scratch, inverse, coset, 1, s))
         return fail(ACEGPU_ECUDA, std::string("NTT launch: ") + cudaGetErrorString(cudaGetLastError()));
-    c->launches += (int)logn > bn::kNttSingleMax ? 2 : 1;
+    c->launches += (int)logn > bn::kNttTwoPassMax ? 3 : (int)logn > bn::kNttSingleMax ? 2 : 1;
     return ACEGPU_OK;
 }
 
 extern "C" int acegpu_bn_ntt(acegpu_ctx* c, uint8_t* data, uint32_t logn, int inverse,
                              int coset) {
-    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^22");
+    if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^28");
     const uint64_t n = 1ull << logn;
     uint8_t* d;
     {
@@ -1735,10 +1738,9 @@ extern "C" int acegpu_bn_msm_params(acegpu_ctx* c, int* window_bits, int* window
     return ACEGPU_OK;
 }
 
-extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* points,
-                                     uint64_t n, int on_device, acegpu_msm_bases** out) {
-    if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
-    if (n == 0 || n > (1ull << 27)) return fail(ACEGPU_EINVAL, "MSM size must be 1..2^27");
+namespace {
+int msm_prepare_impl(acegpu_ctx* c, int group, const uint8_t* points, uint64_t n, int on_device,
+                     int vb, uint64_t sub, acegpu_msm_bases** out) {
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     cudaStream_t s = c->stream;
@@ -1749,6 +1751,22 @@ extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* po
     b->device = c->device;
     b->group = group;
     b->n = n;
+    b->vb = vb;
+    b->vb_sub = sub;
+    const auto kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    if (vb) {
+        // variable base: the bases themselves, converted in place
+        cudaError_t e = cudaMalloc(&b->table, pb * n);
+        if (e != cudaSuccess)
+            return fail(ACEGPU_ECUDA, std::string("msm_prepare alloc: ") + cudaGetErrorString(e));
+        CK(cudaMemcpyAsync(b->table, points, pb * n, kind, s));
+        bn::launch_points_convert(group, b->table, n, 1, s);
+        CKL();
+        CK(cudaStreamSynchronize(s));
+        c->launches += 1;
+        *out = b.release();
+        return ACEGPU_OK;
+    }
     std::unique_ptr<uint8_t, cudaError_t (*)(void*)> tmp(nullptr, cudaFree);
     cudaError_t e = cudaMalloc(&b->table, pb * n * bn::kMsmWindows);
     uint8_t* t = nullptr;
@@ -1756,13 +1774,32 @@ extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* po
     tmp.reset(t);
     if (e != cudaSuccess)
         return fail(ACEGPU_ECUDA, std::string("msm_prepare alloc: ") + cudaGetErrorString(e));
-    CK(cudaMemcpyAsync(t, points, pb * n, on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(t, points, pb * n, kind, s));
     bn::launch_points_convert(group, t, n, 1, s);
     if (bn::msm_prepare(group, t, n, b->table, s)) return fail(ACEGPU_ECUDA, "msm_prepare launch");
     CK(cudaStreamSynchronize(s));
     c->launches += 2;
     *out = b.release();
     return ACEGPU_OK;
+}
+}  // namespace
+
+extern "C" int acegpu_bn_msm_prepare(acegpu_ctx* c, int group, const uint8_t* points,
+                                     uint64_t n, int on_device, acegpu_msm_bases** out) {
+    if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
+    if (n == 0 || n > (1ull << 27)) return fail(ACEGPU_EINVAL, "MSM size must be 1..2^27");
+    if (!points || !out) return fail(ACEGPU_EINVAL, "null argument");
+    return msm_prepare_impl(c, group, points, n, on_device, 0, 0, out);
+}
+
+extern "C" int acegpu_bn_msm_prepare_vb(acegpu_ctx* c, int group, const uint8_t* points,
+                                        uint64_t n, int on_device, uint64_t sub,
+                                        acegpu_msm_bases** out) {
+    if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
+    if (n == 0 || n > (1ull << 31)) return fail(ACEGPU_EINVAL, "MSM size must be 1..2^31");
+    if (sub > bn::kMsmVbSubMax) return fail(ACEGPU_EINVAL, "MSM sub-range above 2^24");
+    if (!points || !out) return fail(ACEGPU_EINVAL, "null argument");
+    return msm_prepare_impl(c, group, points, n, on_device, 1, sub, out);
 }
 
 extern "C" void acegpu_bn_msm_free(acegpu_msm_bases* b) {
@@ -1777,7 +1814,8 @@ extern "C" int acegpu_bn_msm_run_dev(acegpu_ctx* c, void* stream, const acegpu_m
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard g(c->device);
     cudaStream_t s = pick(c, stream);
-    if (bn::msm_run(b->group, b->table, b->n, d_scalars, c->msm, d_out, s))
+    if (b->vb ? bn::msm_run_vb(b->group, b->table, b->n, d_scalars, c->msm, d_out, s, b->vb_sub)
+              : bn::msm_run(b->group, b->table, b->n, d_scalars, c->msm, d_out, s))
         return fail(ACEGPU_ECUDA, std::string("msm_run: ") + cudaGetErrorString(cudaGetLastError()));
     c->launches += bn::kMsmKernels;
     return ACEGPU_OK;
@@ -1906,6 +1944,9 @@ struct acegpu_g16 {
     bn::MsmScratch msm_bl, msm_h, msm_ab;  // one per MSM stream (no cross-stream scratch)
     const acegpu_r1cs* r1cs = nullptr;  // general circuit (setup_r1cs), else the synthetic chain
     uint8_t* zsc = nullptr;             // general path: r, s digest scratch
+    // variable-base key (domain above 2^22, e.g. one proof for a whole block):
+    // bases without window tables, one buffer slot (proofs serialise)
+    bool vb = false;
 };
 
 namespace {
@@ -1973,11 +2014,13 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     for (uint8_t* p : {g->consts, g->cc, g->vk_alpha1, g->vk_g2_std, g->vk_ic, g->vk_digest,
                        g->zsc})
         if (p) cudaFree(p);
-    for (auto& sl : g->slot) {
+    for (int k = 0; k < 2; ++k) {
+        auto& sl = g->slot[k];
+        if (sl.done) cudaEventDestroy(sl.done);
+        if (k == 1 && sl.z && sl.z == g->slot[0].z) continue;  // vb: slot 1 aliases slot 0
         for (uint8_t* p : {sl.z, sl.zb, sl.zl, sl.ea, sl.eb, sl.ec, sl.pts, sl.scaled, sl.rs,
                            sl.digest, sl.dsc})
             if (p) cudaFree(p);
-        if (sl.done) cudaEventDestroy(sl.done);
     }
     if (g->s_w) cudaStreamDestroy(g->s_w);
     if (g->ev_in) cudaEventDestroy(g->ev_in);
@@ -2017,8 +2060,12 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     g->d.V = r ? r->vars : 1 + uint64_t(T) + uint64_t(T) * (K + 1);
     g->d.m = r ? r->rows : uint64_t(T) * K + T + 1;
     while ((1ull << g->logn) < g->d.m) ++g->logn;
-    if (g->logn > uint32_t(bn::kNttMaxLog)) return fail(ACEGPU_EINVAL, "g16: domain above 2^22");
+    if (g->logn > uint32_t(bn::kNttMaxLog)) return fail(ACEGPU_EINVAL, "g16: domain above 2^28");
     g->N = 1ull << g->logn;
+    {
+        const char* e = std::getenv("ACEGPU_G16_VB");  // 1: force variable-base (tests)
+        g->vb = g->logn > uint32_t(bn::kNttTwoPassMax) || (e && e[0] == '1');
+    }
     g->Vp = g->d.V - 1 - T;
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     auto dm = [&](uint8_t** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 16); };
@@ -2026,13 +2073,20 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
         return fail(ACEGPU_ECUDA, "g16 alloc");
     if (r && dm(&g->zsc, bn::g16_long_digest_scratch_bytes(std::max<uint64_t>(g->d.V, T)) + 64))
         return fail(ACEGPU_ECUDA, "g16 alloc");
-    for (auto& sl : g->slot) {
+    for (int k = 0; k < 2; ++k) {
+        auto& sl = g->slot[k];
+        CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
+        if (k == 1 && g->vb) {  // one slot: proofs serialise on slot 0
+            cudaEvent_t ev = sl.done;
+            sl = g->slot[0];
+            sl.done = ev;
+            break;
+        }
         if (dm(&sl.z, 32 * (V + 2)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
             dm(&sl.ea, 32 * N) || dm(&sl.eb, 32 * N) || dm(&sl.ec, 32 * N) || dm(&sl.pts, 512) ||
             dm(&sl.scaled, 256) || dm(&sl.rs, 64) || dm(&sl.digest, 32) ||
             dm(&sl.dsc, bn::g16_digest_scratch_bytes(T, 1) + 32))
             return fail(ACEGPU_ECUDA, "g16 alloc");
-        CK(cudaEventCreateWithFlags(&sl.done, cudaEventDisableTiming));
     }
     CK(cudaStreamCreateWithFlags(&g->s_w, cudaStreamNonBlocking));
     CK(cudaEventCreateWithFlags(&g->ev_in, cudaEventDisableTiming));
@@ -2068,9 +2122,17 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     if (K) bn::g16_chain_consts(K, g->cc, s);
     // query scalars
     uint8_t *L, *su, *sv, *sl, *part, *hs, *gens, *ext, *pts, *icsc;
+    // pts: the bases before their window tables (fixed base), the u, v, w
+    // column sums (general R1CS) and the verifying-key export
+    uint64_t pts_bytes = 448 + 64 * (uint64_t(T) + 1);
+    if (r) pts_bytes = std::max<uint64_t>(pts_bytes, 96 * V);
+    pts_bytes = std::max<uint64_t>(pts_bytes, 32 * bn::kCombEntries);
+    if (!g->vb) pts_bytes = std::max<uint64_t>(pts_bytes, 128 * (std::max(V, N) + 2));
+    uint8_t *tab1, *tab2;
     if (dm(&L, 32 * m) || dm(&su, 32 * V) || dm(&sv, 32 * V) || dm(&sl, 32 * g->Vp) ||
         dm(&part, 256 * 64) || dm(&hs, 32 * N) || dm(&gens, 256) || dm(&ext, 512) ||
-        dm(&pts, 128 * (std::max(V, N) + 2)) || dm(&icsc, 32ull * (T + 1)))
+        dm(&pts, pts_bytes) || dm(&icsc, 32ull * (T + 1)) ||
+        dm(&tab1, 64 * bn::kCombEntries) || dm(&tab2, 128 * bn::kCombEntries))
         return fail(ACEGPU_ECUDA, "g16 setup alloc");
     bn::g16_lagrange(g->consts, m, L, s);
     if (r) {
@@ -2103,31 +2165,49 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     if (dm(&ex2, 256)) return fail(ACEGPU_ECUDA, "g16 setup alloc");
     bn::launch_scalar_muls(2, gens + 64, ext + 256 + 32, 2, ex2, s);  // beta2, delta2
     CKL();
-    // A: [u]1 | alpha1 | delta1
-    bn::launch_scalar_muls(1, gens, su, V, pts, s);
-    CK(cudaMemcpyAsync(pts + 64 * V, ex1, 64, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(pts + 64 * (V + 1), ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
-    RET(bases_from_device(c->device, 1, pts, V + 2, s, &g->qa));
-    // B1: [v]1 | beta1 | delta1
-    bn::launch_scalar_muls(1, gens, sv, V, pts, s);
-    CK(cudaMemcpyAsync(pts + 64 * V, ex1 + 64, 64, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(pts + 64 * (V + 1), ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
-    RET(bases_from_device(c->device, 1, pts, V + 2, s, &g->qb1));
-    // B2: [v]2 | beta2 | delta2
-    bn::launch_scalar_muls(2, gens + 64, sv, V, pts, s);
-    CK(cudaMemcpyAsync(pts + 128 * V, ex2, 256, cudaMemcpyDeviceToDevice, s));
-    RET(bases_from_device(c->device, 2, pts, V + 2, s, &g->qb2));
-    // L: [l]1 (private) | delta1
-    bn::launch_scalar_muls(1, gens, sl, g->Vp, pts, s);
-    CK(cudaMemcpyAsync(pts + 64 * g->Vp, ex1 + 128, 64, cudaMemcpyDeviceToDevice, s));
-    RET(bases_from_device(c->device, 1, pts, g->Vp + 1, s, &g->ql));
+    // bases = scalars x generator by the fixed-base comb (pts as the comb's
+    // scalar scratch first), then the extra points appended
+    bn::launch_comb_table(1, gens, pts, tab1, s);
+    bn::launch_comb_table(2, gens + 64, pts, tab2, s);
+    CKL();
+    auto bases = [&](int group, const uint8_t* scal, uint64_t cnt,
+                     std::initializer_list<const uint8_t*> extra, acegpu_msm_bases** out) -> int {
+        const uint64_t pb = 64ull * group, total = cnt + extra.size();
+        uint8_t* dst = pts;
+        std::unique_ptr<acegpu_msm_bases, void (*)(acegpu_msm_bases*)> b(nullptr,
+                                                                          acegpu_bn_msm_free);
+        if (g->vb) {  // the bases are the MSM table
+            b.reset(new acegpu_msm_bases());
+            b->device = c->device;
+            b->group = group;
+            b->n = total;
+            b->vb = 1;
+            const cudaError_t e = cudaMalloc(&b->table, pb * total);
+            if (e != cudaSuccess)
+                return fail(ACEGPU_ECUDA, std::string("g16 bases alloc: ") + cudaGetErrorString(e));
+            dst = b->table;
+        }
+        bn::launch_comb_muls(group, group == 1 ? tab1 : tab2, scal, cnt, dst, s);
+        uint64_t k = cnt;
+        for (const uint8_t* x : extra)
+            CK(cudaMemcpyAsync(dst + pb * k++, x, pb, cudaMemcpyDeviceToDevice, s));
+        CKL();
+        if (g->vb) {
+            *out = b.release();
+            return ACEGPU_OK;
+        }
+        return bases_from_device(c->device, group, pts, total, s, out);
+    };
+    RET(bases(1, su, V, {ex1, ex1 + 128}, &g->qa));        // A: [u]1 | alpha1 | delta1
+    RET(bases(1, sv, V, {ex1 + 64, ex1 + 128}, &g->qb1));  // B1: [v]1 | beta1 | delta1
+    RET(bases(2, sv, V, {ex2, ex2 + 128}, &g->qb2));       // B2: [v]2 | beta2 | delta2
+    RET(bases(1, sl, g->Vp, {ex1 + 128}, &g->ql));         // L: [l]1 (private) | delta1
     // H: [L^g_j(tau) Z(tau)/delta]1, j < N (coset-Lagrange basis, N points)
-    bn::launch_scalar_muls(1, gens, hs, N, pts, s);
-    RET(bases_from_device(c->device, 1, pts, N, s, &g->qh));
+    RET(bases(1, hs, N, {}, &g->qh));
     // verifying key (the Groth16 verifier, g16_verify.cu)
     if (dm(&g->vk_alpha1, 64) || dm(&g->vk_g2_std, 384) || dm(&g->vk_ic, 64ull * (T + 1)))
         return fail(ACEGPU_ECUDA, "g16 vk alloc");
-    bn::launch_scalar_muls(1, gens, icsc, T + 1, g->vk_ic, s);
+    bn::launch_comb_muls(1, tab1, icsc, T + 1, g->vk_ic, s);
     RET(bases_from_device(c->device, 1, g->vk_ic, T + 1, s, &g->qic));
     CK(cudaMemcpyAsync(g->vk_alpha1, ex1, 64, cudaMemcpyDeviceToDevice, s));
     CK(cudaMemcpyAsync(ext + 256, trapdoor5 + 96, 32, cudaMemcpyHostToDevice, s));  // gamma
@@ -2142,7 +2222,7 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     bn::g16_vk_digest(pts, uint32_t(448 + 64 * (T + 1)), g->vk_digest, s);
     CKL();
     CK(cudaStreamSynchronize(s));
-    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2, icsc}) cudaFree(p);
+    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2, icsc, tab1, tab2}) cudaFree(p);
     if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s)) return fail(ACEGPU_ECUDA, "g16 NTT tables");
     CK(cudaStreamSynchronize(s));
     c->launches += 20;
@@ -2474,7 +2554,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     uint8_t* scratch;
     RET(ws(c, kBnScratch, 32 * N, &scratch));
     // next buffer slot; its previous proof must be assembled before reuse
-    g->cur ^= 1;
+    g->cur = g->vb ? 0 : g->cur ^ 1;
     acegpu_g16::Slot& sl = g->slot[g->cur];
     g->z = sl.z, g->zb = sl.zb, g->zl = sl.zl, g->ea = sl.ea, g->eb = sl.eb, g->ec = sl.ec;
     g->pts = sl.pts, g->scaled = sl.scaled, g->rs = sl.rs, g->digest = sl.digest;
@@ -2532,24 +2612,29 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CKL();
     CK(cudaEventRecord(g->ev_n, sn));
     CK(cudaStreamWaitEvent(sh, g->ev_n, 0));
-    if (bn::msm_run(1, g->qh->table, N, g->ea, g->msm_h, g->pts + 320, sh))
+    auto msm = [](const acegpu_msm_bases* b, uint64_t n, const uint8_t* sc, bn::MsmScratch& scr,
+                  uint8_t* out, cudaStream_t st) {
+        return b->vb ? bn::msm_run_vb(b->group, b->table, n, sc, scr, out, st, b->vb_sub)
+                     : bn::msm_run(b->group, b->table, n, sc, scr, out, st);
+    };
+    if (msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
     // s_bl: [v]2 (B2) and [l] (L)
     CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
-    if (bn::msm_run(2, g->qb2->table, V + 2, g->zb, g->msm_bl, g->pts + 128, g->s_bl) ||
+    if (msm(g->qb2, V + 2, g->zb, g->msm_bl, g->pts + 128, g->s_bl) ||
         (tr.mark("msm_b2", g->s_bl), false) ||
-        bn::msm_run(1, g->ql->table, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
+        msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
         return fail(ACEGPU_ECUDA, "g16 msm B2/L");
     CK(cudaEventRecord(g->ev_bl, g->s_bl));
     tr.mark("msm_l", g->s_bl);
     // s_ab: A and B1, then s*A and r*B1 (one serial scalar multiplication
     // each) on the side stream while the others finish
     CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
-    if (bn::msm_run(1, g->qa->table, V + 2, g->z, g->msm_ab, g->pts, g->s_ab) ||
+    if (msm(g->qa, V + 2, g->z, g->msm_ab, g->pts, g->s_ab) ||
         (tr.mark("msm_a", g->s_ab), false) ||
-        bn::msm_run(1, g->qb1->table, V + 2, g->zb, g->msm_ab, g->pts + 64, g->s_ab))
+        msm(g->qb1, V + 2, g->zb, g->msm_ab, g->pts + 64, g->s_ab))
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
@@ -2589,7 +2674,10 @@ int g16_chunk_inputs(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                      const uint8_t* d_revs, const uint32_t* d_rev_index, uint8_t* d_codes,
                      uint8_t* d_merkle32, uint8_t** pub_out, TreeResult* t) {
     const uint32_t T = g->d.T;
-    if (T & (T - 1)) return fail(ACEGPU_EINVAL, "g16: txs per chunk must be a power of two");
+    // chunk roots must be Merkle-tree nodes: T a power of two, unless one
+    // chunk holds the whole block (a block-size key: one proof per block)
+    if ((T & (T - 1)) && n_total > T)
+        return fail(ACEGPU_EINVAL, "g16: txs per chunk must be a power of two (or >= the block)");
     if (n == 0) return fail(ACEGPU_EINVAL, "g16: empty block or shard");
     RET(check_n(n));
     uint32_t log2_chunk = 0;

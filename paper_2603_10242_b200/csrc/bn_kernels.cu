@@ -30,10 +30,10 @@ __global__ void field_batch_kernel(int op, const uint8_t* a, const uint8_t* b, u
     store<C>(out + 32 * i, from_mont(r));
 }
 
-__device__ __forceinline__ Fq finv1(const Fq& a) { return inv(a); }
+__device__ __forceinline__ Fq finv1(const Fq& a) { return inv_fast(a); }
 __device__ __forceinline__ Fq2 finv1(const Fq2& a) {
     Fq n = add(mul(a.c0, a.c0), mul(a.c1, a.c1));
-    Fq ni = inv(n);
+    Fq ni = inv_fast(n);
     return {mul(a.c0, ni), neg(mul(a.c1, ni))};
 }
 
@@ -66,6 +66,49 @@ __global__ void scalar_muls_kernel(const uint8_t* base, const uint8_t* scalars, 
     F t = finv1(fmul(acc.ZZ, acc.ZZZ));
     fstore(o, fmul(acc.X, fmul(t, acc.ZZZ)));
     fstore(o + E, fmul(acc.Y, fmul(t, acc.ZZ)));
+}
+
+// comb scalars: entry k*256 + j = j * 2^(8k) (32-B LE; < 2^256)
+__global__ void comb_scalars_kernel(uint8_t* sc) {
+    const uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= kCombEntries) return;
+    const uint32_t k = e >> 8, j = e & 255;
+    for (int b = 0; b < 32; ++b) sc[32ull * e + b] = b == (int)k ? (uint8_t)j : 0;
+}
+
+template <class F>
+__global__ void comb_muls_kernel(const uint8_t* tab, const uint8_t* scalars, uint64_t n,
+                                 uint8_t* out) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    constexpr int E = felem_bytes<F>();
+    const uint4* q = reinterpret_cast<const uint4*>(scalars + 32 * i);
+    const uint4 lo = q[0], hi = q[1];
+    const uint32_t s[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+    XYZZ<F> acc = XYZZ<F>::inf();
+#pragma unroll 1
+    for (int k = 0; k < 32; ++k) {
+        const uint32_t j = (s[k >> 2] >> (8 * (k & 3))) & 255u;
+        if (!j) continue;
+        const uint8_t* p = tab + 2ull * E * (256u * k + j);
+        F x, y;
+        fload(x, p);
+        fload(y, p + E);
+        if (fzero(x) && fzero(y)) continue;  // infinity entry
+        acc = xyzz_madd(acc, x, y);
+    }
+    uint8_t* o = out + 2 * E * i;
+    F x, y;
+    if (acc.is_inf()) {
+        fset_zero(x);
+        fset_zero(y);
+    } else {
+        const F t = finv1(fmul(acc.ZZ, acc.ZZZ));
+        x = fmul(acc.X, fmul(t, acc.ZZZ));
+        y = fmul(acc.Y, fmul(t, acc.ZZ));
+    }
+    fstore(o, x);
+    fstore(o + E, y);
 }
 
 // IMAD pipe: 8 independent mad.lo chains per thread.
@@ -123,6 +166,20 @@ void launch_scalar_muls(int group, const uint8_t* base, const uint8_t* scalars, 
     const unsigned g = (unsigned)((n + 63) / 64);
     if (group == 2) scalar_muls_kernel<Fq2><<<g, 64, 0, s>>>(base, scalars, n, out);
     else scalar_muls_kernel<Fq><<<g, 64, 0, s>>>(base, scalars, n, out);
+}
+
+void launch_comb_table(int group, const uint8_t* base, uint8_t* scalar_scratch, uint8_t* tab,
+                       cudaStream_t s) {
+    comb_scalars_kernel<<<kCombEntries / 256, 256, 0, s>>>(scalar_scratch);
+    launch_scalar_muls(group, base, scalar_scratch, kCombEntries, tab, s);
+}
+
+void launch_comb_muls(int group, const uint8_t* tab, const uint8_t* scalars, uint64_t n,
+                      uint8_t* out, cudaStream_t s) {
+    if (!n) return;
+    const unsigned g = (unsigned)((n + 127) / 128);
+    if (group == 2) comb_muls_kernel<Fq2><<<g, 128, 0, s>>>(tab, scalars, n, out);
+    else comb_muls_kernel<Fq><<<g, 128, 0, s>>>(tab, scalars, n, out);
 }
 
 void launch_imad_peak(uint32_t* sink, uint32_t iters, int blocks, int threads, cudaStream_t s) {

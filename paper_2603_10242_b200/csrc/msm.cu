@@ -163,7 +163,9 @@ __device__ __forceinline__ void digits(const uint8_t* s, int32_t d[kMsmWindows])
 #define ACEGPU_SORT_AGG 1
 #endif
 #if !ACEGPU_SORT_AGG
+template <bool VB>
 __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
+    static_assert(!VB, "variable-base MSM needs ACEGPU_SORT_AGG");
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int32_t d[kMsmWindows];
@@ -172,6 +174,7 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
     for (int w = 0; w < kMsmWindows; ++w)
         if (d[w]) atomicAdd(&hist[abs(d[w]) - 1], 1u);
 }
+template <bool VB>
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
                                uint32_t* sorted) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -186,6 +189,14 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
     }
 }
 #else
+// VB (variable base, no window tables): bucket key w * kMsmBuckets + |d| - 1
+// (one bucket set per window) and entry = the point index; fixed base: key
+// |d| - 1 and entry = the table row w n + i.
+template <bool VB>
+__device__ __forceinline__ uint32_t bucket_key(int w, int32_t d) {
+    return VB ? (uint32_t)(w * kMsmBuckets + abs(d) - 1) : (uint32_t)(abs(d) - 1);
+}
+template <bool VB>
 __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     int32_t d[kMsmWindows];
@@ -193,12 +204,13 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int w = 0; w < kMsmWindows; ++w) {
-        const uint32_t key = (i < n && d[w]) ? (uint32_t)(abs(d[w]) - 1) : 0xFFFFFFFFu;
+        const uint32_t key = (i < n && d[w]) ? bucket_key<VB>(w, d[w]) : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, key);
         if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
     }
 }
 
+template <bool VB>
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
                                uint32_t* sorted) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -208,7 +220,7 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
     const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
     for (int w = 0; w < kMsmWindows; ++w) {
-        const uint32_t key = (i < n && d[w]) ? (uint32_t)(abs(d[w]) - 1) : 0xFFFFFFFFu;
+        const uint32_t key = (i < n && d[w]) ? bucket_key<VB>(w, d[w]) : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, key);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
@@ -216,14 +228,15 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
         base = __shfl_sync(0xffffffffu, base, leader);
         if (key != 0xFFFFFFFFu)
             sorted[base + __popc(peers & below)] =
-                (uint32_t)(w * n + i) | (d[w] < 0 ? 0x80000000u : 0u);
+                (uint32_t)(VB ? i : w * n + i) | (d[w] < 0 ? 0x80000000u : 0u);
     }
 }
 #endif
 
-// The non-empty bucket b with offs[b] <= pos < offs[b + 1].
+// The non-empty bucket b with offs[b] <= pos < offs[b + 1] (NB buckets).
+template <int NB = kMsmBuckets>
 __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
-    int lo = 0, hi = kMsmBuckets;
+    int lo = 0, hi = NB;
     while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
         if (offs[mid] <= pos) lo = mid;
@@ -241,19 +254,19 @@ __device__ __forceinline__ void store_inf(uint8_t* p) {
 // bucket: a run that is the whole bucket is stored to buckets[b]; a run cut
 // by the segment edge is stored to partials[2 seg] (first run of the
 // segment) or partials[2 seg + 1] (a later run).
-template <class F>
+template <class F, int NB>
 __global__ void __launch_bounds__(128, Lay<F>::ACC_MIN_CTAS) accumulate_kernel(const uint8_t* table,
                                                          const uint32_t* sorted,
                                                          const uint32_t* offs,
                                                          uint8_t* buckets,
                                                          uint8_t* partials, uint32_t segsz) {
     const uint32_t seg = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t total = offs[kMsmBuckets];
+    const uint32_t total = offs[NB];
     const uint32_t p0 = seg * segsz;
     if (p0 >= total) return;
     constexpr int A = Lay<F>::AFF, X = Lay<F>::XZ;
     const uint32_t p1 = min(total, p0 + segsz);
-    int b = bucket_of(offs, p0);
+    int b = bucket_of<NB>(offs, p0);
     uint32_t bs = offs[b], be = offs[b + 1];
     int slot = 0;
     XYZZ<F> acc = XYZZ<F>::inf();
@@ -333,12 +346,12 @@ constexpr uint32_t kHeavySpan = 64;  // segments; longer buckets go to heavy_ker
 // s0 < s1 sums its run partials (slot 0 or 1 in s0, slot 0 after). Buckets
 // spanning more than kHeavySpan segments (skewed digits, e.g. a witness of
 // 0/1 values) are queued for heavy_kernel instead of one serial thread.
-template <class F>
+template <class F, int NB>
 __global__ void __launch_bounds__(128) fixup_kernel(const uint32_t* offs, const uint8_t* partials,
                                                     uint8_t* buckets, uint32_t* heavy,
                                                     uint32_t segsz) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= kMsmBuckets) return;
+    if (b >= NB) return;
     constexpr int X = Lay<F>::XZ;
     const uint32_t s = offs[b], e = offs[b + 1];
     if (s == e) {
@@ -429,10 +442,13 @@ constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // <= 8192 -> <= 64 CTA part
 // sum = tot + a*run with running sums from the top; one partial per CTA.
 // (A work-efficient multi-level recursion on the run_j measured 2.7x slower
 // here: every level pays a serial chain of point additions.)
+// (blockIdx.y: the window's bucket set in a variable-base run)
 template <class F>
 __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets, uint8_t* segsum) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int X = Lay<F>::XZ;
+    buckets += (uint64_t)X * kMsmBuckets * blockIdx.y;
+    segsum += (uint64_t)X * gridDim.x * blockIdx.y;
     XYZZ<F> tot = XYZZ<F>::inf();
     if (j < kRedThreads) {
         const int a = j * kRedSeg;
@@ -449,10 +465,13 @@ __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets,
 
 // Sum the per-CTA partials of reduce_seg (kRedThreads / 128 <= 64) and
 // write the affine result.
+// (blockIdx.x: the window in a variable-base run -> out[window])
 template <class F>
 __global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum, uint8_t* out) {
     constexpr int X = Lay<F>::XZ;
     constexpr int kParts = kRedThreads / 128;
+    segsum += (uint64_t)X * kParts * blockIdx.x;
+    out += (uint64_t)Lay<F>::AFF * blockIdx.x;
     __shared__ __align__(16) uint8_t sm[2 * sizeof(XYZZ<F>)];
     XYZZ<F> acc = threadIdx.x < kParts ? load_xyzz<F>(segsum + (uint64_t)X * threadIdx.x)
                                        : XYZZ<F>::inf();
@@ -664,6 +683,26 @@ __global__ void __launch_bounds__(128) affine_heavy_kernel(const uint8_t* pts, c
     }
 }
 
+// Variable-base result: win[r * W + w] = the window-w sum of sub-range r
+// (affine); out = sum_w 2^(c w) sum_r win[r W + w] (Horner from the top).
+template <class F>
+__global__ void combine_windows_kernel(const uint8_t* win, uint32_t nsub, uint8_t* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    constexpr int A = Lay<F>::AFF;
+    XYZZ<F> acc = XYZZ<F>::inf();
+    for (int w = kMsmWindows - 1; w >= 0; --w) {
+        for (int d = 0; d < kMsmC; ++d) acc = xyzz_dbl(acc);
+        for (uint32_t r = 0; r < nsub; ++r) {
+            F x, y;
+            if (load_affine<F>(win + (uint64_t)A * (r * kMsmWindows + w), x, y))
+                acc = xyzz_madd<F>(acc, x, y);
+        }
+    }
+    F x, y;
+    to_affine(acc, x, y);
+    store_affine(out, x, y);
+}
+
 __global__ void points_convert_kernel(uint8_t* pts, uint64_t n_elems, int to) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     if (i >= n_elems) return;
@@ -677,48 +716,61 @@ int prepare_t(const uint8_t* bases, uint64_t n, uint8_t* table, cudaStream_t s) 
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
-template <class F>
-int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc, uint8_t* out,
-          cudaStream_t s) {
+// One Pippenger pass. Fixed base (VB = false): table = the window tables,
+// out = the affine result. Variable base (VB = true): table = the n bases
+// themselves, one bucket set per window, out = the kMsmWindows affine window
+// sums (combine_windows_kernel weights them).
+template <class F, bool VB>
+int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
+             uint8_t* out, cudaStream_t s) {
     constexpr int X = Lay<F>::XZ;
+    constexpr int NB = VB ? kMsmWindows * kMsmBuckets : kMsmBuckets;
     const uint64_t cap = (uint64_t)kMsmWindows * n;
     // segment length: kMsmSeg, shorter for small MSMs (>= ~19k threads, so a
     // verifier-size MSM is not a few hundred threads of 64 serial adds)
     uint32_t segsz = kMsmSeg;
     while (segsz > 4 && cap / segsz < 148ull * 128) segsz >>= 1;
     const uint64_t nseg = (cap + segsz - 1) / segsz;
-    if (sc.cap_entries < cap || sc.cap_segs < nseg || !sc.hist) {
+    if (sc.cap_entries < cap || sc.cap_segs < nseg || sc.cap_buckets < (uint64_t)NB || !sc.hist) {
         const uint64_t keep = std::max<uint64_t>(cap, sc.cap_entries);
         const uint64_t keep_segs = std::max<uint64_t>(nseg, sc.cap_segs);
+        const uint64_t nbk = std::max<uint64_t>(NB, sc.cap_buckets);
+        uint8_t* win = sc.win;  // the variable-base window sums survive the regrow
+        const uint64_t win_cap = sc.win_cap;
+        sc.win = nullptr;
         sc.release();
-        if (cudaMalloc(&sc.hist, 4 * (kMsmBuckets + 1)) || cudaMalloc(&sc.offs, 4 * (kMsmBuckets + 1)) ||
-            cudaMalloc(&sc.cursor, 4 * kMsmBuckets) || cudaMalloc(&sc.sorted, 4 * keep) ||
+        sc.win = win;
+        sc.win_cap = win_cap;
+        if (cudaMalloc(&sc.hist, 4 * (nbk + 1)) || cudaMalloc(&sc.offs, 4 * (nbk + 1)) ||
+            cudaMalloc(&sc.cursor, 4 * nbk) || cudaMalloc(&sc.sorted, 4 * keep) ||
             cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||
-            cudaMalloc(&sc.buckets, (size_t)256 * kMsmBuckets) ||
-            cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128)) ||
-            cudaMalloc(&sc.heavy, 4 * (kMsmBuckets + 1)) ||
+            cudaMalloc(&sc.buckets, (size_t)256 * nbk) ||
+            cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128) * (nbk / kMsmBuckets)) ||
+            cudaMalloc(&sc.heavy, 4 * (nbk + 1)) ||
             // slices: <= nseg / kHeavySlice + one partial slice per heavy bucket
             // (each spans > kHeavySpan segments)
             cudaMalloc(&sc.heavy_part,
                        (size_t)256 * (keep_segs / kHeavySlice + keep_segs / kHeavySpan + 16)))
             return -1;
-        cub::DeviceScan::ExclusiveSum(nullptr, sc.scan_bytes, sc.hist, sc.offs, kMsmBuckets + 1, s);
+        cub::DeviceScan::ExclusiveSum(nullptr, sc.scan_bytes, sc.hist, sc.offs, (int)nbk + 1, s);
         if (cudaMalloc(&sc.scan_tmp, sc.scan_bytes)) return -1;
         sc.cap_entries = keep;
         sc.cap_segs = keep_segs;
+        sc.cap_buckets = nbk;
     }
-    cudaMemsetAsync(sc.hist, 0, 4 * (kMsmBuckets + 1), s);
+    cudaMemsetAsync(sc.hist, 0, 4 * (NB + 1), s);
     cudaMemsetAsync(sc.heavy, 0, 4, s);
     const unsigned gb = (unsigned)((n + 255) / 256);
-    count_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.hist);
+    count_kernel<VB><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
     // offs = exclusive scan of hist[0..NB] (hist[NB] = 0 -> offs[NB] = total)
-    if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, sc.scan_bytes, sc.hist, sc.offs,
-                                      kMsmBuckets + 1, s) != cudaSuccess)
+    size_t scan_bytes = sc.scan_bytes;
+    if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, scan_bytes, sc.hist, sc.offs, NB + 1, s) !=
+        cudaSuccess)
         return -1;
-    cudaMemcpyAsync(sc.cursor, sc.offs, 4 * kMsmBuckets, cudaMemcpyDeviceToDevice, s);
-    scatter_kernel<<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
+    cudaMemcpyAsync(sc.cursor, sc.offs, 4 * NB, cudaMemcpyDeviceToDevice, s);
+    scatter_kernel<VB><<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
     bool affine = false;
-    if constexpr (sizeof(F) == sizeof(Fq)) affine = ACEGPU_MSM_AFFINE && affine_enabled();
+    if constexpr (sizeof(F) == sizeof(Fq) && !VB) affine = ACEGPU_MSM_AFFINE && affine_enabled();
     if (affine) {
         // levels until ~1 point per bucket remains for uniform digits (the
         // finish kernel sums what is left); output-slot upper bounds size the
@@ -764,19 +816,52 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
                                                                sc.heavy);
         affine_heavy_kernel<<<148, 128, 0, s>>>(in_pts, in_offs, sc.buckets, sc.heavy);
     } else {
-        accumulate_kernel<F><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
+        accumulate_kernel<F, NB><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
             table, sc.sorted, sc.offs, sc.buckets, sc.partials, segsz);
-        fixup_kernel<F><<<kMsmBuckets / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets,
-                                                          sc.heavy, segsz);
+        fixup_kernel<F, NB><<<NB / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy,
+                                                     segsz);
         heavy_slice_kernel<F><<<4 * 148, 128, 0, s>>>(sc.offs, sc.partials, sc.heavy, segsz,
                                                         sc.heavy_part);
         heavy_final_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.heavy, segsz, sc.heavy_part,
                                                   sc.buckets);
     }
-    reduce_seg_kernel<F><<<kRedThreads / 128, 128, 0, s>>>(sc.buckets, sc.segsum);
+    constexpr unsigned nw = VB ? kMsmWindows : 1;
+    reduce_seg_kernel<F><<<dim3(kRedThreads / 128, nw), 128, 0, s>>>(sc.buckets, sc.segsum);
     static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
-    reduce_final_kernel<F><<<1, 64, 0, s>>>(sc.segsum, out);
+    reduce_final_kernel<F><<<nw, 64, 0, s>>>(sc.segsum, out);
     (void)X;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+template <class F>
+int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc, uint8_t* out,
+          cudaStream_t s) {
+    return run_core<F, false>(table, n, scalars, sc, out, s);
+}
+
+// Variable base: sub-ranges of <= sub points (their W x sub sorted entries
+// stay below 2^32), W window sums each, then one Horner combination.
+template <class F>
+int run_vb(const uint8_t* bases, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
+           uint8_t* out, uint64_t sub, cudaStream_t s) {
+    constexpr int A = Lay<F>::AFF;
+    if (!sub || sub > kMsmVbSubMax) sub = kMsmVbSubMax;
+    const uint64_t nsub = n ? (n + sub - 1) / sub : 1;
+    if (sc.win_cap < nsub) {
+        if (sc.win) cudaFree(sc.win);
+        sc.win = nullptr;
+        sc.win_cap = 0;
+        if (cudaMalloc(&sc.win, (size_t)256 * kMsmWindows * nsub)) return -1;
+        sc.win_cap = nsub;
+    }
+    if (!n) cudaMemsetAsync(sc.win, 0, (size_t)A * kMsmWindows, s);
+    for (uint64_t r = 0; r < n; r += sub) {
+        const uint64_t len = std::min<uint64_t>(sub, n - r);
+        if (run_core<F, true>(bases + (uint64_t)A * r, len, scalars + 32 * r, sc,
+                              sc.win + (uint64_t)A * kMsmWindows * (r / sub), s))
+            return -1;
+    }
+    combine_windows_kernel<F><<<1, 32, 0, s>>>(sc.win, (uint32_t)nsub, out);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -784,7 +869,10 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 
 void MsmScratch::release() {
     void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum, scan_tmp, heavy,
-                  aff_pts[0], aff_pts[1], aff_offs[0], aff_offs[1], aff_cnt};
+                  aff_pts[0], aff_pts[1], aff_offs[0], aff_offs[1], aff_cnt, win};
+    win = nullptr;
+    win_cap = 0;
+    cap_buckets = 0;
     for (void* p : ps)
         if (p) cudaFree(p);
     aff_pts[0] = aff_pts[1] = nullptr;
@@ -808,6 +896,12 @@ int msm_run(int group, const uint8_t* table, uint64_t n, const uint8_t* scalars,
             uint8_t* out, cudaStream_t s) {
     return group == 2 ? run_t<Fq2>(table, n, scalars, sc, out, s)
                       : run_t<Fq>(table, n, scalars, sc, out, s);
+}
+
+int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
+               MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub) {
+    return group == 2 ? run_vb<Fq2>(bases, n, scalars, sc, out, sub, s)
+                      : run_vb<Fq>(bases, n, scalars, sc, out, sub, s);
 }
 
 void launch_points_convert(int group, uint8_t* pts, uint64_t n, int to_mont, cudaStream_t s) {

@@ -36,6 +36,9 @@ struct MsmScratch {
     uint32_t* aff_offs[2] = {nullptr, nullptr};   // and bucket offsets, ping-pong
     uint32_t* aff_cnt = nullptr;
     uint64_t aff_cap = 0;
+    uint8_t* win = nullptr;        // variable base: window sums per sub-range (affine)
+    uint64_t win_cap = 0;
+    uint64_t cap_buckets = 0;      // buckets the hist / offs / buckets arrays hold
     size_t scan_bytes = 0;
     size_t cap_entries = 0;
     uint64_t cap_segs = 0;         // accumulation segments the partials hold
@@ -50,6 +53,15 @@ int msm_prepare(int group, const uint8_t* bases, uint64_t n, uint8_t* table, cud
 // Montgomery form (64 / 128 B).
 int msm_run(int group, const uint8_t* table, uint64_t n, const uint8_t* scalars,
             MsmScratch& sc, uint8_t* out_affine, cudaStream_t s);
+
+// Variable-base form for bases too many to hold window tables of (a whole
+// block's proving key: 2^28 H bases): table = the n bases themselves (affine,
+// Montgomery), one bucket set per window, sub-ranges of <= sub points (0 =
+// kMsmVbSubMax) whose window sums are combined by Horner's rule at the end.
+// Same result as msm_run on msm_prepare'd tables of the same bases.
+constexpr uint64_t kMsmVbSubMax = 1ull << 24;
+int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
+               MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub = 0);
 
 // Point format conversions (standard <-> Montgomery coordinates), in place.
 void launch_points_convert(int group, uint8_t* pts, uint64_t n, int to_mont, cudaStream_t s);

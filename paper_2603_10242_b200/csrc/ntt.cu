@@ -13,8 +13,19 @@
 // tables. Coset scaling (g^i on input) and the inverse's n^-1 (and g^-k) are
 // fused into the loads / stores. Compute: log2(n)/2 + 2 Fr muls per element,
 // IMAD-pipe bound (NTT at 2^21-2^22 is ~8x above the HBM ridge).
+//
+// Above 2^22 (a whole block's domain, up to 2^28 = 8.6 GB per vector) pass A's
+// column DFT of length n2 = p q no longer fits shared memory and is itself
+// split (n = nC p q, i = i1 + nC (u + p v), k2 = s + q t):
+//   pass B1: for each (i1, u), the q-point DFT over v, times w^(nC u s),
+//            written back in place (the CTA rewrites exactly what it read);
+//   pass B2: for each (i1, s), the p-point DFT over u, times w^(i1 k2), to
+//            i1 + nC k2 (scratch) — pass A's output;
+//   pass C : as above with n1 = nC. Twiddle / coset tables are split lo/hi
+//            (the n-entry tables would be 8.6 GB each at 2^28).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "bn254.cuh"
@@ -179,6 +190,47 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_c(PassArgs a) {
     }
 }
 
+// Passes B1 / B2 of the three-pass transform: CTA b handles column i1 =
+// b mod nC (adjacent CTAs read adjacent 32-B elements) and sub-DFT x =
+// b / nC: element j at in_base + in_stride j, result k at out_base +
+// out_stride k times w^(tw_a (tw_b + tw_k k)).
+struct PassB {
+    const uint8_t* in;
+    uint8_t* out;
+    int LC, m, L2;           // log2 nC, log2 of this pass's sub-DFT, log2 n2 (lo/hi split)
+    uint64_t in_xmul, in_stride, out_xmul, out_stride;  // strides in elements
+    int tw_mode;             // 1: exponent nC x k (B1); 2: i1 (x + q k) (B2)
+    uint32_t q;              // B2: q
+    const Fr* w_sub;
+    const Fr* tw_lo;         // w^e, e < n2
+    const Fr* tw_hi;         // w^(n2 e), e < n / n2
+    const Fr* pre_lo;        // coset (B1 of a forward coset transform): g^i1 (nC)
+    const Fr* pre_hi;        // g^(nC i2) (n2)
+};
+__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_b(PassB a) {
+    extern __shared__ uint4 smem_raw[];
+    const uint32_t M = 1u << a.m;
+    const SmemFr s{smem_raw, M};
+    const uint64_t nC = 1ull << a.LC;
+    const uint64_t i1 = blockIdx.x & (nC - 1), x = blockIdx.x >> a.LC;
+    const uint64_t ib = i1 + nC * x * a.in_xmul, ob = i1 + nC * x * a.out_xmul;
+    for (uint32_t j = threadIdx.x; j < M; j += blockDim.x) {
+        const uint64_t idx = ib + a.in_stride * j;
+        Fr v = load<FrCfg>(a.in + 32 * idx);
+        if (a.pre_lo) v = mul(v, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[idx >> a.LC])));
+        s.put(bitrev(j, a.m), v);
+    }
+    __syncthreads();
+    smem_dit<1>(s, a.m, a.w_sub);
+    const uint64_t n2m = (1ull << a.L2) - 1;
+    for (uint32_t k = threadIdx.x; k < M; k += blockDim.x) {
+        Fr v = s.get(k);
+        const uint64_t ex = a.tw_mode == 1 ? nC * x * k : i1 * (x + (uint64_t)a.q * k);
+        if (ex) v = mul(v, mul(ld(&a.tw_lo[ex & n2m]), ld(&a.tw_hi[ex >> a.L2])));
+        store<FrCfg>(a.out + 32 * (ob + a.out_stride * k), v);
+    }
+}
+
 // Whole transform in one CTA (n <= 2^12): pre table g^i (n), post table
 // scale*g^-k (n) or uniform scale.
 __global__ void __launch_bounds__(512) ntt_single(PassArgs a) {
@@ -279,6 +331,26 @@ int ntt_tables(NttTables& t, int L, cudaStream_t s) {
             return -1;
         return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
+    if (L > kNttTwoPassMax) {
+        // three passes: nC = 2^LC (pass C), p = 2^LP (B2), q = 2^LQ (B1); the
+        // lo/hi split of twiddles and coset factors is at n2 = p q
+        t.LQ = L / 3;
+        t.LP = L / 3;
+        t.LC = L - t.LP - t.LQ;
+        t.L1 = t.LC;
+        t.L2 = L - t.LC;
+        const uint32_t nc = 1u << t.LC, m2 = 1u << t.L2, p = 1u << t.LP, q = 1u << t.LQ;
+        if (pw(&t.w_q, w, n / q, q / 2, nullptr) || pw(&t.wi_q, wi, n / q, q / 2, nullptr) ||
+            pw(&t.w_p, w, n / p, p / 2, nullptr) || pw(&t.wi_p, wi, n / p, p / 2, nullptr) ||
+            pw(&t.w_c, w, m2, nc / 2, nullptr) || pw(&t.wi_c, wi, m2, nc / 2, nullptr) ||
+            pw(&t.tw_lo, w, 1, m2, nullptr) || pw(&t.tw_hi, w, m2, nc, nullptr) ||
+            pw(&t.twi_lo, wi, 1, m2, nullptr) || pw(&t.twi_hi, wi, m2, nc, nullptr) ||
+            pw(&t.g_lo, g, 1, nc, nullptr) || pw(&t.g_hi, g, nc, m2, nullptr) ||
+            pw(&t.gi_post_lo, gi, 1, m2, ninv) || pw(&t.gi_post_hi, gi, m2, nc, nullptr))
+            return -1;
+        t.w_a = t.w_q;  // marks the tables built
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
     // pass A: sub-DFT of size n2 -> root w^n1 ; pass C: size n1 -> root w^n2
     if (pw(&t.w_a, w, n1, n2 / 2, nullptr) || pw(&t.wi_a, wi, n1, n2 / 2, nullptr) ||
         pw(&t.w_c, w, n2, n1 / 2, nullptr) || pw(&t.wi_c, wi, n2, n1 / 2, nullptr) ||
@@ -293,13 +365,15 @@ int ntt_tables(NttTables& t, int L, cudaStream_t s) {
 }
 
 void NttTables::release() {
+    if (w_a == w_q) w_a = nullptr;  // three-pass tables alias w_a to w_q
     Fr** all[] = {&consts, &w_a, &wi_a, &w_c, &wi_c, &tw_lo, &tw_hi, &twi_lo, &twi_hi,
                   &g_lo, &g_hi, &gi_post_lo, &gi_post_hi, &tw_full, &twi_full, &g_full,
-                  &gi_post_full};
+                  &gi_post_full, &w_q, &wi_q, &w_p, &wi_p};
     for (Fr** p : all) {
         if (*p) cudaFree(*p);
         *p = nullptr;
     }
+    LC = LP = LQ = 0;
     L = -1;
 }
 
@@ -325,6 +399,54 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
         return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
     const int n1 = 1 << t.L1, n2 = 1 << t.L2;
+    if (L > kNttTwoPassMax) {
+        // B1: in -> out (in place per CTA), B2: out -> scratch, C: scratch -> out
+        const uint64_t nc = 1ull << t.LC, p = 1ull << t.LP, q = 1ull << t.LQ;
+        PassB b{};
+        b.LC = t.LC;
+        b.L2 = t.L2;
+        b.tw_lo = inverse ? t.twi_lo : t.tw_lo;
+        b.tw_hi = inverse ? t.twi_hi : t.tw_hi;
+        b.in = in;
+        b.out = out;
+        b.m = t.LQ;
+        b.in_xmul = 1, b.in_stride = nc * p, b.out_xmul = 1, b.out_stride = nc * p;
+        b.tw_mode = 1;
+        b.w_sub = inverse ? t.wi_q : t.w_q;
+        b.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
+        b.pre_hi = (coset && !inverse) ? t.g_hi : nullptr;
+        size_t sm = sizeof(Fr) << t.LQ;
+        cudaFuncSetAttribute(ntt_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        // one butterfly per thread and stage: M / 2 threads
+        auto thr = [](int m) { return std::max(32, std::min(512, 1 << (m - 1))); };
+        ntt_pass_b<<<(unsigned)(nc * p), thr(t.LQ), sm, s>>>(b);
+        PassB b2 = b;
+        b2.in = out;
+        b2.out = scratch;
+        b2.m = t.LP;
+        b2.in_xmul = p, b2.in_stride = nc, b2.out_xmul = 1, b2.out_stride = nc * q;
+        b2.tw_mode = 2;
+        b2.q = (uint32_t)q;
+        b2.w_sub = inverse ? t.wi_p : t.w_p;
+        b2.pre_lo = b2.pre_hi = nullptr;
+        sm = sizeof(Fr) << t.LP;
+        ntt_pass_b<<<(unsigned)(nc * q), thr(t.LP), sm, s>>>(b2);
+        PassArgs c{};
+        c.L = L;
+        c.L1 = t.L1;
+        c.L2 = t.L2;
+        c.R = kNttR;
+        c.in = scratch;
+        c.out = out;
+        c.w_sub = inverse ? t.wi_c : t.w_c;
+        c.post_lo = (coset && inverse) ? t.gi_post_lo : nullptr;
+        c.post_hi = (coset && inverse) ? t.gi_post_hi : nullptr;
+        if (inverse && !coset) c.scale = t.consts + 4;
+        sm = sizeof(Fr) * (size_t)n1 * kNttR;
+        cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        ntt_pass_c<<<(unsigned)(n2 / kNttR), 512, sm, s>>>(c);
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
     // pass A: in -> scratch
     a.in = in;
     a.out = scratch;

@@ -10,7 +10,8 @@ namespace ace_gpu {
 namespace bn {
 
 constexpr int kNttSingleMax = 12;  // n <= 2^12: one CTA per transform
-constexpr int kNttMaxLog = 22;     // pass A tile = 2^11 x R x 32 B = 64 KB smem (R = 1)
+constexpr int kNttTwoPassMax = 22; // two passes (sub-DFTs <= 2^11 in 64 KB of smem, R = 1)
+constexpr int kNttMaxLog = 28;     // three passes above 2^22 (a 100k-tx block's 2^28 domain)
 constexpr int kNttR = 1;  // columns / rows per CTA: 1 -> 64 KB smem, 3 CTAs/SM (2^22 fwd 1.74 -> 1.60 ms vs R = 2)
 
 // Device tables for one size (Montgomery form).
@@ -22,6 +23,10 @@ struct NttTables {
     Fr *tw_full = nullptr, *twi_full = nullptr;  // w^e, w^-e for e < n (one product per twiddle)
     Fr *g_full = nullptr, *gi_post_full = nullptr;  // g^i, n^-1 g^-i for i < n (coset)
     Fr *g_lo = nullptr, *g_hi = nullptr, *gi_post_lo = nullptr, *gi_post_hi = nullptr;
+    // three-pass sizes (L > kNttTwoPassMax): n = nC * p * q; sub-DFT roots of
+    // the q- and p-point passes (the nC-point pass uses w_c)
+    int LC = 0, LP = 0, LQ = 0;
+    Fr *w_q = nullptr, *wi_q = nullptr, *w_p = nullptr, *wi_p = nullptr;
     void release();
 };
 

@@ -88,11 +88,13 @@ def test_ntt_small_vs_naive_dft(ctx):
         assert data.tobytes() == bytes(ref)
 
 
-@pytest.mark.parametrize("logn", [20, 22])
+@pytest.mark.parametrize("logn", [20, 22, 23, 24])
 def test_ntt_large_roundtrip_and_oracle(ctx, logn):
-    """2^22 (BASELINE configs[1]) and 2^20: forward, inverse and coset-forward
-    transforms each bit-exact vs the oracle's radix-2 NTT (multi-threaded,
-    ~1 s at 2^22), plus iNTT(NTT(x)) = x and the coset round trip."""
+    """2^22 (BASELINE configs[1]) and 2^20 (two passes), 2^23 and 2^24 (the
+    three-pass transform of block-size domains): forward, inverse and
+    coset-forward transforms each bit-exact vs the oracle's radix-2 NTT
+    (multi-threaded, ~1 s at 2^22), plus iNTT(NTT(x)) = x and the coset round
+    trip."""
     import os
     thr = C.c_int(os.cpu_count() or 8)
     rng = np.random.default_rng(logn)
@@ -123,6 +125,50 @@ def test_ntt_large_roundtrip_and_oracle(ctx, logn):
     assert np.array_equal(cos, orig)
 
 
+def test_ntt_2_28_sparse_evaluations_and_roundtrip(ctx):
+    """The 2^28 domain of a whole 100k-tx block (8.6 GB per vector, device
+    resident): a sparse input's forward and coset-forward transforms checked
+    at sampled outputs against X[k] = sum_i x_i (g^c w^k)^i evaluated here,
+    and iNTT(NTT(x)) = x on dense random data."""
+    import torch
+    logn, n = 28, 1 << 28
+    dev = torch.device("cuda:0")
+    rng = random.Random(28)
+    w = pow(5, (R - 1) >> logn, R)
+    pos = sorted(rng.sample(range(n), 64))
+    val = [rng.randrange(R) for _ in pos]
+    ks = [0, 1, 2, n - 1, n // 2, n // 3] + [rng.randrange(n) for _ in range(10)]
+    buf = torch.zeros(n, 32, dtype=torch.uint8, device=dev)
+    src = torch.from_numpy(np.frombuffer(b"".join(le(v) for v in val), np.uint8).reshape(-1, 32).copy())
+    try:
+        for coset in (0, 1):
+            buf.zero_()
+            buf[torch.tensor(pos, device=dev)] = src.to(dev)
+            p = buf.data_ptr()
+            ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 1)
+            ctx.call("acegpu_bn_ntt_dev", None, p, p, logn, 0, coset)
+            ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 0)
+            got = ints(buf[torch.tensor(ks, device=dev)].cpu().numpy().reshape(-1))
+            for k, gk in zip(ks, got):
+                z = pow(w, k, R) * (5 if coset else 1) % R
+                assert gk == sum(v * pow(z, i, R) for i, v in zip(pos, val)) % R, (coset, k)
+        # dense round trip (values < 2^253: canonical)
+        g = torch.Generator(device=dev).manual_seed(7)
+        x = torch.randint(0, 256, (n, 32), dtype=torch.uint8, device=dev, generator=g)
+        x[:, 31] &= 0x1F
+        orig = x.clone()
+        p = x.data_ptr()
+        ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 1)
+        ctx.call("acegpu_bn_ntt_dev", None, p, p, logn, 0, 1)
+        ctx.call("acegpu_bn_ntt_dev", None, p, p, logn, 1, 1)
+        ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 0)
+        assert torch.equal(x, orig)
+        del x, orig
+    finally:
+        del buf
+        torch.cuda.empty_cache()
+
+
 def g_gen(group):
     g = O.buf(64 * group)
     O.oracle().bn_generator(C.c_int(group), g)
@@ -142,10 +188,15 @@ def test_scalar_muls_match_oracle(ctx, group):
         assert out[64 * group * i:64 * group * (i + 1)].tobytes() == bytes(ref), (i, k)
 
 
-def msm_gpu(ctx, group, pts, scalars, n):
+def msm_gpu(ctx, group, pts, scalars, n, vb_sub=None):
+    """Fixed-base MSM, or the variable-base form (vb_sub = its sub-range
+    size, 0 = default) when vb_sub is given."""
     from paper_2603_10242_b200 import _native as N
     h = C.c_void_p()
-    ctx.call("acegpu_bn_msm_prepare", group, pts, n, 0, C.byref(h))
+    if vb_sub is None:
+        ctx.call("acegpu_bn_msm_prepare", group, pts, n, 0, C.byref(h))
+    else:
+        ctx.call("acegpu_bn_msm_prepare_vb", group, pts, n, 0, vb_sub, C.byref(h))
     try:
         out = np.zeros(64 * group, np.uint8)
         ctx.call("acegpu_bn_msm_run", h, scalars, out)
@@ -212,6 +263,29 @@ def test_msm_heavy_buckets(ctx, group, n):
     dl = O.buf(64 * group)
     O.oracle().bn_scalar_mul(C.c_int(group), O.ptr(bytes(G)), O.ptr(le(e)), dl)
     assert got == bytes(dl)
+
+
+@pytest.mark.parametrize("group,n,sub", [(1, 1, 0), (1, 5000, 0), (1, 5000, 777), (2, 3000, 1000),
+                                         (1, 20000, 4096)])
+def test_msm_variable_base_matches_fixed_base_and_oracle(ctx, group, n, sub):
+    """The variable-base MSM (a whole block's keys: no window tables, one
+    bucket set per window, sub-ranges Horner-combined) equals the fixed-base
+    MSM and the oracle on the same bases and scalars, including the 0/1
+    witness shape (heavy buckets) and sub-ranges that do not divide n."""
+    rng = random.Random(7 * n + group + sub)
+    ks = [rng.randrange(1, R) for _ in range(n)]
+    G = np.frombuffer(g_gen(group), np.uint8).copy()
+    pts = np.zeros(64 * group * n, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", group, G, arr(ks), n, pts)
+    for label, sc in [("random", [rng.randrange(R) for _ in range(n)]),
+                      ("0/1", [(i % 3) & 1 for i in range(n)])]:
+        sc[0] = R - 1
+        vb = msm_gpu(ctx, group, pts, arr(sc), n, vb_sub=sub)
+        assert vb == msm_gpu(ctx, group, pts, arr(sc), n), label
+        ref = O.buf(64 * group)
+        O.oracle().bn_msm(C.c_int(group), O.ptr(pts.tobytes()), O.ptr(arr(sc).tobytes()),
+                          C.c_uint64(n), ref, C.c_int(8))
+        assert vb == bytes(ref), label
 
 
 def test_msm_2_20_discrete_log(ctx):

@@ -504,3 +504,71 @@ def test_groth16_mode_attestation_verdicts(ctx):
             assert bad == ([5, 17] if forged else [])
     finally:
         pk.close()
+
+
+@pytest.mark.parametrize("T,K", [(3, 4), (64, 100)])
+def test_variable_base_key_proves_identical_proofs(ctx, T, K, monkeypatch):
+    """A variable-base key (ACEGPU_G16_VB=1: the bases without window tables,
+    one buffer slot — what a block-size key uses above 2^22) gives the same
+    proof bytes as the fixed-base key, equal to the trapdoor oracle's."""
+    from paper_2603_10242_b200 import groth16
+    rng = random.Random(T + 7 * K)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    w = arr([rng.randrange(R) for _ in range(T)])
+    pub = arr([rng.randrange(R) for _ in range(T)])
+    rs = arr([rng.randrange(R), rng.randrange(R)])
+    out = []
+    for vb in ("0", "1"):
+        monkeypatch.setenv("ACEGPU_G16_VB", vb)
+        pk = groth16.ProvingKey(T, K, trap, ctx)
+        try:
+            out.append(pk.prove(w, pub, rs)[:2])
+            out.append(pk.prove(w, pub)[:2])
+        finally:
+            pk.close()
+    assert out[0] == out[2] and out[1] == out[3]
+    assert out[0][1] == b"".join(expected_points(T, K, w, pub, trap, rs))
+
+
+@pytest.mark.parametrize("n", [1, 37, 50])
+def test_single_proof_per_block(ctx, n, monkeypatch):
+    """One Groth16 proof for the whole block (the paper's FC: a single 256-B
+    proof checked by pairings): a key whose T covers the block (T = 50, not
+    a power of two) proves blocks of n <= T txs as one chunk; the FC carries
+    that proof, verify_finality_certificate accepts it with the one proof
+    and rejects tampering; the variable-base key gives the same FC."""
+    from paper_2603_10242_b200 import groth16, prover, wire
+    T, K = 50, 6
+    rng = random.Random(50 + n)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    fb = O.multi_user_block(n, 3)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+    wit = _witnesses(fb, n)
+    fcs = []
+    for vb in ("0", "1"):
+        monkeypatch.setenv("ACEGPU_G16_VB", vb)
+        pk = groth16.ProvingKey(T, K, trap, ctx)
+        try:
+            codes, proof, fc, cps = pk.prove_block(wfb, wit)
+            assert len(cps) == 256 and proof[:256] == cps
+            V = prover.FcCheck
+            assert pk.verify_finality_certificate(fc, wfb, cps) == V.Valid
+            bad = bytearray(cps)
+            bad[5] ^= 1
+            assert pk.verify_finality_certificate(fc, wfb, bytes(bad)) == V.ProofMismatch
+            pay = fb.payloads.copy()
+            pay[int(fb.offs[n - 1]) + 20] ^= 1
+            wfb3 = wire.FlatBlock(pay, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+            assert pk.verify_finality_certificate(fc, wfb3, cps) == V.ProofMismatch
+            fcs.append(fc)
+        finally:
+            pk.close()
+    assert fcs[0] == fcs[1]
+    if n > 32:  # a non-power-of-two key still rejects blocks above T
+        pk = groth16.ProvingKey(32 + 1, K, trap, ctx)
+        try:
+            with pytest.raises(ValueError):
+                pk.prove_block(wire.FlatBlock(fb.payloads, fb.offs, fb.atts,
+                                              np.frombuffer(fb.header, np.uint8).copy()), wit)
+        finally:
+            pk.close()
