@@ -451,6 +451,7 @@ def run_ours(args, rank: int, world: int) -> None:
         if world == 1:
             g16["zkace_hmac"] = bench_zkace_hmac_chunk(ctx, dev, fb, revs, rev_index)
             g16["zkace_block"] = bench_zkace_block(ctx, dev)
+            g16["block_proof"] = bench_groth16_single_block(ctx, dev, fb, revs, rev_index)
         if world == 1 and not args.no_cpu_baseline:
             bn["cpu_oracle"] = bn254_cpu_baseline(msm_in)
 
@@ -534,6 +535,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "attest_many_revs": many_revs,
         "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
         "zkace_hmac_chunk": g16.get("zkace_hmac"), "zkace_block_1024": g16.get("zkace_block"),
+        "groth16_one_proof_block_100000": g16.get("block_proof"),
         "groth16_stream": g16.get("stream"),
         "groth16_roofline": g16_roof, "bn254": bn,
     }
@@ -867,6 +869,74 @@ def bench_groth16_stream(ctx, dev: int, pk, rank: int, world: int, blocks: int =
             "block_interval_ms": 400.0,
             "keeps_up_with_32k_tps": blocks * n / (total_ms * 1e-3) >= 32000,
             "accepted_on_rank": acc, "timing": "CUDA events; H2D on a copy stream ahead of the prover"}
+
+
+def bench_groth16_single_block(ctx, dev: int, fb, revs, rev_index, steps: int = 3,
+                               e2e_steps: int = 2) -> dict:
+    """ONE Groth16 proof for the whole 100k-tx block (the paper's FC: a single
+    256-B proof checked by pairings): a block-size key (T = n txs x 1,400
+    constraints = 140.1 M constraints, domain 2^28; variable-base bases, no
+    window tables: ~62 GB of bases + ~39 GB of per-proof vectors in HBM).
+    Device-resident step (attestation + the proof + tree + FC, CUDA events)
+    and e2e through acegpu_g16_prove_block (host buffers in/out, wall clock),
+    then verify_finality_certificate with that one proof."""
+    import torch
+    from paper_2603_10242_b200 import groth16, prover, shard, wire
+    n = fb.n
+    torch.cuda.empty_cache()
+    wit = make_witnesses(fb, revs, rev_index, ctx)
+    t0 = time.perf_counter()
+    pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx)
+    setup_s = time.perf_counter() - t0
+    try:
+        free, total = torch.cuda.mem_get_info(dev)
+        db = shard.DeviceBlock.upload(fb, 0, n, revs, rev_index, device=dev)
+        db.witnesses = torch.from_numpy(wit).to(f"cuda:{dev}")
+        codes = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{dev}")
+        be = shard.G16Backend(pk, ctx)
+        lg = (n - 1).bit_length()
+        s = torch.cuda.current_stream()
+
+        def step():
+            return shard.prove_sharded(db, n, 0, 1, lg, be, codes=codes, return_roots=True)
+        step()
+        torch.cuda.synchronize()
+        ts = []
+        with ClockSampler(dev) as clocks:
+            for _ in range(steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                proof, fc, roots = step()
+                b.record(s)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+        fcb = fc.cpu().numpy().tobytes()
+        ms = statistics.mean(ts)
+        wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts,
+                             np.frombuffer(bytes(fb.header), np.uint8).copy())
+        e2e = []
+        for _ in range(e2e_steps):
+            t0 = time.perf_counter()
+            c2, p2, fc2, cps = pk.prove_block(wfb, wit, revs, rev_index)
+            e2e.append((time.perf_counter() - t0) * 1e3)
+        t0 = time.perf_counter()
+        v = pk.verify_finality_certificate(fc2, wfb, cps)
+        vms = (time.perf_counter() - t0) * 1e3
+        return {"n_tx": n, "proofs_per_block": 1, "constraints": pk.constraints,
+                "domain_log2": pk.log_domain, "setup_s_once": setup_s,
+                "device_mem_gb_after_setup": (total - free) / 1e9,
+                "latency_ms": ms, "latency_ms_per_step": ts, "steps": steps,
+                "proven_tx_per_s": n / (ms * 1e-3), "vs_400ms_interval": ms / 400.0,
+                "e2e_ms": statistics.mean(e2e), "e2e_ms_per_step": e2e,
+                "e2e_fc_equal": fc2 == fcb, "accepted": int((codes == 0).sum().item()),
+                "fc_bytes": 328, "proof_bytes_beside_fc": len(cps),
+                "verify_fc": v.name, "verify_fc_ms": vms, "fc_sha256": hashlib_sha256(fcb),
+                "clocks": clocks.summary(),
+                "note": "one Groth16 proof for the whole block; 1 GPU (a DIZK-style split of "
+                        "the MSMs / NTTs across GPUs is not built)"}
+    finally:
+        pk.close()
+        torch.cuda.empty_cache()
 
 
 def bench_zkace_block(ctx, dev: int, n: int = 1024, steps: int = 3) -> dict:

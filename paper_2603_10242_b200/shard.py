@@ -129,7 +129,9 @@ class G16Backend(GpuBackend):
 
     def shard_roots(self, db: DeviceBlock, n_total: int, log2_chunk: int, codes=None):
         import torch
-        assert (1 << log2_chunk) == self.pk.T, "chunk size must equal the circuit's txs/chunk"
+        # chunks of pk.T txs, or one chunk for the whole block (a block-size key)
+        assert (1 << log2_chunk) == self.pk.T or (
+            n_total <= self.pk.T <= (1 << log2_chunk)), "chunk size must equal the circuit's txs/chunk"
         c = n_chunks(db.n, log2_chunk)
         roots = torch.empty(max(c, 1) * 289, dtype=torch.uint8, device=db.atts.device)
         merk = torch.empty(max(c, 1) * 32, dtype=torch.uint8, device=db.atts.device)
