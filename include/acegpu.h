@@ -239,9 +239,9 @@ void acegpu_bn_msm_free(acegpu_msm_bases* bases);
 int acegpu_bn_msm_run(acegpu_ctx* ctx, const acegpu_msm_bases* bases, const uint8_t* scalars,
                       uint8_t* out_affine);
 /* Variable-base form (no window tables: n x 64 B / 128 B of bases instead of
- * windows x that — a whole block's proving key): one bucket set per window,
- * sub-ranges of `sub` points (0 = 2^24, the maximum), Horner-combined
- * window sums. Same results as the fixed-base form; run with
+ * windows x that — a whole block's proving key): c = 20-bit windows, one
+ * bucket set per window, sub-ranges of `sub` points (0 = 2^26, the maximum),
+ * Horner-combined window sums. Same results as the fixed-base form; run with
  * acegpu_bn_msm_run(_dev). n up to 2^31. */
 int acegpu_bn_msm_prepare_vb(acegpu_ctx* ctx, int group, const uint8_t* points, uint64_t n,
                              int points_on_device, uint64_t sub, acegpu_msm_bases** out);

@@ -61,6 +61,22 @@ struct Lay {
     static constexpr int ACC_MIN_CTAS = EB == 32 ? ACEGPU_G1_ACC_MINB : ACEGPU_G2_ACC_MINB;
 };
 
+// Window configuration: c-bit signed digits, W windows, NB buckets per
+// window, reduction segments. Fixed base uses c = kMsmC (17); variable base
+// (block-size keys) uses kMsmVbC: with 2^26-point sub-ranges the 2^19
+// buckets of c = 20 cost ~2 % and save 2 of 15 windows.
+template <int C>
+struct Win {
+    static constexpr int c = C;
+    static constexpr int W = (255 + C - 1) / C;
+    static constexpr int NB = 1 << (C - 1);
+    static constexpr int RedSeg = NB / 8192 > 4 ? NB / 8192 : 4;  // buckets per thread
+    static constexpr int RedThreads = NB / RedSeg;                 // <= 8192 -> <= 64 partials
+    static_assert(RedThreads / 128 <= 64, "reduce_final holds one partial per thread");
+};
+using WinFixed = Win<kMsmC>;
+using WinVb = Win<kMsmVbC>;
+
 template <class F>
 __device__ __forceinline__ bool load_affine(const uint8_t* p, F& x, F& y) {
     fload(x, p);
@@ -133,19 +149,21 @@ __global__ void prepare_kernel(const uint8_t* bases, uint64_t n, uint8_t* table)
 // bits [c w, c w + c) (a 64-bit window over two limbs); raw values above
 // 2^(c-1) become raw - 2^c with a carry into the next window. The top window
 // holds < 2^(254 - c (W-1)) <= 2^(c-1), so no carry leaves it.
-__device__ __forceinline__ void digits(const uint8_t* s, int32_t d[kMsmWindows]) {
+template <class Wn = WinFixed>
+__device__ __forceinline__ void digits(const uint8_t* s, int32_t d[Wn::W]) {
+    constexpr int kC = Wn::c;
     const uint4* q = reinterpret_cast<const uint4*>(s);
     uint4 a = q[0], b = q[1];
     const uint32_t limb[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, 0u};
     uint32_t carry = 0;
 #pragma unroll
-    for (int w = 0; w < kMsmWindows; ++w) {
-        const int bit = w * kMsmC, lo = bit >> 5, sh = bit & 31;
+    for (int w = 0; w < Wn::W; ++w) {
+        const int bit = w * kC, lo = bit >> 5, sh = bit & 31;
         const uint64_t v = ((uint64_t)limb[lo + 1] << 32) | limb[lo];
-        const uint32_t raw = (uint32_t)(v >> sh) & ((1u << kMsmC) - 1u);
+        const uint32_t raw = (uint32_t)(v >> sh) & ((1u << kC) - 1u);
         const uint32_t t = raw + carry;
-        if (t > (1u << (kMsmC - 1))) {
-            d[w] = (int32_t)t - (1 << kMsmC);
+        if (t > (1u << (kC - 1))) {
+            d[w] = (int32_t)t - (1 << kC);
             carry = 1;
         } else {
             d[w] = (int32_t)t;
@@ -163,7 +181,7 @@ __device__ __forceinline__ void digits(const uint8_t* s, int32_t d[kMsmWindows])
 #define ACEGPU_SORT_AGG 1
 #endif
 #if !ACEGPU_SORT_AGG
-template <bool VB>
+template <bool VB, class Wn = WinFixed>
 __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
     static_assert(!VB, "variable-base MSM needs ACEGPU_SORT_AGG");
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -174,7 +192,7 @@ __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist)
     for (int w = 0; w < kMsmWindows; ++w)
         if (d[w]) atomicAdd(&hist[abs(d[w]) - 1], 1u);
 }
-template <bool VB>
+template <bool VB, class Wn = WinFixed>
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
                                uint32_t* sorted) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -192,35 +210,35 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
 // VB (variable base, no window tables): bucket key w * kMsmBuckets + |d| - 1
 // (one bucket set per window) and entry = the point index; fixed base: key
 // |d| - 1 and entry = the table row w n + i.
-template <bool VB>
+template <bool VB, class Wn>
 __device__ __forceinline__ uint32_t bucket_key(int w, int32_t d) {
-    return VB ? (uint32_t)(w * kMsmBuckets + abs(d) - 1) : (uint32_t)(abs(d) - 1);
+    return VB ? (uint32_t)(w * Wn::NB + abs(d) - 1) : (uint32_t)(abs(d) - 1);
 }
-template <bool VB>
+template <bool VB, class Wn = WinFixed>
 __global__ void count_kernel(const uint8_t* scalars, uint64_t n, uint32_t* hist) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    int32_t d[kMsmWindows];
-    if (i < n) digits(scalars + 32 * i, d);
+    int32_t d[Wn::W];
+    if (i < n) digits<Wn>(scalars + 32 * i, d);
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int w = 0; w < kMsmWindows; ++w) {
-        const uint32_t key = (i < n && d[w]) ? bucket_key<VB>(w, d[w]) : 0xFFFFFFFFu;
+    for (int w = 0; w < Wn::W; ++w) {
+        const uint32_t key = (i < n && d[w]) ? bucket_key<VB, Wn>(w, d[w]) : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, key);
         if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
     }
 }
 
-template <bool VB>
+template <bool VB, class Wn = WinFixed>
 __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cursor,
                                uint32_t* sorted) {
     const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    int32_t d[kMsmWindows];
-    if (i < n) digits(scalars + 32 * i, d);
+    int32_t d[Wn::W];
+    if (i < n) digits<Wn>(scalars + 32 * i, d);
     const int lane = threadIdx.x & 31;
     const uint32_t below = (1u << lane) - 1u;
 #pragma unroll
-    for (int w = 0; w < kMsmWindows; ++w) {
-        const uint32_t key = (i < n && d[w]) ? bucket_key<VB>(w, d[w]) : 0xFFFFFFFFu;
+    for (int w = 0; w < Wn::W; ++w) {
+        const uint32_t key = (i < n && d[w]) ? bucket_key<VB, Wn>(w, d[w]) : 0xFFFFFFFFu;
         const uint32_t peers = __match_any_sync(0xffffffffu, key);
         const int leader = __ffs(peers) - 1;
         uint32_t base = 0;
@@ -435,19 +453,18 @@ __global__ void __launch_bounds__(128) heavy_final_kernel(const uint32_t* offs,
     }
 }
 
-constexpr int kRedSeg = kMsmBuckets / 8192 > 4 ? kMsmBuckets / 8192 : 4;  // buckets per thread
-constexpr int kRedThreads = kMsmBuckets / kRedSeg;  // <= 8192 -> <= 64 CTA partials
 
 // Segment j covers bucket indices [a, a+kRedSeg), weights a+1 .. a+kRedSeg:
 // sum = tot + a*run with running sums from the top; one partial per CTA.
 // (A work-efficient multi-level recursion on the run_j measured 2.7x slower
 // here: every level pays a serial chain of point additions.)
 // (blockIdx.y: the window's bucket set in a variable-base run)
-template <class F>
+template <class F, class Wn>
 __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets, uint8_t* segsum) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     constexpr int X = Lay<F>::XZ;
-    buckets += (uint64_t)X * kMsmBuckets * blockIdx.y;
+    constexpr int kRedSeg = Wn::RedSeg, kRedThreads = Wn::RedThreads;
+    buckets += (uint64_t)X * Wn::NB * blockIdx.y;
     segsum += (uint64_t)X * gridDim.x * blockIdx.y;
     XYZZ<F> tot = XYZZ<F>::inf();
     if (j < kRedThreads) {
@@ -466,10 +483,10 @@ __global__ void __launch_bounds__(128) reduce_seg_kernel(const uint8_t* buckets,
 // Sum the per-CTA partials of reduce_seg (kRedThreads / 128 <= 64) and
 // write the affine result.
 // (blockIdx.x: the window in a variable-base run -> out[window])
-template <class F>
+template <class F, class Wn>
 __global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum, uint8_t* out) {
     constexpr int X = Lay<F>::XZ;
-    constexpr int kParts = kRedThreads / 128;
+    constexpr int kParts = Wn::RedThreads / 128;
     segsum += (uint64_t)X * kParts * blockIdx.x;
     out += (uint64_t)Lay<F>::AFF * blockIdx.x;
     __shared__ __align__(16) uint8_t sm[2 * sizeof(XYZZ<F>)];
@@ -685,16 +702,16 @@ __global__ void __launch_bounds__(128) affine_heavy_kernel(const uint8_t* pts, c
 
 // Variable-base result: win[r * W + w] = the window-w sum of sub-range r
 // (affine); out = sum_w 2^(c w) sum_r win[r W + w] (Horner from the top).
-template <class F>
+template <class F, class Wn>
 __global__ void combine_windows_kernel(const uint8_t* win, uint32_t nsub, uint8_t* out) {
     if (threadIdx.x || blockIdx.x) return;
     constexpr int A = Lay<F>::AFF;
     XYZZ<F> acc = XYZZ<F>::inf();
-    for (int w = kMsmWindows - 1; w >= 0; --w) {
-        for (int d = 0; d < kMsmC; ++d) acc = xyzz_dbl(acc);
+    for (int w = Wn::W - 1; w >= 0; --w) {
+        for (int d = 0; d < Wn::c; ++d) acc = xyzz_dbl(acc);
         for (uint32_t r = 0; r < nsub; ++r) {
             F x, y;
-            if (load_affine<F>(win + (uint64_t)A * (r * kMsmWindows + w), x, y))
+            if (load_affine<F>(win + (uint64_t)A * (r * Wn::W + w), x, y))
                 acc = xyzz_madd<F>(acc, x, y);
         }
     }
@@ -720,12 +737,12 @@ int prepare_t(const uint8_t* bases, uint64_t n, uint8_t* table, cudaStream_t s) 
 // out = the affine result. Variable base (VB = true): table = the n bases
 // themselves, one bucket set per window, out = the kMsmWindows affine window
 // sums (combine_windows_kernel weights them).
-template <class F, bool VB>
+template <class F, bool VB, class Wn>
 int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
              uint8_t* out, cudaStream_t s) {
     constexpr int X = Lay<F>::XZ;
-    constexpr int NB = VB ? kMsmWindows * kMsmBuckets : kMsmBuckets;
-    const uint64_t cap = (uint64_t)kMsmWindows * n;
+    constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
+    const uint64_t cap = (uint64_t)Wn::W * n;
     // segment length: kMsmSeg, shorter for small MSMs (>= ~19k threads, so a
     // verifier-size MSM is not a few hundred threads of 64 serial adds)
     uint32_t segsz = kMsmSeg;
@@ -743,9 +760,9 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
         sc.win_cap = win_cap;
         if (cudaMalloc(&sc.hist, 4 * (nbk + 1)) || cudaMalloc(&sc.offs, 4 * (nbk + 1)) ||
             cudaMalloc(&sc.cursor, 4 * nbk) || cudaMalloc(&sc.sorted, 4 * keep) ||
-            cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||
+            cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||  // G2 size: scratch shared
             cudaMalloc(&sc.buckets, (size_t)256 * nbk) ||
-            cudaMalloc(&sc.segsum, (size_t)256 * (kRedThreads / 128) * (nbk / kMsmBuckets)) ||
+            cudaMalloc(&sc.segsum, (size_t)256 * 64 * std::max<uint64_t>(Wn::W, 16)) ||
             cudaMalloc(&sc.heavy, 4 * (nbk + 1)) ||
             // slices: <= nseg / kHeavySlice + one partial slice per heavy bucket
             // (each spans > kHeavySpan segments)
@@ -761,14 +778,14 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
     cudaMemsetAsync(sc.hist, 0, 4 * (NB + 1), s);
     cudaMemsetAsync(sc.heavy, 0, 4, s);
     const unsigned gb = (unsigned)((n + 255) / 256);
-    count_kernel<VB><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
+    count_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
     // offs = exclusive scan of hist[0..NB] (hist[NB] = 0 -> offs[NB] = total)
     size_t scan_bytes = sc.scan_bytes;
     if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, scan_bytes, sc.hist, sc.offs, NB + 1, s) !=
         cudaSuccess)
         return -1;
     cudaMemcpyAsync(sc.cursor, sc.offs, 4 * NB, cudaMemcpyDeviceToDevice, s);
-    scatter_kernel<VB><<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
+    scatter_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
     bool affine = false;
     if constexpr (sizeof(F) == sizeof(Fq) && !VB) affine = ACEGPU_MSM_AFFINE && affine_enabled();
     if (affine) {
@@ -825,10 +842,9 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
         heavy_final_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.heavy, segsz, sc.heavy_part,
                                                   sc.buckets);
     }
-    constexpr unsigned nw = VB ? kMsmWindows : 1;
-    reduce_seg_kernel<F><<<dim3(kRedThreads / 128, nw), 128, 0, s>>>(sc.buckets, sc.segsum);
-    static_assert(kRedThreads / 128 <= 64, "reduce_final holds one partial per thread");
-    reduce_final_kernel<F><<<nw, 64, 0, s>>>(sc.segsum, out);
+    constexpr unsigned nw = VB ? Wn::W : 1;
+    reduce_seg_kernel<F, Wn><<<dim3(Wn::RedThreads / 128, nw), 128, 0, s>>>(sc.buckets, sc.segsum);
+    reduce_final_kernel<F, Wn><<<nw, 64, 0, s>>>(sc.segsum, out);
     (void)X;
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
@@ -836,7 +852,7 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
 template <class F>
 int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc, uint8_t* out,
           cudaStream_t s) {
-    return run_core<F, false>(table, n, scalars, sc, out, s);
+    return run_core<F, false, WinFixed>(table, n, scalars, sc, out, s);
 }
 
 // Variable base: sub-ranges of <= sub points (their W x sub sorted entries
@@ -845,23 +861,24 @@ template <class F>
 int run_vb(const uint8_t* bases, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
            uint8_t* out, uint64_t sub, cudaStream_t s) {
     constexpr int A = Lay<F>::AFF;
+    using Wn = WinVb;
     if (!sub || sub > kMsmVbSubMax) sub = kMsmVbSubMax;
     const uint64_t nsub = n ? (n + sub - 1) / sub : 1;
     if (sc.win_cap < nsub) {
         if (sc.win) cudaFree(sc.win);
         sc.win = nullptr;
         sc.win_cap = 0;
-        if (cudaMalloc(&sc.win, (size_t)256 * kMsmWindows * nsub)) return -1;
+        if (cudaMalloc(&sc.win, (size_t)256 * Wn::W * nsub)) return -1;
         sc.win_cap = nsub;
     }
-    if (!n) cudaMemsetAsync(sc.win, 0, (size_t)A * kMsmWindows, s);
+    if (!n) cudaMemsetAsync(sc.win, 0, (size_t)A * Wn::W, s);
     for (uint64_t r = 0; r < n; r += sub) {
         const uint64_t len = std::min<uint64_t>(sub, n - r);
-        if (run_core<F, true>(bases + (uint64_t)A * r, len, scalars + 32 * r, sc,
-                              sc.win + (uint64_t)A * kMsmWindows * (r / sub), s))
+        if (run_core<F, true, Wn>(bases + (uint64_t)A * r, len, scalars + 32 * r, sc,
+                                  sc.win + (uint64_t)A * Wn::W * (r / sub), s))
             return -1;
     }
-    combine_windows_kernel<F><<<1, 32, 0, s>>>(sc.win, (uint32_t)nsub, out);
+    combine_windows_kernel<F, Wn><<<1, 32, 0, s>>>(sc.win, (uint32_t)nsub, out);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -56,10 +56,15 @@ int msm_run(int group, const uint8_t* table, uint64_t n, const uint8_t* scalars,
 
 // Variable-base form for bases too many to hold window tables of (a whole
 // block's proving key: 2^28 H bases): table = the n bases themselves (affine,
-// Montgomery), one bucket set per window, sub-ranges of <= sub points (0 =
-// kMsmVbSubMax) whose window sums are combined by Horner's rule at the end.
+// Montgomery), c = kMsmVbC-bit windows, one bucket set per window, sub-ranges
+// of <= sub points (0 = kMsmVbSubMax) whose window sums are combined by
+// Horner's rule at the end.
 // Same result as msm_run on msm_prepare'd tables of the same bases.
-constexpr uint64_t kMsmVbSubMax = 1ull << 24;
+#ifndef ACEGPU_MSM_VB_C
+#define ACEGPU_MSM_VB_C 20  // 13 windows; the per-window 2^19-bucket reductions amortise over 2^26 points
+#endif
+constexpr int kMsmVbC = ACEGPU_MSM_VB_C;
+constexpr uint64_t kMsmVbSubMax = 1ull << 26;  // W x sub bucket entries < 2^32
 int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
                MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub = 0);
 
