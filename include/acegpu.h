@@ -384,6 +384,31 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                const uint8_t* d_witness256, uint8_t* d_roots289,
                                uint8_t* d_merkle32);
 
+/* ---- one proof per block across ranks (DIZK-style split of the MSMs) ----
+ * setup_slice: the key of rank `rank` of `world` — the same CRS as
+ * acegpu_g16_setup (same trapdoor), but only the rank's slice of every base
+ * array (A, B1, B2, L, H) is stored (variable-base form); the verifying key is
+ * whole. Each rank: block_inputs_dev (verdicts, Merkle root, w, pub for a
+ * block of n <= T txs; every rank holds the whole block), prove_partial_dev
+ * (its partial A | B1 | B2 | L | H, 384 B — the witness and the H
+ * polynomial are computed on every rank), an all-gather of the 384-B
+ * records, finish_dev (sum in rank order, s A + r B1, C, proof, root leaf),
+ * then acegpu_combine_roots_dev with one root. world = 1 with a plain key
+ * gives the same bytes as acegpu_g16_prove_block. Replaces prover.cpp:129-142
+ * in one-proof mode. */
+int acegpu_g16_setup_slice(acegpu_ctx* ctx, uint32_t T, uint32_t K, const uint8_t* trapdoor5,
+                           uint32_t rank, uint32_t world, acegpu_g16** out);
+int acegpu_g16_block_inputs_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
+                                const uint8_t* d_payloads, const uint64_t* d_offs,
+                                const uint8_t* d_atts, uint64_t n, const uint8_t* d_revs,
+                                uint64_t n_revs, const uint32_t* d_rev_index, uint8_t* d_codes,
+                                const uint8_t* d_witness256, uint8_t* d_w, uint8_t* d_pub,
+                                uint8_t* d_merkle32);
+int acegpu_g16_prove_partial_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
+                                 const uint8_t* d_w, const uint8_t* d_pub, uint8_t* d_part384);
+int acegpu_g16_finish_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_parts,
+                          uint32_t world, uint8_t* d_proof256, uint8_t* d_raw256,
+                          uint8_t* d_digest32, uint8_t* d_root289);
 /* The north-star block path through ONE host-buffer call (the Groth16-mode
  * prove_block + build_finality_certificate, prover.cpp:129-156): the block's
  * H2D, batched attestation verdicts (revs / rev_index as

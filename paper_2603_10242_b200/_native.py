@@ -76,6 +76,12 @@ _SIGS = {
     "acegpu_bn_msm_prepare_vb": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, u64,
                                            C.POINTER(C.c_void_p)]),
     "acegpu_bn_msm_free": (None, [C.c_void_p]),
+    "acegpu_g16_setup_slice": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.c_uint32, C.c_uint32,
+                                         C.POINTER(C.c_void_p)]),
+    "acegpu_g16_block_inputs_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, vp, u64, vp,
+                                              vp, vp, vp, vp, vp]),
+    "acegpu_g16_prove_partial_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp]),
+    "acegpu_g16_finish_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, C.c_uint32, vp, vp, vp, vp]),
     "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),
     "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),
     "acegpu_g16_setup": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.POINTER(C.c_void_p)]),

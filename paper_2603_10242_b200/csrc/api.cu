@@ -123,6 +123,7 @@ struct acegpu_msm_bases {
     uint8_t* table = nullptr;  // kMsmWindows * n (vb: n) affine points, Montgomery form
     int vb = 0;
     uint64_t vb_sub = 0;
+    uint64_t lo = 0;  // a split key's slice: bases [lo, lo + n) of the full array
 };
 
 namespace {
@@ -1947,6 +1948,8 @@ struct acegpu_g16 {
     // variable-base key (domain above 2^22, e.g. one proof for a whole block):
     // bases without window tables, one buffer slot (proofs serialise)
     bool vb = false;
+    // split key (acegpu_g16_setup_slice): this rank's slice of every base array
+    uint32_t rank = 0, world = 1;
 };
 
 namespace {
@@ -2049,7 +2052,8 @@ namespace {
 // Proving + verifying key: the synthetic chain circuit (r == nullptr: T txs
 // x K constraints) or a general R1CS r (T = its public inputs, K = 0).
 int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
-                   const uint8_t* trapdoor5, acegpu_g16** out) {
+                   const uint8_t* trapdoor5, acegpu_g16** out, uint32_t rank = 0,
+                   uint32_t world = 1) {
     cudaStream_t s = c->stream;
     auto* g = new acegpu_g16();
     std::unique_ptr<acegpu_g16, void (*)(acegpu_g16*)> own(g, acegpu_g16_free);
@@ -2064,8 +2068,10 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     g->N = 1ull << g->logn;
     {
         const char* e = std::getenv("ACEGPU_G16_VB");  // 1: force variable-base (tests)
-        g->vb = g->logn > uint32_t(bn::kNttTwoPassMax) || (e && e[0] == '1');
+        g->vb = g->logn > uint32_t(bn::kNttTwoPassMax) || (e && e[0] == '1') || world > 1;
     }
+    g->rank = rank;
+    g->world = world;
     g->Vp = g->d.V - 1 - T;
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     auto dm = [&](uint8_t** p, size_t bytes) { return cudaMalloc(p, bytes ? bytes : 16); };
@@ -2173,6 +2179,8 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     auto bases = [&](int group, const uint8_t* scal, uint64_t cnt,
                      std::initializer_list<const uint8_t*> extra, acegpu_msm_bases** out) -> int {
         const uint64_t pb = 64ull * group, total = cnt + extra.size();
+        // a split key holds the slice [lo, hi) of the array (the extras last)
+        const uint64_t lo = total * rank / world, hi = total * (rank + 1) / world;
         uint8_t* dst = pts;
         std::unique_ptr<acegpu_msm_bases, void (*)(acegpu_msm_bases*)> b(nullptr,
                                                                           acegpu_bn_msm_free);
@@ -2180,17 +2188,23 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
             b.reset(new acegpu_msm_bases());
             b->device = c->device;
             b->group = group;
-            b->n = total;
+            b->n = hi - lo;
+            b->lo = lo;
             b->vb = 1;
-            const cudaError_t e = cudaMalloc(&b->table, pb * total);
+            const cudaError_t e = cudaMalloc(&b->table, pb * std::max<uint64_t>(hi - lo, 1));
             if (e != cudaSuccess)
                 return fail(ACEGPU_ECUDA, std::string("g16 bases alloc: ") + cudaGetErrorString(e));
             dst = b->table;
         }
-        bn::launch_comb_muls(group, group == 1 ? tab1 : tab2, scal, cnt, dst, s);
+        if (lo < std::min(hi, cnt))
+            bn::launch_comb_muls(group, group == 1 ? tab1 : tab2, scal + 32 * lo,
+                                 std::min(hi, cnt) - lo, dst, s);
         uint64_t k = cnt;
-        for (const uint8_t* x : extra)
-            CK(cudaMemcpyAsync(dst + pb * k++, x, pb, cudaMemcpyDeviceToDevice, s));
+        for (const uint8_t* x : extra) {
+            if (k >= lo && k < hi)
+                CK(cudaMemcpyAsync(dst + pb * (k - lo), x, pb, cudaMemcpyDeviceToDevice, s));
+            ++k;
+        }
         CKL();
         if (g->vb) {
             *out = b.release();
@@ -2248,6 +2262,17 @@ extern "C" int acegpu_g16_setup_r1cs(acegpu_ctx* c, const acegpu_r1cs* r, const 
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     return g16_setup_impl(c, uint32_t(r->n_pub), 0, r, trapdoor5, out);
+}
+
+extern "C" int acegpu_g16_setup_slice(acegpu_ctx* c, uint32_t T, uint32_t K,
+                                      const uint8_t* trapdoor5, uint32_t rank, uint32_t world,
+                                      acegpu_g16** out) {
+    if (T < 1 || K < 2) return fail(ACEGPU_EINVAL, "g16: need T >= 1 and K >= 2");
+    if (!trapdoor5 || !out) return fail(ACEGPU_EINVAL, "null argument");
+    if (world < 1 || rank >= world) return fail(ACEGPU_EINVAL, "g16: need rank < world");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_setup_impl(c, T, K, nullptr, trapdoor5, out, rank, world);
 }
 
 // ---- witness programs (GPU witness generation for bit circuits) ---------------
@@ -2466,7 +2491,7 @@ namespace {
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr,
-                     const uint8_t* d_z = nullptr);
+                     const uint8_t* d_z = nullptr, uint8_t* d_part384 = nullptr);
 }
 
 // General R1CS: prove from the full assignment z (vars x 32-B standard form,
@@ -2545,7 +2570,9 @@ G16Trace g_g16_trace;
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready,
-                     const uint8_t* d_z) {
+                     const uint8_t* d_z, uint8_t* d_part384) {
+    if (g->world > 1 && !d_part384)
+        return fail(ACEGPU_EINVAL, "g16: a split key proves partials (acegpu_g16_prove_partial_dev)");
     if (!g->r1cs != !d_z)
         return fail(ACEGPU_EINVAL, g->r1cs ? "g16: an R1CS key proves full assignments "
                                              "(acegpu_g16_prove_z)"
@@ -2612,9 +2639,12 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CKL();
     CK(cudaEventRecord(g->ev_n, sn));
     CK(cudaStreamWaitEvent(sh, g->ev_n, 0));
+    // (n: the full array's length; a split key's bases cover [lo, lo + b->n))
     auto msm = [](const acegpu_msm_bases* b, uint64_t n, const uint8_t* sc, bn::MsmScratch& scr,
                   uint8_t* out, cudaStream_t st) {
-        return b->vb ? bn::msm_run_vb(b->group, b->table, n, sc, scr, out, st, b->vb_sub)
+        if (b->vb && b->n == 0) return int(cudaMemsetAsync(out, 0, 64 * b->group, st) != cudaSuccess);
+        return b->vb ? bn::msm_run_vb(b->group, b->table, b->n, sc + 32 * b->lo, scr, out, st,
+                                      b->vb_sub)
                      : bn::msm_run(b->group, b->table, n, sc, scr, out, st);
     };
     if (msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
@@ -2638,6 +2668,16 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
+    if (d_part384) {
+        // this rank's partial points A | B1 | B2 | L | H; the sum over ranks,
+        // s A, r B1 and the assembly follow in acegpu_g16_finish_dev
+        for (cudaEvent_t e : {g->ev_ab, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
+        CK(cudaMemcpyAsync(d_part384, g->pts, 384, cudaMemcpyDeviceToDevice, s));
+        CK(cudaEventRecord(sl.done, s));
+        tr.dump();
+        c->launches += 15 + 5 * bn::kMsmKernels;
+        return ACEGPU_OK;
+    }
     CK(cudaStreamWaitEvent(g->side, g->ev_ab, 0));
     bn::g16_scale(g->pts, g->rs, g->scaled, g->side);
     CK(cudaEventRecord(g->ev_scaled, g->side));
@@ -2757,6 +2797,80 @@ extern "C" int acegpu_g16_shard_roots_dev(acegpu_ctx* c, void* stream, acegpu_g1
     return g16_shard_roots_locked(c, pick(c, stream), g, d_payloads, d_offs, d_atts, n, n_total,
                                   d_revs, n_revs, d_rev_index, d_codes, d_witness256, d_roots289,
                                   d_merkle32);
+}
+
+// ---- one proof per block across ranks (split keys) ----------------------------
+// The block's inputs for a block-size key (n <= T): verdicts, the id_com
+// Merkle root, the zero-padded witnesses w and public inputs pub (T x 32 B).
+extern "C" int acegpu_g16_block_inputs_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                           const uint8_t* d_payloads, const uint64_t* d_offs,
+                                           const uint8_t* d_atts, uint64_t n,
+                                           const uint8_t* d_revs, uint64_t n_revs,
+                                           const uint32_t* d_rev_index, uint8_t* d_codes,
+                                           const uint8_t* d_witness256, uint8_t* d_w,
+                                           uint8_t* d_pub, uint8_t* d_merkle32) {
+    if (!g || !d_witness256 || !d_w || !d_pub || !d_merkle32) return fail(ACEGPU_EINVAL, "null argument");
+    if (n == 0 || n > g->d.T) return fail(ACEGPU_EINVAL, "g16 block inputs: need 1 <= n <= T");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    KeytabScope kts(c);
+    if (d_codes) RET(kts.build(s, d_revs, n_revs, d_atts + 64));
+    TreeResult t;
+    uint8_t* pub;
+    RET(g16_chunk_inputs(c, s, g, d_payloads, d_offs, d_atts, n, n, d_revs, d_rev_index, d_codes,
+                         d_merkle32, &pub, &t));
+    CK(cudaMemcpyAsync(d_pub, pub, 32ull * g->d.T, cudaMemcpyDeviceToDevice, s));
+    bn::g16_gather32(d_witness256, 256, n, g->d.T, d_w, s);
+    CKL();
+    c->launches++;
+    return ACEGPU_OK;
+}
+
+// This rank's partial proof points (A | B1 | B2 | L | H, 384 B, affine
+// Montgomery) over its slice of the bases; every rank computes the same
+// witness, r, s and H polynomial.
+extern "C" int acegpu_g16_prove_partial_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                            const uint8_t* d_w, const uint8_t* d_pub,
+                                            uint8_t* d_part384) {
+    if (!g || !d_w || !d_pub || !d_part384) return fail(ACEGPU_EINVAL, "null argument");
+    if (g->r1cs) return fail(ACEGPU_EINVAL, "g16 partial: synthetic-circuit keys only");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    return g16_prove_locked(c, pick(c, stream), g, d_w, d_pub, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, d_part384);
+}
+
+// Sum the `world` partial records (in rank order), then s A, r B1, C and the
+// proof (EIP-197 256 B), raw points, chunk digest and/or the chunk root
+// (289-B tree leaf: proof | digest | kind Tx) — for the proof whose partial
+// this key computed last.
+extern "C" int acegpu_g16_finish_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                     const uint8_t* d_parts, uint32_t world, uint8_t* d_proof256,
+                                     uint8_t* d_raw256, uint8_t* d_digest32, uint8_t* d_root289) {
+    if (!g || !d_parts || world == 0) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    acegpu_g16::Slot& sl = g->slot[g->cur];
+    CK(cudaStreamWaitEvent(s, sl.done, 0));
+    uint8_t* proof;
+    RET(ws(c, kIn2, 256 + 32 + 320, &proof));
+    bn::g16_sum_parts(d_parts, world, sl.pts, s);
+    bn::g16_scale(sl.pts, sl.rs, sl.scaled, s);
+    bn::g16_assemble(sl.pts, sl.scaled, proof, d_raw256, s);
+    CKL();
+    if (d_proof256) CK(cudaMemcpyAsync(d_proof256, proof, 256, cudaMemcpyDeviceToDevice, s));
+    if (d_digest32) CK(cudaMemcpyAsync(d_digest32, sl.digest, 32, cudaMemcpyDeviceToDevice, s));
+    if (d_root289) {
+        uint8_t* node = proof + 288;
+        bn::g16_chunk_node(proof, sl.digest, node, s);
+        launch_pack_nodes(node, 1, d_root289, s);
+        CKL();
+    }
+    CK(cudaEventRecord(sl.done, s));
+    c->launches += 5;
+    return ACEGPU_OK;
 }
 
 extern "C" int acegpu_g16_prove_block(acegpu_ctx* c, acegpu_g16* g, const uint8_t* payloads,

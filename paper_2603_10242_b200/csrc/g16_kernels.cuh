@@ -57,6 +57,8 @@ void g16_extras(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V, uint64_t Vp, 
 void g16_scale(const uint8_t* pts, const uint8_t* rs, uint8_t* out, cudaStream_t s);
 void g16_assemble(const uint8_t* pts, const uint8_t* scaled, uint8_t* proof, uint8_t* raw,
                   cudaStream_t s);
+// Split keys: pts (A | B1 | B2 | L | H, 384 B) = the sum of `world` partial records.
+void g16_sum_parts(const uint8_t* parts, uint32_t world, uint8_t* pts, cudaStream_t s);
 // Block glue.
 void g16_gather32(const uint8_t* src, uint64_t stride, uint64_t n, uint64_t n_pad, uint8_t* dst,
                   cudaStream_t s);

@@ -410,6 +410,45 @@ __global__ void scale_kernel(const uint8_t* pts, const uint8_t* rs, uint8_t* out
     store<FqCfg>(o + 96, acc.ZZZ);
 }
 
+// Split proving keys (acegpu_g16_setup_slice): the MSM points of `world`
+// ranks' base slices, records A | B1 | B2 (128 B) | L | H of 384 B each
+// (affine Montgomery, all-zero = infinity), summed into pts. Thread k sums
+// point k (k = 2: the G2 point).
+template <class F>
+__device__ void sum_affine(const uint8_t* parts, uint32_t world, int off, uint8_t* out) {
+    constexpr int E = felem_bytes<F>();
+    XYZZ<F> acc = XYZZ<F>::inf();
+    for (uint32_t r = 0; r < world; ++r) {
+        F x, y;
+        fload(x, parts + 384ull * r + off);
+        fload(y, parts + 384ull * r + off + E);
+        if (!(fzero(x) && fzero(y))) acc = xyzz_madd(acc, x, y);
+    }
+    F x, y;
+    fset_zero(x);
+    fset_zero(y);
+    if (!acc.is_inf()) {
+        const F zz = fmul(acc.ZZ, acc.ZZZ);
+        F t;
+        if constexpr (E == 32) {
+            t = inv_fast(zz);
+        } else {
+            const Fq nrm = add(fmul(zz.c0, zz.c0), fmul(zz.c1, zz.c1));
+            const Fq ni = inv_fast(nrm);
+            t = {fmul(zz.c0, ni), neg(fmul(zz.c1, ni))};
+        }
+        x = fmul(acc.X, fmul(t, acc.ZZZ));
+        y = fmul(acc.Y, fmul(t, acc.ZZ));
+    }
+    fstore(out + off, x);
+    fstore(out + off + E, y);
+}
+__global__ void sum_parts_kernel(const uint8_t* parts, uint32_t world, uint8_t* pts) {
+    const int k = threadIdx.x;
+    if (k == 2) sum_affine<Fq2>(parts, world, 128, pts);
+    else if (k < 5) sum_affine<Fq>(parts, world, k == 0 ? 0 : k == 1 ? 64 : k == 3 ? 256 : 320, pts);
+}
+
 __device__ __forceinline__ void put_be(uint8_t* o, const Fq& a) {
     const Fq s = from_mont(a);
     for (int i = 0; i < 32; ++i) o[i] = (uint8_t)(s.v[7 - i / 4] >> (8 * (3 - i % 4)));
@@ -607,6 +646,9 @@ void g16_scale(const uint8_t* pts, const uint8_t* rs, uint8_t* out, cudaStream_t
 void g16_assemble(const uint8_t* pts, const uint8_t* scaled, uint8_t* proof, uint8_t* raw,
                   cudaStream_t s) {
     assemble_kernel<<<1, 1, 0, s>>>(pts, scaled, proof, raw);
+}
+void g16_sum_parts(const uint8_t* parts, uint32_t world, uint8_t* pts, cudaStream_t s) {
+    sum_parts_kernel<<<1, 32, 0, s>>>(parts, world, pts);
 }
 
 }  // namespace bn

@@ -186,6 +186,59 @@ def prove_sharded(local: DeviceBlock, n_total: int, rank: int, world: int,
     return out + (roots,) if return_roots else out
 
 
+def one_proof_partial(local_full: DeviceBlock, pk, codes=None):
+    """One rank's part of ONE Groth16 proof for the whole block (block-size
+    key, T >= n; a split key holds the rank's slice of the bases): the
+    block's inputs (verdicts, Merkle root, w, pub — every rank holds the whole
+    block) and the rank's partial points -> (part384, merkle32) device tensors."""
+    import torch
+    db = local_full
+    dev = db.atts.device
+    w = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
+    pub = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
+    merk = torch.empty(32, dtype=torch.uint8, device=dev)
+    part = torch.empty(384, dtype=torch.uint8, device=dev)
+    sp = _stream()
+    pk.ctx.call("acegpu_g16_block_inputs_dev", sp, pk.h, _ptr(db.payloads), _ptr(db.offs),
+                _ptr(db.atts), db.n, _ptr(db.revs),
+                0 if db.revs is None else db.revs.numel() // 32, _ptr(db.rev_index),
+                _ptr(codes), _ptr(db.witnesses), _ptr(w), _ptr(pub), _ptr(merk))
+    pk.ctx.call("acegpu_g16_prove_partial_dev", sp, pk.h, _ptr(w), _ptr(pub), _ptr(part))
+    return part, merk
+
+
+def one_proof_finish(parts, world: int, merk, n_total: int, header, pk):
+    """Sum the ranks' partial points (world x 384 B, rank order) into the
+    block's proof -> (proof289, fc328) via the reference's tree rule over the
+    one root."""
+    import torch
+    root = torch.empty(289, dtype=torch.uint8, device=merk.device)
+    pk.ctx.call("acegpu_g16_finish_dev", _stream(), pk.h, _ptr(parts), world, None, None, None,
+                _ptr(root))
+    return GpuBackend(pk.ctx).combine(root, merk, 1, n_total, header)
+
+
+def prove_one_proof(local_full: DeviceBlock, n_total: int, rank: int, world: int, pk,
+                    group=None, codes=None):
+    """ONE Groth16 proof for the whole block across `world` ranks (DIZK-style
+    split of the MSMs: every rank computes the witness and the H polynomial,
+    then the MSMs over its slice of the bases; one all-gather of 384-B partial
+    records; every rank sums them in rank order and returns the same
+    (proof289, fc328))."""
+    import torch
+    import torch.distributed as dist
+    part, merk = one_proof_partial(local_full, pk, codes)
+    if world > 1:
+        dev = part.device
+        src = part.cpu() if dist.get_backend(group) == "gloo" else part
+        out = [torch.empty_like(src) for _ in range(world)]
+        dist.all_gather(out, src, group=group)
+        parts = torch.cat(out).to(dev)
+    else:
+        parts = part
+    return one_proof_finish(parts, world, merk, n_total, local_full.header, pk)
+
+
 def prove_sharded_single_process(fb, world: int, log2_chunk: int, ctx=None, pk=None,
                                  witnesses=None, return_roots: bool = False):
     """Emulates `world` ranks one after another on one GPU (no collective):

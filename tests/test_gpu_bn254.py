@@ -125,15 +125,17 @@ def test_ntt_large_roundtrip_and_oracle(ctx, logn):
     assert np.array_equal(cos, orig)
 
 
-def test_ntt_2_28_sparse_evaluations_and_roundtrip(ctx):
-    """The 2^28 domain of a whole 100k-tx block (8.6 GB per vector, device
-    resident): a sparse input's forward and coset-forward transforms checked
-    at sampled outputs against X[k] = sum_i x_i (g^c w^k)^i evaluated here,
-    and iNTT(NTT(x)) = x on dense random data."""
+@pytest.mark.parametrize("logn", [25, 26, 27, 28])
+def test_ntt_block_domains_sparse_evaluations_and_roundtrip(ctx, logn):
+    """Block-size domains up to 2^28 (a whole 100k-tx block: 8.6 GB per
+    vector, device resident; each size has its own three-pass split): a
+    sparse input's forward and coset-forward transforms checked at sampled
+    outputs against X[k] = sum_i x_i (g^c w^k)^i evaluated here, and
+    iNTT(NTT(x)) = x on dense random data."""
     import torch
-    logn, n = 28, 1 << 28
+    n = 1 << logn
     dev = torch.device("cuda:0")
-    rng = random.Random(28)
+    rng = random.Random(logn)
     w = pow(5, (R - 1) >> logn, R)
     pos = sorted(rng.sample(range(n), 64))
     val = [rng.randrange(R) for _ in pos]

@@ -17,6 +17,7 @@ pytestmark = pytest.mark.gpu
 
 WORLD = 2
 T, K = 4, 3
+T1 = 40  # a block-size key for the one-proof mode (not a power of two)
 TRAP = [3, 5, 7, 11, 13]
 
 
@@ -78,6 +79,18 @@ def _rank(rank, port, out_dir, n_mock, n_g16):
         res["g16_proof"] = p.cpu().numpy().tobytes()
         res["g16_bad"] = int((codes[:c] != 0).sum().item())
         pk.close()
+        # one proof for the whole block: split keys (this rank's slice of the
+        # bases), every rank holds the whole block, one all-gather of partials
+        sk = groth16.ProvingKey(T1, K, _trap(), ctx, rank=rank, world=WORLD)
+        db = shard.DeviceBlock.upload(wfb, 0, n_g16, np.frombuffer(fb.revs, np.uint8).copy(),
+                                      np.asarray(fb.rev_index, np.uint32), device=0)
+        db.witnesses = torch.from_numpy(_witnesses(fb, n_g16)).cuda()
+        codes = torch.full((n_g16,), 0xEE, dtype=torch.uint8, device="cuda:0")
+        p, f = shard.prove_one_proof(db, n_g16, rank, WORLD, sk, codes=codes)
+        res["one_fc"] = f.cpu().numpy().tobytes()
+        res["one_proof"] = p.cpu().numpy().tobytes()
+        res["one_bad"] = int((codes != 0).sum().item())
+        sk.close()
         np.save(os.path.join(out_dir, f"rank{rank}.npy"), res, allow_pickle=True)
     finally:
         dist.destroy_process_group()
@@ -109,3 +122,11 @@ def test_two_process_sharded_prove_on_one_gpu(tmp_path):
         pk.close()
     for r in res:
         assert r["g16_proof"] == proof and r["g16_fc"] == fc
+    # one proof per block: both ranks == the whole-key prove_block
+    bk = groth16.ProvingKey(T1, K, _trap(), ctx)
+    try:
+        _, p1, fc1, _ = bk.prove_block(wfb, _witnesses(fb, n_g16))
+    finally:
+        bk.close()
+    for r in res:
+        assert r["one_proof"] == p1 and r["one_fc"] == fc1 and r["one_bad"] == 0

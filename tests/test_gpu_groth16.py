@@ -572,3 +572,53 @@ def test_single_proof_per_block(ctx, n, monkeypatch):
                                               np.frombuffer(fb.header, np.uint8).copy()), wit)
         finally:
             pk.close()
+
+
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_one_proof_split_keys_match_whole_key(ctx, world):
+    """One proof per block across ranks (DIZK-style MSM split), the ranks
+    emulated one after another: each split key holds its slice of the bases
+    (same trapdoor), each rank's partial points summed in rank order give the
+    whole key's proof and FC; world = 1 through the same partial/finish calls
+    with a whole key gives prove_block's bytes. A split key refuses the
+    whole-proof entry points."""
+    import torch
+    from paper_2603_10242_b200 import groth16, prover, shard, wire
+    T, K, n = 45, 5, 37
+    rng = random.Random(world)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    fb = O.multi_user_block(n, 3)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+    wit = _witnesses(fb, n)
+    whole = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        _, p_ref, fc_ref, cps = whole.prove_block(wfb, wit)
+        revs = np.frombuffer(fb.revs, np.uint8).copy()
+        rix = np.asarray(fb.rev_index, np.uint32)
+        db = shard.DeviceBlock.upload(wfb, 0, n, revs, rix, device=0)
+        db.witnesses = torch.from_numpy(wit).cuda()
+        if world == 1:
+            p, f = shard.prove_one_proof(db, n, 0, 1, whole)
+            assert p.cpu().numpy().tobytes() == p_ref and f.cpu().numpy().tobytes() == fc_ref
+            return
+        keys = [groth16.ProvingKey(T, K, trap, ctx, rank=r, world=world) for r in range(world)]
+        try:
+            parts, merks = [], []
+            for k in keys:
+                codes = torch.full((n,), 0xEE, dtype=torch.uint8, device="cuda:0")
+                part, merk = shard.one_proof_partial(db, k, codes)
+                assert int((codes != 0).sum().item()) == 0
+                parts.append(part)
+                merks.append(merk)
+            allp = torch.cat(parts)
+            for k, merk in zip(keys, merks):
+                p, f = shard.one_proof_finish(allp, world, merk, n, db.header, k)
+                assert p.cpu().numpy().tobytes() == p_ref and f.cpu().numpy().tobytes() == fc_ref
+            assert whole.verify_finality_certificate(fc_ref, wfb, cps) == prover.FcCheck.Valid
+            with pytest.raises(ValueError):
+                keys[0].prove_block(wfb, wit)
+        finally:
+            for k in keys:
+                k.close()
+    finally:
+        whole.close()
