@@ -452,6 +452,7 @@ def run_ours(args, rank: int, world: int) -> None:
             g16["zkace_hmac"] = bench_zkace_hmac_chunk(ctx, dev, fb, revs, rev_index)
             g16["zkace_block"] = bench_zkace_block(ctx, dev)
             g16["block_proof"] = bench_groth16_single_block(ctx, dev, fb, revs, rev_index)
+            g16["block_proof_split"] = bench_one_proof_split(ctx, dev, fb, revs, rev_index)
         if world == 1 and not args.no_cpu_baseline:
             bn["cpu_oracle"] = bn254_cpu_baseline(msm_in)
 
@@ -536,6 +537,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
         "zkace_hmac_chunk": g16.get("zkace_hmac"), "zkace_block_1024": g16.get("zkace_block"),
         "groth16_one_proof_block_100000": g16.get("block_proof"),
+        "groth16_one_proof_split_rank0": g16.get("block_proof_split"),
         "groth16_stream": g16.get("stream"),
         "groth16_roofline": g16_roof, "bn254": bn,
     }
@@ -937,6 +939,67 @@ def bench_groth16_single_block(ctx, dev: int, fb, revs, rev_index, steps: int = 
     finally:
         pk.close()
         torch.cuda.empty_cache()
+
+
+def bench_one_proof_split(ctx, dev: int, fb, revs, rev_index, worlds=(2, 4, 8),
+                          steps: int = 2) -> dict:
+    """ONE proof for the 100k block split across `world` ranks (split keys,
+    shard.prove_one_proof): rank 0's share — the block's inputs, the witness,
+    the MSMs over 1/world of the bases, the coset evaluations of the H
+    vectors it owns (vector k on rank k mod world: 2 of the 6 2^28 NTTs at
+    world >= 3), then (a b - c)/Z and [h] on its slice, the sum of all ranks'
+    partial records, s A, r B1, C, the tree and the FC — timed with CUDA
+    events on ONE GPU (the other ranks' same-size shares run on their own
+    GPUs). Not included: the slice exchange (3 x 2^28 x 32 B / world received
+    per rank) and the all-gather of world x 384 B. Stand-ins: the slices of
+    vectors rank 0 does not own are its own buffers' bytes (same sizes; the
+    proof itself is checked by tests/test_gpu_groth16.py)."""
+    import torch
+    from paper_2603_10242_b200 import groth16, shard
+    n = fb.n
+    wit = make_witnesses(fb, revs, rev_index, ctx)
+    db = shard.DeviceBlock.upload(fb, 0, n, revs, rev_index, device=dev)
+    db.witnesses = torch.from_numpy(wit).to(f"cuda:{dev}")
+    codes = torch.zeros(n, dtype=torch.uint8, device=f"cuda:{dev}")
+    s = torch.cuda.current_stream()
+    out = {}
+    for world in worlds:
+        torch.cuda.empty_cache()
+        t0 = time.perf_counter()
+        pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx, rank=0, world=world)
+        setup_s = time.perf_counter() - t0
+        N = 1 << pk.log_domain
+        lo, hi = shard.slice_bounds(N, 0, world)
+        try:
+            def step():
+                own, merk = shard.one_proof_phase1(db, pk, 0, world, codes)
+                sl = torch.cat([own[32 * lo:32 * hi]] * 3)  # a | b | c slice stand-ins
+                del own
+                part = shard.one_proof_phase2(sl, pk)
+                parts = part.repeat(world)  # stand-in for the gathered records
+                return shard.one_proof_finish(parts, world, merk, n, db.header, pk)
+            step()
+            torch.cuda.synchronize()
+            ts = []
+            for _ in range(steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(s)
+                step()
+                b.record(s)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            free, total = torch.cuda.mem_get_info(dev)
+            out[str(world)] = {"rank0_ms": statistics.mean(ts), "rank0_ms_per_step": ts,
+                               "rank0_owned_vectors": bin(shard.owned_mask(0, world)).count("1"),
+                               "setup_s_rank0": setup_s,
+                               "device_mem_gb_rank0": (total - free) / 1e9,
+                               "exchange_bytes_in_per_rank": 3 * 32 * (hi - lo)}
+        finally:
+            pk.close()
+    out["note"] = ("rank 0's share of ONE proof for the 100k block split over `world` GPUs, "
+                   "measured alone on one B200; not included: the slice exchange and the "
+                   "all-gather of world x 384 B")
+    return out
 
 
 def bench_zkace_block(ctx, dev: int, n: int = 1024, steps: int = 3) -> dict:

@@ -406,6 +406,18 @@ int acegpu_g16_block_inputs_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                 uint8_t* d_merkle32);
 int acegpu_g16_prove_partial_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                  const uint8_t* d_w, const uint8_t* d_pub, uint8_t* d_part384);
+/* Owner split of the H polynomial (>= 2 ranks; the witness's NTTs are 6 of
+ * 2^28 points at 100k txs, too much to repeat on every rank): phase1_dev =
+ * witness, r, s, the A / B1 / B2 / L slice MSMs (left running) and the coset
+ * evaluations of the owned vectors (mask a = 1, b = 2, c = 4; vector k is
+ * owned by rank k mod world) into d_own (N x 32 B each, a, b, c order); the
+ * caller scatters slice r = [N r / world, N (r + 1) / world) of every vector
+ * to rank r; phase2_dev = (a b - c) / Z and [h] over the rank's slice
+ * (d_slices = a | b | c slices, overwritten) -> the 384-B partial record. */
+int acegpu_g16_prove_phase1_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_w,
+                                const uint8_t* d_pub, int owned, uint8_t* d_own);
+int acegpu_g16_prove_phase2_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, uint8_t* d_slices,
+                                uint8_t* d_part384);
 int acegpu_g16_finish_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_parts,
                           uint32_t world, uint8_t* d_proof256, uint8_t* d_raw256,
                           uint8_t* d_digest32, uint8_t* d_root289);

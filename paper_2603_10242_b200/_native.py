@@ -81,6 +81,8 @@ _SIGS = {
     "acegpu_g16_block_inputs_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, vp, u64, vp,
                                               vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_partial_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp]),
+    "acegpu_g16_prove_phase1_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, C.c_int, vp]),
+    "acegpu_g16_prove_phase2_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),
     "acegpu_g16_finish_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, C.c_uint32, vp, vp, vp, vp]),
     "acegpu_bn_msm_run": (C.c_int, [ctxp, C.c_void_p, vp, vp]),
     "acegpu_bn_msm_run_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp]),

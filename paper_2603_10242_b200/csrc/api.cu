@@ -2491,7 +2491,8 @@ namespace {
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr,
-                     const uint8_t* d_z = nullptr, uint8_t* d_part384 = nullptr);
+                     const uint8_t* d_z = nullptr, uint8_t* d_part384 = nullptr,
+                     int owned = 7, uint8_t* d_own = nullptr);
 }
 
 // General R1CS: prove from the full assignment z (vars x 32-B standard form,
@@ -2570,8 +2571,8 @@ G16Trace g_g16_trace;
 int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t* d_w,
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready,
-                     const uint8_t* d_z, uint8_t* d_part384) {
-    if (g->world > 1 && !d_part384)
+                     const uint8_t* d_z, uint8_t* d_part384, int owned, uint8_t* d_own) {
+    if (g->world > 1 && !d_part384 && !d_own)
         return fail(ACEGPU_EINVAL, "g16: a split key proves partials (acegpu_g16_prove_partial_dev)");
     if (!g->r1cs != !d_z)
         return fail(ACEGPU_EINVAL, g->r1cs ? "g16: an R1CS key proves full assignments "
@@ -2627,17 +2628,36 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
     cudaStream_t sh = g->s_h, sn = g->s_n;
     CK(cudaStreamWaitEvent(sn, g->ev_z, 0));
+    if (d_own) {
+        // phase 1 of the owner split: only the owned vectors' coset
+        // evaluations (a = bit 0, b = 1, c = 2), copied out for the exchange;
+        // the pointwise step and [h] follow in phase 2 on each rank's slice
+        int k = 0, idx = 0;
+        for (uint8_t* e : {g->ea, g->eb, g->ec}) {
+            if ((owned >> k++) & 1) {
+                if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn) ||
+                    bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn))
+                    return fail(ACEGPU_ECUDA, "g16 ntt");
+                CK(cudaMemcpyAsync(d_own + 32 * N * idx++, e, 32 * N, cudaMemcpyDeviceToDevice, sn));
+            }
+        }
+        CKL();
+        CK(cudaEventRecord(g->ev_n, sn));
+    }
     for (uint8_t* e : {g->ea, g->eb, g->ec}) {
+        if (d_own) break;
         if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn)) return fail(ACEGPU_ECUDA, "g16 intt");
         if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
     }
-    bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
+    if (!d_own) bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
     // H(g w^j) are the MSM scalars as they stand (Lagrange-coset H bases): no
     // coset iNTT back to coefficients
-    bn::launch_fr_convert(g->ea, N, 0, sn);  // -> standard form scalars
+    if (!d_own) {
+        bn::launch_fr_convert(g->ea, N, 0, sn);  // -> standard form scalars
+        CK(cudaEventRecord(g->ev_n, sn));
+    }
     tr.mark("ntt", sn);
     CKL();
-    CK(cudaEventRecord(g->ev_n, sn));
     CK(cudaStreamWaitEvent(sh, g->ev_n, 0));
     // (n: the full array's length; a split key's bases cover [lo, lo + b->n))
     auto msm = [](const acegpu_msm_bases* b, uint64_t n, const uint8_t* sc, bn::MsmScratch& scr,
@@ -2647,7 +2667,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                                       b->vb_sub)
                      : bn::msm_run(b->group, b->table, n, sc, scr, out, st);
     };
-    if (msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
+    if (!d_own && msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
@@ -2668,6 +2688,11 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
+    if (d_own) {  // phase 1 done: the owned evaluations are ready on s
+        CK(cudaStreamWaitEvent(s, g->ev_n, 0));
+        c->launches += 12 + 4 * bn::kMsmKernels;
+        return ACEGPU_OK;
+    }
     if (d_part384) {
         // this rank's partial points A | B1 | B2 | L | H; the sum over ranks,
         // s A, r B1 and the assembly follow in acegpu_g16_finish_dev
@@ -2839,6 +2864,57 @@ extern "C" int acegpu_g16_prove_partial_dev(acegpu_ctx* c, void* stream, acegpu_
     DeviceGuard guard(c->device);
     return g16_prove_locked(c, pick(c, stream), g, d_w, d_pub, nullptr, nullptr, nullptr, nullptr,
                             nullptr, nullptr, d_part384);
+}
+
+// Owner split of the H polynomial (one proof per block across >= 2 ranks):
+// phase 1 = the witness, r, s, the A / B1 / B2 / L MSMs of this rank's slices
+// (left running) and the coset evaluations of the OWNED vectors (mask: a = 1,
+// b = 2, c = 4; vector k owned by rank k mod world) into d_own (one N x 32-B
+// Montgomery vector each, in a, b, c order); after the caller's exchange,
+// phase 2 takes this rank's slice [N rank / world, N (rank + 1) / world) of
+// a, b, c (d_slices: a | b | c, S x 32 B each, overwritten), the pointwise
+// (a b - c) / Z, [h] over the slice, and writes the partial record.
+extern "C" int acegpu_g16_prove_phase1_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                           const uint8_t* d_w, const uint8_t* d_pub, int owned,
+                                           uint8_t* d_own) {
+    if (!g || !d_w || !d_pub || (owned && !d_own)) return fail(ACEGPU_EINVAL, "null argument");
+    if (g->r1cs) return fail(ACEGPU_EINVAL, "g16 partial: synthetic-circuit keys only");
+    if (owned < 0 || owned > 7) return fail(ACEGPU_EINVAL, "g16 phase 1: owned mask in 0..7");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    uint8_t dummy_own = 0;
+    return g16_prove_locked(c, pick(c, stream), g, d_w, d_pub, nullptr, nullptr, nullptr, nullptr,
+                            nullptr, nullptr, nullptr, owned, d_own ? d_own : &dummy_own);
+}
+
+extern "C" int acegpu_g16_prove_phase2_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
+                                           uint8_t* d_slices, uint8_t* d_part384) {
+    if (!g || !d_slices || !d_part384) return fail(ACEGPU_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard guard(c->device);
+    cudaStream_t s = pick(c, stream);
+    acegpu_g16::Slot& sl = g->slot[g->cur];
+    const acegpu_msm_bases* qh = g->qh;
+    if (!qh->vb) return fail(ACEGPU_EINVAL, "g16 phase 2: variable-base keys only");
+    const uint64_t S = qh->n;
+    cudaStream_t sh = g->s_h;
+    CK(cudaEventRecord(g->ev_in, s));  // the exchanged slices are ready on s
+    CK(cudaStreamWaitEvent(sh, g->ev_in, 0));
+    if (S) {
+        bn::g16_pointwise(d_slices, d_slices + 32 * S, d_slices + 64 * S, g->consts, S, sh);
+        bn::launch_fr_convert(d_slices, S, 0, sh);
+        if (bn::msm_run_vb(1, qh->table, S, d_slices, g->msm_h, sl.pts + 320, sh, qh->vb_sub))
+            return fail(ACEGPU_ECUDA, "g16 msm H");
+    } else {
+        CK(cudaMemsetAsync(sl.pts + 320, 0, 64, sh));
+    }
+    CKL();
+    CK(cudaEventRecord(g->ev_h, sh));
+    for (cudaEvent_t e : {g->ev_ab, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
+    CK(cudaMemcpyAsync(d_part384, sl.pts, 384, cudaMemcpyDeviceToDevice, s));
+    CK(cudaEventRecord(sl.done, s));
+    c->launches += 2 + bn::kMsmKernels;
+    return ACEGPU_OK;
 }
 
 // Sum the `world` partial records (in rank order), then s A, r B1, C and the

@@ -207,6 +207,73 @@ def one_proof_partial(local_full: DeviceBlock, pk, codes=None):
     return part, merk
 
 
+def owned_mask(rank: int, world: int) -> int:
+    """H-polynomial vectors a, b, c (bits 0..2) owned by `rank`: k mod world."""
+    return sum(1 << k for k in range(3) if k % world == rank)
+
+
+def slice_bounds(N: int, rank: int, world: int) -> tuple[int, int]:
+    return N * rank // world, N * (rank + 1) // world
+
+
+def one_proof_phase1(local_full: DeviceBlock, pk, rank: int, world: int, codes=None):
+    """Owner split, phase 1: inputs + witness + this rank's A/B1/B2/L slice
+    MSMs (running) + the coset evaluations of its owned vectors ->
+    (own (k x N x 32 B), merkle32)."""
+    import torch
+    db = local_full
+    dev = db.atts.device
+    N = 1 << pk.log_domain
+    mask = owned_mask(rank, world)
+    w = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
+    pub = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
+    merk = torch.empty(32, dtype=torch.uint8, device=dev)
+    own = torch.empty(max(bin(mask).count("1"), 1) * 32 * N, dtype=torch.uint8, device=dev)
+    sp = _stream()
+    pk.ctx.call("acegpu_g16_block_inputs_dev", sp, pk.h, _ptr(db.payloads), _ptr(db.offs),
+                _ptr(db.atts), db.n, _ptr(db.revs),
+                0 if db.revs is None else db.revs.numel() // 32, _ptr(db.rev_index),
+                _ptr(codes), _ptr(db.witnesses), _ptr(w), _ptr(pub), _ptr(merk))
+    pk.ctx.call("acegpu_g16_prove_phase1_dev", sp, pk.h, _ptr(w), _ptr(pub), mask, _ptr(own))
+    return own, merk
+
+
+def one_proof_phase2(slices, pk):
+    """Owner split, phase 2: this rank's a | b | c slices -> partial record."""
+    import torch
+    part = torch.empty(384, dtype=torch.uint8, device=slices.device)
+    pk.ctx.call("acegpu_g16_prove_phase2_dev", _stream(), pk.h, _ptr(slices), _ptr(part))
+    return part
+
+
+def exchange_slices(own, rank: int, world: int, N: int, group=None):
+    """Every owner scatters slice r of each of its vectors to rank r -> this
+    rank's a | b | c slices (S x 32 B each)."""
+    import torch
+    import torch.distributed as dist
+    lo, hi = slice_bounds(N, rank, world)
+    S = hi - lo
+    dev = own.device
+    gloo = dist.get_backend(group) == "gloo"
+    out = torch.empty(3 * 32 * S, dtype=torch.uint8, device=dev)
+    idx = 0
+    for k in range(3):
+        o = k % world
+        dst = torch.empty(32 * S, dtype=torch.uint8, device="cpu" if gloo else dev)
+        lst = None
+        if rank == o:
+            vec = own[32 * N * idx:32 * N * (idx + 1)]
+            idx += 1
+            lst = []
+            for r in range(world):
+                a, b = slice_bounds(N, r, world)
+                t = vec[32 * a:32 * b]
+                lst.append(t.cpu() if gloo else t)
+        dist.scatter(dst, lst, src=o, group=group)
+        out[32 * S * k:32 * S * (k + 1)] = dst.to(dev)
+    return out
+
+
 def one_proof_finish(parts, world: int, merk, n_total: int, header, pk):
     """Sum the ranks' partial points (world x 384 B, rank order) into the
     block's proof -> (proof289, fc328) via the reference's tree rule over the
@@ -221,13 +288,23 @@ def one_proof_finish(parts, world: int, merk, n_total: int, header, pk):
 def prove_one_proof(local_full: DeviceBlock, n_total: int, rank: int, world: int, pk,
                     group=None, codes=None):
     """ONE Groth16 proof for the whole block across `world` ranks (DIZK-style
-    split of the MSMs: every rank computes the witness and the H polynomial,
-    then the MSMs over its slice of the bases; one all-gather of 384-B partial
+    split): every rank computes the witness and the MSMs over its slice of the
+    bases; the H polynomial's vectors a, b, c are transformed by their owners
+    (rank k mod world) and scattered by slices, so each rank forms
+    (a b - c) / Z and [h] on its slice only; one all-gather of 384-B partial
     records; every rank sums them in rank order and returns the same
-    (proof289, fc328))."""
+    (proof289, fc328)."""
     import torch
     import torch.distributed as dist
-    part, merk = one_proof_partial(local_full, pk, codes)
+    if world > 1:
+        # the H polynomial's three vectors are computed by their owners and
+        # exchanged by slices (each rank then does 2 of the 6 NTTs, not 6)
+        own, merk = one_proof_phase1(local_full, pk, rank, world, codes)
+        slices = exchange_slices(own, rank, world, 1 << pk.log_domain, group)
+        del own
+        part = one_proof_phase2(slices, pk)
+    else:
+        part, merk = one_proof_partial(local_full, pk, codes)
     if world > 1:
         dev = part.device
         src = part.cpu() if dist.get_backend(group) == "gloo" else part

@@ -622,3 +622,55 @@ def test_one_proof_split_keys_match_whole_key(ctx, world):
                 k.close()
     finally:
         whole.close()
+
+
+@pytest.mark.parametrize("world", [2, 3, 5])
+def test_one_proof_owner_split_matches_whole_key(ctx, world):
+    """The owner split of the H polynomial (phase 1: each rank transforms the
+    vectors it owns, k mod world; the slices exchanged; phase 2: (a b - c)/Z
+    and [h] on the rank's slice), ranks emulated one after another with the
+    exchange done here: the summed partials give the whole key's proof and
+    FC (world = 5: ranks 3, 4 own no vector)."""
+    import torch
+    from paper_2603_10242_b200 import groth16, shard, wire
+    T, K, n = 45, 5, 37
+    rng = random.Random(10 + world)
+    trap = arr([rng.randrange(1, R) for _ in range(5)])
+    fb = O.multi_user_block(n, 3)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+    wit = _witnesses(fb, n)
+    whole = groth16.ProvingKey(T, K, trap, ctx)
+    try:
+        _, p_ref, fc_ref, _ = whole.prove_block(wfb, wit)
+    finally:
+        whole.close()
+    db = shard.DeviceBlock.upload(wfb, 0, n, np.frombuffer(fb.revs, np.uint8).copy(),
+                                  np.asarray(fb.rev_index, np.uint32), device=0)
+    db.witnesses = torch.from_numpy(wit).cuda()
+    keys = [groth16.ProvingKey(T, K, trap, ctx, rank=r, world=world) for r in range(world)]
+    try:
+        N = 1 << keys[0].log_domain
+        owns, merks = [], []
+        for r, k in enumerate(keys):
+            own, merk = shard.one_proof_phase1(db, k, r, world)
+            owns.append(own)
+            merks.append(merk)
+        vec = {}
+        for r in range(world):
+            idx = 0
+            for v in range(3):
+                if v % world == r:
+                    vec[v] = owns[r][32 * N * idx:32 * N * (idx + 1)]
+                    idx += 1
+        parts = []
+        for r, k in enumerate(keys):
+            lo, hi = shard.slice_bounds(N, r, world)
+            sl = torch.cat([vec[v][32 * lo:32 * hi] for v in range(3)]).contiguous()
+            parts.append(shard.one_proof_phase2(sl, k))
+        allp = torch.cat(parts)
+        for k, merk in zip(keys, merks):
+            p, f = shard.one_proof_finish(allp, world, merk, n, db.header, k)
+            assert p.cpu().numpy().tobytes() == p_ref and f.cpu().numpy().tobytes() == fc_ref
+    finally:
+        for k in keys:
+            k.close()
