@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <array>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -2127,14 +2128,25 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     bn::g16_setup_consts(g->consts, g->logn, s);
     if (K) bn::g16_chain_consts(K, g->cc, s);
     // query scalars
-    uint8_t *L, *su, *sv, *sl, *part, *hs, *gens, *ext, *pts, *icsc;
+    uint8_t *L = nullptr, *su = nullptr, *sv = nullptr, *sl = nullptr, *part = nullptr,
+            *hs = nullptr, *gens = nullptr, *ext = nullptr, *pts = nullptr, *icsc = nullptr,
+            *tab1 = nullptr, *tab2 = nullptr, *ex2 = nullptr;
+    // setup temporaries: freed on every exit (after the stream drains)
+    struct Temps {
+        std::array<uint8_t**, 13> ps;
+        cudaStream_t s;
+        ~Temps() {
+            cudaStreamSynchronize(s);
+            for (uint8_t** p : ps)
+                if (*p) cudaFree(*p);
+        }
+    } temps{{&L, &su, &sv, &sl, &part, &hs, &gens, &ext, &pts, &icsc, &tab1, &tab2, &ex2}, s};
     // pts: the bases before their window tables (fixed base), the u, v, w
     // column sums (general R1CS) and the verifying-key export
     uint64_t pts_bytes = 448 + 64 * (uint64_t(T) + 1);
     if (r) pts_bytes = std::max<uint64_t>(pts_bytes, 96 * V);
     pts_bytes = std::max<uint64_t>(pts_bytes, 32 * bn::kCombEntries);
     if (!g->vb) pts_bytes = std::max<uint64_t>(pts_bytes, 128 * (std::max(V, N) + 2));
-    uint8_t *tab1, *tab2;
     if (dm(&L, 32 * m) || dm(&su, 32 * V) || dm(&sv, 32 * V) || dm(&sl, 32 * g->Vp) ||
         dm(&part, 256 * 64) || dm(&hs, 32 * N) || dm(&gens, 256) || dm(&ext, 512) ||
         dm(&pts, pts_bytes) || dm(&icsc, 32ull * (T + 1)) ||
@@ -2167,7 +2179,6 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     bn::launch_points_convert(2, gens + 64, 1, 1, s);
     uint8_t* ex1 = ext;  // 3 G1 points: alpha1, beta1, delta1 (192 B) -> then G2 below
     bn::launch_scalar_muls(1, gens, ext + 256, 3, ex1, s);
-    uint8_t* ex2;
     if (dm(&ex2, 256)) return fail(ACEGPU_ECUDA, "g16 setup alloc");
     bn::launch_scalar_muls(2, gens + 64, ext + 256 + 32, 2, ex2, s);  // beta2, delta2
     CKL();
@@ -2236,7 +2247,6 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     bn::g16_vk_digest(pts, uint32_t(448 + 64 * (T + 1)), g->vk_digest, s);
     CKL();
     CK(cudaStreamSynchronize(s));
-    for (uint8_t* p : {L, su, sv, sl, part, hs, gens, ext, pts, ex2, icsc, tab1, tab2}) cudaFree(p);
     if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s)) return fail(ACEGPU_ECUDA, "g16 NTT tables");
     CK(cudaStreamSynchronize(s));
     c->launches += 20;
@@ -2492,7 +2502,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready = nullptr,
                      const uint8_t* d_z = nullptr, uint8_t* d_part384 = nullptr,
-                     int owned = 7, uint8_t* d_own = nullptr);
+                     int owned = -1, uint8_t* d_own = nullptr);
 }
 
 // General R1CS: prove from the full assignment z (vars x 32-B standard form,
@@ -2572,7 +2582,8 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                      const uint8_t* d_pub, const uint8_t* d_rs, uint8_t* d_proof256,
                      uint8_t* d_raw256, uint8_t* d_digest32, cudaEvent_t inputs_ready,
                      const uint8_t* d_z, uint8_t* d_part384, int owned, uint8_t* d_own) {
-    if (g->world > 1 && !d_part384 && !d_own)
+    const bool phase1 = owned >= 0;  // owner split, phase 1 (acegpu_g16_prove_phase1_dev)
+    if (g->world > 1 && !d_part384 && !phase1)
         return fail(ACEGPU_EINVAL, "g16: a split key proves partials (acegpu_g16_prove_partial_dev)");
     if (!g->r1cs != !d_z)
         return fail(ACEGPU_EINVAL, g->r1cs ? "g16: an R1CS key proves full assignments "
@@ -2628,7 +2639,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
     cudaStream_t sh = g->s_h, sn = g->s_n;
     CK(cudaStreamWaitEvent(sn, g->ev_z, 0));
-    if (d_own) {
+    if (phase1) {
         // phase 1 of the owner split: only the owned vectors' coset
         // evaluations (a = bit 0, b = 1, c = 2), copied out for the exchange;
         // the pointwise step and [h] follow in phase 2 on each rank's slice
@@ -2645,14 +2656,14 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         CK(cudaEventRecord(g->ev_n, sn));
     }
     for (uint8_t* e : {g->ea, g->eb, g->ec}) {
-        if (d_own) break;
+        if (phase1) break;
         if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn)) return fail(ACEGPU_ECUDA, "g16 intt");
         if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
     }
-    if (!d_own) bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
+    if (!phase1) bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
     // H(g w^j) are the MSM scalars as they stand (Lagrange-coset H bases): no
     // coset iNTT back to coefficients
-    if (!d_own) {
+    if (!phase1) {
         bn::launch_fr_convert(g->ea, N, 0, sn);  // -> standard form scalars
         CK(cudaEventRecord(g->ev_n, sn));
     }
@@ -2667,7 +2678,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                                       b->vb_sub)
                      : bn::msm_run(b->group, b->table, n, sc, scr, out, st);
     };
-    if (!d_own && msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
+    if (!phase1 && msm(g->qh, N, g->ea, g->msm_h, g->pts + 320, sh))
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
@@ -2688,7 +2699,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm A/B1");
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
-    if (d_own) {  // phase 1 done: the owned evaluations are ready on s
+    if (phase1) {  // phase 1 done: the owned evaluations are ready on s
         CK(cudaStreamWaitEvent(s, g->ev_n, 0));
         c->launches += 12 + 4 * bn::kMsmKernels;
         return ACEGPU_OK;
@@ -2882,9 +2893,8 @@ extern "C" int acegpu_g16_prove_phase1_dev(acegpu_ctx* c, void* stream, acegpu_g
     if (owned < 0 || owned > 7) return fail(ACEGPU_EINVAL, "g16 phase 1: owned mask in 0..7");
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
-    uint8_t dummy_own = 0;
     return g16_prove_locked(c, pick(c, stream), g, d_w, d_pub, nullptr, nullptr, nullptr, nullptr,
-                            nullptr, nullptr, nullptr, owned, d_own ? d_own : &dummy_own);
+                            nullptr, nullptr, nullptr, owned, d_own);
 }
 
 extern "C" int acegpu_g16_prove_phase2_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
