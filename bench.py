@@ -537,7 +537,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
         "zkace_hmac_chunk": g16.get("zkace_hmac"), "zkace_block_1024": g16.get("zkace_block"),
         "groth16_one_proof_block_100000": g16.get("block_proof"),
-        "groth16_one_proof_split_rank0": g16.get("block_proof_split"),
+        "groth16_one_proof_split_ranks": g16.get("block_proof_split"),
         "groth16_stream": g16.get("stream"),
         "groth16_roofline": g16_roof, "bn254": bn,
     }
@@ -941,7 +941,7 @@ def bench_groth16_single_block(ctx, dev: int, fb, revs, rev_index, steps: int = 
         torch.cuda.empty_cache()
 
 
-def bench_one_proof_split(ctx, dev: int, fb, revs, rev_index, worlds=(2, 4, 8),
+def bench_one_proof_split(ctx, dev: int, fb, revs, rev_index, worlds=(4, 8),
                           steps: int = 2) -> dict:
     """ONE proof for the 100k block split across `world` ranks (split keys,
     shard.prove_one_proof): rank 0's share — the block's inputs, the witness,
@@ -964,39 +964,50 @@ def bench_one_proof_split(ctx, dev: int, fb, revs, rev_index, worlds=(2, 4, 8),
     s = torch.cuda.current_stream()
     out = {}
     for world in worlds:
-        torch.cuda.empty_cache()
-        t0 = time.perf_counter()
-        pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx, rank=0, world=world)
-        setup_s = time.perf_counter() - t0
-        N = 1 << pk.log_domain
-        lo, hi = shard.slice_bounds(N, 0, world)
-        try:
-            def step():
-                own, merk = shard.one_proof_phase1(db, pk, 0, world, codes)
-                sl = torch.cat([own[32 * lo:32 * hi]] * 3)  # a | b | c slice stand-ins
-                del own
-                part = shard.one_proof_phase2(sl, pk)
-                parts = part.repeat(world)  # stand-in for the gathered records
-                return shard.one_proof_finish(parts, world, merk, n, db.header, pk)
-            step()
-            torch.cuda.synchronize()
-            ts = []
-            for _ in range(steps):
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(s)
+        shares = shard.balanced_shares(world)
+        res = {"shares": shares}
+        # the slowest ranks: an owner of one H vector (rank 0) and a rank that
+        # owns none (the largest MSM share, rank world - 1)
+        for rank in sorted({0, world - 1}):
+            torch.cuda.empty_cache()
+            t0 = time.perf_counter()
+            pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx, rank=rank, world=world,
+                                    shares=shares)
+            setup_s = time.perf_counter() - t0
+            N = 1 << pk.log_domain
+            lo, hi = shard.slice_bounds(N, rank, world, shares)
+            try:
+                def step():
+                    own, merk = shard.one_proof_phase1(db, pk, rank, world, codes)
+                    src = own if own.numel() >= 32 * N else torch.zeros(32 * N, dtype=torch.uint8,
+                                                                       device=own.device)
+                    sl = torch.cat([src[32 * lo:32 * hi]] * 3)  # a | b | c slice stand-ins
+                    del own, src
+                    part = shard.one_proof_phase2(sl, pk)
+                    parts = part.repeat(world)  # stand-in for the gathered records
+                    return shard.one_proof_finish(parts, world, merk, n, db.header, pk)
                 step()
-                b.record(s)
                 torch.cuda.synchronize()
-                ts.append(a.elapsed_time(b))
-            free, total = torch.cuda.mem_get_info(dev)
-            out[str(world)] = {"rank0_ms": statistics.mean(ts), "rank0_ms_per_step": ts,
-                               "rank0_owned_vectors": bin(shard.owned_mask(0, world)).count("1"),
-                               "setup_s_rank0": setup_s,
-                               "device_mem_gb_rank0": (total - free) / 1e9,
-                               "exchange_bytes_in_per_rank": 3 * 32 * (hi - lo)}
-        finally:
-            pk.close()
-    out["note"] = ("rank 0's share of ONE proof for the 100k block split over `world` GPUs, "
+                ts = []
+                for _ in range(steps):
+                    a, b = (torch.cuda.Event(enable_timing=True),
+                            torch.cuda.Event(enable_timing=True))
+                    a.record(s)
+                    step()
+                    b.record(s)
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(b))
+                free, total = torch.cuda.mem_get_info(dev)
+                res[f"rank{rank}"] = {"ms": statistics.mean(ts), "ms_per_step": ts,
+                                      "owned_vectors": bin(shard.owned_mask(rank, world)).count("1"),
+                                      "setup_s": setup_s, "device_mem_gb": (total - free) / 1e9,
+                                      "exchange_bytes_in": 3 * 32 * (hi - lo)}
+            finally:
+                pk.close()
+        res["slowest_rank_ms"] = max(v["ms"] for k, v in res.items() if k.startswith("rank"))
+        out[str(world)] = res
+    out["note"] = ("ONE proof for the 100k block split over `world` GPUs (balanced shares): "
+                   "rank 0 (owns an H vector) and rank world-1 (largest base share) each "
                    "measured alone on one B200; not included: the slice exchange and the "
                    "all-gather of world x 384 B")
     return out

@@ -388,7 +388,9 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
  * setup_slice: the key of rank `rank` of `world` — the same CRS as
  * acegpu_g16_setup (same trapdoor), but only the rank's slice of every base
  * array (A, B1, B2, L, H) is stored (variable-base form); the verifying key is
- * whole. Each rank: block_inputs_dev (verdicts, Merkle root, w, pub for a
+ * whole. Slice r of an array of t bases is [t P_r / S, t (P_r + shares[r]) / S)
+ * with P_r = shares[0] + .. + shares[r-1], S = the sum (shares NULL = equal),
+ * so ranks that also transform H vectors can take fewer bases. Each rank: block_inputs_dev (verdicts, Merkle root, w, pub for a
  * block of n <= T txs; every rank holds the whole block), prove_partial_dev
  * (its partial A | B1 | B2 | L | H, 384 B — the witness and the H
  * polynomial are computed on every rank), an all-gather of the 384-B
@@ -397,7 +399,8 @@ int acegpu_g16_shard_roots_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
  * gives the same bytes as acegpu_g16_prove_block. Replaces prover.cpp:129-142
  * in one-proof mode. */
 int acegpu_g16_setup_slice(acegpu_ctx* ctx, uint32_t T, uint32_t K, const uint8_t* trapdoor5,
-                           uint32_t rank, uint32_t world, acegpu_g16** out);
+                           uint32_t rank, uint32_t world, const uint32_t* shares,
+                           acegpu_g16** out);
 int acegpu_g16_block_inputs_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
                                 const uint8_t* d_payloads, const uint64_t* d_offs,
                                 const uint8_t* d_atts, uint64_t n, const uint8_t* d_revs,
@@ -411,8 +414,8 @@ int acegpu_g16_prove_partial_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g,
  * witness, r, s, the A / B1 / B2 / L slice MSMs (left running) and the coset
  * evaluations of the owned vectors (mask a = 1, b = 2, c = 4; vector k is
  * owned by rank k mod world) into d_own (N x 32 B each, a, b, c order); the
- * caller scatters slice r = [N r / world, N (r + 1) / world) of every vector
- * to rank r; phase2_dev = (a b - c) / Z and [h] over the rank's slice
+ * caller scatters slice r of every vector (the H array's share bounds, as
+ * setup_slice) to rank r; phase2_dev = (a b - c) / Z and [h] over the rank's slice
  * (d_slices = a | b | c slices, overwritten) -> the 384-B partial record. */
 int acegpu_g16_prove_phase1_dev(acegpu_ctx* ctx, void* stream, acegpu_g16* g, const uint8_t* d_w,
                                 const uint8_t* d_pub, int owned, uint8_t* d_own);

@@ -77,7 +77,7 @@ _SIGS = {
                                            C.POINTER(C.c_void_p)]),
     "acegpu_bn_msm_free": (None, [C.c_void_p]),
     "acegpu_g16_setup_slice": (C.c_int, [ctxp, C.c_uint32, C.c_uint32, vp, C.c_uint32, C.c_uint32,
-                                         C.POINTER(C.c_void_p)]),
+                                         vp, C.POINTER(C.c_void_p)]),
     "acegpu_g16_block_inputs_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, u64, vp, u64, vp,
                                               vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_partial_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp]),

@@ -2054,7 +2054,7 @@ namespace {
 // x K constraints) or a general R1CS r (T = its public inputs, K = 0).
 int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
                    const uint8_t* trapdoor5, acegpu_g16** out, uint32_t rank = 0,
-                   uint32_t world = 1) {
+                   uint32_t world = 1, const uint32_t* shares = nullptr) {
     cudaStream_t s = c->stream;
     auto* g = new acegpu_g16();
     std::unique_ptr<acegpu_g16, void (*)(acegpu_g16*)> own(g, acegpu_g16_free);
@@ -2190,8 +2190,18 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     auto bases = [&](int group, const uint8_t* scal, uint64_t cnt,
                      std::initializer_list<const uint8_t*> extra, acegpu_msm_bases** out) -> int {
         const uint64_t pb = 64ull * group, total = cnt + extra.size();
-        // a split key holds the slice [lo, hi) of the array (the extras last)
-        const uint64_t lo = total * rank / world, hi = total * (rank + 1) / world;
+        // a split key holds the slice [lo, hi) of the array (the extras last):
+        // rank r's share of the bases is shares[r] / sum(shares) (equal if null)
+        uint64_t pre = rank, sum = world;
+        if (shares) {
+            pre = sum = 0;
+            for (uint32_t j = 0; j < world; ++j) {
+                if (j < rank) pre += shares[j];
+                sum += shares[j];
+            }
+        }
+        const uint64_t lo = total * pre / sum,
+                       hi = total * (pre + (shares ? shares[rank] : 1)) / sum;
         uint8_t* dst = pts;
         std::unique_ptr<acegpu_msm_bases, void (*)(acegpu_msm_bases*)> b(nullptr,
                                                                           acegpu_bn_msm_free);
@@ -2276,13 +2286,18 @@ extern "C" int acegpu_g16_setup_r1cs(acegpu_ctx* c, const acegpu_r1cs* r, const 
 
 extern "C" int acegpu_g16_setup_slice(acegpu_ctx* c, uint32_t T, uint32_t K,
                                       const uint8_t* trapdoor5, uint32_t rank, uint32_t world,
-                                      acegpu_g16** out) {
+                                      const uint32_t* shares, acegpu_g16** out) {
     if (T < 1 || K < 2) return fail(ACEGPU_EINVAL, "g16: need T >= 1 and K >= 2");
     if (!trapdoor5 || !out) return fail(ACEGPU_EINVAL, "null argument");
     if (world < 1 || rank >= world) return fail(ACEGPU_EINVAL, "g16: need rank < world");
+    if (shares) {
+        uint64_t sum = 0;
+        for (uint32_t j = 0; j < world; ++j) sum += shares[j];
+        if (sum == 0 || sum > (1u << 20)) return fail(ACEGPU_EINVAL, "g16: shares sum in 1..2^20");
+    }
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
-    return g16_setup_impl(c, T, K, nullptr, trapdoor5, out, rank, world);
+    return g16_setup_impl(c, T, K, nullptr, trapdoor5, out, rank, world, shares);
 }
 
 // ---- witness programs (GPU witness generation for bit circuits) ---------------
@@ -2883,7 +2898,8 @@ extern "C" int acegpu_g16_prove_partial_dev(acegpu_ctx* c, void* stream, acegpu_
 // b = 2, c = 4; vector k owned by rank k mod world) into d_own (one N x 32-B
 // Montgomery vector each, in a, b, c order); after the caller's exchange,
 // phase 2 takes this rank's slice [N rank / world, N (rank + 1) / world) of
-// a, b, c (d_slices: a | b | c, S x 32 B each, overwritten), the pointwise
+// a, b, c — the same share-weighted bounds as the key's H slice — (d_slices:
+// a | b | c, S x 32 B each, overwritten), the pointwise
 // (a b - c) / Z, [h] over the slice, and writes the partial record.
 extern "C" int acegpu_g16_prove_phase1_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
                                            const uint8_t* d_w, const uint8_t* d_pub, int owned,

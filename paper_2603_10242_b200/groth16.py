@@ -29,17 +29,20 @@ def deterministic_trapdoor(label: bytes = b"ace-g16-setup-v1", ctx=None) -> np.n
 
 class ProvingKey:
     def __init__(self, T: int, K: int, trapdoor: np.ndarray | None = None, ctx=None,
-                 rank: int = 0, world: int = 1):
+                 rank: int = 0, world: int = 1, shares=None):
         """world > 1: rank `rank`'s split key for one proof per block across
-        ranks (acegpu_g16_setup_slice): its slice of the bases, the whole
+        ranks (acegpu_g16_setup_slice): its slice of the bases (rank r gets
+        shares[r] / sum(shares) of each array; None = equal), the whole
         verifying key; prove with shard.prove_one_proof."""
         self.ctx = ctx or N.context()
         self.T, self.K = T, K
         self.rank, self.world = rank, world
+        self.shares = None if shares is None else np.ascontiguousarray(shares, np.uint32)
         self.trapdoor = deterministic_trapdoor(ctx=self.ctx) if trapdoor is None else trapdoor
         h = C.c_void_p()
         if world > 1:
-            self.ctx.call("acegpu_g16_setup_slice", T, K, self.trapdoor, rank, world, C.byref(h))
+            self.ctx.call("acegpu_g16_setup_slice", T, K, self.trapdoor, rank, world, self.shares,
+                          C.byref(h))
         else:
             self.ctx.call("acegpu_g16_setup", T, K, self.trapdoor, C.byref(h))
         self.h = h
@@ -54,7 +57,7 @@ class ProvingKey:
         self = cls.__new__(cls)
         self.ctx = ctx or r1cs.ctx
         self.T, self.K, self.r1cs = r1cs.n_pub, 0, r1cs
-        self.rank, self.world = 0, 1
+        self.rank, self.world, self.shares = 0, 1, None
         self.trapdoor = deterministic_trapdoor(ctx=self.ctx) if trapdoor is None else trapdoor
         h = C.c_void_p()
         self.ctx.call("acegpu_g16_setup_r1cs", r1cs.h, self.trapdoor, C.byref(h))

@@ -212,8 +212,28 @@ def owned_mask(rank: int, world: int) -> int:
     return sum(1 << k for k in range(3) if k % world == rank)
 
 
-def slice_bounds(N: int, rank: int, world: int) -> tuple[int, int]:
-    return N * rank // world, N * (rank + 1) // world
+def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
+    """Rank `rank`'s slice of an N-entry array (acegpu_g16_setup_slice's rule)."""
+    if shares is None:
+        return N * rank // world, N * (rank + 1) // world
+    sh = [int(x) for x in shares]
+    pre, tot = sum(sh[:rank]), sum(sh)
+    return N * pre // tot, N * (pre + sh[rank]) // tot
+
+
+def balanced_shares(world: int, ntt_frac: float = 0.115, unit: int = 1000) -> list[int]:
+    """Shares of the bases that even out the ranks when vector k of the H
+    polynomial is transformed on rank k mod world: an owned vector (its iNTT
+    + coset NTT, run concurrently with the rank's MSMs) costs ~ntt_frac of
+    the whole proof's MSM work — fitted at 100k txs, 8 ranks, from an owner
+    rank (share 81/1000: 587 ms) and a non-owner (151/1000: 454 ms): ~330 ms
+    per owned vector vs ~2.8 s of MSM work in all — so owners take fewer
+    bases."""
+    own = [bin(owned_mask(r, world)).count("1") for r in range(world)]
+    t = (1.0 + ntt_frac * sum(own)) / world  # per-rank budget, MSM-work units
+    w = [max(t - ntt_frac * o, 0.01) for o in own]
+    tot = sum(w)
+    return [max(1, round(unit * x / tot)) for x in w]
 
 
 def one_proof_phase1(local_full: DeviceBlock, pk, rank: int, world: int, codes=None):
@@ -246,12 +266,13 @@ def one_proof_phase2(slices, pk):
     return part
 
 
-def exchange_slices(own, rank: int, world: int, N: int, group=None):
-    """Every owner scatters slice r of each of its vectors to rank r -> this
-    rank's a | b | c slices (S x 32 B each)."""
+def exchange_slices(own, rank: int, world: int, N: int, group=None, shares=None):
+    """Every owner sends slice r of each of its vectors to rank r (the key's
+    share bounds) -> this rank's a | b | c slices (S x 32 B each). Equal
+    shares: one scatter per vector; weighted: point-to-point sends."""
     import torch
     import torch.distributed as dist
-    lo, hi = slice_bounds(N, rank, world)
+    lo, hi = slice_bounds(N, rank, world, shares)
     S = hi - lo
     dev = own.device
     gloo = dist.get_backend(group) == "gloo"
@@ -260,16 +281,32 @@ def exchange_slices(own, rank: int, world: int, N: int, group=None):
     for k in range(3):
         o = k % world
         dst = torch.empty(32 * S, dtype=torch.uint8, device="cpu" if gloo else dev)
-        lst = None
+        vec = None
         if rank == o:
             vec = own[32 * N * idx:32 * N * (idx + 1)]
             idx += 1
-            lst = []
+        if shares is None:
+            lst = None
+            if rank == o:
+                lst = []
+                for r in range(world):
+                    a, b = slice_bounds(N, r, world)
+                    t = vec[32 * a:32 * b]
+                    lst.append(t.cpu() if gloo else t)
+            dist.scatter(dst, lst, src=o, group=group)
+        elif rank == o:
+            reqs = []
             for r in range(world):
-                a, b = slice_bounds(N, r, world)
+                a, b = slice_bounds(N, r, world, shares)
                 t = vec[32 * a:32 * b]
-                lst.append(t.cpu() if gloo else t)
-        dist.scatter(dst, lst, src=o, group=group)
+                if r == rank:
+                    dst.copy_(t)
+                else:
+                    reqs.append(dist.isend(t.cpu() if gloo else t.contiguous(), r, group=group))
+            for q in reqs:
+                q.wait()
+        else:
+            dist.recv(dst, o, group=group)
         out[32 * S * k:32 * S * (k + 1)] = dst.to(dev)
     return out
 
@@ -300,7 +337,7 @@ def prove_one_proof(local_full: DeviceBlock, n_total: int, rank: int, world: int
         # the H polynomial's three vectors are computed by their owners and
         # exchanged by slices (each rank then does 2 of the 6 NTTs, not 6)
         own, merk = one_proof_phase1(local_full, pk, rank, world, codes)
-        slices = exchange_slices(own, rank, world, 1 << pk.log_domain, group)
+        slices = exchange_slices(own, rank, world, 1 << pk.log_domain, group, pk.shares)
         del own
         part = one_proof_phase2(slices, pk)
     else:

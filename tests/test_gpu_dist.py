@@ -81,7 +81,7 @@ def _rank(rank, port, out_dir, n_mock, n_g16):
         pk.close()
         # one proof for the whole block: split keys (this rank's slice of the
         # bases), every rank holds the whole block, one all-gather of partials
-        sk = groth16.ProvingKey(T1, K, _trap(), ctx, rank=rank, world=WORLD)
+        sk = groth16.ProvingKey(T1, K, _trap(), ctx, rank=rank, world=WORLD, shares=[3, 5])
         db = shard.DeviceBlock.upload(wfb, 0, n_g16, np.frombuffer(fb.revs, np.uint8).copy(),
                                       np.asarray(fb.rev_index, np.uint32), device=0)
         db.witnesses = torch.from_numpy(_witnesses(fb, n_g16)).cuda()

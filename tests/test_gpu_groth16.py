@@ -624,13 +624,15 @@ def test_one_proof_split_keys_match_whole_key(ctx, world):
         whole.close()
 
 
-@pytest.mark.parametrize("world", [2, 3, 5])
-def test_one_proof_owner_split_matches_whole_key(ctx, world):
+@pytest.mark.parametrize("world,shares", [(2, None), (3, None), (5, None), (3, [1, 5, 2]),
+                                          (4, "balanced")])
+def test_one_proof_owner_split_matches_whole_key(ctx, world, shares):
     """The owner split of the H polynomial (phase 1: each rank transforms the
     vectors it owns, k mod world; the slices exchanged; phase 2: (a b - c)/Z
     and [h] on the rank's slice), ranks emulated one after another with the
     exchange done here: the summed partials give the whole key's proof and
-    FC (world = 5: ranks 3, 4 own no vector)."""
+    FC (world = 5: ranks 3, 4 own no vector; weighted shares: uneven slices
+    of every base array and of H)."""
     import torch
     from paper_2603_10242_b200 import groth16, shard, wire
     T, K, n = 45, 5, 37
@@ -647,7 +649,10 @@ def test_one_proof_owner_split_matches_whole_key(ctx, world):
     db = shard.DeviceBlock.upload(wfb, 0, n, np.frombuffer(fb.revs, np.uint8).copy(),
                                   np.asarray(fb.rev_index, np.uint32), device=0)
     db.witnesses = torch.from_numpy(wit).cuda()
-    keys = [groth16.ProvingKey(T, K, trap, ctx, rank=r, world=world) for r in range(world)]
+    if shares == "balanced":
+        shares = shard.balanced_shares(world)
+    keys = [groth16.ProvingKey(T, K, trap, ctx, rank=r, world=world, shares=shares)
+            for r in range(world)]
     try:
         N = 1 << keys[0].log_domain
         owns, merks = [], []
@@ -664,7 +669,7 @@ def test_one_proof_owner_split_matches_whole_key(ctx, world):
                     idx += 1
         parts = []
         for r, k in enumerate(keys):
-            lo, hi = shard.slice_bounds(N, r, world)
+            lo, hi = shard.slice_bounds(N, r, world, shares)
             sl = torch.cat([vec[v][32 * lo:32 * hi] for v in range(3)]).contiguous()
             parts.append(shard.one_proof_phase2(sl, k))
         allp = torch.cat(parts)
