@@ -195,3 +195,58 @@ def test_light_check_counters_accumulate():
     c += pipeline.LightCheckCounters(1, 1, 1)
     assert (c.sha256_ops, c.registry_probes, c.window_checks) == (4, 3, 2)
     assert pipeline.to_string(pipeline.LightCheck.StaleDomain) == "StaleDomain"
+
+
+def _exchange_worker(rank, world, port, N, shares, q):
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2603_10242_b200 import shard
+        # vector k (32-B elements, byte pattern (k, index)) lives on its owner
+        vecs = []
+        for k in range(3):
+            v = torch.zeros(N, 32, dtype=torch.uint8)
+            v[:, 0] = k + 1
+            v[:, 1] = torch.arange(N) % 251
+            v[:, 2] = torch.arange(N) // 251
+            vecs.append(v.reshape(-1))
+        own = [vecs[k] for k in range(3) if k % world == rank]
+        own = torch.cat(own) if own else torch.zeros(32, dtype=torch.uint8)
+        out = shard.exchange_slices(own, rank, world, N, shares=shares)
+        q.put((rank, out.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,shares", [(2, None), (2, [3, 5]), (3, [1, 4, 2])])
+def test_one_proof_slice_exchange_gloo(world, shares):
+    """The one-proof-per-block exchange (shard.exchange_slices): every owner
+    of an H vector (k mod world) sends each rank its share-bounded slice —
+    scatter for equal shares, point-to-point sends for weighted ones — and
+    every rank ends with the a | b | c slices of its own range."""
+    import multiprocessing as mp
+    import random
+
+    import numpy as np
+    from paper_2603_10242_b200 import shard
+    N = 1000
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = random.randrange(20000, 40000)
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, N, shares, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for r in range(world):
+        lo, hi = shard.slice_bounds(N, r, world, shares)
+        got = np.frombuffer(res[r], np.uint8).reshape(3, hi - lo, 32)
+        for k in range(3):
+            idx = np.arange(lo, hi)
+            assert (got[k, :, 0] == k + 1).all()
+            assert (got[k, :, 1] == idx % 251).all() and (got[k, :, 2] == idx // 251).all()
