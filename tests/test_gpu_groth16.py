@@ -679,3 +679,34 @@ def test_one_proof_owner_split_matches_whole_key(ctx, world, shares):
     finally:
         for k in keys:
             k.close()
+
+
+def test_one_proof_entry_points_reject_bad_arguments(ctx):
+    """The split-key / one-proof entry points fail loudly (EINVAL ->
+    ValueError): rank >= world, empty shares, a block larger than the key,
+    an owned mask beyond a|b|c, a whole-proof call on a split key."""
+    import torch
+    from paper_2603_10242_b200 import _native as N, groth16, shard, wire
+    trap = arr([3, 5, 7, 11, 13])
+    h = C.c_void_p()
+    with pytest.raises(ValueError):
+        ctx.call("acegpu_g16_setup_slice", 8, 3, trap, 2, 2, None, C.byref(h))
+    with pytest.raises(ValueError):
+        ctx.call("acegpu_g16_setup_slice", 8, 3, trap, 0, 2, np.zeros(2, np.uint32), C.byref(h))
+    pk = groth16.ProvingKey(8, 3, trap, ctx, rank=0, world=2)
+    try:
+        fb = O.multi_user_block(11, 2)  # 11 txs > T = 8
+        wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+        db = shard.DeviceBlock.upload(wfb, 0, 11, device=0)
+        db.witnesses = torch.zeros(11 * 256, dtype=torch.uint8, device="cuda:0")
+        with pytest.raises(ValueError):
+            shard.one_proof_partial(db, pk)
+        w = torch.zeros(8 * 32, dtype=torch.uint8, device="cuda:0")
+        own = torch.zeros(3 * 32 * (1 << pk.log_domain), dtype=torch.uint8, device="cuda:0")
+        with pytest.raises(ValueError):
+            ctx.call("acegpu_g16_prove_phase1_dev", None, pk.h, w.data_ptr(), w.data_ptr(), 9,
+                     own.data_ptr())
+        with pytest.raises(ValueError):  # a split key has no whole-proof path
+            pk.prove(arr([1] * 8), arr([2] * 8))
+    finally:
+        pk.close()
