@@ -2305,40 +2305,136 @@ struct acegpu_witprog {
     int device = 0;
     bn::WitProg p;
     uint4* ops = nullptr;
-    uint32_t *addtab = nullptr, *var_slot = nullptr;
+    uint32_t *addtab = nullptr, *emit = nullptr;
     ~acegpu_witprog() {
         DeviceGuard g(device);
-        for (void* q : {(void*)ops, (void*)addtab, (void*)var_slot})
+        for (void* q : {(void*)ops, (void*)addtab, (void*)emit})
             if (q) cudaFree(q);
     }
 };
 
 extern "C" void acegpu_witprog_free(acegpu_witprog* w) { delete w; }
 
+namespace {
+// The builder's slot program -> physical slots by liveness: a slot's
+// physical slot is released after its last read (operands are read before
+// the destination is written, so an op may reuse its operands' slots); a
+// slot never read is released right after it is written. Private variables
+// are emitted by the op producing their slot. Errors: operands read before
+// they are produced, a SUMBIT of an addition other than the latest.
+enum : uint32_t { kWpKey = 1, kWpMsg, kWpAnd, kWpXor, kWpChp, kWpCh, kWpMajp, kWpMaj, kWpAdd,
+                  kWpSumbit };
+int witprog_compile(const uint32_t* ops4, uint64_t n_ops, const uint32_t* addtab,
+                    uint64_t n_addtab, uint32_t n_adds, const uint32_t* var_slot, uint32_t n_vars,
+                    uint32_t n_slots, std::vector<uint32_t>& ops, std::vector<uint32_t>& tab,
+                    std::vector<uint32_t>& emit, uint32_t& n_phys) {
+    constexpr uint32_t kNone = 0xFFFFFFFFu;
+    auto nread = [](uint32_t code) { return code == kWpAnd || code == kWpXor ? 2 : code >= kWpChp && code <= kWpMaj ? 3 : 0; };
+    std::vector<int64_t> last(n_slots, -1);
+    std::vector<uint8_t> made(n_slots, 0);
+    made[0] = made[1] = 1;
+    int64_t latest_add = -1;
+    for (uint64_t i = 0; i < n_ops; ++i) {
+        const uint32_t* o = ops4 + 4 * i;
+        const uint32_t code = o[0] >> 24, dst = o[0] & 0xFFFFFFu;
+        if (code < kWpKey || code > kWpSumbit) return fail(ACEGPU_EINVAL, "witprog: bad opcode");
+        auto use = [&](uint32_t sl) -> int {
+            if (sl >= n_slots || !made[sl]) return fail(ACEGPU_EINVAL, "witprog: operand read before written");
+            last[sl] = int64_t(i);
+            return ACEGPU_OK;
+        };
+        for (int k = 0; k < nread(code); ++k) RET(use(o[1 + k]));
+        if (code == kWpAdd) {
+            if (uint64_t(o[1]) + o[2] > n_addtab) return fail(ACEGPU_EINVAL, "witprog: addtab range");
+            for (uint32_t k = 0; k < o[2]; ++k) RET(use(addtab[o[1] + k]));
+            if (dst >= n_adds) return fail(ACEGPU_EINVAL, "witprog: destination out of range");
+            latest_add = dst;
+            continue;
+        }
+        if (code == kWpSumbit && int64_t(o[1]) != latest_add)
+            return fail(ACEGPU_EINVAL, "witprog: SUMBIT of an addition other than the latest");
+        if (dst < 2 || dst >= n_slots) return fail(ACEGPU_EINVAL, "witprog: destination out of range");
+        made[dst] = 1;
+    }
+    std::vector<uint32_t> var_of(n_slots, kNone);
+    for (uint32_t v = 0; v < n_vars; ++v) {
+        if (var_slot[v] < 2 || var_slot[v] >= n_slots || var_of[var_slot[v]] != kNone)
+            return fail(ACEGPU_EINVAL, "witprog: var slot out of range or shared");
+        var_of[var_slot[v]] = v;
+    }
+    std::vector<uint32_t> phys(n_slots, kNone), freel;
+    phys[0] = 0;
+    phys[1] = 1;
+    n_phys = 2;
+    ops.assign(4 * n_ops, 0);
+    tab.assign(addtab, addtab + n_addtab);
+    emit.assign(n_ops, kNone);
+    uint64_t emitted = 0;
+    for (uint64_t i = 0; i < n_ops; ++i) {
+        const uint32_t* o = ops4 + 4 * i;
+        uint32_t* q = &ops[4 * i];
+        const uint32_t code = o[0] >> 24, dst = o[0] & 0xFFFFFFu;
+        std::copy(o, o + 4, q);
+        std::vector<uint32_t> reads;
+        for (int k = 0; k < nread(code); ++k) {
+            q[1 + k] = phys[o[1 + k]];
+            reads.push_back(o[1 + k]);
+        }
+        if (code == kWpAdd) {
+            for (uint32_t k = 0; k < o[2]; ++k) {
+                tab[o[1] + k] = phys[addtab[o[1] + k]];
+                reads.push_back(addtab[o[1] + k]);
+            }
+        }
+        for (uint32_t sl : reads)  // release operands at their last read (once)
+            if (sl >= 2 && last[sl] == int64_t(i) && phys[sl] != kNone) {
+                freel.push_back(phys[sl]);
+                phys[sl] = kNone;
+            }
+        if (code == kWpAdd) continue;
+        uint32_t p;
+        if (!freel.empty()) {
+            p = freel.back();
+            freel.pop_back();
+        } else {
+            p = n_phys++;
+        }
+        q[0] = code << 24 | p;
+        emit[i] = var_of[dst];
+        if (var_of[dst] != kNone) ++emitted;
+        if (last[dst] < 0) freel.push_back(p);  // never read: only its emit
+        else phys[dst] = p;
+    }
+    if (emitted != n_vars) return fail(ACEGPU_EINVAL, "witprog: a private variable is never produced");
+    if (n_phys > bn::kWitprogMaxPhys) return fail(ACEGPU_EINVAL, "witprog: too many live slots");
+    return ACEGPU_OK;
+}
+}  // namespace
+
 extern "C" int acegpu_witprog_create(acegpu_ctx* c, const uint32_t* ops4, uint64_t n_ops,
                                      const uint32_t* addtab, uint64_t n_addtab, uint32_t n_adds,
                                      const uint32_t* var_slot, uint32_t n_vars, uint32_t n_slots,
                                      acegpu_witprog** out) {
-    if (!ops4 || !var_slot || !out || !n_ops || !n_slots) return fail(ACEGPU_EINVAL, "null argument");
+    if (!ops4 || !var_slot || !out || !n_ops || n_slots < 2) return fail(ACEGPU_EINVAL, "null argument");
     if (n_slots >= (1u << 24)) return fail(ACEGPU_EINVAL, "witprog: too many slots");
-    for (uint64_t i = 0; i < n_ops; ++i)
-        if ((ops4[4 * i] & 0xFFFFFFu) >= (ops4[4 * i] >> 24 == 9 ? n_adds : n_slots))
-            return fail(ACEGPU_EINVAL, "witprog: destination out of range");
-    for (uint32_t i = 0; i < n_vars; ++i)
-        if (var_slot[i] >= n_slots) return fail(ACEGPU_EINVAL, "witprog: var slot out of range");
+    std::vector<uint32_t> ops, tab, emit;
+    uint32_t n_phys = 0;
+    RET(witprog_compile(ops4, n_ops, addtab, n_addtab, n_adds, var_slot, n_vars, n_slots, ops, tab,
+                        emit, n_phys));
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     cudaStream_t s = c->stream;
     std::unique_ptr<acegpu_witprog> w(new acegpu_witprog());
     w->device = c->device;
-    if (cudaMalloc(&w->ops, 16 * n_ops) || cudaMalloc(&w->addtab, 4 * (n_addtab ? n_addtab : 1)) ||
-        cudaMalloc(&w->var_slot, 4 * (n_vars ? n_vars : 1)))
+    if (cudaMalloc(&w->ops, 16 * n_ops) || cudaMalloc(&w->emit, 4 * n_ops) ||
+        cudaMalloc(&w->addtab, 4 * (tab.empty() ? 1 : tab.size())))
         return fail(ACEGPU_ECUDA, "witprog alloc");
-    CK(cudaMemcpyAsync(w->ops, ops4, 16 * n_ops, cudaMemcpyHostToDevice, s));
-    if (n_addtab) CK(cudaMemcpyAsync(w->addtab, addtab, 4 * n_addtab, cudaMemcpyHostToDevice, s));
-    if (n_vars) CK(cudaMemcpyAsync(w->var_slot, var_slot, 4 * n_vars, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(w->ops, ops.data(), 16 * n_ops, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(w->emit, emit.data(), 4 * n_ops, cudaMemcpyHostToDevice, s));
+    if (!tab.empty())
+        CK(cudaMemcpyAsync(w->addtab, tab.data(), 4 * tab.size(), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));
-    w->p = {w->ops, n_ops, w->addtab, w->var_slot, n_slots, n_adds, n_vars};
+    w->p = {w->ops, w->emit, n_ops, w->addtab, n_phys, n_vars};
     *out = w.release();
     return ACEGPU_OK;
 }
@@ -2355,14 +2451,9 @@ extern "C" int acegpu_witprog_run_dev(acegpu_ctx* c, void* stream, const acegpu_
     if (Tc == 0) Tc = T;
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
-    uint8_t* scratch;
-    const size_t sb = (size_t)T * w->p.n_slots, ab = 8ull * T * (w->p.n_adds ? w->p.n_adds : 1);
-    RET(ws(c, kG16Wit, ((sb + 255) & ~size_t(255)) + ab, &scratch));
-    bn::witprog_run(w->p, d_keys, key_stride, d_atts, T, Tc, reinterpret_cast<int8_t*>(scratch),
-                    reinterpret_cast<int64_t*>(scratch + ((sb + 255) & ~size_t(255))), d_z,
-                    pick(c, stream));
+    bn::witprog_run(w->p, d_keys, key_stride, d_atts, T, Tc, d_z, pick(c, stream));
     CKL();
-    c->launches += 3;
+    c->launches += 2;
     return ACEGPU_OK;
 }
 

@@ -8,14 +8,15 @@
 // obj_hash / domain / credential packed as big-endian integers.
 //
 // Program encoding (4 x u32 per op): w0 = opcode << 24 | dst (slot, or the
-// addition's ordinal for ADD), then up to three operands:
+// addition's ordinal for ADD), then up to three operands (the host compiles
+// slots to physical slots by liveness, acegpu_witprog_create):
 //   KEY  i          key bit i (MSB first within each byte)
 //   MSG  i          message bit i of obj_hash || domain
 //   AND  a b        a & b          XOR  a b      a ^ b
 //   CHP  e f g      e (f - g)      CH   e f g    e ? f : g
 //   MAJP a b c      a (b ^ c)      MAJ  a b c    majority
 //   ADD  off cnt K  sum[dst] = sum_k slot[addtab[off + k]] 2^(k mod 32) + K
-//   SUMBIT add k    bit k of sum[add]
+//   SUMBIT add k    bit k of sum[add] (always the latest ADD)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -29,78 +30,94 @@ namespace {
 
 enum : uint32_t { kKey = 1, kMsg, kAnd, kXor, kChp, kCh, kMajp, kMaj, kAdd, kSumbit };
 
-// One thread per transaction walks the whole program in lockstep with its
-// warp; slot s of transaction t lives at slots[s T + t] (interleaved), so a
-// warp's slot reads and writes are one coalesced 32-B access each.
-struct Slots {
-    int8_t* p;
-    uint32_t T;
-    __device__ __forceinline__ int8_t& operator[](uint32_t s) const { return p[(uint64_t)s * T]; }
-};
-__global__ void witprog_kernel(const uint4* __restrict__ ops, uint64_t n_ops,
-                               const uint32_t* __restrict__ addtab, uint32_t n_slots,
-                               uint32_t n_adds, const uint8_t* keys, uint64_t key_stride,
-                               const uint8_t* atts, uint32_t T, int8_t* slots, int64_t* sums) {
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= T) return;
-    const Slots sl{slots + t, T};
-    int64_t* su = sums + (uint64_t)t * n_adds;
-    const uint8_t* key = keys + key_stride * t;
-    const uint8_t* att = atts + 104ull * t;
-    sl[0] = 0;
-    sl[1] = 1;
-    for (uint64_t i = 0; i < n_ops; ++i) {
-        const uint4 op = ops[i];
-        const uint32_t code = op.x >> 24, dst = op.x & 0xFFFFFFu;
-        int v = 0;
-        switch (code) {
-            case kKey: v = (key[op.y >> 3] >> (7 - (op.y & 7))) & 1; break;
-            case kMsg: {
-                const uint32_t byte = op.y >> 3;  // obj_hash (att 0..31) || domain (att 64..71)
-                v = (att[byte < 32 ? byte : 32 + byte] >> (7 - (op.y & 7))) & 1;
-                break;
-            }
-            case kAnd: v = sl[op.y] & sl[op.z]; break;
-            case kXor: v = sl[op.y] ^ sl[op.z]; break;
-            case kChp: v = sl[op.y] * (sl[op.z] - sl[op.w]); break;
-            case kCh: v = sl[op.y] ? sl[op.z] : sl[op.w]; break;
-            case kMajp: v = sl[op.y] * (sl[op.z] ^ sl[op.w]); break;
-            case kMaj: {
-                const int a = sl[op.y], b = sl[op.z], c = sl[op.w];
-                v = (a & b) ^ (a & c) ^ (b & c);
-                break;
-            }
-            case kAdd: {
-                int64_t s = op.w;
-                for (uint32_t k = 0; k < op.z; ++k)
-                    s += (int64_t)sl[addtab[op.y + k]] << (k & 31);
-                su[dst] = s;
-                continue;
-            }
-            case kSumbit: v = (int)((su[op.y] >> op.z) & 1); break;
-            default: break;
-        }
-        sl[dst] = (int8_t)v;
-    }
-}
-
-// Per chunk c of Tc transactions (assignment size 1 + 5 Tc + Tc P, chunks
-// back to back): z_c[1 + 5 Tc + l P + i] = slot[var_slot[i]] of its
-// transaction l (-1 -> r - 1); 32-B little-endian standard form.
-__global__ void witprog_expand_kernel(const int8_t* slots, const uint32_t* var_slot, uint32_t P,
-                                      uint32_t T, uint32_t Tc, uint8_t* z) {
-    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (j >= (uint64_t)T * P) return;
-    const uint64_t t = j / P, i = j - t * P;
-    const uint64_t c = t / Tc, l = t - c * Tc, zc = 1 + 5ull * Tc + (uint64_t)Tc * P;
-    const int v = slots[(uint64_t)var_slot[i] * T + t];
+// One warp per 32 transactions, one lane per transaction: the warp stages
+// 32 ops (+ their emit targets) at a time in shared memory and runs them in
+// lockstep; slot values live in shared memory as [physical slot][lane] bytes
+// (a warp's access to one slot is 32 consecutive bytes, conflict-free); the
+// key bits and the message bytes are staged per lane; the one live 32-bit
+// sum stays in a register. A value that is a private variable is written to
+// the assignment when it is produced (32-B standard form, -1 -> r - 1).
+__device__ __forceinline__ void put_fr_small(uint8_t* o, int v) {
     uint32_t w[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) w[k] = v < 0 ? mod_limb<FrCfg>(k) - (k == 0 ? 1u : 0u) : 0u;
     if (v > 0) w[0] = 1;
-    uint4* o = reinterpret_cast<uint4*>(z + 32ull * (c * zc + 1 + 5ull * Tc + l * P + i));
-    o[0] = make_uint4(w[0], w[1], w[2], w[3]);
-    o[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    uint4* q = reinterpret_cast<uint4*>(o);
+    q[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    q[1] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+
+__global__ void __launch_bounds__(kWitprogTxs) witprog_kernel(
+    const uint4* __restrict__ ops, const uint32_t* __restrict__ emit, uint64_t n_ops,
+    const uint32_t* __restrict__ addtab, uint32_t n_phys, const uint8_t* keys,
+    uint64_t key_stride, const uint8_t* atts, uint32_t T, uint32_t Tc, uint32_t P, uint8_t* z) {
+    constexpr int W = kWitprogTxs;
+    extern __shared__ __align__(16) uint8_t sm[];
+    uint4* opbuf = reinterpret_cast<uint4*>(sm);                 // W ops
+    uint32_t* embuf = reinterpret_cast<uint32_t*>(sm + 16 * W);  // W emit targets
+    uint8_t* keys_s = sm + 20 * W;                               // W x 32 key bytes
+    uint8_t* msg_s = keys_s + 32 * W;                            // W x 40 message bytes
+    int8_t* slots = reinterpret_cast<int8_t*>(msg_s + 40 * W);   // n_phys x W
+    const int lane = threadIdx.x;
+    const uint32_t t = blockIdx.x * W + lane;
+    const bool act = t < T;
+    if (act) {
+        const uint8_t* key = keys + key_stride * t;
+        const uint8_t* att = atts + 104ull * t;
+        for (int k = 0; k < 32; ++k) keys_s[32 * lane + k] = key[k];
+        for (int k = 0; k < 40; ++k) msg_s[40 * lane + k] = att[k < 32 ? k : 32 + k];  // obj_hash | domain
+    }
+    slots[lane] = 0;
+    slots[W + lane] = 1;
+    uint8_t* zt = nullptr;
+    if (act) {
+        const uint64_t c = t / Tc, l = t - c * Tc, zc = 1 + 5ull * Tc + (uint64_t)Tc * P;
+        zt = z + 32ull * (c * zc + 1 + 5ull * Tc + l * P);
+    }
+    __syncwarp();
+    auto S = [&](uint32_t p) -> int { return slots[p * W + lane]; };
+    int64_t sum = 0;
+    for (uint64_t base = 0; base < n_ops; base += W) {
+        const uint32_t cnt = n_ops - base < (uint64_t)W ? uint32_t(n_ops - base) : uint32_t(W);
+        if (lane < cnt) {
+            opbuf[lane] = ops[base + lane];
+            embuf[lane] = emit[base + lane];
+        }
+        __syncwarp();
+        for (uint32_t j = 0; j < cnt; ++j) {
+            const uint4 op = opbuf[j];
+            const uint32_t code = op.x >> 24, dst = op.x & 0xFFFFFFu;
+            int v = 0;
+            switch (code) {
+                case kKey: v = (keys_s[32 * lane + (op.y >> 3)] >> (7 - (op.y & 7))) & 1; break;
+                case kMsg: v = (msg_s[40 * lane + (op.y >> 3)] >> (7 - (op.y & 7))) & 1; break;
+                case kAnd: v = S(op.y) & S(op.z); break;
+                case kXor: v = S(op.y) ^ S(op.z); break;
+                case kChp: v = S(op.y) * (S(op.z) - S(op.w)); break;
+                case kCh: v = S(op.y) ? S(op.z) : S(op.w); break;
+                case kMajp: v = S(op.y) * (S(op.z) ^ S(op.w)); break;
+                case kMaj: {
+                    const int a = S(op.y), b = S(op.z), c = S(op.w);
+                    v = (a & b) ^ (a & c) ^ (b & c);
+                    break;
+                }
+                case kAdd: {
+                    int64_t s = op.w;
+#pragma unroll 8
+                    for (uint32_t k = 0; k < op.z; ++k)
+                        s += (int64_t)S(__ldg(&addtab[op.y + k])) << (k & 31);
+                    sum = s;
+                    continue;
+                }
+                case kSumbit: v = (int)((sum >> op.z) & 1); break;
+                default: break;
+            }
+            slots[dst * W + lane] = (int8_t)v;
+            const uint32_t e = embuf[j];
+            if (e != 0xFFFFFFFFu && act) put_fr_small(zt + 32ull * e, v);
+        }
+        __syncwarp();
+    }
 }
 
 // Per chunk: z_c[0] = ONE and the five public inputs of each transaction:
@@ -132,15 +149,14 @@ inline unsigned grid(uint64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 }  // namespace
 
 void witprog_run(const WitProg& p, const uint8_t* keys, uint64_t key_stride, const uint8_t* atts,
-                 uint32_t T, uint32_t Tc, int8_t* slots, int64_t* sums, uint8_t* z,
-                 cudaStream_t s) {
+                 uint32_t T, uint32_t Tc, uint8_t* z, cudaStream_t s) {
     if (!T) return;
-    witprog_kernel<<<grid(T, 64), 64, 0, s>>>(p.ops, p.n_ops, p.addtab, p.n_slots, p.n_adds, keys,
-                                              key_stride, atts, T, slots, sums);
+    const size_t smem = (20 + 32 + 40) * kWitprogTxs + (size_t)p.n_phys * kWitprogTxs;
+    cudaFuncSetAttribute(witprog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    witprog_kernel<<<grid(T, kWitprogTxs), kWitprogTxs, smem, s>>>(
+        p.ops, p.emit, p.n_ops, p.addtab, p.n_phys, keys, key_stride, atts, T, Tc, p.n_vars, z);
     const uint64_t nch = (T + Tc - 1) / Tc;
     witprog_pub_kernel<<<grid(nch * (1 + 5ull * Tc), 128), 128, 0, s>>>(atts, T, Tc, p.n_vars, z);
-    witprog_expand_kernel<<<grid((uint64_t)T * p.n_vars, 256), 256, 0, s>>>(
-        slots, p.var_slot, p.n_vars, T, Tc, z);
 }
 
 }  // namespace bn
