@@ -2353,6 +2353,10 @@ int witprog_compile(const uint32_t* ops4, uint64_t n_ops, const uint32_t* addtab
         }
         if (code == kWpSumbit && int64_t(o[1]) != latest_add)
             return fail(ACEGPU_EINVAL, "witprog: SUMBIT of an addition other than the latest");
+        // key bits < 256, message bits (obj_hash | domain) < 320, sum bits < 64
+        if ((code == kWpKey && o[1] >= 256) || (code == kWpMsg && o[1] >= 320) ||
+            (code == kWpSumbit && o[2] >= 64))
+            return fail(ACEGPU_EINVAL, "witprog: input bit out of range");
         if (dst < 2 || dst >= n_slots) return fail(ACEGPU_EINVAL, "witprog: destination out of range");
         made[dst] = 1;
     }
