@@ -753,12 +753,12 @@ def chunk_work(pk, ctx) -> dict:
     the 6 NTTs)."""
     from paper_2603_10242_b200 import bn254
     T = pk.T
-    V, Np = pk.variables, 1 << pk.log_domain
+    V, Np = pk.variables, pk.domain
     Vp = V - 1 - T
     W = bn254.msm_params(ctx)[1]
     g1_adds = W * ((V + 2) * 2 + Vp + 1 + Np)  # A, B1, L, H (coset-Lagrange, N points)
     g2_adds = W * (V + 2)                       # B2
-    fr_muls = 6 * ((Np // 2) * pk.log_domain + Np)  # 3 iNTT + 3 coset NTT
+    fr_muls = 6 * ((Np // 2) * (Np - 1).bit_length() + Np)  # 3 iNTT + 3 coset NTT
     return {"g1_mixed_adds": g1_adds, "g2_mixed_adds": g2_adds, "ntt_fr_muls": fr_muls,
             "fq_mul_equivalents": g1_adds * 10 + g2_adds * 30 + fr_muls}
 
@@ -791,7 +791,7 @@ def bench_groth16(ctx, dev: int, fq_rate: float, pk, reps: int = 5) -> dict:
     chunk_ms = statistics.median(a.elapsed_time(b) for a, b in evs)
     wk = chunk_work(pk, ctx)
     return {"txs_per_chunk": T, "constraints_per_tx": pk.K, "constraints": pk.constraints,
-            "domain": 1 << pk.log_domain, "chunk_prove_ms": chunk_ms, "reps": reps,
+            "domain": pk.domain, "chunk_prove_ms": chunk_ms, "reps": reps,
             "work": wk, "frac_of_fq_mul_peak": wk["fq_mul_equivalents"] / (chunk_ms * 1e-3) / fq_rate,
             "note": "synthetic stand-in circuit (oracle/bn254_oracle.h); proofs checked "
                     "bit-exact vs the known-trapdoor oracle in tests/test_gpu_groth16.py"}
@@ -934,7 +934,7 @@ def bench_groth16_single_block(ctx, dev: int, fb, revs, rev_index, steps: int = 
         v = pk.verify_finality_certificate(fc2, wfb, cps)
         vms = (time.perf_counter() - t0) * 1e3
         return {"n_tx": n, "proofs_per_block": 1, "constraints": pk.constraints,
-                "domain_log2": pk.log_domain, "setup_s_once": setup_s,
+                "domain": pk.domain, "setup_s_once": setup_s,
                 "device_mem_gb_after_setup": (total - free) / 1e9,
                 "latency_ms": ms, "latency_ms_per_step": ts, "steps": steps,
                 "proven_tx_per_s": n / (ms * 1e-3), "vs_400ms_interval": ms / 400.0,
@@ -1029,7 +1029,7 @@ def bench_one_proof_split(ctx, dev: int, fb, revs, rev_index, worlds=(4, 8),
             pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx, rank=rank, world=world,
                                     shares=shares)
             setup_s = time.perf_counter() - t0
-            N = 1 << pk.log_domain
+            N = pk.domain
             lo, hi = shard.slice_bounds(N, rank, world, shares)
             try:
                 def step():
@@ -1178,7 +1178,7 @@ def bench_zkace_hmac_chunk(ctx, dev: int, fb, revs, rev_index, reps: int = 3) ->
         proof = out[:256].cpu().numpy().tobytes()
         ok = pk.verify_batch([proof], [z.tobytes()[32:32 * (1 + npub)]])
         return {"txs": T, "constraints_per_tx": per_tx, "constraints": pk.constraints,
-                "variables": V, "domain": 1 << pk.log_domain, "public_inputs": npub,
+                "variables": V, "domain": pk.domain, "public_inputs": npub,
                 "prove_ms": ms, "reps": reps, "proven_tx_per_s": T / (ms * 1e-3),
                 "verifies": bool(ok), "setup_s_once": setup_s,
                 "gpu_witness_program_ms": wgen_ms,

@@ -219,11 +219,16 @@ int acegpu_bn_field_batch(acegpu_ctx* ctx, int field, int op, const uint8_t* a, 
 /* In-place standard <-> Montgomery conversion of n device elements. */
 int acegpu_bn_convert_dev(acegpu_ctx* ctx, void* stream, int field, uint8_t* d_data, uint64_t n,
                           int to_mont);
-/* Fr NTT over 2^logn elements (logn <= 22), natural order in and out:
+/* Fr NTT over 2^logn elements (logn <= 28), natural order in and out:
  * omega = 5^((r-1)/2^logn); inverse scales by n^-1; coset multiplies the
  * input by g^i (g = 5) before the forward transform / the output by g^-i
  * after the inverse. Host version: standard form in place. */
 int acegpu_bn_ntt(acegpu_ctx* ctx, uint8_t* data, uint32_t logn, int inverse, int coset);
+/* Mixed radix: N = 3 * 2^logk points (logk <= 26), same conventions (a
+ * 3-point DFT over three 2^logk NTTs; Groth16 domains of 3 * 2^b points). */
+int acegpu_bn_ntt3(acegpu_ctx* ctx, uint8_t* data, uint32_t logk, int inverse, int coset);
+int acegpu_bn_ntt3_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_in, uint8_t* d_out,
+                       uint32_t logk, int inverse, int coset);
 /* Device version: Montgomery form; d_in may equal d_out. */
 int acegpu_bn_ntt_dev(acegpu_ctx* ctx, void* stream, const uint8_t* d_in, uint8_t* d_out,
                       uint32_t logn, int inverse, int coset);
@@ -274,8 +279,12 @@ typedef struct acegpu_g16 acegpu_g16;
 int acegpu_g16_setup(acegpu_ctx* ctx, uint32_t txs_per_chunk, uint32_t constraints_per_tx,
                      const uint8_t* trapdoor5, acegpu_g16** out);
 void acegpu_g16_free(acegpu_g16* g);
+/* shape: log_domain = log2 of the domain's power-of-two factor; domain: N,
+ * the smallest of 2^a and 3 * 2^b that holds the constraints (mixed-radix
+ * NTTs for 3 * 2^b; env ACEGPU_G16_RADIX3=0 keeps powers of two). */
 int acegpu_g16_shape(const acegpu_g16* g, uint64_t* variables, uint64_t* constraints,
                      uint32_t* log_domain);
+int acegpu_g16_domain(const acegpu_g16* g, uint64_t* N);
 int acegpu_g16_prove_chunk(acegpu_ctx* ctx, acegpu_g16* g, const uint8_t* w, const uint8_t* pub,
                            const uint8_t* rs, uint8_t* proof256, uint8_t* raw256,
                            uint8_t* digest32);

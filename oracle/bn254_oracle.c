@@ -239,6 +239,98 @@ static void fr_root(uint32_t logn, int inverse, fe* w) {
     if (inverse) finv(&FR, w, w);
 }
 
+/* w = 5^((r-1)/N) for N = 2^logk (three = 0) or 3 * 2^logk (three = 1;
+ * r - 1 = 2^28 * 3^2 * ...): the exponent is (r-1) >> logk, then / 3. */
+static void fr_root_n(uint32_t logk, int three, int inverse, fe* w) {
+    fe g;
+    uint8_t five[32] = {5};
+    to_mont(&FR, five, &g);
+    uint64_t e[4];
+    memcpy(e, FR.m, 32);
+    e[0] -= 1;
+    for (uint32_t s = 0; s < logk; ++s)
+        for (int i = 0; i < 4; ++i) e[i] = (e[i] >> 1) | (i < 3 ? e[i + 1] << 63 : 0);
+    if (three) { /* long division by 3 from the top limb */
+        unsigned __int128 rem = 0;
+        for (int i = 3; i >= 0; --i) {
+            unsigned __int128 cur = (rem << 64) | e[i];
+            e[i] = (uint64_t)(cur / 3);
+            rem = cur % 3;
+        }
+    }
+    fpow(&FR, &g, e, w);
+    if (inverse) finv(&FR, w, w);
+}
+
+uint64_t bn_g16_domain(uint64_t m, uint32_t* logk, int* three) {
+    /* the smallest N >= m among 2^a and 3 * 2^b (groth16.cu uses the same rule) */
+    uint32_t a = 0;
+    while ((1ull << a) < m) ++a;
+    uint32_t b = 0;
+    while (3ull << b < m) ++b;
+    if ((3ull << b) < (1ull << a)) {
+        *logk = b;
+        *three = 1;
+        return 3ull << b;
+    }
+    *logk = a;
+    *three = 0;
+    return 1ull << a;
+}
+
+/* O(n^2) DFT of any size n = 2^logk or 3 * 2^logk (coset: inputs times 5^i;
+ * inverse: times n^-1 and, with coset, outputs times 5^-k) — the checker for
+ * mixed-radix NTTs. */
+void bn_dft_naive_n(const uint8_t* in, uint32_t logk, int three, int inverse, int coset,
+                    uint8_t* out) {
+    const uint64_t n = (three ? 3ull : 1ull) << logk;
+    fe* a = (fe*)malloc(sizeof(fe) * n);
+    for (uint64_t i = 0; i < n; ++i) to_mont(&FR, in + 32 * i, &a[i]);
+    fe g, gi;
+    {
+        uint8_t five[32] = {5};
+        to_mont(&FR, five, &g);
+        finv(&FR, &g, &gi);
+    }
+    if (coset && !inverse) {
+        fe gp;
+        memcpy(gp.v, FR.one, 32);
+        for (uint64_t i = 0; i < n; ++i) {
+            fmul(&FR, &a[i], &gp, &a[i]);
+            fmul(&FR, &gp, &g, &gp);
+        }
+    }
+    fe w, wi, ninv, gk;
+    fr_root_n(logk, three, inverse, &w);
+    memcpy(wi.v, FR.one, 32);
+    memcpy(gk.v, FR.one, 32);
+    {
+        uint8_t nb[32] = {0};
+        memcpy(nb, &n, 8);
+        fe nn;
+        to_mont(&FR, nb, &nn);
+        finv(&FR, &nn, &ninv);
+    }
+    for (uint64_t i = 0; i < n; ++i) {
+        fe acc = {{0, 0, 0, 0}}, x;
+        memcpy(x.v, FR.one, 32);
+        for (uint64_t j = 0; j < n; ++j) {
+            fe t;
+            fmul(&FR, &a[j], &x, &t);
+            fadd(&FR, &acc, &t, &acc);
+            fmul(&FR, &x, &wi, &x);
+        }
+        if (inverse) {
+            fmul(&FR, &acc, &ninv, &acc);
+            if (coset) fmul(&FR, &acc, &gk, &acc);
+        }
+        from_mont(&FR, &acc, out + 32 * i);
+        fmul(&FR, &wi, &w, &wi);
+        fmul(&FR, &gk, &gi, &gk);
+    }
+    free(a);
+}
+
 void bn_ntt(uint8_t* data, uint32_t logn, int inverse, int coset, int threads) {
     uint64_t n = 1ull << logn;
     fe* a = (fe*)malloc(sizeof(fe) * n);
@@ -734,9 +826,9 @@ int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w_in, const uint8_t* 
                     const uint8_t* trap, const uint8_t* rs2, uint8_t* out, int threads) {
     (void)threads;
     const uint64_t m = (uint64_t)T * K + T + 1;
-    uint32_t logn = 0;
-    while ((1ull << logn) < m) ++logn;
-    const uint64_t N = 1ull << logn;
+    uint32_t logk;
+    int three;
+    const uint64_t N = bn_g16_domain(m, &logk, &three);
     fe tau, alpha, beta, delta, r, s;
     fr_from_le_bytes(trap, &tau);
     fr_from_le_bytes(trap + 32, &alpha);
@@ -748,7 +840,7 @@ int bn_g16_expected(uint32_t T, uint32_t K, const uint8_t* w_in, const uint8_t* 
     memcpy(one.v, FR.one, 32);
     /* L_j(tau) = Z(tau)/N * w^j / (tau - w^j) for j < m */
     fe w;
-    fr_root(logn, 0, &w);
+    fr_root_n(logk, three, 0, &w);
     uint64_t e[4] = {N, 0, 0, 0};
     fe tN, Z, Ninv, nN, coef;
     fpow(&FR, &tau, e, &tN);
@@ -1196,16 +1288,16 @@ void bn_f12_pow(const uint8_t* a384, const uint8_t* e32, uint8_t* out384) {
  * variables; u / v from the row layout in bn254_oracle.h). */
 int bn_g16_vk(uint32_t T, uint32_t K, const uint8_t* trap, uint8_t* out) {
     const uint64_t m = (uint64_t)T * K + T + 1;
-    uint32_t logn = 0;
-    while ((1ull << logn) < m) ++logn;
-    const uint64_t N = 1ull << logn;
+    uint32_t logk;
+    int three;
+    const uint64_t N = bn_g16_domain(m, &logk, &three);
     fe tau, alpha, beta, gamma, one, w, tN, Z, nN, Ninv, coef, t1, t2;
     fr_from_le_bytes(trap, &tau);
     fr_from_le_bytes(trap + 32, &alpha);
     fr_from_le_bytes(trap + 64, &beta);
     fr_from_le_bytes(trap + 96, &gamma);
     memcpy(one.v, FR.one, 32);
-    fr_root(logn, 0, &w);
+    fr_root_n(logk, three, 0, &w);
     uint64_t e[4] = {N, 0, 0, 0};
     fpow(&FR, &tau, e, &tN);
     fsub(&FR, &tN, &one, &Z);

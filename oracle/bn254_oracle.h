@@ -40,6 +40,12 @@ void bn_reduce(int field, const uint8_t* a, uint64_t n, uint8_t* out);
  * inverse one. threads: worker count. */
 void bn_ntt(uint8_t* data, uint32_t logn, int inverse, int coset, int threads);
 void bn_dft_naive(const uint8_t* in, uint32_t logn, int inverse, uint8_t* out);
+/* Groth16 domain rule: the smallest N >= m among 2^a and 3 * 2^b; *logk =
+ * log2 of its power-of-two factor, *three = 1 for 3 * 2^b. */
+uint64_t bn_g16_domain(uint64_t m, uint32_t* logk, int* three);
+/* naive DFT of size 2^logk or 3 * 2^logk (coset shift 5, inverse scaled by 1/n) */
+void bn_dft_naive_n(const uint8_t* in, uint32_t logk, int three, int inverse, int coset,
+                    uint8_t* out);
 
 /* G1 / G2 affine ops (group = 1 or 2). */
 int bn_on_curve(int group, const uint8_t* p);

@@ -70,6 +70,8 @@ _SIGS = {
     "acegpu_bn_convert_dev": (C.c_int, [ctxp, vp, C.c_int, vp, u64, C.c_int]),
     "acegpu_bn_ntt": (C.c_int, [ctxp, vp, C.c_uint32, C.c_int, C.c_int]),
     "acegpu_bn_ntt_dev": (C.c_int, [ctxp, vp, vp, vp, C.c_uint32, C.c_int, C.c_int]),
+    "acegpu_bn_ntt3": (C.c_int, [ctxp, vp, C.c_uint32, C.c_int, C.c_int]),
+    "acegpu_bn_ntt3_dev": (C.c_int, [ctxp, vp, vp, vp, C.c_uint32, C.c_int, C.c_int]),
     "acegpu_bn_scalar_muls": (C.c_int, [ctxp, C.c_int, vp, vp, u64, vp]),
     "acegpu_bn_msm_params": (C.c_int, [ctxp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "acegpu_bn_msm_prepare": (C.c_int, [ctxp, C.c_int, vp, u64, C.c_int, C.POINTER(C.c_void_p)]),
@@ -97,6 +99,7 @@ _SIGS = {
                                          C.c_uint32, vp]),
     "acegpu_r1cs_shape": (C.c_int, [C.c_void_p, C.POINTER(u64), C.POINTER(u64), C.POINTER(u64)]),
     "acegpu_g16_shape": (C.c_int, [C.c_void_p, u64p, u64p, C.POINTER(C.c_uint32)]),
+    "acegpu_g16_domain": (C.c_int, [C.c_void_p, u64p]),
     "acegpu_g16_prove_chunk": (C.c_int, [ctxp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_prove_chunk_dev": (C.c_int, [ctxp, vp, C.c_void_p, vp, vp, vp, vp, vp, vp]),
     "acegpu_g16_vk": (C.c_int, [ctxp, C.c_void_p, vp]),

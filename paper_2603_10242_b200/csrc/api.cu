@@ -95,6 +95,7 @@ struct acegpu_ctx {
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // BN254: NTT twiddle tables per log-size, MSM scratch.
     ace_gpu::bn::NttTables ntt[ace_gpu::bn::kNttMaxLog + 1];
+    ace_gpu::bn::Ntt3Tables ntt3[ace_gpu::bn::kNtt3MaxLog + 1];  // N = 3 * 2^k
     ace_gpu::bn::MsmScratch msm;
     // Segmented block pipeline: sub-contexts (own stream + workspace).
     cudaStream_t copy_stream = nullptr;  // overlapped host-input pipeline
@@ -399,6 +400,7 @@ void acegpu_destroy(acegpu_ctx* c) {
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
     for (auto& t : c->ntt) t.release();
+    for (auto& t : c->ntt3) t.release();
     c->msm.release();
     for (auto& e : c->seg_events) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -1687,6 +1689,47 @@ extern "C" int acegpu_bn_ntt_dev(acegpu_ctx* c, void* stream, const uint8_t* d_i
     return ACEGPU_OK;
 }
 
+// Mixed radix N = 3 * 2^logk (device, Montgomery form).
+extern "C" int acegpu_bn_ntt3_dev(acegpu_ctx* c, void* stream, const uint8_t* d_in,
+                                  uint8_t* d_out, uint32_t logk, int inverse, int coset) {
+    if (logk > (uint32_t)bn::kNtt3MaxLog) return fail(ACEGPU_EINVAL, "NTT size above 3 x 2^26");
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    cudaStream_t s = pick(c, stream);
+    if (bn::ntt_tables(c->ntt[logk], (int)logk, s) || bn::ntt3_tables(c->ntt3[logk], (int)logk, s))
+        return fail(ACEGPU_ECUDA, "NTT tables");
+    const uint64_t M = 1ull << logk;
+    uint8_t* scratch;
+    RET(ws(c, kBnScratch, 32 * (3 * M + 3 * M), &scratch));
+    if (bn::ntt3_run(c->ntt3[logk], c->ntt[logk], d_in, d_out, scratch, scratch + 96 * M, inverse,
+                     coset, s))
+        return fail(ACEGPU_ECUDA, std::string("NTT3 launch: ") + cudaGetErrorString(cudaGetLastError()));
+    c->launches += 5;
+    return ACEGPU_OK;
+}
+
+extern "C" int acegpu_bn_ntt3(acegpu_ctx* c, uint8_t* data, uint32_t logk, int inverse,
+                              int coset) {
+    if (logk > (uint32_t)bn::kNtt3MaxLog) return fail(ACEGPU_EINVAL, "NTT size above 3 x 2^26");
+    const uint64_t n = 3ull << logk;
+    uint8_t* d;
+    {
+        std::lock_guard<std::mutex> lk(c->mu);
+        DeviceGuard g(c->device);
+        RET(h2d_t(c, kBnA, data, 32 * n, c->stream, &d));
+        bn::launch_fr_convert(d, n, 1, c->stream);
+        CKL();
+    }
+    RET(acegpu_bn_ntt3_dev(c, c->stream, d, d, logk, inverse, coset));
+    std::lock_guard<std::mutex> lk(c->mu);
+    DeviceGuard g(c->device);
+    bn::launch_fr_convert(d, n, 0, c->stream);
+    CKL();
+    CK(cudaMemcpyAsync(data, d, 32 * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return ACEGPU_OK;
+}
+
 extern "C" int acegpu_bn_ntt(acegpu_ctx* c, uint8_t* data, uint32_t logn, int inverse,
                              int coset) {
     if (logn > (uint32_t)bn::kNttMaxLog) return fail(ACEGPU_EINVAL, "NTT size above 2^28");
@@ -1951,6 +1994,8 @@ struct acegpu_g16 {
     bool vb = false;
     // split key (acegpu_g16_setup_slice): this rank's slice of every base array
     uint32_t rank = 0, world = 1;
+    // domain N = 2^logn, or 3 * 2^logn (mixed radix) when three
+    bool three = false;
 };
 
 namespace {
@@ -2042,6 +2087,12 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     delete g;
 }
 
+extern "C" int acegpu_g16_domain(const acegpu_g16* g, uint64_t* N) {
+    if (!g || !N) return fail(ACEGPU_EINVAL, "null argument");
+    *N = g->N;
+    return ACEGPU_OK;
+}
+
 extern "C" int acegpu_g16_shape(const acegpu_g16* g, uint64_t* V, uint64_t* m, uint32_t* logn) {
     if (V) *V = g->d.V;
     if (m) *m = g->d.m;
@@ -2064,12 +2115,24 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     g->d.K = K;
     g->d.V = r ? r->vars : 1 + uint64_t(T) + uint64_t(T) * (K + 1);
     g->d.m = r ? r->rows : uint64_t(T) * K + T + 1;
+    // the smallest domain >= m among 2^a and 3 * 2^b (oracle: bn_g16_domain);
+    // ACEGPU_G16_RADIX3=0 keeps powers of two
     while ((1ull << g->logn) < g->d.m) ++g->logn;
+    {
+        const char* e = std::getenv("ACEGPU_G16_RADIX3");
+        uint32_t b = 0;
+        while ((3ull << b) < g->d.m) ++b;
+        if (!(e && e[0] == '0') && (3ull << b) < (1ull << g->logn) &&
+            b <= uint32_t(bn::kNtt3MaxLog)) {
+            g->three = true;
+            g->logn = b;
+        }
+    }
     if (g->logn > uint32_t(bn::kNttMaxLog)) return fail(ACEGPU_EINVAL, "g16: domain above 2^28");
-    g->N = 1ull << g->logn;
+    g->N = (g->three ? 3ull : 1ull) << g->logn;
     {
         const char* e = std::getenv("ACEGPU_G16_VB");  // 1: force variable-base (tests)
-        g->vb = g->logn > uint32_t(bn::kNttTwoPassMax) || (e && e[0] == '1') || world > 1;
+        g->vb = g->N > (1ull << bn::kNttTwoPassMax) || (e && e[0] == '1') || world > 1;
     }
     g->rank = rank;
     g->world = world;
@@ -2125,7 +2188,7 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // constants
     CK(cudaMemcpyAsync(g->consts, trapdoor5, 160, cudaMemcpyHostToDevice, s));
-    bn::g16_setup_consts(g->consts, g->logn, s);
+    bn::g16_setup_consts(g->consts, g->logn, g->three ? 1 : 0, s);
     if (K) bn::g16_chain_consts(K, g->cc, s);
     // query scalars
     uint8_t *L = nullptr, *su = nullptr, *sv = nullptr, *sl = nullptr, *part = nullptr,
@@ -2257,7 +2320,9 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     bn::g16_vk_digest(pts, uint32_t(448 + 64 * (T + 1)), g->vk_digest, s);
     CKL();
     CK(cudaStreamSynchronize(s));
-    if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s)) return fail(ACEGPU_ECUDA, "g16 NTT tables");
+    if (bn::ntt_tables(c->ntt[g->logn], int(g->logn), s) ||
+        (g->three && bn::ntt3_tables(c->ntt3[g->logn], int(g->logn), s)))
+        return fail(ACEGPU_ECUDA, "g16 NTT tables");
     CK(cudaStreamSynchronize(s));
     c->launches += 20;
     *out = own.release();
@@ -2701,7 +2766,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
                                            : "g16: full assignments need an R1CS key");
     const uint64_t V = g->d.V, N = g->N, m = g->d.m;
     uint8_t* scratch;
-    RET(ws(c, kBnScratch, 32 * N, &scratch));
+    RET(ws(c, kBnScratch, (g->three ? 64 : 32) * N, &scratch));  // mixed radix: + the 3 sub-vectors
     // next buffer slot; its previous proof must be assembled before reuse
     g->cur = g->vb ? 0 : g->cur ^ 1;
     acegpu_g16::Slot& sl = g->slot[g->cur];
@@ -2746,8 +2811,14 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     tr.mark("witness", sw);
     // s_h: H(g w^j) = (a b - c) / Z on the coset, then [h] over those evaluations
     const bn::NttTables& t = c->ntt[g->logn];
-    if (t.L != int(g->logn)) return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
+    const bn::Ntt3Tables& t3 = c->ntt3[g->logn];
+    if (t.L != int(g->logn) || (g->three && t3.k != int(g->logn)))
+        return fail(ACEGPU_EINVAL, "g16: NTT tables missing");
     cudaStream_t sh = g->s_h, sn = g->s_n;
+    auto ntt = [&](uint8_t* e, int inverse, int coset) {
+        return g->three ? bn::ntt3_run(t3, t, e, e, scratch, scratch + 32 * N, inverse, coset, sn)
+                        : bn::ntt_run(t, e, e, scratch, inverse, coset, 1, sn);
+    };
     CK(cudaStreamWaitEvent(sn, g->ev_z, 0));
     if (phase1) {
         // phase 1 of the owner split: only the owned vectors' coset
@@ -2756,9 +2827,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         int k = 0, idx = 0;
         for (uint8_t* e : {g->ea, g->eb, g->ec}) {
             if ((owned >> k++) & 1) {
-                if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn) ||
-                    bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn))
-                    return fail(ACEGPU_ECUDA, "g16 ntt");
+                if (ntt(e, 1, 0) || ntt(e, 0, 1)) return fail(ACEGPU_ECUDA, "g16 ntt");
                 CK(cudaMemcpyAsync(d_own + 32 * N * idx++, e, 32 * N, cudaMemcpyDeviceToDevice, sn));
             }
         }
@@ -2767,8 +2836,8 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     }
     for (uint8_t* e : {g->ea, g->eb, g->ec}) {
         if (phase1) break;
-        if (bn::ntt_run(t, e, e, scratch, 1, 0, 1, sn)) return fail(ACEGPU_ECUDA, "g16 intt");
-        if (bn::ntt_run(t, e, e, scratch, 0, 1, 1, sn)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
+        if (ntt(e, 1, 0)) return fail(ACEGPU_ECUDA, "g16 intt");
+        if (ntt(e, 0, 1)) return fail(ACEGPU_ECUDA, "g16 coset ntt");
     }
     if (!phase1) bn::g16_pointwise(g->ea, g->eb, g->ec, g->consts, N, sn);
     // H(g w^j) are the MSM scalars as they stand (Lagrange-coset H bases): no

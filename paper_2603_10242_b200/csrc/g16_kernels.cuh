@@ -17,8 +17,9 @@ struct G16Dims {
 // Setup (CRS from a trapdoor; all Fr in Montgomery form unless noted).
 void g16_chain_consts(uint32_t K, uint8_t* out, cudaStream_t s);
 // c[0..4] = tau, alpha, beta, gamma, delta in standard form -> converted;
-// fills c[5..10] (see groth16.cu).
-void g16_setup_consts(uint8_t* c, uint32_t logn, cudaStream_t s);
+// fills c[5..11] (see groth16.cu) for the domain N = 2^logn, or 3 * 2^logn
+// when three (omega = 5^((r-1)/N)).
+void g16_setup_consts(uint8_t* c, uint32_t logn, int three, cudaStream_t s);
 void g16_lagrange(const uint8_t* c, uint64_t m, uint8_t* L, cudaStream_t s);
 // su, sv: V scalars; sl: V - T - 1 scalars (standard form); part: 256*64 B scratch
 void g16_query_scalars(const G16Dims& d, const uint8_t* L, const uint8_t* c, const uint8_t* cc,

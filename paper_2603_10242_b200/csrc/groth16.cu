@@ -68,7 +68,7 @@ __global__ void chain_consts_kernel(uint32_t K, uint8_t* out) {
 // [4] delta (inputs, standard form, converted here) -> [5] omega_N,
 // [6] Z(tau)/N, [7] Z(tau)/delta, [8] 1/delta, [9] (g^N - 1)^-1, [10] Z(tau),
 // [11] (tau^N - g^N) / (N g^N) * Z(tau)/delta (the coset-Lagrange H bases).
-__global__ void setup_consts_kernel(uint8_t* c, uint32_t logn) {
+__global__ void setup_consts_kernel(uint8_t* c, uint32_t logn, int three) {
     if (threadIdx.x || blockIdx.x) return;
     for (int i = 0; i < 5; ++i) str(c + 32 * i, to_mont(ldr(c + 32 * i)));
     const Fr tau = ldr(c), delta = ldr(c + 128);
@@ -78,13 +78,22 @@ __global__ void setup_consts_kernel(uint8_t* c, uint32_t logn) {
     e[0] -= 1;
     for (uint32_t s = 0; s < logn; ++s)
         for (int i = 0; i < 8; ++i) e[i] = (e[i] >> 1) | (i < 7 ? (e[i + 1] << 31) : 0u);
+    if (three) {  // N = 3 * 2^logn: (r - 1) / N (r - 1 = 2^28 3^2 ...)
+        uint64_t rem = 0;
+        for (int i = 7; i >= 0; --i) {
+            const uint64_t cur = (rem << 32) | e[i];
+            e[i] = (uint32_t)(cur / 3);
+            rem = cur % 3;
+        }
+    }
     Fr five = Fr::zero();
     five.v[0] = 5;
     five = to_mont(five);
     const Fr w = pow(five, e);
     uint32_t en[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (logn < 32) en[0] = 1u << logn;
-    else en[1] = 1u << (logn - 32);
+    const uint64_t Nn = (three ? 3ull : 1ull) << logn;
+    en[0] = (uint32_t)Nn;
+    en[1] = (uint32_t)(Nn >> 32);
     const Fr Z = sub(pow(tau, en), Fr::one());
     Fr n = Fr::zero();
     n.v[0] = en[0];
@@ -547,8 +556,8 @@ void g16_chunk_node(const uint8_t* proof256, const uint8_t* digest32, uint8_t* n
 void g16_chain_consts(uint32_t K, uint8_t* out, cudaStream_t s) {
     chain_consts_kernel<<<grid(K, 128), 128, 0, s>>>(K, out);
 }
-void g16_setup_consts(uint8_t* c, uint32_t logn, cudaStream_t s) {
-    setup_consts_kernel<<<1, 1, 0, s>>>(c, logn);
+void g16_setup_consts(uint8_t* c, uint32_t logn, int three, cudaStream_t s) {
+    setup_consts_kernel<<<1, 1, 0, s>>>(c, logn, three);
 }
 void g16_lagrange(const uint8_t* c, uint64_t m, uint8_t* L, cudaStream_t s) {
     lagrange_kernel<<<grid(m, 128), 128, 0, s>>>(c, m, L);

@@ -129,6 +129,7 @@ struct PassArgs {
     const Fr* post_lo;   // pass C: scale_k2 (n2), e.g. n^-1 g^-k2
     const Fr* post_hi;   // pass C: g^(-n2*k1) (n1)
     const Fr* scale;     // uniform output scale (n^-1) when post tables are absent
+    uint64_t bstride;    // batch (blockIdx.y): elements between transforms (pass A / C)
 };
 
 // Pass A: columns i1 in [cb*R, cb*R+R), DFT length n2 over i2.
@@ -138,11 +139,13 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_a(PassArgs a) {
     constexpr int R = kNttR;
     const SmemFr s{smem_raw, uint32_t(n2 * R)};
     const int i1_0 = blockIdx.x * R;
+    const uint8_t* in = a.in + 32 * a.bstride * blockIdx.y;
+    uint8_t* out = a.out + 32 * a.bstride * blockIdx.y;
     for (int e = threadIdx.x; e < n2 * R; e += blockDim.x) {
         const int r = e % R, i2 = e / R;
         const int i1 = i1_0 + r;
         const uint64_t idx = i1 + (uint64_t)n1 * i2;
-        Fr x = load<FrCfg>(a.in + 32 * idx);
+        Fr x = load<FrCfg>(in + 32 * idx);
         if (a.pre_full) x = mul(x, ld(&a.pre_full[idx]));
         else if (a.pre_lo) x = mul(x, mul(ld(&a.pre_lo[i1]), ld(&a.pre_hi[i2])));
         s.put(bitrev(i2, a.L2) * R + r, x);
@@ -161,7 +164,7 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_a(PassArgs a) {
             const uint32_t lo = ex & (n2 - 1), hi = ex >> a.L2;
             if (ex) x = mul(x, mul(ld(&a.tw_lo[lo]), ld(&a.tw_hi[hi])));
         }
-        store<FrCfg>(a.out + 32 * (i1 + (uint64_t)n1 * k2), x);
+        store<FrCfg>(out + 32 * (i1 + (uint64_t)n1 * k2), x);
     }
 }
 
@@ -172,10 +175,12 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_c(PassArgs a) {
     constexpr int R = kNttR;
     const SmemFr s{smem_raw, uint32_t(n1 * R)};
     const int k2_0 = blockIdx.x * R;
+    const uint8_t* in = a.in + 32 * a.bstride * blockIdx.y;
+    uint8_t* out = a.out + 32 * a.bstride * blockIdx.y;
     for (int e = threadIdx.x; e < n1 * R; e += blockDim.x) {
         const int r = e % R, i1 = e / R;
         const uint64_t idx = i1 + (uint64_t)n1 * (k2_0 + r);
-        s.put(bitrev(i1, a.L1) * R + r, load<FrCfg>(a.in + 32 * idx));
+        s.put(bitrev(i1, a.L1) * R + r, load<FrCfg>(in + 32 * idx));
     }
     __syncthreads();
     smem_dit<R>(s, a.L1, a.w_sub);
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_c(PassArgs a) {
         if (a.post_full) x = mul(x, ld(&a.post_full[k2 + (uint64_t)n2 * k1]));
         else if (a.post_lo) x = mul(x, mul(ld(&a.post_lo[k2]), ld(&a.post_hi[k1])));
         else if (a.scale) x = mul(x, ld(a.scale));
-        store<FrCfg>(a.out + 32 * (k2 + (uint64_t)n2 * k1), x);
+        store<FrCfg>(out + 32 * (k2 + (uint64_t)n2 * k1), x);
     }
 }
 
@@ -300,9 +305,144 @@ __global__ void convert_kernel(uint8_t* data, uint64_t n, int to) {
     store<FrCfg>(data + 32 * i, to ? to_mont(x) : from_mont(x));
 }
 
+// ---- mixed radix 3 * 2^k --------------------------------------------------
+// w3 = w_N^(N/3) and its inverse: 3 * 2^k roots (r - 1 = 2^28 3^2 ...);
+// c: [0] w_N [1] w_N^-1 [2] w3 [3] w3^-1 [4] 3^-1 [5] g [6] g^-1
+__global__ void roots3_kernel(int k, Fr* out) {
+    if (threadIdx.x || blockIdx.x) return;
+    uint32_t e[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) e[i] = mod_limb<FrCfg>(i);
+    e[0] -= 1;
+    for (int s = 0; s < k; ++s)
+        for (int i = 0; i < 8; ++i) e[i] = (e[i] >> 1) | (i < 7 ? (e[i + 1] << 31) : 0u);
+    uint64_t rem = 0;  // e /= 3
+    for (int i = 7; i >= 0; --i) {
+        const uint64_t cur = (rem << 32) | e[i];
+        e[i] = (uint32_t)(cur / 3);
+        rem = cur % 3;
+    }
+    Fr five = Fr::zero();
+    five.v[0] = 5;
+    five = to_mont(five);
+    const Fr w = pow(five, e);
+    out[0] = w;
+    out[1] = inv(w);
+    uint32_t m[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // N / 3 = 2^k
+    m[k >> 5] = 1u << (k & 31);
+    out[2] = pow(w, m);
+    out[3] = inv(out[2]);
+    Fr three = Fr::zero();
+    three.v[0] = 3;
+    out[4] = inv(to_mont(three));
+    out[5] = five;
+    out[6] = inv(five);
+}
+
+__device__ __forceinline__ Fr split_pow(const Fr* lo, const Fr* hi, uint64_t e, int S) {
+    return mul(ld(&lo[e & ((1ull << S) - 1)]), ld(&hi[e >> S]));
+}
+
+// Y_i1[i2] = x[i1 + 3 i2] (times g^(i1 + 3 i2) for a forward coset transform)
+__global__ void deint3_kernel(const uint8_t* in, uint8_t* y, uint64_t M, const Fr* g_lo,
+                              const Fr* g_hi, int S) {
+    const uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (o >= 3 * M) return;
+    const uint64_t i1 = o / M, i2 = o - i1 * M, src = i1 + 3 * i2;
+    Fr v = load<FrCfg>(in + 32 * src);
+    if (g_lo) v = mul(v, split_pow(g_lo, g_hi, src, S));
+    store<FrCfg>(y + 32 * o, v);
+}
+
+// X[k2 + M k1] = sum_i1 w_N^(i1 k2) w3^(i1 k1) Y_i1[k2], with 1 + w3 + w3^2 = 0:
+// X0 = y0 + t1 + t2, X1 = y0 - t2 + w3 (t1 - t2), X2 = y0 - t1 - w3 (t1 - t2).
+// Inverse: w^-1 roots, times 3^-1 (the sub-NTTs applied 2^-k), coset g^-k.
+__global__ void combine3_kernel(const uint8_t* y, uint8_t* out, uint64_t M, const Fr* c,
+                                const Fr* w_lo, const Fr* w_hi, int inverse, const Fr* gi_lo,
+                                const Fr* gi_hi, int S) {
+    const uint64_t k2 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (k2 >= M) return;
+    const Fr y0 = load<FrCfg>(y + 32 * k2), y1 = load<FrCfg>(y + 32 * (M + k2)),
+             y2 = load<FrCfg>(y + 32 * (2 * M + k2));
+    Fr t1 = y1, t2 = y2;
+    if (k2) {
+        const Fr tw = split_pow(w_lo, w_hi, k2, S);
+        t1 = mul(y1, tw);
+        t2 = mul(y2, sqr(tw));
+    }
+    const Fr d = mul(ld(&c[inverse ? 3 : 2]), sub(t1, t2));
+    Fr x[3] = {add(add(y0, t1), t2), add(sub(y0, t2), d), sub(sub(y0, t1), d)};
+#pragma unroll
+    for (int k1 = 0; k1 < 3; ++k1) {
+        const uint64_t k = k2 + M * k1;
+        Fr v = x[k1];
+        if (inverse) {
+            v = mul(v, ld(&c[4]));
+            if (gi_lo) v = mul(v, split_pow(gi_lo, gi_hi, k, S));
+        }
+        store<FrCfg>(out + 32 * k, v);
+    }
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
+int ntt3_tables(Ntt3Tables& t, int k, cudaStream_t s) {
+    if (t.k == k && t.consts) return 0;
+    t.release();
+    if (k < 0 || k > kNtt3MaxLog) return -1;
+    t.k = k;
+    const uint64_t M = 1ull << k, N = 3 * M;
+    t.S = (k + 2) / 2;  // lo tables 2^S entries
+    const uint64_t lo = 1ull << t.S, hi_w = (M + lo - 1) / lo, hi_g = (N + lo - 1) / lo;
+    auto alloc = [&](Fr** p, size_t cnt) { return cudaMalloc(p, sizeof(Fr) * (cnt ? cnt : 1)); };
+    if (alloc(&t.consts, 8)) return -1;
+    roots3_kernel<<<1, 1, 0, s>>>(k, t.consts);
+    auto pw = [&](Fr** dst, const Fr* base, uint32_t step, uint64_t cnt) {
+        if (alloc(dst, cnt)) return -1;
+        powers_kernel<<<(unsigned)((cnt + 255) / 256), 256, 0, s>>>(base, step, (uint32_t)cnt,
+                                                                    nullptr, *dst);
+        return 0;
+    };
+    const uint32_t step = (uint32_t)lo;
+    if (pw(&t.wn_lo, t.consts + 0, 1, lo) || pw(&t.wn_hi, t.consts + 0, step, hi_w) ||
+        pw(&t.wni_lo, t.consts + 1, 1, lo) || pw(&t.wni_hi, t.consts + 1, step, hi_w) ||
+        pw(&t.g_lo, t.consts + 5, 1, lo) || pw(&t.g_hi, t.consts + 5, step, hi_g) ||
+        pw(&t.gi_lo, t.consts + 6, 1, lo) || pw(&t.gi_hi, t.consts + 6, step, hi_g))
+        return -1;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+void Ntt3Tables::release() {
+    Fr** all[] = {&consts, &wn_lo, &wn_hi, &wni_lo, &wni_hi, &g_lo, &g_hi, &gi_lo, &gi_hi};
+    for (Fr** p : all) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    k = -1;
+}
+
+int ntt3_run(const Ntt3Tables& t, const NttTables& tM, const uint8_t* in, uint8_t* out,
+             uint8_t* ybuf, uint8_t* scratch, int inverse, int coset, cudaStream_t s) {
+    if (t.k < 0 || tM.L != t.k) return -1;
+    const uint64_t M = 1ull << t.k;
+    const unsigned g3 = (unsigned)((3 * M + 255) / 256), g1 = (unsigned)((M + 255) / 256);
+    deint3_kernel<<<g3, 256, 0, s>>>(in, ybuf, M, (coset && !inverse) ? t.g_lo : nullptr, t.g_hi,
+                                     t.S);
+    if (t.k <= kNttTwoPassMax) {  // the three sub-NTTs as one batch (scratch: 3 x 2^k)
+        if (ntt_run(tM, ybuf, ybuf, scratch, inverse, 0, 3, s)) return -1;
+    } else {
+        for (int i1 = 0; i1 < 3; ++i1)
+            if (ntt_run(tM, ybuf + 32 * M * i1, ybuf + 32 * M * i1, scratch, inverse, 0, 1, s))
+                return -1;
+    }
+    combine3_kernel<<<g1, 256, 0, s>>>(ybuf, out, M, t.consts, inverse ? t.wni_lo : t.wn_lo,
+                                       inverse ? t.wni_hi : t.wn_hi, inverse,
+                                       (coset && inverse) ? t.gi_lo : nullptr, t.gi_hi, t.S);
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// (power-of-two tables)
 int ntt_tables(NttTables& t, int L, cudaStream_t s) {
     if (t.L == L && t.w_a) return 0;
     t.release();
@@ -442,6 +582,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
         c.post_lo = (coset && inverse) ? t.gi_post_lo : nullptr;
         c.post_hi = (coset && inverse) ? t.gi_post_hi : nullptr;
         if (inverse && !coset) c.scale = t.consts + 4;
+        c.bstride = 0;
         sm = sizeof(Fr) * (size_t)n1 * kNttR;
         cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         ntt_pass_c<<<(unsigned)(n2 / kNttR), 512, sm, s>>>(c);
@@ -459,9 +600,11 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
     a.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
     a.pre_hi = (coset && !inverse) ? t.g_hi : nullptr;
     a.pre_full = (full && coset && !inverse) ? t.g_full : nullptr;
+    // batch > 1: contiguous transforms (scratch holds batch x n)
+    a.bstride = 1ull << L;
     size_t smem = sizeof(Fr) * (size_t)n2 * kNttR;
     cudaFuncSetAttribute(ntt_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_pass_a<<<n1 / kNttR, 512, smem, s>>>(a);
+    ntt_pass_a<<<dim3(n1 / kNttR, batch), 512, smem, s>>>(a);
     // pass C: scratch -> out
     PassArgs c = a;
     c.in = scratch;
@@ -475,7 +618,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
  if (inverse && !coset) c.scale = t.consts + 4;
     smem = sizeof(Fr) * (size_t)n1 * kNttR;
     cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_pass_c<<<n2 / kNttR, 512, smem, s>>>(c);
+    ntt_pass_c<<<dim3(n2 / kNttR, batch), 512, smem, s>>>(c);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

@@ -30,9 +30,29 @@ struct NttTables {
     void release();
 };
 
+// Mixed radix N = 3 * 2^k (k <= kNtt3MaxLog): a 3-point DFT over three
+// 2^k-point NTTs (four-step with n1 = 3): de-interleave (x[i1 + 3 i2] ->
+// Y_i1[i2], coset scale fused), the sub-NTTs (the 2^k tables), then per k2
+// the twiddles w_N^(i1 k2) and the 3-point DFT into natural order (inverse
+// and coset scales fused). Groth16 domains of 3 * 2^b points cut the padding
+// of m just above a power of two (a paper-size chunk: 1.57 M vs 2.10 M).
+constexpr int kNtt3MaxLog = 26;
+struct Ntt3Tables {
+    int k = -1, S = 0;       // N = 3 * 2^k; split tables at S bits
+    Fr* consts = nullptr;    // w_N, w_N^-1, w3, w3^-1, 3^-1, g, g^-1
+    Fr *wn_lo = nullptr, *wn_hi = nullptr, *wni_lo = nullptr, *wni_hi = nullptr;  // w_N^(+-e), e < 2^k
+    Fr *g_lo = nullptr, *g_hi = nullptr, *gi_lo = nullptr, *gi_hi = nullptr;      // g^(+-i), i < N
+    void release();
+};
+int ntt3_tables(Ntt3Tables& t, int k, cudaStream_t s);
+// in/out may alias; ybuf: N x 32 B, scratch: 3 x 2^k x 32 B (the sub-NTTs').
+// Data in Montgomery form; the 2^k tables tM must be built (ntt_tables).
+int ntt3_run(const Ntt3Tables& t, const NttTables& tM, const uint8_t* in, uint8_t* out,
+             uint8_t* ybuf, uint8_t* scratch, int inverse, int coset, cudaStream_t s);
+
 int ntt_tables(NttTables& t, int L, cudaStream_t s);
-// in/out may alias; scratch (n x 32 B) is needed when L > kNttSingleMax.
-// Data in Montgomery form. batch > 1 only for L <= kNttSingleMax.
+// in/out may alias; scratch (batch x n x 32 B) is needed when L > kNttSingleMax.
+// Data in Montgomery form. batch > 1 (contiguous transforms) for L <= kNttTwoPassMax.
 int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratch, int inverse,
             int coset, int batch, cudaStream_t s);
 void launch_fr_convert(uint8_t* data, uint64_t n, int to_mont, cudaStream_t s);

@@ -49,6 +49,9 @@ class ProvingKey:
         V, m, L = C.c_uint64(), C.c_uint64(), C.c_uint32()
         N.lib().acegpu_g16_shape(self.h, C.byref(V), C.byref(m), C.byref(L))
         self.variables, self.constraints, self.log_domain = V.value, m.value, L.value
+        D = C.c_uint64()
+        N.lib().acegpu_g16_domain(self.h, C.byref(D))
+        self.domain = D.value  # 2^log_domain, or 3 x 2^log_domain (mixed radix)
 
     @classmethod
     def from_r1cs(cls, r1cs, trapdoor: np.ndarray | None = None, ctx=None) -> "ProvingKey":
@@ -65,6 +68,9 @@ class ProvingKey:
         V, m, L = C.c_uint64(), C.c_uint64(), C.c_uint32()
         N.lib().acegpu_g16_shape(self.h, C.byref(V), C.byref(m), C.byref(L))
         self.variables, self.constraints, self.log_domain = V.value, m.value, L.value
+        D = C.c_uint64()
+        N.lib().acegpu_g16_domain(self.h, C.byref(D))
+        self.domain = D.value  # 2^log_domain, or 3 x 2^log_domain (mixed radix)
         return self
 
     def prove_z(self, z: np.ndarray, rs: np.ndarray | None = None):

@@ -221,14 +221,14 @@ def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
     return N * pre // tot, N * (pre + sh[rank]) // tot
 
 
-def balanced_shares(world: int, ntt_frac: float = 0.115, unit: int = 1000) -> list[int]:
+def balanced_shares(world: int, ntt_frac: float = 0.092, unit: int = 1000) -> list[int]:
     """Shares of the bases that even out the ranks when vector k of the H
     polynomial is transformed on rank k mod world: an owned vector (its iNTT
     + coset NTT, run concurrently with the rank's MSMs) costs ~ntt_frac of
-    the whole proof's MSM work — fitted at 100k txs, 8 ranks, from an owner
-    rank (share 81/1000: 587 ms) and a non-owner (151/1000: 454 ms): ~330 ms
-    per owned vector vs ~2.8 s of MSM work in all — so owners take fewer
-    bases."""
+    the whole proof's MSM work — fitted at 100k txs (3 x 2^26 domain), 8
+    ranks, from an owner rank (share 53/1000: 429 ms) and a non-owner
+    (168/1000: 494 ms): ~250 ms per owned vector vs ~2.8 s of MSM work in
+    all — so owners take fewer bases."""
     own = [bin(owned_mask(r, world)).count("1") for r in range(world)]
     t = (1.0 + ntt_frac * sum(own)) / world  # per-rank budget, MSM-work units
     w = [max(t - ntt_frac * o, 0.01) for o in own]
@@ -243,7 +243,7 @@ def one_proof_phase1(local_full: DeviceBlock, pk, rank: int, world: int, codes=N
     import torch
     db = local_full
     dev = db.atts.device
-    N = 1 << pk.log_domain
+    N = pk.domain
     mask = owned_mask(rank, world)
     w = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
     pub = torch.empty(32 * pk.T, dtype=torch.uint8, device=dev)
@@ -337,7 +337,7 @@ def prove_one_proof(local_full: DeviceBlock, n_total: int, rank: int, world: int
         # the H polynomial's three vectors are computed by their owners and
         # exchanged by slices (each rank then does 2 of the 6 NTTs, not 6)
         own, merk = one_proof_phase1(local_full, pk, rank, world, codes)
-        slices = exchange_slices(own, rank, world, 1 << pk.log_domain, group, pk.shares)
+        slices = exchange_slices(own, rank, world, pk.domain, group, pk.shares)
         del own
         part = one_proof_phase2(slices, pk)
     else:

@@ -244,3 +244,46 @@ def test_eip196_197_vectors_pin_the_oracle():
     g2 = O.buf(128)
     L.bn_generator(2, g2)
     assert b[128:256] == bytes(g2)
+
+
+def test_groth16_domain_rule_and_mixed_radix_dft():
+    """The Groth16 domain rule (smallest N >= m among 2^a and 3 * 2^b; r - 1 =
+    2^28 * 3^2 * ...) and the oracle's naive DFT of 3 * 2^k points against
+    X_k = sum_j x_j (g^c w^k)^j evaluated here with Python integers (w =
+    5^((r-1)/n), a primitive n-th root); the power-of-two case equals the
+    radix-2 checker."""
+    lib = O.oracle()
+    lib.bn_g16_domain.restype = C.c_uint64
+    for m, want in [(1, 1), (3, 3), (4, 4), (5, 6), (7, 8), (13, 16), (21, 24), (49, 64),
+                    (1501, 1536), (1434625, 3 << 19), (140100001, 3 << 26),
+                    (2065681, 1 << 21), (1 << 20, 1 << 20)]:
+        lk, th = C.c_uint32(), C.c_int()
+        assert lib.bn_g16_domain(C.c_uint64(m), C.byref(lk), C.byref(th)) == want, m
+        assert (3 if th.value else 1) << lk.value == want
+    assert (R - 1) % (3 << 28) == 0
+    rng = random.Random(3)
+    for logk, three in [(0, 1), (1, 1), (3, 1), (2, 0)]:
+        n = (3 if three else 1) << logk
+        w = pow(5, (R - 1) // n, R)
+        assert pow(w, n, R) == 1 and (n == 1 or pow(w, n // (3 if three else 2), R) != 1)
+        x = [rng.randrange(R) for _ in range(n)]
+        buf = b"".join(v.to_bytes(32, "little") for v in x)
+        for inverse in (0, 1):
+            for coset in (0, 1):
+                out = O.buf(32 * n)
+                lib.bn_dft_naive_n(O.ptr(buf), C.c_uint32(logk), C.c_int(three), C.c_int(inverse),
+                                   C.c_int(coset), out)
+                got = [int.from_bytes(bytes(out)[32 * k:32 * k + 32], "little") for k in range(n)]
+                wi = pow(w, R - 2, R) if inverse else w
+                ninv = pow(n, R - 2, R)
+                for k in range(n):
+                    acc = 0
+                    for j, v in enumerate(x):
+                        xj = v * pow(5, j, R) % R if (coset and not inverse) else v
+                        acc += xj * pow(wi, j * k, R)
+                    acc %= R
+                    if inverse:
+                        acc = acc * ninv % R
+                        if coset:
+                            acc = acc * pow(pow(5, R - 2, R), k, R) % R
+                    assert got[k] == acc, (n, inverse, coset, k)

@@ -349,3 +349,70 @@ def test_eip196_vectors_on_gpu(ctx):
             got = bases.run(one)
         bases.close()
         assert got.tobytes() == exp, v["name"]
+
+
+@pytest.mark.parametrize("logk", [0, 1, 2, 5, 8, 10, 12, 13])
+def test_ntt3_matches_naive_dft(ctx, logk):
+    """Mixed-radix NTT of 3 * 2^k points (Groth16 domains just above a power
+    of two) vs the oracle's O(n^2) DFT (bn_dft_naive_n), forward / inverse /
+    coset both ways, plus the round trips."""
+    n = 3 << logk
+    rng = random.Random(100 + logk)
+    vals = [rng.randrange(R) for _ in range(n)]
+    modes = [(i, c) for i in (0, 1) for c in (0, 1)] if logk <= 10 else [(0, 1), (1, 1)]
+    for inverse, coset in modes:
+        if True:
+            data = arr(vals)
+            ctx.call("acegpu_bn_ntt3", data, logk, inverse, coset)
+            ref = O.buf(32 * n)
+            O.oracle().bn_dft_naive_n(O.ptr(arr(vals).tobytes()), C.c_uint32(logk), C.c_int(1),
+                                      C.c_int(inverse), C.c_int(coset), ref)
+            assert data.tobytes() == bytes(ref), (inverse, coset)
+    for coset in (0, 1):
+        data = arr(vals)
+        ctx.call("acegpu_bn_ntt3", data, logk, 0, coset)
+        ctx.call("acegpu_bn_ntt3", data, logk, 1, coset)
+        assert ints(data) == vals
+
+
+@pytest.mark.parametrize("logk", [19, 26])
+def test_ntt3_large_sparse_evaluations_and_roundtrip(ctx, logk):
+    """3 * 2^19 (a paper-size chunk's domain) and 3 * 2^26 (a 100k block's):
+    sampled outputs of sparse inputs vs sums evaluated here, and the coset
+    round trip on dense device data."""
+    import torch
+    n = 3 << logk
+    dev = torch.device("cuda:0")
+    rng = random.Random(logk)
+    w = pow(5, (R - 1) // n, R)
+    pos = sorted(rng.sample(range(n), 48))
+    val = [rng.randrange(R) for _ in pos]
+    ks = [0, 1, 2, n - 1, n // 3, 2 * n // 3 + 5] + [rng.randrange(n) for _ in range(8)]
+    buf = torch.zeros(n, 32, dtype=torch.uint8, device=dev)
+    src = torch.from_numpy(np.frombuffer(b"".join(le(v) for v in val), np.uint8).reshape(-1, 32).copy())
+    try:
+        for coset in (0, 1):
+            buf.zero_()
+            buf[torch.tensor(pos, device=dev)] = src.to(dev)
+            p = buf.data_ptr()
+            ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 1)
+            ctx.call("acegpu_bn_ntt3_dev", None, p, p, logk, 0, coset)
+            ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 0)
+            got = ints(buf[torch.tensor(ks, device=dev)].cpu().numpy().reshape(-1))
+            for k, gk in zip(ks, got):
+                z = pow(w, k, R) * (5 if coset else 1) % R
+                assert gk == sum(v * pow(z, i, R) for i, v in zip(pos, val)) % R, (coset, k)
+        g = torch.Generator(device=dev).manual_seed(9)
+        x = torch.randint(0, 256, (n, 32), dtype=torch.uint8, device=dev, generator=g)
+        x[:, 31] &= 0x1F
+        orig = x.clone()
+        p = x.data_ptr()
+        ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 1)
+        ctx.call("acegpu_bn_ntt3_dev", None, p, p, logk, 0, 1)
+        ctx.call("acegpu_bn_ntt3_dev", None, p, p, logk, 1, 1)
+        ctx.call("acegpu_bn_convert_dev", None, 1, p, n, 0)
+        assert torch.equal(x, orig)
+        del x, orig
+    finally:
+        del buf
+        torch.cuda.empty_cache()

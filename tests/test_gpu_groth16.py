@@ -53,8 +53,10 @@ def ctx():
     return N.context(0)
 
 
-@pytest.mark.parametrize("T,K", [(1, 2), (3, 4), (8, 5), (64, 100)])
+@pytest.mark.parametrize("T,K", [(1, 2), (3, 4), (8, 5), (64, 100), (5, 3), (11, 15), (100, 14)])
 def test_groth16_chunk_matches_trapdoor_oracle(ctx, T, K):
+    """(5, 3), (11, 15), (100, 14): m = 21, 177, 1,501 -> mixed-radix domains
+    of 24, 192, 1,536 points (3 x 2^b below the next power of two)."""
     from paper_2603_10242_b200 import groth16
     rng = random.Random(T * 1000 + K)
     trap = arr([rng.randrange(1, R) for _ in range(5)])
@@ -191,7 +193,7 @@ def test_groth16_paper_size_chunk(ctx):
     trap = rnd(5)
     pk = groth16.ProvingKey(T, K, trap, ctx)
     try:
-        assert pk.constraints == 1_434_625 and pk.log_domain == 21
+        assert pk.constraints == 1_434_625 and pk.domain == 3 << 19  # 1.57 M (2^21 = 2.10 M)
         w, pub, rs = rnd(T), rnd(T), rnd(2)
         proof, raw, _ = pk.prove(w, pub, rs)
         A, B, Cc = expected_points(T, K, w, pub, trap, rs)
@@ -264,7 +266,7 @@ def _vk_oracle(T, K, trap):
     return bytes(vk)
 
 
-@pytest.mark.parametrize("T,K", [(1, 2), (4, 3), (64, 20)])
+@pytest.mark.parametrize("T,K", [(1, 2), (4, 3), (64, 20), (5, 3), (100, 14)])
 def test_verifying_key_matches_oracle(ctx, T, K):
     from paper_2603_10242_b200 import _native as N, groth16
     rng = random.Random(T + 7 * K)
@@ -654,7 +656,7 @@ def test_one_proof_owner_split_matches_whole_key(ctx, world, shares):
     keys = [groth16.ProvingKey(T, K, trap, ctx, rank=r, world=world, shares=shares)
             for r in range(world)]
     try:
-        N = 1 << keys[0].log_domain
+        N = keys[0].domain
         owns, merks = [], []
         for r, k in enumerate(keys):
             own, merk = shard.one_proof_phase1(db, k, r, world)
@@ -702,7 +704,7 @@ def test_one_proof_entry_points_reject_bad_arguments(ctx):
         with pytest.raises(ValueError):
             shard.one_proof_partial(db, pk)
         w = torch.zeros(8 * 32, dtype=torch.uint8, device="cuda:0")
-        own = torch.zeros(3 * 32 * (1 << pk.log_domain), dtype=torch.uint8, device="cuda:0")
+        own = torch.zeros(3 * 32 * pk.domain, dtype=torch.uint8, device="cuda:0")
         with pytest.raises(ValueError):
             ctx.call("acegpu_g16_prove_phase1_dev", None, pk.h, w.data_ptr(), w.data_ptr(), 9,
                      own.data_ptr())
