@@ -2152,7 +2152,7 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
             sl.done = ev;
             break;
         }
-        if (dm(&sl.z, 32 * (V + 2)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
+        if (dm(&sl.z, 32 * (V + 3)) || dm(&sl.zb, 32 * (V + 2)) || dm(&sl.zl, 32 * (g->Vp + 1)) ||
             dm(&sl.ea, 32 * N) || dm(&sl.eb, 32 * N) || dm(&sl.ec, 32 * N) || dm(&sl.pts, 512) ||
             dm(&sl.scaled, 256) || dm(&sl.rs, 64) || dm(&sl.digest, 32) ||
             dm(&sl.dsc, bn::g16_digest_scratch_bytes(T, 1) + 32))
@@ -2193,17 +2193,17 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
     // query scalars
     uint8_t *L = nullptr, *su = nullptr, *sv = nullptr, *sl = nullptr, *part = nullptr,
             *hs = nullptr, *gens = nullptr, *ext = nullptr, *pts = nullptr, *icsc = nullptr,
-            *tab1 = nullptr, *tab2 = nullptr, *ex2 = nullptr;
+            *tab1 = nullptr, *tab2 = nullptr, *ex2 = nullptr, *inf = nullptr;
     // setup temporaries: freed on every exit (after the stream drains)
     struct Temps {
-        std::array<uint8_t**, 13> ps;
+        std::array<uint8_t**, 14> ps;
         cudaStream_t s;
         ~Temps() {
             cudaStreamSynchronize(s);
             for (uint8_t** p : ps)
                 if (*p) cudaFree(*p);
         }
-    } temps{{&L, &su, &sv, &sl, &part, &hs, &gens, &ext, &pts, &icsc, &tab1, &tab2, &ex2}, s};
+    } temps{{&L, &su, &sv, &sl, &part, &hs, &gens, &ext, &pts, &icsc, &tab1, &tab2, &ex2, &inf}, s};
     // pts: the bases before their window tables (fixed base), the u, v, w
     // column sums (general R1CS) and the verifying-key export
     uint64_t pts_bytes = 448 + 64 * (uint64_t(T) + 1);
@@ -2296,9 +2296,13 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
         }
         return bases_from_device(c->device, group, pts, total, s, out);
     };
-    RET(bases(1, su, V, {ex1, ex1 + 128}, &g->qa));        // A: [u]1 | alpha1 | delta1
-    RET(bases(1, sv, V, {ex1 + 64, ex1 + 128}, &g->qb1));  // B1: [v]1 | beta1 | delta1
-    RET(bases(2, sv, V, {ex2, ex2 + 128}, &g->qb2));       // B2: [v]2 | beta2 | delta2
+    // A, B1, B2 take the same scalars z | 1 | r | s (one digit sort per proof):
+    // A: [u]1 | alpha1 | delta1 | O, B: [v] | beta | O | delta (O = infinity)
+    if (dm(&inf, 128)) return fail(ACEGPU_ECUDA, "g16 setup alloc");
+    CK(cudaMemsetAsync(inf, 0, 128, s));
+    RET(bases(1, su, V, {ex1, ex1 + 128, inf}, &g->qa));
+    RET(bases(1, sv, V, {ex1 + 64, inf, ex1 + 128}, &g->qb1));
+    RET(bases(2, sv, V, {ex2, inf, ex2 + 128}, &g->qb2));
     RET(bases(1, sl, g->Vp, {ex1 + 128}, &g->ql));         // L: [l]1 (private) | delta1
     // H: [L^g_j(tau) Z(tau)/delta]1, j < N (coset-Lagrange basis, N points)
     RET(bases(1, hs, N, {}, &g->qh));
@@ -2803,7 +2807,6 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     }
     if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, sw));
     // scalar vectors with their extras
-    CK(cudaMemcpyAsync(g->zb, g->z, 32 * V, cudaMemcpyDeviceToDevice, sw));
     CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, sw));
     bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, sw);
     CKL();
@@ -2861,21 +2864,31 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
-    // s_bl: [v]2 (B2) and [l] (L)
+    // s_bl: [l] (L)
     CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
-    if (msm(g->qb2, V + 2, g->zb, g->msm_bl, g->pts + 128, g->s_bl) ||
-        (tr.mark("msm_b2", g->s_bl), false) ||
-        msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
-        return fail(ACEGPU_ECUDA, "g16 msm B2/L");
+    if (msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
+        return fail(ACEGPU_ECUDA, "g16 msm L");
     CK(cudaEventRecord(g->ev_bl, g->s_bl));
     tr.mark("msm_l", g->s_bl);
-    // s_ab: A and B1, then s*A and r*B1 (one serial scalar multiplication
-    // each) on the side stream while the others finish
+    // s_ab: A, B1 (G1) and B2 (G2) over the same scalars z | 1 | r | s — one
+    // digit sort, three accumulations; then s*A and r*B1 on the side stream
     CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
-    if (msm(g->qa, V + 2, g->z, g->msm_ab, g->pts, g->s_ab) ||
-        (tr.mark("msm_a", g->s_ab), false) ||
-        msm(g->qb1, V + 2, g->zb, g->msm_ab, g->pts + 64, g->s_ab))
-        return fail(ACEGPU_ECUDA, "g16 msm A/B1");
+    {
+        const int groups[3] = {1, 1, 2};
+        const uint8_t* tabs[3] = {g->qa->table, g->qb1->table, g->qb2->table};
+        uint8_t* outs[3] = {g->pts, g->pts + 64, g->pts + 128};
+        const acegpu_msm_bases* qa = g->qa;
+        int rc = 0;
+        if (qa->vb && qa->n == 0) {
+            rc = cudaMemsetAsync(g->pts, 0, 256, g->s_ab) != cudaSuccess;
+        } else if (qa->vb) {
+            rc = bn::msm_run_vb_multi(3, groups, tabs, qa->n, g->z + 32 * qa->lo, g->msm_ab, outs,
+                                      g->s_ab, qa->vb_sub);
+        } else {
+            rc = bn::msm_run_multi(3, groups, tabs, V + 3, g->z, g->msm_ab, outs, g->s_ab);
+        }
+        if (rc) return fail(ACEGPU_ECUDA, "g16 msm A/B1/B2");
+    }
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
     if (phase1) {  // phase 1 done: the owned evaluations are ready on s

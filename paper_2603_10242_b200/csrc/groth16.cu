@@ -391,10 +391,12 @@ __global__ void extras_kernel(uint8_t* za, uint8_t* zb, uint8_t* zl, uint64_t V,
     Fr one = Fr::zero();
     one.v[0] = 1;
     const Fr r = ldr(rs), s = ldr(rs + 32);
+    // A, B1 and B2 share these scalars (one digit sort): A's bases are
+    // [u] | alpha | delta | O, B's [v] | beta | O | delta (O = infinity)
     str(za + 32 * V, one);
     str(za + 32 * (V + 1), r);
-    str(zb + 32 * V, one);
-    str(zb + 32 * (V + 1), s);
+    str(za + 32 * (V + 2), s);
+    (void)zb;
     str(zl + 32 * Vp, from_mont(neg(mul(to_mont(r), to_mont(s)))));
 }
 

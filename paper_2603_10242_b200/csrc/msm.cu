@@ -737,10 +737,11 @@ int prepare_t(const uint8_t* bases, uint64_t n, uint8_t* table, cudaStream_t s) 
 // out = the affine result. Variable base (VB = true): table = the n bases
 // themselves, one bucket set per window, out = the kMsmWindows affine window
 // sums (combine_windows_kernel weights them).
-template <class F, bool VB, class Wn>
-int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
-             uint8_t* out, cudaStream_t s) {
-    constexpr int X = Lay<F>::XZ;
+// Phase 1 of a Pippenger pass: the scalars' signed digits sorted into bucket
+// order (sc.offs, sc.sorted); several tables over the same scalars share it.
+template <bool VB, class Wn>
+int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s,
+              uint32_t& segsz_out, uint64_t& nseg_out) {
     constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
     const uint64_t cap = (uint64_t)Wn::W * n;
     // segment length: kMsmSeg, shorter for small MSMs (>= ~19k threads, so a
@@ -776,7 +777,6 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
         sc.cap_buckets = nbk;
     }
     cudaMemsetAsync(sc.hist, 0, 4 * (NB + 1), s);
-    cudaMemsetAsync(sc.heavy, 0, 4, s);
     const unsigned gb = (unsigned)((n + 255) / 256);
     count_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
     // offs = exclusive scan of hist[0..NB] (hist[NB] = 0 -> offs[NB] = total)
@@ -786,6 +786,21 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
         return -1;
     cudaMemcpyAsync(sc.cursor, sc.offs, 4 * NB, cudaMemcpyDeviceToDevice, s);
     scatter_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.cursor, sc.sorted);
+    segsz_out = segsz;
+    nseg_out = nseg;
+    return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Phase 2: bucket accumulation of `table` over the sorted entries, fixup,
+// heavy buckets, reduction -> out (fixed base: the affine result; variable
+// base: the W window sums).
+template <class F, bool VB, class Wn>
+int acc_core(const uint8_t* table, uint64_t n, MsmScratch& sc, uint32_t segsz, uint64_t nseg,
+             uint8_t* out, cudaStream_t s) {
+    constexpr int X = Lay<F>::XZ;
+    constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
+    const uint64_t cap = (uint64_t)Wn::W * n;
+    cudaMemsetAsync(sc.heavy, 0, 4, s);
     bool affine = false;
     if constexpr (sizeof(F) == sizeof(Fq) && !VB) affine = ACEGPU_MSM_AFFINE && affine_enabled();
     if (affine) {
@@ -849,6 +864,22 @@ int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratc
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
+template <class F, bool VB, class Wn>
+int run_core(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
+             uint8_t* out, cudaStream_t s) {
+    uint32_t segsz;
+    uint64_t nseg;
+    if (sort_core<VB, Wn>(n, scalars, sc, s, segsz, nseg)) return -1;
+    return acc_core<F, VB, Wn>(table, n, sc, segsz, nseg, out, s);
+}
+
+template <bool VB, class Wn>
+int acc_any(int group, const uint8_t* table, uint64_t n, MsmScratch& sc, uint32_t segsz,
+            uint64_t nseg, uint8_t* out, cudaStream_t s) {
+    return group == 2 ? acc_core<Fq2, VB, Wn>(table, n, sc, segsz, nseg, out, s)
+                      : acc_core<Fq, VB, Wn>(table, n, sc, segsz, nseg, out, s);
+}
+
 template <class F>
 int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& sc, uint8_t* out,
           cudaStream_t s) {
@@ -856,29 +887,41 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 }
 
 // Variable base: sub-ranges of <= sub points (their W x sub sorted entries
-// stay below 2^32), W window sums each, then one Horner combination.
-template <class F>
-int run_vb(const uint8_t* bases, uint64_t n, const uint8_t* scalars, MsmScratch& sc,
-           uint8_t* out, uint64_t sub, cudaStream_t s) {
-    constexpr int A = Lay<F>::AFF;
+// stay below 2^32), W window sums each, then one Horner combination; k
+// tables (G1 or G2) over the same scalars share each sub-range's sort.
+int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
+                 const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
+                 cudaStream_t s) {
     using Wn = WinVb;
     if (!sub || sub > kMsmVbSubMax) sub = kMsmVbSubMax;
     const uint64_t nsub = n ? (n + sub - 1) / sub : 1;
-    if (sc.win_cap < nsub) {
+    const uint64_t per = (uint64_t)256 * Wn::W * nsub;  // one table's window sums
+    if (sc.win_cap < k * nsub) {
         if (sc.win) cudaFree(sc.win);
         sc.win = nullptr;
         sc.win_cap = 0;
-        if (cudaMalloc(&sc.win, (size_t)256 * Wn::W * nsub)) return -1;
-        sc.win_cap = nsub;
+        if (cudaMalloc(&sc.win, per * k)) return -1;
+        sc.win_cap = k * nsub;
     }
-    if (!n) cudaMemsetAsync(sc.win, 0, (size_t)A * Wn::W, s);
+    if (!n) cudaMemsetAsync(sc.win, 0, per * k, s);
     for (uint64_t r = 0; r < n; r += sub) {
         const uint64_t len = std::min<uint64_t>(sub, n - r);
-        if (run_core<F, true, Wn>(bases + (uint64_t)A * r, len, scalars + 32 * r, sc,
-                                  sc.win + (uint64_t)A * Wn::W * (r / sub), s))
-            return -1;
+        uint32_t segsz;
+        uint64_t nseg;
+        if (sort_core<true, Wn>(len, scalars + 32 * r, sc, s, segsz, nseg)) return -1;
+        for (int i = 0; i < k; ++i) {
+            const uint64_t A = 64ull * groups[i];
+            if (acc_any<true, Wn>(groups[i], bases[i] + A * r, len, sc, segsz, nseg,
+                                  sc.win + per * i + A * Wn::W * (r / sub), s))
+                return -1;
+        }
     }
-    combine_windows_kernel<F, Wn><<<1, 32, 0, s>>>(sc.win, (uint32_t)nsub, out);
+    for (int i = 0; i < k; ++i) {
+        if (groups[i] == 2)
+            combine_windows_kernel<Fq2, Wn><<<1, 32, 0, s>>>(sc.win + per * i, (uint32_t)nsub, outs[i]);
+        else
+            combine_windows_kernel<Fq, Wn><<<1, 32, 0, s>>>(sc.win + per * i, (uint32_t)nsub, outs[i]);
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 
@@ -917,8 +960,24 @@ int msm_run(int group, const uint8_t* table, uint64_t n, const uint8_t* scalars,
 
 int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
                MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub) {
-    return group == 2 ? run_vb<Fq2>(bases, n, scalars, sc, out, sub, s)
-                      : run_vb<Fq>(bases, n, scalars, sc, out, sub, s);
+    return run_vb_multi(1, &group, &bases, n, scalars, sc, &out, sub, s);
+}
+
+int msm_run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
+                     const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, cudaStream_t s,
+                     uint64_t sub) {
+    return run_vb_multi(k, groups, bases, n, scalars, sc, outs, sub, s);
+}
+
+int msm_run_multi(int k, const int* groups, const uint8_t* const* tables, uint64_t n,
+                  const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, cudaStream_t s) {
+    uint32_t segsz;
+    uint64_t nseg;
+    if (sort_core<false, WinFixed>(n, scalars, sc, s, segsz, nseg)) return -1;
+    for (int i = 0; i < k; ++i)
+        if (acc_any<false, WinFixed>(groups[i], tables[i], n, sc, segsz, nseg, outs[i], s))
+            return -1;
+    return 0;
 }
 
 void launch_points_convert(int group, uint8_t* pts, uint64_t n, int to_mont, cudaStream_t s) {

@@ -68,6 +68,14 @@ constexpr uint64_t kMsmVbSubMax = 1ull << 26;  // W x sub bucket entries < 2^32
 int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
                MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub = 0);
 
+// k tables (group 1 or 2 each) over the SAME scalars: one digit sort, then
+// each table's accumulation and reduction (Groth16's A, B1, B2 share z).
+int msm_run_multi(int k, const int* groups, const uint8_t* const* tables, uint64_t n,
+                  const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, cudaStream_t s);
+int msm_run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
+                     const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, cudaStream_t s,
+                     uint64_t sub = 0);
+
 // Point format conversions (standard <-> Montgomery coordinates), in place.
 void launch_points_convert(int group, uint8_t* pts, uint64_t n, int to_mont, cudaStream_t s);
 void launch_fq_convert(uint8_t* elems, uint64_t n, int to_mont, cudaStream_t s);

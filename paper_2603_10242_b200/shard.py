@@ -221,14 +221,14 @@ def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
     return N * pre // tot, N * (pre + sh[rank]) // tot
 
 
-def balanced_shares(world: int, ntt_frac: float = 0.092, unit: int = 1000) -> list[int]:
+def balanced_shares(world: int, ntt_frac: float = 0.103, unit: int = 1000) -> list[int]:
     """Shares of the bases that even out the ranks when vector k of the H
     polynomial is transformed on rank k mod world: an owned vector (its iNTT
     + coset NTT, run concurrently with the rank's MSMs) costs ~ntt_frac of
-    the whole proof's MSM work — fitted at 100k txs (3 x 2^26 domain), 8
-    ranks, from an owner rank (share 53/1000: 429 ms) and a non-owner
-    (168/1000: 494 ms): ~250 ms per owned vector vs ~2.8 s of MSM work in
-    all — so owners take fewer bases."""
+    the whole proof's MSM work — fitted at 100k txs (3 x 2^26 domain, A / B1
+    / B2 sharing one digit sort), 8 ranks, from an owner rank (share 68/1000:
+    462 ms) and a non-owner (160/1000: 435 ms): ~260 ms per owned vector vs
+    ~2.5 s of MSM work in all — so owners take fewer bases."""
     own = [bin(owned_mask(r, world)).count("1") for r in range(world)]
     t = (1.0 + ntt_frac * sum(own)) / world  # per-rank budget, MSM-work units
     w = [max(t - ntt_frac * o, 0.01) for o in own]
