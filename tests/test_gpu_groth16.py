@@ -712,3 +712,24 @@ def test_one_proof_entry_points_reject_bad_arguments(ctx):
             pk.prove(arr([1] * 8), arr([2] * 8))
     finally:
         pk.close()
+
+
+def test_variable_base_key_block_equals_fixed_key_block(ctx, monkeypatch):
+    """A multi-chunk Groth16 block through a variable-base key (one buffer
+    slot: the chunks serialise) gives the same chunk proofs and FC as the
+    fixed-base key (two slots, chunk k+1's witness under chunk k's MSMs)."""
+    from paper_2603_10242_b200 import groth16, wire
+    T, K, n = 4, 3, 23
+    trap = arr([5, 7, 11, 13, 17])
+    fb = O.multi_user_block(n, 3)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(fb.header, np.uint8).copy())
+    wit = _witnesses(fb, n)
+    out = []
+    for vb in ("0", "1"):
+        monkeypatch.setenv("ACEGPU_G16_VB", vb)
+        pk = groth16.ProvingKey(T, K, trap, ctx)
+        try:
+            out.append(pk.prove_block(wfb, wit)[1:])
+        finally:
+            pk.close()
+    assert out[0] == out[1]
