@@ -103,7 +103,7 @@ def test_groth16_deterministic_rs(ctx):
         pk.close()
 
 
-@pytest.mark.parametrize("T", [5, 33, 64])
+@pytest.mark.parametrize("T", [5, 33, 64, 1100, 2100])
 def test_groth16_binding_covers_every_input(ctx, T):
     """Binding v2: flipping one MIDDLE public input changes r, s,
     the chunk digest and the verifier's weight seed; flipping a middle
