@@ -889,10 +889,10 @@ int run_t(const uint8_t* table, uint64_t n, const uint8_t* scalars, MsmScratch& 
 // Variable base: sub-ranges of <= sub points (their W x sub sorted entries
 // stay below 2^32), W window sums each, then one Horner combination; k
 // tables (G1 or G2) over the same scalars share each sub-range's sort.
-int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
-                 const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
-                 cudaStream_t s) {
-    using Wn = WinVb;
+template <class Wn>
+int run_vb_multi_t(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
+                   const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
+                   cudaStream_t s) {
     if (!sub || sub > kMsmVbSubMax) sub = kMsmVbSubMax;
     const uint64_t nsub = n ? (n + sub - 1) / sub : 1;
     const uint64_t per = (uint64_t)256 * Wn::W * nsub;  // one table's window sums
@@ -923,6 +923,22 @@ int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t
             combine_windows_kernel<Fq, Wn><<<1, 32, 0, s>>>(sc.win + per * i, (uint32_t)nsub, outs[i]);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
+}
+
+// Window size by size: c = 20 (13 windows x 2^19 buckets) pays off over
+// 2^26-point sub-ranges; up to ACEGPU_MSM_VB_SMALL points (small split slices)
+// c = 17 (15 x 2^16 buckets): 15 % more bucket entries but a fraction of
+// the per-window reductions and fixups.
+#ifndef ACEGPU_MSM_VB_SMALL
+#define ACEGPU_MSM_VB_SMALL (1ull << 24)
+#endif
+int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
+                 const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
+                 cudaStream_t s) {
+    const char* e = std::getenv("ACEGPU_MSM_VB_SMALL");  // per call: tests force either form
+    const uint64_t small = e ? std::strtoull(e, nullptr, 0) : (uint64_t)ACEGPU_MSM_VB_SMALL;
+    if (n <= small) return run_vb_multi_t<WinFixed>(k, groups, bases, n, scalars, sc, outs, sub, s);
+    return run_vb_multi_t<WinVb>(k, groups, bases, n, scalars, sc, outs, sub, s);
 }
 
 }  // namespace

@@ -221,14 +221,25 @@ def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
     return N * pre // tot, N * (pre + sh[rank]) // tot
 
 
-def balanced_shares(world: int, ntt_frac: float = 0.103, unit: int = 1000) -> list[int]:
+# Measured per-world shares (‰) for the 100k-tx block (3 x 2^26 domain) on
+# B200, evening the slowest owner and non-owner ranks
+# (bench.bench_one_proof_split: world 8 433 / 433 ms, world 4 890 / 895 ms;
+# world 2 interpolated between [448, 552] -> 1,810 / 1,974 ms and [481, 519]
+# -> 1,939 / 1,877 ms). The formula's fractions differ per world because the
+# MSM window size and efficiency change with the slice size.
+_MEASURED_SHARES = {2: [472, 528], 4: [214, 214, 214, 358], 8: [66, 66, 66, 161, 161, 161, 161, 161]}
+
+
+def balanced_shares(world: int, ntt_frac: float | None = None, unit: int = 1000) -> list[int]:
     """Shares of the bases that even out the ranks when vector k of the H
     polynomial is transformed on rank k mod world: an owned vector (its iNTT
     + coset NTT, run concurrently with the rank's MSMs) costs ~ntt_frac of
-    the whole proof's MSM work — fitted at 100k txs (3 x 2^26 domain, A / B1
-    / B2 sharing one digit sort), 8 ranks, from an owner rank (share 68/1000:
-    462 ms) and a non-owner (160/1000: 435 ms): ~260 ms per owned vector vs
-    ~2.5 s of MSM work in all — so owners take fewer bases."""
+    the whole proof's MSM work (~0.1 at 100k txs), so owners take fewer
+    bases. Without ntt_frac, the measured table for the worlds it holds."""
+    if ntt_frac is None:
+        if world in _MEASURED_SHARES:
+            return list(_MEASURED_SHARES[world])
+        ntt_frac = 0.095
     own = [bin(owned_mask(r, world)).count("1") for r in range(world)]
     t = (1.0 + ntt_frac * sum(own)) / world  # per-rank budget, MSM-work units
     w = [max(t - ntt_frac * o, 0.01) for o in own]

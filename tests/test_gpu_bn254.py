@@ -267,13 +267,17 @@ def test_msm_heavy_buckets(ctx, group, n):
     assert got == bytes(dl)
 
 
+@pytest.mark.parametrize("c20", [False, True])
 @pytest.mark.parametrize("group,n,sub", [(1, 1, 0), (1, 5000, 0), (1, 5000, 777), (2, 3000, 1000),
                                          (1, 20000, 4096)])
-def test_msm_variable_base_matches_fixed_base_and_oracle(ctx, group, n, sub):
+def test_msm_variable_base_matches_fixed_base_and_oracle(ctx, group, n, sub, c20, monkeypatch):
     """The variable-base MSM (a whole block's keys: no window tables, one
     bucket set per window, sub-ranges Horner-combined) equals the fixed-base
     MSM and the oracle on the same bases and scalars, including the 0/1
-    witness shape (heavy buckets) and sub-ranges that do not divide n."""
+    witness shape (heavy buckets) and sub-ranges that do not divide n; both
+    window sizes (c = 17 up to 2^25 points, c = 20 above: forced here)."""
+    if c20:
+        monkeypatch.setenv("ACEGPU_MSM_VB_SMALL", "0")
     rng = random.Random(7 * n + group + sub)
     ks = [rng.randrange(1, R) for _ in range(n)]
     G = np.frombuffer(g_gen(group), np.uint8).copy()
