@@ -1996,6 +1996,8 @@ struct acegpu_g16 {
     uint32_t rank = 0, world = 1;
     // domain N = 2^logn, or 3 * 2^logn (mixed radix) when three
     bool three = false;
+    // split-proof protocol state: 1 = phase 1 done, 2 = partial record ready
+    int split_state = 0;
 };
 
 namespace {
@@ -2892,6 +2894,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CK(cudaEventRecord(g->ev_ab, g->s_ab));
     tr.mark("msm_b1", g->s_ab);
     if (phase1) {  // phase 1 done: the owned evaluations are ready on s
+        g->split_state = 1;
         CK(cudaStreamWaitEvent(s, g->ev_n, 0));
         c->launches += 12 + 4 * bn::kMsmKernels;
         return ACEGPU_OK;
@@ -2902,6 +2905,7 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         for (cudaEvent_t e : {g->ev_ab, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
         CK(cudaMemcpyAsync(d_part384, g->pts, 384, cudaMemcpyDeviceToDevice, s));
         CK(cudaEventRecord(sl.done, s));
+        g->split_state = 2;
         tr.dump();
         c->launches += 15 + 5 * bn::kMsmKernels;
         return ACEGPU_OK;
@@ -3099,6 +3103,7 @@ extern "C" int acegpu_g16_prove_phase2_dev(acegpu_ctx* c, void* stream, acegpu_g
     acegpu_g16::Slot& sl = g->slot[g->cur];
     const acegpu_msm_bases* qh = g->qh;
     if (!qh->vb) return fail(ACEGPU_EINVAL, "g16 phase 2: variable-base keys only");
+    if (g->split_state != 1) return fail(ACEGPU_EINVAL, "g16 phase 2 before phase 1");
     const uint64_t S = qh->n;
     cudaStream_t sh = g->s_h;
     CK(cudaEventRecord(g->ev_in, s));  // the exchanged slices are ready on s
@@ -3116,6 +3121,7 @@ extern "C" int acegpu_g16_prove_phase2_dev(acegpu_ctx* c, void* stream, acegpu_g
     for (cudaEvent_t e : {g->ev_ab, g->ev_bl, g->ev_h}) CK(cudaStreamWaitEvent(s, e, 0));
     CK(cudaMemcpyAsync(d_part384, sl.pts, 384, cudaMemcpyDeviceToDevice, s));
     CK(cudaEventRecord(sl.done, s));
+    g->split_state = 2;
     c->launches += 2 + bn::kMsmKernels;
     return ACEGPU_OK;
 }
@@ -3131,6 +3137,8 @@ extern "C" int acegpu_g16_finish_dev(acegpu_ctx* c, void* stream, acegpu_g16* g,
     std::lock_guard<std::mutex> lk(c->mu);
     DeviceGuard guard(c->device);
     cudaStream_t s = pick(c, stream);
+    if (g->split_state != 2) return fail(ACEGPU_EINVAL, "g16 finish before this key's partial");
+    g->split_state = 0;
     acegpu_g16::Slot& sl = g->slot[g->cur];
     CK(cudaStreamWaitEvent(s, sl.done, 0));
     uint8_t* proof;

@@ -710,6 +710,13 @@ def test_one_proof_entry_points_reject_bad_arguments(ctx):
                      own.data_ptr())
         with pytest.raises(ValueError):  # a split key has no whole-proof path
             pk.prove(arr([1] * 8), arr([2] * 8))
+        parts = torch.zeros(2 * 384, dtype=torch.uint8, device="cuda:0")
+        with pytest.raises(ValueError):  # finish before this key's partial
+            ctx.call("acegpu_g16_finish_dev", None, pk.h, parts.data_ptr(), 2, None, None, None,
+                     None)
+        with pytest.raises(ValueError):  # phase 2 before phase 1
+            ctx.call("acegpu_g16_prove_phase2_dev", None, pk.h, own.data_ptr(),
+                     parts.data_ptr())
     finally:
         pk.close()
 
