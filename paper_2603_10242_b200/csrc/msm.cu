@@ -70,9 +70,13 @@ struct Win {
     static constexpr int c = C;
     static constexpr int W = (255 + C - 1) / C;
     static constexpr int NB = 1 << (C - 1);
-    static constexpr int RedSeg = NB / 8192 > 4 ? NB / 8192 : 4;  // buckets per thread
-    static constexpr int RedThreads = NB / RedSeg;                 // <= 8192 -> <= 64 partials
-    static_assert(RedThreads / 128 <= 64, "reduce_final holds one partial per thread");
+#ifndef ACEGPU_RED_THREADS
+#define ACEGPU_RED_THREADS 8192
+#endif
+    // buckets per reduction thread: NB / ACEGPU_RED_THREADS, at least 2
+    static constexpr int RedSeg = NB / ACEGPU_RED_THREADS > 2 ? NB / ACEGPU_RED_THREADS : 2;
+    static constexpr int RedThreads = NB / RedSeg;
+    static_assert(RedThreads / 128 <= 1024, "reduce_final partials");
 };
 using WinFixed = Win<kMsmC>;
 using WinVb = Win<kMsmVbC>;
@@ -490,8 +494,9 @@ __global__ void __launch_bounds__(64) reduce_final_kernel(const uint8_t* segsum,
     segsum += (uint64_t)X * kParts * blockIdx.x;
     out += (uint64_t)Lay<F>::AFF * blockIdx.x;
     __shared__ __align__(16) uint8_t sm[2 * sizeof(XYZZ<F>)];
-    XYZZ<F> acc = threadIdx.x < kParts ? load_xyzz<F>(segsum + (uint64_t)X * threadIdx.x)
-                                       : XYZZ<F>::inf();
+    XYZZ<F> acc = XYZZ<F>::inf();
+    for (int p = threadIdx.x; p < kParts; p += 64)
+        acc = xyzz_add(acc, load_xyzz<F>(segsum + (uint64_t)X * p));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
@@ -763,7 +768,7 @@ int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s
             cudaMalloc(&sc.cursor, 4 * nbk) || cudaMalloc(&sc.sorted, 4 * keep) ||
             cudaMalloc(&sc.partials, (size_t)256 * 2 * keep_segs) ||  // G2 size: scratch shared
             cudaMalloc(&sc.buckets, (size_t)256 * nbk) ||
-            cudaMalloc(&sc.segsum, (size_t)256 * 64 * std::max<uint64_t>(Wn::W, 16)) ||
+            cudaMalloc(&sc.segsum, (size_t)256 * 1024 * std::max<uint64_t>(Wn::W, 16)) ||
             cudaMalloc(&sc.heavy, 4 * (nbk + 1)) ||
             // slices: <= nseg / kHeavySlice + one partial slice per heavy bucket
             // (each spans > kHeavySpan segments)
