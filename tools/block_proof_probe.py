@@ -13,6 +13,7 @@ import bench  # noqa: E402
 from paper_2603_10242_b200 import _native as N, groth16, prover, wire  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 100000
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 K = 1400
 ctx = N.context(0)
 fb, revs, rix = bench.canonical_block_host(n, ctx)
@@ -29,7 +30,7 @@ print("before setup:", mem(), flush=True)
 t0 = time.perf_counter()
 pk = groth16.ProvingKey(n, K, ctx=ctx)
 print(f"setup T={n} K={K}: {time.perf_counter() - t0:.1f} s; {mem()}", flush=True)
-for i in range(3):
+for i in range(reps):
     t0 = time.perf_counter()
     codes, proof, fc, cps = pk.prove_block(wfb, wit, revs, rix)
     print(f"prove_block {i}: {(time.perf_counter() - t0) * 1e3:.0f} ms; accepted "
