@@ -65,11 +65,20 @@ struct Lay {
 // window, reduction segments. Fixed base uses c = kMsmC (17); variable base
 // (block-size keys) uses kMsmVbC: with 2^26-point sub-ranges the 2^19
 // buckets of c = 20 cost ~2 % and save 2 of 15 windows.
-template <int C>
+// NARROW: the last NARROW windows are one bit narrower (widths C ... C,
+// C-1 ... C-1 summing to >= 255), so the top window is nearly full — with
+// uniform 20-bit windows the top one holds 14 bits, 2^13 buckets of 2^13
+// entries each at 2^26 points: all "heavy".
+template <int C, int NARROW = 0>
 struct Win {
     static constexpr int c = C;
-    static constexpr int W = (255 + C - 1) / C;
+    static constexpr int W = (255 + NARROW + C - 1) / C;
     static constexpr int NB = 1 << (C - 1);
+    __host__ __device__ static constexpr int width(int w) { return w < W - NARROW ? C : C - 1; }
+    __host__ __device__ static constexpr int off(int w) {
+        return w <= W - NARROW ? C * w : C * (W - NARROW) + (C - 1) * (w - (W - NARROW));
+    }
+    static_assert(C * (W - NARROW) + (C - 1) * NARROW >= 255, "windows cover 255 bits");
 #ifndef ACEGPU_RED_THREADS
 #define ACEGPU_RED_THREADS 8192
 #endif
@@ -79,7 +88,10 @@ struct Win {
     static_assert(RedThreads / 128 <= 1024, "reduce_final partials");
 };
 using WinFixed = Win<kMsmC>;
-using WinVb = Win<kMsmVbC>;
+#ifndef ACEGPU_MSM_VB_NARROW
+#define ACEGPU_MSM_VB_NARROW 5  // c = 20: 8 x 20 + 5 x 19 = 255 bits (13 windows)
+#endif
+using WinVb = Win<kMsmVbC, ACEGPU_MSM_VB_NARROW>;
 
 template <class F>
 __device__ __forceinline__ bool load_affine(const uint8_t* p, F& x, F& y) {
@@ -155,14 +167,14 @@ __global__ void prepare_kernel(const uint8_t* bases, uint64_t n, uint8_t* table)
 // holds < 2^(254 - c (W-1)) <= 2^(c-1), so no carry leaves it.
 template <class Wn = WinFixed>
 __device__ __forceinline__ void digits(const uint8_t* s, int32_t d[Wn::W]) {
-    constexpr int kC = Wn::c;
     const uint4* q = reinterpret_cast<const uint4*>(s);
     uint4 a = q[0], b = q[1];
     const uint32_t limb[9] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, 0u};
     uint32_t carry = 0;
 #pragma unroll
     for (int w = 0; w < Wn::W; ++w) {
-        const int bit = w * kC, lo = bit >> 5, sh = bit & 31;
+        const int kC = Wn::width(w);
+        const int bit = Wn::off(w), lo = bit >> 5, sh = bit & 31;
         const uint64_t v = ((uint64_t)limb[lo + 1] << 32) | limb[lo];
         const uint32_t raw = (uint32_t)(v >> sh) & ((1u << kC) - 1u);
         const uint32_t t = raw + carry;
@@ -713,7 +725,7 @@ __global__ void combine_windows_kernel(const uint8_t* win, uint32_t nsub, uint8_
     constexpr int A = Lay<F>::AFF;
     XYZZ<F> acc = XYZZ<F>::inf();
     for (int w = Wn::W - 1; w >= 0; --w) {
-        for (int d = 0; d < Wn::c; ++d) acc = xyzz_dbl(acc);
+        for (int d = 0; d < Wn::width(w); ++d) acc = xyzz_dbl(acc);
         for (uint32_t r = 0; r < nsub; ++r) {
             F x, y;
             if (load_affine<F>(win + (uint64_t)A * (r * Wn::W + w), x, y))
