@@ -740,3 +740,28 @@ def test_variable_base_key_block_equals_fixed_key_block(ctx, monkeypatch):
         finally:
             pk.close()
     assert out[0] == out[1]
+
+
+def test_one_proof_for_the_100k_block_verifies(ctx):
+    """BASELINE configs[3] in one-proof mode at full size: the canonical 100k
+    block (the reference's acceptance generator) proven as ONE Groth16 proof
+    (140.1 M constraints, 3 x 2^26 domain, ~100 GB of key and vectors in
+    HBM), the FC carrying it; verify_finality_certificate accepts it with the
+    one 256-B proof and rejects a flipped proof byte."""
+    import bench
+    from paper_2603_10242_b200 import groth16, prover, wire
+    n = 100_000
+    fb, revs, rix = bench.canonical_block_host(n, ctx)
+    wit = bench.make_witnesses(fb, revs, rix, ctx)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(bytes(fb.header), np.uint8).copy())
+    pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx)
+    try:
+        assert pk.constraints == 140_100_001 and pk.domain == 3 << 26
+        codes, proof, fc, cps = pk.prove_block(wfb, wit, revs, rix)
+        assert (codes == 0).all() and len(cps) == 256 and proof[:256] == cps
+        assert pk.verify_finality_certificate(fc, wfb, cps) == prover.FcCheck.Valid
+        bad = bytearray(cps)
+        bad[200] ^= 1
+        assert pk.verify_finality_certificate(fc, wfb, bytes(bad)) == prover.FcCheck.ProofMismatch
+    finally:
+        pk.close()
