@@ -1986,6 +1986,9 @@ struct acegpu_g16 {
     cudaStream_t s_n = nullptr;   // the H-polynomial NTTs (then ev_n -> the H MSM on s_h)
     cudaEvent_t ev_n = nullptr;
     cudaEvent_t ev_z = nullptr, ev_bl = nullptr, ev_h = nullptr;
+    // fixed-base keys: A / B1 / B2 share one digit sort (msm_ab's), B2
+    // accumulates on s_bl: ev_sorted = sorted, ev_b2 = B2 done with them
+    cudaEvent_t ev_sorted = nullptr, ev_b2 = nullptr;
     bn::MsmScratch msm_bl, msm_h, msm_ab;  // one per MSM stream (no cross-stream scratch)
     const acegpu_r1cs* r1cs = nullptr;  // general circuit (setup_r1cs), else the synthetic chain
     uint8_t* zsc = nullptr;             // general path: r, s digest scratch
@@ -2081,7 +2084,7 @@ extern "C" void acegpu_g16_free(acegpu_g16* g) {
     for (cudaStream_t t : {g->s_bl, g->s_h, g->s_ab, g->s_n})
         if (t) cudaStreamDestroy(t);
     if (g->ev_n) cudaEventDestroy(g->ev_n);
-    for (cudaEvent_t e : {g->ev_z, g->ev_bl, g->ev_h})
+    for (cudaEvent_t e : {g->ev_z, g->ev_bl, g->ev_h, g->ev_sorted, g->ev_b2})
         if (e) cudaEventDestroy(e);
     g->msm_bl.release();
     g->msm_h.release();
@@ -2186,7 +2189,7 @@ int g16_setup_impl(acegpu_ctx* c, uint32_t T, uint32_t K, const acegpu_r1cs* r,
         CK(cudaStreamCreateWithPriority(&g->s_n, cudaStreamNonBlocking, n_top ? greatest : lvl("h")));
         CK(cudaEventCreateWithFlags(&g->ev_n, cudaEventDisableTiming));
     }
-    for (cudaEvent_t* e : {&g->ev_z, &g->ev_bl, &g->ev_h})
+    for (cudaEvent_t* e : {&g->ev_z, &g->ev_bl, &g->ev_h, &g->ev_sorted, &g->ev_b2})
         CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     // constants
     CK(cudaMemcpyAsync(g->consts, trapdoor5, 160, cudaMemcpyHostToDevice, s));
@@ -2866,29 +2869,47 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         return fail(ACEGPU_ECUDA, "g16 msm H");
     CK(cudaEventRecord(g->ev_h, sh));
     tr.mark("msm_h", sh);
-    // s_bl: [l] (L)
-    CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
-    if (msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
-        return fail(ACEGPU_ECUDA, "g16 msm L");
-    CK(cudaEventRecord(g->ev_bl, g->s_bl));
-    tr.mark("msm_l", g->s_bl);
-    // s_ab: A, B1 (G1) and B2 (G2) over the same scalars z | 1 | r | s — one
-    // digit sort, three accumulations; then s*A and r*B1 on the side stream
-    CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
-    {
-        const int groups[3] = {1, 1, 2};
-        const uint8_t* tabs[3] = {g->qa->table, g->qb1->table, g->qb2->table};
-        uint8_t* outs[3] = {g->pts, g->pts + 64, g->pts + 128};
-        const acegpu_msm_bases* qa = g->qa;
+    const int groups[3] = {1, 1, 2};
+    const uint8_t* tabs[3] = {g->qa->table, g->qb1->table, g->qb2->table};
+    uint8_t* outs[3] = {g->pts, g->pts + 64, g->pts + 128};
+    const acegpu_msm_bases* qa = g->qa;
+    if (!qa->vb) {
+        // fixed base: s_ab sorts z | 1 | r | s once (after the previous
+        // proof's B2 has finished reading msm_ab's sorted entries) and
+        // accumulates A, B1; s_bl accumulates B2 from the same sort, then L
+        bn::MsmSorted info;
+        CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
+        CK(cudaStreamWaitEvent(g->s_ab, g->ev_b2, 0));
+        if (bn::msm_sort(V + 3, g->z, g->msm_ab, info, g->s_ab))
+            return fail(ACEGPU_ECUDA, "g16 msm sort");
+        CK(cudaEventRecord(g->ev_sorted, g->s_ab));
+        CK(cudaStreamWaitEvent(g->s_bl, g->ev_sorted, 0));
+        if (bn::msm_accumulate(2, tabs[2], g->msm_ab, info, g->msm_bl, outs[2], g->s_bl))
+            return fail(ACEGPU_ECUDA, "g16 msm B2");
+        CK(cudaEventRecord(g->ev_b2, g->s_bl));
+        tr.mark("msm_b2", g->s_bl);
+        if (msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
+            return fail(ACEGPU_ECUDA, "g16 msm L");
+        CK(cudaEventRecord(g->ev_bl, g->s_bl));
+        tr.mark("msm_l", g->s_bl);
+        for (int i = 0; i < 2; ++i)
+            if (bn::msm_accumulate(1, tabs[i], g->msm_ab, info, g->msm_ab, outs[i], g->s_ab))
+                return fail(ACEGPU_ECUDA, "g16 msm A/B1");
+    } else {
+        // variable base (block-size keys): s_bl: [l]; s_ab: A, B1, B2 over
+        // the same scalars, each sub-range sorted once
+        CK(cudaStreamWaitEvent(g->s_bl, g->ev_z, 0));
+        if (msm(g->ql, g->Vp + 1, g->zl, g->msm_bl, g->pts + 256, g->s_bl))
+            return fail(ACEGPU_ECUDA, "g16 msm L");
+        CK(cudaEventRecord(g->ev_bl, g->s_bl));
+        tr.mark("msm_l", g->s_bl);
+        CK(cudaStreamWaitEvent(g->s_ab, g->ev_z, 0));
         int rc = 0;
-        if (qa->vb && qa->n == 0) {
+        if (qa->n == 0)
             rc = cudaMemsetAsync(g->pts, 0, 256, g->s_ab) != cudaSuccess;
-        } else if (qa->vb) {
+        else
             rc = bn::msm_run_vb_multi(3, groups, tabs, qa->n, g->z + 32 * qa->lo, g->msm_ab, outs,
                                       g->s_ab, qa->vb_sub);
-        } else {
-            rc = bn::msm_run_multi(3, groups, tabs, V + 3, g->z, g->msm_ab, outs, g->s_ab);
-        }
         if (rc) return fail(ACEGPU_ECUDA, "g16 msm A/B1/B2");
     }
     CK(cudaEventRecord(g->ev_ab, g->s_ab));

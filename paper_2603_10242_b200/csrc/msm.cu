@@ -756,9 +756,10 @@ int prepare_t(const uint8_t* bases, uint64_t n, uint8_t* table, cudaStream_t s) 
 // sums (combine_windows_kernel weights them).
 // Phase 1 of a Pippenger pass: the scalars' signed digits sorted into bucket
 // order (sc.offs, sc.sorted); several tables over the same scalars share it.
+// The segment size for n scalars, and the scratch grown to hold them.
 template <bool VB, class Wn>
-int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s,
-              uint32_t& segsz_out, uint64_t& nseg_out) {
+int ensure_core(uint64_t n, MsmScratch& sc, cudaStream_t s, uint32_t& segsz_out,
+                uint64_t& nseg_out) {
     constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
     const uint64_t cap = (uint64_t)Wn::W * n;
     // segment length: kMsmSeg, shorter for small MSMs (>= ~19k threads, so a
@@ -793,6 +794,18 @@ int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s
         sc.cap_segs = keep_segs;
         sc.cap_buckets = nbk;
     }
+    segsz_out = segsz;
+    nseg_out = nseg;
+    return 0;
+}
+
+template <bool VB, class Wn>
+int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s,
+              uint32_t& segsz_out, uint64_t& nseg_out) {
+    constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
+    uint32_t segsz;
+    uint64_t nseg;
+    if (ensure_core<VB, Wn>(n, sc, s, segsz, nseg)) return -1;
     cudaMemsetAsync(sc.hist, 0, 4 * (NB + 1), s);
     const unsigned gb = (unsigned)((n + 255) / 256);
     count_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
@@ -811,12 +824,16 @@ int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s
 // Phase 2: bucket accumulation of `table` over the sorted entries, fixup,
 // heavy buckets, reduction -> out (fixed base: the affine result; variable
 // base: the W window sums).
+// (srt: the scratch holding the sorted entries when another stream's scratch
+// sorted them; sc: this accumulation's buckets, partials and reductions)
 template <class F, bool VB, class Wn>
 int acc_core(const uint8_t* table, uint64_t n, MsmScratch& sc, uint32_t segsz, uint64_t nseg,
-             uint8_t* out, cudaStream_t s) {
+             uint8_t* out, cudaStream_t s, const MsmScratch* srt = nullptr) {
     constexpr int X = Lay<F>::XZ;
     constexpr int NB = VB ? Wn::W * Wn::NB : Wn::NB;
     const uint64_t cap = (uint64_t)Wn::W * n;
+    const uint32_t* sorted = srt ? srt->sorted : sc.sorted;
+    const uint32_t* offs = srt ? srt->offs : sc.offs;
     cudaMemsetAsync(sc.heavy, 0, 4, s);
     bool affine = false;
     if constexpr (sizeof(F) == sizeof(Fq) && !VB) affine = ACEGPU_MSM_AFFINE && affine_enabled();
@@ -866,12 +883,12 @@ int acc_core(const uint8_t* table, uint64_t n, MsmScratch& sc, uint32_t segsz, u
         affine_heavy_kernel<<<148, 128, 0, s>>>(in_pts, in_offs, sc.buckets, sc.heavy);
     } else {
         accumulate_kernel<F, NB><<<(unsigned)((nseg + 127) / 128), 128, 0, s>>>(
-            table, sc.sorted, sc.offs, sc.buckets, sc.partials, segsz);
-        fixup_kernel<F, NB><<<NB / 128, 128, 0, s>>>(sc.offs, sc.partials, sc.buckets, sc.heavy,
+            table, sorted, offs, sc.buckets, sc.partials, segsz);
+        fixup_kernel<F, NB><<<NB / 128, 128, 0, s>>>(offs, sc.partials, sc.buckets, sc.heavy,
                                                      segsz);
-        heavy_slice_kernel<F><<<4 * 148, 128, 0, s>>>(sc.offs, sc.partials, sc.heavy, segsz,
+        heavy_slice_kernel<F><<<4 * 148, 128, 0, s>>>(offs, sc.partials, sc.heavy, segsz,
                                                         sc.heavy_part);
-        heavy_final_kernel<F><<<148, 128, 0, s>>>(sc.offs, sc.heavy, segsz, sc.heavy_part,
+        heavy_final_kernel<F><<<148, 128, 0, s>>>(offs, sc.heavy, segsz, sc.heavy_part,
                                                   sc.buckets);
     }
     constexpr unsigned nw = VB ? Wn::W : 1;
@@ -1000,6 +1017,23 @@ int msm_run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint
                      const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, cudaStream_t s,
                      uint64_t sub) {
     return run_vb_multi(k, groups, bases, n, scalars, sc, outs, sub, s);
+}
+
+int msm_sort(uint64_t n, const uint8_t* scalars, MsmScratch& sc, MsmSorted& info,
+             cudaStream_t s) {
+    info.n = n;
+    return sort_core<false, WinFixed>(n, scalars, sc, s, info.segsz, info.nseg);
+}
+
+int msm_accumulate(int group, const uint8_t* table, const MsmScratch& srt, const MsmSorted& info,
+                   MsmScratch& acc, uint8_t* out, cudaStream_t s) {
+    uint32_t segsz;
+    uint64_t nseg;
+    if (ensure_core<false, WinFixed>(info.n, acc, s, segsz, nseg)) return -1;
+    return group == 2 ? acc_core<Fq2, false, WinFixed>(table, info.n, acc, info.segsz, info.nseg,
+                                                       out, s, &srt)
+                      : acc_core<Fq, false, WinFixed>(table, info.n, acc, info.segsz, info.nseg,
+                                                      out, s, &srt);
 }
 
 int msm_run_multi(int k, const int* groups, const uint8_t* const* tables, uint64_t n,

@@ -68,6 +68,18 @@ constexpr uint64_t kMsmVbSubMax = 1ull << 26;  // W x sub bucket entries < 2^32
 int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
                MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub = 0);
 
+// Fixed base in two phases, so tables over the same scalars can accumulate
+// on different streams: msm_sort (digits into bucket order in sc), then
+// msm_accumulate per table with its own scratch `acc` reading srt's sorted
+// entries (srt must not be re-sorted until those accumulations are done).
+struct MsmSorted {
+    uint64_t n = 0, nseg = 0;
+    uint32_t segsz = 0;
+};
+int msm_sort(uint64_t n, const uint8_t* scalars, MsmScratch& sc, MsmSorted& info,
+             cudaStream_t s);
+int msm_accumulate(int group, const uint8_t* table, const MsmScratch& srt, const MsmSorted& info,
+                   MsmScratch& acc, uint8_t* out, cudaStream_t s);
 // k tables (group 1 or 2 each) over the SAME scalars: one digit sort, then
 // each table's accumulation and reduction (Groth16's A, B1, B2 share z).
 int msm_run_multi(int k, const int* groups, const uint8_t* const* tables, uint64_t n,
