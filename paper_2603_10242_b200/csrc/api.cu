@@ -2790,8 +2790,13 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
     CK(cudaStreamWaitEvent(sw, sl.done, 0));
     G16Trace& tr = g_g16_trace;
     tr.mark("start", sw);
-    for (uint8_t* e : {g->ea, g->eb, g->ec})
-        if (N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), sw));
+    // phase 1 of the owner split needs only the owned row vectors (the
+    // others arrive as slices): skip writing the rest
+    const int rows_needed = phase1 ? owned : 7;
+    uint8_t* e3w[3] = {(rows_needed & 1) ? g->ea : nullptr, (rows_needed & 2) ? g->eb : nullptr,
+                       (rows_needed & 4) ? g->ec : nullptr};
+    for (uint8_t* e : e3w)
+        if (e && N > m) CK(cudaMemsetAsync(e + 32 * m, 0, 32 * (N - m), sw));
     if (g->r1cs) {
         // general R1CS: the caller's full assignment z (standard form); the
         // row evaluations a, b, c = A z, B z, C z by SpMV (zb holds z in
@@ -2807,12 +2812,22 @@ int g16_prove_locked(acegpu_ctx* c, cudaStream_t s, acegpu_g16* g, const uint8_t
         bn::g16_derive_rs_long(g->z + 32 * (1 + g->d.T), V - 1 - g->d.T, g->z + 32, g->d.T,
                                g->zsc, g->rs, g->digest, sw);
     } else {
-        bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, g->ea, g->eb, g->ec, sw);
+        bn::g16_witness(g->d, d_w, d_pub, g->cc, g->z, e3w[0], e3w[1], e3w[2], sw);
         bn::g16_derive_rs(d_w, d_pub, g->d.T, sl.dsc, g->rs, g->digest, sw);
     }
     if (d_rs) CK(cudaMemcpyAsync(g->rs, d_rs, 64, cudaMemcpyDeviceToDevice, sw));
     // scalar vectors with their extras
-    CK(cudaMemcpyAsync(g->zl, g->z + 32 * (1 + g->d.T), 32 * g->Vp, cudaMemcpyDeviceToDevice, sw));
+    {
+        // L's scalars: the private part of z (a split key needs its slice only)
+        uint64_t lo = 0, cnt = g->Vp;
+        if (g->ql->vb && g->world > 1) {
+            lo = std::min<uint64_t>(g->ql->lo, g->Vp);
+            cnt = std::min<uint64_t>(g->ql->lo + g->ql->n, g->Vp) - lo;
+        }
+        if (cnt)
+            CK(cudaMemcpyAsync(g->zl + 32 * lo, g->z + 32 * (1 + g->d.T + lo), 32 * cnt,
+                               cudaMemcpyDeviceToDevice, sw));
+    }
     bn::g16_extras(g->z, g->zb, g->zl, V, g->Vp, g->rs, sw);
     CKL();
     CK(cudaEventRecord(g->ev_z, sw));

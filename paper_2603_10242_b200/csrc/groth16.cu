@@ -255,18 +255,20 @@ __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w
     if (act) {
         const Fr ws = reduce256(ldr(w_in + 32ull * t).v), ps = reduce256(ldr(pub_in + 32ull * t).v);
         const Fr wt = to_mont(ws), pt = to_mont(ps);
+        // (ea / eb / ec may be null: a split rank's phase 1 writes only the
+        // row vectors it transforms)
         if (t == 0) {
             Fr o = Fr::zero();
             o.v[0] = 1;
             str(z, o);
-            str(ea + 32 * P0, one);  // public row of ONE: a = 1
-            str(eb + 32 * P0, Fr::zero());
-            str(ec + 32 * P0, Fr::zero());
+            if (ea) str(ea + 32 * P0, one);  // public row of ONE: a = 1
+            if (eb) str(eb + 32 * P0, Fr::zero());
+            if (ec) str(ec + 32 * P0, Fr::zero());
         }
         str(z + 32 * (1 + t), ps);
-        str(ea + 32 * (P0 + 1 + t), pt);  // public row of pub_t
-        str(eb + 32 * (P0 + 1 + t), Fr::zero());
-        str(ec + 32 * (P0 + 1 + t), Fr::zero());
+        if (ea) str(ea + 32 * (P0 + 1 + t), pt);  // public row of pub_t
+        if (eb) str(eb + 32 * (P0 + 1 + t), Fr::zero());
+        if (ec) str(ec + 32 * (P0 + 1 + t), Fr::zero());
         str(z + 32 * (1 + d.T + (uint64_t)t * (d.K + 1)), ws);  // w_t
         x = add(wt, pt);
     }
@@ -305,14 +307,20 @@ __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w
             const uint4* src1 = reinterpret_cast<const uint4*>(tile[1][j][l]);
             const uint4* src2 = reinterpret_cast<const uint4*>(tile[2][j][l]);
             const uint4* src3 = reinterpret_cast<const uint4*>(tile[3][j][l]);
-            uint4* d0 = reinterpret_cast<uint4*>(ea + 32 * row);
-            uint4* d1 = reinterpret_cast<uint4*>(eb + 32 * row);
-            uint4* d2 = reinterpret_cast<uint4*>(ec + 32 * row);
             uint4* d3 = reinterpret_cast<uint4*>(z + 32 * zi);
-            d0[0] = src0[0]; d0[1] = src0[1];
-            d1[0] = src1[0]; d1[1] = src1[1];
-            d2[0] = src2[0]; d2[1] = src2[1];
             d3[0] = src3[0]; d3[1] = src3[1];
+            if (ea) {
+                uint4* d0 = reinterpret_cast<uint4*>(ea + 32 * row);
+                d0[0] = src0[0]; d0[1] = src0[1];
+            }
+            if (eb) {
+                uint4* d1 = reinterpret_cast<uint4*>(eb + 32 * row);
+                d1[0] = src1[0]; d1[1] = src1[1];
+            }
+            if (ec) {
+                uint4* d2 = reinterpret_cast<uint4*>(ec + 32 * row);
+                d2[0] = src2[0]; d2[1] = src2[1];
+            }
         }
         __syncwarp();
     }
