@@ -343,15 +343,21 @@ __device__ __forceinline__ Fr split_pow(const Fr* lo, const Fr* hi, uint64_t e, 
     return mul(ld(&lo[e & ((1ull << S) - 1)]), ld(&hi[e >> S]));
 }
 
-// Y_i1[i2] = x[i1 + 3 i2] (times g^(i1 + 3 i2) for a forward coset transform)
+// Y_i1[i2] = x[i1 + 3 i2] (times g^(i1 + 3 i2) for a forward coset
+// transform); thread i2 reads its three contiguous elements (one 96-B run:
+// reading the groups in separate threads pulled every line from DRAM three
+// times) and writes one element of each sub-vector.
 __global__ void deint3_kernel(const uint8_t* in, uint8_t* y, uint64_t M, const Fr* g_lo,
                               const Fr* g_hi, int S) {
-    const uint64_t o = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-    if (o >= 3 * M) return;
-    const uint64_t i1 = o / M, i2 = o - i1 * M, src = i1 + 3 * i2;
-    Fr v = load<FrCfg>(in + 32 * src);
-    if (g_lo) v = mul(v, split_pow(g_lo, g_hi, src, S));
-    store<FrCfg>(y + 32 * o, v);
+    const uint64_t i2 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i2 >= M) return;
+#pragma unroll
+    for (int i1 = 0; i1 < 3; ++i1) {
+        const uint64_t src = i1 + 3 * i2;
+        Fr v = load<FrCfg>(in + 32 * src);
+        if (g_lo) v = mul(v, split_pow(g_lo, g_hi, src, S));
+        store<FrCfg>(y + 32 * (M * i1 + i2), v);
+    }
 }
 
 // X[k2 + M k1] = sum_i1 w_N^(i1 k2) w3^(i1 k1) Y_i1[k2], with 1 + w3 + w3^2 = 0:
@@ -426,8 +432,8 @@ int ntt3_run(const Ntt3Tables& t, const NttTables& tM, const uint8_t* in, uint8_
              uint8_t* ybuf, uint8_t* scratch, int inverse, int coset, cudaStream_t s) {
     if (t.k < 0 || tM.L != t.k) return -1;
     const uint64_t M = 1ull << t.k;
-    const unsigned g3 = (unsigned)((3 * M + 255) / 256), g1 = (unsigned)((M + 255) / 256);
-    deint3_kernel<<<g3, 256, 0, s>>>(in, ybuf, M, (coset && !inverse) ? t.g_lo : nullptr, t.g_hi,
+    const unsigned g1 = (unsigned)((M + 255) / 256);
+    deint3_kernel<<<g1, 256, 0, s>>>(in, ybuf, M, (coset && !inverse) ? t.g_lo : nullptr, t.g_hi,
                                      t.S);
     if (t.k <= kNttTwoPassMax) {  // the three sub-NTTs as one batch (scratch: 3 x 2^k)
         if (ntt_run(tM, ybuf, ybuf, scratch, inverse, 0, 3, s)) return -1;
