@@ -211,6 +211,7 @@ struct PassB {
     const Fr* tw_hi;         // w^(n2 e), e < n / n2
     const Fr* pre_lo;        // coset (B1 of a forward coset transform): g^i1 (nC)
     const Fr* pre_hi;        // g^(nC i2) (n2)
+    const Fr* tw_b;          // B1: w^(nC e), e < p q (one product instead of lo * hi)
 };
 __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_b(PassB a) {
     extern __shared__ uint4 smem_raw[];
@@ -230,8 +231,13 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_b(PassB a) {
     const uint64_t n2m = (1ull << a.L2) - 1;
     for (uint32_t k = threadIdx.x; k < M; k += blockDim.x) {
         Fr v = s.get(k);
-        const uint64_t ex = a.tw_mode == 1 ? nC * x * k : i1 * (x + (uint64_t)a.q * k);
-        if (ex) v = mul(v, mul(ld(&a.tw_lo[ex & n2m]), ld(&a.tw_hi[ex >> a.L2])));
+        if (a.tw_mode == 1) {
+            const uint64_t e = x * k;  // w^(nC u s), u s < p q
+            if (e) v = mul(v, ld(&a.tw_b[e]));
+        } else {
+            const uint64_t ex = i1 * (x + (uint64_t)a.q * k);
+            if (ex) v = mul(v, mul(ld(&a.tw_lo[ex & n2m]), ld(&a.tw_hi[ex >> a.L2])));
+        }
         store<FrCfg>(a.out + 32 * (ob + a.out_stride * k), v);
     }
 }
@@ -492,7 +498,8 @@ int ntt_tables(NttTables& t, int L, cudaStream_t s) {
             pw(&t.tw_lo, w, 1, m2, nullptr) || pw(&t.tw_hi, w, m2, nc, nullptr) ||
             pw(&t.twi_lo, wi, 1, m2, nullptr) || pw(&t.twi_hi, wi, m2, nc, nullptr) ||
             pw(&t.g_lo, g, 1, nc, nullptr) || pw(&t.g_hi, g, nc, m2, nullptr) ||
-            pw(&t.gi_post_lo, gi, 1, m2, ninv) || pw(&t.gi_post_hi, gi, m2, nc, nullptr))
+            pw(&t.gi_post_lo, gi, 1, m2, ninv) || pw(&t.gi_post_hi, gi, m2, nc, nullptr) ||
+            pw(&t.tw_full, w, nc, m2, nullptr) || pw(&t.twi_full, wi, nc, m2, nullptr))
             return -1;
         t.w_a = t.w_q;  // marks the tables built
         return cudaGetLastError() == cudaSuccess ? 0 : -1;
@@ -561,6 +568,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
         b.w_sub = inverse ? t.wi_q : t.w_q;
         b.pre_lo = (coset && !inverse) ? t.g_lo : nullptr;
         b.pre_hi = (coset && !inverse) ? t.g_hi : nullptr;
+        b.tw_b = inverse ? t.twi_full : t.tw_full;  // three-pass: w^(nC e), e < p q
         size_t sm = sizeof(Fr) << t.LQ;
         cudaFuncSetAttribute(ntt_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         // one butterfly per thread and stage: M / 2 threads

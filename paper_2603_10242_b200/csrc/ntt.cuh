@@ -20,7 +20,8 @@ struct NttTables {
     Fr* consts = nullptr;  // w, w^-1, g, g^-1, n^-1
     Fr *w_a = nullptr, *wi_a = nullptr, *w_c = nullptr, *wi_c = nullptr;
     Fr *tw_lo = nullptr, *tw_hi = nullptr, *twi_lo = nullptr, *twi_hi = nullptr;
-    Fr *tw_full = nullptr, *twi_full = nullptr;  // w^e, w^-e for e < n (one product per twiddle)
+    Fr *tw_full = nullptr, *twi_full = nullptr;  // w^e, w^-e for e < n (one product per twiddle);
+                                                 // three-pass: w^(nC e), e < p q (pass B1)
     Fr *g_full = nullptr, *gi_post_full = nullptr;  // g^i, n^-1 g^-i for i < n (coset)
     Fr *g_lo = nullptr, *g_hi = nullptr, *gi_post_lo = nullptr, *gi_post_hi = nullptr;
     // three-pass sizes (L > kNttTwoPassMax): n = nC * p * q; sub-DFT roots of
