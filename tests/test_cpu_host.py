@@ -250,3 +250,26 @@ def test_one_proof_slice_exchange_gloo(world, shares):
             idx = np.arange(lo, hi)
             assert (got[k, :, 0] == k + 1).all()
             assert (got[k, :, 1] == idx % 251).all() and (got[k, :, 2] == idx // 251).all()
+
+
+def test_one_proof_shares_and_slices_partition_the_arrays():
+    """Split one-proof keys (acegpu_g16_setup_slice): the share-weighted slices
+    of an array cover it exactly once, in rank order, for the measured
+    tables and the formula alike; vector k of the H polynomial is owned by
+    rank k mod world (every vector exactly once)."""
+    from paper_2603_10242_b200 import shard
+    for world in (1, 2, 3, 4, 5, 8):
+        shares = shard.balanced_shares(world) if world > 1 else None
+        if shares is not None:
+            assert len(shares) == world and min(shares) >= 1
+        for N in (1, 7, 24, 3 << 19, 140_100_004, 3 << 26):
+            prev = 0
+            for r in range(world):
+                lo, hi = shard.slice_bounds(N, r, world, shares)
+                assert lo == prev and hi >= lo
+                prev = hi
+            assert prev == N
+        owners = [shard.owned_mask(r, world) for r in range(world)]
+        assert sum(bin(m).count("1") for m in owners) == 3
+        assert owners[0] & 1 and (owners[1 % world] >> 1) & 1 and (owners[2 % world] >> 2) & 1
+    assert shard.balanced_shares(8, ntt_frac=0.1) != shard.balanced_shares(8, ntt_frac=0.0)
