@@ -267,6 +267,40 @@ __global__ void scatter_kernel(const uint8_t* scalars, uint64_t n, uint32_t* cur
 }
 #endif
 
+// Large variable-base sorts in window passes: the digits once into a
+// window-major key array (coalesced), the bucket histogram alongside; then,
+// per window and bucket range, a scatter whose destinations span a region
+// the L2 can hold — one pass over all windows at once scatters 4-B entries
+// over the whole sorted array, and every partial-sector write becomes a DRAM
+// read-modify-write (ncu at 2^26 points: 27.5 GB read + 30.4 GB written for
+// 3.5 GB of entries).
+template <class Wn>
+__global__ void digits_keys_kernel(const uint8_t* scalars, uint64_t n, uint32_t* keys,
+                                   uint32_t* hist) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    int32_t d[Wn::W];
+    if (i < n) digits<Wn>(scalars + 32 * i, d);
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int w = 0; w < Wn::W; ++w) {
+        const uint32_t key = (i < n && d[w]) ? bucket_key<true, Wn>(w, d[w]) : 0xFFFFFFFFu;
+        if (i < n)
+            keys[(uint64_t)w * n + i] =
+                d[w] ? (uint32_t)(abs(d[w]) - 1) | (d[w] < 0 ? 0x80000000u : 0u) : 0xFFFFFFFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, key);
+        if (key != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(&hist[key], __popc(peers));
+    }
+}
+__global__ void scatter_range_kernel(const uint32_t* keys_w, uint64_t n, uint32_t lo, uint32_t hi,
+                                     uint32_t* cursor_w, uint32_t* sorted) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = keys_w[i];
+    const uint32_t b = k & 0x7FFFFFFFu;
+    if (k == 0xFFFFFFFFu || b < lo || b >= hi) return;
+    sorted[atomicAdd(&cursor_w[b], 1u)] = (uint32_t)i | (k & 0x80000000u);
+}
+
 // The non-empty bucket b with offs[b] <= pos < offs[b + 1] (NB buckets).
 template <int NB = kMsmBuckets>
 __device__ __forceinline__ int bucket_of(const uint32_t* offs, uint32_t pos) {
@@ -808,6 +842,40 @@ int sort_core(uint64_t n, const uint8_t* scalars, MsmScratch& sc, cudaStream_t s
     if (ensure_core<VB, Wn>(n, sc, s, segsz, nseg)) return -1;
     cudaMemsetAsync(sc.hist, 0, 4 * (NB + 1), s);
     const unsigned gb = (unsigned)((n + 255) / 256);
+    // large variable-base sorts: window passes over a key array (see
+    // digits_keys_kernel); ACEGPU_SORT_SPLIT = bucket ranges per window (0: off)
+    static const int split = [] {
+        const char* e = std::getenv("ACEGPU_SORT_SPLIT");
+        return e ? std::atoi(e) : 2;
+    }();
+    if (VB && split > 0 && n >= (1ull << 22)) {
+        if (sc.keys_cap < (uint64_t)Wn::W * n) {
+            if (sc.keys) cudaFree(sc.keys);
+            sc.keys = nullptr;
+            sc.keys_cap = 0;
+            if (cudaMalloc(&sc.keys, 4ull * Wn::W * n)) return -1;
+            sc.keys_cap = (uint64_t)Wn::W * n;
+        }
+        digits_keys_kernel<Wn><<<gb, 256, 0, s>>>(scalars, n, sc.keys, sc.hist);
+        size_t scan_bytes = sc.scan_bytes;
+        if (cub::DeviceScan::ExclusiveSum(sc.scan_tmp, scan_bytes, sc.hist, sc.offs, NB + 1, s) !=
+            cudaSuccess)
+            return -1;
+        cudaMemcpyAsync(sc.cursor, sc.offs, 4 * NB, cudaMemcpyDeviceToDevice, s);
+        for (int w = 0; w < Wn::W; ++w) {
+            const uint32_t nbw = 1u << (Wn::width(w) - 1);  // buckets this window uses
+            for (int r = 0; r < split; ++r) {
+                const uint32_t lo = (uint32_t)((uint64_t)nbw * r / split),
+                               hi = (uint32_t)((uint64_t)nbw * (r + 1) / split);
+                scatter_range_kernel<<<gb, 256, 0, s>>>(sc.keys + (uint64_t)w * n, n, lo, hi,
+                                                        sc.cursor + (uint64_t)w * Wn::NB,
+                                                        sc.sorted);
+            }
+        }
+        segsz_out = segsz;
+        nseg_out = nseg;
+        return cudaGetLastError() == cudaSuccess ? 0 : -1;
+    }
     count_kernel<VB, Wn><<<gb, 256, 0, s>>>(scalars, n, sc.hist);
     // offs = exclusive scan of hist[0..NB] (hist[NB] = 0 -> offs[NB] = total)
     size_t scan_bytes = sc.scan_bytes;
@@ -979,7 +1047,9 @@ int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t
 
 void MsmScratch::release() {
     void* ps[] = {hist, offs, cursor, sorted, partials, buckets, segsum, scan_tmp, heavy,
-                  aff_pts[0], aff_pts[1], aff_offs[0], aff_offs[1], aff_cnt, win};
+                  aff_pts[0], aff_pts[1], aff_offs[0], aff_offs[1], aff_cnt, win, keys};
+    keys = nullptr;
+    keys_cap = 0;
     win = nullptr;
     win_cap = 0;
     cap_buckets = 0;

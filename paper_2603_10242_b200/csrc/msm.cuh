@@ -36,6 +36,8 @@ struct MsmScratch {
     uint32_t* aff_offs[2] = {nullptr, nullptr};   // and bucket offsets, ping-pong
     uint32_t* aff_cnt = nullptr;
     uint64_t aff_cap = 0;
+    uint32_t* keys = nullptr;      // large variable-base sorts: window-major digit keys
+    uint64_t keys_cap = 0;
     uint8_t* win = nullptr;        // variable base: window sums per sub-range (affine)
     uint64_t win_cap = 0;
     uint64_t cap_buckets = 0;      // buckets the hist / offs / buckets arrays hold
