@@ -222,13 +222,12 @@ def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
 
 
 # Measured per-world shares (‰) for the 100k-tx block (3 x 2^26 domain) on
-# B200, evening the slowest owner and non-owner ranks
-# (bench.bench_one_proof_split, after the windowed digit sort: world 8
-# [70 x3, 158 x5] 429 / 421 ms, world 4 [214 x3, 358] 837 / 863 ms, world 2
-# [472, 528] 1,755 / 1,763 ms;
-# world 2 interpolated between [448, 552] -> 1,810 / 1,974 ms and [481, 519]
-# -> 1,939 / 1,877 ms). The formula's fractions differ per world because the
-# MSM window size and efficiency change with the slice size.
+# B200, evening the slowest owner and non-owner ranks; the last measurement
+# (bench.bench_one_proof_split, owner / non-owner): world 8 [70 x3, 158 x5]
+# 429 / 421 ms, world 4 [214 x3, 358] 837 / 863 ms, world 2 [472, 528]
+# 1,755 / 1,763 ms — the table moves each toward even. The formula's
+# fractions differ per world because the MSM window size and efficiency
+# change with the slice size.
 _MEASURED_SHARES = {2: [472, 528], 4: [217, 217, 217, 349], 8: [69, 69, 69, 159, 159, 159, 158, 158]}
 
 
