@@ -245,7 +245,7 @@ int acegpu_bn_msm_run(acegpu_ctx* ctx, const acegpu_msm_bases* bases, const uint
                       uint8_t* out_affine);
 /* Variable-base form (no window tables: n x 64 B / 128 B of bases instead of
  * windows x that — a whole block's proving key): c = 20-bit windows, one
- * bucket set per window, sub-ranges of `sub` points (0 = 2^26, the maximum),
+ * bucket set per window, balanced sub-ranges of <= `sub` points (0 = 80 Mi, the maximum),
  * Horner-combined window sums. Same results as the fixed-base form; run with
  * acegpu_bn_msm_run(_dev). n up to 2^31. */
 int acegpu_bn_msm_prepare_vb(acegpu_ctx* ctx, int group, const uint8_t* points, uint64_t n,

@@ -1842,7 +1842,7 @@ extern "C" int acegpu_bn_msm_prepare_vb(acegpu_ctx* c, int group, const uint8_t*
                                         acegpu_msm_bases** out) {
     if (group != 1 && group != 2) return fail(ACEGPU_EINVAL, "group must be 1 or 2");
     if (n == 0 || n > (1ull << 31)) return fail(ACEGPU_EINVAL, "MSM size must be 1..2^31");
-    if (sub > bn::kMsmVbSubMax) return fail(ACEGPU_EINVAL, "MSM sub-range above 2^26");
+    if (sub > bn::kMsmVbSubMax) return fail(ACEGPU_EINVAL, "MSM sub-range above 80 Mi points");
     if (!points || !out) return fail(ACEGPU_EINVAL, "null argument");
     return msm_prepare_impl(c, group, points, n, on_device, 1, sub, out);
 }

@@ -996,7 +996,10 @@ int run_vb_multi_t(int k, const int* groups, const uint8_t* const* bases, uint64
                    const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
                    cudaStream_t s) {
     if (!sub || sub > kMsmVbSubMax) sub = kMsmVbSubMax;
-    const uint64_t nsub = n ? (n + sub - 1) / sub : 1;
+    uint64_t nsub = n ? (n + sub - 1) / sub : 1;
+    // balanced sub-ranges (each pays its own per-window reductions and
+    // fixups: 140 M points as 2 x 70 M instead of 67 + 67 + 6 M)
+    if (n) sub = (n + nsub - 1) / nsub;
     const uint64_t per = (uint64_t)256 * Wn::W * nsub;  // one table's window sums
     if (sc.win_cap < k * nsub) {
         if (sc.win) cudaFree(sc.win);

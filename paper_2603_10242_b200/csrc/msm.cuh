@@ -66,7 +66,7 @@ int msm_run(int group, const uint8_t* table, uint64_t n, const uint8_t* scalars,
 #define ACEGPU_MSM_VB_C 20  // 13 windows; the per-window 2^19-bucket reductions amortise over 2^26 points
 #endif
 constexpr int kMsmVbC = ACEGPU_MSM_VB_C;
-constexpr uint64_t kMsmVbSubMax = 1ull << 26;  // W x sub bucket entries < 2^32
+constexpr uint64_t kMsmVbSubMax = 80ull << 20;  // 80 Mi points: W x sub bucket entries < 2^32
 int msm_run_vb(int group, const uint8_t* bases, uint64_t n, const uint8_t* scalars,
                MsmScratch& sc, uint8_t* out, cudaStream_t s, uint64_t sub = 0);
 
