@@ -92,6 +92,7 @@ using WinFixed = Win<kMsmC>;
 #define ACEGPU_MSM_VB_NARROW 5  // c = 20: 8 x 20 + 5 x 19 = 255 bits (13 windows)
 #endif
 using WinVb = Win<kMsmVbC, ACEGPU_MSM_VB_NARROW>;
+using WinMid = Win<19, 11>;  // 3 x 19 + 11 x 18 = 255 bits, 14 windows x 2^18 buckets
 
 template <class F>
 __device__ __forceinline__ bool load_affine(const uint8_t* p, F& x, F& y) {
@@ -1037,12 +1038,18 @@ int run_vb_multi_t(int k, const int* groups, const uint8_t* const* bases, uint64
 #ifndef ACEGPU_MSM_VB_SMALL
 #define ACEGPU_MSM_VB_SMALL (1ull << 24)
 #endif
+#ifndef ACEGPU_MSM_VB_MID
+#define ACEGPU_MSM_VB_MID 0  // c = 19 tier off: measured within noise (8 ranks -1 %, 4 ranks +2 %)
+#endif
 int run_vb_multi(int k, const int* groups, const uint8_t* const* bases, uint64_t n,
                  const uint8_t* scalars, MsmScratch& sc, uint8_t* const* outs, uint64_t sub,
                  cudaStream_t s) {
     const char* e = std::getenv("ACEGPU_MSM_VB_SMALL");  // per call: tests force either form
     const uint64_t small = e ? std::strtoull(e, nullptr, 0) : (uint64_t)ACEGPU_MSM_VB_SMALL;
+    const char* em = std::getenv("ACEGPU_MSM_VB_MID");   // c = 19 up to this size
+    const uint64_t mid = em ? std::strtoull(em, nullptr, 0) : (uint64_t)ACEGPU_MSM_VB_MID;
     if (n <= small) return run_vb_multi_t<WinFixed>(k, groups, bases, n, scalars, sc, outs, sub, s);
+    if (n <= mid) return run_vb_multi_t<WinMid>(k, groups, bases, n, scalars, sc, outs, sub, s);
     return run_vb_multi_t<WinVb>(k, groups, bases, n, scalars, sc, outs, sub, s);
 }
 
