@@ -420,3 +420,42 @@ def test_ntt3_large_sparse_evaluations_and_roundtrip(ctx, logk):
     finally:
         del buf
         torch.cuda.empty_cache()
+
+
+def test_msm_variable_base_windowed_sort_large(ctx):
+    """From 2^22 points the variable-base digit sort runs in window passes
+    (window-major keys, L2-sized scatter ranges) and the windows are c = 20
+    (8 x 20 + 5 x 19 bits): at 2^22 + 5 points (bases tiled from 2^16
+    generated points, random scalars, the first few edge values) the result
+    equals the fixed-base MSM over the same bases."""
+    import torch
+    n0, n = 1 << 16, (1 << 22) + 5
+    rng = np.random.default_rng(22)
+    k = rng.integers(0, 2**63, size=(n0, 4), dtype=np.uint64)
+    k[:, 3] &= (1 << 61) - 1
+    G = np.frombuffer(g_gen(1), np.uint8).copy()
+    base = np.zeros(64 * n0, np.uint8)
+    ctx.call("acegpu_bn_scalar_muls", 1, G, k.view(np.uint8).reshape(-1), n0, base)
+    pts = torch.from_numpy(base).cuda().repeat((n + n0 - 1) // n0)[:64 * n].contiguous()
+    sc = torch.randint(0, 256, (n, 32), dtype=torch.uint8, device="cuda")
+    sc[:, 31] &= 0x1F
+    edge = torch.from_numpy(arr([0, 1, R - 1, 2, R - 2])).cuda().view(5, 32)
+    sc[:5] = edge
+    outs = []
+    try:
+        for vb in (1, 0):
+            h = C.c_void_p()
+            if vb:
+                ctx.call("acegpu_bn_msm_prepare_vb", 1, pts.data_ptr(), n, 1, 0, C.byref(h))
+            else:
+                ctx.call("acegpu_bn_msm_prepare", 1, pts.data_ptr(), n, 1, C.byref(h))
+            out = torch.empty(64, dtype=torch.uint8, device="cuda")
+            ctx.call("acegpu_bn_msm_run_dev", None, h, sc.data_ptr(), out.data_ptr())
+            torch.cuda.synchronize()
+            outs.append(out.cpu().numpy().tobytes())
+            from paper_2603_10242_b200 import _native as N
+            N.lib().acegpu_bn_msm_free(h)
+        assert outs[0] == outs[1] and any(outs[0])
+    finally:
+        del pts, sc
+        torch.cuda.empty_cache()
