@@ -989,7 +989,8 @@ def bench_one_proof_dist(ctx, dev: int, fb, revs, rev_index, rank: int, world: i
             b.record(s)
             torch.cuda.synchronize()
             ts.append(a.elapsed_time(b))
-        t = torch.tensor([statistics.mean(ts)], device=f"cuda:{dev}")
+        t = torch.tensor([statistics.mean(ts)],
+                         device="cpu" if dist.get_backend() == "gloo" else f"cuda:{dev}")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return {"n_tx": n, "world": world, "shares": shares, "latency_ms": float(t.item()),
                 "rank_ms_per_step": ts, "setup_s": setup_s, "proofs_per_block": 1,

@@ -130,3 +130,53 @@ def test_two_process_sharded_prove_on_one_gpu(tmp_path):
         bk.close()
     for r in res:
         assert r["one_proof"] == p1 and r["one_fc"] == fc1 and r["one_bad"] == 0
+
+
+def _bench_rank(rank, port, out_dir, n):
+    import sys
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        import bench
+        from paper_2603_10242_b200 import _native as N
+        torch.cuda.set_device(0)
+        ctx = N.context(0)
+        fb, revs, rix = bench.canonical_block_host(n, ctx)
+        r = bench.bench_one_proof_dist(ctx, 0, fb, revs, rix, rank, WORLD, steps=1, warmup=1)
+        np.save(os.path.join(out_dir, f"bench{rank}.npy"), r, allow_pickle=True)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_bench_one_proof_dist_two_processes(tmp_path):
+    """bench.bench_one_proof_dist — the N-GPU one-proof measurement of a real
+    multi-GPU run — driven by two processes over gloo on one GPU (small
+    canonical block, paper-size K): both ranks report the same FC, equal to
+    the whole key's prove_block FC, every transaction accepted."""
+    import hashlib
+    import sys
+
+    import torch.multiprocessing as mp
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    from paper_2603_10242_b200 import _native as N, groth16, wire
+    n = 37
+    mp.start_processes(_bench_rank, args=(_port(), str(tmp_path), n), nprocs=WORLD, join=True,
+                       start_method="spawn")
+    res = [np.load(tmp_path / f"bench{r}.npy", allow_pickle=True).item() for r in range(WORLD)]
+    ctx = N.context(0)
+    fb, revs, rix = bench.canonical_block_host(n, ctx)
+    wit = bench.make_witnesses(fb, revs, rix, ctx)
+    wfb = wire.FlatBlock(fb.payloads, fb.offs, fb.atts, np.frombuffer(bytes(fb.header), np.uint8).copy())
+    pk = groth16.ProvingKey(n, groth16.PAPER_K, ctx=ctx)
+    try:
+        _, _, fc, _ = pk.prove_block(wfb, wit, revs, rix)
+    finally:
+        pk.close()
+    want = hashlib.sha256(fc).hexdigest()
+    for r in res:
+        assert r["fc_sha256"] == want and r["accepted"] == n and r["latency_ms"] > 0
