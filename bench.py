@@ -436,6 +436,8 @@ def run_ours(args, rank: int, world: int) -> None:
         g16["100000"] = run_groth16_block(ctx, dev, fb, revs, rev_index, rank, world, steps=3,
                                           warmup=1, pk=pk, e2e=True, verify=True)
         g16["100000"]["chunk_prove_ms_alone"] = chunk["chunk_prove_ms"]
+        if world == 1:
+            g16["rank_shares"] = bench_chunked_rank_shares(ctx, dev, fb, revs, rev_index, pk)
         wk = chunk["work"]
         ach = wk["fq_mul_equivalents"] / (chunk["chunk_prove_ms"] * 1e-3)
         g16_roof = {"bound": "fmaheavy issue pipe (IMAD / IMAD.HI / DFMA share it)",
@@ -544,6 +546,7 @@ def run_ours(args, rank: int, world: int) -> None:
         "attest_many_revs": many_revs,
         "groth16_block_100000": g16.get("100000"), "groth16_block_16384": g16.get("16384"),
         "zkace_hmac_chunk": g16.get("zkace_hmac"), "zkace_block_1024": g16.get("zkace_block"),
+        "groth16_chunked_rank_shares": g16.get("rank_shares"),
         "groth16_one_proof_block_100000": g16.get("block_proof"),
         "groth16_one_proof_split_ranks": g16.get("block_proof_split"),
         "groth16_one_proof_block_dist": g16.get("block_proof_dist"),
@@ -954,6 +957,46 @@ def bench_groth16_single_block(ctx, dev: int, fb, revs, rev_index, steps: int = 
     finally:
         pk.close()
         torch.cuda.empty_cache()
+
+
+def bench_chunked_rank_shares(ctx, dev: int, fb, revs, rev_index, pk, worlds=(2, 4, 8),
+                              steps: int = 3) -> dict:
+    """The chunked Groth16 block's busiest rank at 2 / 4 / 8 GPUs, measured
+    alone on one GPU: the rank's contiguous whole chunks (shard.partition:
+    49 / 25 / 13 of the 98) — attestation verdicts, leaves, Merkle lift and
+    one Groth16 proof per chunk (acegpu_g16_shard_roots_dev), CUDA events.
+    Not included: the all-gather of 289 + 32 B per chunk and the 7-level
+    combine + FC over the 98 roots (both on every rank, ~0.3 ms)."""
+    import torch
+    from paper_2603_10242_b200 import shard
+    n = fb.n
+    wit = make_witnesses(fb, revs, rev_index, ctx)
+    be = shard.G16Backend(pk, ctx)
+    s = torch.cuda.current_stream()
+    out = {}
+    for world in worlds:
+        parts = shard.partition(n, world, shard.LOG2_CHUNK)
+        r = max(range(world), key=lambda k: parts[k][1])
+        start, count = parts[r]
+        db = shard.DeviceBlock.upload(fb, start, count, revs, rev_index, device=dev)
+        db.witnesses = torch.from_numpy(wit[256 * start:256 * (start + count)].copy()).to(f"cuda:{dev}")
+        codes = torch.zeros(count, dtype=torch.uint8, device=f"cuda:{dev}")
+        be.shard_roots(db, n, shard.LOG2_CHUNK, codes)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            be.shard_roots(db, n, shard.LOG2_CHUNK, codes)
+            b.record(s)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        out[str(world)] = {"busiest_rank": r, "txs": count, "chunks": -(-count // pk.T),
+                           "ms": statistics.mean(ts), "ms_per_step": ts,
+                           "accepted": int((codes == 0).sum().item())}
+    out["note"] = ("busiest rank of the chunked 100k block at N GPUs, measured alone on one "
+                   "B200 (the gather + combine of 98 roots, ~0.3 ms, not included)")
+    return out
 
 
 def bench_one_proof_dist(ctx, dev: int, fb, revs, rev_index, rank: int, world: int,
