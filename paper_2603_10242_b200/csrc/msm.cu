@@ -69,7 +69,7 @@ struct Lay {
 // C-1 ... C-1 summing to >= 255), so the top window is nearly full — with
 // uniform 20-bit windows the top one holds 14 bits, 2^13 buckets of 2^13
 // entries each at 2^26 points: all "heavy".
-template <int C, int NARROW = 0>
+template <int C, int NARROW = 0, int RED_THREADS = 0>
 struct Win {
     static constexpr int c = C;
     static constexpr int W = (255 + NARROW + C - 1) / C;
@@ -83,7 +83,8 @@ struct Win {
 #define ACEGPU_RED_THREADS 8192
 #endif
     // buckets per reduction thread: NB / ACEGPU_RED_THREADS, at least 2
-    static constexpr int RedSeg = NB / ACEGPU_RED_THREADS > 2 ? NB / ACEGPU_RED_THREADS : 2;
+    static constexpr int RT = RED_THREADS ? RED_THREADS : ACEGPU_RED_THREADS;
+    static constexpr int RedSeg = NB / RT > 2 ? NB / RT : 2;
     static constexpr int RedThreads = NB / RedSeg;
     static_assert(RedThreads / 128 <= 1024, "reduce_final partials");
 };
@@ -91,7 +92,10 @@ using WinFixed = Win<kMsmC>;
 #ifndef ACEGPU_MSM_VB_NARROW
 #define ACEGPU_MSM_VB_NARROW 5  // c = 20: 8 x 20 + 5 x 19 = 255 bits (13 windows)
 #endif
-using WinVb = Win<kMsmVbC, ACEGPU_MSM_VB_NARROW>;
+#ifndef ACEGPU_VB_RED_THREADS
+#define ACEGPU_VB_RED_THREADS 8192
+#endif
+using WinVb = Win<kMsmVbC, ACEGPU_MSM_VB_NARROW, ACEGPU_VB_RED_THREADS>;
 using WinMid = Win<19, 11>;  // 3 x 19 + 11 x 18 = 255 bits, 14 windows x 2^18 buckets
 
 template <class F>
