@@ -39,13 +39,19 @@ namespace {
 __device__ __forceinline__ Fr ld(const Fr* p) { return load<FrCfg>(p); }
 __device__ __forceinline__ void st(Fr* p, const Fr& x) { store<FrCfg>(p, x); }
 
-// Pass kernels' occupancy: 512-thread CTAs with 64 KB of shared memory; the
-// FP64 product needs ~84 registers, which allows only one CTA per SM, so the
-// passes are capped at 64 registers for two (loads of one CTA overlap the
-// other's butterflies). ACEGPU_NTT_CIOS=1 uses the IMAD product (fewer
-// registers) inside the NTT instead.
-#ifndef ACEGPU_NTT_MINB
-#define ACEGPU_NTT_MINB 2
+// Pass kernels' occupancy: the FP64 product needs ~84 registers; the passes
+// are sized so several CTAs share an SM (loads of one CTA overlap another's
+// butterflies). ACEGPU_NTT_CIOS=1 uses the IMAD product (fewer registers)
+// inside the NTT instead.
+// Passes A / C run 256-thread CTAs, three per SM (the 64 KB sub-DFT of
+// 2^21-2^22 allows three): 80 registers without spills, against 512 x 2 at
+// 64 registers with 150-200 B of spills (2^21 forward 0.631 -> 0.564 ms,
+// 2^22 1.261 -> 1.124, 2^26 23.6 -> 22.2; 256 x 2 and 256 x 4 in between).
+#ifndef ACEGPU_NTT_AC_THREADS
+#define ACEGPU_NTT_AC_THREADS 256
+#endif
+#ifndef ACEGPU_NTT_AC_MINB
+#define ACEGPU_NTT_AC_MINB 3
 #endif
 #ifndef ACEGPU_NTT_CIOS
 #define ACEGPU_NTT_CIOS 0
@@ -133,7 +139,7 @@ struct PassArgs {
 };
 
 // Pass A: columns i1 in [cb*R, cb*R+R), DFT length n2 over i2.
-__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_a(PassArgs a) {
+__global__ void __launch_bounds__(ACEGPU_NTT_AC_THREADS, ACEGPU_NTT_AC_MINB) ntt_pass_a(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
     const int n1 = 1 << a.L1, n2 = 1 << a.L2;
     constexpr int R = kNttR;
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_a(PassArgs a) {
 }
 
 // Pass C: rows k2 in [rb*R, rb*R+R), DFT length n1 over i1; natural output.
-__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_c(PassArgs a) {
+__global__ void __launch_bounds__(ACEGPU_NTT_AC_THREADS, ACEGPU_NTT_AC_MINB) ntt_pass_c(PassArgs a) {
     extern __shared__ uint4 smem_raw[];
     const int n1 = 1 << a.L1, n2 = 1 << a.L2;
     constexpr int R = kNttR;
@@ -213,7 +219,17 @@ struct PassB {
     const Fr* pre_hi;        // g^(nC i2) (n2)
     const Fr* tw_b;          // B1: w^(nC e), e < p q (one product instead of lo * hi)
 };
-__global__ void __launch_bounds__(512, ACEGPU_NTT_MINB) ntt_pass_b(PassB a) {
+// Pass B CTAs have at most 256 threads (m <= 9 for n <= 2^28): bounds
+// (256, 3) give it 80 registers instead of 64 with 200 B of spills (2^26
+// forward 24.2 -> 23.7 ms, 2^28 107.7 -> 105.4 ms; (256, 2): 118 registers,
+// slower at 24.8 / 115.2 ms).
+#ifndef ACEGPU_NTT_B_THREADS
+#define ACEGPU_NTT_B_THREADS 256
+#endif
+#ifndef ACEGPU_NTT_B_MINB
+#define ACEGPU_NTT_B_MINB 3
+#endif
+__global__ void __launch_bounds__(ACEGPU_NTT_B_THREADS, ACEGPU_NTT_B_MINB) ntt_pass_b(PassB a) {
     extern __shared__ uint4 smem_raw[];
     const uint32_t M = 1u << a.m;
     const SmemFr s{smem_raw, M};
@@ -599,7 +615,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
         c.bstride = 0;
         sm = sizeof(Fr) * (size_t)n1 * kNttR;
         cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        ntt_pass_c<<<(unsigned)(n2 / kNttR), 512, sm, s>>>(c);
+        ntt_pass_c<<<(unsigned)(n2 / kNttR), ACEGPU_NTT_AC_THREADS, sm, s>>>(c);
         return cudaGetLastError() == cudaSuccess ? 0 : -1;
     }
     // pass A: in -> scratch
@@ -618,7 +634,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
     a.bstride = 1ull << L;
     size_t smem = sizeof(Fr) * (size_t)n2 * kNttR;
     cudaFuncSetAttribute(ntt_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_pass_a<<<dim3(n1 / kNttR, batch), 512, smem, s>>>(a);
+    ntt_pass_a<<<dim3(n1 / kNttR, batch), ACEGPU_NTT_AC_THREADS, smem, s>>>(a);
     // pass C: scratch -> out
     PassArgs c = a;
     c.in = scratch;
@@ -632,7 +648,7 @@ int ntt_run(const NttTables& t, const uint8_t* in, uint8_t* out, uint8_t* scratc
  if (inverse && !coset) c.scale = t.consts + 4;
     smem = sizeof(Fr) * (size_t)n1 * kNttR;
     cudaFuncSetAttribute(ntt_pass_c, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    ntt_pass_c<<<dim3(n2 / kNttR, batch), 512, smem, s>>>(c);
+    ntt_pass_c<<<dim3(n2 / kNttR, batch), ACEGPU_NTT_AC_THREADS, smem, s>>>(c);
     return cudaGetLastError() == cudaSuccess ? 0 : -1;
 }
 

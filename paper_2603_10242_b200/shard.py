@@ -228,7 +228,7 @@ def slice_bounds(N: int, rank: int, world: int, shares=None) -> tuple[int, int]:
 # 1,755 / 1,763 ms — the table moves each toward even. The formula's
 # fractions differ per world because the MSM window size and efficiency
 # change with the slice size.
-_MEASURED_SHARES = {2: [472, 528], 4: [217, 217, 217, 349], 8: [69, 69, 69, 159, 159, 159, 158, 158]}
+_MEASURED_SHARES = {2: [472, 528], 4: [217, 217, 217, 349], 8: [70, 70, 70, 158, 158, 158, 158, 158]}
 
 
 def balanced_shares(world: int, ntt_frac: float | None = None, unit: int = 1000) -> list[int]:
