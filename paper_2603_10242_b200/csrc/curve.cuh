@@ -428,11 +428,14 @@ __device__ __forceinline__ XYZZ<F> xyzz_neg(const XYZZ<F>& p) {
     return r;
 }
 
-// k * p for a small scalar k (double-and-add, MSB first).
+// k * p for a small scalar k (double-and-add, MSB first, from k's top bit:
+// the bucket weights of a reduction are < 2^20, so 12+ doublings of the
+// point at infinity are skipped).
 template <class F>
 __device__ XYZZ<F> xyzz_mul_small(const XYZZ<F>& p, uint32_t k) {
-    XYZZ<F> r = XYZZ<F>::inf();
-    for (int b = 31; b >= 0; --b) {
+    if (!k) return XYZZ<F>::inf();
+    XYZZ<F> r = p;
+    for (int b = 30 - __clz(k); b >= 0; --b) {
         r = xyzz_dbl(r);
         if ((k >> b) & 1) r = xyzz_add(r, p);
     }
