@@ -239,12 +239,25 @@ __global__ void h_scalars_kernel(const uint8_t* c, uint64_t n, uint8_t* out) {
 // ea / eb / ec (Montgomery, zeroed beyond m) and its chain values in z
 // (standard form) are contiguous, so the stores go out as 256-B runs instead
 // of one 32-B row per tx 45 KB apart.
+// A paper-size chunk (1,024 txs) has only 32 warps in flight: one warp per
+// SM, whose chain is latency-bound, so every instruction in the step loop
+// adds to it. Below kWitFuseMinT txs (and when ec is written) the chain
+// leaves z to witness_z_kernel (parallel, from ec) instead of converting
+// each value in the loop, and its tile is one step (chunk witness 2.09 ->
+// 1.28 + 0.03 ms; an 8-step tile 1.48; chunk alone 39.2 -> 38.4 ms).
 constexpr int kWitTile = 8;
+#ifndef ACEGPU_WIT_FUSE_MIN_T
+#define ACEGPU_WIT_FUSE_MIN_T 20000
+#endif
+constexpr uint32_t kWitFuseMinT = ACEGPU_WIT_FUSE_MIN_T;
+#ifndef ACEGPU_WIT_SMALL_S
+#define ACEGPU_WIT_SMALL_S 1
+#endif
+template <int S, bool FZ>
 __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w_in,
                                                      const uint8_t* pub_in, const uint8_t* cc,
                                                      uint8_t* z, uint8_t* ea, uint8_t* eb,
                                                      uint8_t* ec) {
-    constexpr int S = kWitTile;
     __shared__ __align__(16) uint8_t tile[4][S][32][32];  // ea | eb | ec | z
     const int lane = threadIdx.x;
     const uint32_t t0 = blockIdx.x * 32, t = t0 + lane;
@@ -292,7 +305,7 @@ __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w
             str(tile[0][j][lane], a);
             str(tile[1][j][lane], b);
             str(tile[2][j][lane], c);
-            str(tile[3][j][lane], from_mont(c));  // z_{t,k} = x_{t,k}
+            if constexpr (FZ) str(tile[3][j][lane], from_mont(c));  // z_{t,k} = x_{t,k}
         }
         __syncwarp();
         // lane l of the store loop: tx (e / S), step (e % S) — consecutive
@@ -307,8 +320,10 @@ __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w
             const uint4* src1 = reinterpret_cast<const uint4*>(tile[1][j][l]);
             const uint4* src2 = reinterpret_cast<const uint4*>(tile[2][j][l]);
             const uint4* src3 = reinterpret_cast<const uint4*>(tile[3][j][l]);
-            uint4* d3 = reinterpret_cast<uint4*>(z + 32 * zi);
-            d3[0] = src3[0]; d3[1] = src3[1];
+            if constexpr (FZ) {
+                uint4* d3 = reinterpret_cast<uint4*>(z + 32 * zi);
+                d3[0] = src3[0]; d3[1] = src3[1];
+            }
             if (ea) {
                 uint4* d0 = reinterpret_cast<uint4*>(ea + 32 * row);
                 d0[0] = src0[0]; d0[1] = src0[1];
@@ -324,6 +339,14 @@ __global__ void __launch_bounds__(32) witness_kernel(G16Dims d, const uint8_t* w
         }
         __syncwarp();
     }
+}
+
+// z_{t,k} (standard form) = c row t*K + k (Montgomery): x_{t,0} = x, x_{t,k} = y_k^2.
+__global__ void witness_z_kernel(G16Dims d, const uint8_t* ec, uint8_t* z) {
+    const uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    if (j >= (uint64_t)d.T * d.K) return;
+    const uint64_t t = j / d.K, k = j - t * d.K;
+    str(z + 32 * (1 + d.T + t * (d.K + 1) + 1 + k), from_mont(ldr(ec + 32 * j)));
 }
 
 // h_j = (a_j b_j - c_j) / (g^N - 1) on the coset (Montgomery, in place into ea).
@@ -624,7 +647,12 @@ void g16_h_scalars(const uint8_t* c, uint64_t n, uint8_t* out, cudaStream_t s) {
 }
 void g16_witness(const G16Dims& d, const uint8_t* w, const uint8_t* pub, const uint8_t* cc,
                  uint8_t* z, uint8_t* ea, uint8_t* eb, uint8_t* ec, cudaStream_t s) {
-    witness_kernel<<<grid(d.T, 32), 32, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+    if (d.T < kWitFuseMinT && ec) {
+        witness_kernel<ACEGPU_WIT_SMALL_S, false><<<grid(d.T, 32), 32, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+        witness_z_kernel<<<grid((uint64_t)d.T * d.K, 256), 256, 0, s>>>(d, ec, z);
+    } else {
+        witness_kernel<kWitTile, true><<<grid(d.T, 32), 32, 0, s>>>(d, w, pub, cc, z, ea, eb, ec);
+    }
 }
 void g16_pointwise(uint8_t* ea, const uint8_t* eb, const uint8_t* ec, const uint8_t* c,
                    uint64_t n, cudaStream_t s) {
