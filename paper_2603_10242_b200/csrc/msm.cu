@@ -56,8 +56,8 @@ struct Lay {
     static constexpr int AFF = 2 * EB;
     static constexpr int XZ = 4 * EB;
     // accumulate_kernel min CTAs/SM (register cap): G2's Fq2 temporaries
-    // take 216 registers -> 2 CTAs (8 warps) per SM; capping them spills
-    // and measured slower
+    // fill 255 registers (and spill 172 B) -> 2 CTAs (8 warps) per SM;
+    // capping them lower spills more and measured slower
     static constexpr int ACC_MIN_CTAS = EB == 32 ? ACEGPU_G1_ACC_MINB : ACEGPU_G2_ACC_MINB;
 };
 
